@@ -1,0 +1,241 @@
+/*
+ * gnn_b200.h — C ABI of the B200-native sparse GNN hot path (libgnnb200.so).
+ *
+ * Everything here is plain C: device pointers, sizes, and an opaque CUDA
+ * stream handle.  No torch types cross this boundary.  Every entry point
+ * returns a gnn_status (0 = ok); the Python host layer maps the codes to the
+ * reference's exception taxonomy (gsbench/errors.py:5-29).
+ *
+ * Ownership: all buffers are caller-owned.  The library never allocates
+ * persistent device memory; scratch comes in through (ws, ws_bytes), sized by
+ * the matching *_workspace() query, so the caller's allocator accounts for
+ * every byte of peak memory.
+ *
+ * Threading: every compute entry point is stream-ordered, reentrant and free
+ * of host synchronisation (CUDA-graph capturable).  The *builders* (CSR/CSC
+ * construction, validation) synchronise the stream once at the end, because
+ * they must report the reference's validation errors before returning
+ * (graph.py:95-102, sampler.py:250-251).
+ *
+ * Reference interfaces replaced (file:line under the reference tree):
+ *   gnn_csr_from_edges      <- gsbench.graph.csr_from_edges   graph.py:106-114
+ *   gnn_csr_validate        <- gsbench.graph.make_csr         graph.py:91-103
+ *   gnn_subgraph_csr        <- gsbench.build_subgraph_csr     sampler.py:242-256
+ *   gnn_degrees             <- CsrGraph.degrees               graph.py:39-41
+ *   gnn_csc_from_csr        <- csr_from_edges(V, targets, rows) (transposed CSR)
+ *   gnn_generate_powerlaw   <- gsbench.graph.generate, power-law branch  graph.py:254-262
+ *   gnn_spmm                <- GraphPy SpMMv / SpMMve (+T)    PAPER.md:264-278 (prose only)
+ *   gnn_degree_norm_inplace <- GraphPy in-place degree-norm
+ *   gnn_sddmm               <- GraphPy SDDMM on CSR-style COO PAPER.md:281-287
+ *   gnn_gat_*               <- GAT edge-softmax state tensor
+ *   gnn_gemm*               <- the dense X.W transform, modelled as b_f*V*K in
+ *                              execmodel.py:374-378
+ */
+#ifndef GNN_B200_H
+#define GNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *gnn_stream_t; /* a cudaStream_t (CUstream); NULL = legacy default stream */
+
+typedef enum gnn_status {
+  GNN_OK = 0,
+  GNN_ERR_INVALID_ARGUMENT = 1, /* bad shape / pointer / flag combination       -> ValueError  */
+  GNN_ERR_CSR_INVARIANT = 2,    /* offsets malformed (graph.py:95-100)           -> ValueError  */
+  GNN_ERR_RANGE = 3,            /* target id outside [0, V) (graph.py:101-102)   -> RangeError  */
+  GNN_ERR_INDEX = 4,            /* subgraph source id out of range (sampler.py:250-251) -> IndexError */
+  GNN_ERR_WORKSPACE = 5,        /* ws_bytes smaller than the *_workspace() query */
+  GNN_ERR_CUDA = 6,             /* a CUDA runtime error (gnn_last_cuda_error())  -> RuntimeError */
+  GNN_ERR_UNSUPPORTED = 7,      /* shape the kernels do not cover                -> ValueError  */
+  GNN_ERR_SOURCE_RANGE = 8      /* csr_from_edges source id outside [0, V): numpy's bincount/cumsum
+                                   shape error in the reference (graph.py:110-112) -> ValueError */
+} gnn_status;
+
+/* ---------------------------------------------------------------- misc */
+int gnn_abi_version(void);                 /* bumped on any signature change */
+const char *gnn_strerror(int status);
+int gnn_last_cuda_error(void);             /* cudaError_t of the last GNN_ERR_CUDA */
+int gnn_device_sm_count(void);             /* SMs of the current device */
+int64_t gnn_launch_counter(void);          /* kernels launched by this library so far */
+
+/* ------------------------------------------------------- graph builders */
+/* Stable counting sort of (src,dst) pairs into CSR: offsets[V+1] int64,
+ * targets[E] int32, bit-exact with graph.py:106-114 (stable within a row,
+ * multigraph duplicates kept).  Errors: GNN_ERR_SOURCE_RANGE if a src is
+ * outside [0,V); GNN_ERR_RANGE if a dst is outside [0,V) (make_csr check). */
+size_t gnn_csr_from_edges_workspace(int64_t num_vertices, int64_t num_edges);
+int gnn_csr_from_edges(int64_t num_vertices, int64_t num_edges, const int64_t *src,
+                       const int64_t *dst, int64_t *offsets, int32_t *targets, void *ws,
+                       size_t ws_bytes, gnn_stream_t stream);
+
+/* build_subgraph_csr (sampler.py:242-256): same stable build over local ids;
+ * GNN_ERR_INDEX if a source is outside [0,num_local_src); dst is truncated to
+ * int32 without a range check, as LOCAL_DTYPE astype does. */
+size_t gnn_subgraph_csr_workspace(int64_t num_local_src, int64_t num_edges);
+int gnn_subgraph_csr(int64_t num_local_src, int64_t num_edges, const int64_t *edge_src,
+                     const int64_t *edge_dst, int64_t *offsets, int32_t *targets, void *ws,
+                     size_t ws_bytes, gnn_stream_t stream);
+
+/* make_csr invariants (graph.py:95-102) on device arrays. */
+size_t gnn_csr_validate_workspace(int64_t num_vertices, int64_t num_edges);
+int gnn_csr_validate(int64_t num_vertices, int64_t num_edges, const int64_t *offsets,
+                     const int32_t *targets, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* degrees = diff(offsets) (graph.py:39-41). */
+int gnn_degrees(int64_t num_vertices, const int64_t *offsets, int64_t *degrees,
+                gnn_stream_t stream);
+
+/* Transposed CSR (CSC) by a stable sort of the CSR by column id:
+ * t_offsets[num_cols+1], t_rows[nnz]; optional t_eid[nnz] = CSR position of
+ * each CSC entry (the GraphPy edge-ID array).  Equal to
+ * csr_from_edges(num_cols, targets, rows) of the reference. */
+size_t gnn_csc_from_csr_workspace(int64_t num_rows, int64_t num_cols, int64_t nnz);
+int gnn_csc_from_csr(int64_t num_rows, int64_t num_cols, int64_t nnz, const int64_t *offsets,
+                     const int32_t *cols, int64_t *t_offsets, int32_t *t_rows, int32_t *t_eid,
+                     void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* Multigraph coalescing of a CSR whose rows are sorted by column (e.g. the
+ * transpose of a CSC): unique (row,col) pairs with their multiplicity as a
+ * float edge value.  out_offsets[num_rows+1], out_cols/out_mult sized nnz
+ * (upper bound); *out_nnz (host) receives the unique count (one sync). */
+size_t gnn_csr_coalesce_workspace(int64_t num_rows, int64_t nnz);
+int gnn_csr_coalesce(int64_t num_rows, int64_t nnz, const int64_t *offsets, const int32_t *cols,
+                     int64_t *out_offsets, int32_t *out_cols, float *out_mult, int64_t *out_nnz,
+                     void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* Chung-Lu power-law edge draws of graph.py:256-261, bit-exact: numpy PCG64
+ * (state,inc given as 128-bit hi/lo words of the SeedSequence-seeded
+ * generator) position k -> double (raw>>11)*2^-53; src uses positions
+ * [0,m), dst [m,2m); endpoint = searchsorted(cdf, u, 'right').  cdf is the
+ * host-computed float64 CDF of graph.py:256-259 (length n). */
+size_t gnn_generate_powerlaw_workspace(int64_t n);
+int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t state_hi,
+                          uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src,
+                          int64_t *dst, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* ----------------------------------------------------------- sparse ops */
+/* A device CSR (or CSC, which is the CSR of the transpose). */
+typedef struct gnn_csr_view {
+  int64_t num_rows;
+  int64_t num_cols;
+  int64_t nnz;
+  const int64_t *offsets;     /* [num_rows+1] */
+  const int32_t *cols;        /* [nnz] column ids */
+  const float *vals;          /* [nnz*heads] edge values, or NULL (SpMMv: implicit 1, no |E| tensor) */
+  const int32_t *eid;         /* [nnz] or NULL: edge value of entry j is vals[eid[j]] (SpMMve^T) */
+  const int64_t *deg_offsets; /* degree source for GNN_EPI_NORM, NULL = offsets */
+} gnn_csr_view_t;
+
+/* Epilogue applied per output row v, in this order:
+ *   y  = acc                           (acc = sum_e val_e * X[col_e])
+ *   y *= 1/deg(v)       if NORM        (deg(v)==0 -> y = 0, no clamp buffer)
+ *   y += self_scale*S[v] if SELF       (GIN (1+eps) self term)
+ *   y += bias           if BIAS
+ *   y  = max(y,0)       if RELU
+ *   y  = M[v]>0 ? y : 0 if MASK        (ReLU backward against a saved activation)
+ *   y *= 1/pdeg(v)      if POSTNORM    (degree-norm of the NEXT backward SpMM's input)
+ */
+enum {
+  GNN_EPI_NORM = 1u << 0,
+  GNN_EPI_SELF = 1u << 1,
+  GNN_EPI_BIAS = 1u << 2,
+  GNN_EPI_RELU = 1u << 3,
+  GNN_EPI_MASK = 1u << 4,
+  GNN_EPI_POSTNORM = 1u << 5
+};
+typedef struct gnn_epilogue {
+  uint32_t flags;
+  float self_scale;
+  const float *self_x; /* [num_rows, ld_self] */
+  int64_t ld_self;
+  const float *bias; /* [K] */
+  const float *mask; /* [num_rows, ld_mask] */
+  int64_t ld_mask;
+  const int64_t *post_deg_offsets; /* [num_rows+1] */
+} gnn_epilogue_t;
+
+/* Per-graph SpMM schedule (built once, reused by every call; the build
+ * synchronises once to learn the list lengths so that gnn_spmm never does).
+ * The nnz range is cut into chunks of edges_per_warp edges, one warp each;
+ * rows spanning several chunks ("split" rows, the power-law mega rows) and
+ * empty rows are listed for the finishing passes. */
+typedef struct gnn_spmm_plan {
+  int64_t edges_per_warp;
+  int64_t num_warps;           /* ceil(nnz / edges_per_warp) */
+  int64_t num_split;
+  const int32_t *split_rows;   /* [num_split], caller-owned device memory */
+  int64_t num_empty;
+  const int32_t *empty_rows;   /* [num_empty], caller-owned device memory */
+} gnn_spmm_plan_t;
+
+size_t gnn_spmm_plan_workspace(int64_t num_rows);
+/* split_rows / empty_rows: device buffers of num_rows entries each. */
+int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *split_rows,
+                        int32_t *empty_rows, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
+                        gnn_stream_t stream);
+
+/* Y[num_rows,K] = epilogue(A . X), X[num_cols,K].  heads>=1 splits K into
+ * `heads` slices scaled by their own edge value (vals is [nnz,heads]).
+ * Deterministic (fixed summation order), no atomics on Y. */
+size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t K);
+int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+             const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
+             const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* X[v,:] /= deg(v) in place (deg 0 -> row zeroed). */
+int gnn_degree_norm_inplace(int64_t num_rows, const int64_t *offsets, float *X, int64_t ldx,
+                            int64_t K, gnn_stream_t stream);
+
+/* ---------------------------------------------------------- dense ops */
+/* C[M,N] = op(A) . B (+bias)(relu), fp32 in/out, fp32-accurate.
+ * trans_a = 0: A is [M,Kd] (lda);  trans_a = 1: A is [Kd,M] (lda), i.e. C = A^T B
+ * (the weight-gradient shape, reduction over the vertex dimension). */
+size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a);
+int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+             const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
+             int relu, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* out[N] = sum over rows of X[M,N] (deterministic two-level reduction). */
+size_t gnn_colsum_workspace(int64_t M, int64_t N);
+int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, void *ws,
+               size_t ws_bytes, gnn_stream_t stream);
+
+/* Backward helper of a GCN/GIN layer: out = (mask>0 ? X : 0) * 1/deg(row)
+ * (deg from deg_offsets; NULL = no norm; mask NULL = no mask) and, if colsum
+ * is non-NULL, colsum = column sums of the masked, un-normalised values (the
+ * bias gradient), deterministic.  out may alias X. */
+size_t gnn_mask_norm_colsum_workspace(int64_t M, int64_t N);
+int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+                         int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
+                         float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* Mean softmax cross-entropy over M rows of C logits: *loss (device) and,
+ * if dZ != NULL, dZ = (softmax(Z) - onehot(labels)) * grad_scale. */
+size_t gnn_softmax_xent_workspace(int64_t M);
+int gnn_softmax_xent(int64_t M, int64_t C, const float *Z, int64_t ldz, const int64_t *labels,
+                     float grad_scale, float *dZ, int64_t ldd, float *loss, void *ws,
+                     size_t ws_bytes, gnn_stream_t stream);
+
+/* Adam over a device table of parameters; the step counter lives on device
+ * (read for bias correction, then incremented) so the update can sit inside
+ * a captured CUDA graph. */
+typedef struct gnn_adam_param {
+  float *param;
+  const float *grad;
+  float *exp_avg;
+  float *exp_avg_sq;
+  int64_t numel;
+} gnn_adam_param_t;
+int gnn_adam_step(int nparams, const void *param_table /* device gnn_adam_param_t[nparams] */,
+                  float lr, float beta1, float beta2, float eps, float weight_decay,
+                  int64_t *step /* device */, gnn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNN_B200_H */

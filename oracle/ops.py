@@ -1,0 +1,158 @@
+"""float64 restatement of the GraphPy kernel semantics and GCN math (test
+oracle only; PARITY UNPINNED — the reference has no implementation of these,
+SURVEY.md §8c).  Semantics follow SURVEY.md Appendix A:
+
+* A[v,u] = multiplicity of (v,u) in CSR row v (duplicates summed, A.1);
+* deg(v) = offsets[v+1]-offsets[v]; degree-norm divides by deg(v), rows with
+  deg 0 give 0 (A.2, A.3);
+* SpMMv: Y = A X (no edge tensor); SpMMve: Y[v] =
+  sum_e ev_e X[col_e] per head;
+* SDDMM: out[e,h] = <X[row_e,h,:], Y[col_e,h,:]> (A.7);
+* GCN: Z = norm_A(X W) + b, ReLU between layers, mean cross-entropy (A.4).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_CHUNK = 1 << 24  # gathered elements per block (bounds oracle memory)
+
+
+def _row_blocks(offsets, K):
+    R = offsets.size - 1
+    per = max(1, _CHUNK // max(K, 1))
+    r0 = 0
+    while r0 < R:
+        # grow the block until it holds ~per edges (at least one row)
+        target = offsets[r0] + per
+        r1 = int(np.searchsorted(offsets, target, side="right")) - 1
+        r1 = min(max(r1, r0 + 1), R)
+        yield r0, r1
+        r0 = r1
+
+
+def spmm(offsets, cols, X, vals=None, heads=1, norm=False, deg_offsets=None):
+    """Y[v] = sum_{e in row v} w_e * X[cols_e] (w_e = vals[e, head] or 1)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    X = np.asarray(X, dtype=np.float64)
+    R = offsets.size - 1
+    K = X.shape[1]
+    F = K // heads
+    Y = np.zeros((R, K), dtype=np.float64)
+    for r0, r1 in _row_blocks(offsets, K):
+        e0, e1 = int(offsets[r0]), int(offsets[r1])
+        if e1 == e0:
+            continue
+        G = X[cols[e0:e1]]
+        if vals is not None:
+            w = np.asarray(vals[e0:e1], dtype=np.float64).reshape(e1 - e0, heads)
+            G = (G.reshape(e1 - e0, heads, F) * w[:, :, None]).reshape(e1 - e0, K)
+        starts = offsets[r0:r1] - e0
+        nz = np.nonzero(offsets[r0 + 1:r1 + 1] > offsets[r0:r1])[0]
+        Y[r0 + nz] = np.add.reduceat(G, starts[nz], axis=0)
+    if norm:
+        d = np.diff(offsets if deg_offsets is None else np.asarray(deg_offsets)).astype(np.float64)
+        inv = np.divide(1.0, d, out=np.zeros_like(d), where=d > 0)
+        Y *= inv[:, None]
+    return Y
+
+
+def degree_norm(offsets, X):
+    d = np.diff(np.asarray(offsets)).astype(np.float64)
+    inv = np.divide(1.0, d, out=np.zeros_like(d), where=d > 0)
+    return np.asarray(X, dtype=np.float64) * inv[:, None]
+
+
+def sddmm(offsets, cols, X, Y, heads=1):
+    """out[e,h] = <X[row_e,h,:], Y[col_e,h,:]> in CSR edge order."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    X = np.asarray(X, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    K = X.shape[1]
+    F = K // heads
+    E = int(offsets[-1])
+    out = np.zeros((E, heads), dtype=np.float64)
+    rows = np.repeat(np.arange(offsets.size - 1), np.diff(offsets))
+    step = max(1, _CHUNK // max(K, 1))
+    for e0 in range(0, E, step):
+        e1 = min(E, e0 + step)
+        p = X[rows[e0:e1]].reshape(-1, heads, F) * Y[cols[e0:e1]].reshape(-1, heads, F)
+        out[e0:e1] = p.sum(axis=2)
+    return out
+
+
+def edge_softmax(offsets, s):
+    """alpha_e = exp(s_e - max_row) / sum_row exp(...) per head, CSR rows."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    s = np.asarray(s, dtype=np.float64)
+    s2 = s.reshape(s.shape[0], -1)
+    out = np.zeros_like(s2)
+    nz = np.nonzero(np.diff(offsets) > 0)[0]
+    if nz.size == 0:
+        return out.reshape(s.shape)
+    starts = offsets[nz]
+    deg = np.diff(offsets)[nz]
+    mx = np.maximum.reduceat(s2, starts, axis=0)
+    ex = np.exp(s2 - np.repeat(mx, deg, axis=0))
+    sm = np.add.reduceat(ex, starts, axis=0)
+    out[:] = ex / np.repeat(sm, deg, axis=0)
+    return out.reshape(s.shape)
+
+
+def edge_softmax_backward(offsets, alpha, dalpha):
+    """dS = alpha * (dalpha - sum_row alpha * dalpha)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    a = np.asarray(alpha, dtype=np.float64).reshape(alpha.shape[0], -1)
+    da = np.asarray(dalpha, dtype=np.float64).reshape(a.shape)
+    nz = np.nonzero(np.diff(offsets) > 0)[0]
+    out = np.zeros_like(a)
+    if nz.size:
+        starts = offsets[nz]
+        deg = np.diff(offsets)[nz]
+        dot = np.add.reduceat(a * da, starts, axis=0)
+        out[:] = a * (da - np.repeat(dot, deg, axis=0))
+    return out.reshape(np.shape(alpha))
+
+
+def cross_entropy(logits, labels):
+    """Mean softmax cross-entropy and its gradient w.r.t. the logits."""
+    z = np.asarray(logits, dtype=np.float64)
+    z = z - z.max(axis=1, keepdims=True)
+    lse = np.log(np.exp(z).sum(axis=1))
+    n = z.shape[0]
+    loss = float(np.mean(lse - z[np.arange(n), labels]))
+    p = np.exp(z - lse[:, None])
+    p[np.arange(n), labels] -= 1.0
+    return loss, p / n
+
+
+def gcn2_step(offsets, cols, t_offsets, t_cols, X, W1, b1, W2, b2, labels):
+    """2-layer GCN forward + backward (Appendix A.4): returns loss, logits and
+    the parameter gradients, all float64."""
+    X = np.asarray(X, dtype=np.float64)
+    H1 = X @ W1
+    P1 = spmm(offsets, cols, H1, norm=True)
+    Z1 = P1 + b1
+    Y1 = np.maximum(Z1, 0.0)
+    H2 = Y1 @ W2
+    Z2 = spmm(offsets, cols, H2, norm=True) + b2
+    loss, dZ2 = cross_entropy(Z2, labels)
+    db2 = dZ2.sum(axis=0)
+    dH2 = spmm(t_offsets, t_cols, degree_norm(offsets, dZ2))
+    dW2 = Y1.T @ dH2
+    dY1 = dH2 @ W2.T
+    dZ1 = dY1 * (Z1 > 0)
+    db1 = dZ1.sum(axis=0)
+    dH1 = spmm(t_offsets, t_cols, degree_norm(offsets, dZ1))
+    dW1 = X.T @ dH1
+    return {"loss": loss, "logits": Z2, "W1": dW1, "b1": db1, "W2": dW2, "b2": db2}
+
+
+def close(gpu, ref, ref_abs=None, rtol=1e-5):
+    """Appendix A.8 criterion: |gpu-ref| <= rtol * max(|ref|, ref_abs)."""
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = np.abs(ref) if ref_abs is None else np.maximum(np.abs(ref), np.asarray(ref_abs))
+    err = np.abs(gpu - ref)
+    ok = err <= rtol * scale + 1e-30
+    return bool(np.all(ok)), float(np.max(err / np.maximum(scale, 1e-30))) if err.size else 0.0

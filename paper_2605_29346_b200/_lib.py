@@ -1,0 +1,227 @@
+"""ctypes binding of the C ABI in include/gnn_b200.h.
+
+This is the exact binding a maintainer of the reference would add on their
+side: plain pointers, sizes and a stream handle.  The
+library is loaded from the package directory (built in-tree by
+``__graft_entry__.build()`` / ``make -C paper_2605_29346_b200/csrc``); if it is
+missing, or there is no CUDA device, every op raises ``ExtensionMissing`` —
+there is no CPU fallback on the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from .errors import ExtensionMissing, RangeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgnnb200.so")
+
+GNN_OK = 0
+GNN_ERR_INVALID_ARGUMENT = 1
+GNN_ERR_CSR_INVARIANT = 2
+GNN_ERR_RANGE = 3
+GNN_ERR_INDEX = 4
+GNN_ERR_WORKSPACE = 5
+GNN_ERR_CUDA = 6
+GNN_ERR_UNSUPPORTED = 7
+GNN_ERR_SOURCE_RANGE = 8
+
+EPI_NORM = 1 << 0
+EPI_SELF = 1 << 1
+EPI_BIAS = 1 << 2
+EPI_RELU = 1 << 3
+EPI_MASK = 1 << 4
+EPI_POSTNORM = 1 << 5
+
+c_i64 = C.c_int64
+c_u64 = C.c_uint64
+c_ptr = C.c_void_p
+c_sz = C.c_size_t
+c_int = C.c_int
+
+
+class CsrView(C.Structure):
+    _fields_ = [
+        ("num_rows", c_i64),
+        ("num_cols", c_i64),
+        ("nnz", c_i64),
+        ("offsets", c_ptr),
+        ("cols", c_ptr),
+        ("vals", c_ptr),
+        ("eid", c_ptr),
+        ("deg_offsets", c_ptr),
+    ]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [
+        ("flags", C.c_uint32),
+        ("self_scale", C.c_float),
+        ("self_x", c_ptr),
+        ("ld_self", c_i64),
+        ("bias", c_ptr),
+        ("mask", c_ptr),
+        ("ld_mask", c_i64),
+        ("post_deg_offsets", c_ptr),
+    ]
+
+
+class SpmmPlan(C.Structure):
+    _fields_ = [
+        ("edges_per_warp", c_i64),
+        ("num_warps", c_i64),
+        ("num_split", c_i64),
+        ("split_rows", c_ptr),
+        ("num_empty", c_i64),
+        ("empty_rows", c_ptr),
+    ]
+
+
+# name -> (restype, argtypes).  Keep in sync with include/gnn_b200.h; the CPU
+# test suite checks that every declared symbol is exported.
+SIGNATURES = {
+    "gnn_abi_version": (c_int, []),
+    "gnn_strerror": (C.c_char_p, [c_int]),
+    "gnn_last_cuda_error": (c_int, []),
+    "gnn_device_sm_count": (c_int, []),
+    "gnn_launch_counter": (c_i64, []),
+    "gnn_csr_from_edges_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_csr_from_edges": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
+    "gnn_subgraph_csr_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_subgraph_csr": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
+    "gnn_csr_validate_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_csr_validate": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
+    "gnn_degrees": (c_int, [c_i64, c_ptr, c_ptr, c_ptr]),
+    "gnn_csc_from_csr_workspace": (c_sz, [c_i64, c_i64, c_i64]),
+    "gnn_csc_from_csr": (
+        c_int,
+        [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_csr_coalesce_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_csr_coalesce": (
+        c_int,
+        [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, C.POINTER(c_i64), c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_generate_powerlaw_workspace": (c_sz, [c_i64]),
+    "gnn_generate_powerlaw": (
+        c_int,
+        [c_i64, c_i64, c_ptr, c_u64, c_u64, c_u64, c_u64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_spmm_plan_workspace": (c_sz, [c_i64]),
+    "gnn_spmm_plan_build": (
+        c_int,
+        [C.POINTER(CsrView), c_i64, c_ptr, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_spmm_workspace": (c_sz, [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64]),
+    "gnn_spmm": (
+        c_int,
+        [
+            C.POINTER(CsrView),
+            C.POINTER(SpmmPlan),
+            c_i64,
+            c_ptr,
+            c_i64,
+            c_ptr,
+            c_i64,
+            c_i64,
+            C.POINTER(Epilogue),
+            c_ptr,
+            c_sz,
+            c_ptr,
+        ],
+    ),
+    "gnn_degree_norm_inplace": (c_int, [c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
+    "gnn_gemm_workspace": (c_sz, [c_i64, c_i64, c_i64, c_int]),
+    "gnn_gemm": (
+        c_int,
+        [c_i64, c_i64, c_i64, c_ptr, c_i64, c_int, c_ptr, c_i64, c_int, c_ptr, c_i64, c_ptr,
+         c_int, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_colsum_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_colsum": (c_int, [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr]),
+    "gnn_mask_norm_colsum_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_mask_norm_colsum": (
+        c_int,
+        [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_softmax_xent_workspace": (c_sz, [c_i64]),
+    "gnn_softmax_xent": (
+        c_int,
+        [c_i64, c_i64, c_ptr, c_i64, c_ptr, C.c_float, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_adam_step": (
+        c_int,
+        [c_int, c_ptr, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, c_ptr, c_ptr],
+    ),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(require_cuda: bool = True):
+    """Load libgnnb200.so and bind its signatures (cached)."""
+    global _lib
+    if require_cuda and not torch.cuda.is_available():
+        raise ExtensionMissing("no CUDA device: the sparse GNN path has no CPU fallback")
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ExtensionMissing(
+                    f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def lib():
+    return load_library(True)
+
+
+def strerror(status: int) -> str:
+    return load_library(False).gnn_strerror(status).decode()
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a gnn_status to the reference's exception taxonomy."""
+    if status == GNN_OK:
+        return
+    msg = f"{what}: {strerror(status)}" if what else strerror(status)
+    if status == GNN_ERR_RANGE:
+        raise RangeError("target vertex id out of range")
+    if status == GNN_ERR_INDEX:
+        raise IndexError("edge source local id out of range")
+    if status == GNN_ERR_CSR_INVARIANT:
+        raise ValueError("offsets must start at 0, end at num_edges and be nondecreasing")
+    if status == GNN_ERR_SOURCE_RANGE:
+        raise ValueError("source vertex id outside [0, num_vertices)")
+    if status in (GNN_ERR_INVALID_ARGUMENT, GNN_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if status == GNN_ERR_CUDA:
+        raise RuntimeError(f"{msg} (cudaError {load_library(False).gnn_last_cuda_error()})")
+    raise RuntimeError(msg)
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Scratch from torch's caching allocator, so peak-memory accounting sees it."""
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)

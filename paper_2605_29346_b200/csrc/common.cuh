@@ -1,0 +1,136 @@
+// Shared device/host helpers for libgnnb200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gnn_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libgnnb200 targets sm_100a only"
+#endif
+
+namespace gnn {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Last CUDA error seen by a GNN_ERR_CUDA return (per process; informative only).
+void set_cuda_error(cudaError_t e);
+
+#define GNN_CUDA_TRY(expr)                     \
+  do {                                         \
+    cudaError_t _e = (expr);                   \
+    if (_e != cudaSuccess) {                   \
+      ::gnn::set_cuda_error(_e);               \
+      return GNN_ERR_CUDA;                     \
+    }                                          \
+  } while (0)
+
+// Every kernel launch is followed by GNN_LAUNCH_CHECK(), which also bumps the
+// process-wide launch counter (gnn_launch_counter()).
+void note_launch();
+#define GNN_LAUNCH_CHECK()                    \
+  do {                                        \
+    ::gnn::note_launch();                     \
+    GNN_CUDA_TRY(cudaGetLastError());         \
+  } while (0)
+
+#define GNN_TRY(expr)        \
+  do {                       \
+    int _s = (expr);         \
+    if (_s != GNN_OK) return _s; \
+  } while (0)
+
+inline cudaStream_t as_stream(gnn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+// Bump allocator over a caller-provided workspace.
+struct WsArena {
+  char *base;
+  size_t cap;
+  size_t used = 0;
+  WsArena(void *b, size_t c) : base(static_cast<char *>(b)), cap(c) {}
+  template <class T>
+  T *take(int64_t count) {
+    size_t off = align_up(used, 256);
+    size_t bytes = static_cast<size_t>(count > 0 ? count : 0) * sizeof(T);
+    used = off + bytes;
+    return reinterpret_cast<T *>(base + off);
+  }
+  bool ok() const { return used <= cap; }
+};
+
+// Size-only twin of WsArena for *_workspace() queries.
+struct WsCounter {
+  size_t used = 0;
+  template <class T>
+  void take(int64_t count) {
+    used = align_up(used, 256) + static_cast<size_t>(count > 0 ? count : 0) * sizeof(T);
+  }
+};
+
+int sm_count();
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Read-only, L1-allocating 128-bit gather (feature rows are reused across edges).
+__device__ __forceinline__ float4 ldg_f4(const float *p) {
+  return __ldg(reinterpret_cast<const float4 *>(p));
+}
+// Streaming loads for data touched once (index arrays).
+__device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4_fma(float s, float4 b, float4 a) {
+  return make_float4(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y), fmaf(s, b.z, a.z), fmaf(s, b.w, a.w));
+}
+
+// First index i in [lo,hi) with a[i] > x (upper bound), a nondecreasing.
+template <class T>
+__device__ __forceinline__ int64_t upper_bound_dev(const T *a, int64_t lo, int64_t hi, T x) {
+  while (lo < hi) {
+    int64_t mid = lo + ((hi - lo) >> 1);
+    if (a[mid] <= x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+// First index i in [lo,hi) with a[i] >= x (lower bound).
+template <class T>
+__device__ __forceinline__ int64_t lower_bound_dev(const T *a, int64_t lo, int64_t hi, T x) {
+  while (lo < hi) {
+    int64_t mid = lo + ((hi - lo) >> 1);
+    if (a[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// ---- device-wide primitives (scan.cu) ----
+// Exclusive scan of int64 values: out[i] = sum_{j<i} in[i]; out[n] = total if out has n+1 slots
+// (write_total). in and out may alias.
+size_t scan_i64_workspace(int64_t n);
+int exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, bool write_total, void *ws,
+                       size_t ws_bytes, cudaStream_t st);
+size_t scan_u32_workspace(int64_t n);
+int exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws, size_t ws_bytes,
+                       cudaStream_t st);
+
+}  // namespace gnn

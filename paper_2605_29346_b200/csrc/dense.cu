@@ -1,0 +1,483 @@
+// Dense pieces of the path: fp32 GEMM for the X.W transforms (SIMT fallback
+// used where the tcgen05 kernel does not apply), split-K weight gradients, and
+// deterministic column sums (bias gradients).
+#include "common.cuh"
+
+namespace gnn {
+namespace {
+
+constexpr int kGemmRows = 256;  // rows of C per CTA (one per thread)
+constexpr int kGemmBK = 32;
+
+// C[m, n0:n0+NT] for one row per thread; A tile staged through shared memory
+// (coalesced either orientation), B tile broadcast from shared memory.
+template <int NT>
+__global__ void __launch_bounds__(kGemmRows) gemm_rowtile_kernel(
+    int64_t M, int64_t N, int64_t Kd, const float *__restrict__ A, int64_t lda, int trans_a,
+    const float *__restrict__ B, int64_t ldb, int trans_b, float *__restrict__ C, int64_t ldc,
+    const float *__restrict__ bias, int relu, int64_t k_per_split, float *partials) {
+  __shared__ float As[kGemmRows][kGemmBK + 1];
+  __shared__ __align__(16) float Bs[kGemmBK][NT];
+  const int tid = threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.x * kGemmRows;
+  const int64_t n0 = (int64_t)blockIdx.y * NT;
+  const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+  const int64_t kend = min(Kd, kbeg + k_per_split);
+  float acc[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j] = 0.f;
+
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kGemmBK) {
+    // ---- A tile: rows m0..m0+255, k0..k0+31
+    if (!trans_a) {
+#pragma unroll 4
+      for (int i = 0; i < kGemmBK; ++i) {
+        int idx = i * kGemmRows + tid;
+        int r = idx / kGemmBK, k = idx % kGemmBK;
+        int64_t gm = m0 + r, gk = k0 + k;
+        As[r][k] = (gm < M && gk < kend) ? A[gm * lda + gk] : 0.f;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = 0; i < kGemmBK; ++i) {
+        int64_t gm = m0 + tid, gk = k0 + i;
+        As[tid][i] = (gm < M && gk < kend) ? A[gk * lda + gm] : 0.f;
+      }
+    }
+    // ---- B tile: k0..k0+31, n0..n0+NT-1
+    for (int idx = tid; idx < kGemmBK * NT; idx += kGemmRows) {
+      int k = idx / NT, n = idx % NT;
+      int64_t gk = k0 + k, gn = n0 + n;
+      float v = 0.f;
+      if (gk < kend && gn < N) v = trans_b ? B[gn * ldb + gk] : B[gk * ldb + gn];
+      Bs[k][n] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < kGemmBK; ++k) {
+      float a = As[tid][k];
+#pragma unroll
+      for (int j = 0; j < NT; j += 4) {
+        float4 b = *reinterpret_cast<const float4 *>(&Bs[k][j]);
+        acc[j] = fmaf(a, b.x, acc[j]);
+        acc[j + 1] = fmaf(a, b.y, acc[j + 1]);
+        acc[j + 2] = fmaf(a, b.z, acc[j + 2]);
+        acc[j + 3] = fmaf(a, b.w, acc[j + 3]);
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t m = m0 + tid;
+  if (m >= M) return;
+  if (partials) {
+    float *p = partials + ((int64_t)blockIdx.z * M + m) * N;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      if (n0 + j < N) p[n0 + j] = acc[j];
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    int64_t n = n0 + j;
+    if (n < N) {
+      float v = acc[j];
+      if (bias) v += bias[n];
+      if (relu) v = fmaxf(v, 0.f);
+      C[m * ldc + n] = v;
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int64_t splits,
+                                     const float *__restrict__ partials, float *C, int64_t ldc,
+                                     const float *__restrict__ bias, int relu) {
+  const int64_t total = M * N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = t / N, n = t % N;
+    float s = 0.f;
+    for (int64_t z = 0; z < splits; ++z) s += partials[z * total + t];
+    if (bias) s += bias[n];
+    if (relu) s = fmaxf(s, 0.f);
+    C[m * ldc + n] = s;
+  }
+}
+
+struct GemmShape {
+  int nt;
+  int64_t mtiles, ntiles, splits, k_per_split;
+};
+
+GemmShape gemm_shape(int64_t M, int64_t N, int64_t Kd) {
+  GemmShape g;
+  g.nt = N <= 16 ? 16 : (N <= 32 ? 32 : 64);
+  g.mtiles = ceil_div(M, kGemmRows);
+  g.ntiles = ceil_div(N, g.nt);
+  int64_t ctas = g.mtiles * g.ntiles;
+  int64_t want = 2 * (int64_t)sm_count();
+  g.splits = 1;
+  if (ctas < want && Kd >= 4 * kGemmBK) {
+    g.splits = ceil_div(want, ctas);
+    int64_t max_splits = ceil_div(Kd, 4 * kGemmBK);
+    if (g.splits > max_splits) g.splits = max_splits;
+  }
+  g.k_per_split = ceil_div(ceil_div(Kd, g.splits), kGemmBK) * kGemmBK;
+  g.splits = ceil_div(Kd, g.k_per_split);
+  if (g.splits < 1) g.splits = 1;
+  return g;
+}
+
+constexpr int kColsumRows = 4096;
+__global__ void colsum_partial_kernel(int64_t M, int64_t N, const float *__restrict__ X,
+                                      int64_t ldx, float *partials) {
+  // block b sums rows [b*kColsumRows, ...) for every column; threads stride columns
+  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
+  const int64_t r1 = min(M, r0 + kColsumRows);
+  for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+    float s = 0.f;
+    for (int64_t r = r0; r < r1; ++r) s += X[r * ldx + c];
+    partials[(int64_t)blockIdx.x * N + c] = s;
+  }
+}
+// narrow N: threads cover (row-slot, column) pairs, then a fixed-order smem reduction
+template <int NCOL>
+__global__ void __launch_bounds__(256) colsum_narrow_kernel(int64_t M, int64_t N,
+                                                            const float *__restrict__ X,
+                                                            int64_t ldx, float *partials) {
+  constexpr int SLOTS = 256 / NCOL;
+  __shared__ float red[SLOTS][NCOL];
+  const int c = threadIdx.x % NCOL, s = threadIdx.x / NCOL;
+  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
+  const int64_t r1 = min(M, r0 + kColsumRows);
+  float acc = 0.f;
+  if (c < N)
+    for (int64_t r = r0 + s; r < r1; r += SLOTS) acc += X[r * ldx + c];
+  red[s][c] = acc;
+  __syncthreads();
+  if (s == 0 && c < N) {
+    float t = 0.f;
+    for (int k = 0; k < SLOTS; ++k) t += red[k][c];
+    partials[(int64_t)blockIdx.x * N + c] = t;
+  }
+}
+__global__ void colsum_final_kernel(int64_t nb, int64_t N, const float *__restrict__ partials,
+                                    float *out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t b = 0; b < nb; ++b) s += partials[b * N + c];
+    out[c] = s;
+  }
+}
+
+}  // namespace
+
+// Exposed for the tcgen05 path's fallbacks.
+int gemm_simt(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+              const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
+              int relu, void *ws, size_t ws_bytes, cudaStream_t st) {
+  GemmShape g = gemm_shape(M, N, Kd);
+  float *partials = nullptr;
+  if (g.splits > 1) {
+    if (ws_bytes < sizeof(float) * (size_t)(g.splits * M * N)) return GNN_ERR_WORKSPACE;
+    partials = static_cast<float *>(ws);
+  }
+  dim3 grid((unsigned)g.mtiles, (unsigned)g.ntiles, (unsigned)g.splits);
+#define GNN_GEMM_LAUNCH(NT)                                                                    \
+  gemm_rowtile_kernel<NT><<<grid, kGemmRows, 0, st>>>(M, N, Kd, A, lda, trans_a, B, ldb,       \
+                                                      trans_b, C, ldc, bias, relu,             \
+                                                      g.k_per_split, partials)
+  if (g.nt == 16)
+    GNN_GEMM_LAUNCH(16);
+  else if (g.nt == 32)
+    GNN_GEMM_LAUNCH(32);
+  else
+    GNN_GEMM_LAUNCH(64);
+#undef GNN_GEMM_LAUNCH
+  GNN_LAUNCH_CHECK();
+  if (partials) {
+    int64_t total = M * N;
+    int64_t nblk = ceil_div(total, 256), cap = (int64_t)sm_count() * 8;
+    unsigned blocks = (unsigned)(nblk < cap ? nblk : cap);
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, g.splits, partials, C, ldc, bias, relu);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+size_t gemm_simt_workspace(int64_t M, int64_t N, int64_t Kd) {
+  GemmShape g = gemm_shape(M, N, Kd);
+  return g.splits > 1 ? sizeof(float) * (size_t)(g.splits * M * N) + 256 : 256;
+}
+
+}  // namespace gnn
+
+using namespace gnn;
+
+extern "C" {
+
+size_t gnn_colsum_workspace(int64_t M, int64_t N) {
+  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, kColsumRows) * (N > 0 ? N : 1)) + 256;
+}
+
+int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, void *ws,
+               size_t ws_bytes, gnn_stream_t stream) {
+  if (M < 0 || N < 0 || ldx < N || (N > 0 && !out) || (M > 0 && N > 0 && !X))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (N == 0) return GNN_OK;
+  if (ws_bytes < gnn_colsum_workspace(M, N)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  if (M == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * N, st));
+    return GNN_OK;
+  }
+  int64_t nb = ceil_div(M, kColsumRows);
+  float *partials = static_cast<float *>(ws);
+  if (N <= 16)
+    colsum_narrow_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+  else if (N <= 64)
+    colsum_narrow_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+  else
+    colsum_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+  GNN_LAUNCH_CHECK();
+  colsum_final_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, out);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a) {
+  (void)trans_a;
+  return gemm_simt_workspace(M, N, Kd);
+}
+
+int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+             const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
+             int relu, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (M < 0 || N < 0 || Kd < 0 || (M > 0 && N > 0 && (!C || ldc < N)) ||
+      (M > 0 && Kd > 0 && (!A || (trans_a ? lda < M : lda < Kd))) ||
+      (N > 0 && Kd > 0 && (!B || (trans_b ? ldb < Kd : ldb < N))))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (M == 0 || N == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
+                   st);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------
+// Fused row-wise helpers of the GNN layers' backward pass and loss.
+namespace gnn {
+namespace {
+
+constexpr int kRowBlock = 2048;  // rows per CTA for the partial column sums
+
+__device__ __forceinline__ float inv_deg_of(const int64_t *off, int64_t r) {
+  int64_t d = off[r + 1] - off[r];
+  return d > 0 ? 1.0f / (float)d : 0.0f;
+}
+
+// out = (mask>0 ? X : 0) * (1/deg(row) if deg_offsets); colsum partials of the
+// masked, un-normalised values (the bias gradient).  Threads: (slot, column).
+template <int NCOL>
+__global__ void __launch_bounds__(256) mask_norm_colsum_kernel(
+    int64_t M, int64_t N, const float *__restrict__ X, int64_t ldx, const float *__restrict__ mask,
+    int64_t ldm, const int64_t *__restrict__ deg_offsets, float *out, int64_t ldo,
+    float *partials) {
+  constexpr int SLOTS = 256 / NCOL;
+  __shared__ float red[SLOTS][NCOL];
+  const int s = threadIdx.x / NCOL;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowBlock;
+  const int64_t r1 = min(M, r0 + kRowBlock);
+  for (int64_t c0 = 0; c0 < N; c0 += NCOL) {
+    const int64_t c = c0 + threadIdx.x % NCOL;
+    float acc = 0.f;
+    if (c < N) {
+      for (int64_t r = r0 + s; r < r1; r += SLOTS) {
+        float v = X[r * ldx + c];
+        if (mask && !(mask[r * ldm + c] > 0.f)) v = 0.f;
+        acc += v;
+        if (out) out[r * ldo + c] = deg_offsets ? v * inv_deg_of(deg_offsets, r) : v;
+      }
+    }
+    red[s][threadIdx.x % NCOL] = acc;
+    __syncthreads();
+    if (s == 0 && c < N && partials) {
+      float t = 0.f;
+      for (int k = 0; k < SLOTS; ++k) t += red[k][threadIdx.x % NCOL];
+      partials[(int64_t)blockIdx.x * N + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void sum_partials_kernel(int64_t nb, int64_t N, const float *__restrict__ partials,
+                                    float *out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t b = 0; b < nb; ++b) s += partials[b * N + c];
+    out[c] = s;
+  }
+}
+
+// One warp per row: numerically stable log-softmax cross-entropy; writes
+// dlogits = (softmax - onehot) * scale and a per-CTA partial of the loss.
+__global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t C,
+                                                           const float *__restrict__ Z,
+                                                           int64_t ldz,
+                                                           const int64_t *__restrict__ labels,
+                                                           float scale, float *dZ, int64_t ldd,
+                                                           float *loss_partials) {
+  __shared__ float wl[8];
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  float lsum = 0.f;
+  const int64_t rows_per_cta = 8 * 16;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  for (int64_t r = r0 + warp; r < min(M, r0 + rows_per_cta); r += 8) {
+    const float *z = Z + r * ldz;
+    float mx = -INFINITY;
+    for (int64_t c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    float se = 0.f;
+    for (int64_t c = lane; c < C; c += 32) se += expf(z[c] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
+    const float lse = mx + logf(se);
+    const int64_t y = labels[r];
+    if (lane == 0) lsum += lse - z[y];
+    if (dZ) {
+      for (int64_t c = lane; c < C; c += 32) {
+        float p = expf(z[c] - lse);
+        dZ[r * ldd + c] = (p - (c == y ? 1.f : 0.f)) * scale;
+      }
+    }
+  }
+  if (lane == 0) wl[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += wl[k];
+    loss_partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void loss_final_kernel(int64_t nb, const float *__restrict__ partials, float scale,
+                                  float *loss) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < nb; i += 256) s += (double)partials[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = (float)(red[0] * (double)scale);
+}
+
+struct AdamParam {
+  float *p;
+  const float *g;
+  float *m;
+  float *v;
+  int64_t n;
+};
+
+// Step count lives on device so a captured CUDA graph replays correctly.
+__global__ void adam_kernel(const AdamParam *__restrict__ params, int nparams, float lr,
+                            float beta1, float beta2, float eps, float weight_decay,
+                            const int64_t *__restrict__ step) {
+  const float t = (float)(*step + 1);
+  const float bc1 = 1.f - powf(beta1, t), bc2 = 1.f - powf(beta2, t);
+  for (int i = blockIdx.y; i < nparams; i += gridDim.y) {
+    AdamParam P = params[i];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P.n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      float g = P.g[j] + weight_decay * P.p[j];
+      float m = beta1 * P.m[j] + (1.f - beta1) * g;
+      float v = beta2 * P.v[j] + (1.f - beta2) * g * g;
+      P.m[j] = m;
+      P.v[j] = v;
+      P.p[j] -= lr * (m / bc1) / (sqrtf(v / bc2) + eps);
+    }
+  }
+}
+
+__global__ void step_increment_kernel(int64_t *step) { *step += 1; }
+
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+size_t gnn_mask_norm_colsum_workspace(int64_t M, int64_t N) {
+  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, kRowBlock) * (N > 0 ? N : 1)) + 256;
+}
+
+int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+                         int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
+                         float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (M < 0 || N <= 0 || ldx < N || (mask && ldm < N) || (out && ldo < N) || (M > 0 && !X))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (colsum && ws_bytes < gnn_mask_norm_colsum_workspace(M, N)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  if (M == 0) {
+    if (colsum) GNN_CUDA_TRY(cudaMemsetAsync(colsum, 0, sizeof(float) * N, st));
+    return GNN_OK;
+  }
+  const int64_t nb = ceil_div(M, kRowBlock);
+  float *partials = colsum ? static_cast<float *>(ws) : nullptr;
+  if (N <= 16)
+    mask_norm_colsum_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                             deg_offsets, out, ldo, partials);
+  else if (N <= 64)
+    mask_norm_colsum_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                             deg_offsets, out, ldo, partials);
+  else
+    mask_norm_colsum_kernel<256><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                              deg_offsets, out, ldo, partials);
+  GNN_LAUNCH_CHECK();
+  if (colsum) {
+    sum_partials_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, colsum);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+size_t gnn_softmax_xent_workspace(int64_t M) {
+  return sizeof(float) * (size_t)ceil_div(M > 0 ? M : 1, 128) + 256;
+}
+
+int gnn_softmax_xent(int64_t M, int64_t C, const float *Z, int64_t ldz, const int64_t *labels,
+                     float grad_scale, float *dZ, int64_t ldd, float *loss, void *ws,
+                     size_t ws_bytes, gnn_stream_t stream) {
+  if (M <= 0 || C <= 0 || !Z || ldz < C || !labels || !loss || (dZ && ldd < C))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_softmax_xent_workspace(M)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int64_t nb = ceil_div(M, 128);
+  float *partials = static_cast<float *>(ws);
+  softmax_xent_kernel<<<(unsigned)nb, 256, 0, st>>>(M, C, Z, ldz, labels, grad_scale, dZ, ldd,
+                                                    partials);
+  GNN_LAUNCH_CHECK();
+  loss_final_kernel<<<1, 256, 0, st>>>(nb, partials, 1.0f / (float)M, loss);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_adam_step(int nparams, const void *param_table, float lr, float beta1, float beta2,
+                  float eps, float weight_decay, int64_t *step, gnn_stream_t stream) {
+  if (nparams <= 0 || !param_table || !step) return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  dim3 grid(64u, (unsigned)(nparams < 65535 ? nparams : 65535));
+  adam_kernel<<<grid, 256, 0, st>>>(static_cast<const AdamParam *>(param_table), nparams, lr,
+                                    beta1, beta2, eps, weight_decay, step);
+  GNN_LAUNCH_CHECK();
+  step_increment_kernel<<<1, 1, 0, st>>>(step);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,741 @@
+// Device graph builders: stable counting sort (LSD radix) of edge pairs into
+// CSR, the transposed CSR (CSC) with edge ids, multigraph coalescing,
+// make_csr validation, degrees, and the bit-exact PCG64 power-law generator.
+//
+// Reference semantics:
+//   csr_from_edges      graph.py:106-114  (bincount -> cumsum -> argsort(kind="stable"))
+//   make_csr            graph.py:91-103   (ValueError / RangeError)
+//   build_subgraph_csr  sampler.py:242-256 (IndexError on source range)
+//   generate/power-law  graph.py:254-262  (PCG64 stream, searchsorted side="right")
+//
+// Stability argument: every radix pass ranks the items of a tile in original
+// order (warp-major rounds of 32 consecutive items, __match_any_sync peers,
+// warp-private running counts), and tiles are laid out digit-major in the
+// scanned count table, so each pass is a stable counting sort; LSD passes of
+// stable sorts give the stable sort by the full key = argsort(kind="stable").
+#include "common.cuh"
+
+namespace gnn {
+namespace {
+
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsIpt = 16;
+constexpr int kRsTile = kRsThreads * kRsIpt;  // 4096 items per tile
+constexpr int kRsRounds = kRsIpt;            // rounds of 32 items per warp
+
+enum SrcKind : int { SRC_I64 = 0, SRC_I32 = 1, SRC_IOTA = 2 };
+
+struct SrcDesc {
+  int kind;
+  const void *p;
+};
+
+struct PassArgs {
+  int64_t n;
+  int64_t ntiles;
+  int shift;
+  SrcDesc key;
+  int64_t key_limit;  // keys are clamped into [0, key_limit) for memory safety
+  int nvals;
+  SrcDesc val[2];
+  int32_t *key_out;
+  int32_t *val_out[2];
+  uint32_t *counts;        // [R][ntiles]; raw counts (hist) / scanned bases (scatter)
+  long long *minmax;       // [4] kmin,kmax,v0min,v0max, or null
+};
+
+__device__ __forceinline__ int64_t load_src_raw(const SrcDesc &s, int64_t i) {
+  if (s.kind == SRC_I64) return static_cast<const int64_t *>(s.p)[i];
+  if (s.kind == SRC_I32) return static_cast<const int32_t *>(s.p)[i];
+  return i;
+}
+
+__device__ __forceinline__ int32_t clamp_key(int64_t k, int64_t limit) {
+  k = k < 0 ? 0 : k;
+  k = k >= limit ? limit - 1 : k;
+  return static_cast<int32_t>(k);
+}
+
+__device__ __forceinline__ void block_minmax(long long lo, long long hi, long long *dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFull, lo, o));
+    hi = max(hi, __shfl_xor_sync(kFull, hi, o));
+  }
+  if (lane_id() == 0) {
+    atomicMin(dst, lo);
+    atomicMax(dst + 1, hi);
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(PassArgs a) {
+  constexpr int R = 1 << BITS;
+  extern __shared__ uint32_t smem_u32[];
+  uint32_t *wh = smem_u32;  // [kRsWarps][R]
+  const int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRsWarps * R; i += kRsThreads) wh[i] = 0;
+  __syncthreads();
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kRsTile + (int64_t)w * 32 * kRsRounds + lane_id();
+  long long kmin = LLONG_MAX, kmax = LLONG_MIN;
+#pragma unroll 4
+  for (int r = 0; r < kRsRounds; ++r) {
+    int64_t i = base + (int64_t)r * 32;
+    if (i < a.n) {
+      int64_t raw = load_src_raw(a.key, i);
+      kmin = min(kmin, (long long)raw);
+      kmax = max(kmax, (long long)raw);
+      int32_t k = clamp_key(raw, a.key_limit);
+      atomicAdd(&wh[w * R + ((k >> a.shift) & (R - 1))], 1u);
+    }
+  }
+  if (a.minmax) block_minmax(kmin, kmax, a.minmax);
+  __syncthreads();
+  for (int d = threadIdx.x; d < R; d += kRsThreads) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRsWarps; ++ww) s += wh[ww * R + d];
+    a.counts[(int64_t)d * a.ntiles + tile] = s;
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(PassArgs a) {
+  constexpr int R = 1 << BITS;
+  extern __shared__ uint32_t smem_u32[];
+  uint32_t *wc = smem_u32;  // [kRsWarps][R] running counts, then bases
+  const int w = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
+  for (int i = threadIdx.x; i < kRsWarps * R; i += kRsThreads) wc[i] = 0;
+  __syncthreads();
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kRsTile + (int64_t)w * 32 * kRsRounds + lane;
+
+  int32_t key[kRsRounds];
+  uint32_t rank[kRsRounds];
+#pragma unroll
+  for (int r = 0; r < kRsRounds; ++r) {
+    int64_t i = base + (int64_t)r * 32;
+    bool valid = i < a.n;
+    key[r] = valid ? clamp_key(load_src_raw(a.key, i), a.key_limit) : 0;
+    unsigned d = valid ? ((unsigned)(key[r] >> a.shift) & (R - 1)) : (unsigned)R;
+    unsigned peers = __match_any_sync(kFull, d);
+    unsigned lt = __popc(peers & lanemask_lt());
+    uint32_t cnt = valid ? wc[w * R + d] : 0u;
+    rank[r] = cnt + lt;
+    __syncwarp();
+    if (valid && lt == 0) wc[w * R + d] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < R; d += kRsThreads) {
+    uint32_t run = a.counts[(int64_t)d * a.ntiles + tile];
+#pragma unroll
+    for (int ww = 0; ww < kRsWarps; ++ww) {
+      uint32_t c = wc[ww * R + d];
+      wc[ww * R + d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  long long vmin = LLONG_MAX, vmax = LLONG_MIN;
+#pragma unroll
+  for (int r = 0; r < kRsRounds; ++r) {
+    int64_t i = base + (int64_t)r * 32;
+    if (i < a.n) {
+      unsigned d = (unsigned)(key[r] >> a.shift) & (R - 1);
+      int64_t pos = (int64_t)wc[w * R + d] + rank[r];
+      a.key_out[pos] = key[r];
+      int64_t v0 = load_src_raw(a.val[0], i);
+      vmin = min(vmin, (long long)v0);
+      vmax = max(vmax, (long long)v0);
+      a.val_out[0][pos] = static_cast<int32_t>(v0);
+      if (a.nvals > 1) a.val_out[1][pos] = static_cast<int32_t>(load_src_raw(a.val[1], i));
+    }
+  }
+  if (a.minmax) block_minmax(vmin, vmax, a.minmax + 2);
+}
+
+template <int BITS>
+int launch_pass(const PassArgs &a, cudaStream_t st, void *scan_ws, size_t scan_ws_bytes) {
+  constexpr int R = 1 << BITS;
+  const size_t smem = sizeof(uint32_t) * kRsWarps * R;
+  static bool attr_set = false;  // idempotent; benign race
+  if (!attr_set) {
+    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_hist_kernel<BITS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<BITS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  rs_hist_kernel<BITS><<<(unsigned)a.ntiles, kRsThreads, smem, st>>>(a);
+  GNN_LAUNCH_CHECK();
+  GNN_TRY(exclusive_scan_u32(a.counts, a.counts, (int64_t)R * a.ntiles, scan_ws, scan_ws_bytes, st));
+  PassArgs b = a;
+  b.minmax = a.minmax ? a.minmax : nullptr;
+  rs_scatter_kernel<BITS><<<(unsigned)a.ntiles, kRsThreads, smem, st>>>(b);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int launch_pass_bits(int bits, const PassArgs &a, cudaStream_t st, void *sws, size_t sws_bytes) {
+  switch (bits) {
+    case 4: return launch_pass<4>(a, st, sws, sws_bytes);
+    case 6: return launch_pass<6>(a, st, sws, sws_bytes);
+    case 8: return launch_pass<8>(a, st, sws, sws_bytes);
+    case 9: return launch_pass<9>(a, st, sws, sws_bytes);
+    case 10: return launch_pass<10>(a, st, sws, sws_bytes);
+    case 11: return launch_pass<11>(a, st, sws, sws_bytes);
+    default: return GNN_ERR_UNSUPPORTED;
+  }
+}
+
+int bit_width_u64(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
+
+struct RadixPlan {
+  int nbits;
+  int passes;
+  int bits;  // per pass (instantiated width >= needed)
+};
+
+RadixPlan plan_radix(int64_t key_limit) {
+  RadixPlan p;
+  p.nbits = key_limit > 1 ? bit_width_u64((uint64_t)(key_limit - 1)) : 1;
+  p.passes = (p.nbits + 10) / 11;
+  int need = (p.nbits + p.passes - 1) / p.passes;
+  static const int widths[] = {4, 6, 8, 9, 10, 11};
+  p.bits = 11;
+  for (int wdt : widths)
+    if (wdt >= need) {
+      p.bits = wdt;
+      break;
+    }
+  return p;
+}
+
+// ------------------------------------------------------ stable sort driver
+struct SortIO {
+  int64_t n;
+  int64_t key_limit;
+  SrcDesc key;
+  int nvals;
+  SrcDesc val[2];
+  int32_t *keys_sorted;  // final sorted keys [n]
+  int32_t *vals_sorted[2];
+};
+
+void sort_ws_count(WsCounter &c, int64_t n, int64_t key_limit, int nvals) {
+  RadixPlan p = plan_radix(key_limit);
+  int64_t ntiles = ceil_div(n > 0 ? n : 1, kRsTile);
+  int64_t cnt = ((int64_t)1 << p.bits) * ntiles;
+  c.take<int32_t>(n);              // key ping
+  c.take<int32_t>(n);              // key pong
+  for (int v = 0; v < nvals; ++v) {
+    c.take<int32_t>(n);
+    c.take<int32_t>(n);
+  }
+  c.take<uint32_t>(cnt);
+  c.take<long long>(4);
+  c.used += scan_u32_workspace(cnt) + 256;
+}
+
+// Runs all passes; final outputs land in io.keys_sorted / io.vals_sorted.
+// minmax (device [4]) receives key/val0 min/max of the pass-0 sources if non-null.
+int stable_sort(const SortIO &io, long long *minmax, WsArena &ar, cudaStream_t st) {
+  RadixPlan p = plan_radix(io.key_limit);
+  const int64_t n = io.n;
+  if (n == 0) return GNN_OK;
+  int64_t ntiles = ceil_div(n, kRsTile);
+  int64_t cnt = ((int64_t)1 << p.bits) * ntiles;
+  int32_t *kb[2] = {ar.take<int32_t>(n), ar.take<int32_t>(n)};
+  int32_t *vb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  for (int v = 0; v < io.nvals; ++v) {
+    vb[v][0] = ar.take<int32_t>(n);
+    vb[v][1] = ar.take<int32_t>(n);
+  }
+  uint32_t *counts = ar.take<uint32_t>(cnt);
+  size_t sws_bytes = scan_u32_workspace(cnt);
+  void *sws = ar.take<char>((int64_t)sws_bytes);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+
+  SrcDesc kin = io.key;
+  SrcDesc vin[2] = {io.val[0], io.val[1]};
+  for (int pass = 0; pass < p.passes; ++pass) {
+    const bool last = pass == p.passes - 1;
+    PassArgs a{};
+    a.n = n;
+    a.ntiles = ntiles;
+    a.shift = pass * p.bits;
+    a.key = kin;
+    a.key_limit = io.key_limit;
+    a.nvals = io.nvals;
+    a.val[0] = vin[0];
+    a.val[1] = vin[1];
+    a.key_out = last ? io.keys_sorted : kb[pass & 1];
+    for (int v = 0; v < io.nvals; ++v) a.val_out[v] = last ? io.vals_sorted[v] : vb[v][pass & 1];
+    a.counts = counts;
+    a.minmax = (pass == 0) ? minmax : nullptr;
+    GNN_TRY(launch_pass_bits(p.bits, a, st, sws, sws_bytes));
+    kin = SrcDesc{SRC_I32, a.key_out};
+    for (int v = 0; v < io.nvals; ++v) vin[v] = SrcDesc{SRC_I32, a.val_out[v]};
+  }
+  return GNN_OK;
+}
+
+// ------------------------------------------------ offsets from sorted keys
+__global__ void run_start_kernel(const int32_t *__restrict__ keys, int64_t n, int64_t *rstart) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) rstart[k] = i;
+  }
+}
+__global__ void run_end_kernel(const int32_t *__restrict__ keys, int64_t n,
+                               const int64_t *rstart, int64_t *deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k = keys[i];
+    if (i == n - 1 || keys[i + 1] != k) deg[k] = i + 1 - rstart[k];
+  }
+}
+
+unsigned grid_for(int64_t n, int threads) {
+  int64_t b = ceil_div(n > 0 ? n : 1, threads);
+  int64_t cap = (int64_t)sm_count() * 16;
+  return (unsigned)(b < cap ? b : cap);
+}
+
+void offsets_ws_count(WsCounter &c, int64_t V) {
+  c.take<int64_t>(V);
+  c.used += scan_i64_workspace(V) + 256;
+}
+
+// offsets[V+1] = [0, cumsum(run lengths of sorted keys per key value)]
+int offsets_from_sorted(const int32_t *keys, int64_t n, int64_t V, int64_t *offsets, WsArena &ar,
+                        cudaStream_t st) {
+  int64_t *rstart = ar.take<int64_t>(V);
+  size_t sws_bytes = scan_i64_workspace(V);
+  void *sws = ar.take<char>((int64_t)sws_bytes);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  if (V > 0) GNN_CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * V, st));
+  if (n > 0) {
+    run_start_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys, n, rstart);
+    GNN_LAUNCH_CHECK();
+    run_end_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys, n, rstart, offsets);
+    GNN_LAUNCH_CHECK();
+  }
+  return exclusive_scan_i64(offsets, offsets, V, true, sws, sws_bytes, st);
+}
+
+__global__ void init_minmax_kernel(long long *mm) {
+  mm[0] = LLONG_MAX;
+  mm[1] = LLONG_MIN;
+  mm[2] = LLONG_MAX;
+  mm[3] = LLONG_MIN;
+}
+
+// Shared by csr_from_edges and build_subgraph_csr.
+size_t edges_ws(int64_t V, int64_t E) {
+  WsCounter c;
+  sort_ws_count(c, E, V > 0 ? V : 1, 1);
+  c.take<int32_t>(E);  // sorted keys
+  offsets_ws_count(c, V);
+  c.take<long long>(4);
+  return c.used + 1024;
+}
+
+// mode 0: csr_from_edges (src range -> SOURCE_RANGE, dst range -> RANGE)
+// mode 1: build_subgraph_csr (src range -> INDEX, dst unchecked)
+int build_from_edges(int mode, int64_t V, int64_t E, const int64_t *src, const int64_t *dst,
+                     int64_t *offsets, int32_t *targets, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  if (V < 0 || E < 0 || (E > 0 && (!src || !dst || !targets)) || !offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (E >= ((int64_t)1 << 32) || V > ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < edges_ws(V, E)) return GNN_ERR_WORKSPACE;
+  if (V == 0) {
+    if (E > 0) return mode == 0 ? GNN_ERR_SOURCE_RANGE : GNN_ERR_INDEX;
+    GNN_CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  long long *mm = ar.take<long long>(4);
+  int32_t *skeys = ar.take<int32_t>(E);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  init_minmax_kernel<<<1, 1, 0, st>>>(mm);
+  GNN_LAUNCH_CHECK();
+  SortIO io{};
+  io.n = E;
+  io.key_limit = V;
+  io.key = SrcDesc{SRC_I64, src};
+  io.nvals = 1;
+  io.val[0] = SrcDesc{SRC_I64, dst};
+  io.keys_sorted = skeys;
+  io.vals_sorted[0] = targets;
+  GNN_TRY(stable_sort(io, mm, ar, st));
+  GNN_TRY(offsets_from_sorted(skeys, E, V, offsets, ar, st));
+  long long h[4];
+  GNN_CUDA_TRY(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  if (E > 0) {
+    if (h[0] < 0 || h[1] >= V) return mode == 0 ? GNN_ERR_SOURCE_RANGE : GNN_ERR_INDEX;
+    if (mode == 0 && (h[2] < 0 || h[3] >= V)) return GNN_ERR_RANGE;
+  }
+  return GNN_OK;
+}
+
+// ---------------------------------------------------------- CSC (transpose)
+// rows_of_edge[e] = r with offsets[r] <= e < offsets[r+1]; one tile of edges
+// per block, offsets of the tile's row span staged in shared memory.
+constexpr int kExpTile = 4096;
+__global__ void __launch_bounds__(256) expand_rows_kernel(const int64_t *__restrict__ offsets,
+                                                          int64_t num_rows, int64_t nnz,
+                                                          int32_t *rows) {
+  __shared__ int64_t soff[kExpTile + 2];
+  __shared__ int64_t span[2];
+  const int64_t e0 = (int64_t)blockIdx.x * kExpTile;
+  const int64_t e1 = min(e0 + kExpTile, nnz);
+  if (threadIdx.x == 0) {
+    span[0] = upper_bound_dev(offsets, 0, num_rows + 1, e0) - 1;
+    span[1] = upper_bound_dev(offsets, 0, num_rows + 1, e1 - 1) - 1;
+  }
+  __syncthreads();
+  const int64_t r0 = span[0], r1 = span[1];
+  const int64_t cnt = r1 - r0 + 2;  // offsets[r0 .. r1+1]
+  const bool staged = cnt <= kExpTile + 2;
+  if (staged)
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) soff[i] = offsets[r0 + i];
+  __syncthreads();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    int64_t r;
+    if (staged)
+      r = r0 + upper_bound_dev(soff, 0, cnt, e) - 1;
+    else
+      r = upper_bound_dev(offsets, r0, r1 + 2, e) - 1;
+    rows[e] = (int32_t)r;
+  }
+}
+
+size_t csc_ws(int64_t R, int64_t C, int64_t nnz) {
+  WsCounter c;
+  c.take<int32_t>(nnz);  // expanded rows
+  c.take<int32_t>(nnz);  // sorted keys
+  c.take<int32_t>(nnz);  // eid scratch when t_eid is null
+  sort_ws_count(c, nnz, C > 0 ? C : 1, 2);
+  offsets_ws_count(c, C);
+  (void)R;
+  return c.used + 1024;
+}
+
+int csc_impl(int64_t R, int64_t C, int64_t nnz, const int64_t *offsets, const int32_t *cols,
+             int64_t *t_offsets, int32_t *t_rows, int32_t *t_eid, void *ws, size_t ws_bytes,
+             cudaStream_t st) {
+  if (R < 0 || C < 0 || nnz < 0 || !offsets || !t_offsets || (nnz > 0 && (!cols || !t_rows)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (nnz >= ((int64_t)1 << 31) || C > ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < csc_ws(R, C, nnz)) return GNN_ERR_WORKSPACE;
+  if (C == 0) {
+    if (nnz > 0) return GNN_ERR_RANGE;
+    GNN_CUDA_TRY(cudaMemsetAsync(t_offsets, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  int32_t *rows = ar.take<int32_t>(nnz);
+  int32_t *skeys = ar.take<int32_t>(nnz);
+  int32_t *eid_scratch = ar.take<int32_t>(nnz);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  if (nnz > 0) {
+    expand_rows_kernel<<<(unsigned)ceil_div(nnz, kExpTile), 256, 0, st>>>(offsets, R, nnz, rows);
+    GNN_LAUNCH_CHECK();
+    SortIO io{};
+    io.n = nnz;
+    io.key_limit = C;
+    io.key = SrcDesc{SRC_I32, cols};
+    io.nvals = 2;
+    io.val[0] = SrcDesc{SRC_I32, rows};
+    io.val[1] = SrcDesc{SRC_IOTA, nullptr};
+    io.keys_sorted = skeys;
+    io.vals_sorted[0] = t_rows;
+    io.vals_sorted[1] = t_eid ? t_eid : eid_scratch;
+    GNN_TRY(stable_sort(io, nullptr, ar, st));
+  }
+  return offsets_from_sorted(skeys, nnz, C, t_offsets, ar, st);
+}
+
+// ------------------------------------------------------------- coalescing
+__global__ void mark_row_starts_kernel(const int64_t *__restrict__ offsets, int64_t R, int64_t nnz,
+                                       int64_t *flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offsets[r];
+    if (o < nnz) flag[o] = 1;
+  }
+}
+__global__ void mark_col_changes_kernel(const int32_t *__restrict__ cols, int64_t nnz,
+                                        int64_t *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0 || cols[i] != cols[i - 1]) flag[i] = 1;
+  }
+}
+// u = exclusive scan of flags, with u[nnz] = total.  Run index of i = u[i+1]-1.
+__global__ void coalesce_scatter_kernel(const int32_t *__restrict__ cols, int64_t nnz,
+                                        const int64_t *__restrict__ u, int32_t *out_cols,
+                                        int64_t *start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = u[i], b = u[i + 1];
+    if (b != a) {
+      out_cols[a] = cols[i];
+      start[a] = i;
+    }
+    if (i == 0) start[u[nnz]] = nnz;
+  }
+}
+__global__ void coalesce_mult_kernel(const int64_t *__restrict__ u, int64_t nnz,
+                                     const int64_t *__restrict__ start, float *mult) {
+  const int64_t total = u[nnz];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+       j += (int64_t)gridDim.x * blockDim.x)
+    mult[j] = (float)(start[j + 1] - start[j]);
+}
+__global__ void coalesce_offsets_kernel(const int64_t *__restrict__ offsets, int64_t R,
+                                        int64_t nnz, const int64_t *__restrict__ u,
+                                        int64_t *out_offsets) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = offsets[r];
+    out_offsets[r] = o < nnz ? u[o] : u[nnz];
+  }
+}
+
+size_t coalesce_ws(int64_t R, int64_t nnz) {
+  WsCounter c;
+  c.take<int64_t>(nnz + 1);
+  c.take<int64_t>(nnz + 1);
+  c.used += scan_i64_workspace(nnz) + 256;
+  (void)R;
+  return c.used + 1024;
+}
+
+// ----------------------------------------------------------- validation
+__global__ void validate_kernel(const int64_t *__restrict__ offsets, int64_t V, int64_t E,
+                                const int32_t *__restrict__ targets, int *flags) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int f = 0;
+  if (tid == 0 && (offsets[0] != 0 || offsets[V] != E)) f |= 1;
+  for (int64_t v = tid; v < V; v += stride)
+    if (offsets[v + 1] < offsets[v]) f |= 1;
+  for (int64_t e = tid; e < E; e += stride) {
+    int32_t t = targets[e];
+    if (t < 0 || (int64_t)t >= V) f |= 2;
+  }
+  f = __reduce_or_sync(kFull, f);
+  if (lane_id() == 0 && f) atomicOr(flags, f);
+}
+
+__global__ void degrees_kernel(const int64_t *__restrict__ offsets, int64_t V, int64_t *deg) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    deg[v] = offsets[v + 1] - offsets[v];
+}
+
+// ------------------------------------------------------- PCG64 generator
+struct U128 {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ U128 u128_mul(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.hi * b.lo + a.lo * b.hi;
+  return r;
+}
+__device__ __forceinline__ U128 u128_add(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+// numpy PCG64 = pcg_setseq_128_xsl_rr_64: state = state*M + inc; out = rotr(hi^lo, state>>122)
+__device__ __constant__ U128 kPcgMult = {0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull};
+
+__device__ __forceinline__ U128 pcg_advance(U128 state, U128 inc, uint64_t delta) {
+  U128 acc_mult = {0, 1}, acc_plus = {0, 0};
+  U128 cur_mult = kPcgMult, cur_plus = inc;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult = u128_mul(acc_mult, cur_mult);
+      acc_plus = u128_add(u128_mul(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = u128_mul(u128_add(cur_mult, U128{0, 1}), cur_plus);
+    cur_mult = u128_mul(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  return u128_add(u128_mul(acc_mult, state), acc_plus);
+}
+__device__ __forceinline__ uint64_t pcg_output(U128 s) {
+  uint64_t v = s.hi ^ s.lo;
+  unsigned rot = (unsigned)(s.hi >> 58);
+  return (v >> rot) | (v << ((64u - rot) & 63u));
+}
+
+constexpr int kGuideBits = 20;
+constexpr int64_t kGuide = (int64_t)1 << kGuideBits;
+
+__global__ void guide_kernel(const double *__restrict__ cdf, int64_t n, int32_t *guide) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= kGuide;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double x = (double)b / (double)kGuide;  // exact: power-of-two denominator
+    guide[b] = (int32_t)upper_bound_dev(cdf, 0, n, x);
+  }
+}
+
+constexpr int kGenChunk = 64;
+__global__ void __launch_bounds__(256) powerlaw_kernel(const double *__restrict__ cdf, int64_t n,
+                                                       int64_t m, const int32_t *__restrict__ guide,
+                                                       U128 state0, U128 inc, int64_t *src,
+                                                       int64_t *dst) {
+  const int64_t total = 2 * m;
+  const int64_t nchunks = ceil_div(total, kGenChunk);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p0 = c * kGenChunk;
+    U128 s = pcg_advance(state0, inc, (uint64_t)p0);
+    int64_t p1 = min(p0 + kGenChunk, total);
+    for (int64_t p = p0; p < p1; ++p) {
+      s = u128_add(u128_mul(s, kPcgMult), inc);
+      double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+      int64_t b = (int64_t)(u * (double)kGuide);  // u in [b/G,(b+1)/G) exactly (power-of-two scale)
+      int64_t idx = upper_bound_dev(cdf, (int64_t)guide[b], (int64_t)guide[b + 1], u);
+      if (p < m)
+        src[p] = idx;
+      else
+        dst[p - m] = idx;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace gnn
+
+using namespace gnn;
+
+extern "C" {
+
+size_t gnn_csr_from_edges_workspace(int64_t V, int64_t E) { return edges_ws(V, E); }
+int gnn_csr_from_edges(int64_t V, int64_t E, const int64_t *src, const int64_t *dst,
+                       int64_t *offsets, int32_t *targets, void *ws, size_t ws_bytes,
+                       gnn_stream_t stream) {
+  return build_from_edges(0, V, E, src, dst, offsets, targets, ws, ws_bytes, as_stream(stream));
+}
+
+size_t gnn_subgraph_csr_workspace(int64_t n, int64_t E) { return edges_ws(n, E); }
+int gnn_subgraph_csr(int64_t n, int64_t E, const int64_t *edge_src, const int64_t *edge_dst,
+                     int64_t *offsets, int32_t *targets, void *ws, size_t ws_bytes,
+                     gnn_stream_t stream) {
+  return build_from_edges(1, n, E, edge_src, edge_dst, offsets, targets, ws, ws_bytes,
+                          as_stream(stream));
+}
+
+size_t gnn_csr_validate_workspace(int64_t V, int64_t E) {
+  (void)V;
+  (void)E;
+  return 256;
+}
+int gnn_csr_validate(int64_t V, int64_t E, const int64_t *offsets, const int32_t *targets,
+                     void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (V < 0 || E < 0 || !offsets || (E > 0 && !targets) || !ws) return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < sizeof(int)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  int *flags = static_cast<int *>(ws);
+  GNN_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), st));
+  int64_t work = V > E ? V : E;
+  validate_kernel<<<grid_for(work, 256), 256, 0, st>>>(offsets, V, E, targets, flags);
+  GNN_LAUNCH_CHECK();
+  int h = 0;
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h & 1) return GNN_ERR_CSR_INVARIANT;
+  if (h & 2) return GNN_ERR_RANGE;
+  return GNN_OK;
+}
+
+int gnn_degrees(int64_t V, const int64_t *offsets, int64_t *deg, gnn_stream_t stream) {
+  if (V < 0 || (V > 0 && (!offsets || !deg))) return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  degrees_kernel<<<grid_for(V, 256), 256, 0, st>>>(offsets, V, deg);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_csc_from_csr_workspace(int64_t R, int64_t C, int64_t nnz) { return csc_ws(R, C, nnz); }
+int gnn_csc_from_csr(int64_t R, int64_t C, int64_t nnz, const int64_t *offsets,
+                     const int32_t *cols, int64_t *t_offsets, int32_t *t_rows, int32_t *t_eid,
+                     void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  return csc_impl(R, C, nnz, offsets, cols, t_offsets, t_rows, t_eid, ws, ws_bytes,
+                  as_stream(stream));
+}
+
+size_t gnn_csr_coalesce_workspace(int64_t R, int64_t nnz) { return coalesce_ws(R, nnz); }
+int gnn_csr_coalesce(int64_t R, int64_t nnz, const int64_t *offsets, const int32_t *cols,
+                     int64_t *out_offsets, int32_t *out_cols, float *out_mult, int64_t *out_nnz,
+                     void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (R < 0 || nnz < 0 || !offsets || !out_offsets || !out_nnz ||
+      (nnz > 0 && (!cols || !out_cols || !out_mult)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < coalesce_ws(R, nnz)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  WsArena ar(ws, ws_bytes);
+  int64_t *u = ar.take<int64_t>(nnz + 1);
+  int64_t *start = ar.take<int64_t>(nnz + 1);
+  size_t sws_bytes = scan_i64_workspace(nnz);
+  void *sws = ar.take<char>((int64_t)sws_bytes);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  if (nnz > 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(int64_t) * nnz, st));
+    mark_row_starts_kernel<<<grid_for(R, 256), 256, 0, st>>>(offsets, R, nnz, u);
+    GNN_LAUNCH_CHECK();
+    mark_col_changes_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, nnz, u);
+    GNN_LAUNCH_CHECK();
+  }
+  GNN_TRY(exclusive_scan_i64(u, u, nnz, true, sws, sws_bytes, st));
+  if (nnz > 0) {
+    coalesce_scatter_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, nnz, u, out_cols, start);
+    GNN_LAUNCH_CHECK();
+    coalesce_mult_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(u, nnz, start, out_mult);
+    GNN_LAUNCH_CHECK();
+  }
+  coalesce_offsets_kernel<<<grid_for(R + 1, 256), 256, 0, st>>>(offsets, R, nnz, u, out_offsets);
+  GNN_LAUNCH_CHECK();
+  GNN_CUDA_TRY(cudaMemcpyAsync(out_nnz, u + nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  return GNN_OK;
+}
+
+size_t gnn_generate_powerlaw_workspace(int64_t n) {
+  (void)n;
+  return sizeof(int32_t) * (size_t)(kGuide + 1) + 256;
+}
+int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t state_hi,
+                          uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src,
+                          int64_t *dst, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (n < 1 || m < 0 || !cdf || (m > 0 && (!src || !dst))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_generate_powerlaw_workspace(n)) return GNN_ERR_WORKSPACE;
+  if (m == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  int32_t *guide = static_cast<int32_t *>(ws);
+  guide_kernel<<<grid_for(kGuide + 1, 256), 256, 0, st>>>(cdf, n, guide);
+  GNN_LAUNCH_CHECK();
+  int64_t nchunks = ceil_div(2 * m, kGenChunk);
+  powerlaw_kernel<<<grid_for(nchunks, 256), 256, 0, st>>>(cdf, n, m, guide, U128{state_hi, state_lo},
+                                                          U128{inc_hi, inc_lo}, src, dst);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,491 @@
+// SpMMv / SpMMve (and their transposes via the CSC view) with a fused row
+// epilogue (degree-norm, GIN self term, bias, ReLU, ReLU-backward mask,
+// post-norm).  GraphPy semantics: PAPER.md:264-278 — no dummy |E| edge tensor
+// for SpMMv, degree-norm fused in the same kernel, edge values of the
+// transpose fetched through the edge-ID array (no eShuffle).
+//
+// Work decomposition (nnz-balanced, skew-proof):
+//   * the nnz range is cut into chunks of P edges, one warp per chunk;
+//   * a warp owns every non-empty row whose first edge lies in its chunk and
+//     sums it over the chunk; rows that continue past the chunk end leave a
+//     partial in slot[w][1]; the chunk's leading piece of a row that started
+//     earlier leaves a partial in slot[w][0];
+//   * within a warp, 32/G lane groups take consecutive edges of the row and
+//     each lane gathers VW-wide vectors (float4 = 128-bit loads) of the
+//     feature row; groups are combined with xor-shuffles;
+//   * split rows (spanning >1 chunk; the power-law "mega rows") are finished
+//     by one CTA per row that sums its partials in a fixed tree order, and
+//     empty rows get epilogue(0) from a list — both lists come from the
+//     per-graph plan, so a call never synchronises with the host.
+// Summation order is fixed, so results are deterministic run to run.
+#include "common.cuh"
+
+namespace gnn {
+namespace {
+
+struct SpmmArgs {
+  int64_t R, nnz;
+  const int64_t *offsets;
+  const int32_t *cols;
+  const float *vals;
+  const int32_t *eid;
+  const int64_t *deg_offsets;
+  int heads;
+  int64_t F;  // features per head
+  const float *X;
+  int64_t ldx;
+  float *Y;
+  int64_t ldy;
+  int64_t K;
+  gnn_epilogue_t epi;
+  int64_t P;
+  int64_t nwarps;
+  float *slots;  // [nwarps][2][K]
+};
+
+template <int VW>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  static __device__ __forceinline__ T ld(const float *p) { return ldg_f4(p); }
+  static __device__ __forceinline__ T ldc(const float *p) {
+    return *reinterpret_cast<const float4 *>(p);
+  }
+  static __device__ __forceinline__ void st(float *p, T v) { *reinterpret_cast<float4 *>(p) = v; }
+  static __device__ __forceinline__ T fma(float s, T b, T a) { return f4_fma(s, b, a); }
+  static __device__ __forceinline__ T add(T a, T b) { return f4_add(a, b); }
+  static __device__ __forceinline__ T shfl_xor(T v, int o) {
+    return make_float4(__shfl_xor_sync(kFull, v.x, o), __shfl_xor_sync(kFull, v.y, o),
+                       __shfl_xor_sync(kFull, v.z, o), __shfl_xor_sync(kFull, v.w, o));
+  }
+};
+template <>
+struct VecT<1> {
+  using T = float;
+  static __device__ __forceinline__ T zero() { return 0.f; }
+  static __device__ __forceinline__ T ld(const float *p) { return __ldg(p); }
+  static __device__ __forceinline__ T ldc(const float *p) { return *p; }
+  static __device__ __forceinline__ void st(float *p, T v) { *p = v; }
+  static __device__ __forceinline__ T fma(float s, T b, T a) { return fmaf(s, b, a); }
+  static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+  static __device__ __forceinline__ T shfl_xor(T v, int o) { return __shfl_xor_sync(kFull, v, o); }
+};
+
+__device__ __forceinline__ float inv_deg(const int64_t *off, int64_t r) {
+  int64_t d = off[r + 1] - off[r];
+  return d > 0 ? 1.0f / (float)d : 0.0f;
+}
+
+// Row epilogue for one scalar column.
+__device__ __forceinline__ float epi_scalar(float y, int64_t r, int64_t c, const SpmmArgs &a,
+                                            float norm_scale, float post_scale) {
+  const gnn_epilogue_t &e = a.epi;
+  if (e.flags & GNN_EPI_NORM) y *= norm_scale;
+  if (e.flags & GNN_EPI_SELF) y = fmaf(e.self_scale, e.self_x[r * e.ld_self + c], y);
+  if (e.flags & GNN_EPI_BIAS) y += e.bias[c];
+  if (e.flags & GNN_EPI_RELU) y = fmaxf(y, 0.f);
+  if (e.flags & GNN_EPI_MASK) y = e.mask[r * e.ld_mask + c] > 0.f ? y : 0.f;
+  if (e.flags & GNN_EPI_POSTNORM) y *= post_scale;
+  return y;
+}
+
+template <int VW>
+__device__ __forceinline__ typename VecT<VW>::T epi_vec(typename VecT<VW>::T y, int64_t r,
+                                                        int64_t c, const SpmmArgs &a, float ns,
+                                                        float ps) {
+  if constexpr (VW == 4) {
+    const gnn_epilogue_t &e = a.epi;
+    if (e.flags & GNN_EPI_NORM) y = make_float4(y.x * ns, y.y * ns, y.z * ns, y.w * ns);
+    if (e.flags & GNN_EPI_SELF) y = f4_fma(e.self_scale, VecT<4>::ldc(e.self_x + r * e.ld_self + c), y);
+    if (e.flags & GNN_EPI_BIAS) y = f4_add(y, VecT<4>::ldc(e.bias + c));
+    if (e.flags & GNN_EPI_RELU)
+      y = make_float4(fmaxf(y.x, 0.f), fmaxf(y.y, 0.f), fmaxf(y.z, 0.f), fmaxf(y.w, 0.f));
+    if (e.flags & GNN_EPI_MASK) {
+      float4 m = VecT<4>::ldc(e.mask + r * e.ld_mask + c);
+      y = make_float4(m.x > 0.f ? y.x : 0.f, m.y > 0.f ? y.y : 0.f, m.z > 0.f ? y.z : 0.f,
+                      m.w > 0.f ? y.w : 0.f);
+    }
+    if (e.flags & GNN_EPI_POSTNORM) y = make_float4(y.x * ps, y.y * ps, y.z * ps, y.w * ps);
+    return y;
+  } else {
+    return epi_scalar(y, r, c, a, ns, ps);
+  }
+}
+
+// G lanes per group, VPL vectors of VW floats per lane, U-way unrolled edge loop.
+template <int G, int VPL, int VW>
+struct Tile {
+  static constexpr int NG = 32 / G;
+  static constexpr int KB = G * VPL * VW;  // columns covered by one block-column
+};
+
+template <int G, int VPL, int VW, bool HAS_VALS>
+__device__ __forceinline__ void seg_sum(const SpmmArgs &a, int64_t es, int64_t ee, int64_t cbase,
+                                        typename VecT<VW>::T (&acc)[VPL]) {
+  using V = VecT<VW>;
+  constexpr int NG = 32 / G;
+  constexpr int U = 4;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
+  int64_t col[VPL];
+  bool act[VPL];
+  int head[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    col[v] = cbase + (int64_t)(v * G + gl) * VW;
+    act[v] = col[v] < a.K;
+    head[v] = HAS_VALS ? (int)(col[v] / a.F) : 0;
+  }
+  for (int64_t e = es + g; e < ee; e += (int64_t)NG * U) {
+    int32_t c[U];
+    float w[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t ei = e + (int64_t)u * NG;
+      c[u] = ei < ee ? __ldg(a.cols + ei) : -1;
+      if constexpr (HAS_VALS) {
+        int64_t vi = ei < ee ? (a.eid ? (int64_t)__ldg(a.eid + ei) : ei) : 0;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          w[u][v] = (ei < ee && act[v]) ? __ldg(a.vals + vi * a.heads + head[v]) : 0.f;
+      }
+    }
+    typename V::T x[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        x[u][v] = (c[u] >= 0 && act[v]) ? V::ld(a.X + (int64_t)c[u] * a.ldx + col[v]) : V::zero();
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        if constexpr (HAS_VALS)
+          acc[v] = V::fma(w[u][v], x[u][v], acc[v]);
+        else
+          acc[v] = V::add(acc[v], x[u][v]);
+      }
+  }
+#pragma unroll
+  for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = V::add(acc[v], V::shfl_xor(acc[v], o));
+}
+
+template <int G, int VPL, int VW>
+__device__ __forceinline__ void store_row(const SpmmArgs &a, float *dst, int64_t cbase,
+                                          const typename VecT<VW>::T (&acc)[VPL], bool final_row,
+                                          int64_t r) {
+  using V = VecT<VW>;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  if (g != 0) return;
+  float ns = 1.f, ps = 1.f;
+  if (final_row) {
+    if (a.epi.flags & GNN_EPI_NORM) ns = inv_deg(a.deg_offsets, r);
+    if (a.epi.flags & GNN_EPI_POSTNORM) ps = inv_deg(a.epi.post_deg_offsets, r);
+  }
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    int64_t col = cbase + (int64_t)(v * G + gl) * VW;
+    if (col < a.K) {
+      typename V::T y = acc[v];
+      if (final_row) y = epi_vec<VW>(y, r, col, a, ns, ps);
+      V::st(dst + col, y);
+    }
+  }
+}
+
+template <int G, int VPL, int VW, bool HAS_VALS>
+__global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
+  using V = VecT<VW>;
+  constexpr int KB = G * VPL * VW;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int64_t cbase = (int64_t)blockIdx.y * KB;
+  const int64_t e0 = w * a.P;
+  const int64_t e1 = min(e0 + a.P, a.nnz);
+  if (e0 >= e1) return;
+  typename V::T acc[VPL];
+  // row containing e0
+  int64_t r = upper_bound_dev(a.offsets, 0, a.R + 1, e0) - 1;
+  int64_t rs = a.offsets[r];
+  int64_t re = a.offsets[r + 1];
+  if (rs < e0) {  // carry-in piece of a row owned by an earlier warp
+    int64_t ee = min(re, e1);
+    seg_sum<G, VPL, VW, HAS_VALS>(a, e0, ee, cbase, acc);
+    store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+    if (re >= e1) return;
+    ++r;
+    rs = re;
+    re = a.offsets[r + 1];
+  }
+  while (rs < e1) {
+    if (re > rs) {
+      int64_t ee = min(re, e1);
+      seg_sum<G, VPL, VW, HAS_VALS>(a, rs, ee, cbase, acc);
+      if (re <= e1)
+        store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
+      else
+        store_row<G, VPL, VW>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
+    }
+    ++r;
+    if (r >= a.R) break;
+    rs = re;
+    re = a.offsets[r + 1];
+  }
+}
+
+// One CTA per split row: sum slot[wa][1], slot[wa+1][0] ... slot[wb][0] in a fixed order.
+__global__ void __launch_bounds__(256) spmm_split_finish_kernel(SpmmArgs a,
+                                                                const int32_t *__restrict__ rows,
+                                                                int64_t nrows) {
+  __shared__ float red[8][33];
+  const int64_t i = blockIdx.x;
+  if (i >= nrows) return;
+  const int64_t r = rows[i];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  const int64_t np = wb - wa + 1;
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
+  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
+  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
+    const int64_t c = c0 + lane;
+    float s = 0.f;
+    if (c < a.K) {
+      for (int64_t j = warp; j < np; j += 8) {
+        const float *p = a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
+        s += p[c];
+      }
+    }
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0) {
+      float t = red[0][lane];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t += red[k][lane];
+      if (c < a.K) a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
+                                       int64_t nrows) {
+  const int64_t total = nrows * a.K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / a.K, c = t % a.K;
+    int64_t r = rows[i];
+    float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
+    a.Y[r * a.ldy + c] = epi_scalar(0.f, r, c, a, 0.f, ps);
+  }
+}
+
+// ------------------------------------------------------------- planning
+__global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
+                                  int64_t *fsplit, int64_t *fempty) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rs = off[r], re = off[r + 1];
+    fempty[r] = re == rs ? 1 : 0;
+    fsplit[r] = (re > rs && rs / P != (re - 1) / P) ? 1 : 0;
+  }
+}
+__global__ void plan_scatter_kernel(int64_t R, const int64_t *__restrict__ us,
+                                    const int64_t *__restrict__ ue, int32_t *split_rows,
+                                    int32_t *empty_rows) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (us[r + 1] != us[r]) split_rows[us[r]] = (int32_t)r;
+    if (ue[r + 1] != ue[r]) empty_rows[ue[r]] = (int32_t)r;
+  }
+}
+
+unsigned grid_1d(int64_t n, int threads) {
+  int64_t b = ceil_div(n > 0 ? n : 1, threads);
+  int64_t cap = (int64_t)sm_count() * 32;
+  return (unsigned)(b < cap ? b : cap);
+}
+
+template <int G, int VPL, int VW>
+int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
+  constexpr int KB = G * VPL * VW;
+  dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
+  if (has_vals)
+    spmm_main_kernel<G, VPL, VW, true><<<grid, 256, 0, st>>>(a);
+  else
+    spmm_main_kernel<G, VPL, VW, false><<<grid, 256, 0, st>>>(a);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+}  // namespace gnn
+
+using namespace gnn;
+
+extern "C" {
+
+size_t gnn_spmm_plan_workspace(int64_t num_rows) {
+  WsCounter c;
+  c.take<int64_t>(num_rows + 1);
+  c.take<int64_t>(num_rows + 1);
+  c.used += 2 * (scan_i64_workspace(num_rows) + 256);
+  return c.used + 512;
+}
+
+int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *split_rows,
+                        int32_t *empty_rows, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
+                        gnn_stream_t stream) {
+  if (!A || !plan || edges_per_warp <= 0 || A->num_rows < 0 || !A->offsets ||
+      (A->num_rows > 0 && (!split_rows || !empty_rows)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->num_rows >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_spmm_plan_workspace(A->num_rows)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int64_t R = A->num_rows;
+  WsArena ar(ws, ws_bytes);
+  int64_t *fs = ar.take<int64_t>(R + 1);
+  int64_t *fe = ar.take<int64_t>(R + 1);
+  size_t sb = scan_i64_workspace(R);
+  void *s1 = ar.take<char>((int64_t)sb);
+  void *s2 = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  if (R > 0) {
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, edges_per_warp, fs, fe);
+    GNN_LAUNCH_CHECK();
+  }
+  GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
+  GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
+  if (R > 0) {
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(R, fs, fe, split_rows, empty_rows);
+    GNN_LAUNCH_CHECK();
+  }
+  int64_t h[2] = {0, 0};
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h[0], fs + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h[1], fe + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  plan->edges_per_warp = edges_per_warp;
+  plan->num_warps = ceil_div(A->nnz, edges_per_warp);
+  plan->num_split = h[0];
+  plan->split_rows = split_rows;
+  plan->num_empty = h[1];
+  plan->empty_rows = empty_rows;
+  return GNN_OK;
+}
+
+size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t K) {
+  if (!A || !plan || K <= 0) return 0;
+  return sizeof(float) * (size_t)(plan->num_warps * 2 * K) + 256;
+}
+
+int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+             const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
+             const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (!A || !plan || !Y || K <= 0 || heads <= 0 || K % heads != 0 || ldy < K ||
+      (A->nnz > 0 && (!X || ldx < K || !A->cols)) || !A->offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->eid && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
+  if (heads > 1 && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  gnn_epilogue_t e{};
+  if (epi) e = *epi;
+  if (((e.flags & GNN_EPI_SELF) && (!e.self_x || e.ld_self < K)) ||
+      ((e.flags & GNN_EPI_BIAS) && !e.bias) || ((e.flags & GNN_EPI_MASK) && (!e.mask || e.ld_mask < K)) ||
+      ((e.flags & GNN_EPI_POSTNORM) && !e.post_deg_offsets))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_spmm_workspace(A, plan, K)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+
+  SpmmArgs a{};
+  a.R = A->num_rows;
+  a.nnz = A->nnz;
+  a.offsets = A->offsets;
+  a.cols = A->cols;
+  a.vals = A->vals;
+  a.eid = A->eid;
+  a.deg_offsets = A->deg_offsets ? A->deg_offsets : A->offsets;
+  a.heads = (int)heads;
+  a.F = K / heads;
+  a.X = X;
+  a.ldx = ldx;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.K = K;
+  a.epi = e;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.slots = static_cast<float *>(ws);
+
+  if (a.nwarps > 0) {
+    const bool hv = A->vals != nullptr;
+    // float4 path needs 16B-aligned rows and heads that do not straddle a vector
+    bool vec4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
+                (a.F % 4 == 0);
+    if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
+    if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
+    if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
+    int s;
+    if (vec4) {
+      if (K <= 16)
+        s = launch_main<4, 1, 4>(a, hv, st);
+      else if (K <= 32)
+        s = launch_main<8, 1, 4>(a, hv, st);
+      else if (K <= 64)
+        s = launch_main<16, 1, 4>(a, hv, st);
+      else if (K <= 128)
+        s = launch_main<32, 1, 4>(a, hv, st);
+      else
+        s = launch_main<32, 2, 4>(a, hv, st);  // 256 columns per block-column
+    } else {
+      if (K <= 32)
+        s = launch_main<32, 1, 1>(a, hv, st);
+      else
+        s = launch_main<32, 4, 1>(a, hv, st);  // 128 columns per block-column
+    }
+    GNN_TRY(s);
+  }
+  if (plan->num_split > 0) {
+    spmm_split_finish_kernel<<<(unsigned)plan->num_split, 256, 0, st>>>(a, plan->split_rows,
+                                                                      plan->num_split);
+    GNN_LAUNCH_CHECK();
+  }
+  if (plan->num_empty > 0) {
+    spmm_empty_rows_kernel<<<grid_1d(plan->num_empty * K, 256), 256, 0, st>>>(a, plan->empty_rows,
+                                                                            plan->num_empty);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+__global__ void degree_norm_kernel(int64_t R, const int64_t *__restrict__ off, float *X,
+                                   int64_t ldx, int64_t K) {
+  const int64_t total = R * K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / K, c = t % K;
+    X[r * ldx + c] *= inv_deg(off, r);
+  }
+}
+
+int gnn_degree_norm_inplace(int64_t R, const int64_t *offsets, float *X, int64_t ldx, int64_t K,
+                            gnn_stream_t stream) {
+  if (R < 0 || K < 0 || ldx < K || (R > 0 && K > 0 && (!offsets || !X)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (R == 0 || K == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  degree_norm_kernel<<<grid_1d(R * K, 256), 256, 0, st>>>(R, offsets, X, ldx, K);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,572 @@
+"""Device-resident CSR graph with the reference's graph API.
+
+Mirrors ``gsbench.graph`` (graph.py:19-262) and ``gsbench.build_subgraph_csr``
+(sampler.py:242-256) name for name, argument for argument, and exception for
+exception, but every array-sized step runs on the GPU through libgnnb200:
+
+* ``csr_from_edges`` / ``build_subgraph_csr`` -> stable device radix sort
+  (bit-exact with numpy's ``argsort(kind="stable")`` build);
+* ``make_csr`` -> device invariant check;
+* ``generate`` power-law -> on-device PCG64 jump-ahead draws, bit-exact with
+  ``numpy.random.default_rng(SeedSequence(seed)).random`` + ``searchsorted``;
+* the transposed CSR (CSC + edge-ID), multigraph coalescing and the SpMM
+  schedules are built lazily, once, on device.
+
+Host views (``offsets``, ``targets``, ``degrees``) are materialised on first
+access, read-only, with the reference's dtypes (int64 / int32 / int64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+from typing import IO, Iterable, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, ExtensionMissing, ParseError, RangeError
+
+OFFSET_DTYPE = np.int64
+TARGET_DTYPE = np.int32
+MAX_VERTEX_ID = int(np.iinfo(TARGET_DTYPE).max)
+_CSR_MAGIC = b"CSR1"
+
+GraphSource = Union[str, Path, IO[str], Iterable[str]]
+
+
+def _device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise ExtensionMissing("no CUDA device: the graph builders run on the GPU only")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"graphs live on a CUDA device, got {d}")
+    if d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
+def _to_device_i64(a, dev) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=torch.int64).contiguous()
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+    return torch.from_numpy(arr).to(dev)
+
+
+def _readonly(a: np.ndarray) -> np.ndarray:
+    a.setflags(write=False)
+    return a
+
+
+def _default_edges_per_warp(nnz: int, sms: int) -> int:
+    """Chunk length of the SpMM schedule: long chunks amortise per-warp setup,
+    but there must be enough warps to fill every SM several times."""
+    p = 1024
+    while p > 32 and nnz // p < sms * 64:
+        p //= 2
+    return p
+
+
+class SparseOperand:
+    """One device sparse matrix in CSR layout (a graph's CSR, or its CSC which
+    is the CSR of the transpose), plus cached SpMM schedules."""
+
+    def __init__(self, num_rows, num_cols, offsets, cols, vals=None, eid=None, deg_offsets=None):
+        self.num_rows = int(num_rows)
+        self.num_cols = int(num_cols)
+        self.nnz = int(cols.numel())
+        self.offsets = offsets
+        self.cols = cols
+        self.vals = vals
+        self.eid = eid
+        self.deg_offsets = deg_offsets
+        self._plans = {}
+
+    @property
+    def device(self):
+        return self.offsets.device
+
+    def view(self, vals=None, eid=None) -> _lib.CsrView:
+        v = _lib.CsrView()
+        v.num_rows = self.num_rows
+        v.num_cols = self.num_cols
+        v.nnz = self.nnz
+        v.offsets = self.offsets.data_ptr()
+        v.cols = self.cols.data_ptr() if self.nnz else None
+        vv = vals if vals is not None else self.vals
+        v.vals = vv.data_ptr() if vv is not None else None
+        ee = eid if eid is not None else self.eid
+        v.eid = ee.data_ptr() if ee is not None else None
+        v.deg_offsets = self.deg_offsets.data_ptr() if self.deg_offsets is not None else None
+        return v
+
+    def plan(self, edges_per_warp: int | None = None) -> _lib.SpmmPlan:
+        lib = _lib.lib()
+        if edges_per_warp is None:
+            with torch.cuda.device(self.device):
+                sms = lib.gnn_device_sm_count()
+            edges_per_warp = _default_edges_per_warp(self.nnz, sms)
+        key = int(edges_per_warp)
+        if key in self._plans:
+            return self._plans[key][0]
+        dev = self.device
+        with torch.cuda.device(dev):
+            split = torch.empty(max(self.num_rows, 1), dtype=torch.int32, device=dev)
+            empty = torch.empty(max(self.num_rows, 1), dtype=torch.int32, device=dev)
+            ws = _lib.workspace(lib.gnn_spmm_plan_workspace(self.num_rows), dev)
+            plan = _lib.SpmmPlan()
+            view = self.view()
+            _lib.check(
+                lib.gnn_spmm_plan_build(C.byref(view), key, split.data_ptr(), empty.data_ptr(),
+                                        C.byref(plan), ws.data_ptr(), ws.numel(),
+                                        _lib.stream_handle(dev)),
+                "spmm plan",
+            )
+        self._plans[key] = (plan, split, empty)
+        return plan
+
+    def nbytes(self) -> int:
+        n = self.offsets.numel() * 8 + self.cols.numel() * 4
+        if self.vals is not None:
+            n += self.vals.numel() * self.vals.element_size()
+        if self.eid is not None:
+            n += self.eid.numel() * 4
+        for _, s, e in self._plans.values():
+            n += (s.numel() + e.numel()) * 4
+        return n
+
+
+class CsrGraph:
+    """Compressed sparse row adjacency, immutable after construction.
+
+    Same public surface as ``gsbench.graph.CsrGraph`` (graph.py:30-47):
+    ``num_vertices``, ``num_edges``, ``offsets`` (int64, V+1), ``targets``
+    (int32, E), ``degrees``, ``degree(v)``, ``neighbors(v)``; the arrays live
+    on a CUDA device (``d_offsets`` / ``d_targets``) and the host views are
+    lazily copied, read-only.
+    """
+
+    __slots__ = ("num_vertices", "num_edges", "d_offsets", "d_targets", "_h_offsets",
+                 "_h_targets", "_csr", "_csc", "_csr_co", "_csc_co", "__weakref__")
+
+    def __init__(self, num_vertices: int, num_edges: int, d_offsets: torch.Tensor,
+                 d_targets: torch.Tensor, h_offsets=None, h_targets=None):
+        object.__setattr__(self, "num_vertices", int(num_vertices))
+        object.__setattr__(self, "num_edges", int(num_edges))
+        object.__setattr__(self, "d_offsets", d_offsets)
+        object.__setattr__(self, "d_targets", d_targets)
+        object.__setattr__(self, "_h_offsets", h_offsets)
+        object.__setattr__(self, "_h_targets", h_targets)
+        object.__setattr__(self, "_csr", None)
+        object.__setattr__(self, "_csc", None)
+        object.__setattr__(self, "_csr_co", None)
+        object.__setattr__(self, "_csc_co", None)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("CsrGraph is immutable")
+
+    # ---- host views (reference surface)
+    @property
+    def offsets(self) -> np.ndarray:
+        if self._h_offsets is None:
+            object.__setattr__(self, "_h_offsets", _readonly(self.d_offsets.cpu().numpy()))
+        return self._h_offsets
+
+    @property
+    def targets(self) -> np.ndarray:
+        if self._h_targets is None:
+            object.__setattr__(self, "_h_targets", _readonly(self.d_targets.cpu().numpy()))
+        return self._h_targets
+
+    @property
+    def degrees(self) -> np.ndarray:
+        return self.device_degrees().cpu().numpy()
+
+    def degree(self, v: int) -> int:
+        return int(self.offsets[v + 1] - self.offsets[v])
+
+    def neighbors(self, v: int) -> np.ndarray:
+        return self.targets[self.offsets[v]: self.offsets[v + 1]]
+
+    # ---- device side
+    @property
+    def device(self) -> torch.device:
+        return self.d_offsets.device
+
+    def device_degrees(self) -> torch.Tensor:
+        """int64 [V] out-degrees computed on device (graph.py:39-41)."""
+        lib = _lib.lib()
+        with torch.cuda.device(self.device):
+            deg = torch.empty(self.num_vertices, dtype=torch.int64, device=self.device)
+            _lib.check(lib.gnn_degrees(self.num_vertices, self.d_offsets.data_ptr(),
+                                       deg.data_ptr() if self.num_vertices else None,
+                                       _lib.stream_handle(self.device)), "degrees")
+        return deg
+
+    def csr(self) -> SparseOperand:
+        if self._csr is None:
+            object.__setattr__(self, "_csr", SparseOperand(self.num_vertices, self.num_vertices,
+                                                           self.d_offsets, self.d_targets))
+        return self._csr
+
+    def csc(self, with_eid: bool = False) -> SparseOperand:
+        """Transposed CSR; with the edge-ID array only when
+        asked — GCN's backward needs the topology alone,
+        so the |E| edge-ID array is not allocated for it."""
+        if self._csc is None or (with_eid and self._csc.eid is None):
+            t_off, t_rows, t_eid = _transpose(self.num_vertices, self.num_vertices,
+                                              self.d_offsets, self.d_targets, with_eid=with_eid)
+            object.__setattr__(self, "_csc", SparseOperand(self.num_vertices, self.num_vertices,
+                                                           t_off, t_rows, eid=t_eid))
+        return self._csc
+
+    def drop_csc(self) -> None:
+        """Release the canonical CSC (e.g. after building the coalesced forms)."""
+        object.__setattr__(self, "_csc", None)
+
+    def csr_coalesced(self) -> SparseOperand:
+        """Unique (row,col) pairs with multiplicities, columns ascending per row.
+        An internal SpMM accelerator for multigraphs; NORM still uses the
+        canonical degree (duplicates counted), so results equal the canonical
+        SpMMv up to fp32 summation order."""
+        if self._csr_co is None:
+            csc = self.csc()
+            s_off, s_cols, _ = _transpose(self.num_vertices, self.num_vertices, csc.offsets,
+                                          csc.cols, with_eid=False)
+            off, cols, mult = _coalesce(self.num_vertices, s_off, s_cols)
+            del s_off, s_cols
+            object.__setattr__(self, "_csr_co", SparseOperand(
+                self.num_vertices, self.num_vertices, off, cols, vals=mult,
+                deg_offsets=self.d_offsets))
+        return self._csr_co
+
+    def csc_coalesced(self) -> SparseOperand:
+        if self._csc_co is None:
+            csc = self.csc()
+            off, cols, mult = _coalesce(self.num_vertices, csc.offsets, csc.cols)
+            object.__setattr__(self, "_csc_co", SparseOperand(
+                self.num_vertices, self.num_vertices, off, cols, vals=mult,
+                deg_offsets=csc.offsets))
+        return self._csc_co
+
+    def operand(self, kind: str) -> SparseOperand:
+        return {"csr": self.csr, "csc": self.csc, "csr_coalesced": self.csr_coalesced,
+                "csc_coalesced": self.csc_coalesced}[kind]()
+
+    def device_nbytes(self) -> int:
+        n = 0
+        for op in (self._csr, self._csc, self._csr_co, self._csc_co):
+            if op is not None:
+                n += op.nbytes()
+        if self._csr is None:
+            n += self.d_offsets.numel() * 8 + self.d_targets.numel() * 4
+        return n
+
+    def __repr__(self):
+        return f"CsrGraph(num_vertices={self.num_vertices}, num_edges={self.num_edges}, device={self.device})"
+
+
+# --------------------------------------------------------------- builders
+def _transpose(R, Ccols, offsets, cols, with_eid):
+    lib = _lib.lib()
+    dev = offsets.device
+    nnz = cols.numel()
+    with torch.cuda.device(dev):
+        t_off = torch.empty(Ccols + 1, dtype=torch.int64, device=dev)
+        t_rows = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
+        t_eid = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz] if with_eid else None
+        ws = _lib.workspace(lib.gnn_csc_from_csr_workspace(R, Ccols, nnz), dev)
+        _lib.check(lib.gnn_csc_from_csr(R, Ccols, nnz, offsets.data_ptr(),
+                                        cols.data_ptr() if nnz else None, t_off.data_ptr(),
+                                        t_rows.data_ptr() if nnz else None,
+                                        t_eid.data_ptr() if (with_eid and nnz) else None,
+                                        ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
+                   "csc_from_csr")
+    return t_off, t_rows, t_eid
+
+
+def _coalesce(R, offsets, cols):
+    lib = _lib.lib()
+    dev = offsets.device
+    nnz = cols.numel()
+    with torch.cuda.device(dev):
+        out_off = torch.empty(R + 1, dtype=torch.int64, device=dev)
+        out_cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        out_mult = torch.empty(max(nnz, 1), dtype=torch.float32, device=dev)
+        n_out = C.c_int64(0)
+        ws = _lib.workspace(lib.gnn_csr_coalesce_workspace(R, nnz), dev)
+        _lib.check(lib.gnn_csr_coalesce(R, nnz, offsets.data_ptr(), cols.data_ptr() if nnz else None,
+                                        out_off.data_ptr(), out_cols.data_ptr(),
+                                        out_mult.data_ptr(), C.byref(n_out), ws.data_ptr(),
+                                        ws.numel(), _lib.stream_handle(dev)), "coalesce")
+        u = int(n_out.value)
+        out_cols = out_cols[:u].clone()
+        out_mult = out_mult[:u].clone()
+    return out_off, out_cols, out_mult
+
+
+def _build_from_edges(fn_ws, fn, n, src, dst, device, what):
+    lib = _lib.lib()
+    dev = _device(device)
+    s = _to_device_i64(src, dev)
+    d = _to_device_i64(dst, dev)
+    if s.numel() != d.numel():
+        raise ValueError("src and dst must have the same length")
+    E = int(s.numel())
+    with torch.cuda.device(dev):
+        offsets = torch.empty(max(n, 0) + 1, dtype=torch.int64, device=dev)
+        targets = torch.empty(max(E, 1), dtype=torch.int32, device=dev)[:E]
+        ws = _lib.workspace(getattr(lib, fn_ws)(n, E), dev)
+        _lib.check(getattr(lib, fn)(n, E, s.data_ptr() if E else None, d.data_ptr() if E else None,
+                                    offsets.data_ptr(), targets.data_ptr() if E else None,
+                                    ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)), what)
+    return offsets, targets
+
+
+def make_csr(num_vertices: int, offsets, targets, device=None) -> CsrGraph:
+    """Validate the CSR invariants and build an immutable graph (graph.py:91-103).
+
+    Same checks and exception types: ValueError for a bad offsets shape, a
+    wrong first/last offset, or decreasing offsets; RangeError for a target
+    outside [0, num_vertices)."""
+    dev = _device(device)
+    if isinstance(offsets, torch.Tensor):
+        d_off = offsets.to(device=dev, dtype=torch.int64).contiguous()
+    else:
+        d_off = torch.from_numpy(np.ascontiguousarray(offsets, dtype=OFFSET_DTYPE)).to(dev)
+    if isinstance(targets, torch.Tensor):
+        d_tgt = targets.to(device=dev, dtype=torch.int32).contiguous()
+    else:
+        d_tgt = torch.from_numpy(np.ascontiguousarray(targets, dtype=TARGET_DTYPE)).to(dev)
+    if tuple(d_off.shape) != (num_vertices + 1,):
+        raise ValueError("offsets must have length num_vertices + 1")
+    lib = _lib.lib()
+    E = int(d_tgt.numel())
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(lib.gnn_csr_validate_workspace(num_vertices, E), dev)
+        _lib.check(lib.gnn_csr_validate(num_vertices, E, d_off.data_ptr(),
+                                        d_tgt.data_ptr() if E else None, ws.data_ptr(),
+                                        ws.numel(), _lib.stream_handle(dev)), "make_csr")
+    return CsrGraph(num_vertices, E, d_off, d_tgt)
+
+
+def csr_from_edges(num_vertices: int, src, dst, device=None) -> CsrGraph:
+    """Counting-sort edge pairs into CSR; stable within each source segment
+    (graph.py:106-114), on device."""
+    off, tgt = _build_from_edges("gnn_csr_from_edges_workspace", "gnn_csr_from_edges",
+                                 int(num_vertices), src, dst, device, "csr_from_edges")
+    return CsrGraph(num_vertices, int(tgt.numel()), off, tgt)
+
+
+def build_subgraph_csr(edge_src, edge_dst, num_local_src: int, device=None):
+    """Exclusive prefix sum of per-source degrees plus stable grouping
+    (sampler.py:242-256).  Returns host ``(offsets int64, targets int32)`` like
+    the reference when given host arrays, device tensors when given CUDA
+    tensors.  IndexError if a source id is outside [0, num_local_src)."""
+    on_device = isinstance(edge_src, torch.Tensor) and edge_src.is_cuda
+    off, tgt = _build_from_edges("gnn_subgraph_csr_workspace", "gnn_subgraph_csr",
+                                 int(num_local_src), edge_src, edge_dst,
+                                 edge_src.device if on_device else device, "build_subgraph_csr")
+    if on_device:
+        return off, tgt
+    return off.cpu().numpy(), tgt.cpu().numpy()
+
+
+def total_degree(graph: CsrGraph) -> int:
+    """Sum of out-degrees; equals num_edges by the CSR invariant (graph.py:117-119)."""
+    return int(graph.d_offsets[-1].item())
+
+
+# ------------------------------------------------------------ edge-list IO
+def _lines(source: GraphSource):
+    if isinstance(source, (str, Path)):
+        with open(source, "r", encoding="utf-8") as fh:
+            yield from fh
+    else:
+        yield from source
+
+
+def load_edge_list(source: GraphSource, *, symmetrize: bool = False, compact_ids: bool = False,
+                   device=None) -> CsrGraph:
+    """Parse "src dst" lines into a CsrGraph (graph.py:134-196 semantics):
+    '#' comments, optional "n=<count>" header, ParseError with the 1-based
+    line number, RangeError for ids beyond 32 bits or the declared count,
+    optional symmetrize / compact_ids.  Parsing is host text IO; the CSR build
+    runs on device."""
+    pairs_s: list[int] = []
+    pairs_d: list[int] = []
+    declared = None
+    for lineno, raw in enumerate(_lines(source), start=1):
+        text = raw.strip()
+        if not text or text[0] == "#":
+            continue
+        if text.startswith("n="):
+            try:
+                declared = int(text[2:])
+            except ValueError:
+                raise ParseError(lineno, f"bad vertex-count header {text!r}") from None
+            if declared < 0:
+                raise ParseError(lineno, "declared vertex count must be nonnegative")
+            continue
+        fields = text.split()
+        if len(fields) != 2:
+            raise ParseError(lineno, f"expected 'src dst', got {text!r}")
+        try:
+            a, b = int(fields[0]), int(fields[1])
+        except ValueError:
+            raise ParseError(lineno, f"expected 'src dst', got {text!r}") from None
+        if a < 0 or b < 0:
+            raise ParseError(lineno, "vertex ids must be nonnegative")
+        if a > MAX_VERTEX_ID or b > MAX_VERTEX_ID:
+            raise RangeError(f"line {lineno}: vertex id exceeds 32-bit id space")
+        pairs_s.append(a)
+        pairs_d.append(b)
+    src = np.asarray(pairs_s, dtype=np.int64)
+    dst = np.asarray(pairs_d, dtype=np.int64)
+    if symmetrize and src.size:
+        src, dst = np.concatenate([src, dst]), np.concatenate([dst, src])
+    if compact_ids:
+        ids = np.unique(np.concatenate([src, dst]))
+        src = np.searchsorted(ids, src)
+        dst = np.searchsorted(ids, dst)
+        n = int(ids.size)
+    else:
+        top = max(int(src.max()) if src.size else -1, int(dst.max()) if dst.size else -1)
+        n = top + 1
+        if declared is not None:
+            if declared < n:
+                raise RangeError(f"vertex id {top} outside declared range n={declared}")
+            n = declared
+    return csr_from_edges(n, src, dst, device=device)
+
+
+# ------------------------------------------------------------- binary IO
+def save_csr(graph: CsrGraph, path) -> None:
+    """Binary "CSR1" file: magic, <QQ (V, E), <i8 offsets, <i4 targets (graph.py:199-209)."""
+    with open(path, "wb") as fh:
+        fh.write(_CSR_MAGIC)
+        fh.write(struct.pack("<QQ", graph.num_vertices, graph.num_edges))
+        fh.write(np.asarray(graph.offsets, dtype="<i8").tobytes())
+        fh.write(np.asarray(graph.targets, dtype="<i4").tobytes())
+
+
+def load_csr(path, device=None) -> CsrGraph:
+    """Read a "CSR1" file straight into device memory and validate it on
+    device (graph.py:212-220); ParseError on a bad magic."""
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != _CSR_MAGIC:
+            raise ParseError(1, f"bad magic {magic!r}, expected {_CSR_MAGIC!r}")
+        n, m = struct.unpack("<QQ", fh.read(16))
+        off = np.frombuffer(fh.read(8 * (n + 1)), dtype="<i8")
+        tgt = np.frombuffer(fh.read(4 * m), dtype="<i4")
+    return make_csr(int(n), off.astype(OFFSET_DTYPE), tgt.astype(TARGET_DTYPE), device=device)
+
+
+# -------------------------------------------------------------- generators
+@dataclass(frozen=True)
+class GraphGenSpec:
+    """Parameters for one synthetic graph family (graph.py:50-83)."""
+
+    kind: str  # uniform-random | power-law | star | ring | complete
+    num_vertices: int
+    target_edges: int | float | None = None
+    exponent: float | None = None
+
+    _KINDS = ("uniform-random", "power-law", "star", "ring", "complete")
+
+    def __post_init__(self):
+        if self.kind not in self._KINDS:
+            raise ConfigError(f"unknown graph kind {self.kind!r}")
+        if self.num_vertices < 1:
+            raise ConfigError("num_vertices must be positive")
+        if self.kind in ("uniform-random", "power-law"):
+            if self.target_edges is None:
+                raise ConfigError(f"{self.kind} requires target_edges")
+            if isinstance(self.target_edges, float) and not 0 < self.target_edges < 1:
+                raise ConfigError("edge probability must lie in (0, 1)")
+        if self.kind == "power-law" and (self.exponent is None or self.exponent <= 1):
+            raise ConfigError("power-law requires exponent > 1")
+
+    def edge_count(self) -> int:
+        n = self.num_vertices
+        if isinstance(self.target_edges, float):
+            return int(round(self.target_edges * n * n))
+        return int(self.target_edges or 0)
+
+
+def powerlaw_cdf(n: int, exponent: float) -> np.ndarray:
+    """The float64 CDF of graph.py:256-259 (host, numpy pairwise sum — the
+    device draws must search exactly this array to stay bit-exact)."""
+    w = (np.arange(n, dtype=np.float64) + 1.0) ** (-1.0 / (exponent - 1.0))
+    cdf = np.cumsum(w / w.sum())
+    cdf[-1] = 1.0
+    return cdf
+
+
+def pcg64_seed_state(seed: int) -> tuple[int, int]:
+    """(state, inc) of numpy's PCG64 seeded by SeedSequence(seed) — the
+    generator graph.py:230 builds."""
+    st = np.random.PCG64(np.random.SeedSequence(seed)).state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+def powerlaw_edges_device(n: int, m: int, exponent: float, seed: int, device=None):
+    """Device (src, dst) int64 draws of graph.py:260-261, bit-exact."""
+    lib = _lib.lib()
+    dev = _device(device)
+    cdf = torch.from_numpy(powerlaw_cdf(n, exponent)).to(dev)
+    state, inc = pcg64_seed_state(seed)
+    mask = (1 << 64) - 1
+    with torch.cuda.device(dev):
+        src = torch.empty(max(m, 1), dtype=torch.int64, device=dev)[:m]
+        dst = torch.empty(max(m, 1), dtype=torch.int64, device=dev)[:m]
+        ws = _lib.workspace(lib.gnn_generate_powerlaw_workspace(n), dev)
+        _lib.check(lib.gnn_generate_powerlaw(n, m, cdf.data_ptr(), state >> 64, state & mask,
+                                             inc >> 64, inc & mask,
+                                             src.data_ptr() if m else None,
+                                             dst.data_ptr() if m else None, ws.data_ptr(),
+                                             ws.numel(), _lib.stream_handle(dev)),
+                   "generate_powerlaw")
+    return src, dst
+
+
+def generate(spec: GraphGenSpec, seed: int, device=None) -> CsrGraph:
+    """Deterministically generate a graph from (spec, seed) (graph.py:227-262).
+
+    power-law: draws and CSR build on device, bit-exact with the reference.
+    uniform-random: numpy's bounded-integer stream is not position-addressable,
+    so the draws stay on the host (same calls as the reference) and only the
+    CSR build runs on device.  star / ring / complete: closed-form CSR."""
+    n = spec.num_vertices
+    dev = _device(device)
+    if spec.kind == "star":
+        off = np.full(n + 1, n - 1, dtype=OFFSET_DTYPE)
+        off[0] = 0
+        return make_csr(n, off, np.arange(1, n, dtype=TARGET_DTYPE), device=dev)
+    if spec.kind == "ring":
+        off = np.arange(n + 1, dtype=OFFSET_DTYPE)
+        tgt = ((np.arange(n, dtype=np.int64) + 1) % n).astype(TARGET_DTYPE)
+        return make_csr(n, off, tgt, device=dev)
+    if spec.kind == "complete":
+        off = np.arange(n + 1, dtype=OFFSET_DTYPE) * (n - 1)
+        ids = np.arange(n, dtype=np.int64)
+        tgt = np.broadcast_to(ids, (n, n))[~np.eye(n, dtype=bool)].astype(TARGET_DTYPE)
+        return make_csr(n, off, tgt, device=dev)
+    m = spec.edge_count()
+    if m > n * n:
+        raise ConfigError(f"target_edges {m} exceeds n^2 = {n * n}")
+    if spec.kind == "uniform-random":
+        rng = np.random.default_rng(np.random.SeedSequence(seed))
+        src = rng.integers(0, n, size=m, dtype=np.int64)
+        dst = rng.integers(0, n, size=m, dtype=np.int64)
+        return csr_from_edges(n, src, dst, device=dev)
+    src, dst = powerlaw_edges_device(n, m, spec.exponent, seed, device=dev)
+    g = csr_from_edges(n, src, dst, device=dev)
+    del src, dst
+    return g

@@ -1,0 +1,133 @@
+"""Pre-bound kernel launches for the fused training engines.
+
+Each ``*Call`` object resolves its C-ABI arguments (views, plans, epilogue,
+workspace) once; ``__call__`` only reads the current CUDA stream and launches,
+so a step built from these objects is cheap on the host and capturable in a
+CUDA graph (no allocation, no host sync inside).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .graph import SparseOperand
+
+
+class SpmmCall:
+    def __init__(self, op: SparseOperand, X: torch.Tensor, Y: torch.Tensor, *, flags=0, heads=1,
+                 vals=None, eid=None, bias=None, self_x=None, self_scale=1.0, mask=None,
+                 post_deg_offsets=None, edges_per_warp=None):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.K = int(X.shape[1])
+        assert Y.shape[1] == self.K and X.stride(1) == 1 and Y.stride(1) == 1
+        self.view = op.view(vals=vals, eid=eid)
+        self.plan = op.plan(edges_per_warp)
+        self.epi = _lib.Epilogue()
+        self.epi.flags = flags
+        self.epi.self_scale = float(self_scale)
+        if self_x is not None:
+            self.epi.self_x, self.epi.ld_self = self_x.data_ptr(), self_x.stride(0)
+        if bias is not None:
+            self.epi.bias = bias.data_ptr()
+        if mask is not None:
+            self.epi.mask, self.epi.ld_mask = mask.data_ptr(), mask.stride(0)
+        if post_deg_offsets is not None:
+            self.epi.post_deg_offsets = post_deg_offsets.data_ptr()
+        self.heads = heads
+        self.X, self.Y = X, Y
+        self._keep = (op, vals, eid, bias, self_x, mask, post_deg_offsets)
+        nbytes = self.lib.gnn_spmm_workspace(C.byref(self.view), C.byref(self.plan), self.K)
+        self.ws = _lib.workspace(nbytes, self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_spmm(C.byref(self.view), C.byref(self.plan), self.heads,
+                                     self.X.data_ptr(), self.X.stride(0), self.Y.data_ptr(),
+                                     self.Y.stride(0), self.K, C.byref(self.epi),
+                                     self.ws.data_ptr(), self.ws.numel(),
+                                     _lib.stream_handle(self.dev)), "spmm")
+
+
+class GemmCall:
+    """C = op(A) op(B) (+bias)(relu)."""
+
+    def __init__(self, A, B, Cout, *, trans_a=False, trans_b=False, bias=None, relu=False):
+        self.lib = _lib.lib()
+        self.dev = A.device
+        self.M = A.shape[1] if trans_a else A.shape[0]
+        self.Kd = A.shape[0] if trans_a else A.shape[1]
+        self.N = B.shape[0] if trans_b else B.shape[1]
+        assert tuple(Cout.shape) == (self.M, self.N)
+        self.A, self.B, self.C, self.bias = A, B, Cout, bias
+        self.ta, self.tb, self.relu = int(trans_a), int(trans_b), int(relu)
+        self.ws = _lib.workspace(self.lib.gnn_gemm_workspace(self.M, self.N, self.Kd, self.ta),
+                                 self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_gemm(self.M, self.N, self.Kd, self.A.data_ptr(),
+                                     self.A.stride(0), self.ta, self.B.data_ptr(),
+                                     self.B.stride(0), self.tb, self.C.data_ptr(),
+                                     self.C.stride(0),
+                                     self.bias.data_ptr() if self.bias is not None else None,
+                                     self.relu, self.ws.data_ptr(), self.ws.numel(),
+                                     _lib.stream_handle(self.dev)), "gemm")
+
+
+class MaskNormColsumCall:
+    def __init__(self, X, out, *, mask=None, deg_offsets=None, colsum=None):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.M, self.N = X.shape
+        self.X, self.out, self.mask, self.deg, self.colsum = X, out, mask, deg_offsets, colsum
+        self.ws = _lib.workspace(self.lib.gnn_mask_norm_colsum_workspace(self.M, self.N), self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_mask_norm_colsum(
+            self.M, self.N, self.X.data_ptr(), self.X.stride(0),
+            self.mask.data_ptr() if self.mask is not None else None,
+            self.mask.stride(0) if self.mask is not None else 0,
+            self.deg.data_ptr() if self.deg is not None else None,
+            self.out.data_ptr() if self.out is not None else None,
+            self.out.stride(0) if self.out is not None else 0,
+            self.colsum.data_ptr() if self.colsum is not None else None,
+            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "mask_norm_colsum")
+
+
+class XentCall:
+    def __init__(self, Z, labels, loss, dZ=None, grad_scale=None):
+        self.lib = _lib.lib()
+        self.dev = Z.device
+        self.M, self.Cn = Z.shape
+        self.Z, self.labels, self.loss, self.dZ = Z, labels, loss, dZ
+        self.scale = float(1.0 / self.M if grad_scale is None else grad_scale)
+        self.ws = _lib.workspace(self.lib.gnn_softmax_xent_workspace(self.M), self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_softmax_xent(
+            self.M, self.Cn, self.Z.data_ptr(), self.Z.stride(0), self.labels.data_ptr(),
+            self.scale, self.dZ.data_ptr() if self.dZ is not None else None,
+            self.dZ.stride(0) if self.dZ is not None else 0, self.loss.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "softmax_xent")
+
+
+class AdamCall:
+    def __init__(self, params, grads, lr=0.01, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0):
+        self.lib = _lib.lib()
+        self.dev = params[0].device
+        self.params, self.grads = list(params), list(grads)
+        self.m = [torch.zeros_like(p) for p in self.params]
+        self.v = [torch.zeros_like(p) for p in self.params]
+        rows = [[p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel()]
+                for p, g, m, v in zip(self.params, self.grads, self.m, self.v)]
+        self.table = torch.tensor(rows, dtype=torch.int64, device=self.dev)
+        self.step = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.lr, self.b1, self.b2, self.eps, self.wd = lr, betas[0], betas[1], eps, weight_decay
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_adam_step(len(self.params), self.table.data_ptr(), self.lr,
+                                          self.b1, self.b2, self.eps, self.wd,
+                                          self.step.data_ptr(), _lib.stream_handle(self.dev)),
+                   "adam")

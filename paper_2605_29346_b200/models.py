@@ -1,0 +1,232 @@
+"""GNN layers (autograd) and the fused full-graph GCN trainer.
+
+Layer math follows SURVEY.md Appendix A (GCN A.4, GIN A.5) and the GraphPy
+prose: bias is part of the layer, degree-norm fused in the
+forward SpMM and applied to the INPUT of the backward SpMM,
+state tensors are materialised for backward.
+
+``GCNTrainer`` is the benchmarked hot path: one epoch = forward, loss,
+backward and Adam, built only from libgnnb200 kernels with every buffer
+preallocated, so the whole epoch is captured in a CUDA graph and replayed.
+Layer 2 aggregates before it transforms (A (Y W) = (A Y) W, width 16 < 41)
+so every SpMM of the epoch runs at the hidden width.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import CsrGraph
+from .kernels import AdamCall, GemmCall, MaskNormColsumCall, SpmmCall, XentCall
+from .ops import colsum, gemm, linear, spmm_raw
+
+
+def glorot(fan_in: int, fan_out: int, seed: int, index: int = 0) -> np.ndarray:
+    """Glorot-uniform weights from SeedSequence(seed, spawn_key=(12, index))
+    (SURVEY.md §8d seeding idiom)."""
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(12, index)))
+    a = math.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-a, a, (fan_in, fan_out)).astype(np.float32)
+
+
+# ------------------------------------------------------------ autograd layer
+class _GCNAggregate(torch.autograd.Function):
+    """Y = act(D^-1 A H + b) with NORM|BIAS(|RELU) fused in the SpMM epilogue."""
+
+    @staticmethod
+    def forward(ctx, H, b, g, relu, coalesced):
+        op = g.csr_coalesced() if coalesced else g.csr()
+        flags = _lib.EPI_NORM | _lib.EPI_BIAS | (_lib.EPI_RELU if relu else 0)
+        Y = spmm_raw(op, H.contiguous(), flags=flags, bias=b.contiguous())
+        ctx.save_for_backward(Y if relu else None)
+        ctx.g, ctx.relu, ctx.coalesced = g, relu, coalesced
+        return Y
+
+    @staticmethod
+    def backward(ctx, dY):
+        (Y,) = ctx.saved_tensors
+        g = ctx.g
+        dY = dY.contiguous()
+        lib = _lib.lib()
+        dev = dY.device
+        M, N = dY.shape
+        dZn = torch.empty_like(dY)
+        db = torch.empty(N, dtype=torch.float32, device=dev)
+        ws = _lib.workspace(lib.gnn_mask_norm_colsum_workspace(M, N), dev)
+        _lib.check(lib.gnn_mask_norm_colsum(
+            M, N, dY.data_ptr(), dY.stride(0), Y.data_ptr() if Y is not None else None,
+            Y.stride(0) if Y is not None else 0, g.d_offsets.data_ptr(), dZn.data_ptr(),
+            dZn.stride(0), db.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
+            "gcn backward")
+        op = g.csc_coalesced() if ctx.coalesced else g.csc()
+        dH = spmm_raw(op, dZn)
+        return dH, db, None, None, None
+
+
+class GCNConv(torch.nn.Module):
+    """GCN layer Z = D^-1 A (X W) + b (Appendix A.4), optional fused ReLU.
+    When in_feats < out_feats the aggregation runs first on the narrower side
+    (same function)."""
+
+    def __init__(self, in_feats: int, out_feats: int, seed: int = 0, index: int = 0,
+                 device=None):
+        super().__init__()
+        self.in_feats, self.out_feats = in_feats, out_feats
+        self.weight = torch.nn.Parameter(torch.from_numpy(glorot(in_feats, out_feats, seed, index)).to(device))
+        self.bias = torch.nn.Parameter(torch.zeros(out_feats, device=device))
+
+    def forward(self, g: CsrGraph, X: torch.Tensor, relu: bool = False, coalesced: bool = False):
+        if self.in_feats > self.out_feats:
+            H = linear(X, self.weight)
+            return _GCNAggregate.apply(H, self.bias, g, relu, coalesced)
+        from .ops import spmmv
+
+        P = spmmv(g, X, norm=True, coalesced=coalesced)
+        Z = linear(P, self.weight, self.bias)
+        return torch.relu(Z) if relu else Z
+
+
+class GCN(torch.nn.Module):
+    """Stack of GCNConv layers with ReLU between them."""
+
+    def __init__(self, in_feats: int, hidden: int, classes: int, num_layers: int = 2,
+                 seed: int = 0, device=None):
+        super().__init__()
+        dims = [in_feats] + [hidden] * (num_layers - 1) + [classes]
+        self.layers = torch.nn.ModuleList(
+            GCNConv(dims[i], dims[i + 1], seed=seed, index=2 * i, device=device)
+            for i in range(num_layers))
+
+    def forward(self, g, X, coalesced: bool = False):
+        h = X
+        for i, layer in enumerate(self.layers):
+            h = layer(g, h, relu=i < len(self.layers) - 1, coalesced=coalesced)
+        return h
+
+
+# ----------------------------------------------------------- fused trainer
+class GCNTrainer:
+    """Full-graph 2-layer GCN training step on libgnnb200 kernels only.
+
+    Schedule of one epoch (all buffers preallocated; ``capture()`` records it
+    as one CUDA graph):
+
+      H1  = X W1                               gemm
+      Y1  = relu(D^-1 A H1 + b1)               spmm  (NORM|BIAS|RELU epilogue)
+      P2  = D^-1 A Y1                          spmm  (NORM)
+      Z2  = P2 W2 + b2                         gemm
+      loss, dZ2 = xent(Z2, labels)             softmax-xent (mean)
+      db2 = colsum(dZ2);  dW2 = P2^T dZ2       colsum, split-K gemm
+      dP2 = dZ2 W2^T                           gemm
+      dP2 <- D^-1 dP2 (in place)               degree-norm (input of backward SpMM)
+      dZ1 = (A^T dP2) * [Y1 > 0]               spmm over CSC (MASK epilogue)
+      db1 = colsum(dZ1); dZ1 <- D^-1 dZ1       mask_norm_colsum (in place)
+      dH1 = A^T dZ1                            spmm over CSC
+      dW1 = X^T dH1                            split-K gemm
+      Adam(W1,b1,W2,b2)                        adam
+    """
+
+    def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, *, lr=0.01,
+                 seed: int = 0, coalesced: bool = False, drop_canonical_csc: bool = False):
+        self.g = g
+        dev = g.device
+        self.dev = dev
+        V = g.num_vertices
+        self.V, self.F, self.Hd, self.C = V, in_feats, hidden, classes
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.W1 = torch.from_numpy(glorot(in_feats, hidden, seed, 0)).to(dev)
+        self.b1 = torch.zeros(hidden, **f32)
+        self.W2 = torch.from_numpy(glorot(hidden, classes, seed, 2)).to(dev)
+        self.b2 = torch.zeros(classes, **f32)
+        self.dW1, self.db1 = torch.empty_like(self.W1), torch.empty_like(self.b1)
+        self.dW2, self.db2 = torch.empty_like(self.W2), torch.empty_like(self.b2)
+        self.X = torch.empty(V, in_feats, **f32)
+        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
+        self.H1, self.Y1, self.P2 = e(hidden), e(hidden), e(hidden)
+        self.Z2, self.dZ2 = e(classes), e(classes)
+        self.dP2, self.dZ1, self.dH1 = e(hidden), e(hidden), e(hidden)
+        self.loss = torch.zeros(1, **f32)
+
+        if coalesced:
+            A, AT = g.csr_coalesced(), g.csc_coalesced()
+            if drop_canonical_csc:
+                g.drop_csc()
+        else:
+            A, AT = g.csr(), g.csc()
+        self.A, self.AT = A, AT
+        deg_off = g.d_offsets  # out-degree source for every norm
+        N, B, R, M = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        self.k_gemm1 = GemmCall(self.X, self.W1, self.H1)
+        self.k_agg1 = SpmmCall(A, self.H1, self.Y1, flags=N | B | R, bias=self.b1)
+        self.k_agg2 = SpmmCall(A, self.Y1, self.P2, flags=N)
+        self.k_gemm2 = GemmCall(self.P2, self.W2, self.Z2, bias=self.b2)
+        self.k_xent = XentCall(self.Z2, self.labels, self.loss, dZ=self.dZ2)
+        self.k_db2 = MaskNormColsumCall(self.dZ2, None, colsum=self.db2)
+        self.k_dW2 = GemmCall(self.P2, self.dZ2, self.dW2, trans_a=True)
+        self.k_dP2 = GemmCall(self.dZ2, self.W2, self.dP2, trans_b=True)
+        self.k_norm2 = MaskNormColsumCall(self.dP2, self.dP2, deg_offsets=deg_off)
+        self.k_bagg2 = SpmmCall(AT, self.dP2, self.dZ1, flags=M, mask=self.Y1)
+        self.k_norm1 = MaskNormColsumCall(self.dZ1, self.dZ1, deg_offsets=deg_off, colsum=self.db1)
+        self.k_bagg1 = SpmmCall(AT, self.dZ1, self.dH1)
+        self.k_dW1 = GemmCall(self.X, self.dH1, self.dW1, trans_a=True)
+        self.k_adam = AdamCall([self.W1, self.b1, self.W2, self.b2],
+                               [self.dW1, self.db1, self.dW2, self.db2], lr=lr)
+        self.graph = None
+
+    # kernels launched per epoch (our .so only)
+    LAUNCHES_PER_STEP = None
+
+    def set_inputs(self, X: torch.Tensor, labels: torch.Tensor, non_blocking: bool = False):
+        self.X.copy_(X, non_blocking=non_blocking)
+        self.labels.copy_(labels, non_blocking=non_blocking)
+
+    def forward_backward(self):
+        self.k_gemm1()
+        self.k_agg1()
+        self.k_agg2()
+        self.k_gemm2()
+        self.k_xent()
+        self.k_db2()
+        self.k_dW2()
+        self.k_dP2()
+        self.k_norm2()
+        self.k_bagg2()
+        self.k_norm1()
+        self.k_bagg1()
+        self.k_dW1()
+
+    def step(self):
+        self.forward_backward()
+        self.k_adam()
+        return self.loss
+
+    def capture(self):
+        """Record one epoch (fwd+bwd+Adam) as a CUDA graph; replay with run()."""
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            # warm the allocator-free path once outside capture
+            self.forward_backward()
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        self.graph = g
+        return g
+
+    def run(self):
+        if self.graph is None:
+            return self.step()
+        self.graph.replay()
+        return self.loss
+
+    def params(self):
+        return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}
+
+    def grads(self):
+        return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
