@@ -162,22 +162,29 @@ typedef struct gnn_epilogue {
 /* Per-graph SpMM schedule (built once, reused by every call; the build
  * synchronises once to learn the list lengths so that gnn_spmm never does).
  * The nnz range is cut into chunks of edges_per_warp edges, one warp each;
- * rows spanning several chunks ("split" rows, the power-law mega rows) and
- * empty rows are listed for the finishing passes. */
+ * chunk_row[w] is the row holding chunk w's first edge.  Rows spanning
+ * several chunks ("split" rows, the power-law mega rows) are finished by a
+ * two-level fixed-order reduction over tasks of <= 128 partials; empty rows
+ * are listed for the epilogue-only pass.  All arrays live in one caller
+ * buffer of gnn_spmm_plan_buffer_ints() int32 entries. */
 typedef struct gnn_spmm_plan {
-  int64_t edges_per_warp;
-  int64_t num_warps;           /* ceil(nnz / edges_per_warp) */
+  int64_t edges_per_warp;          /* multiple of 4, <= 2048 */
+  int64_t num_warps;               /* ceil(nnz / edges_per_warp) */
+  const int32_t *chunk_row;        /* [num_warps+1] */
   int64_t num_split;
-  const int32_t *split_rows;   /* [num_split], caller-owned device memory */
+  const int32_t *split_rows;       /* [num_split] */
+  const int32_t *split_task_begin; /* [num_split+1] */
+  int64_t num_tasks;
+  const int32_t *task_split;       /* [num_tasks] index into split_rows */
+  const int32_t *task_p0;          /* [num_tasks] first partial of the task */
   int64_t num_empty;
-  const int32_t *empty_rows;   /* [num_empty], caller-owned device memory */
+  const int32_t *empty_rows;       /* [num_empty] */
 } gnn_spmm_plan_t;
 
+size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_per_warp);
 size_t gnn_spmm_plan_workspace(int64_t num_rows);
-/* split_rows / empty_rows: device buffers of num_rows entries each. */
-int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *split_rows,
-                        int32_t *empty_rows, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
-                        gnn_stream_t stream);
+int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *plan_buf,
+                        gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
 /* Y[num_rows,K] = epilogue(A . X), X[num_cols,K].  heads>=1 splits K into
  * `heads` slices scaled by their own edge value (vals is [nnz,heads]).

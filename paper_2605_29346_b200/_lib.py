@@ -74,8 +74,13 @@ class SpmmPlan(C.Structure):
     _fields_ = [
         ("edges_per_warp", c_i64),
         ("num_warps", c_i64),
+        ("chunk_row", c_ptr),
         ("num_split", c_i64),
         ("split_rows", c_ptr),
+        ("split_task_begin", c_ptr),
+        ("num_tasks", c_i64),
+        ("task_split", c_ptr),
+        ("task_p0", c_ptr),
         ("num_empty", c_i64),
         ("empty_rows", c_ptr),
     ]
@@ -111,10 +116,11 @@ SIGNATURES = {
         c_int,
         [c_i64, c_i64, c_ptr, c_u64, c_u64, c_u64, c_u64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_spmm_plan_buffer_ints": (c_sz, [c_i64, c_i64, c_i64]),
     "gnn_spmm_plan_workspace": (c_sz, [c_i64]),
     "gnn_spmm_plan_build": (
         c_int,
-        [C.POINTER(CsrView), c_i64, c_ptr, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
+        [C.POINTER(CsrView), c_i64, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
     ),
     "gnn_spmm_workspace": (c_sz, [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64]),
     "gnn_spmm": (

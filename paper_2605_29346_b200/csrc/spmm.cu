@@ -40,8 +40,14 @@ struct SpmmArgs {
   gnn_epilogue_t epi;
   int64_t P;
   int64_t nwarps;
-  float *slots;  // [nwarps][2][K]
+  const int32_t *chunk_row;  // [nwarps+1]
+  float *slots;              // [nwarps][2][K]
+  int stage;                 // StageMode
+  int bulk_ok;
+  int warp_smem;             // bytes of shared memory per warp
 };
+
+constexpr int64_t kMaxEdgesPerWarp = 2048;
 
 template <int VW>
 struct VecT;
@@ -114,19 +120,21 @@ __device__ __forceinline__ typename VecT<VW>::T epi_vec(typename VecT<VW>::T y, 
   }
 }
 
-// G lanes per group, VPL vectors of VW floats per lane, U-way unrolled edge loop.
-template <int G, int VPL, int VW>
-struct Tile {
-  static constexpr int NG = 32 / G;
-  static constexpr int KB = G * VPL * VW;  // columns covered by one block-column
-};
+// -------------------------------------------------------------- main kernel
+// Per warp: one chunk of P edges.  Lane 0 stages the chunk's column ids (and
+// its edge values or edge ids) into shared memory with a 1-D bulk async copy
+// (the TMA engine) while the warp reads its row bounds; the gather loop then
+// only waits on the feature loads.  U edges per group are in flight per
+// iteration (U*32/G per warp).
+enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
 
 template <int G, int VPL, int VW, bool HAS_VALS>
-__device__ __forceinline__ void seg_sum(const SpmmArgs &a, int64_t es, int64_t ee, int64_t cbase,
-                                        typename VecT<VW>::T (&acc)[VPL]) {
+__device__ __forceinline__ void seg_sum(const SpmmArgs &a, const int32_t *scol, const void *sval,
+                                        int stage, int64_t e0, int64_t es, int64_t ee,
+                                        int64_t cbase, typename VecT<VW>::T (&acc)[VPL]) {
   using V = VecT<VW>;
   constexpr int NG = 32 / G;
-  constexpr int U = 4;
+  constexpr int U = (VPL * VW >= 8) ? 4 : 8;
   const int lane = (int)lane_id();
   const int g = lane / G, gl = lane % G;
 #pragma unroll
@@ -140,18 +148,28 @@ __device__ __forceinline__ void seg_sum(const SpmmArgs &a, int64_t es, int64_t e
     act[v] = col[v] < a.K;
     head[v] = HAS_VALS ? (int)(col[v] / a.F) : 0;
   }
+  const float *__restrict__ X = a.X;
   for (int64_t e = es + g; e < ee; e += (int64_t)NG * U) {
     int32_t c[U];
     float w[U][VPL];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      int64_t ei = e + (int64_t)u * NG;
-      c[u] = ei < ee ? __ldg(a.cols + ei) : -1;
+      const int64_t ei = e + (int64_t)u * NG;
+      const bool in = ei < ee;
+      c[u] = in ? scol[ei - e0] : -1;
       if constexpr (HAS_VALS) {
-        int64_t vi = ei < ee ? (a.eid ? (int64_t)__ldg(a.eid + ei) : ei) : 0;
+        if (stage == STAGE_VALS) {
+          const float wv = in ? static_cast<const float *>(sval)[ei - e0] : 0.f;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          w[u][v] = (ei < ee && act[v]) ? __ldg(a.vals + vi * a.heads + head[v]) : 0.f;
+          for (int v = 0; v < VPL; ++v) w[u][v] = wv;
+        } else {
+          const int64_t vi =
+              in ? (stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[ei - e0] : ei)
+                 : 0;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            w[u][v] = (in && act[v]) ? __ldg(a.vals + vi * a.heads + head[v]) : 0.f;
+        }
       }
     }
     typename V::T x[U][VPL];
@@ -159,7 +177,7 @@ __device__ __forceinline__ void seg_sum(const SpmmArgs &a, int64_t es, int64_t e
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
-        x[u][v] = (c[u] >= 0 && act[v]) ? V::ld(a.X + (int64_t)c[u] * a.ldx + col[v]) : V::zero();
+        x[u][v] = (c[u] >= 0 && act[v]) ? V::ld(X + (int64_t)c[u] * a.ldx + col[v]) : V::zero();
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -200,34 +218,76 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, float *dst, int64_t
   }
 }
 
+__device__ __forceinline__ int64_t shfl_i64(int64_t v, int src) {
+  int lo = __shfl_sync(kFull, (int)(v & 0xffffffff), src);
+  int hi = __shfl_sync(kFull, (int)(v >> 32), src);
+  return ((int64_t)hi << 32) | (uint32_t)lo;
+}
+
 template <int G, int VPL, int VW, bool HAS_VALS>
 __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
+  extern __shared__ __align__(16) uint8_t spmm_smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = (int)lane_id();
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= a.nwarps) return;
+  uint8_t *wbase = spmm_smem + (size_t)warp * a.warp_smem;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);
+  int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);
+  void *sval = scol + a.P;
   const int64_t cbase = (int64_t)blockIdx.y * KB;
   const int64_t e0 = w * a.P;
   const int64_t e1 = min(e0 + a.P, a.nnz);
-  if (e0 >= e1) return;
-  typename V::T acc[VPL];
-  // row containing e0
-  int64_t r = upper_bound_dev(a.offsets, 0, a.R + 1, e0) - 1;
+  const int n = (int)(e1 - e0);
+  const int stage = a.stage;
+
+  // ---- stage this chunk's column ids (+ edge values / ids) into shared memory
+  const int nbulk = a.bulk_ok ? (n & ~3) : 0;  // elements moved by the bulk copy (16B multiple)
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t bytes = (uint32_t)nbulk * 4u;
+    mbar_arrive_expect_tx(bar, stage != STAGE_NONE ? 2u * bytes : bytes);
+    if (bytes) {
+      bulk_g2s(scol, a.cols + e0, bytes, bar);
+      if (stage == STAGE_VALS) bulk_g2s(sval, a.vals + e0, bytes, bar);
+      if (stage == STAGE_EID) bulk_g2s(sval, a.eid + e0, bytes, bar);
+    }
+  }
+  for (int i = nbulk + lane; i < n; i += 32) {
+    scol[i] = a.cols[e0 + i];
+    if (stage == STAGE_VALS) static_cast<float *>(sval)[i] = a.vals[e0 + i];
+    if (stage == STAGE_EID) static_cast<int32_t *>(sval)[i] = a.eid[e0 + i];
+  }
+  // ---- row bounds while the copy is in flight: 32 row ends per batched load
+  int64_t r = a.chunk_row[w];
   int64_t rs = a.offsets[r];
-  int64_t re = a.offsets[r + 1];
+  int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
+  int bi = 0;
+  int64_t re = shfl_i64(obuf, 0);
+  mbar_wait(bar, 0);
+  __syncwarp();
+
+  typename V::T acc[VPL];
   if (rs < e0) {  // carry-in piece of a row owned by an earlier warp
-    int64_t ee = min(re, e1);
-    seg_sum<G, VPL, VW, HAS_VALS>(a, e0, ee, cbase, acc);
+    const int64_t ee = min(re, e1);
+    seg_sum<G, VPL, VW, HAS_VALS>(a, scol, sval, stage, e0, e0, ee, cbase, acc);
     store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
     if (re >= e1) return;
     ++r;
+    ++bi;
     rs = re;
-    re = a.offsets[r + 1];
+    re = shfl_i64(obuf, bi);
   }
   while (rs < e1) {
     if (re > rs) {
-      int64_t ee = min(re, e1);
-      seg_sum<G, VPL, VW, HAS_VALS>(a, rs, ee, cbase, acc);
+      const int64_t ee = min(re, e1);
+      seg_sum<G, VPL, VW, HAS_VALS>(a, scol, sval, stage, e0, rs, ee, cbase, acc);
       if (re <= e1)
         store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
       else
@@ -236,21 +296,37 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
     ++r;
     if (r >= a.R) break;
     rs = re;
-    re = a.offsets[r + 1];
+    if (++bi == 32) {
+      obuf = a.offsets[min(r + 1 + lane, a.R)];
+      bi = 0;
+    }
+    re = shfl_i64(obuf, bi);
   }
 }
 
-// One CTA per split row: sum slot[wa][1], slot[wa+1][0] ... slot[wb][0] in a fixed order.
-__global__ void __launch_bounds__(256) spmm_split_finish_kernel(SpmmArgs a,
-                                                                const int32_t *__restrict__ rows,
-                                                                int64_t nrows) {
-  __shared__ float red[8][33];
-  const int64_t i = blockIdx.x;
-  if (i >= nrows) return;
-  const int64_t r = rows[i];
+// ---------------------------------------------------------- split-row finish
+// Partial j of split row r (spanning warps wa..wb): j==0 -> slot[wa][1],
+// j>=1 -> slot[wa+j][0].  Level 1: one 128-thread CTA per task of <=128
+// partials (fixed order), final store when the row has a single task, else a
+// level-2 partial; level 2: one warp per multi-task row.
+constexpr int kTaskPartials = 128;
+
+__device__ __forceinline__ const float *partial_ptr(const SpmmArgs &a, int64_t wa, int64_t j) {
+  return a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
+}
+
+__global__ void __launch_bounds__(128) spmm_finish1_kernel(SpmmArgs a, gnn_spmm_plan_t p,
+                                                           float *l2) {
+  __shared__ float red[4][33];
+  const int64_t t = blockIdx.x;
+  const int64_t sidx = p.task_split[t];
+  const int64_t r = p.split_rows[sidx];
   const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
   const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
   const int64_t np = wb - wa + 1;
+  const int64_t p0 = p.task_p0[t];
+  const int64_t p1 = min(np, p0 + kTaskPartials);
+  const bool single = (p.split_task_begin[sidx + 1] - p.split_task_begin[sidx]) == 1;
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
   const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
@@ -258,20 +334,36 @@ __global__ void __launch_bounds__(256) spmm_split_finish_kernel(SpmmArgs a,
     const int64_t c = c0 + lane;
     float s = 0.f;
     if (c < a.K) {
-      for (int64_t j = warp; j < np; j += 8) {
-        const float *p = a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
-        s += p[c];
-      }
+#pragma unroll 8
+      for (int64_t j = p0 + warp; j < p1; j += 4) s += partial_ptr(a, wa, j)[c];
     }
     red[warp][lane] = s;
     __syncthreads();
-    if (warp == 0) {
-      float t = red[0][lane];
-#pragma unroll
-      for (int k = 1; k < 8; ++k) t += red[k][lane];
-      if (c < a.K) a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+    if (warp == 0 && c < a.K) {
+      float tsum = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
+      if (single)
+        a.Y[r * a.ldy + c] = epi_scalar(tsum, r, c, a, ns, ps);
+      else
+        l2[t * a.K + c] = tsum;
     }
     __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(32) spmm_finish2_kernel(SpmmArgs a, gnn_spmm_plan_t p,
+                                                          const float *__restrict__ l2) {
+  const int64_t sidx = blockIdx.x;
+  const int64_t tb = p.split_task_begin[sidx], te = p.split_task_begin[sidx + 1];
+  if (te - tb <= 1) return;
+  const int64_t r = p.split_rows[sidx];
+  const int lane = (int)lane_id();
+  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
+  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
+  for (int64_t c = lane; c < a.K; c += 32) {
+    float s = 0.f;
+#pragma unroll 8
+    for (int64_t t = tb; t < te; ++t) s += l2[t * a.K + c];
+    a.Y[r * a.ldy + c] = epi_scalar(s, r, c, a, ns, ps);
   }
 }
 
@@ -288,22 +380,43 @@ __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ r
 }
 
 // ------------------------------------------------------------- planning
+__global__ void plan_chunk_rows_kernel(const int64_t *__restrict__ off, int64_t R, int64_t nnz,
+                                       int64_t P, int64_t nw, int32_t *chunk_row) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= nw;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = w * P;
+    chunk_row[w] = (w == nw || e >= nnz) ? (int32_t)R
+                                         : (int32_t)(upper_bound_dev(off, 0, R + 1, e) - 1);
+  }
+}
 __global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                  int64_t *fsplit, int64_t *fempty) {
+                                  int64_t *fsplit, int64_t *fempty, int64_t *ntask) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t rs = off[r], re = off[r + 1];
     fempty[r] = re == rs ? 1 : 0;
-    fsplit[r] = (re > rs && rs / P != (re - 1) / P) ? 1 : 0;
+    const bool split = re > rs && rs / P != (re - 1) / P;
+    fsplit[r] = split ? 1 : 0;
+    ntask[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kTaskPartials) : 0;
   }
 }
 __global__ void plan_scatter_kernel(int64_t R, const int64_t *__restrict__ us,
-                                    const int64_t *__restrict__ ue, int32_t *split_rows,
-                                    int32_t *empty_rows) {
+                                    const int64_t *__restrict__ ue, const int64_t *__restrict__ ut,
+                                    int32_t *split_rows, int32_t *split_task_begin,
+                                    int32_t *task_split, int32_t *task_p0, int32_t *empty_rows) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    if (us[r + 1] != us[r]) split_rows[us[r]] = (int32_t)r;
+    if (us[r + 1] != us[r]) {
+      const int64_t si = us[r];
+      split_rows[si] = (int32_t)r;
+      split_task_begin[si] = (int32_t)ut[r];
+      for (int64_t t = ut[r]; t < ut[r + 1]; ++t) {
+        task_split[t] = (int32_t)si;
+        task_p0[t] = (int32_t)((t - ut[r]) * kTaskPartials);
+      }
+    }
     if (ue[r + 1] != ue[r]) empty_rows[ue[r]] = (int32_t)r;
+    if (r == 0) split_task_begin[us[R]] = (int32_t)ut[R];
   }
 }
 
@@ -317,15 +430,46 @@ template <int G, int VPL, int VW>
 int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
-  if (has_vals)
-    spmm_main_kernel<G, VPL, VW, true><<<grid, 256, 0, st>>>(a);
-  else
-    spmm_main_kernel<G, VPL, VW, false><<<grid, 256, 0, st>>>(a);
+  const size_t smem = (size_t)a.warp_smem * 8;
+  if (has_vals) {
+    GNN_CUDA_TRY(cudaFuncSetAttribute(spmm_main_kernel<G, VPL, VW, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    spmm_main_kernel<G, VPL, VW, true><<<grid, 256, smem, st>>>(a);
+  } else {
+    GNN_CUDA_TRY(cudaFuncSetAttribute(spmm_main_kernel<G, VPL, VW, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    spmm_main_kernel<G, VPL, VW, false><<<grid, 256, smem, st>>>(a);
+  }
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct PlanLayout {
+  int64_t nw, tmax;
+  int64_t o_chunk, o_split, o_stb, o_tsplit, o_tp0, o_empty, total;
+};
+PlanLayout plan_layout(int64_t R, int64_t nnz, int64_t P) {
+  PlanLayout L;
+  L.nw = ceil_div(nnz, P);
+  L.tmax = R + ceil_div(2 * L.nw, kTaskPartials) + 1;
+  int64_t o = 0;
+  L.o_chunk = o;
+  o += L.nw + 1;
+  L.o_split = o;
+  o += R;
+  L.o_stb = o;
+  o += R + 1;
+  L.o_tsplit = o;
+  o += L.tmax;
+  L.o_tp0 = o;
+  o += L.tmax;
+  L.o_empty = o;
+  o += R;
+  L.total = o;
+  return L;
+}
 
 }  // namespace
 }  // namespace gnn
@@ -334,57 +478,76 @@ using namespace gnn;
 
 extern "C" {
 
+size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_per_warp) {
+  if (edges_per_warp <= 0) return 0;
+  return (size_t)plan_layout(num_rows, nnz, edges_per_warp).total;
+}
+
 size_t gnn_spmm_plan_workspace(int64_t num_rows) {
   WsCounter c;
-  c.take<int64_t>(num_rows + 1);
-  c.take<int64_t>(num_rows + 1);
-  c.used += 2 * (scan_i64_workspace(num_rows) + 256);
+  for (int i = 0; i < 3; ++i) c.take<int64_t>(num_rows + 1);
+  c.used += 3 * (scan_i64_workspace(num_rows) + 256);
   return c.used + 512;
 }
 
-int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *split_rows,
-                        int32_t *empty_rows, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
-                        gnn_stream_t stream) {
-  if (!A || !plan || edges_per_warp <= 0 || A->num_rows < 0 || !A->offsets ||
-      (A->num_rows > 0 && (!split_rows || !empty_rows)))
+int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_spmm_plan_t *plan,
+                        void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (!A || !plan || !buf || P <= 0 || P > kMaxEdgesPerWarp || P % 4 != 0 || A->num_rows < 0 ||
+      !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
-  if (A->num_rows >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 31))
+    return GNN_ERR_UNSUPPORTED;
   if (ws_bytes < gnn_spmm_plan_workspace(A->num_rows)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
   const int64_t R = A->num_rows;
+  const PlanLayout L = plan_layout(R, A->nnz, P);
   WsArena ar(ws, ws_bytes);
   int64_t *fs = ar.take<int64_t>(R + 1);
   int64_t *fe = ar.take<int64_t>(R + 1);
+  int64_t *ft = ar.take<int64_t>(R + 1);
   size_t sb = scan_i64_workspace(R);
   void *s1 = ar.take<char>((int64_t)sb);
   void *s2 = ar.take<char>((int64_t)sb);
+  void *s3 = ar.take<char>((int64_t)sb);
   if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, A->nnz, P, L.nw,
+                                                                 buf + L.o_chunk);
+  GNN_LAUNCH_CHECK();
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, edges_per_warp, fs, fe);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, ft);
     GNN_LAUNCH_CHECK();
   }
   GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
   GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
+  GNN_TRY(exclusive_scan_i64(ft, ft, R, true, s3, sb, st));
   if (R > 0) {
-    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(R, fs, fe, split_rows, empty_rows);
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(R, fs, fe, ft, buf + L.o_split,
+                                                         buf + L.o_stb, buf + L.o_tsplit,
+                                                         buf + L.o_tp0, buf + L.o_empty);
     GNN_LAUNCH_CHECK();
   }
-  int64_t h[2] = {0, 0};
+  int64_t h[3] = {0, 0, 0};
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[0], fs + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[1], fe + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], ft + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaStreamSynchronize(st));
-  plan->edges_per_warp = edges_per_warp;
-  plan->num_warps = ceil_div(A->nnz, edges_per_warp);
+  plan->edges_per_warp = P;
+  plan->num_warps = L.nw;
+  plan->chunk_row = buf + L.o_chunk;
   plan->num_split = h[0];
-  plan->split_rows = split_rows;
+  plan->split_rows = buf + L.o_split;
+  plan->split_task_begin = buf + L.o_stb;
+  plan->num_tasks = h[2];
+  plan->task_split = buf + L.o_tsplit;
+  plan->task_p0 = buf + L.o_tp0;
   plan->num_empty = h[1];
-  plan->empty_rows = empty_rows;
+  plan->empty_rows = buf + L.o_empty;
   return GNN_OK;
 }
 
 size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t K) {
   if (!A || !plan || K <= 0) return 0;
-  return sizeof(float) * (size_t)(plan->num_warps * 2 * K) + 256;
+  return sizeof(float) * (size_t)((plan->num_warps * 2 + plan->num_tasks) * K) + 512;
 }
 
 int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
@@ -395,7 +558,8 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->eid && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
   if (heads > 1 && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+  if (plan->edges_per_warp <= 0 || plan->edges_per_warp > kMaxEdgesPerWarp ||
+      plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   gnn_epilogue_t e{};
   if (epi) e = *epi;
@@ -424,7 +588,13 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   a.epi = e;
   a.P = plan->edges_per_warp;
   a.nwarps = plan->num_warps;
+  a.chunk_row = plan->chunk_row;
   a.slots = static_cast<float *>(ws);
+  float *l2 = a.slots + plan->num_warps * 2 * K;
+  a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
+  a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
+              (a.stage != STAGE_EID || aligned16(A->eid));
+  a.warp_smem = (int)(16 + a.P * 4 * (a.stage != STAGE_NONE ? 2 : 1));
 
   if (a.nwarps > 0) {
     const bool hv = A->vals != nullptr;
@@ -454,9 +624,10 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     }
     GNN_TRY(s);
   }
-  if (plan->num_split > 0) {
-    spmm_split_finish_kernel<<<(unsigned)plan->num_split, 256, 0, st>>>(a, plan->split_rows,
-                                                                      plan->num_split);
+  if (plan->num_tasks > 0) {
+    spmm_finish1_kernel<<<(unsigned)plan->num_tasks, 128, 0, st>>>(a, *plan, l2);
+    GNN_LAUNCH_CHECK();
+    spmm_finish2_kernel<<<(unsigned)plan->num_split, 32, 0, st>>>(a, *plan, l2);
     GNN_LAUNCH_CHECK();
   }
   if (plan->num_empty > 0) {

@@ -67,7 +67,7 @@ def _default_edges_per_warp(nnz: int, sms: int) -> int:
     """Chunk length of the SpMM schedule: long chunks amortise per-warp setup,
     but there must be enough warps to fill every SM several times."""
     p = 1024
-    while p > 32 and nnz // p < sms * 64:
+    while p > 64 and nnz // p < sms * 64:
         p //= 2
     return p
 
@@ -116,18 +116,17 @@ class SparseOperand:
             return self._plans[key][0]
         dev = self.device
         with torch.cuda.device(dev):
-            split = torch.empty(max(self.num_rows, 1), dtype=torch.int32, device=dev)
-            empty = torch.empty(max(self.num_rows, 1), dtype=torch.int32, device=dev)
+            nint = lib.gnn_spmm_plan_buffer_ints(self.num_rows, self.nnz, key)
+            buf = torch.empty(max(int(nint), 1), dtype=torch.int32, device=dev)
             ws = _lib.workspace(lib.gnn_spmm_plan_workspace(self.num_rows), dev)
             plan = _lib.SpmmPlan()
             view = self.view()
             _lib.check(
-                lib.gnn_spmm_plan_build(C.byref(view), key, split.data_ptr(), empty.data_ptr(),
-                                        C.byref(plan), ws.data_ptr(), ws.numel(),
-                                        _lib.stream_handle(dev)),
+                lib.gnn_spmm_plan_build(C.byref(view), key, buf.data_ptr(), C.byref(plan),
+                                        ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
                 "spmm plan",
             )
-        self._plans[key] = (plan, split, empty)
+        self._plans[key] = (plan, buf)
         return plan
 
     def nbytes(self) -> int:
@@ -136,8 +135,8 @@ class SparseOperand:
             n += self.vals.numel() * self.vals.element_size()
         if self.eid is not None:
             n += self.eid.numel() * 4
-        for _, s, e in self._plans.values():
-            n += (s.numel() + e.numel()) * 4
+        for _, buf in self._plans.values():
+            n += buf.numel() * 4
         return n
 
 
