@@ -91,11 +91,32 @@ __device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
   return v;
 }
 
-__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
-  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+// Packed fp32 pair arithmetic (sm_100 FADD2 / FFMA2): two lanes of a float4 per instruction.
+__device__ __forceinline__ unsigned long long f2_bits(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
 }
+__device__ __forceinline__ void f2_unbits(unsigned long long b, float &lo, float &hi) {
+  lo = __uint_as_float((unsigned)(b & 0xffffffffull));
+  hi = __uint_as_float((unsigned)(b >> 32));
+}
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  unsigned long long r0, r1;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r0) : "l"(f2_bits(a.x, a.y)), "l"(f2_bits(b.x, b.y)));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r1) : "l"(f2_bits(a.z, a.w)), "l"(f2_bits(b.z, b.w)));
+  float4 o;
+  f2_unbits(r0, o.x, o.y);
+  f2_unbits(r1, o.z, o.w);
+  return o;
+}
+// a + s * b
 __device__ __forceinline__ float4 f4_fma(float s, float4 b, float4 a) {
-  return make_float4(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y), fmaf(s, b.z, a.z), fmaf(s, b.w, a.w));
+  unsigned long long r0, r1, ss = f2_bits(s, s);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r0) : "l"(ss), "l"(f2_bits(b.x, b.y)), "l"(f2_bits(a.x, a.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r1) : "l"(ss), "l"(f2_bits(b.z, b.w)), "l"(f2_bits(a.z, a.w)));
+  float4 o;
+  f2_unbits(r0, o.x, o.y);
+  f2_unbits(r1, o.z, o.w);
+  return o;
 }
 
 // First index i in [lo,hi) with a[i] > x (upper bound), a nondecreasing.

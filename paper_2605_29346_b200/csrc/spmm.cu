@@ -128,65 +128,87 @@ __device__ __forceinline__ typename VecT<VW>::T epi_vec(typename VecT<VW>::T y, 
 // iteration (U*32/G per warp).
 enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
 
+// Lane-invariant part of the gather: per-vector base pointers (column offset
+// folded in; columns past K are clamped to column 0 and simply not stored).
+template <int G, int VPL, int VW>
+struct LaneCols {
+  const char *xb[VPL];
+  int head[VPL];
+  __device__ __forceinline__ LaneCols(const SpmmArgs &a, int64_t cbase) {
+    const int gl = (int)lane_id() % G;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      int64_t col = cbase + (int64_t)(v * G + gl) * VW;
+      if (col >= a.K) col = 0;
+      xb[v] = reinterpret_cast<const char *>(a.X + col);
+      head[v] = (int)(col / a.F);
+    }
+  }
+};
+
+template <int VW>
+__device__ __forceinline__ typename VecT<VW>::T gather(const char *xb, int32_t c, uint32_t ldxb) {
+  return VecT<VW>::ld(reinterpret_cast<const float *>(xb + (uint64_t)(uint32_t)c * ldxb));
+}
+
+// acc[v] = sum over this group's edges of w_e * X[c_e, cols of v]; chunk-local
+// edge indices [is, ie); group g takes is+g, is+g+NG, ...  Summation order is
+// fixed by (G, U), hence deterministic.
 template <int G, int VPL, int VW, bool HAS_VALS>
-__device__ __forceinline__ void seg_sum(const SpmmArgs &a, const int32_t *scol, const void *sval,
-                                        int stage, int64_t e0, int64_t es, int64_t ee,
-                                        int64_t cbase, typename VecT<VW>::T (&acc)[VPL]) {
+__device__ __forceinline__ void seg_sum(const SpmmArgs &a, const LaneCols<G, VPL, VW> &lc,
+                                        const int32_t *scol, const void *sval, int stage,
+                                        int64_t e0, int is, int ie,
+                                        typename VecT<VW>::T (&acc)[VPL]) {
   using V = VecT<VW>;
   constexpr int NG = 32 / G;
   constexpr int U = (VPL * VW >= 8) ? 4 : 8;
-  const int lane = (int)lane_id();
-  const int g = lane / G, gl = lane % G;
+  const int g = (int)lane_id() / G;
+  const uint32_t ldxb = (uint32_t)a.ldx * 4u;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
-  int64_t col[VPL];
-  bool act[VPL];
-  int head[VPL];
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    col[v] = cbase + (int64_t)(v * G + gl) * VW;
-    act[v] = col[v] < a.K;
-    head[v] = HAS_VALS ? (int)(col[v] / a.F) : 0;
-  }
-  const float *__restrict__ X = a.X;
-  for (int64_t e = es + g; e < ee; e += (int64_t)NG * U) {
+  auto weight = [&](int i, int v) -> float {
+    if (stage == STAGE_VALS) return static_cast<const float *>(sval)[i];
+    const int64_t vi =
+        stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[i] : e0 + i;
+    return __ldg(a.vals + vi * a.heads + lc.head[v]);
+  };
+  int i = is + g;
+  for (; i + (U - 1) * NG < ie; i += NG * U) {  // full blocks: no bounds predicates
     int32_t c[U];
-    float w[U][VPL];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t ei = e + (int64_t)u * NG;
-      const bool in = ei < ee;
-      c[u] = in ? scol[ei - e0] : -1;
-      if constexpr (HAS_VALS) {
-        if (stage == STAGE_VALS) {
-          const float wv = in ? static_cast<const float *>(sval)[ei - e0] : 0.f;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) w[u][v] = wv;
-        } else {
-          const int64_t vi =
-              in ? (stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[ei - e0] : ei)
-                 : 0;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            w[u][v] = (in && act[v]) ? __ldg(a.vals + vi * a.heads + head[v]) : 0.f;
-        }
-      }
-    }
+    for (int u = 0; u < U; ++u) c[u] = scol[i + u * NG];
     typename V::T x[U][VPL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        x[u][v] = (c[u] >= 0 && act[v]) ? V::ld(X + (int64_t)c[u] * a.ldx + col[v]) : V::zero();
+      for (int v = 0; v < VPL; ++v) x[u][v] = gather<VW>(lc.xb[v], c[u], ldxb);
+    if constexpr (HAS_VALS) {
+      float w[U][VPL];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        if constexpr (HAS_VALS)
-          acc[v] = V::fma(w[u][v], x[u][v], acc[v]);
-        else
-          acc[v] = V::add(acc[v], x[u][v]);
-      }
+        for (int v = 0; v < VPL; ++v) w[u][v] = weight(i + u * NG, v);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::fma(w[u][v], x[u][v], acc[v]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::add(acc[v], x[u][v]);
+    }
+  }
+  for (; i < ie; i += NG) {  // tail: < U edges per group
+    const int32_t c = scol[i];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      typename V::T x = gather<VW>(lc.xb[v], c, ldxb);
+      if constexpr (HAS_VALS)
+        acc[v] = V::fma(weight(i, v), x, acc[v]);
+      else
+        acc[v] = V::add(acc[v], x);
+    }
   }
 #pragma unroll
   for (int o = G; o < 32; o <<= 1)
@@ -274,9 +296,10 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   __syncwarp();
 
   typename V::T acc[VPL];
+  const LaneCols<G, VPL, VW> lc(a, cbase);
   if (rs < e0) {  // carry-in piece of a row owned by an earlier warp
     const int64_t ee = min(re, e1);
-    seg_sum<G, VPL, VW, HAS_VALS>(a, scol, sval, stage, e0, e0, ee, cbase, acc);
+    seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, 0, (int)(ee - e0), acc);
     store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
     if (re >= e1) return;
     ++r;
@@ -287,7 +310,8 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   while (rs < e1) {
     if (re > rs) {
       const int64_t ee = min(re, e1);
-      seg_sum<G, VPL, VW, HAS_VALS>(a, scol, sval, stage, e0, rs, ee, cbase, acc);
+      seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, (int)(rs - e0), (int)(ee - e0),
+                                    acc);
       if (re <= e1)
         store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
       else
