@@ -162,21 +162,22 @@ typedef struct gnn_epilogue {
 /* Per-graph SpMM schedule (built once, reused by every call; the build
  * synchronises once to learn the list lengths so that gnn_spmm never does).
  * The nnz range is cut into chunks of edges_per_warp edges, one warp each;
- * chunk_row[w] is the row holding chunk w's first edge.  Rows spanning
- * several chunks ("split" rows, the power-law mega rows) are finished by a
- * two-level fixed-order reduction over tasks of <= 128 partials; empty rows
- * are listed for the epilogue-only pass.  All arrays live in one caller
- * buffer of gnn_spmm_plan_buffer_ints() int32 entries. */
+ * chunk_row[w] is the row holding chunk w's first edge.  A row spanning
+ * several chunks ("split" row) is finished inside the SpMM kernel by the last
+ * warp to deliver a partial (fence + arrival counter; partials summed in a
+ * fixed two-level order, groups of 64).  Empty rows are listed for the
+ * epilogue-only pass.  All arrays live in one caller buffer of
+ * gnn_spmm_plan_buffer_ints() int32 entries; the plan is read-only, so one
+ * plan may serve concurrent calls on different streams. */
 typedef struct gnn_spmm_plan {
   int64_t edges_per_warp;          /* multiple of 4, <= 2048 */
   int64_t num_warps;               /* ceil(nnz / edges_per_warp) */
   const int32_t *chunk_row;        /* [num_warps+1] */
+  const int32_t *chunk_split;      /* [2*num_warps] split index of carry-in / trailing row or -1 */
   int64_t num_split;
   const int32_t *split_rows;       /* [num_split] */
-  const int32_t *split_task_begin; /* [num_split+1] */
-  int64_t num_tasks;
-  const int32_t *task_split;       /* [num_tasks] index into split_rows */
-  const int32_t *task_p0;          /* [num_tasks] first partial of the task */
+  const int32_t *split_group_base; /* [num_split+1] prefix of ceil(partials/64) */
+  int64_t num_groups;
   int64_t num_empty;
   const int32_t *empty_rows;       /* [num_empty] */
 } gnn_spmm_plan_t;

@@ -75,12 +75,11 @@ class SpmmPlan(C.Structure):
         ("edges_per_warp", c_i64),
         ("num_warps", c_i64),
         ("chunk_row", c_ptr),
+        ("chunk_split", c_ptr),
         ("num_split", c_i64),
         ("split_rows", c_ptr),
-        ("split_task_begin", c_ptr),
-        ("num_tasks", c_i64),
-        ("task_split", c_ptr),
-        ("task_p0", c_ptr),
+        ("split_group_base", c_ptr),
+        ("num_groups", c_i64),
         ("num_empty", c_i64),
         ("empty_rows", c_ptr),
     ]

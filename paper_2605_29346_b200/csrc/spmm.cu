@@ -40,8 +40,14 @@ struct SpmmArgs {
   gnn_epilogue_t epi;
   int64_t P;
   int64_t nwarps;
-  const int32_t *chunk_row;  // [nwarps+1]
-  float *slots;              // [nwarps][2][K]
+  const int32_t *chunk_row;    // [nwarps+1]
+  const int32_t *chunk_split;  // [2*nwarps]: split index of carry-in / trailing row, or -1
+  const int32_t *split_rows;
+  const int32_t *split_group_base;  // [num_split+1]
+  int *cnt1;                   // [num_groups] level-1 arrival counters (zeroed per call)
+  int *cnt2;                   // [num_split]  level-2 arrival counters
+  float *l2;                   // [num_groups][K] level-2 partials
+  float *slots;                // [nwarps][2][K]
   int stage;                 // StageMode
   int bulk_ok;
   int warp_smem;             // bytes of shared memory per warp
@@ -246,6 +252,71 @@ __device__ __forceinline__ int64_t shfl_i64(int64_t v, int src) {
   return ((int64_t)hi << 32) | (uint32_t)lo;
 }
 
+// ---------------------------------------------------------- split rows
+// Partial j of split row s (spanning warps wa..wb, np = wb-wa+1): j==0 ->
+// slot[wa][1], j>=1 -> slot[wa+j][0].  Partials are grouped by 64; the last
+// warp to arrive at a group (fence + counter) sums the group in fixed order,
+// and the last group to finish sums the group sums in fixed order and applies
+// the epilogue.  Which warp arrives last varies, the summation order does not:
+// results are deterministic.
+constexpr int kGroupPartials = 64;
+
+__device__ __forceinline__ const float *partial_ptr(const SpmmArgs &a, int64_t wa, int64_t j) {
+  return a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
+}
+
+// Called by a whole warp right after it stored partial j of split row s.
+__device__ __noinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t j) {
+  const int lane = (int)lane_id();
+  const int64_t r = a.split_rows[s];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  const int64_t np = wb - wa + 1;
+  const int64_t gi = j / kGroupPartials;
+  const int64_t ng = ceil_div(np, kGroupPartials);
+  const int64_t gbase = a.split_group_base[s];
+  const int64_t rem = np - gi * kGroupPartials;
+  const int m = (int)(rem < kGroupPartials ? rem : kGroupPartials);
+  __threadfence();  // every lane publishes its part of the partial before the arrival
+  __syncwarp();
+  int old = 0;
+  if (lane == 0) old = atomicAdd(&a.cnt1[gbase + gi], 1);
+  old = __shfl_sync(kFull, old, 0);
+  if (old != m - 1) return;
+  __threadfence();
+  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
+  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
+  const int64_t j0 = gi * kGroupPartials;
+  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
+    const int64_t c = c0 + lane;
+    if (c < a.K) {
+      float t = 0.f;
+#pragma unroll 8
+      for (int k = 0; k < m; ++k) t += __ldcg(partial_ptr(a, wa, j0 + k) + c);
+      if (ng == 1)
+        a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+      else
+        a.l2[(gbase + gi) * a.K + c] = t;
+    }
+  }
+  if (ng == 1) return;
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) old = atomicAdd(&a.cnt2[s], 1);
+  old = __shfl_sync(kFull, old, 0);
+  if (old != (int)ng - 1) return;
+  __threadfence();
+  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
+    const int64_t c = c0 + lane;
+    if (c < a.K) {
+      float t = 0.f;
+#pragma unroll 8
+      for (int64_t g2 = 0; g2 < ng; ++g2) t += __ldcg(a.l2 + (gbase + g2) * a.K + c);
+      a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+    }
+  }
+}
+
 template <int G, int VPL, int VW, bool HAS_VALS>
 __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
@@ -292,6 +363,8 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
   int bi = 0;
   int64_t re = shfl_i64(obuf, 0);
+  const int split_in = a.chunk_split[2 * w];
+  const int split_out = a.chunk_split[2 * w + 1];
   mbar_wait(bar, 0);
   __syncwarp();
 
@@ -301,6 +374,8 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
     const int64_t ee = min(re, e1);
     seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, 0, (int)(ee - e0), acc);
     store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+    __syncwarp();
+    split_arrive(a, split_in, w - rs / a.P);
     if (re >= e1) return;
     ++r;
     ++bi;
@@ -312,10 +387,14 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
       const int64_t ee = min(re, e1);
       seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, (int)(rs - e0), (int)(ee - e0),
                                     acc);
-      if (re <= e1)
+      if (re <= e1) {
         store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
-      else
+      } else {
         store_row<G, VPL, VW>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
+        __syncwarp();
+        split_arrive(a, split_out, 0);
+        return;
+      }
     }
     ++r;
     if (r >= a.R) break;
@@ -325,69 +404,6 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
       bi = 0;
     }
     re = shfl_i64(obuf, bi);
-  }
-}
-
-// ---------------------------------------------------------- split-row finish
-// Partial j of split row r (spanning warps wa..wb): j==0 -> slot[wa][1],
-// j>=1 -> slot[wa+j][0].  Level 1: one 128-thread CTA per task of <=128
-// partials (fixed order), final store when the row has a single task, else a
-// level-2 partial; level 2: one warp per multi-task row.
-constexpr int kTaskPartials = 128;
-
-__device__ __forceinline__ const float *partial_ptr(const SpmmArgs &a, int64_t wa, int64_t j) {
-  return a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
-}
-
-__global__ void __launch_bounds__(128) spmm_finish1_kernel(SpmmArgs a, gnn_spmm_plan_t p,
-                                                           float *l2) {
-  __shared__ float red[4][33];
-  const int64_t t = blockIdx.x;
-  const int64_t sidx = p.task_split[t];
-  const int64_t r = p.split_rows[sidx];
-  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
-  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
-  const int64_t np = wb - wa + 1;
-  const int64_t p0 = p.task_p0[t];
-  const int64_t p1 = min(np, p0 + kTaskPartials);
-  const bool single = (p.split_task_begin[sidx + 1] - p.split_task_begin[sidx]) == 1;
-  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
-  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
-  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
-    const int64_t c = c0 + lane;
-    float s = 0.f;
-    if (c < a.K) {
-#pragma unroll 8
-      for (int64_t j = p0 + warp; j < p1; j += 4) s += partial_ptr(a, wa, j)[c];
-    }
-    red[warp][lane] = s;
-    __syncthreads();
-    if (warp == 0 && c < a.K) {
-      float tsum = ((red[0][lane] + red[1][lane]) + red[2][lane]) + red[3][lane];
-      if (single)
-        a.Y[r * a.ldy + c] = epi_scalar(tsum, r, c, a, ns, ps);
-      else
-        l2[t * a.K + c] = tsum;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(32) spmm_finish2_kernel(SpmmArgs a, gnn_spmm_plan_t p,
-                                                          const float *__restrict__ l2) {
-  const int64_t sidx = blockIdx.x;
-  const int64_t tb = p.split_task_begin[sidx], te = p.split_task_begin[sidx + 1];
-  if (te - tb <= 1) return;
-  const int64_t r = p.split_rows[sidx];
-  const int lane = (int)lane_id();
-  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
-  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
-  for (int64_t c = lane; c < a.K; c += 32) {
-    float s = 0.f;
-#pragma unroll 8
-    for (int64_t t = tb; t < te; ++t) s += l2[t * a.K + c];
-    a.Y[r * a.ldy + c] = epi_scalar(s, r, c, a, ns, ps);
   }
 }
 
@@ -414,33 +430,33 @@ __global__ void plan_chunk_rows_kernel(const int64_t *__restrict__ off, int64_t 
   }
 }
 __global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                  int64_t *fsplit, int64_t *fempty, int64_t *ntask) {
+                                  int64_t *fsplit, int64_t *fempty, int64_t *ngroups) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t rs = off[r], re = off[r + 1];
     fempty[r] = re == rs ? 1 : 0;
     const bool split = re > rs && rs / P != (re - 1) / P;
     fsplit[r] = split ? 1 : 0;
-    ntask[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kTaskPartials) : 0;
+    ngroups[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kGroupPartials) : 0;
   }
 }
-__global__ void plan_scatter_kernel(int64_t R, const int64_t *__restrict__ us,
-                                    const int64_t *__restrict__ ue, const int64_t *__restrict__ ut,
-                                    int32_t *split_rows, int32_t *split_task_begin,
-                                    int32_t *task_split, int32_t *task_p0, int32_t *empty_rows) {
+__global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
+                                    const int64_t *__restrict__ us, const int64_t *__restrict__ ue,
+                                    const int64_t *__restrict__ ug, int32_t *split_rows,
+                                    int32_t *split_group_base, int32_t *chunk_split,
+                                    int32_t *empty_rows) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     if (us[r + 1] != us[r]) {
       const int64_t si = us[r];
       split_rows[si] = (int32_t)r;
-      split_task_begin[si] = (int32_t)ut[r];
-      for (int64_t t = ut[r]; t < ut[r + 1]; ++t) {
-        task_split[t] = (int32_t)si;
-        task_p0[t] = (int32_t)((t - ut[r]) * kTaskPartials);
-      }
+      split_group_base[si] = (int32_t)ug[r];
+      const int64_t wa = off[r] / P, wb = (off[r + 1] - 1) / P;
+      chunk_split[2 * wa + 1] = (int32_t)si;  // trailing partial of the owner chunk
+      for (int64_t w = wa + 1; w <= wb; ++w) chunk_split[2 * w] = (int32_t)si;  // carry-ins
     }
     if (ue[r + 1] != ue[r]) empty_rows[ue[r]] = (int32_t)r;
-    if (r == 0) split_task_begin[us[R]] = (int32_t)ut[R];
+    if (r == 0) split_group_base[us[R]] = (int32_t)ug[R];
   }
 }
 
@@ -455,15 +471,15 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
   const size_t smem = (size_t)a.warp_smem * 8;
-  if (has_vals) {
-    GNN_CUDA_TRY(cudaFuncSetAttribute(spmm_main_kernel<G, VPL, VW, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    spmm_main_kernel<G, VPL, VW, true><<<grid, 256, smem, st>>>(a);
-  } else {
-    GNN_CUDA_TRY(cudaFuncSetAttribute(spmm_main_kernel<G, VPL, VW, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    spmm_main_kernel<G, VPL, VW, false><<<grid, 256, smem, st>>>(a);
-  }
+  // Shared memory only holds the staged index chunks; give the rest of the
+  // unified L1/shared array to L1 so hot feature rows stay cached.
+  auto kern = has_vals ? spmm_main_kernel<G, VPL, VW, true> : spmm_main_kernel<G, VPL, VW, false>;
+  GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm_kb = (int)((smem * 8 + 1023) / 1024);  // up to 8 resident CTAs
+  const int carve = per_sm_kb * 100 / 228 + 1;
+  GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    carve > 100 ? 100 : carve));
+  kern<<<grid, 256, smem, st>>>(a);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -471,24 +487,21 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct PlanLayout {
-  int64_t nw, tmax;
-  int64_t o_chunk, o_split, o_stb, o_tsplit, o_tp0, o_empty, total;
+  int64_t nw;
+  int64_t o_chunk, o_csplit, o_split, o_sgb, o_empty, total;
 };
 PlanLayout plan_layout(int64_t R, int64_t nnz, int64_t P) {
   PlanLayout L;
   L.nw = ceil_div(nnz, P);
-  L.tmax = R + ceil_div(2 * L.nw, kTaskPartials) + 1;
   int64_t o = 0;
   L.o_chunk = o;
   o += L.nw + 1;
+  L.o_csplit = o;
+  o += 2 * L.nw;
   L.o_split = o;
   o += R;
-  L.o_stb = o;
+  L.o_sgb = o;
   o += R + 1;
-  L.o_tsplit = o;
-  o += L.tmax;
-  L.o_tp0 = o;
-  o += L.tmax;
   L.o_empty = o;
   o += R;
   L.total = o;
@@ -519,7 +532,7 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   if (!A || !plan || !buf || P <= 0 || P > kMaxEdgesPerWarp || P % 4 != 0 || A->num_rows < 0 ||
       !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
-  if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 31))
+  if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 30))
     return GNN_ERR_UNSUPPORTED;
   if (ws_bytes < gnn_spmm_plan_workspace(A->num_rows)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
@@ -528,7 +541,7 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   WsArena ar(ws, ws_bytes);
   int64_t *fs = ar.take<int64_t>(R + 1);
   int64_t *fe = ar.take<int64_t>(R + 1);
-  int64_t *ft = ar.take<int64_t>(R + 1);
+  int64_t *fg = ar.take<int64_t>(R + 1);
   size_t sb = scan_i64_workspace(R);
   void *s1 = ar.take<char>((int64_t)sb);
   void *s2 = ar.take<char>((int64_t)sb);
@@ -537,41 +550,54 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, A->nnz, P, L.nw,
                                                                  buf + L.o_chunk);
   GNN_LAUNCH_CHECK();
+  if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, ft);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg);
     GNN_LAUNCH_CHECK();
   }
   GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
   GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
-  GNN_TRY(exclusive_scan_i64(ft, ft, R, true, s3, sb, st));
+  GNN_TRY(exclusive_scan_i64(fg, fg, R, true, s3, sb, st));
   if (R > 0) {
-    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(R, fs, fe, ft, buf + L.o_split,
-                                                         buf + L.o_stb, buf + L.o_tsplit,
-                                                         buf + L.o_tp0, buf + L.o_empty);
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg,
+                                                         buf + L.o_split, buf + L.o_sgb,
+                                                         buf + L.o_csplit, buf + L.o_empty);
     GNN_LAUNCH_CHECK();
   }
   int64_t h[3] = {0, 0, 0};
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[0], fs + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[1], fe + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], ft + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], fg + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaStreamSynchronize(st));
   plan->edges_per_warp = P;
   plan->num_warps = L.nw;
   plan->chunk_row = buf + L.o_chunk;
+  plan->chunk_split = buf + L.o_csplit;
   plan->num_split = h[0];
   plan->split_rows = buf + L.o_split;
-  plan->split_task_begin = buf + L.o_stb;
-  plan->num_tasks = h[2];
-  plan->task_split = buf + L.o_tsplit;
-  plan->task_p0 = buf + L.o_tp0;
+  plan->split_group_base = buf + L.o_sgb;
+  plan->num_groups = h[2];
   plan->num_empty = h[1];
   plan->empty_rows = buf + L.o_empty;
   return GNN_OK;
 }
 
+static size_t spmm_ws_layout(const gnn_spmm_plan_t *plan, int64_t K, size_t *o_slots, size_t *o_l2,
+                             size_t *o_cnt) {
+  WsCounter c;
+  *o_slots = 0;
+  c.take<float>(plan->num_warps * 2 * K);
+  *o_l2 = align_up(c.used, 256);
+  c.take<float>(plan->num_groups * K);
+  *o_cnt = align_up(c.used, 256);
+  c.take<int>(plan->num_groups + plan->num_split);
+  return c.used + 256;
+}
+
 size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t K) {
   if (!A || !plan || K <= 0) return 0;
-  return sizeof(float) * (size_t)((plan->num_warps * 2 + plan->num_tasks) * K) + 512;
+  size_t a, b, c;
+  return spmm_ws_layout(plan, K, &a, &b, &c);
 }
 
 int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
@@ -613,8 +639,18 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   a.P = plan->edges_per_warp;
   a.nwarps = plan->num_warps;
   a.chunk_row = plan->chunk_row;
-  a.slots = static_cast<float *>(ws);
-  float *l2 = a.slots + plan->num_warps * 2 * K;
+  a.chunk_split = plan->chunk_split;
+  a.split_rows = plan->split_rows;
+  a.split_group_base = plan->split_group_base;
+  size_t o_slots, o_l2, o_cnt;
+  spmm_ws_layout(plan, K, &o_slots, &o_l2, &o_cnt);
+  char *wsb = static_cast<char *>(ws);
+  a.slots = reinterpret_cast<float *>(wsb + o_slots);
+  a.l2 = reinterpret_cast<float *>(wsb + o_l2);
+  a.cnt1 = reinterpret_cast<int *>(wsb + o_cnt);
+  a.cnt2 = a.cnt1 + plan->num_groups;
+  if (plan->num_groups + plan->num_split > 0)
+    GNN_CUDA_TRY(cudaMemsetAsync(a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split), st));
   a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
@@ -647,12 +683,6 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
         s = launch_main<32, 4, 1>(a, hv, st);  // 128 columns per block-column
     }
     GNN_TRY(s);
-  }
-  if (plan->num_tasks > 0) {
-    spmm_finish1_kernel<<<(unsigned)plan->num_tasks, 128, 0, st>>>(a, *plan, l2);
-    GNN_LAUNCH_CHECK();
-    spmm_finish2_kernel<<<(unsigned)plan->num_split, 32, 0, st>>>(a, *plan, l2);
-    GNN_LAUNCH_CHECK();
   }
   if (plan->num_empty > 0) {
     spmm_empty_rows_kernel<<<grid_1d(plan->num_empty * K, 256), 256, 0, st>>>(a, plan->empty_rows,
