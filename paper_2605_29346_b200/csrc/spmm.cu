@@ -46,6 +46,7 @@ struct SpmmArgs {
   const int32_t *split_group_base;  // [num_split+1]
   int *cnt1;                   // [num_groups] level-1 arrival counters (zeroed per call)
   int *cnt2;                   // [num_split]  level-2 arrival counters
+  int64_t ncb;                 // column blocks (gridDim.y); counters are per column block
   float *l2;                   // [num_groups][K] level-2 partials
   float *slots;                // [nwarps][2][K]
   int stage;                 // StageMode
@@ -265,8 +266,26 @@ __device__ __forceinline__ const float *partial_ptr(const SpmmArgs &a, int64_t w
   return a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K;
 }
 
-// Called by a whole warp right after it stored partial j of split row s.
-__device__ __noinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t j) {
+// Arrival: release-ordered atomic (MEMBAR.ALL.GPU + ATOMG, no L1 invalidate —
+// a gpu-scope acquire/sc fence would flush the SM's L1 and with it the
+// feature rows the other warps are reusing).  The last arriver reads the
+// partials with strong relaxed loads served by L2, the point of coherence,
+// issued under a control dependency on the atomic's result.
+__device__ __forceinline__ int atom_add_release_gpu(int *p, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ float ld_relaxed_gpu(const float *p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Called by a whole warp right after it stored partial j of split row s for
+// the column block [cbase, cbase+kb).
+__device__ __noinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t j, int64_t cbase,
+                                          int kb) {
   const int lane = (int)lane_id();
   const int64_t r = a.split_rows[s];
   const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
@@ -277,43 +296,34 @@ __device__ __noinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t 
   const int64_t gbase = a.split_group_base[s];
   const int64_t rem = np - gi * kGroupPartials;
   const int m = (int)(rem < kGroupPartials ? rem : kGroupPartials);
-  __threadfence();  // every lane publishes its part of the partial before the arrival
-  __syncwarp();
+  const int64_t cend = min(cbase + (int64_t)kb, a.K);
+  __syncwarp();  // the partial's lanes happen-before lane 0's release
   int old = 0;
-  if (lane == 0) old = atomicAdd(&a.cnt1[gbase + gi], 1);
+  if (lane == 0) old = atom_add_release_gpu(&a.cnt1[(gbase + gi) * a.ncb + blockIdx.y], 1);
   old = __shfl_sync(kFull, old, 0);
   if (old != m - 1) return;
-  __threadfence();
   const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
   const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
   const int64_t j0 = gi * kGroupPartials;
-  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
-    const int64_t c = c0 + lane;
-    if (c < a.K) {
-      float t = 0.f;
+  for (int64_t c = cbase + lane; c < cend; c += 32) {
+    float t = 0.f;
 #pragma unroll 8
-      for (int k = 0; k < m; ++k) t += __ldcg(partial_ptr(a, wa, j0 + k) + c);
-      if (ng == 1)
-        a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
-      else
-        a.l2[(gbase + gi) * a.K + c] = t;
-    }
+    for (int k = 0; k < m; ++k) t += ld_relaxed_gpu(partial_ptr(a, wa, j0 + k) + c);
+    if (ng == 1)
+      a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+    else
+      a.l2[(gbase + gi) * a.K + c] = t;
   }
   if (ng == 1) return;
-  __threadfence();
   __syncwarp();
-  if (lane == 0) old = atomicAdd(&a.cnt2[s], 1);
+  if (lane == 0) old = atom_add_release_gpu(&a.cnt2[s * a.ncb + blockIdx.y], 1);
   old = __shfl_sync(kFull, old, 0);
   if (old != (int)ng - 1) return;
-  __threadfence();
-  for (int64_t c0 = 0; c0 < a.K; c0 += 32) {
-    const int64_t c = c0 + lane;
-    if (c < a.K) {
-      float t = 0.f;
+  for (int64_t c = cbase + lane; c < cend; c += 32) {
+    float t = 0.f;
 #pragma unroll 8
-      for (int64_t g2 = 0; g2 < ng; ++g2) t += __ldcg(a.l2 + (gbase + g2) * a.K + c);
-      a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
-    }
+    for (int64_t g2 = 0; g2 < ng; ++g2) t += ld_relaxed_gpu(a.l2 + (gbase + g2) * a.K + c);
+    a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
   }
 }
 
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
     seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, 0, (int)(ee - e0), acc);
     store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
     __syncwarp();
-    split_arrive(a, split_in, w - rs / a.P);
+    split_arrive(a, split_in, w - rs / a.P, cbase, KB);
     if (re >= e1) return;
     ++r;
     ++bi;
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
       } else {
         store_row<G, VPL, VW>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
         __syncwarp();
-        split_arrive(a, split_out, 0);
+        split_arrive(a, split_out, 0, cbase, KB);
         return;
       }
     }
@@ -582,6 +592,9 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   return GNN_OK;
 }
 
+// Upper bound on gridDim.y of the main kernel (column blocks of >= 128 columns).
+static int64_t spmm_column_blocks(int64_t K) { return ceil_div(K, 128); }
+
 static size_t spmm_ws_layout(const gnn_spmm_plan_t *plan, int64_t K, size_t *o_slots, size_t *o_l2,
                              size_t *o_cnt) {
   WsCounter c;
@@ -590,7 +603,7 @@ static size_t spmm_ws_layout(const gnn_spmm_plan_t *plan, int64_t K, size_t *o_s
   *o_l2 = align_up(c.used, 256);
   c.take<float>(plan->num_groups * K);
   *o_cnt = align_up(c.used, 256);
-  c.take<int>(plan->num_groups + plan->num_split);
+  c.take<int>((plan->num_groups + plan->num_split) * spmm_column_blocks(K));
   return c.used + 256;
 }
 
@@ -647,10 +660,12 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   char *wsb = static_cast<char *>(ws);
   a.slots = reinterpret_cast<float *>(wsb + o_slots);
   a.l2 = reinterpret_cast<float *>(wsb + o_l2);
+  a.ncb = spmm_column_blocks(K);
   a.cnt1 = reinterpret_cast<int *>(wsb + o_cnt);
-  a.cnt2 = a.cnt1 + plan->num_groups;
+  a.cnt2 = a.cnt1 + plan->num_groups * a.ncb;
   if (plan->num_groups + plan->num_split > 0)
-    GNN_CUDA_TRY(cudaMemsetAsync(a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split), st));
+    GNN_CUDA_TRY(cudaMemsetAsync(
+        a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split) * a.ncb, st));
   a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
