@@ -284,7 +284,7 @@ __device__ __forceinline__ float ld_relaxed_gpu(const float *p) {
 
 // Called by a whole warp right after it stored partial j of split row s for
 // the column block [cbase, cbase+kb).
-__device__ __noinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t j, int64_t cbase,
+__device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64_t j, int64_t cbase,
                                           int kb) {
   const int lane = (int)lane_id();
   const int64_t r = a.split_rows[s];
