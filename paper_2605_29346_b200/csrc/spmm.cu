@@ -54,7 +54,6 @@ struct SpmmArgs {
   int warp_smem;             // bytes of shared memory per warp
 };
 
-constexpr int64_t kMaxEdgesPerWarp = 2048;
 
 template <int VW>
 struct VecT;
@@ -158,29 +157,29 @@ __device__ __forceinline__ typename VecT<VW>::T gather(const char *xb, int32_t c
   return VecT<VW>::ld(reinterpret_cast<const float *>(xb + (uint64_t)(uint32_t)c * ldxb));
 }
 
-// acc[v] = sum over this group's edges of w_e * X[c_e, cols of v]; chunk-local
-// edge indices [is, ie); group g takes is+g, is+g+NG, ...  Summation order is
-// fixed by (G, U), hence deterministic.
+// acc[v] += sum over this group's edges of w_e * X[c_e, cols of v] for the
+// buffer-local edge range [is, ie); group g takes is+g, is+g+NG, ...  Full
+// blocks of U edges per group run unpredicated; the remainder is one
+// predicated block, so a piece costs a single gather latency.  The order is
+// fixed by (G, U, piece bounds): deterministic.
 template <int G, int VPL, int VW, bool HAS_VALS>
-__device__ __forceinline__ void seg_sum(const SpmmArgs &a, const LaneCols<G, VPL, VW> &lc,
-                                        const int32_t *scol, const void *sval, int stage,
-                                        int64_t e0, int is, int ie,
-                                        typename VecT<VW>::T (&acc)[VPL]) {
+__device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols<G, VPL, VW> &lc,
+                                               const int32_t *scol, const void *sval, int stage,
+                                               int64_t ebase, int is, int ie,
+                                               typename VecT<VW>::T (&acc)[VPL]) {
   using V = VecT<VW>;
   constexpr int NG = 32 / G;
   constexpr int U = (VPL * VW >= 8) ? 4 : 8;
   const int g = (int)lane_id() / G;
   const uint32_t ldxb = (uint32_t)a.ldx * 4u;
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
   auto weight = [&](int i, int v) -> float {
     if (stage == STAGE_VALS) return static_cast<const float *>(sval)[i];
     const int64_t vi =
-        stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[i] : e0 + i;
+        stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[i] : ebase + i;
     return __ldg(a.vals + vi * a.heads + lc.head[v]);
   };
   int i = is + g;
-  for (; i + (U - 1) * NG < ie; i += NG * U) {  // full blocks: no bounds predicates
+  for (; i + (U - 1) * NG < ie; i += NG * U) {
     int32_t c[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) c[u] = scol[i + u * NG];
@@ -206,17 +205,34 @@ __device__ __forceinline__ void seg_sum(const SpmmArgs &a, const LaneCols<G, VPL
         for (int v = 0; v < VPL; ++v) acc[v] = V::add(acc[v], x[u][v]);
     }
   }
-  for (; i < ie; i += NG) {  // tail: < U edges per group
-    const int32_t c = scol[i];
+  if (i < ie) {  // one predicated block: < U edges left for this group
+    int32_t c[U];
+    bool ok[U];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      typename V::T x = gather<VW>(lc.xb[v], c, ldxb);
-      if constexpr (HAS_VALS)
-        acc[v] = V::fma(weight(i, v), x, acc[v]);
-      else
-        acc[v] = V::add(acc[v], x);
+    for (int u = 0; u < U; ++u) {
+      ok[u] = i + u * NG < ie;
+      c[u] = ok[u] ? scol[i + u * NG] : 0;
     }
+    typename V::T x[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather<VW>(lc.xb[v], c[u], ldxb) : V::zero();
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        if constexpr (HAS_VALS)
+          acc[v] = V::fma(ok[u] ? weight(i + u * NG, v) : 0.f, x[u][v], acc[v]);
+        else
+          acc[v] = V::add(acc[v], x[u][v]);
+      }
   }
+}
+
+template <int G, int VPL, int VW>
+__device__ __forceinline__ void group_reduce(typename VecT<VW>::T (&acc)[VPL]) {
+  using V = VecT<VW>;
 #pragma unroll
   for (int o = G; o < 32; o <<= 1)
 #pragma unroll
@@ -327,8 +343,17 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
   }
 }
 
+// ------------------------------------------------------------- main kernel
+// Persistent streaming: warp w owns the contiguous edge range [w*P, (w+1)*P)
+// (P ~ nnz / resident warps) and streams it through a two-stage shared-memory
+// ring of kSub-edge sub-chunks filled by 1-D bulk async copies (the TMA
+// engine): column ids (+ edge values or edge ids).  Row accumulators carry
+// across sub-chunk boundaries in registers; only rows crossing the warp's
+// range boundaries produce partials (split rows, finished by split_arrive).
+constexpr int kSub = 256;
+
 template <int G, int VPL, int VW, bool HAS_VALS>
-__global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
+__global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
   extern __shared__ __align__(16) uint8_t spmm_smem[];
@@ -336,84 +361,107 @@ __global__ void __launch_bounds__(256) spmm_main_kernel(SpmmArgs a) {
   const int lane = (int)lane_id();
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= a.nwarps) return;
+  const int stage = a.stage;
   uint8_t *wbase = spmm_smem + (size_t)warp * a.warp_smem;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);
-  int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);
-  void *sval = scol + a.P;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);           // [2]
+  int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);       // [2][kSub]
+  int32_t *sval = scol + 2 * kSub;                               // [2][kSub] (vals or eid bits)
   const int64_t cbase = (int64_t)blockIdx.y * KB;
   const int64_t e0 = w * a.P;
   const int64_t e1 = min(e0 + a.P, a.nnz);
-  const int n = (int)(e1 - e0);
-  const int stage = a.stage;
+  const int nsub = (int)ceil_div(e1 - e0, kSub);
 
-  // ---- stage this chunk's column ids (+ edge values / ids) into shared memory
-  const int nbulk = a.bulk_ok ? (n & ~3) : 0;  // elements moved by the bulk copy (16B multiple)
   if (lane == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   __syncwarp();
-  if (lane == 0) {
-    const uint32_t bytes = (uint32_t)nbulk * 4u;
-    mbar_arrive_expect_tx(bar, stage != STAGE_NONE ? 2u * bytes : bytes);
-    if (bytes) {
-      bulk_g2s(scol, a.cols + e0, bytes, bar);
-      if (stage == STAGE_VALS) bulk_g2s(sval, a.vals + e0, bytes, bar);
-      if (stage == STAGE_EID) bulk_g2s(sval, a.eid + e0, bytes, bar);
+  auto issue = [&](int sc) {
+    const int b = sc & 1;
+    const int64_t s0 = e0 + (int64_t)sc * kSub;
+    const int n = (int)min((int64_t)kSub, e1 - s0);
+    const int nbulk = a.bulk_ok ? (n & ~3) : 0;
+    int32_t *dc = scol + b * kSub;
+    int32_t *dv = sval + b * kSub;
+    for (int i = nbulk + lane; i < n; i += 32) {
+      dc[i] = a.cols[s0 + i];
+      if (stage == STAGE_VALS) dv[i] = __float_as_int(a.vals[s0 + i]);
+      if (stage == STAGE_EID) dv[i] = a.eid[s0 + i];
     }
-  }
-  for (int i = nbulk + lane; i < n; i += 32) {
-    scol[i] = a.cols[e0 + i];
-    if (stage == STAGE_VALS) static_cast<float *>(sval)[i] = a.vals[e0 + i];
-    if (stage == STAGE_EID) static_cast<int32_t *>(sval)[i] = a.eid[e0 + i];
-  }
-  // ---- row bounds while the copy is in flight: 32 row ends per batched load
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)nbulk * 4u;
+      mbar_arrive_expect_tx(bar + b, stage != STAGE_NONE ? 2u * bytes : bytes);
+      if (bytes) {
+        bulk_g2s(dc, a.cols + s0, bytes, bar + b);
+        if (stage == STAGE_VALS) bulk_g2s(dv, a.vals + s0, bytes, bar + b);
+        if (stage == STAGE_EID) bulk_g2s(dv, a.eid + s0, bytes, bar + b);
+      }
+    }
+  };
+  issue(0);
+
+  // row bounds: 32 row ends per batched load
   int64_t r = a.chunk_row[w];
   int64_t rs = a.offsets[r];
   int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
   int bi = 0;
   int64_t re = shfl_i64(obuf, 0);
-  const int split_in = a.chunk_split[2 * w];
-  const int split_out = a.chunk_split[2 * w + 1];
-  mbar_wait(bar, 0);
-  __syncwarp();
-
-  typename V::T acc[VPL];
   const LaneCols<G, VPL, VW> lc(a, cbase);
-  if (rs < e0) {  // carry-in piece of a row owned by an earlier warp
-    const int64_t ee = min(re, e1);
-    seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, 0, (int)(ee - e0), acc);
-    store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+  typename V::T acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
+  bool done = false;
+
+  for (int sc = 0; sc < nsub && !done; ++sc) {
+    const int b = sc & 1;
+    const int64_t s0 = e0 + (int64_t)sc * kSub;
+    const int64_t s1 = min(s0 + kSub, e1);
+    if (sc + 1 < nsub) issue(sc + 1);
+    mbar_wait(bar + b, (uint32_t)((sc >> 1) & 1));
     __syncwarp();
-    split_arrive(a, split_in, w - rs / a.P, cbase, KB);
-    if (re >= e1) return;
-    ++r;
-    ++bi;
-    rs = re;
-    re = shfl_i64(obuf, bi);
-  }
-  while (rs < e1) {
-    if (re > rs) {
-      const int64_t ee = min(re, e1);
-      seg_sum<G, VPL, VW, HAS_VALS>(a, lc, scol, sval, stage, e0, (int)(rs - e0), (int)(ee - e0),
-                                    acc);
-      if (re <= e1) {
-        store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
-      } else {
-        store_row<G, VPL, VW>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
-        __syncwarp();
-        split_arrive(a, split_out, 0, cbase, KB);
-        return;
+    const int32_t *bc = scol + b * kSub;
+    const int32_t *bv = sval + b * kSub;
+    while (true) {
+      const int64_t lo = max(rs, s0), hi = min(re, s1);
+      if (hi > lo)
+        seg_accumulate<G, VPL, VW, HAS_VALS>(a, lc, bc, bv, stage, s0, (int)(lo - s0),
+                                             (int)(hi - s0), acc);
+      if (re > s1) break;  // row continues in the next sub-chunk (or the next warp)
+      if (re > rs) {       // a row ends here
+        group_reduce<G, VPL, VW>(acc);
+        if (rs < e0) {     // carry-in piece of a row owned by an earlier warp
+          store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+          split_arrive(a, a.chunk_split[2 * w], w - rs / a.P, cbase, KB);
+        } else {
+          store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
+        }
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
       }
+      ++r;
+      rs = re;
+      if (rs >= e1 || r >= a.R) {
+        done = true;
+        break;
+      }
+      if (++bi == 32) {
+        obuf = a.offsets[min(r + 1 + lane, a.R)];
+        bi = 0;
+      }
+      re = shfl_i64(obuf, bi);
     }
-    ++r;
-    if (r >= a.R) break;
-    rs = re;
-    if (++bi == 32) {
-      obuf = a.offsets[min(r + 1 + lane, a.R)];
-      bi = 0;
+    __syncwarp();  // buffer b fully consumed before issue(sc + 2) refills it
+  }
+  if (!done && re > e1) {  // the range ends inside row r
+    group_reduce<G, VPL, VW>(acc);
+    if (rs < e0) {         // whole range inside one row: a carry-in piece
+      store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+      split_arrive(a, a.chunk_split[2 * w], w - rs / a.P, cbase, KB);
+    } else {               // trailing piece of a row this warp owns
+      store_row<G, VPL, VW>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
+      split_arrive(a, a.chunk_split[2 * w + 1], 0, cbase, KB);
     }
-    re = shfl_i64(obuf, bi);
   }
 }
 
@@ -485,7 +533,7 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
   // unified L1/shared array to L1 so hot feature rows stay cached.
   auto kern = has_vals ? spmm_main_kernel<G, VPL, VW, true> : spmm_main_kernel<G, VPL, VW, false>;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm_kb = (int)((smem * 8 + 1023) / 1024);  // up to 8 resident CTAs
+  const int per_sm_kb = (int)((smem * 3 + 1023) / 1024);  // 3 resident CTAs (persistent grid)
   const int carve = per_sm_kb * 100 / 228 + 1;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     carve > 100 ? 100 : carve));
@@ -539,7 +587,7 @@ size_t gnn_spmm_plan_workspace(int64_t num_rows) {
 
 int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_spmm_plan_t *plan,
                         void *ws, size_t ws_bytes, gnn_stream_t stream) {
-  if (!A || !plan || !buf || P <= 0 || P > kMaxEdgesPerWarp || P % 4 != 0 || A->num_rows < 0 ||
+  if (!A || !plan || !buf || P <= 0 || P % 4 != 0 || A->num_rows < 0 ||
       !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 30))
@@ -621,7 +669,7 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->eid && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
   if (heads > 1 && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->edges_per_warp > kMaxEdgesPerWarp ||
+  if (plan->edges_per_warp <= 0 || plan->edges_per_warp % 4 != 0 ||
       plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   gnn_epilogue_t e{};
@@ -669,7 +717,7 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
-  a.warp_smem = (int)(16 + a.P * 4 * (a.stage != STAGE_NONE ? 2 : 1));
+  a.warp_smem = (int)(16 + 2 * kSub * 4 * (a.stage != STAGE_NONE ? 2 : 1));
 
   if (a.nwarps > 0) {
     const bool hv = A->vals != nullptr;

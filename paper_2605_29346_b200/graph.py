@@ -64,12 +64,13 @@ def _readonly(a: np.ndarray) -> np.ndarray:
 
 
 def _default_edges_per_warp(nnz: int, sms: int) -> int:
-    """Chunk length of the SpMM schedule: long chunks amortise per-warp setup,
-    but there must be enough warps to fill every SM several times."""
-    p = 1024
-    while p > 64 and nnz // p < sms * 64:
-        p //= 2
-    return p
+    """Edge range per warp of the persistent SpMM: one contiguous range per
+    resident warp (3 CTAs x 8 warps per SM), a multiple of 4 edges (16-byte
+    bulk copies), at least one 256-edge sub-chunk."""
+    warps = sms * 24
+    p = -(-nnz // warps)
+    p = (p + 3) // 4 * 4
+    return max(p, 256)
 
 
 class SparseOperand:
