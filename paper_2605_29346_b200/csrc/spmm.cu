@@ -18,6 +18,9 @@
 //     empty rows get epilogue(0) from a list — both lists come from the
 //     per-graph plan, so a call never synchronises with the host.
 // Summation order is fixed, so results are deterministic run to run.
+#include <cuda.h>  // CUtensorMap (encode entry point fetched through the runtime)
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gnn {
@@ -465,6 +468,236 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
   }
 }
 
+// ------------------------------------------------------ TMA gather kernel
+// Blackwell-native SpMM: the feature rows X[col_e, cbase:cbase+KB] of every
+// edge are fetched by the TMA engine with cp.async.bulk.tensor.2d
+// .tile::gather4 (4 indexed rows per instruction) into a per-warp 3-stage
+// shared-memory ring, so no gather latency sits on a register dependency
+// chain.  Each warp owns a contiguous edge range (persistent, 8 warps/SM,
+// one CTA per SM); S = 8 KB/(4*KB) edges per stage; the S/4 issuing lanes
+// prefetch their 4 column ids (and edge values) one stage ahead.  The
+// consumers sum rows from shared memory with 128-bit LDS; row accumulators
+// carry across stages; range-boundary rows go through split_arrive.  Every
+// issued stage is consumed before the warp exits (a warp only finishes early
+// inside its last stage), so no TMA write can outlive the CTA.
+constexpr int kTmaStageBytes = 8192;
+constexpr int kTmaStages = 3;
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int c0, int4 rows,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w), "r"(bar)
+      : "memory");
+}
+
+template <int KB, bool HAS_VALS>
+__global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                          SpmmArgs a) {
+  constexpr int G = KB >= 128 ? 32 : KB / 4;   // lanes per row
+  constexpr int VPL = KB == 256 ? 2 : 1;       // float4 per lane
+  constexpr int NG = 32 / G;
+  constexpr int S = kTmaStageBytes / (KB * 4); // edges per stage
+  constexpr int NI = S / 4;                    // issuing lanes (one gather4 each)
+  constexpr int U = (S / NG) >= 8 ? 8 : (S / NG);
+  using V = VecT<4>;
+  extern __shared__ __align__(128) uint8_t tma_smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = (int)lane_id();
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  constexpr int kWarpBytes = kTmaStages * kTmaStageBytes + kTmaStages * S * 4 + 64;
+  uint8_t *wb = tma_smem + (size_t)warp * kWarpBytes;
+  float *sdata = reinterpret_cast<float *>(wb);                                // [3][S][KB]
+  float *svals = reinterpret_cast<float *>(wb + kTmaStages * kTmaStageBytes);  // [3][S]
+  uint64_t *bar =
+      reinterpret_cast<uint64_t *>(wb + kTmaStages * kTmaStageBytes + kTmaStages * S * 4);
+  const int64_t cbase = (int64_t)blockIdx.y * KB;
+  const int64_t e0 = w * a.P;
+  const int64_t e1 = min(e0 + a.P, a.nnz);
+  const int nsub = (int)ceil_div(e1 - e0, S);
+
+  if (lane == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(bar + i, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // lane l < NI owns edges [4l, 4l+4) of every stage
+  auto load_idx = [&](int sc, int4 &rows, float4 &vv) {
+    rows = make_int4(0, 0, 0, 0);
+    vv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sc >= nsub || lane >= NI) return;
+    const int64_t e = e0 + (int64_t)sc * S + 4 * lane;
+    if (e + 4 <= e1) {
+      rows = __ldg(reinterpret_cast<const int4 *>(a.cols + e));
+      if (HAS_VALS) vv = __ldg(reinterpret_cast<const float4 *>(a.vals + e));
+    } else if (e < e1) {
+      int t[4] = {0, 0, 0, 0};
+      float f[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = 0; k < 4; ++k)
+        if (e + k < e1) {
+          t[k] = a.cols[e + k];
+          if (HAS_VALS) f[k] = a.vals[e + k];
+        }
+      rows = make_int4(t[0], t[1], t[2], t[3]);
+      vv = make_float4(f[0], f[1], f[2], f[3]);
+    }
+  };
+  auto issue = [&](int sc, int4 rows, float4 vv) {
+    if (sc >= nsub) return;
+    const int st = sc % kTmaStages;
+    const int n = (int)min((int64_t)S, e1 - (e0 + (int64_t)sc * S));
+    const int ng4 = (n + 3) >> 2;
+    if (lane == 0) mbar_arrive_expect_tx(bar + st, (uint32_t)(ng4 * 4 * KB * 4));
+    __syncwarp();
+    if (lane < ng4) {
+      if (HAS_VALS) *reinterpret_cast<float4 *>(svals + st * S + 4 * lane) = vv;
+      tma_gather4(smem_u32(sdata + (size_t)st * S * KB + 4 * lane * KB), &tmX, (int)cbase, rows,
+                  smem_u32(bar + st));
+    }
+  };
+
+  int4 ri;
+  float4 vi;
+  load_idx(0, ri, vi);
+  issue(0, ri, vi);
+  load_idx(1, ri, vi);
+  issue(1, ri, vi);
+  load_idx(2, ri, vi);
+
+  int64_t r = a.chunk_row[w];
+  int64_t rs = a.offsets[r];
+  int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
+  int bi = 0;
+  int64_t re = shfl_i64(obuf, 0);
+  const int g = lane / G, gl = lane % G;
+  typename V::T acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
+  bool done = false;
+
+  for (int sc = 0; sc < nsub && !done; ++sc) {
+    issue(sc + 2, ri, vi);  // stage (sc+2)%3 was consumed in iteration sc-1
+    load_idx(sc + 3, ri, vi);
+    const int st = sc % kTmaStages;
+    const int64_t s0 = e0 + (int64_t)sc * S;
+    const int64_t s1 = min(s0 + S, e1);
+    mbar_wait(bar + st, (uint32_t)((sc / kTmaStages) & 1));
+    const float *bd = sdata + (size_t)st * S * KB + gl * 4;
+    const float *bv = svals + st * S;
+    while (true) {
+      const int lo = (int)(max(rs, s0) - s0), hi = (int)(min(re, s1) - s0);
+      int i = lo + g;  // group g takes lo+g, lo+g+NG, ...
+      for (; i + (U - 1) * NG < hi; i += NG * U) {
+        float4 x[U][VPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            x[u][v] = *reinterpret_cast<const float4 *>(bd + (i + u * NG) * KB + v * 128);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            if constexpr (HAS_VALS)
+              acc[v] = V::fma(bv[i + u * NG], x[u][v], acc[v]);
+            else
+              acc[v] = V::add(acc[v], x[u][v]);
+          }
+      }
+      for (; i < hi; i += NG) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          float4 x = *reinterpret_cast<const float4 *>(bd + i * KB + v * 128);
+          if constexpr (HAS_VALS)
+            acc[v] = V::fma(bv[i], x, acc[v]);
+          else
+            acc[v] = V::add(acc[v], x);
+        }
+      }
+      if (re > s1) break;
+      if (re > rs) {
+        group_reduce<G, VPL, 4>(acc);
+        if (rs < e0) {
+          store_row<G, VPL, 4>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+          split_arrive(a, a.chunk_split[2 * w], w - rs / a.P, cbase, KB);
+        } else {
+          store_row<G, VPL, 4>(a, a.Y + r * a.ldy, cbase, acc, true, r);
+        }
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
+      }
+      ++r;
+      rs = re;
+      if (rs >= e1 || r >= a.R) {
+        done = true;
+        break;
+      }
+      if (++bi == 32) {
+        obuf = a.offsets[min(r + 1 + lane, a.R)];
+        bi = 0;
+      }
+      re = shfl_i64(obuf, bi);
+    }
+    __syncwarp();  // stage st consumed before issue() refills it
+  }
+  if (!done && re > e1) {
+    group_reduce<G, VPL, 4>(acc);
+    if (rs < e0) {
+      store_row<G, VPL, 4>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
+      split_arrive(a, a.chunk_split[2 * w], w - rs / a.P, cbase, KB);
+    } else {
+      store_row<G, VPL, 4>(a, a.slots + (w * 2 + 1) * a.K, cbase, acc, false, r);
+      split_arrive(a, a.chunk_split[2 * w + 1], 0, cbase, KB);
+    }
+  }
+}
+
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                      const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                      const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+TensorMapEncodeFn get_encode_fn() {
+  static TensorMapEncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<TensorMapEncodeFn>(p);
+  }
+  return fn;
+}
+
+// Row-gather tensor map over X[rows, K] (row stride ldx floats), box {KB, 1}.
+bool make_gather_map(CUtensorMap *tm, const float *X, int64_t rows, int64_t K, int64_t ldx, int KB) {
+  TensorMapEncodeFn enc = get_encode_fn();
+  if (!enc || rows <= 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
+  cuuint32_t box[2] = {(cuuint32_t)KB, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int KB>
+int launch_tma(const SpmmArgs &a, bool has_vals, const CUtensorMap &tm, cudaStream_t st) {
+  constexpr int S = kTmaStageBytes / (KB * 4);
+  const size_t smem = (size_t)8 * (kTmaStages * kTmaStageBytes + kTmaStages * S * 4 + 64);
+  dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
+  auto kern = has_vals ? spmm_tma_kernel<KB, true> : spmm_tma_kernel<KB, false>;
+  GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, 256, smem, st>>>(tm, a);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
 __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                        int64_t nrows) {
   const int64_t total = nrows * a.K;
@@ -728,7 +961,20 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
     if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
     int s;
-    if (vec4) {
+    const bool tma_ok = vec4 && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
+                        a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
+                        getenv("GNN_SPMM_NO_TMA") == nullptr;
+    CUtensorMap tm;
+    const int kb = K <= 16 ? 16 : K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+    if (tma_ok && make_gather_map(&tm, X, A->num_cols, K, ldx, kb)) {
+      switch (kb) {
+        case 16: s = launch_tma<16>(a, hv, tm, st); break;
+        case 32: s = launch_tma<32>(a, hv, tm, st); break;
+        case 64: s = launch_tma<64>(a, hv, tm, st); break;
+        case 128: s = launch_tma<128>(a, hv, tm, st); break;
+        default: s = launch_tma<256>(a, hv, tm, st); break;
+      }
+    } else if (vec4) {
       if (K <= 16)
         s = launch_main<4, 1, 4>(a, hv, st);
       else if (K <= 32)

@@ -65,9 +65,10 @@ def _readonly(a: np.ndarray) -> np.ndarray:
 
 def _default_edges_per_warp(nnz: int, sms: int) -> int:
     """Edge range per warp of the persistent SpMM: one contiguous range per
-    resident warp (3 CTAs x 8 warps per SM), a multiple of 4 edges (16-byte
-    bulk copies), at least one 256-edge sub-chunk."""
-    warps = sms * 24
+    resident warp (the TMA-gather kernel runs one 8-warp CTA per SM), a
+    multiple of 4 edges (16-byte aligned index/value vectors), at least one
+    256-edge sub-chunk."""
+    warps = sms * 8
     p = -(-nnz // warps)
     p = (p + 3) // 4 * 4
     return max(p, 256)
