@@ -492,6 +492,12 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm,
       : "memory");
 }
 
+template <int KB>
+constexpr int tma_warp_bytes() {
+  return (kTmaStages * kTmaStageBytes + kTmaStages * (kTmaStageBytes / (KB * 4)) * 4 + 64 + 1023) /
+         1024 * 1024;
+}
+
 template <int KB, bool HAS_VALS>
 __global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant__ CUtensorMap tmX,
                                                           SpmmArgs a) {
@@ -502,12 +508,12 @@ __global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant_
   constexpr int NI = S / 4;                    // issuing lanes (one gather4 each)
   constexpr int U = (S / NG) >= 8 ? 8 : (S / NG);
   using V = VecT<4>;
-  extern __shared__ __align__(128) uint8_t tma_smem[];
+  extern __shared__ __align__(1024) uint8_t tma_smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= a.nwarps) return;
-  constexpr int kWarpBytes = kTmaStages * kTmaStageBytes + kTmaStages * S * 4 + 64;
+  constexpr int kWarpBytes = tma_warp_bytes<KB>();  // 1 KB aligned: TMA smem destinations
   uint8_t *wb = tma_smem + (size_t)warp * kWarpBytes;
   float *sdata = reinterpret_cast<float *>(wb);                                // [3][S][KB]
   float *svals = reinterpret_cast<float *>(wb + kTmaStages * kTmaStageBytes);  // [3][S]
@@ -689,7 +695,8 @@ bool make_gather_map(CUtensorMap *tm, const float *X, int64_t rows, int64_t K, i
 template <int KB>
 int launch_tma(const SpmmArgs &a, bool has_vals, const CUtensorMap &tm, cudaStream_t st) {
   constexpr int S = kTmaStageBytes / (KB * 4);
-  const size_t smem = (size_t)8 * (kTmaStages * kTmaStageBytes + kTmaStages * S * 4 + 64);
+  const size_t smem = (size_t)8 * tma_warp_bytes<KB>();
+  (void)S;
   dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
   auto kern = has_vals ? spmm_tma_kernel<KB, true> : spmm_tma_kernel<KB, false>;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
