@@ -172,7 +172,14 @@ __global__ void colsum_final_kernel(int64_t nb, int64_t N, const float *__restri
 
 }  // namespace
 
-// Exposed for the tcgen05 path's fallbacks.
+// tcgen05 tensor-core path (gemm_tc.cu)
+bool gemm_tc_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int trans_a);
+size_t gemm_tc_workspace(int64_t N, int64_t K);
+int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+            int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias, int relu, void *ws,
+            size_t ws_bytes, cudaStream_t st);
+
+// SIMT fallback (transposed A, unaligned strides, small M).
 int gemm_simt(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
               const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
               int relu, void *ws, size_t ws_bytes, cudaStream_t st) {
@@ -246,8 +253,9 @@ int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, vo
 }
 
 size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a) {
-  (void)trans_a;
-  return gemm_simt_workspace(M, N, Kd);
+  size_t a = gemm_simt_workspace(M, N, Kd);
+  size_t b = trans_a ? 0 : gemm_tc_workspace(N, Kd);
+  return a > b ? a : b;
 }
 
 int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
@@ -259,6 +267,8 @@ int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int 
     return GNN_ERR_INVALID_ARGUMENT;
   if (M == 0 || N == 0) return GNN_OK;
   cudaStream_t st = as_stream(stream);
+  if (gemm_tc_supported(M, N, Kd, A, lda, trans_a))
+    return gemm_tc(M, N, Kd, A, lda, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes, st);
   return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
                    st);
 }

@@ -1,0 +1,387 @@
+// fp32-accurate dense transform C[M,N] = A[M,K] . B[K,N] (+bias)(relu) on the
+// 5th-generation tensor cores (tcgen05, kind::tf32) with the 3xTF32 split
+//   A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi,   x_hi = x & 0xffffe000, x_lo = x - x_hi
+// (x_hi is exactly representable in TF32; the dropped A_lo.B_lo term is
+// ~2^-22 relative), accumulated in fp32 in tensor memory.  This is the only
+// dense contraction on the path: X.W with X [V,K] fp32,
+// W [K,N<=256] — HBM-bound (arithmetic intensity ~8 flop/B for N=16), so the
+// design goal is to stream A at HBM speed.
+//
+// One persistent CTA per SM, 12 warps, warp-specialised:
+//   warp 0      TMA producer: A tile [128 x 32] fp32 (SWIZZLE_128B) + B_hi/B_lo
+//               tiles [N x 32] per k-block into a 5-stage smem ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, K=8)
+//   warps 4-7   split warps: A -> A_hi (in place) + A_lo (second buffer)
+//   warps 8-11  epilogue warpgroup: tcgen05.ld (32x32b) -> bias/relu -> global
+// TMEM holds two accumulators so the epilogue of tile i overlaps tile i+1.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace gnn {
+namespace {
+
+constexpr int kTcM = 128;
+constexpr int kTcBK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
+// smem ring depth: 192 KB of stages whatever the B tile width
+template <int NPAD>
+constexpr int tc_stages() {
+  return NPAD <= 32 ? 5 : (NPAD <= 64 ? 4 : 3);
+}
+constexpr int kTcThreads = 384;
+
+struct TcArgs {
+  int64_t M, N, K;
+  int Npad;
+  int nkb;
+  int64_t mtiles;
+  float *C;
+  int64_t ldc;
+  const float *bias;
+  int relu;
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tm, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// K-major, SWIZZLE_128B operand descriptor (sm_100 "version 1"): rows of 128 B,
+// 8-row core groups 1024 B apart (SBO); LBO unused for swizzled K-major.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+template <int NPAD>
+constexpr size_t tc_smem_bytes() {
+  return (size_t)tc_stages<NPAD>() * (2 * kTcM * kTcBK + 2 * NPAD * kTcBK) * 4 + 1024 + 1024;
+}
+
+template <int NPAD>
+__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                const __grid_constant__ CUtensorMap tmBhi,
+                                                                const __grid_constant__ CUtensorMap tmBlo,
+                                                                TcArgs p) {
+  constexpr int kTcStages = tc_stages<NPAD>();
+  extern __shared__ __align__(1024) uint8_t tc_raw[];
+  // carve 1024-aligned regions
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr size_t kA = (size_t)kTcM * kTcBK * 4;
+  constexpr size_t kB = (size_t)NPAD * kTcBK * 4;
+  float *sa = reinterpret_cast<float *>(base);
+  float *salo = reinterpret_cast<float *>(base + kTcStages * kA);
+  float *sbhi = reinterpret_cast<float *>(base + 2 * kTcStages * kA);
+  float *sblo = reinterpret_cast<float *>(base + 2 * kTcStages * kA + kTcStages * kB);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTcStages * kA + 2 * kTcStages * kB);
+  uint64_t *full = bars, *split = bars + kTcStages, *empty = bars + 2 * kTcStages;
+  uint64_t *acc_full = bars + 3 * kTcStages, *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = (int)lane_id();
+  constexpr uint32_t kTxBytes = (uint32_t)(kA + 2 * kB);
+  constexpr int kTmemCols = (2 * NPAD) <= 32 ? 32 : (2 * NPAD) <= 64 ? 64 : (2 * NPAD) <= 128 ? 128 : (2 * NPAD) <= 256 ? 256 : 512;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(split + s, 4);  // one elected arrival per split warp
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 4);  // one per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // idesc: D f32, A/B tf32, K-major both, N, M=128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NPAD >> 3) << 17) |
+                         ((uint32_t)(kTcM >> 4) << 24);
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+        const int m0 = (int)(t * kTcM);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_arrive_expect_tx(full + s, kTxBytes);
+          tma_load_2d(smem_u32(sa + (size_t)s * kTcM * kTcBK), &tmA, kb * kTcBK, m0, smem_u32(full + s));
+          tma_load_2d(smem_u32(sbhi + (size_t)s * NPAD * kTcBK), &tmBhi, kb * kTcBK, 0, smem_u32(full + s));
+          tma_load_2d(smem_u32(sblo + (size_t)s * NPAD * kTcBK), &tmBlo, kb * kTcBK, 0, smem_u32(full + s));
+          if (++s == kTcStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+        mbar_wait(acc_empty + ab, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ab * NPAD);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(split + s, ph);
+          tc_fence_after();
+          const uint64_t ah = sw128_desc(smem_u32(sa + (size_t)s * kTcM * kTcBK));
+          const uint64_t al = sw128_desc(smem_u32(salo + (size_t)s * kTcM * kTcBK));
+          const uint64_t bh = sw128_desc(smem_u32(sbhi + (size_t)s * NPAD * kTcBK));
+          const uint64_t bl = sw128_desc(smem_u32(sblo + (size_t)s * NPAD * kTcBK));
+#pragma unroll
+          for (int k = 0; k < kTcBK / 8; ++k) {  // K=8 tf32 = 32 bytes per MMA: +2 in the >>4 address field
+            const uint64_t o = (uint64_t)(k * 2);
+            tc_mma_tf32(d, ah + o, bh + o, idesc, (kb | k) != 0);
+            tc_mma_tf32(d, ah + o, bl + o, idesc, 1);
+            tc_mma_tf32(d, al + o, bh + o, idesc, 1);
+          }
+          tc_commit(empty + s);  // smem stage free once these MMAs retire
+          if (kb == p.nkb - 1) tc_commit(acc_full + ab);
+          if (++s == kTcStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- split warps: A -> (A_hi in place, A_lo)
+    const int tid = threadIdx.x - 128;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+      for (int kb = 0; kb < p.nkb; ++kb) {
+        mbar_wait(full + s, ph);
+        float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
+        float4 *l4 = reinterpret_cast<float4 *>(salo + (size_t)s * kTcM * kTcBK);
+#pragma unroll 4
+        for (int i = tid; i < kTcM * kTcBK / 4; i += 128) {
+          float4 x = a4[i];
+          float4 h;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+          a4[i] = h;
+          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split + s);
+        if (++s == kTcStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- epilogue warpgroup: TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+      mbar_wait(acc_full + ab, aph);
+      tc_fence_after();
+      const int64_t row = t * kTcM + q * 32 + lane;
+      float *crow = p.C + row * p.ldc;
+      for (int c0 = 0; c0 < NPAD; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NPAD + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t c = c0 + j;
+            if (c < p.N) {
+              float y = __uint_as_float(v[j]);
+              if (p.bias) y += p.bias[c];
+              if (p.relu) y = fmaxf(y, 0.f);
+              crow[c] = y;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + ab);
+      if (++ab == 2) {
+        ab = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+}
+
+// B [K,N] row-major (ldb) or B^T [N,K] (trans_b) -> Bt_hi / Bt_lo [Npad, Kpad] K-major, zero padded.
+__global__ void split_b_kernel(const float *__restrict__ B, int64_t ldb, int trans_b, int64_t N,
+                               int64_t K, int Npad, int64_t Kpad, float *bhi, float *blo) {
+  const int64_t total = (int64_t)Npad * Kpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / Kpad, k = i % Kpad;
+    float x = 0.f;
+    if (n < N && k < K) x = trans_b ? B[n * ldb + k] : B[k * ldb + n];
+    const float h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    bhi[i] = h;
+    blo[i] = x - h;
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                             const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                             const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  }
+  return fn;
+}
+bool map_2d_sw128(CUtensorMap *tm, const float *base, int64_t inner, int64_t outer, int64_t ld,
+                  int box_outer) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NPAD>
+int launch_tc(const CUtensorMap &ta, const CUtensorMap &tbh, const CUtensorMap &tbl,
+              const TcArgs &p, cudaStream_t st) {
+  const size_t smem = tc_smem_bytes<NPAD>();
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<NPAD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = p.mtiles < sm_count() ? p.mtiles : sm_count();
+  gemm_tc_kernel<NPAD><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tbh, tbl, p);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // namespace
+
+// Tensor-core path applicability: A row-major with a 16-byte-multiple row
+// stride (TMA), 16-byte aligned base, N <= 128.
+bool gemm_tc_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int trans_a) {
+  return !trans_a && M >= kTcM && N >= 1 && N <= 128 && K >= 1 && (lda * 4) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && encode_fn() != nullptr &&
+         getenv("GNN_GEMM_NO_TC") == nullptr;
+}
+
+static int tc_npad(int64_t N) { return N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : 128; }
+
+size_t gemm_tc_workspace(int64_t N, int64_t K) {
+  const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
+  return sizeof(float) * (size_t)(2 * tc_npad(N) * kpad) + 512;
+}
+
+int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+            int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias, int relu, void *ws,
+            size_t ws_bytes, cudaStream_t st) {
+  const int npad = tc_npad(N);
+  const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
+  if (ws_bytes < gemm_tc_workspace(N, K)) return GNN_ERR_WORKSPACE;
+  float *bhi = static_cast<float *>(ws);
+  float *blo = bhi + (size_t)npad * kpad;
+  split_b_kernel<<<(unsigned)ceil_div((int64_t)npad * kpad, 256), 256, 0, st>>>(
+      B, ldb, trans_b, N, K, npad, kpad, bhi, blo);
+  GNN_LAUNCH_CHECK();
+  CUtensorMap ta, tbh, tbl;
+  if (!map_2d_sw128(&ta, A, K, M, lda, kTcM) || !map_2d_sw128(&tbh, bhi, kpad, npad, kpad, npad) ||
+      !map_2d_sw128(&tbl, blo, kpad, npad, kpad, npad))
+    return GNN_ERR_UNSUPPORTED;
+  TcArgs p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Npad = npad;
+  p.nkb = (int)(kpad / kTcBK);
+  p.mtiles = ceil_div(M, kTcM);
+  p.C = C;
+  p.ldc = ldc;
+  p.bias = bias;
+  p.relu = relu;
+  switch (npad) {
+    case 16: return launch_tc<16>(ta, tbh, tbl, p, st);
+    case 32: return launch_tc<32>(ta, tbh, tbl, p, st);
+    case 64: return launch_tc<64>(ta, tbh, tbl, p, st);
+    default: return launch_tc<128>(ta, tbh, tbl, p, st);
+  }
+}
+
+}  // namespace gnn

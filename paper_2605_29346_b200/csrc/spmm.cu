@@ -970,7 +970,7 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     int s;
     const bool tma_ok = vec4 && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
                         a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
-                        getenv("GNN_SPMM_NO_TMA") == nullptr;
+                        getenv("GNN_SPMM_TMA") != nullptr;
     CUtensorMap tm;
     const int kb = K <= 16 ? 16 : K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
     if (tma_ok && make_gather_map(&tm, X, A->num_cols, K, ldx, kb)) {

@@ -64,14 +64,15 @@ def _readonly(a: np.ndarray) -> np.ndarray:
 
 
 def _default_edges_per_warp(nnz: int, sms: int) -> int:
-    """Edge range per warp of the persistent SpMM: one contiguous range per
-    resident warp (the TMA-gather kernel runs one 8-warp CTA per SM), a
-    multiple of 4 edges (16-byte aligned index/value vectors), at least one
-    256-edge sub-chunk."""
-    warps = sms * 8
-    p = -(-nnz // warps)
-    p = (p + 3) // 4 * 4
-    return max(p, 256)
+    """Edge range per warp of the SpMM (a multiple of 4: 16-byte aligned index
+    vectors).  2048-edge ranges (measured best on Reddit-size graphs: long
+    enough to amortise row-bound loads and split-row arrivals, short enough for
+    ~56k warps of parallelism); smaller graphs shrink it so every SM still
+    gets several waves."""
+    p = 2048
+    while p > 256 and nnz // p < sms * 64:
+        p //= 2
+    return p
 
 
 class SparseOperand:

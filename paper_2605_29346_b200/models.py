@@ -144,7 +144,11 @@ class GCNTrainer:
         self.b2 = torch.zeros(classes, **f32)
         self.dW1, self.db1 = torch.empty_like(self.W1), torch.empty_like(self.b1)
         self.dW2, self.db2 = torch.empty_like(self.W2), torch.empty_like(self.b2)
-        self.X = torch.empty(V, in_feats, **f32)
+        # X keeps a 128-byte-multiple row stride so TMA can stream it into the
+        # tcgen05 GEMM (602 floats = 2408 B is not a 16 B multiple)
+        self.Fpad = -(-in_feats // 32) * 32
+        self._Xstore = torch.empty(V, self.Fpad, **f32)
+        self.X = self._Xstore[:, :in_feats]
         self.labels = torch.empty(V, dtype=torch.int64, device=dev)
         e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
         self.H1, self.Y1, self.P2 = e(hidden), e(hidden), e(hidden)

@@ -22,7 +22,7 @@ for K in [int(k) for k in (sys.argv[1:] or ["16", "32"])]:
     X = torch.rand(V, K, device="cuda")
     Y = torch.empty_like(X)
     for layout in ("csr", "csr_coalesced", "csc", "csc_coalesced"):
-        for P in (None,):
+        for P in [int(x) for x in os.environ.get('SWEEP_P', '512,1024,2048').split(',')]:
             call = SpmmCall(g.operand(layout), X, Y, flags=_lib.EPI_NORM if "csr" in layout else 0,
                             edges_per_warp=P)
             ts = []
@@ -37,4 +37,4 @@ for K in [int(k) for k in (sys.argv[1:] or ["16", "32"])]:
                 b.synchronize()
                 ts.append(a.elapsed_time(b))
             res[f"K{K} {layout} P{P}"] = round(statistics.median(ts[2:]), 4)
-            print(f"K={K:3d} {layout:14s} P={str(P):5s}  {res[f'K{K} {layout} P{P}']:.4f} ms", flush=True)
+            print(f"K={K:3d} {layout:14s} P={P:5d}  {res[f'K{K} {layout} P{P}']:.4f} ms", flush=True)
