@@ -229,6 +229,17 @@ int gnn_softmax_xent(int64_t M, int64_t C, const float *Z, int64_t ldz, const in
                      float grad_scale, float *dZ, int64_t ldd, float *loss, void *ws,
                      size_t ws_bytes, gnn_stream_t stream);
 
+/* Fused output layer of the GCN/GIN trainers (one warp per row):
+ *   Z = P W + b (P [M,Din], W [Din,C] row-major, Din,C <= 64);
+ *   *loss = mean_r (logsumexp(Z[r]) - Z[r,y_r]);  dZ = (softmax(Z) - onehot(y)) / M;
+ *   dP = (dZ W^T) * 1/deg(r)  (deg from deg_offsets; NULL = no scaling);
+ *   dW = P^T dZ [Din,C];  db = colsum(dZ).   Deterministic (fixed-order reductions). */
+size_t gnn_gcn_head_workspace(int64_t M, int64_t Din, int64_t C);
+int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, const float *W,
+                 const float *b, const int64_t *labels, const int64_t *deg_offsets, float *dP,
+                 int64_t lddp, float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
+                 gnn_stream_t stream);
+
 /* Adam over a device table of parameters; the step counter lives on device
  * (read for bias correction, then incremented) so the update can sit inside
  * a captured CUDA graph. */

@@ -145,7 +145,15 @@ def gcn2_step(offsets, cols, t_offsets, t_cols, X, W1, b1, W2, b2, labels):
     db1 = dZ1.sum(axis=0)
     dH1 = spmm(t_offsets, t_cols, degree_norm(offsets, dZ1))
     dW1 = X.T @ dH1
-    return {"loss": loss, "logits": Z2, "W1": dW1, "b1": db1, "W2": dW2, "b2": db2}
+    # Appendix A.8 scale: the same contractions on absolute values (guards the
+    # cancellation in bias sums and weight gradients)
+    absd = {
+        "W1": np.abs(X).T @ spmm(t_offsets, t_cols, degree_norm(offsets, np.abs(dZ1))),
+        "b1": np.abs(dZ1).sum(axis=0),
+        "W2": np.abs(Y1).T @ spmm(t_offsets, t_cols, degree_norm(offsets, np.abs(dZ2))),
+        "b2": np.abs(dZ2).sum(axis=0),
+    }
+    return {"loss": loss, "logits": Z2, "W1": dW1, "b1": db1, "W2": dW2, "b2": db2, "abs": absd}
 
 
 def close(gpu, ref, ref_abs=None, rtol=1e-5):

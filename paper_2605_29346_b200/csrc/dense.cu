@@ -491,3 +491,185 @@ int gnn_adam_step(int nparams, const void *param_table, float lr, float beta1, f
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// Fused output layer (GCN/GIN trainers): one warp per row computes
+//   z = P[r] W + b;  loss += lse(z) - z[y];  dz = (softmax(z) - onehot(y)) / M
+//   dP[r] = (dz W^T) * rowscale(r)   (rowscale = 1/deg(r): the degree-norm of
+//                                     the next backward SpMM's INPUT)
+//   dW += P[r]^T dz;  db += dz       (register accumulators, fixed-order CTA reduction)
+// Replaces gemm + xent + colsum + 2 gemms + norm (~9 launches) with 2.
+namespace gnn {
+namespace {
+
+constexpr int kHeadWarps = 8;
+constexpr int kHeadRowsPerWarp = 64;
+
+// partials layout: float [nb][din*C + C] then double loss[nb] (8-byte aligned)
+inline int64_t head_float_slots(int64_t nb, int64_t din, int64_t C) {
+  return (nb * (din * C + C) + 1) / 2 * 2;
+}
+
+template <int DIN>
+__global__ void __launch_bounds__(256) gcn_head_kernel(
+    int64_t M, int din, int C, const float *__restrict__ P, int64_t ldp,
+    const float *__restrict__ W, const float *__restrict__ b, const int64_t *__restrict__ labels,
+    const int64_t *__restrict__ deg_offsets, float scale, float *dP, int64_t lddp,
+    float *partials, double *lpart) {
+  __shared__ float sW[DIN * 64];
+  __shared__ float sb[64];
+  __shared__ float stage[kHeadWarps][32];
+  __shared__ double lred[kHeadWarps];
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  for (int i = threadIdx.x; i < DIN * 64; i += blockDim.x) {
+    const int k = i / 64, c = i % 64;
+    sW[i] = (k < din && c < C) ? W[k * C + c] : 0.f;
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sb[i] = i < C ? b[i] : 0.f;
+  __syncthreads();
+  const bool v0 = lane < C, v1 = lane + 32 < C;
+  float aw0[DIN], aw1[DIN];
+#pragma unroll
+  for (int k = 0; k < DIN; ++k) aw0[k] = aw1[k] = 0.f;
+  float ab0 = 0.f, ab1 = 0.f;
+  double lsum = 0.0;
+  const int64_t r0 = ((int64_t)blockIdx.x * kHeadWarps + warp) * kHeadRowsPerWarp;
+  const int64_t r1 = min(M, r0 + kHeadRowsPerWarp);
+  for (int64_t r = r0; r < r1; ++r) {
+    const float pv = lane < din ? P[r * ldp + lane] : 0.f;
+    float z0 = sb[lane], z1 = sb[lane + 32];
+#pragma unroll
+    for (int k = 0; k < DIN; ++k) {
+      const float pk = __shfl_sync(kFull, pv, k);
+      z0 = fmaf(pk, sW[k * 64 + lane], z0);
+      z1 = fmaf(pk, sW[k * 64 + 32 + lane], z1);
+    }
+    float mx = fmaxf(v0 ? z0 : -INFINITY, v1 ? z1 : -INFINITY);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    float se = (v0 ? expf(z0 - mx) : 0.f) + (v1 ? expf(z1 - mx) : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
+    const float lse = mx + logf(se);
+    const int y = (int)labels[r];
+    const float zy = __shfl_sync(kFull, y < 32 ? z0 : z1, y & 31);
+    if (lane == 0) lsum += (double)(lse - zy);
+    const float d0 = v0 ? (expf(z0 - lse) - (lane == y ? 1.f : 0.f)) * scale : 0.f;
+    const float d1 = v1 ? (expf(z1 - lse) - (lane + 32 == y ? 1.f : 0.f)) * scale : 0.f;
+    ab0 += d0;
+    ab1 += d1;
+#pragma unroll
+    for (int k = 0; k < DIN; ++k) {
+      const float pk = __shfl_sync(kFull, pv, k);
+      aw0[k] = fmaf(pk, d0, aw0[k]);
+      aw1[k] = fmaf(pk, d1, aw1[k]);
+    }
+    // dP[k] = sum_c dz_c W[k][c]: lane k accumulates over the broadcast dz
+    float dp = 0.f;
+    const int kk = lane < DIN ? lane : 0;
+    for (int c = 0; c < C; ++c) {
+      const float dc = __shfl_sync(kFull, c < 32 ? d0 : d1, c & 31);
+      dp = fmaf(dc, sW[kk * 64 + c], dp);
+    }
+    if (lane < din) {
+      float rs = 1.f;
+      if (deg_offsets) {
+        const int64_t dg = deg_offsets[r + 1] - deg_offsets[r];
+        rs = dg > 0 ? 1.f / (float)dg : 0.f;
+      }
+      dP[r * lddp + lane] = dp * rs;
+    }
+  }
+  // CTA reduction in fixed warp order: rows k<din of dW (two column halves), then db
+  const int64_t NPF = (int64_t)din * C + C;
+  float *out = partials + (int64_t)blockIdx.x * NPF;
+#pragma unroll
+  for (int k = 0; k <= DIN; ++k) {
+    if (k < din || k == DIN) {
+      const int kr = k < din ? k : din;  // row index in the partial (din == the db row)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        stage[warp][lane] = k < DIN ? (half ? aw1[k] : aw0[k]) : (half ? ab1 : ab0);
+        __syncthreads();
+        if (warp == 0) {
+          float t = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < kHeadWarps; ++w2) t += stage[w2][lane];
+          const int c = lane + 32 * half;
+          if (c < C) out[(int64_t)kr * C + c] = t;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (lane == 0) lred[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < kHeadWarps; ++w2) t += lred[w2];
+    lpart[blockIdx.x] = t;
+  }
+}
+
+__global__ void gcn_head_reduce_kernel(int64_t nb, int din, int C, const float *__restrict__ partials,
+                                       const double *__restrict__ lpart, float *dW, float *db,
+                                       float *loss, float loss_scale) {
+  const int64_t NPF = (int64_t)din * C + C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= NPF;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < NPF) {
+      float t = 0.f;
+      for (int64_t b2 = 0; b2 < nb; ++b2) t += partials[b2 * NPF + i];
+      if (i < (int64_t)din * C)
+        dW[i] = t;
+      else
+        db[i - (int64_t)din * C] = t;
+    } else {
+      double t = 0.0;
+      for (int64_t b2 = 0; b2 < nb; ++b2) t += lpart[b2];
+      *loss = (float)(t * (double)loss_scale);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+size_t gnn_gcn_head_workspace(int64_t M, int64_t Din, int64_t C) {
+  const int64_t nb = ceil_div(M > 0 ? M : 1, (int64_t)kHeadWarps * kHeadRowsPerWarp);
+  return sizeof(float) * (size_t)head_float_slots(nb, Din, C) + sizeof(double) * (size_t)nb + 512;
+}
+
+int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, const float *W,
+                 const float *b, const int64_t *labels, const int64_t *deg_offsets, float *dP,
+                 int64_t lddp, float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
+                 gnn_stream_t stream) {
+  if (M <= 0 || Din <= 0 || Din > 64 || C <= 0 || C > 64 || !P || ldp < Din || !W || !b ||
+      !labels || !dP || lddp < Din || !dW || !db || !loss)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_gcn_head_workspace(M, Din, C)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int64_t nb = ceil_div(M, (int64_t)kHeadWarps * kHeadRowsPerWarp);
+  float *partials = static_cast<float *>(ws);
+  double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
+  const float scale = 1.0f / (float)M;
+#define GNN_HEAD(DN)                                                                            \
+  gcn_head_kernel<DN><<<(unsigned)nb, 256, 0, st>>>(M, (int)Din, (int)C, P, ldp, W, b, labels, \
+                                                    deg_offsets, scale, dP, lddp, partials, lpart)
+  if (Din <= 16)
+    GNN_HEAD(16);
+  else if (Din <= 32)
+    GNN_HEAD(32);
+  else
+    GNN_HEAD(64);
+#undef GNN_HEAD
+  GNN_LAUNCH_CHECK();
+  gcn_head_reduce_kernel<<<(unsigned)ceil_div(Din * C + C + 1, 256), 256, 0, st>>>(
+      nb, (int)Din, (int)C, partials, lpart, dW, db, loss, 1.0f / (float)M);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -131,3 +131,25 @@ class AdamCall:
                                           self.b1, self.b2, self.eps, self.wd,
                                           self.step.data_ptr(), _lib.stream_handle(self.dev)),
                    "adam")
+
+
+class HeadCall:
+    """Fused output layer: logits, mean cross-entropy, dP (degree-normed), dW, db."""
+
+    def __init__(self, P, W, b, labels, dP, dW, db, loss, deg_offsets=None):
+        self.lib = _lib.lib()
+        self.dev = P.device
+        self.M, self.Din = P.shape
+        self.C = W.shape[1]
+        self.P, self.W, self.b, self.labels, self.dP = P, W, b, labels, dP
+        self.dW, self.db, self.loss, self.deg = dW, db, loss, deg_offsets
+        self.ws = _lib.workspace(self.lib.gnn_gcn_head_workspace(self.M, self.Din, self.C),
+                                 self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_gcn_head(
+            self.M, self.Din, self.C, self.P.data_ptr(), self.P.stride(0), self.W.data_ptr(),
+            self.b.data_ptr(), self.labels.data_ptr(),
+            self.deg.data_ptr() if self.deg is not None else None, self.dP.data_ptr(),
+            self.dP.stride(0), self.dW.data_ptr(), self.db.data_ptr(), self.loss.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "gcn_head")

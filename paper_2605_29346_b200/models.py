@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .graph import CsrGraph
-from .kernels import AdamCall, GemmCall, MaskNormColsumCall, SpmmCall, XentCall
+from .kernels import AdamCall, GemmCall, HeadCall, MaskNormColsumCall, SpmmCall
 from .ops import colsum, gemm, linear, spmm_raw
 
 
@@ -115,14 +115,11 @@ class GCNTrainer:
     Schedule of one epoch (all buffers preallocated; ``capture()`` records it
     as one CUDA graph):
 
-      H1  = X W1                               gemm
+      H1  = X W1                               tcgen05 3xTF32 gemm (X streamed by TMA)
       Y1  = relu(D^-1 A H1 + b1)               spmm  (NORM|BIAS|RELU epilogue)
       P2  = D^-1 A Y1                          spmm  (NORM)
-      Z2  = P2 W2 + b2                         gemm
-      loss, dZ2 = xent(Z2, labels)             softmax-xent (mean)
-      db2 = colsum(dZ2);  dW2 = P2^T dZ2       colsum, split-K gemm
-      dP2 = dZ2 W2^T                           gemm
-      dP2 <- D^-1 dP2 (in place)               degree-norm (input of backward SpMM)
+      head: Z2 = P2 W2 + b2; loss, dZ2 = xent; fused output layer, one warp per row
+            dP2 = D^-1 (dZ2 W2^T); dW2 = P2^T dZ2; db2 = colsum(dZ2)
       dZ1 = (A^T dP2) * [Y1 > 0]               spmm over CSC (MASK epilogue)
       db1 = colsum(dZ1); dZ1 <- D^-1 dZ1       mask_norm_colsum (in place)
       dH1 = A^T dZ1                            spmm over CSC
@@ -152,7 +149,6 @@ class GCNTrainer:
         self.labels = torch.empty(V, dtype=torch.int64, device=dev)
         e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
         self.H1, self.Y1, self.P2 = e(hidden), e(hidden), e(hidden)
-        self.Z2, self.dZ2 = e(classes), e(classes)
         self.dP2, self.dZ1, self.dH1 = e(hidden), e(hidden), e(hidden)
         self.loss = torch.zeros(1, **f32)
 
@@ -168,12 +164,8 @@ class GCNTrainer:
         self.k_gemm1 = GemmCall(self.X, self.W1, self.H1)
         self.k_agg1 = SpmmCall(A, self.H1, self.Y1, flags=N | B | R, bias=self.b1)
         self.k_agg2 = SpmmCall(A, self.Y1, self.P2, flags=N)
-        self.k_gemm2 = GemmCall(self.P2, self.W2, self.Z2, bias=self.b2)
-        self.k_xent = XentCall(self.Z2, self.labels, self.loss, dZ=self.dZ2)
-        self.k_db2 = MaskNormColsumCall(self.dZ2, None, colsum=self.db2)
-        self.k_dW2 = GemmCall(self.P2, self.dZ2, self.dW2, trans_a=True)
-        self.k_dP2 = GemmCall(self.dZ2, self.W2, self.dP2, trans_b=True)
-        self.k_norm2 = MaskNormColsumCall(self.dP2, self.dP2, deg_offsets=deg_off)
+        self.k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
+                               self.db2, self.loss, deg_offsets=deg_off)
         self.k_bagg2 = SpmmCall(AT, self.dP2, self.dZ1, flags=M, mask=self.Y1)
         self.k_norm1 = MaskNormColsumCall(self.dZ1, self.dZ1, deg_offsets=deg_off, colsum=self.db1)
         self.k_bagg1 = SpmmCall(AT, self.dZ1, self.dH1)
@@ -193,21 +185,38 @@ class GCNTrainer:
         self.k_gemm1()
         self.k_agg1()
         self.k_agg2()
-        self.k_gemm2()
-        self.k_xent()
-        self.k_db2()
-        self.k_dW2()
-        self.k_dP2()
-        self.k_norm2()
+        self.k_head()
         self.k_bagg2()
         self.k_norm1()
         self.k_bagg1()
         self.k_dW1()
 
+    def schedule(self):
+        """(name, call) pairs of one epoch, in launch order."""
+        return [("X.W1", self.k_gemm1), ("agg1", self.k_agg1), ("agg2", self.k_agg2),
+                ("head", self.k_head), ("bagg2", self.k_bagg2), ("mask_norm_db1", self.k_norm1),
+                ("bagg1", self.k_bagg1), ("X^T.dH1", self.k_dW1), ("adam", self.k_adam)]
+
     def step(self):
         self.forward_backward()
         self.k_adam()
         return self.loss
+
+    def timed_step(self):
+        """One eager epoch with CUDA events between launches on the launching
+        stream (a GPU sleep first lets the host enqueue ahead, so gaps are not
+        timed).  Returns {name: ms}."""
+        st = torch.cuda.current_stream(self.dev)
+        sched = self.schedule()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(sched) + 1)]
+        torch.cuda.synchronize(self.dev)
+        torch.cuda._sleep(5_000_000)
+        ev[0].record(st)
+        for i, (_, call) in enumerate(sched):
+            call()
+            ev[i + 1].record(st)
+        torch.cuda.synchronize(self.dev)
+        return {name: ev[i].elapsed_time(ev[i + 1]) for i, (name, _) in enumerate(sched)}
 
     def capture(self):
         """Record one epoch (fwd+bwd+Adam) as a CUDA graph; replay with run()."""
