@@ -179,6 +179,12 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
             int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias, int relu, void *ws,
             size_t ws_bytes, cudaStream_t st);
 
+bool gemm_tc_tn_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                          const float *B, int64_t ldb);
+size_t gemm_tc_tn_workspace(int64_t M, int64_t N, int64_t K);
+int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // SIMT fallback (transposed A, unaligned strides, small M).
 int gemm_simt(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
               const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
@@ -254,7 +260,7 @@ int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, vo
 
 size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a) {
   size_t a = gemm_simt_workspace(M, N, Kd);
-  size_t b = trans_a ? 0 : gemm_tc_workspace(N, Kd);
+  size_t b = trans_a ? gemm_tc_tn_workspace(M, N, Kd) : gemm_tc_workspace(N, Kd);
   return a > b ? a : b;
 }
 
@@ -269,6 +275,8 @@ int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int 
   cudaStream_t st = as_stream(stream);
   if (gemm_tc_supported(M, N, Kd, A, lda, trans_a))
     return gemm_tc(M, N, Kd, A, lda, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes, st);
+  if (trans_a && !trans_b && !bias && !relu && gemm_tc_tn_supported(M, N, Kd, A, lda, B, ldb))
+    return gemm_tc_tn(M, N, Kd, A, lda, B, ldb, C, ldc, ws, ws_bytes, st);
   return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
                    st);
 }
@@ -502,82 +510,116 @@ int gnn_adam_step(int nparams, const void *param_table, float lr, float beta1, f
 namespace gnn {
 namespace {
 
-constexpr int kHeadWarps = 8;
-constexpr int kHeadRowsPerWarp = 64;
+constexpr int kHeadWarps = 4;
+constexpr int kHeadRowsPerWarp = 32;
 
 // partials layout: float [nb][din*C + C] then double loss[nb] (8-byte aligned)
 inline int64_t head_float_slots(int64_t nb, int64_t din, int64_t C) {
   return (nb * (din * C + C) + 1) / 2 * 2;
 }
 
+// Butterfly transpose-reduction: every lane holds v[0..NV) (NV = 16 or 32);
+// afterwards lane l holds sum over all 32 lanes of v[l * NV / 32] in v[0]
+// (NV=16: lanes 2k and 2k+1 hold value k; NV=32: lane k holds value k).
+// NV/2 + NV/4 + ... + 1 (+1) shuffles instead of NV * 5.
+template <int NV>
+__device__ __forceinline__ float butterfly_reduce(float (&v)[NV]) {
+  const int lane = (int)lane_id();
+#pragma unroll
+  for (int w = NV / 2, m = 16; w >= 1; w >>= 1, m >>= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      const float send = upper ? v[j] : v[j + w];
+      const float keep = upper ? v[j + w] : v[j];
+      v[j] = keep + __shfl_xor_sync(kFull, send, m);
+    }
+  }
+  // NV=32 consumed masks 16..1 (5 steps); NV=16 consumed 16..2: one more fold over bit 0
+  if (NV == 16) v[0] += __shfl_xor_sync(kFull, v[0], 1);
+  return v[0];
+}
+
+// One warp per row; lane l owns logit columns l and l+32.  Weights live in
+// registers (W[k][l], W[k][l+32]); the row's P values are broadcast once and
+// reused for the logits and the dW outer product; dP is one butterfly.
 template <int DIN>
-__global__ void __launch_bounds__(256) gcn_head_kernel(
+__global__ void __launch_bounds__(128) gcn_head_kernel(
     int64_t M, int din, int C, const float *__restrict__ P, int64_t ldp,
     const float *__restrict__ W, const float *__restrict__ b, const int64_t *__restrict__ labels,
     const int64_t *__restrict__ deg_offsets, float scale, float *dP, int64_t lddp,
     float *partials, double *lpart) {
-  __shared__ float sW[DIN * 64];
-  __shared__ float sb[64];
-  __shared__ float stage[kHeadWarps][32];
-  __shared__ double lred[kHeadWarps];
+  constexpr int NW = 4;  // warps per CTA
+  constexpr int NV = DIN <= 16 ? 16 : 32;
+  __shared__ float stage[NW][32];
+  __shared__ double lred[NW];
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-  for (int i = threadIdx.x; i < DIN * 64; i += blockDim.x) {
-    const int k = i / 64, c = i % 64;
-    sW[i] = (k < din && c < C) ? W[k * C + c] : 0.f;
-  }
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) sb[i] = i < C ? b[i] : 0.f;
-  __syncthreads();
   const bool v0 = lane < C, v1 = lane + 32 < C;
+  float w0[DIN], w1[DIN];
+#pragma unroll
+  for (int k = 0; k < DIN; ++k) {
+    w0[k] = (k < din && v0) ? W[k * C + lane] : 0.f;
+    w1[k] = (k < din && v1) ? W[k * C + lane + 32] : 0.f;
+  }
+  const float bb0 = v0 ? b[lane] : 0.f, bb1 = v1 ? b[lane + 32] : 0.f;
   float aw0[DIN], aw1[DIN];
 #pragma unroll
   for (int k = 0; k < DIN; ++k) aw0[k] = aw1[k] = 0.f;
   float ab0 = 0.f, ab1 = 0.f;
   double lsum = 0.0;
-  const int64_t r0 = ((int64_t)blockIdx.x * kHeadWarps + warp) * kHeadRowsPerWarp;
+  const int64_t r0 = ((int64_t)blockIdx.x * NW + warp) * kHeadRowsPerWarp;
   const int64_t r1 = min(M, r0 + kHeadRowsPerWarp);
   for (int64_t r = r0; r < r1; ++r) {
-    const float pv = lane < din ? P[r * ldp + lane] : 0.f;
-    float z0 = sb[lane], z1 = sb[lane + 32];
+    float pk[DIN];
 #pragma unroll
-    for (int k = 0; k < DIN; ++k) {
-      const float pk = __shfl_sync(kFull, pv, k);
-      z0 = fmaf(pk, sW[k * 64 + lane], z0);
-      z1 = fmaf(pk, sW[k * 64 + 32 + lane], z1);
+    for (int k0 = 0; k0 < DIN; k0 += 32) {
+      const float pv = (k0 + lane < din) ? __ldg(P + r * ldp + k0 + lane) : 0.f;
+#pragma unroll
+      for (int k = 0; k < 32 && k0 + k < DIN; ++k) pk[k0 + k] = __shfl_sync(kFull, pv, k);
     }
+    float z0a = bb0, z0b = 0.f, z1a = bb1, z1b = 0.f;  // two chains each for ILP
+#pragma unroll
+    for (int k = 0; k < DIN; k += 2) {
+      z0a = fmaf(pk[k], w0[k], z0a);
+      z1a = fmaf(pk[k], w1[k], z1a);
+      z0b = fmaf(pk[k + 1], w0[k + 1], z0b);
+      z1b = fmaf(pk[k + 1], w1[k + 1], z1b);
+    }
+    const float z0 = z0a + z0b, z1 = z1a + z1b;
     float mx = fmaxf(v0 ? z0 : -INFINITY, v1 ? z1 : -INFINITY);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-    float se = (v0 ? expf(z0 - mx) : 0.f) + (v1 ? expf(z1 - mx) : 0.f);
+    const float e0 = v0 ? __expf(z0 - mx) : 0.f, e1 = v1 ? __expf(z1 - mx) : 0.f;
+    float se = e0 + e1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
-    const float lse = mx + logf(se);
-    const int y = (int)labels[r];
+    const float inv = 1.f / se;
+    const int y = (int)__ldg(labels + r);
     const float zy = __shfl_sync(kFull, y < 32 ? z0 : z1, y & 31);
-    if (lane == 0) lsum += (double)(lse - zy);
-    const float d0 = v0 ? (expf(z0 - lse) - (lane == y ? 1.f : 0.f)) * scale : 0.f;
-    const float d1 = v1 ? (expf(z1 - lse) - (lane + 32 == y ? 1.f : 0.f)) * scale : 0.f;
+    if (lane == 0) lsum += (double)(mx + logf(se) - zy);
+    const float d0 = v0 ? (e0 * inv - (lane == y ? 1.f : 0.f)) * scale : 0.f;
+    const float d1 = v1 ? (e1 * inv - (lane + 32 == y ? 1.f : 0.f)) * scale : 0.f;
     ab0 += d0;
     ab1 += d1;
 #pragma unroll
     for (int k = 0; k < DIN; ++k) {
-      const float pk = __shfl_sync(kFull, pv, k);
-      aw0[k] = fmaf(pk, d0, aw0[k]);
-      aw1[k] = fmaf(pk, d1, aw1[k]);
+      aw0[k] = fmaf(pk[k], d0, aw0[k]);
+      aw1[k] = fmaf(pk[k], d1, aw1[k]);
     }
-    // dP[k] = sum_c dz_c W[k][c]: lane k accumulates over the broadcast dz
-    float dp = 0.f;
-    const int kk = lane < DIN ? lane : 0;
-    for (int c = 0; c < C; ++c) {
-      const float dc = __shfl_sync(kFull, c < 32 ? d0 : d1, c & 31);
-      dp = fmaf(dc, sW[kk * 64 + c], dp);
+    // dP[k] = sum_c dz_c W[k][c]: per-lane partials for every k, one butterfly per 32 k's
+    float rs = 1.f;
+    if (deg_offsets) {
+      const int64_t dg = __ldg(deg_offsets + r + 1) - __ldg(deg_offsets + r);
+      rs = dg > 0 ? 1.f / (float)dg : 0.f;
     }
-    if (lane < din) {
-      float rs = 1.f;
-      if (deg_offsets) {
-        const int64_t dg = deg_offsets[r + 1] - deg_offsets[r];
-        rs = dg > 0 ? 1.f / (float)dg : 0.f;
-      }
-      dP[r * lddp + lane] = dp * rs;
+#pragma unroll
+    for (int k0 = 0; k0 < DIN; k0 += NV) {
+      float part[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) part[j] = d0 * w0[k0 + j] + d1 * w1[k0 + j];
+      const float dp = butterfly_reduce<NV>(part);
+      const int k = k0 + (NV == 16 ? lane >> 1 : lane);
+      if ((NV == 32 || (lane & 1) == 0) && k < din) dP[r * lddp + k] = dp * rs;
     }
   }
   // CTA reduction in fixed warp order: rows k<din of dW (two column halves), then db
@@ -586,7 +628,7 @@ __global__ void __launch_bounds__(256) gcn_head_kernel(
 #pragma unroll
   for (int k = 0; k <= DIN; ++k) {
     if (k < din || k == DIN) {
-      const int kr = k < din ? k : din;  // row index in the partial (din == the db row)
+      const int kr = k < din ? k : din;  // partial row index (row din = db)
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         stage[warp][lane] = k < DIN ? (half ? aw1[k] : aw0[k]) : (half ? ab1 : ab0);
@@ -594,7 +636,7 @@ __global__ void __launch_bounds__(256) gcn_head_kernel(
         if (warp == 0) {
           float t = 0.f;
 #pragma unroll
-          for (int w2 = 0; w2 < kHeadWarps; ++w2) t += stage[w2][lane];
+          for (int w2 = 0; w2 < NW; ++w2) t += stage[w2][lane];
           const int c = lane + 32 * half;
           if (c < C) out[(int64_t)kr * C + c] = t;
         }
@@ -606,7 +648,7 @@ __global__ void __launch_bounds__(256) gcn_head_kernel(
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w2 = 0; w2 < kHeadWarps; ++w2) t += lred[w2];
+    for (int w2 = 0; w2 < NW; ++w2) t += lred[w2];
     lpart[blockIdx.x] = t;
   }
 }
@@ -656,7 +698,7 @@ int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
   double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
   const float scale = 1.0f / (float)M;
 #define GNN_HEAD(DN)                                                                            \
-  gcn_head_kernel<DN><<<(unsigned)nb, 256, 0, st>>>(M, (int)Din, (int)C, P, ldp, W, b, labels, \
+  gcn_head_kernel<DN><<<(unsigned)nb, 128, 0, st>>>(M, (int)Din, (int)C, P, ldp, W, b, labels, \
                                                     deg_offsets, scale, dP, lddp, partials, lpart)
   if (Din <= 16)
     GNN_HEAD(16);

@@ -277,6 +277,248 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
                  : "memory");
 }
 
+// ------------------------------------------------------------------------
+// Weight-gradient shape C[M,N] = A^T B, A [K,M] (row stride lda), B [K,N]
+// (ldb): the contraction runs over the K = |V| rows, so both operands are
+// MN-major in shared memory.  Canonical MN-major layouts (tcgen05 smem
+// descriptors): A uses SWIZZLE_128B atoms of 32 fp32 (MN) x 8 rows (K),
+// LBO = 4 KB between the four 32-column TMA boxes of a 128-wide M tile,
+// SBO = 1 KB between 8-row K groups; B (N <= 16) uses SWIZZLE_64B atoms
+// (16 fp32 x 8 rows, SBO = 512 B).  Both operands are split hi/lo in shared
+// memory by the split warps.  Work units = (m-tile, k-split); each unit's
+// [128 x N] partial is written to global and summed in a fixed order.
+__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                            uint32_t layout) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+
+constexpr int kTnStages = 4;
+
+struct TnArgs {
+  int64_t M, N, K;
+  int nkb_total;      // ceil(K / 32)
+  int kb_per_split;
+  int splits;
+  int64_t mtiles;
+  float *partials;    // [splits][M][N]
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnArgs p) {
+  static_assert(NPAD == 16, "MN-major B path is instantiated for N <= 16");
+  extern __shared__ __align__(1024) uint8_t tn_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tn_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr size_t kA = (size_t)kTcM * kTcBK * 4;   // 16 KB: 4 boxes of [32 rows x 128 B]
+  constexpr size_t kB = (size_t)kTcBK * NPAD * 4;   // 2 KB: [32 rows x 64 B]
+  float *sa = reinterpret_cast<float *>(base);
+  float *salo = reinterpret_cast<float *>(base + kTnStages * kA);
+  float *sb = reinterpret_cast<float *>(base + 2 * kTnStages * kA);
+  float *sblo = reinterpret_cast<float *>(base + 2 * kTnStages * kA + kTnStages * kB);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTnStages * kA + 2 * kTnStages * kB);
+  uint64_t *full = bars, *split = bars + kTnStages, *empty = bars + 2 * kTnStages;
+  uint64_t *acc_full = bars + 3 * kTnStages, *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5;
+  const int lane = (int)lane_id();
+  constexpr uint32_t kTx = (uint32_t)(kA + kB);
+  constexpr int kTmemCols = 32;
+  const int64_t units = p.mtiles * p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTnStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(split + s, 4);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // idesc: D f32, A/B tf32, A and B MN-major, N=NPAD, M=128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                         ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+  auto unit_kb = [&](int64_t u, int &kb0, int &kb1, int &m0) {
+    const int64_t mt = u % p.mtiles, sp = u / p.mtiles;
+    m0 = (int)(mt * kTcM);
+    kb0 = (int)(sp * p.kb_per_split);
+    kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int kb0, kb1, m0;
+        unit_kb(u, kb0, kb1, m0);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_arrive_expect_tx(full + s, kTx);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            tma_load_2d(smem_u32(sa + (size_t)s * kTcM * kTcBK + j * 32 * kTcBK), &tmA, m0 + 32 * j,
+                        kb * kTcBK, smem_u32(full + s));
+          tma_load_2d(smem_u32(sb + (size_t)s * kTcBK * NPAD), &tmB, 0, kb * kTcBK, smem_u32(full + s));
+          if (++s == kTnStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int kb0, kb1, m0;
+        unit_kb(u, kb0, kb1, m0);
+        mbar_wait(acc_empty + ab, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ab * NPAD);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(split + s, ph);
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(sa + (size_t)s * kTcM * kTcBK);
+          const uint32_t a_lo = smem_u32(salo + (size_t)s * kTcM * kTcBK);
+          const uint32_t b_hi = smem_u32(sb + (size_t)s * kTcBK * NPAD);
+          const uint32_t b_lo = smem_u32(sblo + (size_t)s * kTcBK * NPAD);
+#pragma unroll
+          for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA: +1 KB (A, SW128), +512 B (B, SW64)
+            const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 1024, 2);
+            const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 1024, 2);
+            const uint64_t bh = mn_desc(b_hi + k * 512, 16, 512, 4);
+            const uint64_t bl = mn_desc(b_lo + k * 512, 16, 512, 4);
+            tc_mma_tf32(d, ah, bh, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            tc_mma_tf32(d, ah, bl, idesc, 1);
+            tc_mma_tf32(d, al, bh, idesc, 1);
+          }
+          tc_commit(empty + s);
+          if (kb == kb1 - 1) tc_commit(acc_full + ab);
+          if (++s == kTnStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    const int tid = threadIdx.x - 128;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int kb0, kb1, m0;
+      unit_kb(u, kb0, kb1, m0);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(full + s, ph);
+        float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
+        float4 *l4 = reinterpret_cast<float4 *>(salo + (size_t)s * kTcM * kTcBK);
+#pragma unroll 4
+        for (int i = tid; i < kTcM * kTcBK / 4; i += 128) {
+          const float4 x = a4[i];
+          float4 h;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+          a4[i] = h;
+          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        float4 *b4 = reinterpret_cast<float4 *>(sb + (size_t)s * kTcBK * NPAD);
+        float4 *bl4 = reinterpret_cast<float4 *>(sblo + (size_t)s * kTcBK * NPAD);
+        for (int i = tid; i < kTcBK * NPAD / 4; i += 128) {
+          const float4 x = b4[i];
+          float4 h;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+          b4[i] = h;
+          bl4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split + s);
+        if (++s == kTnStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    const int q = warp & 3;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int kb0, kb1, m0;
+      unit_kb(u, kb0, kb1, m0);
+      const int64_t sp = u / p.mtiles;
+      mbar_wait(acc_full + ab, aph);
+      tc_fence_after();
+      uint32_t v[16];
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NPAD);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + ab);
+      const int64_t m = (int64_t)m0 + q * 32 + lane;
+      if (m < p.M) {
+        float *dst = p.partials + (sp * p.M + m) * p.N;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < p.N) dst[j] = __uint_as_float(v[j]);
+      }
+      if (++ab == 2) {
+        ab = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+}
+
+__global__ void tn_reduce_kernel(int64_t M, int64_t N, int splits, const float *__restrict__ partials,
+                                 float *C, int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += partials[(int64_t)z * total + t];
+    C[(t / N) * ldc + (t % N)] = s;
+  }
+}
+
 // B [K,N] row-major (ldb) or B^T [N,K] (trans_b) -> Bt_hi / Bt_lo [Npad, Kpad] K-major, zero padded.
 __global__ void split_b_kernel(const float *__restrict__ B, int64_t ldb, int trans_b, int64_t N,
                                int64_t K, int Npad, int64_t Kpad, float *bhi, float *blo) {
@@ -319,6 +561,19 @@ bool map_2d_sw128(CUtensorMap *tm, const float *base, int64_t inner, int64_t out
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool map_2d(CUtensorMap *tm, const float *base, int64_t inner, int64_t outer, int64_t ld,
+            int box_inner, int box_outer, CUtensorMapSwizzle sw) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int NPAD>
@@ -382,6 +637,63 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
     case 64: return launch_tc<64>(ta, tbh, tbl, p, st);
     default: return launch_tc<128>(ta, tbh, tbl, p, st);
   }
+}
+
+// ---- A^T B (weight gradient) on tcgen05
+bool gemm_tc_tn_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                          const float *B, int64_t ldb) {
+  return M >= 1 && N >= 1 && N <= 16 && K >= 1024 && (lda * 4) % 16 == 0 && (ldb * 4) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && (reinterpret_cast<uintptr_t>(B) & 15u) == 0 &&
+         encode_fn() != nullptr && getenv("GNN_GEMM_NO_TC") == nullptr;
+}
+
+static void tn_plan(int64_t M, int64_t K, int64_t &mtiles, int &nkb, int &kbps, int &splits) {
+  mtiles = ceil_div(M, kTcM);
+  nkb = (int)ceil_div(K, kTcBK);
+  int64_t want = 2 * (int64_t)sm_count();  // units
+  int64_t sp = ceil_div(want, mtiles);
+  if (sp > nkb) sp = nkb;
+  kbps = (int)ceil_div(nkb, sp);
+  splits = (int)ceil_div(nkb, kbps);
+}
+
+size_t gemm_tc_tn_workspace(int64_t M, int64_t N, int64_t K) {
+  int64_t mtiles;
+  int nkb, kbps, splits;
+  tn_plan(M, K, mtiles, nkb, kbps, splits);
+  return sizeof(float) * (size_t)(splits * M * N) + 512;
+}
+
+int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st) {
+  TnArgs p{};
+  int kbps, splits, nkb;
+  int64_t mtiles;
+  tn_plan(M, K, mtiles, nkb, kbps, splits);
+  if (ws_bytes < gemm_tc_tn_workspace(M, N, K)) return GNN_ERR_WORKSPACE;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.nkb_total = nkb;
+  p.kb_per_split = kbps;
+  p.splits = splits;
+  p.mtiles = mtiles;
+  p.partials = static_cast<float *>(ws);
+  CUtensorMap ta, tb;
+  // A [K rows, M cols]: boxes of 32 cols x 32 rows (SW128); B [K rows, N cols]: 16 x 32 (SW64)
+  if (!map_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !map_2d(&tb, B, N, K, ldb, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return GNN_ERR_UNSUPPORTED;
+  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + 2 * kTcBK * 16) * 4 + 2048;
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<16>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t units = mtiles * splits;
+  const int64_t grid = units < sm_count() ? units : sm_count();
+  gemm_tc_tn_kernel<16><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tb, p);
+  GNN_LAUNCH_CHECK();
+  tn_reduce_kernel<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(M, N, splits, p.partials, C, ldc);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
 }
 
 }  // namespace gnn

@@ -73,3 +73,16 @@ def test_colsum(gb):
     ref = X.double().sum(0).cpu().numpy()
     got = gb.colsum(X).cpu().numpy()
     assert oo.close(got, ref, X.abs().double().sum(0).cpu().numpy())[0]
+
+
+@pytest.mark.parametrize("K,M,ld,N", [(5000, 602, 608, 16), (3000, 100, 100, 7), (70_001, 64, 64, 16),
+                                      (232_965, 602, 608, 16), (2048, 1433, 1440, 12)])
+def test_gemm_tn_weight_gradient(gb, K, M, ld, N):
+    """dW = X^T dH (contraction over the vertex rows) — the tcgen05 MN-major path."""
+    rng = np.random.default_rng(K + M)
+    A, a = padded(K, M, ld, rng)
+    d = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    G = gb.gemm(A, torch.from_numpy(d).cuda(), trans_a=True)
+    ref = a.T.astype(np.float64) @ d.astype(np.float64)
+    ok, worst = oo.close(G.cpu().numpy(), ref, np.abs(a.T).astype(np.float64) @ np.abs(d))
+    assert ok, worst
