@@ -16,6 +16,7 @@
 // TMEM holds two accumulators so the epilogue of tile i overlaps tile i+1.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -280,12 +281,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
 // ------------------------------------------------------------------------
 // Weight-gradient shape C[M,N] = A^T B, A [K,M] (row stride lda), B [K,N]
 // (ldb): the contraction runs over the K = |V| rows, so both operands are
-// MN-major in shared memory.  Canonical MN-major layouts (tcgen05 smem
-// descriptors): A uses SWIZZLE_128B atoms of 32 fp32 (MN) x 8 rows (K),
-// LBO = 4 KB between the four 32-column TMA boxes of a 128-wide M tile,
-// SBO = 1 KB between 8-row K groups; B (N <= 16) uses SWIZZLE_64B atoms
-// (16 fp32 x 8 rows, SBO = 512 B).  Both operands are split hi/lo in shared
-// memory by the split warps.  Work units = (m-tile, k-split); each unit's
+// MN-major in shared memory.  MN-major tf32 operands have exactly one legal
+// smem layout, SWIZZLE_128B_BASE32B (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
+// 128-byte MN rows (32 fp32), 4-row K groups (SBO = 512 B), MN atoms = the
+// 32-column TMA boxes, 4 KB apart (LBO).  A is a 128-wide M tile (4 boxes),
+// B one box of 32 columns (N <= 32, OOB zero-filled).  Both operands are
+// split hi/lo in shared memory by the split warps.
+// Work units = (m-tile, k-split); each unit's
 // [128 x N] partial is written to global and summed in a fixed order.
 __device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                             uint32_t layout) {
@@ -307,11 +309,11 @@ struct TnArgs {
 template <int NPAD>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnArgs p) {
-  static_assert(NPAD == 16, "MN-major B path is instantiated for N <= 16");
+  static_assert(NPAD == 32, "MN-major B tile: one 128-byte SW128 atom (N <= 32, OOB-filled)");
   extern __shared__ __align__(1024) uint8_t tn_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tn_raw) + 1023) & ~(uintptr_t)1023);
   constexpr size_t kA = (size_t)kTcM * kTcBK * 4;   // 16 KB: 4 boxes of [32 rows x 128 B]
-  constexpr size_t kB = (size_t)kTcBK * NPAD * 4;   // 2 KB: [32 rows x 64 B]
+  constexpr size_t kB = (size_t)kTcBK * NPAD * 4;   // 4 KB: [32 rows x 128 B]
   float *sa = reinterpret_cast<float *>(base);
   float *salo = reinterpret_cast<float *>(base + kTnStages * kA);
   float *sb = reinterpret_cast<float *>(base + 2 * kTnStages * kA);
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   constexpr uint32_t kTx = (uint32_t)(kA + kB);
-  constexpr int kTmemCols = 32;
+  constexpr int kTmemCols = 64;
   const int64_t units = p.mtiles * p.splits;
 
   if (threadIdx.x == 0) {
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
   const uint32_t tmem = *tmem_slot;
   // idesc: D f32, A/B tf32, A and B MN-major, N=NPAD, M=128
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
-                         ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+                   ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+
   auto unit_kb = [&](int64_t u, int &kb0, int &kb1, int &m0) {
     const int64_t mt = u % p.mtiles, sp = u / p.mtiles;
     m0 = (int)(mt * kTcM);
@@ -400,11 +403,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
           const uint32_t b_hi = smem_u32(sb + (size_t)s * kTcBK * NPAD);
           const uint32_t b_lo = smem_u32(sblo + (size_t)s * kTcBK * NPAD);
 #pragma unroll
-          for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA: +1 KB (A, SW128), +512 B (B, SW64)
-            const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 1024, 2);
-            const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 1024, 2);
-            const uint64_t bh = mn_desc(b_hi + k * 512, 16, 512, 4);
-            const uint64_t bl = mn_desc(b_lo + k * 512, 16, 512, 4);
+          for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA = one 1 KB SW128 atom row group
+            // SWIZZLE_128B_BASE32B (layout 1): 128-byte MN rows, 4-row K groups (SBO 512 B),
+            // MN atoms (the 32-column TMA boxes) 4 KB apart (LBO)
+            const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 512, 1);
+            const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 512, 1);
+            const uint64_t bh = mn_desc(b_hi + k * 1024, 4096, 512, 1);
+            const uint64_t bl = mn_desc(b_lo + k * 1024, 4096, 512, 1);
             tc_mma_tf32(d, ah, bh, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             tc_mma_tf32(d, ah, bl, idesc, 1);
             tc_mma_tf32(d, al, bh, idesc, 1);
@@ -433,6 +438,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
         mbar_wait(full + s, ph);
         float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
         float4 *l4 = reinterpret_cast<float4 *>(salo + (size_t)s * kTcM * kTcBK);
+#ifdef GNN_TN_DEBUG
+        if (blockIdx.x == 0 && tid == 0 && kb == kb0)
+          printf("TN dbg smem A[0..3]=%f %f %f %f B[0..3]=%f %f %f %f\n", sa[s * kTcM * kTcBK],
+                 sa[s * kTcM * kTcBK + 1], sa[s * kTcM * kTcBK + 2], sa[s * kTcM * kTcBK + 3],
+                 sb[s * kTcBK * NPAD], sb[s * kTcBK * NPAD + 1], sb[s * kTcBK * NPAD + 2],
+                 sb[s * kTcBK * NPAD + 3]);
+#endif
 #pragma unroll 4
         for (int i = tid; i < kTcM * kTcBK / 4; i += 128) {
           const float4 x = a4[i];
@@ -484,6 +496,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
             "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef GNN_TN_DEBUG
+      if (blockIdx.x == 0 && q == 0 && lane < 2)
+        printf("TN dbg u=%lld lane=%d v0=%f v1=%f kb0=%d kb1=%d m0=%d\n", (long long)u, lane,
+               __uint_as_float(v[0]), __uint_as_float(v[1]), kb0, kb1, m0);
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + ab);
@@ -680,16 +697,17 @@ int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, con
   p.mtiles = mtiles;
   p.partials = static_cast<float *>(ws);
   CUtensorMap ta, tb;
-  // A [K rows, M cols]: boxes of 32 cols x 32 rows (SW128); B [K rows, N cols]: 16 x 32 (SW64)
-  if (!map_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !map_2d(&tb, B, N, K, ldb, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+  // A [K rows, M cols] and B [K rows, N cols]: boxes of 32 cols x 32 rows
+  // MN-major tf32 operands: the only legal smem layout is SWIZZLE_128B_BASE32B
+  if (!map_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+      !map_2d(&tb, B, N, K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return GNN_ERR_UNSUPPORTED;
-  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + 2 * kTcBK * 16) * 4 + 2048;
-  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<16>,
+  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + 2 * kTcBK * 32) * 4 + 2048;
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = mtiles * splits;
   const int64_t grid = units < sm_count() ? units : sm_count();
-  gemm_tc_tn_kernel<16><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tb, p);
+  gemm_tc_tn_kernel<32><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tb, p);
   GNN_LAUNCH_CHECK();
   tn_reduce_kernel<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(M, N, splits, p.partials, C, ldc);
   GNN_LAUNCH_CHECK();
