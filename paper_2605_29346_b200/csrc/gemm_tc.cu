@@ -1,8 +1,11 @@
 // fp32-accurate dense transform C[M,N] = A[M,K] . B[K,N] (+bias)(relu) on the
-// 5th-generation tensor cores (tcgen05, kind::tf32) with the 3xTF32 split
-//   A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi,   x_hi = x & 0xffffe000, x_lo = x - x_hi
-// (x_hi is exactly representable in TF32; the dropped A_lo.B_lo term is
-// ~2^-22 relative), accumulated in fp32 in tensor memory.  This is the only
+// 5th-generation tensor cores (tcgen05, kind::tf32) with a split-TF32 scheme
+//   A.B = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi + A_lo.B_lo,  x_hi = x & 0xffffe000, x_lo = x - x_hi
+// The tensor core truncates fp32 operands to TF32 (measured), so the raw A
+// tile IS A_hi and only A_lo is materialised; B is tiny and pre-split into a
+// [B_hi | B_lo] operand of width 2N, so each K-step is two MMAs
+//   D[:, 0:2N] += A_raw . [B_hi|B_lo]^T  and  D += A_lo . [B_hi|B_lo]^T
+// and the epilogue adds the two halves.  fp32 accumulation in tensor memory.  This is the only
 // dense contraction on the path: X.W with X [V,K] fp32,
 // W [K,N<=256] — HBM-bound (arithmetic intensity ~8 flop/B for N=16), so the
 // design goal is to stream A at HBM speed.
@@ -26,10 +29,10 @@ namespace {
 
 constexpr int kTcM = 128;
 constexpr int kTcBK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
-// smem ring depth: 192 KB of stages whatever the B tile width
+// smem ring depth: ~200 KB of stages whatever the B tile width
 template <int NPAD>
 constexpr int tc_stages() {
-  return NPAD <= 32 ? 5 : (NPAD <= 64 ? 4 : 3);
+  return NPAD <= 16 ? 6 : (NPAD <= 32 ? 5 : (NPAD <= 64 ? 4 : 3));
 }
 constexpr int kTcThreads = 384;
 
@@ -83,6 +86,15 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
 template <int NPAD>
 constexpr size_t tc_smem_bytes() {
   return (size_t)tc_stages<NPAD>() * (2 * kTcM * kTcBK + 2 * NPAD * kTcBK) * 4 + 1024 + 1024;
@@ -101,8 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   constexpr size_t kB = (size_t)NPAD * kTcBK * 4;
   float *sa = reinterpret_cast<float *>(base);
   float *salo = reinterpret_cast<float *>(base + kTcStages * kA);
-  float *sbhi = reinterpret_cast<float *>(base + 2 * kTcStages * kA);
-  float *sblo = reinterpret_cast<float *>(base + 2 * kTcStages * kA + kTcStages * kB);
+  float *sbhi = reinterpret_cast<float *>(base + 2 * kTcStages * kA);  // [stage][hi rows|lo rows]
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTcStages * kA + 2 * kTcStages * kB);
   uint64_t *full = bars, *split = bars + kTcStages, *empty = bars + 2 * kTcStages;
   uint64_t *acc_full = bars + 3 * kTcStages, *acc_empty = acc_full + 2;
@@ -111,7 +122,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   constexpr uint32_t kTxBytes = (uint32_t)(kA + 2 * kB);
-  constexpr int kTmemCols = (2 * NPAD) <= 32 ? 32 : (2 * NPAD) <= 64 ? 64 : (2 * NPAD) <= 128 ? 128 : (2 * NPAD) <= 256 ? 256 : 512;
+  constexpr int kAcc = 2 * NPAD;  // accumulator width: [hi half | lo half]
+  constexpr int kTmemCols = (2 * kAcc) <= 32 ? 32 : (2 * kAcc) <= 64 ? 64 : (2 * kAcc) <= 128 ? 128 : (2 * kAcc) <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -136,8 +148,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // idesc: D f32, A/B tf32, K-major both, N, M=128
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NPAD >> 3) << 17) |
+  // idesc: D f32, A/B tf32, K-major both, N = 2*NPAD, M=128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kAcc >> 3) << 17) |
                          ((uint32_t)(kTcM >> 4) << 24);
 
   if (warp == 0) {
@@ -151,8 +163,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
           mbar_wait(empty + s, ph ^ 1);
           mbar_arrive_expect_tx(full + s, kTxBytes);
           tma_load_2d(smem_u32(sa + (size_t)s * kTcM * kTcBK), &tmA, kb * kTcBK, m0, smem_u32(full + s));
-          tma_load_2d(smem_u32(sbhi + (size_t)s * NPAD * kTcBK), &tmBhi, kb * kTcBK, 0, smem_u32(full + s));
-          tma_load_2d(smem_u32(sblo + (size_t)s * NPAD * kTcBK), &tmBlo, kb * kTcBK, 0, smem_u32(full + s));
+          tma_load_2d(smem_u32(sbhi + (size_t)s * 2 * NPAD * kTcBK), &tmBhi, kb * kTcBK, 0,
+                      smem_u32(full + s));
+          tma_load_2d(smem_u32(sbhi + (size_t)s * 2 * NPAD * kTcBK + NPAD * kTcBK), &tmBlo, kb * kTcBK,
+                      0, smem_u32(full + s));
           if (++s == kTcStages) {
             s = 0;
             ph ^= 1;
@@ -170,20 +184,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
         mbar_wait(acc_empty + ab, aph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(ab * NPAD);
+        const uint32_t d = tmem + (uint32_t)(ab * kAcc);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(split + s, ph);
           tc_fence_after();
           const uint64_t ah = sw128_desc(smem_u32(sa + (size_t)s * kTcM * kTcBK));
           const uint64_t al = sw128_desc(smem_u32(salo + (size_t)s * kTcM * kTcBK));
-          const uint64_t bh = sw128_desc(smem_u32(sbhi + (size_t)s * NPAD * kTcBK));
-          const uint64_t bl = sw128_desc(smem_u32(sblo + (size_t)s * NPAD * kTcBK));
+          const uint64_t bc = sw128_desc(smem_u32(sbhi + (size_t)s * 2 * NPAD * kTcBK));  // [hi|lo] rows
 #pragma unroll
           for (int k = 0; k < kTcBK / 8; ++k) {  // K=8 tf32 = 32 bytes per MMA: +2 in the >>4 address field
             const uint64_t o = (uint64_t)(k * 2);
-            tc_mma_tf32(d, ah + o, bh + o, idesc, (kb | k) != 0);
-            tc_mma_tf32(d, ah + o, bl + o, idesc, 1);
-            tc_mma_tf32(d, al + o, bh + o, idesc, 1);
+            tc_mma_tf32(d, ah + o, bc + o, idesc, (kb | k) != 0);
+            tc_mma_tf32(d, al + o, bc + o, idesc, 1);
           }
           tc_commit(empty + s);  // smem stage free once these MMAs retire
           if (kb == p.nkb - 1) tc_commit(acc_full + ab);
@@ -216,8 +228,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
           h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
           h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
           h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-          a4[i] = h;
-          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);  // raw A is A_hi to the MMA
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
@@ -239,21 +250,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       const int64_t row = t * kTcM + q * 32 + lane;
       float *crow = p.C + row * p.ldc;
       for (int c0 = 0; c0 < NPAD; c0 += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NPAD + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
+        uint32_t v[16], u[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
+        tmem_ld16(taddr, v);
+        tmem_ld16(taddr + NPAD, u);  // the B_lo half
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < p.M) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int64_t c = c0 + j;
             if (c < p.N) {
-              float y = __uint_as_float(v[j]);
+              float y = __uint_as_float(v[j]) + __uint_as_float(u[j]);
               if (p.bias) y += p.bias[c];
               if (p.relu) y = fmaxf(y, 0.f);
               crow[c] = y;
@@ -295,7 +302,7 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
-constexpr int kTnStages = 4;
+constexpr int kTnStages = 6;
 
 struct TnArgs {
   int64_t M, N, K;
@@ -317,15 +324,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
   float *sa = reinterpret_cast<float *>(base);
   float *salo = reinterpret_cast<float *>(base + kTnStages * kA);
   float *sb = reinterpret_cast<float *>(base + 2 * kTnStages * kA);
-  float *sblo = reinterpret_cast<float *>(base + 2 * kTnStages * kA + kTnStages * kB);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTnStages * kA + 2 * kTnStages * kB);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTnStages * kA + kTnStages * kB);
   uint64_t *full = bars, *split = bars + kTnStages, *empty = bars + 2 * kTnStages;
   uint64_t *acc_full = bars + 3 * kTnStages, *acc_empty = acc_full + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   constexpr uint32_t kTx = (uint32_t)(kA + kB);
-  constexpr int kTmemCols = 64;
+  constexpr int kTmemCols = 64;  // two accumulators x 32 columns ([B_hi | B_lo] halves)
   const int64_t units = p.mtiles * p.splits;
 
   if (threadIdx.x == 0) {
@@ -401,18 +407,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
           const uint32_t a_hi = smem_u32(sa + (size_t)s * kTcM * kTcBK);
           const uint32_t a_lo = smem_u32(salo + (size_t)s * kTcM * kTcBK);
           const uint32_t b_hi = smem_u32(sb + (size_t)s * kTcBK * NPAD);
-          const uint32_t b_lo = smem_u32(sblo + (size_t)s * kTcBK * NPAD);
 #pragma unroll
           for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA = one 1 KB SW128 atom row group
             // SWIZZLE_128B_BASE32B (layout 1): 128-byte MN rows, 4-row K groups (SBO 512 B),
             // MN atoms (the 32-column TMA boxes) 4 KB apart (LBO)
             const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 512, 1);
             const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 512, 1);
-            const uint64_t bh = mn_desc(b_hi + k * 1024, 4096, 512, 1);
-            const uint64_t bl = mn_desc(b_lo + k * 1024, 4096, 512, 1);
-            tc_mma_tf32(d, ah, bh, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-            tc_mma_tf32(d, ah, bl, idesc, 1);
-            tc_mma_tf32(d, al, bh, idesc, 1);
+            const uint64_t bc = mn_desc(b_hi + k * 1024, 4096, 512, 1);  // cols [0,16) hi, [16,32) lo
+            tc_mma_tf32(d, ah, bc, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            tc_mma_tf32(d, al, bc, idesc, 1);
           }
           tc_commit(empty + s);
           if (kb == kb1 - 1) tc_commit(acc_full + ab);
@@ -438,13 +441,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
         mbar_wait(full + s, ph);
         float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
         float4 *l4 = reinterpret_cast<float4 *>(salo + (size_t)s * kTcM * kTcBK);
-#ifdef GNN_TN_DEBUG
-        if (blockIdx.x == 0 && tid == 0 && kb == kb0)
-          printf("TN dbg smem A[0..3]=%f %f %f %f B[0..3]=%f %f %f %f\n", sa[s * kTcM * kTcBK],
-                 sa[s * kTcM * kTcBK + 1], sa[s * kTcM * kTcBK + 2], sa[s * kTcM * kTcBK + 3],
-                 sb[s * kTcBK * NPAD], sb[s * kTcBK * NPAD + 1], sb[s * kTcBK * NPAD + 2],
-                 sb[s * kTcBK * NPAD + 3]);
-#endif
 #pragma unroll 4
         for (int i = tid; i < kTcM * kTcBK / 4; i += 128) {
           const float4 x = a4[i];
@@ -453,20 +449,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
           h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
           h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
           h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-          a4[i] = h;
-          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+          l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);  // raw A = A_hi
         }
-        float4 *b4 = reinterpret_cast<float4 *>(sb + (size_t)s * kTcBK * NPAD);
-        float4 *bl4 = reinterpret_cast<float4 *>(sblo + (size_t)s * kTcBK * NPAD);
+        // B rows are 128 B (32 columns; 16 real + 16 TMA zero-fill).  Put B_lo of
+        // column n into column n+16: under the 32B-atom swizzle (phys chunk =
+        // logical chunk ^ (row & 3)) that partner is the byte offset ^ 64.
+        uint8_t *bb = reinterpret_cast<uint8_t *>(sb + (size_t)s * kTcBK * NPAD);
         for (int i = tid; i < kTcBK * NPAD / 4; i += 128) {
-          const float4 x = b4[i];
-          float4 h;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-          b4[i] = h;
-          bl4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+          const int off = i * 16;
+          const int logical_chunk = ((off >> 5) & 3) ^ ((off >> 7) & 3);
+          if (logical_chunk < 2) {
+            const float4 x = *reinterpret_cast<const float4 *>(bb + off);
+            float4 lo;
+            lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+            lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+            lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+            lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+            *reinterpret_cast<float4 *>(bb + (off ^ 64)) = lo;
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -487,20 +487,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
       const int64_t sp = u / p.mtiles;
       mbar_wait(acc_full + ab, aph);
       tc_fence_after();
-      uint32_t v[16];
+      uint32_t v[16], w[16];
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NPAD);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
+      tmem_ld16(taddr, v);
+      tmem_ld16(taddr + 16, w);  // B_lo half
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifdef GNN_TN_DEBUG
-      if (blockIdx.x == 0 && q == 0 && lane < 2)
-        printf("TN dbg u=%lld lane=%d v0=%f v1=%f kb0=%d kb1=%d m0=%d\n", (long long)u, lane,
-               __uint_as_float(v[0]), __uint_as_float(v[1]), kb0, kb1, m0);
-#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + ab);
@@ -509,7 +500,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
         float *dst = p.partials + (sp * p.M + m) * p.N;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (j < p.N) dst[j] = __uint_as_float(v[j]);
+          if (j < p.N) dst[j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
       }
       if (++ab == 2) {
         ab = 0;
@@ -702,7 +693,7 @@ int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, con
   if (!map_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
       !map_2d(&tb, B, N, K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return GNN_ERR_UNSUPPORTED;
-  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + 2 * kTcBK * 32) * 4 + 2048;
+  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + kTcBK * 32) * 4 + 2048;
   GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = mtiles * splits;
