@@ -182,6 +182,8 @@ class CsrGraph:
     @property
     def targets(self) -> np.ndarray:
         if self._h_targets is None:
+            if self.d_targets is None:
+                raise RuntimeError("targets released without a host view")
             object.__setattr__(self, "_h_targets", _readonly(self.d_targets.cpu().numpy()))
         return self._h_targets
 
@@ -213,7 +215,7 @@ class CsrGraph:
     def csr(self) -> SparseOperand:
         if self._csr is None:
             object.__setattr__(self, "_csr", SparseOperand(self.num_vertices, self.num_vertices,
-                                                           self.d_offsets, self.d_targets))
+                                                           self.d_offsets, self._device_targets()))
         return self._csr
 
     def csc(self, with_eid: bool = False) -> SparseOperand:
@@ -222,7 +224,8 @@ class CsrGraph:
         so the |E| edge-ID array is not allocated for it."""
         if self._csc is None or (with_eid and self._csc.eid is None):
             t_off, t_rows, t_eid = _transpose(self.num_vertices, self.num_vertices,
-                                              self.d_offsets, self.d_targets, with_eid=with_eid)
+                                              self.d_offsets, self._device_targets(),
+                                              with_eid=with_eid)
             object.__setattr__(self, "_csc", SparseOperand(self.num_vertices, self.num_vertices,
                                                            t_off, t_rows, eid=t_eid))
         return self._csc
@@ -230,6 +233,21 @@ class CsrGraph:
     def drop_csc(self) -> None:
         """Release the canonical CSC (e.g. after building the coalesced forms)."""
         object.__setattr__(self, "_csc", None)
+
+    def release_device_targets(self) -> None:
+        """Keep the canonical targets only as the (materialised) host view and
+        free the device copy — for trainers that run on the coalesced forms.
+        Degree-norms keep using the device offsets; any later op that needs
+        the canonical device CSR re-uploads it."""
+        _ = self.targets  # materialise the read-only host view first
+        object.__setattr__(self, "d_targets", None)
+        object.__setattr__(self, "_csr", None)
+
+    def _device_targets(self) -> torch.Tensor:
+        if self.d_targets is None:
+            object.__setattr__(self, "d_targets", torch.from_numpy(
+                np.ascontiguousarray(self._h_targets)).to(self.d_offsets.device))
+        return self.d_targets
 
     def csr_coalesced(self) -> SparseOperand:
         """Unique (row,col) pairs with multiplicities, columns ascending per row.
@@ -266,7 +284,9 @@ class CsrGraph:
             if op is not None:
                 n += op.nbytes()
         if self._csr is None:
-            n += self.d_offsets.numel() * 8 + self.d_targets.numel() * 4
+            n += self.d_offsets.numel() * 8
+            if self.d_targets is not None:
+                n += self.d_targets.numel() * 4
         return n
 
     def __repr__(self):

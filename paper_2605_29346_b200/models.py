@@ -128,7 +128,8 @@ class GCNTrainer:
     """
 
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, *, lr=0.01,
-                 seed: int = 0, coalesced: bool = False, drop_canonical_csc: bool = False):
+                 seed: int = 0, coalesced: bool = False, drop_canonical_csc: bool = False,
+                 release_canonical: bool = False):
         self.g = g
         dev = g.device
         self.dev = dev
@@ -154,8 +155,10 @@ class GCNTrainer:
 
         if coalesced:
             A, AT = g.csr_coalesced(), g.csc_coalesced()
-            if drop_canonical_csc:
+            if drop_canonical_csc or release_canonical:
                 g.drop_csc()
+            if release_canonical:  # canonical CSR stays on the host only
+                g.release_device_targets()
         else:
             A, AT = g.csr(), g.csc()
         self.A, self.AT = A, AT
