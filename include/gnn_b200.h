@@ -199,6 +199,59 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
 int gnn_degree_norm_inplace(int64_t num_rows, const int64_t *offsets, float *X, int64_t ldx,
                             int64_t K, gnn_stream_t stream);
 
+/* ------------------------------------------------- SDDMM / edge softmax */
+/* SDDMM on the CSR (GraphPy "CSR-style COO"):
+ *   out[e,h] = < X[row_e, h*F:(h+1)*F], Y[col_e, h*F:(h+1)*F] >,  F = K/heads,
+ * in CSR edge order.  Edge-parallel over the plan's chunks; the row operand
+ * is loaded once per row run and reused across the run's edges.  Also the
+ * SpMMve backward w.r.t. the edge values (dalpha = SDDMM(dY, X)). */
+int gnn_sddmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads, const float *X,
+              int64_t ldx, const float *Y, int64_t ldy, int64_t K, float *out,
+              gnn_stream_t stream);
+
+/* Edge scores for the edge softmax: given (s = [nnz, heads]) or, when s is
+ * NULL, the GAT score of SURVEY Appendix A.6 computed on the fly:
+ *   s[e,h] = LeakyReLU(el[col_e,h] + er[row_e,h], slope)   (el [num_cols,H], er [num_rows,H]). */
+typedef struct gnn_edge_scores {
+  const float *s;
+  const float *el;
+  const float *er;
+  float slope;
+} gnn_edge_scores_t;
+
+/* alpha[e,h] = exp(s[e,h] - max_row) / sum_row exp(.)  over each CSR row (per
+ * head); the attention state tensor of PAPER.md:606-617.  alpha may alias s.
+ * Deterministic (fixed-order reductions; rows spanning several chunks are
+ * combined from per-chunk partials).  heads <= 16. */
+size_t gnn_edge_softmax_workspace(const gnn_spmm_plan_t *plan, int64_t heads);
+int gnn_edge_softmax_fwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const gnn_edge_scores_t *scores, float *alpha, void *ws, size_t ws_bytes,
+                         gnn_stream_t stream);
+/* ds[e,h] = alpha (dalpha - sum_row alpha*dalpha); when scores->el is given
+ * (GAT mode) also times LeakyReLU'(el[col]+er[row]).  ds may alias dalpha. */
+int gnn_edge_softmax_bwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const float *alpha, const float *dalpha, const gnn_edge_scores_t *scores,
+                         float *ds, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
+/* GAT attention projections (Appendix A.6): el[v,h] = <Wh[v,h,:], a_l[h,:]>,
+ * er[v,h] = <Wh[v,h,:], a_r[h,:]>; a_l/a_r are [heads, F]. */
+int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,
+                      const float *a_l, const float *a_r, float *el, float *er,
+                      gnn_stream_t stream);
+/* Backward: dWh += del (x) a_l + der (x) a_r (in place); da_l = sum_v Wh*del,
+ * da_r = sum_v Wh*der (deterministic two-level reduction). */
+size_t gnn_gat_attn_proj_bwd_workspace(int64_t heads, int64_t F);
+int gnn_gat_attn_proj_bwd(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,
+                          const float *a_l, const float *a_r, const float *del, const float *der,
+                          float *dWh, int64_t ldd, float *da_l, float *da_r, void *ws,
+                          size_t ws_bytes, gnn_stream_t stream);
+/* Last GAT layer: out[v,f] = mean_h Y[v,h*F+f] (+ bias[f]); and its backward
+ * dY[v,h*F+f] = dout[v,f] / heads. */
+int gnn_head_mean(int64_t V, int64_t heads, int64_t F, const float *Y, int64_t ldy,
+                  const float *bias, float *out, int64_t ldo, gnn_stream_t stream);
+int gnn_head_mean_bwd(int64_t V, int64_t heads, int64_t F, const float *dout, int64_t ldo,
+                      float *dY, int64_t ldy, gnn_stream_t stream);
+
 /* ---------------------------------------------------------- dense ops */
 /* C[M,N] = op(A) . B (+bias)(relu), fp32 in/out, fp32-accurate.
  * trans_a = 0: A is [M,Kd] (lda);  trans_a = 1: A is [Kd,M] (lda), i.e. C = A^T B

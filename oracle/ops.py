@@ -164,3 +164,124 @@ def close(gpu, ref, ref_abs=None, rtol=1e-5):
     err = np.abs(gpu - ref)
     ok = err <= rtol * scale + 1e-30
     return bool(np.all(ok)), float(np.max(err / np.maximum(scale, 1e-30))) if err.size else 0.0
+
+
+# ------------------------------------------------------------------- GAT
+def leaky_relu(x, slope):
+    return np.where(x > 0, x, slope * x)
+
+
+def _rows_of(offsets):
+    offsets = np.asarray(offsets, dtype=np.int64)
+    return np.repeat(np.arange(offsets.size - 1), np.diff(offsets))
+
+
+def gat_scores(offsets, cols, el, er, slope=0.2):
+    """Appendix A.6: s_e,h = LeakyReLU(el[col_e,h] + er[row_e,h]) for NZE
+    e = (row v, col u) — the degenerate (K=1) SDDMM of PAPER.md:281-283.
+    Returns (s, pre)."""
+    el = np.asarray(el, dtype=np.float64)
+    er = np.asarray(er, dtype=np.float64)
+    pre = el[np.asarray(cols)] + er[_rows_of(offsets)]
+    return leaky_relu(pre, slope), pre
+
+
+def attn_proj(Wh, a, heads):
+    """el[v,h] = <Wh[v,h,:], a[h,:]> (a is [heads, F])."""
+    V = Wh.shape[0]
+    return (np.asarray(Wh, np.float64).reshape(V, heads, -1) * np.asarray(a, np.float64)[None]).sum(-1)
+
+
+def gat_layer_fwd(offsets, cols, X, W, a_l, a_r, b, heads, mean=False, relu=False, slope=0.2):
+    """One GAT layer (Appendix A.6; state tensor alpha saved):
+    Wh = X W; el/er = attention projections; alpha = edge_softmax(scores);
+    Y = SpMMve(A, alpha, Wh) per head; heads concatenated (+b, optional ReLU)
+    or averaged (+b) in the last layer."""
+    X = np.asarray(X, dtype=np.float64)
+    Wh = X @ np.asarray(W, np.float64)
+    V = Wh.shape[0]
+    F = Wh.shape[1] // heads
+    el, er = attn_proj(Wh, a_l, heads), attn_proj(Wh, a_r, heads)
+    s, pre = gat_scores(offsets, cols, el, er, slope)
+    alpha = edge_softmax(offsets, s)
+    Yc = spmm(offsets, cols, Wh, vals=alpha, heads=heads)
+    if mean:
+        Z = Yc.reshape(V, heads, F).mean(axis=1) + b
+    else:
+        Z = Yc + b
+    out = np.maximum(Z, 0.0) if relu else Z
+    cache = dict(X=X, W=np.asarray(W, np.float64), Wh=Wh, el=el, er=er, pre=pre, alpha=alpha,
+                 Z=Z, a_l=np.asarray(a_l, np.float64), a_r=np.asarray(a_r, np.float64),
+                 heads=heads, mean=mean, relu=relu, slope=slope)
+    return out, cache
+
+
+def gat_layer_bwd(offsets, cols, c, dout, absmode=False):
+    """Hand-derived backward of gat_layer_fwd.  SpMMve^T for dWh (PAPER.md:
+    264-265), dalpha by the dot SDDMM, softmax backward, LeakyReLU backward,
+    attention-projection backward, then the dense transform.  absmode=True
+    runs the same contractions on absolute values with every subtraction
+    turned into an addition: the Appendix A.8 ``ref_abs`` scale."""
+    A = np.abs if absmode else (lambda t: t)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    cols = np.asarray(cols)
+    H, mean, slope = c["heads"], c["mean"], c["slope"]
+    V = c["Wh"].shape[0]
+    F = c["Wh"].shape[1] // H
+    dZ = A(np.asarray(dout, np.float64))
+    if c["relu"]:
+        dZ = dZ * (c["Z"] > 0)
+    db = dZ.sum(axis=0)
+    dY = np.repeat(dZ[:, None, :] / H, H, axis=1).reshape(V, H * F) if mean else dZ
+    Wh, alpha = A(c["Wh"]), c["alpha"]
+    rows = _rows_of(offsets)
+    # dWh (aggregation part) = A^T_alpha dY: scatter-add over the edge list
+    dWh = np.zeros_like(Wh)
+    contrib = dY[rows].reshape(-1, H, F) * alpha[:, :, None]
+    np.add.at(dWh, cols, contrib.reshape(-1, H * F))
+    dalpha = sddmm(offsets, cols, dY, Wh, heads=H)
+    if absmode:
+        srow = spmm(offsets, cols, np.ones((V, H)), vals=alpha * dalpha, heads=H)
+        ds = alpha * (dalpha + srow[rows])
+        ds = ds * np.where(c["pre"] > 0, 1.0, abs(slope))
+    else:
+        ds = edge_softmax_backward(offsets, alpha, dalpha) * np.where(c["pre"] > 0, 1.0, slope)
+    der = spmm(offsets, cols, np.ones((V, H)), vals=ds, heads=H)
+    dl = np.zeros((V, H))
+    np.add.at(dl, cols, ds)
+    a_l, a_r = A(c["a_l"]), A(c["a_r"])
+    dWh = dWh + (dl[:, :, None] * a_l[None] + der[:, :, None] * a_r[None]).reshape(V, H * F)
+    da_l = (Wh.reshape(V, H, F) * dl[:, :, None]).sum(axis=0)
+    da_r = (Wh.reshape(V, H, F) * der[:, :, None]).sum(axis=0)
+    dW = A(c["X"]).T @ dWh
+    dX = dWh @ A(c["W"]).T
+    return {"W": dW, "a_l": da_l, "a_r": da_r, "b": db, "X": dX, "Wh": dWh, "alpha": dalpha,
+            "ds": ds, "el": dl, "er": der}
+
+
+# ------------------------------------------------------------------- GIN
+def gin_layer_fwd(offsets, cols, X, W1, b1, W2, b2, eps=0.0, relu_out=False):
+    """Appendix A.5: Z = MLP((1+eps) X + A X), MLP = Linear -> ReLU -> Linear
+    (SpMMv without norm, PAPER.md:2320-2321 class B)."""
+    X = np.asarray(X, dtype=np.float64)
+    Hs = (1.0 + eps) * X + spmm(offsets, cols, X)
+    U = Hs @ W1 + b1
+    Ur = np.maximum(U, 0.0)
+    Z = Ur @ W2 + b2
+    out = np.maximum(Z, 0.0) if relu_out else Z
+    return out, dict(X=X, Hs=Hs, U=U, Ur=Ur, Z=Z, W1=W1, W2=W2, eps=eps, relu_out=relu_out)
+
+
+def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False):
+    A = np.abs if absmode else (lambda t: t)
+    dZ = A(np.asarray(dout, np.float64))
+    if c["relu_out"]:
+        dZ = dZ * (c["Z"] > 0)
+    db2 = dZ.sum(axis=0)
+    dW2 = A(c["Ur"]).T @ dZ
+    dU = (dZ @ A(np.asarray(c["W2"], np.float64)).T) * (c["U"] > 0)
+    db1 = dU.sum(axis=0)
+    dW1 = A(c["Hs"]).T @ dU
+    dHs = dU @ A(np.asarray(c["W1"], np.float64)).T
+    dX = (1.0 + c["eps"]) * dHs + spmm(t_offsets, t_cols, dHs)
+    return {"W1": dW1, "b1": db1, "W2": dW2, "b2": db2, "X": dX}

@@ -70,6 +70,10 @@ class Epilogue(C.Structure):
     ]
 
 
+class EdgeScores(C.Structure):
+    _fields_ = [("s", c_ptr), ("el", c_ptr), ("er", c_ptr), ("slope", C.c_float)]
+
+
 class SpmmPlan(C.Structure):
     _fields_ = [
         ("edges_per_warp", c_i64),
@@ -140,6 +144,32 @@ SIGNATURES = {
         ],
     ),
     "gnn_degree_norm_inplace": (c_int, [c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
+    "gnn_sddmm": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr,
+         c_ptr],
+    ),
+    "gnn_edge_softmax_workspace": (c_sz, [C.POINTER(SpmmPlan), c_i64]),
+    "gnn_edge_softmax_fwd": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, C.POINTER(EdgeScores), c_ptr, c_ptr,
+         c_sz, c_ptr],
+    ),
+    "gnn_edge_softmax_bwd": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, C.POINTER(EdgeScores),
+         c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_gat_attn_proj": (
+        c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "gnn_gat_attn_proj_bwd_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_gat_attn_proj_bwd": (
+        c_int,
+        [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr,
+         c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_head_mean": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
+    "gnn_head_mean_bwd": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "gnn_gemm_workspace": (c_sz, [c_i64, c_i64, c_i64, c_int]),
     "gnn_gemm": (
         c_int,

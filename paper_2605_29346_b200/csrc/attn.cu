@@ -1,0 +1,810 @@
+// SDDMM, edge-softmax and the GAT per-vertex helpers (GraphPy class-A
+// kernels; GAT math of SURVEY.md Appendix A.6).
+//
+// Work decomposition: every edge kernel reuses the SpMM plan of the operand
+// (gnn_spmm_plan_t): the nnz range is cut into chunks of P edges, one warp per
+// chunk, chunk_row[w] = row of the chunk's first edge.  A warp walks the rows
+// of its chunk in order, so the row side of every edge (X[row] for SDDMM,
+// er[row] for GAT scores, the softmax row statistics) is loaded once per row
+// piece and reused across its edges ("row-run reuse") —
+// there is no materialised COO row array.
+//
+// Edge-softmax is a per-row reduction over edges; rows that span several
+// chunks (the power-law mega rows) leave per-chunk partial statistics in
+// workspace slots, a finalize kernel combines them in a fixed order, and an
+// apply kernel normalises those rows' edges.  Rows inside one chunk are
+// finished in the first kernel.  Every summation order is fixed: results are
+// deterministic run to run, no atomics.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace gnn {
+namespace {
+
+constexpr float kNegInf = -INFINITY;
+
+unsigned grid_warps(int64_t nwarps, int threads) {
+  return (unsigned)ceil_div(nwarps * 32, threads);
+}
+unsigned grid_1d_a(int64_t n, int threads) {
+  int64_t b = ceil_div(n > 0 ? n : 1, threads);
+  int64_t cap = (int64_t)sm_count() * 32;
+  return (unsigned)(b < cap ? b : cap);
+}
+bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Walks the rows of one chunk [e0,e1): row r with bounds [rs,re); offsets are
+// fetched 32 row-ends per batched load and broadcast by shuffle.
+struct RowWalk {
+  const int64_t *off;
+  int64_t R, r, rs, re, obuf;
+  int bi;
+  __device__ __forceinline__ RowWalk(const int64_t *o, int64_t nrows, int64_t r0) : off(o), R(nrows) {
+    r = r0;
+    rs = off[r];
+    obuf = off[min(r + 1 + (int64_t)lane_id(), R)];
+    bi = 0;
+    re = shfl64(obuf, 0);
+  }
+  static __device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+    int lo = __shfl_sync(kFull, (int)(v & 0xffffffff), src);
+    int hi = __shfl_sync(kFull, (int)(v >> 32), src);
+    return ((int64_t)hi << 32) | (uint32_t)lo;
+  }
+  // advance to the next row (whole warp)
+  __device__ __forceinline__ void next() {
+    ++r;
+    rs = re;
+    if (++bi == 32) {
+      obuf = off[min(r + 1 + (int64_t)lane_id(), R)];
+      bi = 0;
+    }
+    re = shfl64(obuf, bi);
+  }
+};
+
+// ------------------------------------------------------------------ SDDMM
+struct SddmmArgs {
+  int64_t R, nnz, P, nwarps;
+  const int64_t *offsets;
+  const int32_t *cols;
+  const int32_t *chunk_row;
+  int H;
+  int64_t F, K;
+  const float *X;  // row side  [R, ldx]
+  int64_t ldx;
+  const float *Y;  // col side  [C, ldy]
+  int64_t ldy;
+  float *out;      // [nnz, H]
+};
+
+// Fast path: G lanes per edge, each lane owns float4 columns q = v*G + gl
+// (v < VPL); LPH = F/4 lanes per head (power of two, <= G) reduce a head's dot
+// by xor shuffles inside the group.  NG = 32/G edges per warp step, U steps
+// unrolled so U gathers per lane are in flight.
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) sddmm_vec_kernel(SddmmArgs a, int LPH) {
+  constexpr int NG = 32 / G;
+  constexpr int U = VPL >= 2 ? 2 : 4;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (g * G));
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  int64_t col[VPL];
+  bool cv[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    col[v] = (int64_t)(v * G + gl) * 4;
+    cv[v] = col[v] < a.K;
+    if (!cv[v]) col[v] = 0;
+  }
+  int64_t r = a.chunk_row[w];
+  int64_t re = a.offsets[r + 1];
+  int64_t xr = -1;
+  float4 xv[VPL];
+  for (int64_t eb = e0 + g; eb < e1; eb += (int64_t)NG * U) {
+    int32_t c[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = eb + (int64_t)u * NG;
+      ok[u] = e < e1;
+      c[u] = ok[u] ? __ldg(a.cols + e) : 0;
+    }
+    float4 yv[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        yv[u][v] = ok[u] ? ldg_f4(a.Y + (int64_t)c[u] * a.ldy + col[v]) : make_float4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) break;  // group-uniform
+      const int64_t e = eb + (int64_t)u * NG;
+      while (e >= re) {
+        ++r;
+        re = a.offsets[r + 1];
+      }
+      if (r != xr) {
+        xr = r;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) xv[v] = ldg_f4(a.X + r * a.ldx + col[v]);
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        float p = xv[v].x * yv[u][v].x;
+        p = fmaf(xv[v].y, yv[u][v].y, p);
+        p = fmaf(xv[v].z, yv[u][v].z, p);
+        p = fmaf(xv[v].w, yv[u][v].w, p);
+        for (int o = 1; o < LPH; o <<= 1) p += __shfl_xor_sync(gmask, p, o);
+        if (cv[v] && (gl & (LPH - 1)) == 0) a.out[e * a.H + col[v] / a.F] = p;
+      }
+    }
+  }
+}
+
+// Generic path (any F, K): one lane per (edge), loop heads and features.
+__global__ void __launch_bounds__(256) sddmm_scalar_kernel(SddmmArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int lane = (int)lane_id();
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  int64_t r = a.chunk_row[w];
+  int64_t re = a.offsets[r + 1];
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    while (e >= re) {
+      ++r;
+      re = a.offsets[r + 1];
+    }
+    const int64_t c = a.cols[e];
+    const float *x = a.X + r * a.ldx;
+    const float *y = a.Y + c * a.ldy;
+    for (int h = 0; h < a.H; ++h) {
+      float p = 0.f;
+      for (int64_t f = h * a.F; f < (h + 1) * a.F; ++f) p = fmaf(__ldg(x + f), __ldg(y + f), p);
+      a.out[e * a.H + h] = p;
+    }
+  }
+}
+
+// ------------------------------------------------------------ edge softmax
+// Scores: either given (s[e*H+h]) or the GAT score computed on the fly,
+// LeakyReLU(el[col*H+h] + er[row*H+h], slope).
+struct SoftmaxArgs {
+  int64_t R, nnz, P, nwarps;
+  const int64_t *offsets;
+  const int32_t *cols;
+  const int32_t *chunk_row;
+  const int32_t *chunk_split;
+  const int32_t *split_rows;
+  int64_t num_split;
+  int H;
+  const float *s;
+  const float *el, *er;
+  float slope;
+  // forward
+  float *alpha;
+  // backward
+  const float *alpha_in;
+  const float *dalpha;
+  float *ds;
+  // workspace
+  float *slots;  // [nwarps][2][2*H]
+  float *stat;   // [num_split][2*H]
+};
+
+template <int HM>
+struct Scores {
+  float v[HM];
+};
+
+// Load the H scores of edge e (row r): GAT mode recomputes them from el/er.
+template <int HM, bool GAT>
+__device__ __forceinline__ void load_scores(const SoftmaxArgs &a, int64_t e, const float (&erow)[HM],
+                                            float (&s)[HM]) {
+  if constexpr (GAT) {
+    const int64_t c = a.cols[e];
+    if (HM == 4 && a.H == 4) {
+      const float4 l = ldg_f4(a.el + c * 4);
+      s[0] = l.x + erow[0];
+      s[1] = l.y + erow[1];
+      s[2] = l.z + erow[2];
+      s[3] = l.w + erow[3];
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h) s[h] = h < a.H ? __ldg(a.el + c * a.H + h) + erow[h] : 0.f;
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) s[h] = s[h] > 0.f ? s[h] : a.slope * s[h];
+  } else {
+    if (HM == 4 && a.H == 4) {
+      const float4 l = *reinterpret_cast<const float4 *>(a.s + e * 4);
+      s[0] = l.x;
+      s[1] = l.y;
+      s[2] = l.z;
+      s[3] = l.w;
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h) s[h] = h < a.H ? a.s[e * a.H + h] : 0.f;
+    }
+  }
+}
+
+template <int HM, bool GAT>
+__device__ __forceinline__ void load_erow(const SoftmaxArgs &a, int64_t r, float (&erow)[HM]) {
+#pragma unroll
+  for (int h = 0; h < HM; ++h) erow[h] = (GAT && h < a.H) ? __ldg(a.er + r * a.H + h) : 0.f;
+}
+
+__device__ __forceinline__ float rescale(float mo, float mn) {
+  return mo == kNegInf ? 0.f : expf(mo - mn);
+}
+// (m,l) <- combine((m,l), (m2,l2)): online-softmax merge, fixed operand order.
+__device__ __forceinline__ void ml_merge(float &m, float &l, float m2, float l2) {
+  const float mn = fmaxf(m, m2);
+  l = l * rescale(m, mn) + l2 * rescale(m2, mn);
+  m = mn;
+}
+
+template <int HM>
+__device__ __forceinline__ void warp_ml_reduce(float (&m)[HM], float (&l)[HM]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+      const float m2 = __shfl_xor_sync(kFull, m[h], o);
+      const float l2 = __shfl_xor_sync(kFull, l[h], o);
+      ml_merge(m[h], l[h], m2, l2);
+    }
+}
+
+template <int HM>
+__device__ __forceinline__ void warp_sum_reduce(float (&t)[HM]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int h = 0; h < HM; ++h) t[h] += __shfl_xor_sync(kFull, t[h], o);
+}
+
+// Forward statistics + normalisation of one row piece [lo,hi) of row r.
+template <int HM, bool GAT>
+__device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, int64_t lo, int64_t hi,
+                                              bool whole, float *slot) {
+  const int lane = (int)lane_id();
+  float erow[HM];
+  load_erow<HM, GAT>(a, r, erow);
+  float m[HM], l[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) {
+    m[h] = kNegInf;
+    l[h] = 0.f;
+  }
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    float s[HM];
+    load_scores<HM, GAT>(a, e, erow, s);
+#pragma unroll
+    for (int h = 0; h < HM; ++h) ml_merge(m[h], l[h], s[h], 1.f);
+  }
+  warp_ml_reduce<HM>(m, l);
+  if (!whole) {
+    if (lane == 0)
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) {
+          slot[h] = m[h];
+          slot[a.H + h] = l[h];
+        }
+    return;
+  }
+  float inv[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) inv[h] = 1.f / l[h];
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    float s[HM];
+    load_scores<HM, GAT>(a, e, erow, s);
+    if (HM == 4 && a.H == 4) {
+      *reinterpret_cast<float4 *>(a.alpha + e * 4) =
+          make_float4(expf(s[0] - m[0]) * inv[0], expf(s[1] - m[1]) * inv[1],
+                      expf(s[2] - m[2]) * inv[2], expf(s[3] - m[3]) * inv[3]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) a.alpha[e * a.H + h] = expf(s[h] - m[h]) * inv[h];
+    }
+  }
+}
+
+// Backward of one row piece: S = sum alpha*dalpha; whole rows write
+// ds = alpha (dalpha - S) (* LeakyReLU'(pre) in GAT mode).
+template <int HM, bool GAT>
+__device__ __forceinline__ void softmax_bwd_apply(const SoftmaxArgs &a, int64_t r, int64_t lo,
+                                                  int64_t hi, const float (&S)[HM]) {
+  const int lane = (int)lane_id();
+  float erow[HM];
+  load_erow<HM, GAT>(a, r, erow);
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    float pre[HM];
+    if constexpr (GAT) {
+      const int64_t c = a.cols[e];
+#pragma unroll
+      for (int h = 0; h < HM; ++h) pre[h] = h < a.H ? __ldg(a.el + c * a.H + h) + erow[h] : 0.f;
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) {
+        const float al = a.alpha_in[e * a.H + h];
+        const float da = a.dalpha[e * a.H + h];
+        float d = al * (da - S[h]);
+        if constexpr (GAT) d = pre[h] > 0.f ? d : a.slope * d;
+        a.ds[e * a.H + h] = d;
+      }
+  }
+}
+
+template <int HM, bool GAT>
+__device__ __forceinline__ void softmax_bwd_piece(const SoftmaxArgs &a, int64_t r, int64_t lo,
+                                                  int64_t hi, bool whole, float *slot) {
+  const int lane = (int)lane_id();
+  float S[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) S[h] = 0.f;
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) S[h] = fmaf(a.alpha_in[e * a.H + h], a.dalpha[e * a.H + h], S[h]);
+  }
+  warp_sum_reduce<HM>(S);
+  if (!whole) {
+    if (lane == 0)
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) slot[h] = S[h];
+    return;
+  }
+  softmax_bwd_apply<HM, GAT>(a, r, lo, hi, S);
+}
+
+// Kernel 1: one warp per chunk; whole rows finished, split-row pieces leave
+// partials in slot[w][0] (carry-in piece) / slot[w][1] (trailing piece).
+template <int HM, bool GAT, bool BWD>
+__global__ void __launch_bounds__(256) softmax_rows_kernel(SoftmaxArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
+  while (true) {
+    const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if (hi > lo) {
+      const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
+      float *slot = a.slots + (w * 2 + (carry ? 0 : 1)) * 2 * a.H;
+      if (BWD)
+        softmax_bwd_piece<HM, GAT>(a, rw.r, lo, hi, !(carry || trail), slot);
+      else
+        softmax_piece<HM, GAT>(a, rw.r, lo, hi, !(carry || trail), slot);
+    }
+    if (rw.re >= e1 || rw.r + 1 >= a.R) break;
+    rw.next();
+  }
+}
+
+// Kernel 2: one warp per split row; partial j of row (chunks wa..wb) is
+// slot[wa][1] for j = 0 and slot[wa+j][0] for j >= 1 (same convention as the
+// SpMM).  Lane-strided merge in j order, then a fixed xor tree.
+template <int HM, bool BWD>
+__global__ void __launch_bounds__(256) softmax_split_finalize_kernel(SoftmaxArgs a) {
+  const int64_t si = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (si >= a.num_split) return;
+  const int lane = (int)lane_id();
+  const int64_t r = a.split_rows[si];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  const int64_t np = wb - wa + 1;
+  float m[HM], l[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) {
+    m[h] = BWD ? 0.f : kNegInf;
+    l[h] = 0.f;
+  }
+  for (int64_t j = lane; j < np; j += 32) {
+    const float *slot = a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * 2 * a.H;
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) {
+        if (BWD)
+          m[h] += slot[h];
+        else
+          ml_merge(m[h], l[h], slot[h], slot[a.H + h]);
+      }
+  }
+  if (BWD)
+    warp_sum_reduce<HM>(m);
+  else
+    warp_ml_reduce<HM>(m, l);
+  if (lane == 0)
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) {
+        a.stat[si * 2 * a.H + h] = m[h];
+        a.stat[si * 2 * a.H + a.H + h] = l[h];
+      }
+}
+
+// Kernel 3: one warp per chunk; normalises the chunk's split-row pieces.
+template <int HM, bool GAT, bool BWD>
+__global__ void __launch_bounds__(256) softmax_split_apply_kernel(SoftmaxArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  const int lane = (int)lane_id();
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    const int32_t si = a.chunk_split[2 * w + which];
+    if (si < 0) continue;
+    const int64_t r = a.split_rows[si];
+    const int64_t lo = max(a.offsets[r], e0), hi = min(a.offsets[r + 1], e1);
+    float m[HM], l[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+      m[h] = h < a.H ? a.stat[si * 2 * a.H + h] : 0.f;
+      l[h] = h < a.H ? a.stat[si * 2 * a.H + a.H + h] : 1.f;
+    }
+    if (BWD) {
+      softmax_bwd_apply<HM, GAT>(a, r, lo, hi, m);
+      continue;
+    }
+    float erow[HM];
+    load_erow<HM, GAT>(a, r, erow);
+    float inv[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) inv[h] = 1.f / l[h];
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+      float s[HM];
+      load_scores<HM, GAT>(a, e, erow, s);
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) a.alpha[e * a.H + h] = expf(s[h] - m[h]) * inv[h];
+    }
+  }
+}
+
+template <int HM, bool GAT, bool BWD>
+int launch_softmax(const SoftmaxArgs &a, cudaStream_t st) {
+  if (a.nwarps > 0) {
+    softmax_rows_kernel<HM, GAT, BWD><<<grid_warps(a.nwarps, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_split > 0) {
+    softmax_split_finalize_kernel<HM, BWD><<<grid_warps(a.num_split, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+    softmax_split_apply_kernel<HM, GAT, BWD><<<grid_warps(a.nwarps, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+template <bool GAT, bool BWD>
+int dispatch_softmax(const SoftmaxArgs &a, cudaStream_t st) {
+  if (a.H == 1) return launch_softmax<1, GAT, BWD>(a, st);
+  if (a.H <= 4) return launch_softmax<4, GAT, BWD>(a, st);
+  if (a.H <= 8) return launch_softmax<8, GAT, BWD>(a, st);
+  return launch_softmax<16, GAT, BWD>(a, st);
+}
+
+size_t softmax_ws_layout(const gnn_spmm_plan_t *plan, int64_t H, size_t *o_stat) {
+  WsCounter c;
+  c.take<float>(plan->num_warps * 2 * 2 * H);
+  *o_stat = align_up(c.used, 256);
+  c.take<float>(plan->num_split * 2 * H);
+  return c.used + 256;
+}
+
+int softmax_common(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                   const gnn_edge_scores_t *sc, void *ws, size_t ws_bytes, SoftmaxArgs &a) {
+  if (!A || !plan || heads <= 0 || heads > 16 || !A->offsets || (A->nnz > 0 && !A->cols))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_edge_softmax_workspace(plan, heads)) return GNN_ERR_WORKSPACE;
+  a = SoftmaxArgs{};
+  a.R = A->num_rows;
+  a.nnz = A->nnz;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.offsets = A->offsets;
+  a.cols = A->cols;
+  a.chunk_row = plan->chunk_row;
+  a.chunk_split = plan->chunk_split;
+  a.split_rows = plan->split_rows;
+  a.num_split = plan->num_split;
+  a.H = (int)heads;
+  if (sc) {
+    a.s = sc->s;
+    a.el = sc->el;
+    a.er = sc->er;
+    a.slope = sc->slope;
+  }
+  size_t o_stat;
+  softmax_ws_layout(plan, heads, &o_stat);
+  a.slots = static_cast<float *>(ws);
+  a.stat = reinterpret_cast<float *>(static_cast<char *>(ws) + o_stat);
+  return GNN_OK;
+}
+
+// -------------------------------------------------- GAT per-vertex helpers
+// el[v,h] = <Wh[v,h,:], a_l[h,:]>, er likewise: one thread per (v,h).
+__global__ void attn_proj_kernel(int64_t V, int H, int64_t F, const float *__restrict__ Wh,
+                                 int64_t ldw, const float *__restrict__ al,
+                                 const float *__restrict__ ar, float *el, float *er) {
+  const int64_t total = V * H;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / H;
+    const int h = (int)(t % H);
+    const float *x = Wh + v * ldw + h * F;
+    float sl = 0.f, sr = 0.f;
+    for (int64_t f = 0; f < F; ++f) {
+      const float xv = __ldg(x + f);
+      sl = fmaf(xv, __ldg(al + h * F + f), sl);
+      sr = fmaf(xv, __ldg(ar + h * F + f), sr);
+    }
+    el[t] = sl;
+    er[t] = sr;
+  }
+}
+
+// dWh[v,h,f] += del[v,h] a_l[h,f] + der[v,h] a_r[h,f]
+__global__ void attn_proj_bwd_dwh_kernel(int64_t V, int H, int64_t F, const float *__restrict__ del,
+                                         const float *__restrict__ der, const float *__restrict__ al,
+                                         const float *__restrict__ ar, float *dWh, int64_t ldd) {
+  const int64_t K = (int64_t)H * F;
+  const int64_t total = V * K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / K, k = t % K;
+    const int64_t h = k / F;
+    float d = dWh[v * ldd + k];
+    d = fmaf(del[v * H + h], al[k], d);
+    d = fmaf(der[v * H + h], ar[k], d);
+    dWh[v * ldd + k] = d;
+  }
+}
+
+// da_l[k] = sum_v Wh[v,k] del[v,k/F] (and da_r): block partials over vertex
+// ranges (fixed order), then a fixed-order sum over blocks.
+constexpr int kProjBlocks = 1024;
+__global__ void attn_proj_bwd_da_partial_kernel(int64_t V, int H, int64_t F,
+                                                const float *__restrict__ Wh, int64_t ldw,
+                                                const float *__restrict__ del,
+                                                const float *__restrict__ der, float *part) {
+  const int64_t K = (int64_t)H * F;
+  const int64_t per = ceil_div(V, gridDim.x);
+  const int64_t v0 = blockIdx.x * per, v1 = min(v0 + per, V);
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const int64_t h = k / F;
+    float sl = 0.f, sr = 0.f;
+    for (int64_t v = v0; v < v1; ++v) {
+      const float x = __ldg(Wh + v * ldw + k);
+      sl = fmaf(x, __ldg(del + v * H + h), sl);
+      sr = fmaf(x, __ldg(der + v * H + h), sr);
+    }
+    part[(int64_t)blockIdx.x * 2 * K + k] = sl;
+    part[(int64_t)blockIdx.x * 2 * K + K + k] = sr;
+  }
+}
+__global__ void attn_proj_bwd_da_final_kernel(int64_t K, int nb, const float *__restrict__ part,
+                                              float *dal, float *dar) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 2 * K;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += part[(int64_t)b * 2 * K + k];
+    if (k < K)
+      dal[k] = s;
+    else
+      dar[k - K] = s;
+  }
+}
+
+// out[v,f] = (1/H) sum_h Y[v,h*F+f] (+ bias[f]);  backward: dY[v,h*F+f] = dout[v,f]/H
+__global__ void head_mean_kernel(int64_t V, int H, int64_t F, const float *__restrict__ Y,
+                                 int64_t ldy, const float *__restrict__ bias, float *out,
+                                 int64_t ldo) {
+  const int64_t total = V * F;
+  const float inv = 1.f / (float)H;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / F, f = t % F;
+    float s = 0.f;
+    for (int h = 0; h < H; ++h) s += Y[v * ldy + h * F + f];
+    s *= inv;
+    if (bias) s += bias[f];
+    out[v * ldo + f] = s;
+  }
+}
+__global__ void head_mean_bwd_kernel(int64_t V, int H, int64_t F, const float *__restrict__ dout,
+                                     int64_t ldo, float *dY, int64_t ldy) {
+  const int64_t K = (int64_t)H * F;
+  const int64_t total = V * K;
+  const float inv = 1.f / (float)H;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / K, k = t % K;
+    dY[v * ldy + k] = dout[v * ldo + k % F] * inv;
+  }
+}
+
+}  // namespace
+}  // namespace gnn
+
+using namespace gnn;
+
+extern "C" {
+
+int gnn_sddmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads, const float *X,
+              int64_t ldx, const float *Y, int64_t ldy, int64_t K, float *out,
+              gnn_stream_t stream) {
+  if (!A || !plan || heads <= 0 || K <= 0 || K % heads != 0 || !A->offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz > 0 && (!A->cols || !X || !Y || !out || ldx < K || ldy < K))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  SddmmArgs a{};
+  a.R = A->num_rows;
+  a.nnz = A->nnz;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.offsets = A->offsets;
+  a.cols = A->cols;
+  a.chunk_row = plan->chunk_row;
+  a.H = (int)heads;
+  a.F = K / heads;
+  a.K = K;
+  a.X = X;
+  a.ldx = ldx;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.out = out;
+  const int64_t q = K / 4;  // float4 columns
+  int G = 1;
+  while (G < q && G < 32) G <<= 1;
+  const int64_t lph = a.F / 4;
+  const bool lph_pow2 = lph > 0 && (lph & (lph - 1)) == 0;
+  const bool vec = K % 4 == 0 && a.F % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && al16(X) &&
+                   al16(Y) && lph_pow2 && lph <= G && ceil_div(q, G) <= 4;
+  const unsigned grid = grid_warps(a.nwarps, 256);
+  if (vec) {
+    const int LPH = (int)lph;
+    const int VPL = (int)ceil_div(q, G);
+    switch (G) {
+      case 1: sddmm_vec_kernel<1, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 2: sddmm_vec_kernel<2, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 4: sddmm_vec_kernel<4, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 8: sddmm_vec_kernel<8, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 16: sddmm_vec_kernel<16, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      default:
+        if (VPL == 1)
+          sddmm_vec_kernel<32, 1><<<grid, 256, 0, st>>>(a, LPH);
+        else if (VPL == 2)
+          sddmm_vec_kernel<32, 2><<<grid, 256, 0, st>>>(a, LPH);
+        else
+          sddmm_vec_kernel<32, 4><<<grid, 256, 0, st>>>(a, LPH);
+    }
+  } else {
+    sddmm_scalar_kernel<<<grid, 256, 0, st>>>(a);
+  }
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_edge_softmax_workspace(const gnn_spmm_plan_t *plan, int64_t heads) {
+  if (!plan || heads <= 0) return 0;
+  size_t o;
+  return softmax_ws_layout(plan, heads, &o);
+}
+
+int gnn_edge_softmax_fwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const gnn_edge_scores_t *sc, float *alpha, void *ws, size_t ws_bytes,
+                         gnn_stream_t stream) {
+  SoftmaxArgs a;
+  GNN_TRY(softmax_common(A, plan, heads, sc, ws, ws_bytes, a));
+  if (!sc) return GNN_ERR_INVALID_ARGUMENT;
+  const bool gat = sc->s == nullptr;
+  if (A->nnz > 0 && (!alpha || (gat && (!sc->el || !sc->er)))) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz == 0) return GNN_OK;
+  if (heads == 4 && (!al16(alpha) || (gat ? !al16(sc->el) : !al16(sc->s))))
+    return GNN_ERR_INVALID_ARGUMENT;
+  a.alpha = alpha;
+  cudaStream_t st = as_stream(stream);
+  return gat ? dispatch_softmax<true, false>(a, st) : dispatch_softmax<false, false>(a, st);
+}
+
+int gnn_edge_softmax_bwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const float *alpha, const float *dalpha, const gnn_edge_scores_t *sc,
+                         float *ds, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  SoftmaxArgs a;
+  GNN_TRY(softmax_common(A, plan, heads, sc, ws, ws_bytes, a));
+  const bool gat = sc && sc->el;
+  if (A->nnz > 0 && (!alpha || !dalpha || !ds || (gat && !sc->er))) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz == 0) return GNN_OK;
+  a.alpha_in = alpha;
+  a.dalpha = dalpha;
+  a.ds = ds;
+  cudaStream_t st = as_stream(stream);
+  return gat ? dispatch_softmax<true, true>(a, st) : dispatch_softmax<false, true>(a, st);
+}
+
+int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,
+                      const float *a_l, const float *a_r, float *el, float *er,
+                      gnn_stream_t stream) {
+  if (V < 0 || heads <= 0 || F <= 0 || ldw < heads * F) return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!Wh || !a_l || !a_r || !el || !er) return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  attn_proj_kernel<<<grid_1d_a(V * heads, 256), 256, 0, st>>>(V, (int)heads, F, Wh, ldw, a_l, a_r,
+                                                              el, er);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_gat_attn_proj_bwd_workspace(int64_t heads, int64_t F) {
+  return (size_t)kProjBlocks * 2 * heads * F * sizeof(float) + 256;
+}
+
+int gnn_gat_attn_proj_bwd(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,
+                          const float *a_l, const float *a_r, const float *del, const float *der,
+                          float *dWh, int64_t ldd, float *da_l, float *da_r, void *ws,
+                          size_t ws_bytes, gnn_stream_t stream) {
+  if (V < 0 || heads <= 0 || F <= 0 || ldw < heads * F || ldd < heads * F)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (!a_l || !a_r || !da_l || !da_r) return GNN_ERR_INVALID_ARGUMENT;
+  if (V > 0 && (!Wh || !del || !der || !dWh)) return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_gat_attn_proj_bwd_workspace(heads, F)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int64_t K = heads * F;
+  float *part = static_cast<float *>(ws);
+  const int nb = (int)(V < kProjBlocks ? (V > 0 ? V : 1) : kProjBlocks);
+  if (V > 0) {
+    // partials read Wh before dWh is updated (they may not alias anyway)
+    attn_proj_bwd_da_partial_kernel<<<nb, 128, 0, st>>>(V, (int)heads, F, Wh, ldw, del, der, part);
+    GNN_LAUNCH_CHECK();
+    attn_proj_bwd_dwh_kernel<<<grid_1d_a(V * K, 256), 256, 0, st>>>(V, (int)heads, F, del, der,
+                                                                    a_l, a_r, dWh, ldd);
+    GNN_LAUNCH_CHECK();
+  } else {
+    GNN_CUDA_TRY(cudaMemsetAsync(part, 0, sizeof(float) * 2 * K, st));
+  }
+  attn_proj_bwd_da_final_kernel<<<(unsigned)ceil_div(2 * K, 256), 256, 0, st>>>(K, nb, part, da_l,
+                                                                                da_r);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_head_mean(int64_t V, int64_t heads, int64_t F, const float *Y, int64_t ldy,
+                  const float *bias, float *out, int64_t ldo, gnn_stream_t stream) {
+  if (V < 0 || heads <= 0 || F <= 0 || ldy < heads * F || ldo < F) return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!Y || !out) return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  head_mean_kernel<<<grid_1d_a(V * F, 256), 256, 0, st>>>(V, (int)heads, F, Y, ldy, bias, out, ldo);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_head_mean_bwd(int64_t V, int64_t heads, int64_t F, const float *dout, int64_t ldo,
+                      float *dY, int64_t ldy, gnn_stream_t stream) {
+  if (V < 0 || heads <= 0 || F <= 0 || ldy < heads * F || ldo < F) return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!dY || !dout) return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  head_mean_bwd_kernel<<<grid_1d_a(V * heads * F, 256), 256, 0, st>>>(V, (int)heads, F, dout, ldo,
+                                                                       dY, ldy);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -275,6 +275,15 @@ int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int 
   cudaStream_t st = as_stream(stream);
   if (gemm_tc_supported(M, N, Kd, A, lda, trans_a))
     return gemm_tc(M, N, Kd, A, lda, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes, st);
+  if (N > 128 && gemm_tc_supported(M, 128, Kd, A, lda, trans_a)) {
+    // wide outputs (e.g. GAT's heads x classes): 128-column slabs, A re-streamed per slab
+    for (int64_t n0 = 0; n0 < N; n0 += 128) {
+      const int64_t nb = N - n0 < 128 ? N - n0 : 128;
+      GNN_TRY(gemm_tc(M, nb, Kd, A, lda, trans_b ? B + n0 * ldb : B + n0, ldb, trans_b, C + n0,
+                      ldc, bias ? bias + n0 : nullptr, relu, ws, ws_bytes, st));
+    }
+    return GNN_OK;
+  }
   if (trans_a && !trans_b && !bias && !relu && gemm_tc_tn_supported(M, N, Kd, A, lda, B, ldb))
     return gemm_tc_tn(M, N, Kd, A, lda, B, ldb, C, ldc, ws, ws_bytes, st);
   return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,

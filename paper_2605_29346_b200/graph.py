@@ -104,7 +104,9 @@ class SparseOperand:
         vv = vals if vals is not None else self.vals
         v.vals = vv.data_ptr() if vv is not None else None
         ee = eid if eid is not None else self.eid
-        v.eid = ee.data_ptr() if ee is not None else None
+        # the edge-ID indirection only applies to edge values (SpMMve^T); a
+        # topology-only SpMMv over a CSC that happens to carry eid ignores it
+        v.eid = ee.data_ptr() if (ee is not None and vv is not None) else None
         v.deg_offsets = self.deg_offsets.data_ptr() if self.deg_offsets is not None else None
         return v
 

@@ -153,3 +153,127 @@ class HeadCall:
             self.deg.data_ptr() if self.deg is not None else None, self.dP.data_ptr(),
             self.dP.stride(0), self.dW.data_ptr(), self.db.data_ptr(), self.loss.data_ptr(),
             self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "gcn_head")
+
+
+class ColsumCall:
+    def __init__(self, X, out):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.M, self.N = X.shape
+        self.X, self.out = X, out
+        self.ws = _lib.workspace(self.lib.gnn_colsum_workspace(self.M, self.N), self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_colsum(self.M, self.N, self.X.data_ptr(), self.X.stride(0),
+                                       self.out.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                       _lib.stream_handle(self.dev)), "colsum")
+
+
+class SddmmCall:
+    """out[e,h] = <X[row_e,h,:], Y[col_e,h,:]> over op's edges."""
+
+    def __init__(self, op: SparseOperand, X, Y, out, heads=1):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.K = int(X.shape[1])
+        self.view, self.plan = op.view(), op.plan()
+        self.X, self.Y, self.out, self.heads, self._op = X, Y, out, heads, op
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_sddmm(C.byref(self.view), C.byref(self.plan), self.heads,
+                                      self.X.data_ptr(), self.X.stride(0), self.Y.data_ptr(),
+                                      self.Y.stride(0), self.K, self.out.data_ptr(),
+                                      _lib.stream_handle(self.dev)), "sddmm")
+
+
+class EdgeSoftmaxCall:
+    """Forward (alpha from s, or from GAT el/er) or backward (ds from alpha,
+    dalpha[, GAT el/er]) edge softmax over op's rows."""
+
+    def __init__(self, op: SparseOperand, heads, out, *, s=None, el=None, er=None, slope=0.2,
+                 backward=False, alpha=None, dalpha=None):
+        self.lib = _lib.lib()
+        self.dev = out.device
+        self.view, self.plan = op.view(), op.plan()
+        self.heads, self.out, self.backward = heads, out, backward
+        self.sc = _lib.EdgeScores()
+        self.sc.s = s.data_ptr() if s is not None else None
+        self.sc.el = el.data_ptr() if el is not None else None
+        self.sc.er = er.data_ptr() if er is not None else None
+        self.sc.slope = float(slope)
+        self.alpha, self.dalpha = alpha, dalpha
+        self._keep = (op, s, el, er)
+        self.ws = _lib.workspace(self.lib.gnn_edge_softmax_workspace(C.byref(self.plan), heads),
+                                 self.dev)
+
+    def __call__(self):
+        st = _lib.stream_handle(self.dev)
+        if self.backward:
+            _lib.check(self.lib.gnn_edge_softmax_bwd(
+                C.byref(self.view), C.byref(self.plan), self.heads, self.alpha.data_ptr(),
+                self.dalpha.data_ptr(), C.byref(self.sc), self.out.data_ptr(),
+                self.ws.data_ptr(), self.ws.numel(), st), "edge_softmax backward")
+        else:
+            _lib.check(self.lib.gnn_edge_softmax_fwd(
+                C.byref(self.view), C.byref(self.plan), self.heads, C.byref(self.sc),
+                self.out.data_ptr(), self.ws.data_ptr(), self.ws.numel(), st), "edge_softmax")
+
+
+class AttnProjCall:
+    def __init__(self, Wh, a_l, a_r, el, er, heads):
+        self.lib = _lib.lib()
+        self.dev = Wh.device
+        self.V = int(Wh.shape[0])
+        self.H = heads
+        self.F = int(a_l.numel()) // heads
+        self.Wh, self.a_l, self.a_r, self.el, self.er = Wh, a_l, a_r, el, er
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_gat_attn_proj(self.V, self.H, self.F, self.Wh.data_ptr(),
+                                              self.Wh.stride(0), self.a_l.data_ptr(),
+                                              self.a_r.data_ptr(), self.el.data_ptr(),
+                                              self.er.data_ptr(), _lib.stream_handle(self.dev)),
+                   "gat attn_proj")
+
+
+class AttnProjBwdCall:
+    def __init__(self, Wh, a_l, a_r, del_, der, dWh, da_l, da_r, heads):
+        self.lib = _lib.lib()
+        self.dev = Wh.device
+        self.V = int(Wh.shape[0])
+        self.H = heads
+        self.F = int(a_l.numel()) // heads
+        self.t = (Wh, a_l, a_r, del_, der, dWh, da_l, da_r)
+        self.ws = _lib.workspace(self.lib.gnn_gat_attn_proj_bwd_workspace(self.H, self.F),
+                                 self.dev)
+
+    def __call__(self):
+        Wh, a_l, a_r, del_, der, dWh, da_l, da_r = self.t
+        _lib.check(self.lib.gnn_gat_attn_proj_bwd(
+            self.V, self.H, self.F, Wh.data_ptr(), Wh.stride(0), a_l.data_ptr(), a_r.data_ptr(),
+            del_.data_ptr(), der.data_ptr(), dWh.data_ptr(), dWh.stride(0), da_l.data_ptr(),
+            da_r.data_ptr(), self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+            "gat attn_proj backward")
+
+
+class HeadMeanCall:
+    """out[v,f] = mean_h Y[v,h*F+f] (+bias); backward=True: Y <- dout/heads broadcast."""
+
+    def __init__(self, Y, out, heads, F, bias=None, backward=False):
+        self.lib = _lib.lib()
+        self.dev = Y.device
+        self.V = int(Y.shape[0])
+        self.H, self.F = heads, F
+        self.Y, self.out, self.bias, self.backward = Y, out, bias, backward
+
+    def __call__(self):
+        st = _lib.stream_handle(self.dev)
+        if self.backward:
+            _lib.check(self.lib.gnn_head_mean_bwd(self.V, self.H, self.F, self.out.data_ptr(),
+                                                  self.out.stride(0), self.Y.data_ptr(),
+                                                  self.Y.stride(0), st), "head_mean backward")
+        else:
+            _lib.check(self.lib.gnn_head_mean(
+                self.V, self.H, self.F, self.Y.data_ptr(), self.Y.stride(0),
+                self.bias.data_ptr() if self.bias is not None else None, self.out.data_ptr(),
+                self.out.stride(0), st), "head_mean")

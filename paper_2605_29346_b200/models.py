@@ -246,3 +246,190 @@ class GCNTrainer:
 
     def grads(self):
         return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
+
+
+# ===================================================================== GAT
+class _GATAggregate(torch.autograd.Function):
+    """Appendix A.6 aggregation of one GAT layer, given Wh = X W:
+    el/er projections, alpha = edge_softmax(LeakyReLU(el[col] + er[row]))
+    (scores never materialised), Y = SpMMve(A, alpha, Wh) per head, then
+    heads concatenated (+b, optional ReLU — fused in the SpMM epilogue) or
+    averaged (+b).  alpha is the saved state tensor."""
+
+    @staticmethod
+    def forward(ctx, Wh, a_l, a_r, b, g, heads, mean, relu, slope):
+        from .kernels import AttnProjCall, EdgeSoftmaxCall, HeadMeanCall
+
+        Wh = Wh.contiguous()
+        V, K = Wh.shape
+        F = K // heads
+        dev = Wh.device
+        el = torch.empty(V, heads, dtype=torch.float32, device=dev)
+        er = torch.empty_like(el)
+        AttnProjCall(Wh, a_l.contiguous(), a_r.contiguous(), el, er, heads)()
+        A = g.csr()
+        alpha = torch.empty(A.nnz, heads, dtype=torch.float32, device=dev)
+        EdgeSoftmaxCall(A, heads, alpha, el=el, er=er, slope=slope)()
+        if mean:
+            Yc = spmm_raw(A, Wh, heads=heads, vals=alpha)
+            out = torch.empty(V, F, dtype=torch.float32, device=dev)
+            HeadMeanCall(Yc, out, heads, F, bias=b.contiguous())()
+        else:
+            flags = _lib.EPI_BIAS | (_lib.EPI_RELU if relu else 0)
+            out = spmm_raw(A, Wh, heads=heads, vals=alpha, flags=flags, bias=b.contiguous())
+        ctx.save_for_backward(Wh, a_l, a_r, alpha, el, er, out if relu else None)
+        ctx.g, ctx.heads, ctx.mean, ctx.relu, ctx.slope = g, heads, mean, relu, slope
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        from .kernels import (AttnProjBwdCall, ColsumCall, EdgeSoftmaxCall, HeadMeanCall,
+                              MaskNormColsumCall, SddmmCall)
+
+        Wh, a_l, a_r, alpha, el, er, out = ctx.saved_tensors
+        g, H = ctx.g, ctx.heads
+        V, K = Wh.shape
+        F = K // H
+        dev = Wh.device
+        dout = dout.contiguous()
+        db = torch.empty(dout.shape[1], dtype=torch.float32, device=dev)
+        if ctx.relu:
+            dY = torch.empty_like(dout)
+            MaskNormColsumCall(dout, dY, mask=out, colsum=db)()
+        else:
+            ColsumCall(dout, db)()
+            if ctx.mean:
+                dY = torch.empty(V, K, dtype=torch.float32, device=dev)
+                HeadMeanCall(dY, dout, H, F, backward=True)()
+            else:
+                dY = dout
+        A, AT = g.csr(), g.csc(with_eid=True)
+        dWh = spmm_raw(AT, dY, heads=H, vals=alpha, eid=AT.eid)  # SpMMve^T, alpha via edge-ID
+        ds = torch.empty(A.nnz, H, dtype=torch.float32, device=dev)
+        SddmmCall(A, dY, Wh, ds, heads=H)()                       # dalpha
+        EdgeSoftmaxCall(A, H, ds, el=el, er=er, slope=ctx.slope, backward=True, alpha=alpha,
+                        dalpha=ds)()                               # ds (in place)
+        ones = torch.ones(V, H, dtype=torch.float32, device=dev)
+        der = spmm_raw(A, ones, heads=H, vals=ds)
+        del_ = spmm_raw(AT, ones, heads=H, vals=ds, eid=AT.eid)
+        da_l = torch.empty_like(a_l)
+        da_r = torch.empty_like(a_r)
+        AttnProjBwdCall(Wh, a_l, a_r, del_, der, dWh, da_l, da_r, H)()
+        return dWh, da_l, da_r, db, None, None, None, None, None
+
+
+def glorot_heads(heads: int, F: int, seed: int, index: int) -> np.ndarray:
+    """Attention vectors a_l/a_r [heads, F], Glorot-uniform over (F, 1)."""
+    rng = np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(12, index)))
+    a = math.sqrt(6.0 / (F + 1))
+    return rng.uniform(-a, a, (heads, F)).astype(np.float32)
+
+
+class GATConv(torch.nn.Module):
+    """GAT layer (Appendix A.6): Wh = X W; per head h, alpha = softmax over
+    row v's edges of LeakyReLU(<Wh[u,h], a_l[h]> + <Wh[v,h], a_r[h]>);
+    Y_h[v] = sum_e alpha_e Wh[u,h].  ``mean=False`` concatenates heads
+    (+bias, optional fused ReLU), ``mean=True`` averages them (+bias)."""
+
+    def __init__(self, in_feats: int, out_feats: int, heads: int, *, mean: bool = False,
+                 slope: float = 0.2, seed: int = 0, index: int = 0, device=None):
+        super().__init__()
+        self.in_feats, self.out_feats, self.heads = in_feats, out_feats, heads
+        self.mean, self.slope = mean, slope
+        self.weight = torch.nn.Parameter(
+            torch.from_numpy(glorot(in_feats, heads * out_feats, seed, index)).to(device))
+        self.attn_l = torch.nn.Parameter(
+            torch.from_numpy(glorot_heads(heads, out_feats, seed, index + 100)).to(device))
+        self.attn_r = torch.nn.Parameter(
+            torch.from_numpy(glorot_heads(heads, out_feats, seed, index + 200)).to(device))
+        nb = out_feats if mean else heads * out_feats
+        self.bias = torch.nn.Parameter(torch.zeros(nb, device=device))
+
+    def forward(self, g: CsrGraph, X: torch.Tensor, relu: bool = False):
+        if relu and self.mean:
+            raise ValueError("GATConv: fused ReLU is for concatenated (hidden) layers")
+        Wh = linear(X, self.weight)
+        return _GATAggregate.apply(Wh, self.attn_l, self.attn_r, self.bias, g, self.heads,
+                                   self.mean, relu, self.slope)
+
+
+class GAT(torch.nn.Module):
+    """2-layer GAT: hidden layer concatenates heads (ReLU), output averages them."""
+
+    def __init__(self, in_feats: int, hidden: int, classes: int, heads: int = 4, seed: int = 0,
+                 device=None):
+        super().__init__()
+        self.l1 = GATConv(in_feats, hidden, heads, seed=seed, index=0, device=device)
+        self.l2 = GATConv(hidden * heads, classes, heads, mean=True, seed=seed, index=2,
+                          device=device)
+
+    def forward(self, g, X):
+        return self.l2(g, self.l1(g, X, relu=True))
+
+
+# ===================================================================== GIN
+class _GINAggregate(torch.autograd.Function):
+    """U = act(A H + (1+eps) H + b): SpMMv without norm, GIN self term, bias
+    and ReLU all in the SpMM epilogue.  Backward: dH = A^T dU' + (1+eps) dU'."""
+
+    @staticmethod
+    def forward(ctx, H, b, g, eps, relu, coalesced):
+        H = H.contiguous()
+        op = g.csr_coalesced() if coalesced else g.csr()
+        flags = _lib.EPI_SELF | _lib.EPI_BIAS | (_lib.EPI_RELU if relu else 0)
+        U = spmm_raw(op, H, flags=flags, bias=b.contiguous(), self_x=H, self_scale=1.0 + eps)
+        ctx.save_for_backward(U if relu else None)
+        ctx.g, ctx.eps, ctx.relu, ctx.coalesced = g, eps, relu, coalesced
+        return U
+
+    @staticmethod
+    def backward(ctx, dU):
+        from .kernels import ColsumCall, MaskNormColsumCall
+
+        (U,) = ctx.saved_tensors
+        g = ctx.g
+        dU = dU.contiguous()
+        db = torch.empty(dU.shape[1], dtype=torch.float32, device=dU.device)
+        if ctx.relu:
+            dUm = torch.empty_like(dU)
+            MaskNormColsumCall(dU, dUm, mask=U, colsum=db)()
+        else:
+            ColsumCall(dU, db)()
+            dUm = dU
+        op = g.csc_coalesced() if ctx.coalesced else g.csc()
+        dH = spmm_raw(op, dUm, flags=_lib.EPI_SELF, self_x=dUm, self_scale=1.0 + ctx.eps)
+        return dH, db, None, None, None, None
+
+
+class GINConv(torch.nn.Module):
+    """GIN layer (Appendix A.5): Z = MLP((1+eps) X + A X), MLP = Linear ->
+    ReLU -> Linear.  By linearity the first Linear runs before the
+    aggregation, so the SpMM works at the hidden width:
+    ((1+eps) X + A X) W1 = (1+eps) X W1 + A (X W1)."""
+
+    def __init__(self, in_feats: int, hidden: int, out_feats: int, eps: float = 0.0, seed: int = 0,
+                 index: int = 0, device=None):
+        super().__init__()
+        self.eps = float(eps)
+        self.w1 = torch.nn.Parameter(torch.from_numpy(glorot(in_feats, hidden, seed, index)).to(device))
+        self.b1 = torch.nn.Parameter(torch.zeros(hidden, device=device))
+        self.w2 = torch.nn.Parameter(torch.from_numpy(glorot(hidden, out_feats, seed, index + 1)).to(device))
+        self.b2 = torch.nn.Parameter(torch.zeros(out_feats, device=device))
+
+    def forward(self, g: CsrGraph, X: torch.Tensor, coalesced: bool = False, relu: bool = False):
+        H = linear(X, self.w1)
+        U = _GINAggregate.apply(H, self.b1, g, self.eps, True, coalesced)
+        return linear(U, self.w2, self.b2, relu=relu)
+
+
+class GIN(torch.nn.Module):
+    """2-layer GIN with ReLU between layers."""
+
+    def __init__(self, in_feats: int, hidden: int, classes: int, eps: float = 0.0, seed: int = 0,
+                 device=None):
+        super().__init__()
+        self.l1 = GINConv(in_feats, hidden, hidden, eps, seed=seed, index=0, device=device)
+        self.l2 = GINConv(hidden, hidden, classes, eps, seed=seed, index=2, device=device)
+
+    def forward(self, g, X, coalesced: bool = False):
+        return self.l2(g, self.l1(g, X, coalesced, relu=True), coalesced)

@@ -201,21 +201,31 @@ def colsum(X: torch.Tensor, out=None) -> torch.Tensor:
 
 class _Linear(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, X, W, b):
-        ctx.save_for_backward(X, W)
-        ctx.has_b = b is not None
-        return gemm(X.contiguous(), W.contiguous(), bias=b)
+    def forward(ctx, X, W, b, relu):
+        Y = gemm(X.contiguous(), W.contiguous(), bias=b, relu=relu)
+        ctx.save_for_backward(X, W, Y if relu else None)
+        ctx.has_b, ctx.relu = b is not None, relu
+        return Y
 
     @staticmethod
     def backward(ctx, dY):
-        X, W = ctx.saved_tensors
+        X, W, Y = ctx.saved_tensors
         dY = dY.contiguous()
+        db = None
+        if ctx.relu:  # ReLU backward against the saved output, bias grad in the same pass
+            from .kernels import MaskNormColsumCall
+
+            dYm = torch.empty_like(dY)
+            db = torch.empty(dY.shape[1], dtype=torch.float32, device=dY.device)
+            MaskNormColsumCall(dY, dYm, mask=Y, colsum=db if ctx.has_b else None)()
+            dY = dYm
         dX = gemm(dY, W, trans_b=True) if ctx.needs_input_grad[0] else None
         dW = gemm(X, dY, trans_a=True) if ctx.needs_input_grad[1] else None
-        db = colsum(dY) if ctx.has_b and ctx.needs_input_grad[2] else None
-        return dX, dW, db
+        if ctx.has_b and ctx.needs_input_grad[2] and db is None:
+            db = colsum(dY)
+        return dX, dW, db if ctx.has_b else None, None
 
 
-def linear(X: torch.Tensor, W: torch.Tensor, b=None) -> torch.Tensor:
-    """X[M,Kin] . W[Kin,N] (+ b), differentiable, on libgnnb200."""
-    return _Linear.apply(X, W, b)
+def linear(X: torch.Tensor, W: torch.Tensor, b=None, relu: bool = False) -> torch.Tensor:
+    """X[M,Kin] . W[Kin,N] (+ b)(ReLU fused), differentiable, on libgnnb200."""
+    return _Linear.apply(X, W, b, bool(relu))
