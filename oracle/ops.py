@@ -285,3 +285,41 @@ def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False):
     dHs = dU @ A(np.asarray(c["W1"], np.float64)).T
     dX = (1.0 + c["eps"]) * dHs + spmm(t_offsets, t_cols, dHs)
     return {"W1": dW1, "b1": db1, "W2": dW2, "b2": db2, "X": dX}
+
+
+def gat2_step(offsets, cols, X, p, labels, heads, slope=0.2):
+    """2-layer GAT (hidden: heads concatenated + ReLU; output: heads
+    averaged), mean cross-entropy, all gradients (+ Appendix A.8 scales)."""
+    h1, c1 = gat_layer_fwd(offsets, cols, X, p["W1"], p["al1"], p["ar1"], p["b1"], heads,
+                           relu=True, slope=slope)
+    Z, c2 = gat_layer_fwd(offsets, cols, h1, p["W2"], p["al2"], p["ar2"], p["b2"], heads,
+                          mean=True, slope=slope)
+    loss, dZ = cross_entropy(Z, labels)
+    g2 = gat_layer_bwd(offsets, cols, c2, dZ)
+    g1 = gat_layer_bwd(offsets, cols, c1, g2["X"])
+    a2 = gat_layer_bwd(offsets, cols, c2, dZ, absmode=True)
+    a1 = gat_layer_bwd(offsets, cols, c1, a2["X"], absmode=True)
+    names = {"W": "W", "a_l": "al", "a_r": "ar", "b": "b"}
+    grads, absd = {}, {}
+    for k, n in names.items():
+        grads[n + "1"], grads[n + "2"] = g1[k], g2[k]
+        absd[n + "1"], absd[n + "2"] = a1[k], a2[k]
+    return {"loss": loss, "logits": Z, "alpha1": c1["alpha"], "alpha2": c2["alpha"], **grads,
+            "abs": absd}
+
+
+def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0):
+    """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients."""
+    h1, c1 = gin_layer_fwd(offsets, cols, X, p["W1a"], p["b1a"], p["W1b"], p["b1b"], eps,
+                           relu_out=True)
+    Z, c2 = gin_layer_fwd(offsets, cols, h1, p["W2a"], p["b2a"], p["W2b"], p["b2b"], eps)
+    loss, dZ = cross_entropy(Z, labels)
+    g2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ)
+    g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"])
+    a2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ, absmode=True)
+    a1 = gin_layer_bwd(t_offsets, t_cols, c1, a2["X"], absmode=True)
+    grads, absd = {}, {}
+    for k, n in {"W1": "W{}a", "b1": "b{}a", "W2": "W{}b", "b2": "b{}b"}.items():
+        grads[n.format(1)], grads[n.format(2)] = g1[k], g2[k]
+        absd[n.format(1)], absd[n.format(2)] = a1[k], a2[k]
+    return {"loss": loss, "logits": Z, **grads, "abs": absd}

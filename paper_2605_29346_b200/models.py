@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .graph import CsrGraph
-from .kernels import AdamCall, GemmCall, HeadCall, MaskNormColsumCall, SpmmCall
+from .kernels import AdamCall, GemmCall, HeadCall, MaskNormColsumCall, SpmmCall, XentCall
 from .ops import colsum, gemm, linear, spmm_raw
 
 
@@ -433,3 +433,279 @@ class GIN(torch.nn.Module):
 
     def forward(self, g, X, coalesced: bool = False):
         return self.l2(g, self.l1(g, X, coalesced, relu=True), coalesced)
+
+
+# ======================================================= fused trainers (2)
+class _FusedEpoch:
+    """Shared driver of the fused full-graph trainers: ``schedule()`` lists
+    the epoch's pre-bound launches; ``step()`` runs them eagerly,
+    ``capture()`` records one epoch as a CUDA graph that ``run()`` replays."""
+
+    graph = None
+
+    def schedule(self):  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def set_inputs(self, X: torch.Tensor, labels: torch.Tensor, non_blocking: bool = False):
+        self.X.copy_(X, non_blocking=non_blocking)
+        self.labels.copy_(labels, non_blocking=non_blocking)
+
+    def forward_backward(self):
+        for name, call in self.schedule():
+            if name != "adam":
+                call()
+
+    def step(self):
+        for _, call in self.schedule():
+            call()
+        return self.loss
+
+    def timed_step(self):
+        st = torch.cuda.current_stream(self.dev)
+        sched = self.schedule()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(sched) + 1)]
+        torch.cuda.synchronize(self.dev)
+        torch.cuda._sleep(5_000_000)
+        ev[0].record(st)
+        for i, (_, call) in enumerate(sched):
+            call()
+            ev[i + 1].record(st)
+        torch.cuda.synchronize(self.dev)
+        out = {}
+        for i, (name, _) in enumerate(sched):
+            out[name] = out.get(name, 0.0) + ev[i].elapsed_time(ev[i + 1])
+        return out
+
+    def capture(self):
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self.forward_backward()
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        self.graph = g
+        return g
+
+    def run(self):
+        if self.graph is None:
+            return self.step()
+        self.graph.replay()
+        return self.loss
+
+
+class GATTrainer(_FusedEpoch):
+    """Full-graph 2-layer GAT training epoch on libgnnb200 kernels only
+    (Appendix A.6; hidden layer = heads x hidden concatenated + ReLU, output
+    layer = heads x classes averaged; mean cross-entropy; Adam).
+
+    Forward per layer: Wh = X W (tcgen05 GEMM); el/er = attention
+    projections; alpha = edge_softmax(LeakyReLU(el[col] + er[row])) with the
+    scores recomputed inside the softmax kernels (never stored); Y =
+    SpMMve(A, alpha, Wh) per head (+bias/ReLU in the epilogue, or head mean).
+    Backward per layer: SpMMve^T over the CSC reading alpha through the
+    edge-ID array (no eShuffle, PAPER.md:264-266); dalpha = SDDMM(dY, Wh);
+    ds = softmax+LeakyReLU backward (in place); der/del = row / column sums
+    of ds; projection backward; weight gradient GEMMs.
+
+    The output layer's per-head width is padded to a multiple of 4 (zero
+    weight columns, which stay exactly zero: their gradients are zero) so
+    every edge kernel takes its float4 path."""
+
+    def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
+                 lr=0.01, slope=0.2, seed: int = 0):
+        from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
+                              HeadMeanCall, SddmmCall, XentCall)
+
+        self.g = g
+        dev = g.device
+        self.dev = dev
+        V, H = g.num_vertices, heads
+        self.V, self.F, self.Hd, self.C, self.H = V, in_feats, hidden, classes, heads
+        Cp = -(-classes // 4) * 4
+        self.Cp = Cp
+        f32 = dict(dtype=torch.float32, device=dev)
+        K1, K2 = H * hidden, H * Cp
+        # ---- parameters (oracle-facing values are the unpadded slices)
+        self.W1 = torch.from_numpy(glorot(in_feats, K1, seed, 0)).to(dev)
+        self.al1 = torch.from_numpy(glorot_heads(H, hidden, seed, 100)).to(dev)
+        self.ar1 = torch.from_numpy(glorot_heads(H, hidden, seed, 200)).to(dev)
+        self.b1 = torch.zeros(K1, **f32)
+        w2 = glorot(K1, H * classes, seed, 2).reshape(K1, H, classes)
+        W2p = np.zeros((K1, H, Cp), np.float32)
+        W2p[:, :, :classes] = w2
+        self.W2 = torch.from_numpy(W2p.reshape(K1, K2)).to(dev)
+        al2 = np.zeros((H, Cp), np.float32)
+        ar2 = np.zeros((H, Cp), np.float32)
+        al2[:, :classes] = glorot_heads(H, classes, seed, 102)
+        ar2[:, :classes] = glorot_heads(H, classes, seed, 202)
+        self.al2, self.ar2 = torch.from_numpy(al2).to(dev), torch.from_numpy(ar2).to(dev)
+        self.b2 = torch.zeros(Cp, **f32)
+        plist = [self.W1, self.al1, self.ar1, self.b1, self.W2, self.al2, self.ar2, self.b2]
+        self.grads_ = [torch.zeros_like(p) for p in plist]
+        (self.dW1, self.dal1, self.dar1, self.db1, self.dW2, self.dal2, self.dar2,
+         self.db2) = self.grads_
+        # ---- inputs (X row stride padded to 128 B for TMA)
+        self.Fpad = -(-in_feats // 32) * 32
+        self._Xstore = torch.zeros(V, self.Fpad, **f32)
+        self.X = self._Xstore[:, :in_feats]
+        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        # ---- activations / state tensors
+        A, AT = g.csr(), g.csc(with_eid=True)
+        self.A, self.AT = A, AT
+        E = A.nnz
+        e = lambda *s: torch.empty(*s, **f32)  # noqa: E731
+        self.Wh1, self.Y1 = e(V, K1), e(V, K1)
+        self.el1, self.er1, self.el2, self.er2 = e(V, H), e(V, H), e(V, H), e(V, H)
+        self.alpha1, self.alpha2 = e(E, H), e(E, H)
+        self.Wh2, self.Yc2 = e(V, K2), e(V, K2)
+        self.Z = torch.zeros(V, Cp, **f32)
+        self.dZ = torch.zeros(V, Cp, **f32)  # pad column never written: stays 0
+        self.dYc2, self.dWh2 = e(V, K2), e(V, K2)
+        self.ds = e(E, H)
+        self.der, self.del_ = e(V, H), e(V, H)
+        self.ones = torch.ones(V, H, **f32)
+        self.dY1, self.dY1m, self.dWh1 = e(V, K1), e(V, K1), e(V, K1)
+        self.loss = torch.zeros(1, **f32)
+        Bf, R = _lib.EPI_BIAS, _lib.EPI_RELU
+        k = {}
+        # forward
+        k["X.W1"] = GemmCall(self.X, self.W1, self.Wh1)
+        k["proj1"] = AttnProjCall(self.Wh1, self.al1, self.ar1, self.el1, self.er1, H)
+        k["softmax1"] = EdgeSoftmaxCall(A, H, self.alpha1, el=self.el1, er=self.er1, slope=slope)
+        k["agg1"] = SpmmCall(A, self.Wh1, self.Y1, flags=Bf | R, heads=H, vals=self.alpha1,
+                             bias=self.b1)
+        k["Y1.W2"] = GemmCall(self.Y1, self.W2, self.Wh2)
+        k["proj2"] = AttnProjCall(self.Wh2, self.al2, self.ar2, self.el2, self.er2, H)
+        k["softmax2"] = EdgeSoftmaxCall(A, H, self.alpha2, el=self.el2, er=self.er2, slope=slope)
+        k["agg2"] = SpmmCall(A, self.Wh2, self.Yc2, heads=H, vals=self.alpha2)
+        k["mean2"] = HeadMeanCall(self.Yc2, self.Z, H, Cp, bias=self.b2)
+        k["xent"] = XentCall(self.Z[:, :classes], self.labels, self.loss, dZ=self.dZ[:, :classes])
+        # backward, layer 2
+        k["db2"] = ColsumCall(self.dZ, self.db2)
+        k["mean2_bwd"] = HeadMeanCall(self.dYc2, self.dZ, H, Cp, backward=True)
+        k["bagg2"] = SpmmCall(AT, self.dYc2, self.dWh2, heads=H, vals=self.alpha2, eid=AT.eid)
+        k["sddmm2"] = SddmmCall(A, self.dYc2, self.Wh2, self.ds, heads=H)
+        k["softmax2_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el2, er=self.er2, slope=slope,
+                                            backward=True, alpha=self.alpha2, dalpha=self.ds)
+        k["der2"] = SpmmCall(A, self.ones, self.der, heads=H, vals=self.ds)
+        k["del2"] = SpmmCall(AT, self.ones, self.del_, heads=H, vals=self.ds, eid=AT.eid)
+        k["proj2_bwd"] = AttnProjBwdCall(self.Wh2, self.al2, self.ar2, self.del_, self.der,
+                                         self.dWh2, self.dal2, self.dar2, H)
+        k["Y1^T.dWh2"] = GemmCall(self.Y1, self.dWh2, self.dW2, trans_a=True)
+        k["dWh2.W2^T"] = GemmCall(self.dWh2, self.W2, self.dY1, trans_b=True)
+        # backward, layer 1
+        k["relu1_bwd"] = MaskNormColsumCall(self.dY1, self.dY1m, mask=self.Y1, colsum=self.db1)
+        k["bagg1"] = SpmmCall(AT, self.dY1m, self.dWh1, heads=H, vals=self.alpha1, eid=AT.eid)
+        k["sddmm1"] = SddmmCall(A, self.dY1m, self.Wh1, self.ds, heads=H)
+        k["softmax1_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el1, er=self.er1, slope=slope,
+                                            backward=True, alpha=self.alpha1, dalpha=self.ds)
+        k["der1"] = SpmmCall(A, self.ones, self.der, heads=H, vals=self.ds)
+        k["del1"] = SpmmCall(AT, self.ones, self.del_, heads=H, vals=self.ds, eid=AT.eid)
+        k["proj1_bwd"] = AttnProjBwdCall(self.Wh1, self.al1, self.ar1, self.del_, self.der,
+                                         self.dWh1, self.dal1, self.dar1, H)
+        k["X^T.dWh1"] = GemmCall(self.X, self.dWh1, self.dW1, trans_a=True)
+        k["adam"] = AdamCall(plist, self.grads_, lr=lr)
+        self.k = k
+
+    def schedule(self):
+        return list(self.k.items())
+
+    def params(self):
+        """Unpadded parameters in the oracle's naming (gat2_step)."""
+        H, C, Cp, K1 = self.H, self.C, self.Cp, self.H * self.Hd
+        return {"W1": self.W1, "al1": self.al1, "ar1": self.ar1, "b1": self.b1,
+                "W2": self.W2.reshape(K1, H, Cp)[:, :, :C].reshape(K1, H * C),
+                "al2": self.al2[:, :C], "ar2": self.ar2[:, :C], "b2": self.b2[:C]}
+
+    def grads(self):
+        H, C, Cp, K1 = self.H, self.C, self.Cp, self.H * self.Hd
+        return {"W1": self.dW1, "al1": self.dal1, "ar1": self.dar1, "b1": self.db1,
+                "W2": self.dW2.reshape(K1, H, Cp)[:, :, :C].reshape(K1, H * C),
+                "al2": self.dal2[:, :C], "ar2": self.dar2[:, :C], "b2": self.db2[:C]}
+
+    def pad_grads(self):
+        """Gradients of the padding (must stay exactly zero)."""
+        H, C, Cp, K1 = self.H, self.C, self.Cp, self.H * self.Hd
+        return [self.dW2.reshape(K1, H, Cp)[:, :, C:], self.dal2[:, C:], self.dar2[:, C:],
+                self.db2[C:]]
+
+
+class GINTrainer(_FusedEpoch):
+    """Full-graph 2-layer GIN training epoch (Appendix A.5, eps fixed; hidden
+    width ``hidden``; ReLU between layers; mean cross-entropy; Adam) on
+    libgnnb200 kernels only.  Each layer's first Linear runs before its
+    aggregation (linearity), so both SpMMs of a layer work at the hidden
+    width, with the (1+eps) self term, bias and ReLU in the SpMM epilogue:
+
+      H1 = X W1a;  U1 = relu(A H1 + (1+eps) H1 + b1a);  Y1 = relu(U1 W1b + b1b)
+      H2 = Y1 W2a; U2 = relu(A H2 + (1+eps) H2 + b2a);  Z  = U2 W2b + b2b
+    """
+
+    def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, *, eps=0.0,
+                 lr=0.01, seed: int = 0, coalesced: bool = True):
+        self.g = g
+        dev = g.device
+        self.dev = dev
+        V = g.num_vertices
+        self.V, self.F, self.Hd, self.C, self.eps = V, in_feats, hidden, classes, float(eps)
+        f32 = dict(dtype=torch.float32, device=dev)
+        mk = lambda fi, fo, i: torch.from_numpy(glorot(fi, fo, seed, i)).to(dev)  # noqa: E731
+        self.W1a, self.W1b = mk(in_feats, hidden, 0), mk(hidden, hidden, 1)
+        self.W2a, self.W2b = mk(hidden, hidden, 2), mk(hidden, classes, 3)
+        self.b1a, self.b1b = torch.zeros(hidden, **f32), torch.zeros(hidden, **f32)
+        self.b2a, self.b2b = torch.zeros(hidden, **f32), torch.zeros(classes, **f32)
+        plist = [self.W1a, self.b1a, self.W1b, self.b1b, self.W2a, self.b2a, self.W2b, self.b2b]
+        self.grads_ = [torch.zeros_like(p) for p in plist]
+        (self.dW1a, self.db1a, self.dW1b, self.db1b, self.dW2a, self.db2a, self.dW2b,
+         self.db2b) = self.grads_
+        self.Fpad = -(-in_feats // 32) * 32
+        self._Xstore = torch.zeros(V, self.Fpad, **f32)
+        self.X = self._Xstore[:, :in_feats]
+        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
+        self.H1, self.U1, self.Y1, self.H2, self.U2 = (e(hidden) for _ in range(5))
+        self.dU2, self.dH2, self.dY1, self.dU1, self.dH1 = (e(hidden) for _ in range(5))
+        self.loss = torch.zeros(1, **f32)
+        if coalesced:
+            A, AT = g.csr_coalesced(), g.csc_coalesced()
+        else:
+            A, AT = g.csr(), g.csc()
+        self.A, self.AT = A, AT
+        S, Bf, R, M = _lib.EPI_SELF, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        s1 = 1.0 + self.eps
+        k = {}
+        k["X.W1a"] = GemmCall(self.X, self.W1a, self.H1)
+        k["agg1"] = SpmmCall(A, self.H1, self.U1, flags=S | Bf | R, self_x=self.H1, self_scale=s1,
+                             bias=self.b1a)
+        k["U1.W1b"] = GemmCall(self.U1, self.W1b, self.Y1, bias=self.b1b, relu=True)
+        k["Y1.W2a"] = GemmCall(self.Y1, self.W2a, self.H2)
+        k["agg2"] = SpmmCall(A, self.H2, self.U2, flags=S | Bf | R, self_x=self.H2, self_scale=s1,
+                             bias=self.b2a)
+        k["head"] = HeadCall(self.U2, self.W2b, self.b2b, self.labels, self.dU2, self.dW2b,
+                             self.db2b, self.loss)
+        k["relu_bwd_U2"] = MaskNormColsumCall(self.dU2, self.dU2, mask=self.U2, colsum=self.db2a)
+        k["bagg2"] = SpmmCall(AT, self.dU2, self.dH2, flags=S, self_x=self.dU2, self_scale=s1)
+        k["Y1^T.dH2"] = GemmCall(self.Y1, self.dH2, self.dW2a, trans_a=True)
+        k["dH2.W2a^T"] = GemmCall(self.dH2, self.W2a, self.dY1, trans_b=True)
+        k["relu_bwd_Y1"] = MaskNormColsumCall(self.dY1, self.dY1, mask=self.Y1, colsum=self.db1b)
+        k["U1^T.dY1"] = GemmCall(self.U1, self.dY1, self.dW1b, trans_a=True)
+        k["dY1.W1b^T"] = GemmCall(self.dY1, self.W1b, self.dU1, trans_b=True)
+        k["relu_bwd_U1"] = MaskNormColsumCall(self.dU1, self.dU1, mask=self.U1, colsum=self.db1a)
+        k["bagg1"] = SpmmCall(AT, self.dU1, self.dH1, flags=S, self_x=self.dU1, self_scale=s1)
+        k["X^T.dH1"] = GemmCall(self.X, self.dH1, self.dW1a, trans_a=True)
+        k["adam"] = AdamCall(plist, self.grads_, lr=lr)
+        _ = M
+        self.k = k
+
+    def schedule(self):
+        return list(self.k.items())
+
+    def params(self):
+        return {"W1a": self.W1a, "b1a": self.b1a, "W1b": self.W1b, "b1b": self.b1b,
+                "W2a": self.W2a, "b2a": self.b2a, "W2b": self.W2b, "b2b": self.b2b}
+
+    def grads(self):
+        return {"W1a": self.dW1a, "b1a": self.db1a, "W1b": self.dW1b, "b1b": self.db1b,
+                "W2a": self.dW2a, "b2a": self.db2a, "W2b": self.dW2b, "b2b": self.db2b}
