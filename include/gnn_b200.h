@@ -233,6 +233,13 @@ int gnn_edge_softmax_bwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, i
                          const float *alpha, const float *dalpha, const gnn_edge_scores_t *scores,
                          float *ds, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Row sums of an edge tensor: out[r,h] = sum_{j in row r} vals[idx_j*heads + h],
+ * idx_j = A->eid[j] when the view carries an edge-ID array (column sums of a
+ * CSR-ordered edge tensor through the CSC), else j.  Empty rows give 0.
+ * Workspace: gnn_edge_softmax_workspace(plan, heads).  Deterministic. */
+int gnn_segment_sum(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                    const float *vals, float *out, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
 /* GAT attention projections (Appendix A.6): el[v,h] = <Wh[v,h,:], a_l[h,:]>,
  * er[v,h] = <Wh[v,h,:], a_r[h,:]>; a_l/a_r are [heads, F]. */
 int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,

@@ -160,6 +160,10 @@ SIGNATURES = {
         [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, C.POINTER(EdgeScores),
          c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_segment_sum": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
     "gnn_gat_attn_proj": (
         c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "gnn_gat_attn_proj_bwd_workspace": (c_sz, [c_i64, c_i64]),

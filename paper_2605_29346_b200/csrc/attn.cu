@@ -83,7 +83,10 @@ struct SddmmArgs {
 // (v < VPL); LPH = F/4 lanes per head (power of two, <= G) reduce a head's dot
 // by xor shuffles inside the group.  NG = 32/G edges per warp step, U steps
 // unrolled so U gathers per lane are in flight.
-template <int G, int VPL>
+// HM > 0 selects the general head mapping (any F % 4 == 0): each lane sums
+// its vectors per head in registers and every head is reduced over the whole
+// G-lane group; group lane 0 writes the edge's H outputs.
+template <int G, int VPL, int HM>
 __global__ void __launch_bounds__(256) sddmm_vec_kernel(SddmmArgs a, int LPH) {
   constexpr int NG = 32 / G;
   constexpr int U = VPL >= 2 ? 2 : 4;
@@ -133,14 +136,45 @@ __global__ void __launch_bounds__(256) sddmm_vec_kernel(SddmmArgs a, int LPH) {
 #pragma unroll
         for (int v = 0; v < VPL; ++v) xv[v] = ldg_f4(a.X + r * a.ldx + col[v]);
       }
+      if constexpr (HM == 0) {
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        float p = xv[v].x * yv[u][v].x;
-        p = fmaf(xv[v].y, yv[u][v].y, p);
-        p = fmaf(xv[v].z, yv[u][v].z, p);
-        p = fmaf(xv[v].w, yv[u][v].w, p);
-        for (int o = 1; o < LPH; o <<= 1) p += __shfl_xor_sync(gmask, p, o);
-        if (cv[v] && (gl & (LPH - 1)) == 0) a.out[e * a.H + col[v] / a.F] = p;
+        for (int v = 0; v < VPL; ++v) {
+          float p = xv[v].x * yv[u][v].x;
+          p = fmaf(xv[v].y, yv[u][v].y, p);
+          p = fmaf(xv[v].z, yv[u][v].z, p);
+          p = fmaf(xv[v].w, yv[u][v].w, p);
+          for (int o = 1; o < LPH; o <<= 1) p += __shfl_xor_sync(gmask, p, o);
+          if (cv[v] && (gl & (LPH - 1)) == 0) a.out[e * a.H + col[v] / a.F] = p;
+        }
+      } else {
+        float ph[HM];
+#pragma unroll
+        for (int h = 0; h < HM; ++h) ph[h] = 0.f;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          float p = xv[v].x * yv[u][v].x;
+          p = fmaf(xv[v].y, yv[u][v].y, p);
+          p = fmaf(xv[v].z, yv[u][v].z, p);
+          p = fmaf(xv[v].w, yv[u][v].w, p);
+          if (cv[v]) {
+            const int hv = (int)(col[v] / a.F);
+#pragma unroll
+            for (int h = 0; h < HM; ++h) ph[h] += h == hv ? p : 0.f;
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+          for (int h = 0; h < HM; ++h) ph[h] += __shfl_xor_sync(gmask, ph[h], o);
+        if (gl == 0) {
+          if (HM == 4 && a.H == 4 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0) {
+            *reinterpret_cast<float4 *>(a.out + e * 4) = make_float4(ph[0], ph[1], ph[2], ph[3]);
+          } else {
+#pragma unroll
+            for (int h = 0; h < HM; ++h)
+              if (h < a.H) a.out[e * a.H + h] = ph[h];
+          }
+        }
       }
     }
   }
@@ -194,6 +228,8 @@ struct SoftmaxArgs {
   // workspace
   float *slots;  // [nwarps][2][2*H]
   float *stat;   // [num_split][2*H]
+  // segment sum: out[r,h] = sum over row r of vals[(eid ? eid[j] : j)*H + h]
+  const int32_t *eid;
 };
 
 template <int HM>
@@ -470,6 +506,98 @@ __global__ void __launch_bounds__(256) softmax_split_apply_kernel(SoftmaxArgs a)
   }
 }
 
+// ------------------------------------------------------------ segment sum
+// Row sums of an edge tensor (GAT's der = rowsum(ds), del = colsum(ds) via
+// the CSC + edge-ID).  Same chunk walk; whole rows write out[r], split-row
+// pieces leave partials that the finalize kernel sums in fixed order.
+template <int HM, bool EID>
+__device__ __forceinline__ void segsum_piece(const SoftmaxArgs &a, int64_t r, int64_t lo, int64_t hi,
+                                             bool whole, float *slot) {
+  const int lane = (int)lane_id();
+  float S[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) S[h] = 0.f;
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    const int64_t src = EID ? (int64_t)a.eid[e] : e;
+    if (HM == 4 && a.H == 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(a.alpha_in + src * 4);
+      S[0] += v.x;
+      S[1] += v.y;
+      S[2] += v.z;
+      S[3] += v.w;
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) S[h] += a.alpha_in[src * a.H + h];
+    }
+  }
+  warp_sum_reduce<HM>(S);
+  if (lane == 0)
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) (whole ? a.ds + r * a.H : slot)[h] = S[h];
+}
+
+template <int HM, bool EID>
+__global__ void __launch_bounds__(256) segsum_rows_kernel(SoftmaxArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
+  while (true) {
+    const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if (hi > lo) {
+      const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
+      float *slot = a.slots + (w * 2 + (carry ? 0 : 1)) * 2 * a.H;
+      segsum_piece<HM, EID>(a, rw.r, lo, hi, !(carry || trail), slot);
+    }
+    if (rw.re >= e1 || rw.r + 1 >= a.R) break;
+    rw.next();
+  }
+}
+
+template <int HM>
+__global__ void __launch_bounds__(256) segsum_split_finalize_kernel(SoftmaxArgs a) {
+  const int64_t si = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (si >= a.num_split) return;
+  const int lane = (int)lane_id();
+  const int64_t r = a.split_rows[si];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  const int64_t np = wb - wa + 1;
+  float S[HM];
+#pragma unroll
+  for (int h = 0; h < HM; ++h) S[h] = 0.f;
+  for (int64_t j = lane; j < np; j += 32) {
+    const float *slot = a.slots + ((wa + j) * 2 + (j == 0 ? 1 : 0)) * 2 * a.H;
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) S[h] += slot[h];
+  }
+  warp_sum_reduce<HM>(S);
+  if (lane == 0)
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) a.ds[r * a.H + h] = S[h];
+}
+
+template <int HM>
+int launch_segsum(const SoftmaxArgs &a, bool eid, cudaStream_t st) {
+  GNN_CUDA_TRY(cudaMemsetAsync(a.ds, 0, sizeof(float) * a.R * a.H, st));  // empty rows
+  if (a.nwarps > 0) {
+    if (eid)
+      segsum_rows_kernel<HM, true><<<grid_warps(a.nwarps, 256), 256, 0, st>>>(a);
+    else
+      segsum_rows_kernel<HM, false><<<grid_warps(a.nwarps, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_split > 0) {
+    segsum_split_finalize_kernel<HM><<<grid_warps(a.num_split, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
 template <int HM, bool GAT, bool BWD>
 int launch_softmax(const SoftmaxArgs &a, cudaStream_t st) {
   if (a.nwarps > 0) {
@@ -675,24 +803,48 @@ int gnn_sddmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t head
   const int64_t lph = a.F / 4;
   const bool lph_pow2 = lph > 0 && (lph & (lph - 1)) == 0;
   const bool vec = K % 4 == 0 && a.F % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && al16(X) &&
-                   al16(Y) && lph_pow2 && lph <= G && ceil_div(q, G) <= 4;
+                   al16(Y) && ceil_div(q, G) <= 4;
+  const bool pow2 = lph_pow2 && lph <= G;
   const unsigned grid = grid_warps(a.nwarps, 256);
-  if (vec) {
-    const int LPH = (int)lph;
-    const int VPL = (int)ceil_div(q, G);
+  const int VPL = (int)ceil_div(q, G);
+  const int LPH = (int)lph;
+  if (vec && pow2) {
     switch (G) {
-      case 1: sddmm_vec_kernel<1, 1><<<grid, 256, 0, st>>>(a, LPH); break;
-      case 2: sddmm_vec_kernel<2, 1><<<grid, 256, 0, st>>>(a, LPH); break;
-      case 4: sddmm_vec_kernel<4, 1><<<grid, 256, 0, st>>>(a, LPH); break;
-      case 8: sddmm_vec_kernel<8, 1><<<grid, 256, 0, st>>>(a, LPH); break;
-      case 16: sddmm_vec_kernel<16, 1><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 1: sddmm_vec_kernel<1, 1, 0><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 2: sddmm_vec_kernel<2, 1, 0><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 4: sddmm_vec_kernel<4, 1, 0><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 8: sddmm_vec_kernel<8, 1, 0><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 16: sddmm_vec_kernel<16, 1, 0><<<grid, 256, 0, st>>>(a, LPH); break;
       default:
         if (VPL == 1)
-          sddmm_vec_kernel<32, 1><<<grid, 256, 0, st>>>(a, LPH);
+          sddmm_vec_kernel<32, 1, 0><<<grid, 256, 0, st>>>(a, LPH);
         else if (VPL == 2)
-          sddmm_vec_kernel<32, 2><<<grid, 256, 0, st>>>(a, LPH);
+          sddmm_vec_kernel<32, 2, 0><<<grid, 256, 0, st>>>(a, LPH);
         else
-          sddmm_vec_kernel<32, 4><<<grid, 256, 0, st>>>(a, LPH);
+          sddmm_vec_kernel<32, 4, 0><<<grid, 256, 0, st>>>(a, LPH);
+    }
+  } else if (vec && heads <= 8) {
+    // general head mapping (e.g. GAT's 4 x 48 output heads); G >= 2 here
+    const bool h4 = heads <= 4;
+    switch (G) {
+      case 2: h4 ? sddmm_vec_kernel<2, 1, 4><<<grid, 256, 0, st>>>(a, LPH)
+                 : sddmm_vec_kernel<2, 1, 8><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 4: h4 ? sddmm_vec_kernel<4, 1, 4><<<grid, 256, 0, st>>>(a, LPH)
+                 : sddmm_vec_kernel<4, 1, 8><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 8: h4 ? sddmm_vec_kernel<8, 1, 4><<<grid, 256, 0, st>>>(a, LPH)
+                 : sddmm_vec_kernel<8, 1, 8><<<grid, 256, 0, st>>>(a, LPH); break;
+      case 16: h4 ? sddmm_vec_kernel<16, 1, 4><<<grid, 256, 0, st>>>(a, LPH)
+                  : sddmm_vec_kernel<16, 1, 8><<<grid, 256, 0, st>>>(a, LPH); break;
+      default:
+        if (VPL == 1)
+          h4 ? sddmm_vec_kernel<32, 1, 4><<<grid, 256, 0, st>>>(a, LPH)
+             : sddmm_vec_kernel<32, 1, 8><<<grid, 256, 0, st>>>(a, LPH);
+        else if (VPL == 2)
+          h4 ? sddmm_vec_kernel<32, 2, 4><<<grid, 256, 0, st>>>(a, LPH)
+             : sddmm_vec_kernel<32, 2, 8><<<grid, 256, 0, st>>>(a, LPH);
+        else
+          h4 ? sddmm_vec_kernel<32, 4, 4><<<grid, 256, 0, st>>>(a, LPH)
+             : sddmm_vec_kernel<32, 4, 8><<<grid, 256, 0, st>>>(a, LPH);
     }
   } else {
     sddmm_scalar_kernel<<<grid, 256, 0, st>>>(a);
@@ -736,6 +888,25 @@ int gnn_edge_softmax_bwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, i
   a.ds = ds;
   cudaStream_t st = as_stream(stream);
   return gat ? dispatch_softmax<true, true>(a, st) : dispatch_softmax<false, true>(a, st);
+}
+
+int gnn_segment_sum(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                    const float *vals, float *out, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  SoftmaxArgs a;
+  GNN_TRY(softmax_common(A, plan, heads, nullptr, ws, ws_bytes, a));
+  if (A->num_rows > 0 && !out) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz > 0 && !vals) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->num_rows == 0) return GNN_OK;
+  if (heads == 4 && !al16(vals)) return GNN_ERR_INVALID_ARGUMENT;
+  a.alpha_in = vals;
+  a.ds = out;
+  a.eid = A->eid;
+  cudaStream_t st = as_stream(stream);
+  const bool e = A->eid != nullptr;
+  if (heads == 1) return launch_segsum<1>(a, e, st);
+  if (heads <= 4) return launch_segsum<4>(a, e, st);
+  if (heads <= 8) return launch_segsum<8>(a, e, st);
+  return launch_segsum<16>(a, e, st);
 }
 
 int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,

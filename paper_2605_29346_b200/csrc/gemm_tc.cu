@@ -291,51 +291,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
 // MN-major in shared memory.  MN-major tf32 operands have exactly one legal
 // smem layout, SWIZZLE_128B_BASE32B (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
 // 128-byte MN rows (32 fp32), 4-row K groups (SBO = 512 B), MN atoms = the
-// 32-column TMA boxes, 4 KB apart (LBO).  A is a 128-wide M tile (4 boxes),
-// B one box of 32 columns (N <= 32, OOB zero-filled).  Both operands are
-// split hi/lo in shared memory by the split warps.
-// Work units = (m-tile, k-split); each unit's
-// [128 x N] partial is written to global and summed in a fixed order.
+// 32-column TMA boxes, 4 KB apart (LBO).  A is a 128-wide M tile (4 atoms,
+// OOB columns zero-filled); B is an NB-wide N tile (NB/32 atoms) followed in
+// shared memory by NB/32 atoms of B_lo written by the split warps, so
+// [B_hi | B_lo] is ONE 2*NB-wide MN-major operand (same atom stride) and each
+// 8-row K step is two MMAs (A_hi and A_lo against [B_hi|B_lo]).
+// Work units = (m-tile, n-tile, k-split); each unit's [128 x NB] partial is
+// written to global and the splits are summed in a fixed order.
 __device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                             uint32_t layout) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
-constexpr int kTnStages = 6;
+template <int NB>
+constexpr int tn_stages() {
+  return NB <= 32 ? 5 : (NB <= 64 ? 4 : 3);
+}
+template <int NB>
+constexpr size_t tn_smem_bytes() {
+  return (size_t)tn_stages<NB>() * (2 * kTcM * kTcBK + 2 * NB * kTcBK) * 4 + 2048;
+}
 
 struct TnArgs {
   int64_t M, N, K;
   int nkb_total;      // ceil(K / 32)
   int kb_per_split;
   int splits;
-  int64_t mtiles;
+  int64_t mtiles, ntiles;
   float *partials;    // [splits][M][N]
 };
 
-template <int NPAD>
+template <int NB>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnArgs p) {
-  static_assert(NPAD == 32, "MN-major B tile: one 128-byte SW128 atom (N <= 32, OOB-filled)");
+  static_assert(NB == 32 || NB == 64 || NB == 128, "N tile = whole 32-column atoms, 2*NB <= 256");
+  constexpr int kStages = tn_stages<NB>();
+  constexpr int kAtomsB = NB / 32;
   extern __shared__ __align__(1024) uint8_t tn_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tn_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr size_t kA = (size_t)kTcM * kTcBK * 4;   // 16 KB: 4 boxes of [32 rows x 128 B]
-  constexpr size_t kB = (size_t)kTcBK * NPAD * 4;   // 4 KB: [32 rows x 128 B]
+  constexpr size_t kA = (size_t)kTcM * kTcBK * 4;   // 16 KB: 4 atoms of [32 rows x 128 B]
+  constexpr size_t kB = (size_t)kTcBK * NB * 4;     // hi atoms; the lo atoms follow
   float *sa = reinterpret_cast<float *>(base);
-  float *salo = reinterpret_cast<float *>(base + kTnStages * kA);
-  float *sb = reinterpret_cast<float *>(base + 2 * kTnStages * kA);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kTnStages * kA + kTnStages * kB);
-  uint64_t *full = bars, *split = bars + kTnStages, *empty = bars + 2 * kTnStages;
-  uint64_t *acc_full = bars + 3 * kTnStages, *acc_empty = acc_full + 2;
+  float *salo = reinterpret_cast<float *>(base + kStages * kA);
+  float *sb = reinterpret_cast<float *>(base + 2 * kStages * kA);  // [stage][hi atoms | lo atoms]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * kStages * kA + 2 * kStages * kB);
+  uint64_t *full = bars, *split = bars + kStages, *empty = bars + 2 * kStages;
+  uint64_t *acc_full = bars + 3 * kStages, *acc_empty = acc_full + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   constexpr uint32_t kTx = (uint32_t)(kA + kB);
-  constexpr int kTmemCols = 64;  // two accumulators x 32 columns ([B_hi | B_lo] halves)
-  const int64_t units = p.mtiles * p.splits;
+  constexpr int kAcc = 2 * NB;                 // [hi | lo] accumulator columns
+  constexpr int kTmemCols = 2 * kAcc < 32 ? 32 : 2 * kAcc;  // two accumulators
+  const int64_t units = p.mtiles * p.ntiles * p.splits;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTnStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
       mbar_init(split + s, 4);
       mbar_init(empty + s, 1);
@@ -356,13 +368,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // idesc: D f32, A/B tf32, A and B MN-major, N=NPAD, M=128
+  // idesc: D f32, A/B tf32, A and B MN-major, N = 2*NB, M = 128
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
-                   ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+                         ((uint32_t)(kAcc >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
 
-  auto unit_kb = [&](int64_t u, int &kb0, int &kb1, int &m0) {
-    const int64_t mt = u % p.mtiles, sp = u / p.mtiles;
+  auto unit_of = [&](int64_t u, int &kb0, int &kb1, int &m0, int &n0, int64_t &sp) {
+    const int64_t mt = u % p.mtiles;
+    const int64_t nt = (u / p.mtiles) % p.ntiles;
+    sp = u / (p.mtiles * p.ntiles);
     m0 = (int)(mt * kTcM);
+    n0 = (int)(nt * NB);
     kb0 = (int)(sp * p.kb_per_split);
     kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
   };
@@ -372,8 +387,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
       int s = 0;
       uint32_t ph = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        int kb0, kb1, m0;
-        unit_kb(u, kb0, kb1, m0);
+        int kb0, kb1, m0, n0;
+        int64_t sp;
+        unit_of(u, kb0, kb1, m0, n0, sp);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
           mbar_arrive_expect_tx(full + s, kTx);
@@ -381,8 +397,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
           for (int j = 0; j < 4; ++j)
             tma_load_2d(smem_u32(sa + (size_t)s * kTcM * kTcBK + j * 32 * kTcBK), &tmA, m0 + 32 * j,
                         kb * kTcBK, smem_u32(full + s));
-          tma_load_2d(smem_u32(sb + (size_t)s * kTcBK * NPAD), &tmB, 0, kb * kTcBK, smem_u32(full + s));
-          if (++s == kTnStages) {
+#pragma unroll
+          for (int j = 0; j < kAtomsB; ++j)
+            tma_load_2d(smem_u32(sb + (size_t)s * 2 * NB * kTcBK + j * 32 * kTcBK), &tmB,
+                        n0 + 32 * j, kb * kTcBK, smem_u32(full + s));
+          if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
@@ -396,30 +415,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
       int ab = 0;
       uint32_t aph = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        int kb0, kb1, m0;
-        unit_kb(u, kb0, kb1, m0);
+        int kb0, kb1, m0, n0;
+        int64_t sp;
+        unit_of(u, kb0, kb1, m0, n0, sp);
         mbar_wait(acc_empty + ab, aph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(ab * NPAD);
+        const uint32_t d = tmem + (uint32_t)(ab * kAcc);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(split + s, ph);
           tc_fence_after();
           const uint32_t a_hi = smem_u32(sa + (size_t)s * kTcM * kTcBK);
           const uint32_t a_lo = smem_u32(salo + (size_t)s * kTcM * kTcBK);
-          const uint32_t b_hi = smem_u32(sb + (size_t)s * kTcBK * NPAD);
+          const uint32_t b_hl = smem_u32(sb + (size_t)s * 2 * NB * kTcBK);
 #pragma unroll
-          for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA = one 1 KB SW128 atom row group
-            // SWIZZLE_128B_BASE32B (layout 1): 128-byte MN rows, 4-row K groups (SBO 512 B),
-            // MN atoms (the 32-column TMA boxes) 4 KB apart (LBO)
+          for (int k = 0; k < kTcBK / 8; ++k) {  // 8 K-rows per MMA = 1 KB of every atom
             const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 512, 1);
             const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 512, 1);
-            const uint64_t bc = mn_desc(b_hi + k * 1024, 4096, 512, 1);  // cols [0,16) hi, [16,32) lo
+            const uint64_t bc = mn_desc(b_hl + k * 1024, 4096, 512, 1);  // [hi atoms | lo atoms]
             tc_mma_tf32(d, ah, bc, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             tc_mma_tf32(d, al, bc, idesc, 1);
           }
           tc_commit(empty + s);
           if (kb == kb1 - 1) tc_commit(acc_full + ab);
-          if (++s == kTnStages) {
+          if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
@@ -435,8 +453,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
     int s = 0;
     uint32_t ph = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      int kb0, kb1, m0;
-      unit_kb(u, kb0, kb1, m0);
+      int kb0, kb1, m0, n0;
+      int64_t sp;
+      unit_of(u, kb0, kb1, m0, n0, sp);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(full + s, ph);
         float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
@@ -451,27 +470,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
           h.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
           l4[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);  // raw A = A_hi
         }
-        // B rows are 128 B (32 columns; 16 real + 16 TMA zero-fill).  Put B_lo of
-        // column n into column n+16: under the 32B-atom swizzle (phys chunk =
-        // logical chunk ^ (row & 3)) that partner is the byte offset ^ 64.
-        uint8_t *bb = reinterpret_cast<uint8_t *>(sb + (size_t)s * kTcBK * NPAD);
-        for (int i = tid; i < kTcBK * NPAD / 4; i += 128) {
-          const int off = i * 16;
-          const int logical_chunk = ((off >> 5) & 3) ^ ((off >> 7) & 3);
-          if (logical_chunk < 2) {
-            const float4 x = *reinterpret_cast<const float4 *>(bb + off);
-            float4 lo;
-            lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
-            lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
-            lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
-            lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-            *reinterpret_cast<float4 *>(bb + (off ^ 64)) = lo;
-          }
+        // B_lo atoms sit kB bytes after the hi atoms: same swizzle phase (4 KB multiple)
+        const float4 *b4 = reinterpret_cast<const float4 *>(sb + (size_t)s * 2 * NB * kTcBK);
+        float4 *bl4 = reinterpret_cast<float4 *>(sb + (size_t)s * 2 * NB * kTcBK + NB * kTcBK);
+#pragma unroll 4
+        for (int i = tid; i < NB * kTcBK / 4; i += 128) {
+          const float4 x = b4[i];
+          float4 lo;
+          lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+          lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+          lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+          lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+          bl4[i] = lo;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(split + s);
-        if (++s == kTnStages) {
+        if (++s == kStages) {
           s = 0;
           ph ^= 1;
         }
@@ -482,26 +497,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
     int ab = 0;
     uint32_t aph = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      int kb0, kb1, m0;
-      unit_kb(u, kb0, kb1, m0);
-      const int64_t sp = u / p.mtiles;
+      int kb0, kb1, m0, n0;
+      int64_t sp;
+      unit_of(u, kb0, kb1, m0, n0, sp);
       mbar_wait(acc_full + ab, aph);
       tc_fence_after();
-      uint32_t v[16], w[16];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NPAD);
-      tmem_ld16(taddr, v);
-      tmem_ld16(taddr + 16, w);  // B_lo half
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int64_t m = (int64_t)m0 + q * 32 + lane;
+      float *dst = p.partials + (sp * p.M + m) * p.N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        uint32_t v[16], w[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
+        tmem_ld16(taddr, v);
+        tmem_ld16(taddr + NB, w);  // B_lo half
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (m < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + c0 + j < p.N) dst[n0 + c0 + j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + ab);
-      const int64_t m = (int64_t)m0 + q * 32 + lane;
-      if (m < p.M) {
-        float *dst = p.partials + (sp * p.M + m) * p.N;
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (j < p.N) dst[j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
-      }
       if (++ab == 2) {
         ab = 0;
         aph ^= 1;
@@ -650,34 +668,51 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
 // ---- A^T B (weight gradient) on tcgen05
 bool gemm_tc_tn_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                           const float *B, int64_t ldb) {
-  return M >= 1 && N >= 1 && N <= 16 && K >= 1024 && (lda * 4) % 16 == 0 && (ldb * 4) % 16 == 0 &&
+  return M >= 1 && N >= 1 && K >= 256 && (lda * 4) % 16 == 0 && (ldb * 4) % 16 == 0 &&
          (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && (reinterpret_cast<uintptr_t>(B) & 15u) == 0 &&
          encode_fn() != nullptr && getenv("GNN_GEMM_NO_TC") == nullptr;
 }
 
-static void tn_plan(int64_t M, int64_t K, int64_t &mtiles, int &nkb, int &kbps, int &splits) {
+static int tn_nb(int64_t N) { return N <= 32 ? 32 : N <= 64 ? 64 : 128; }
+
+static void tn_plan(int64_t M, int64_t N, int64_t K, int64_t &mtiles, int64_t &ntiles, int &nkb,
+                    int &kbps, int &splits) {
   mtiles = ceil_div(M, kTcM);
+  ntiles = ceil_div(N, tn_nb(N));
   nkb = (int)ceil_div(K, kTcBK);
   int64_t want = 2 * (int64_t)sm_count();  // units
-  int64_t sp = ceil_div(want, mtiles);
+  int64_t sp = ceil_div(want, mtiles * ntiles);
   if (sp > nkb) sp = nkb;
   kbps = (int)ceil_div(nkb, sp);
   splits = (int)ceil_div(nkb, kbps);
 }
 
 size_t gemm_tc_tn_workspace(int64_t M, int64_t N, int64_t K) {
-  int64_t mtiles;
+  int64_t mtiles, ntiles;
   int nkb, kbps, splits;
-  tn_plan(M, K, mtiles, nkb, kbps, splits);
+  tn_plan(M, N, K, mtiles, ntiles, nkb, kbps, splits);
   return sizeof(float) * (size_t)(splits * M * N) + 512;
+}
+
+template <int NB>
+static int launch_tn(const CUtensorMap &ta, const CUtensorMap &tb, const TnArgs &p,
+                     cudaStream_t st) {
+  constexpr size_t smem = tn_smem_bytes<NB>();
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<NB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t units = p.mtiles * p.ntiles * p.splits;
+  const int64_t grid = units < sm_count() ? units : sm_count();
+  gemm_tc_tn_kernel<NB><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tb, p);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
 }
 
 int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
                int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st) {
   TnArgs p{};
   int kbps, splits, nkb;
-  int64_t mtiles;
-  tn_plan(M, K, mtiles, nkb, kbps, splits);
+  int64_t mtiles, ntiles;
+  tn_plan(M, N, K, mtiles, ntiles, nkb, kbps, splits);
   if (ws_bytes < gemm_tc_tn_workspace(M, N, K)) return GNN_ERR_WORKSPACE;
   p.M = M;
   p.N = N;
@@ -686,20 +721,19 @@ int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, con
   p.kb_per_split = kbps;
   p.splits = splits;
   p.mtiles = mtiles;
+  p.ntiles = ntiles;
   p.partials = static_cast<float *>(ws);
   CUtensorMap ta, tb;
-  // A [K rows, M cols] and B [K rows, N cols]: boxes of 32 cols x 32 rows
+  // A [K rows, M cols] and B [K rows, N cols]: boxes of 32 cols x 32 rows (OOB zero-filled)
   // MN-major tf32 operands: the only legal smem layout is SWIZZLE_128B_BASE32B
   if (!map_2d(&ta, A, M, K, lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
       !map_2d(&tb, B, N, K, ldb, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return GNN_ERR_UNSUPPORTED;
-  constexpr size_t smem = (size_t)kTnStages * (2 * kTcM * kTcBK + kTcBK * 32) * 4 + 2048;
-  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_tn_kernel<32>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t units = mtiles * splits;
-  const int64_t grid = units < sm_count() ? units : sm_count();
-  gemm_tc_tn_kernel<32><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tb, p);
-  GNN_LAUNCH_CHECK();
+  switch (tn_nb(N)) {
+    case 32: GNN_TRY(launch_tn<32>(ta, tb, p, st)); break;
+    case 64: GNN_TRY(launch_tn<64>(ta, tb, p, st)); break;
+    default: GNN_TRY(launch_tn<128>(ta, tb, p, st)); break;
+  }
   tn_reduce_kernel<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(M, N, splits, p.partials, C, ldc);
   GNN_LAUNCH_CHECK();
   return GNN_OK;

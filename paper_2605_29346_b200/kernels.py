@@ -277,3 +277,25 @@ class HeadMeanCall:
                 self.V, self.H, self.F, self.Y.data_ptr(), self.Y.stride(0),
                 self.bias.data_ptr() if self.bias is not None else None, self.out.data_ptr(),
                 self.out.stride(0), st), "head_mean")
+
+
+class SegmentSumCall:
+    """out[r,h] = sum over op's row r of vals[(eid ? eid[j] : j), h] (row sums of
+    an edge tensor; column sums through the CSC + edge-ID)."""
+
+    def __init__(self, op: SparseOperand, vals, out, heads, use_eid=False):
+        self.lib = _lib.lib()
+        self.dev = out.device
+        self.view = op.view(vals=vals, eid=op.eid if use_eid else None)
+        if not use_eid:
+            self.view.eid = None
+        self.plan = op.plan()
+        self.heads, self.vals, self.out, self._op = heads, vals, out, op
+        self.ws = _lib.workspace(self.lib.gnn_edge_softmax_workspace(C.byref(self.plan), heads),
+                                 self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_segment_sum(C.byref(self.view), C.byref(self.plan), self.heads,
+                                            self.vals.data_ptr(), self.out.data_ptr(),
+                                            self.ws.data_ptr(), self.ws.numel(),
+                                            _lib.stream_handle(self.dev)), "segment_sum")

@@ -284,7 +284,7 @@ class _GATAggregate(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dout):
         from .kernels import (AttnProjBwdCall, ColsumCall, EdgeSoftmaxCall, HeadMeanCall,
-                              MaskNormColsumCall, SddmmCall)
+                              MaskNormColsumCall, SddmmCall, SegmentSumCall)
 
         Wh, a_l, a_r, alpha, el, er, out = ctx.saved_tensors
         g, H = ctx.g, ctx.heads
@@ -309,9 +309,10 @@ class _GATAggregate(torch.autograd.Function):
         SddmmCall(A, dY, Wh, ds, heads=H)()                       # dalpha
         EdgeSoftmaxCall(A, H, ds, el=el, er=er, slope=ctx.slope, backward=True, alpha=alpha,
                         dalpha=ds)()                               # ds (in place)
-        ones = torch.ones(V, H, dtype=torch.float32, device=dev)
-        der = spmm_raw(A, ones, heads=H, vals=ds)
-        del_ = spmm_raw(AT, ones, heads=H, vals=ds, eid=AT.eid)
+        der = torch.empty(V, H, dtype=torch.float32, device=dev)
+        del_ = torch.empty_like(der)
+        SegmentSumCall(A, ds, der, H)()
+        SegmentSumCall(AT, ds, del_, H, use_eid=True)()
         da_l = torch.empty_like(a_l)
         da_r = torch.empty_like(a_r)
         AttnProjBwdCall(Wh, a_l, a_r, del_, der, dWh, da_l, da_r, H)()
@@ -516,7 +517,7 @@ class GATTrainer(_FusedEpoch):
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
                  lr=0.01, slope=0.2, seed: int = 0):
         from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
-                              HeadMeanCall, SddmmCall, XentCall)
+                              HeadMeanCall, SddmmCall, SegmentSumCall)
 
         self.g = g
         dev = g.device
@@ -565,7 +566,6 @@ class GATTrainer(_FusedEpoch):
         self.dYc2, self.dWh2 = e(V, K2), e(V, K2)
         self.ds = e(E, H)
         self.der, self.del_ = e(V, H), e(V, H)
-        self.ones = torch.ones(V, H, **f32)
         self.dY1, self.dY1m, self.dWh1 = e(V, K1), e(V, K1), e(V, K1)
         self.loss = torch.zeros(1, **f32)
         Bf, R = _lib.EPI_BIAS, _lib.EPI_RELU
@@ -589,8 +589,8 @@ class GATTrainer(_FusedEpoch):
         k["sddmm2"] = SddmmCall(A, self.dYc2, self.Wh2, self.ds, heads=H)
         k["softmax2_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el2, er=self.er2, slope=slope,
                                             backward=True, alpha=self.alpha2, dalpha=self.ds)
-        k["der2"] = SpmmCall(A, self.ones, self.der, heads=H, vals=self.ds)
-        k["del2"] = SpmmCall(AT, self.ones, self.del_, heads=H, vals=self.ds, eid=AT.eid)
+        k["der2"] = SegmentSumCall(A, self.ds, self.der, H)
+        k["del2"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
         k["proj2_bwd"] = AttnProjBwdCall(self.Wh2, self.al2, self.ar2, self.del_, self.der,
                                          self.dWh2, self.dal2, self.dar2, H)
         k["Y1^T.dWh2"] = GemmCall(self.Y1, self.dWh2, self.dW2, trans_a=True)
@@ -601,8 +601,8 @@ class GATTrainer(_FusedEpoch):
         k["sddmm1"] = SddmmCall(A, self.dY1m, self.Wh1, self.ds, heads=H)
         k["softmax1_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el1, er=self.er1, slope=slope,
                                             backward=True, alpha=self.alpha1, dalpha=self.ds)
-        k["der1"] = SpmmCall(A, self.ones, self.der, heads=H, vals=self.ds)
-        k["del1"] = SpmmCall(AT, self.ones, self.del_, heads=H, vals=self.ds, eid=AT.eid)
+        k["der1"] = SegmentSumCall(A, self.ds, self.der, H)
+        k["del1"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
         k["proj1_bwd"] = AttnProjBwdCall(self.Wh1, self.al1, self.ar1, self.del_, self.der,
                                          self.dWh1, self.dal1, self.dar1, H)
         k["X^T.dWh1"] = GemmCall(self.X, self.dWh1, self.dW1, trans_a=True)

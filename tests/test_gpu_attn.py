@@ -227,3 +227,28 @@ def test_gat_model_trains(gb, graphs):
         opt.step()
         losses.append(loss.item())
     assert losses[-1] < losses[0] - 0.1
+
+
+@pytest.mark.parametrize("gname", GNAMES)
+@pytest.mark.parametrize("heads", [1, 4, 6])
+def test_segment_sum_rows_and_columns(gb, graphs, gname, heads):
+    from paper_2605_29346_b200.kernels import SegmentSumCall
+
+    g = graphs[gname]
+    V, E = g.num_vertices, g.num_edges
+    rng = np.random.default_rng(heads)
+    vals = rng.normal(size=(E, heads)).astype(np.float32)
+    vt = torch.from_numpy(vals).cuda()
+    rows = torch.empty(V, heads, device="cuda")
+    cols = torch.empty(V, heads, device="cuda")
+    SegmentSumCall(g.csr(), vt, rows, heads)()
+    SegmentSumCall(g.csc(with_eid=True), vt, cols, heads, use_eid=True)()
+    ones = np.ones((V, heads))
+    ref_r = oo.spmm(g.offsets, g.targets, ones, vals=vals, heads=heads)
+    ref_c = np.zeros((V, heads))
+    np.add.at(ref_c, g.targets, vals.astype(np.float64))
+    abs_r = oo.spmm(g.offsets, g.targets, ones, vals=np.abs(vals), heads=heads)
+    abs_c = np.zeros((V, heads))
+    np.add.at(abs_c, g.targets, np.abs(vals).astype(np.float64))
+    assert_close(rows, ref_r, abs_r, "row sums")
+    assert_close(cols, ref_c, abs_c, "column sums via edge-ID")

@@ -86,3 +86,24 @@ def test_gemm_tn_weight_gradient(gb, K, M, ld, N):
     ref = a.T.astype(np.float64) @ d.astype(np.float64)
     ok, worst = oo.close(G.cpu().numpy(), ref, np.abs(a.T).astype(np.float64) @ np.abs(d))
     assert ok, worst
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 192, 300_000), (100, 64, 200_000), (602, 64, 50_000),
+                                   (16, 16, 4096), (64, 64, 1000), (33, 130, 5000)])
+def test_weight_gradient_gemm_tn_shapes(M, N, K):
+    """C = A^T B over a long vertex dimension on the tcgen05 MN-major path
+    (N tiles of 32/64/128 columns, OOB-filled M tiles)."""
+    import numpy as np
+    import torch
+
+    from oracle import ops as oo
+    from paper_2605_29346_b200.ops import gemm
+
+    rng = np.random.default_rng(M + N)
+    A = rng.uniform(-1, 1, (K, M)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C = gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), trans_a=True)
+    ref = A.astype(np.float64).T @ B.astype(np.float64)
+    ra = np.abs(A).astype(np.float64).T @ np.abs(B).astype(np.float64)
+    ok, worst = oo.close(C.cpu().numpy(), ref, ra)
+    assert ok, worst

@@ -1,0 +1,151 @@
+"""Model-level measurements beside bench.py's headline (GCN epoch):
+
+  gin      2-layer GIN epoch, Reddit shape (K=602 -> 64 -> 41)        [BASELINE configs[2]]
+  gat      2-layer GAT epoch, products shape (K=100 -> 4x16 -> 4x47)   [BASELINE configs[3]]
+  sweep    SpMMv / SpMMve K sweep 16..256, Reddit shape               [BASELINE configs[1]]
+
+Prints one JSON object per item: device-timed ms (CUDA-graph replay), per-
+kernel ms inside eager epochs, peak memory.  Usage:
+    python tools/bench_models.py gin gat sweep
+"""
+import json
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2605_29346_b200 as gb
+from paper_2605_29346_b200 import _lib
+from paper_2605_29346_b200.kernels import SpmmCall
+
+REDDIT = dict(V=232_965, E=114_615_892)
+PRODUCTS = dict(V=2_449_029, E=123_718_280)
+
+
+def peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(os.path.dirname(__file__), "..",
+                                                 "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def time_graph(tr, steps=10, warmup=3):
+    tr.capture()
+    for _ in range(warmup):
+        tr.run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        tr.run()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def kernel_ms(tr, reps=3):
+    per = [tr.timed_step() for _ in range(reps)]
+    return {k: round(statistics.median(p[k] for p in per), 4) for k in per[0]}
+
+
+def run_gin():
+    from paper_2605_29346_b200.models import GINTrainer
+
+    g = gb.generate(gb.GraphGenSpec("power-law", REDDIT["V"], REDDIT["E"], exponent=2.1), 42)
+    V = g.num_vertices
+    torch.cuda.reset_peak_memory_stats()
+    tr = GINTrainer(g, 602, 64, 41, seed=42, coalesced=True)
+    g.drop_csc()
+    X = torch.rand(V, 602) * 2e-3 - 1e-3
+    y = torch.randint(0, 41, (V,))
+    tr.set_inputs(X, y)
+    c0 = _lib.lib().gnn_launch_counter()
+    tr.step()
+    torch.cuda.synchronize()
+    launches = _lib.lib().gnn_launch_counter() - c0
+    ms = time_graph(tr)
+    return {"item": "gin_epoch_ms", "workload": "2-layer GIN (hidden 64) full-graph epoch, Reddit shape",
+            "ms": round(ms, 4), "launches_per_step": int(launches), "kernels_ms": kernel_ms(tr),
+            "peak_mb": round(torch.cuda.max_memory_allocated() / 2**20, 1),
+            "loss": float(tr.loss.item())}
+
+
+def run_gat():
+    from paper_2605_29346_b200.models import GATTrainer
+
+    t0 = time.perf_counter()
+    g = gb.generate(gb.GraphGenSpec("power-law", PRODUCTS["V"], PRODUCTS["E"], exponent=2.1), 42)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    V = g.num_vertices
+    torch.cuda.reset_peak_memory_stats()
+    tr = GATTrainer(g, 100, 16, 47, heads=4, seed=42)
+    X = torch.rand(V, 100) * 2 - 1
+    y = torch.randint(0, 47, (V,))
+    tr.set_inputs(X, y)
+    c0 = _lib.lib().gnn_launch_counter()
+    tr.step()
+    torch.cuda.synchronize()
+    launches = _lib.lib().gnn_launch_counter() - c0
+    ms = time_graph(tr)
+    km = kernel_ms(tr)
+    E, H = g.num_edges, 4
+    # SURVEY §8d official bytes: fused score+softmax 8(V+1)+4E+8VH+4EH; SDDMM F=16 per head
+    b_soft = 8 * (V + 1) + 4 * E + 8 * V * H + 4 * E * H
+    b_sddmm1 = 8 * (V + 1) + 4 * E + 8 * V * H * 16 + 4 * E * H
+    hbm = peak_hbm()
+    return {"item": "gat_epoch_ms",
+            "workload": "2-layer GAT (4 heads x 16 hidden, 4 x 47 out averaged) full-graph epoch, products shape",
+            "ms": round(ms, 4), "launches_per_step": int(launches), "kernels_ms": km,
+            "softmax1_gbs": round(b_soft / (km["softmax1"] * 1e-3) / 1e9, 1),
+            "sddmm1_gbs": round(b_sddmm1 / (km["sddmm1"] * 1e-3) / 1e9, 1), "hbm_peak": hbm,
+            "peak_mb": round(torch.cuda.max_memory_allocated() / 2**20, 1), "generate_s": round(t_gen, 2),
+            "loss": float(tr.loss.item())}
+
+
+def run_sweep():
+    V, E = REDDIT["V"], REDDIT["E"]
+    g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=2.1), 42)
+    g.csc()
+    flush = torch.empty(64 * 2**20, device="cuda")
+    hbm = peak_hbm()
+    out = []
+    ev = torch.rand(E, device="cuda")
+    for K in (16, 32, 64, 128, 256):
+        X = torch.rand(V, K, device="cuda")
+        Y = torch.empty_like(X)
+        row = {"item": "spmm_sweep", "K": K}
+        for name, call in (
+                ("spmmv_norm", SpmmCall(g.csr(), X, Y, flags=_lib.EPI_NORM)),
+                ("spmmv_norm_coalesced", SpmmCall(g.csr_coalesced(), X, Y, flags=_lib.EPI_NORM)),
+                ("spmmve", SpmmCall(g.csr(), X, Y, vals=ev)),
+                ("spmmvT", SpmmCall(g.csc(), X, Y))):
+            ts = []
+            for _ in range(12):
+                flush.add_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                call()
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            ms = statistics.median(ts[2:])
+            byt = 8 * (V + 1) + 4 * E + 8 * V * K + (4 * E if name == "spmmve" else 0)
+            row[name] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
+                         "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 4),
+                         "gather_tbs": round(4 * E * K / (ms * 1e-3) / 1e12, 2)}
+        out.append(row)
+    return out
+
+
+if __name__ == "__main__":
+    for item in sys.argv[1:] or ["gin", "gat", "sweep"]:
+        r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep}[item]()
+        for x in (r if isinstance(r, list) else [r]):
+            print(json.dumps(x), flush=True)
+        torch.cuda.empty_cache()
