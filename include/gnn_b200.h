@@ -299,6 +299,20 @@ int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
                  const float *b, const int64_t *labels, const int64_t *deg_offsets, float *dP,
                  int64_t lddp, float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
                  gnn_stream_t stream);
+/* Same with an explicit loss/gradient scale: *loss = grad_scale * sum_r (lse - z_y),
+ * dZ = (softmax - onehot) * grad_scale.  A row-partitioned rank passes 1/V_global so
+ * the all-reduced loss and gradients equal the single-GPU mean. */
+int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
+                        const float *W, const float *b, const int64_t *labels,
+                        const int64_t *deg_offsets, float grad_scale, float *dP, int64_t lddp,
+                        float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
+                        gnn_stream_t stream);
+
+/* Remap global vertex ids to positions in a row-partitioned, padded exchange
+ * buffer: owner p = max{q : bounds[q] <= id}; out = p * block_stride + (id - bounds[p]).
+ * bounds[0..P] nondecreasing (SURVEY §8e 1D row partition). */
+int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bounds, int64_t P,
+                  int64_t block_stride, int32_t *out, gnn_stream_t stream);
 
 /* Adam over a device table of parameters; the step counter lives on device
  * (read for bias correction, then incremented) so the update can sit inside

@@ -198,6 +198,12 @@ SIGNATURES = {
         [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr,
          c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_gcn_head_scaled": (
+        c_int,
+        [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, C.c_float, c_ptr, c_i64,
+         c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_remap_ids": (c_int, [c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr]),
     "gnn_adam_step": (
         c_int,
         [c_int, c_ptr, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, c_ptr, c_ptr],

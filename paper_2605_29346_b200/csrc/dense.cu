@@ -693,10 +693,11 @@ size_t gnn_gcn_head_workspace(int64_t M, int64_t Din, int64_t C) {
   return sizeof(float) * (size_t)head_float_slots(nb, Din, C) + sizeof(double) * (size_t)nb + 512;
 }
 
-int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, const float *W,
-                 const float *b, const int64_t *labels, const int64_t *deg_offsets, float *dP,
-                 int64_t lddp, float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
-                 gnn_stream_t stream) {
+int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
+                        const float *W, const float *b, const int64_t *labels,
+                        const int64_t *deg_offsets, float grad_scale, float *dP, int64_t lddp,
+                        float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
+                        gnn_stream_t stream) {
   if (M <= 0 || Din <= 0 || Din > 64 || C <= 0 || C > 64 || !P || ldp < Din || !W || !b ||
       !labels || !dP || lddp < Din || !dW || !db || !loss)
     return GNN_ERR_INVALID_ARGUMENT;
@@ -705,7 +706,7 @@ int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
   const int64_t nb = ceil_div(M, (int64_t)kHeadWarps * kHeadRowsPerWarp);
   float *partials = static_cast<float *>(ws);
   double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
-  const float scale = 1.0f / (float)M;
+  const float scale = grad_scale;
 #define GNN_HEAD(DN)                                                                            \
   gcn_head_kernel<DN><<<(unsigned)nb, 128, 0, st>>>(M, (int)Din, (int)C, P, ldp, W, b, labels, \
                                                     deg_offsets, scale, dP, lddp, partials, lpart)
@@ -718,9 +719,18 @@ int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
 #undef GNN_HEAD
   GNN_LAUNCH_CHECK();
   gcn_head_reduce_kernel<<<(unsigned)ceil_div(Din * C + C + 1, 256), 256, 0, st>>>(
-      nb, (int)Din, (int)C, partials, lpart, dW, db, loss, 1.0f / (float)M);
+      nb, (int)Din, (int)C, partials, lpart, dW, db, loss, grad_scale);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
+}
+
+int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, const float *W,
+                 const float *b, const int64_t *labels, const int64_t *deg_offsets, float *dP,
+                 int64_t lddp, float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
+                 gnn_stream_t stream) {
+  if (M <= 0) return GNN_ERR_INVALID_ARGUMENT;
+  return gnn_gcn_head_scaled(M, Din, C, P, ldp, W, b, labels, deg_offsets, 1.0f / (float)M, dP,
+                             lddp, dW, db, loss, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -739,3 +739,41 @@ int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t stat
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ row-partition id remap
+namespace gnn {
+namespace {
+__global__ void remap_ids_kernel(int64_t n, const int32_t *__restrict__ ids,
+                                 const int64_t *__restrict__ bounds, int64_t P, int64_t stride,
+                                 int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = ids[i];
+    int64_t lo = 0, hi = P;  // largest q in [0,P) with bounds[q] <= id
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (bounds[mid] <= id)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    out[i] = (int32_t)(lo * stride + (id - bounds[lo]));
+  }
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bounds, int64_t P,
+                             int64_t block_stride, int32_t *out, gnn_stream_t stream) {
+  using namespace gnn;
+  if (n < 0 || P <= 0 || block_stride <= 0 || (n > 0 && (!ids || !bounds || !out)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (P * block_stride >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (n == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  int64_t blocks = ceil_div(n, 256), cap = (int64_t)sm_count() * 16;
+  remap_ids_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, st>>>(n, ids, bounds, P,
+                                                                            block_stride, out);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}

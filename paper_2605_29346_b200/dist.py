@@ -1,0 +1,285 @@
+"""1D row-partitioned multi-GPU GCN training.
+
+One process per GPU.  Rank p owns the vertex range [bounds[p], bounds[p+1])
+— contiguous row blocks balanced by EDGE count, not vertex count (the
+power-law skew puts 28% of Reddit's edges in 115 rows) — and holds
+
+  * its rows of the CSR (forward aggregation) and its rows of the CSC
+    (= in-edges of its vertices, for the backward aggregation; SURVEY §8e
+    option 1, symmetric with the forward so the kernels are identical);
+  * column ids remapped once, on device, from global vertex ids to positions
+    in a padded exchange buffer [P * Bmax, width]: vertex v of block q lives
+    at q * Bmax + (v - bounds[q]).
+
+Every layer writes its rows straight into its own slot of that buffer, and
+one in-place all-gather (NCCL over NVLink / NVSwitch) fills the other slots
+before the aggregation that needs them: four [V, hidden] all-gathers per GCN
+epoch (H1, Y1 forward; dP2, dZ1 backward) plus one all-reduce of the ~42 KB of
+weight gradients and the loss.  The exchanges are pluggable so the same
+schedule runs on NCCL (``TorchDistExchange``) or as P virtual ranks inside one
+process (``LocalExchange``, used by the single-GPU parity tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import CsrGraph, SparseOperand
+from .kernels import AdamCall, GemmCall, MaskNormColsumCall, SpmmCall
+from .models import glorot
+
+
+# ----------------------------------------------------------- host logic
+def partition_bounds(offsets: np.ndarray, parts: int) -> np.ndarray:
+    """Row boundaries [P+1] of contiguous blocks holding ~E/P edges each
+    (searchsorted on the CSR offsets; every block non-empty when V >= P)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    V = offsets.size - 1
+    E = int(offsets[-1])
+    if parts <= 0:
+        raise ValueError("parts must be positive")
+    targets = (E * np.arange(parts + 1, dtype=np.float64) / parts).astype(np.int64)
+    b = np.searchsorted(offsets, targets, side="left").astype(np.int64)
+    b[0], b[-1] = 0, V
+    b = np.maximum.accumulate(np.minimum(b, V))
+    # keep every block non-empty in rows when possible (P <= V)
+    if V >= parts:
+        for p in range(1, parts):
+            b[p] = min(max(b[p], b[p - 1] + 1), V - (parts - p))
+    return b
+
+
+def remap_ids_host(ids: np.ndarray, bounds: np.ndarray, stride: int) -> np.ndarray:
+    """Host statement of gnn_remap_ids (used by the CPU tests)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    owner = np.searchsorted(bounds[1:-1], ids, side="right")
+    return (owner * stride + ids - bounds[owner]).astype(np.int32)
+
+
+def block_stride(bounds: np.ndarray) -> int:
+    return int(max(1, np.max(np.diff(bounds))))
+
+
+# ---------------------------------------------------------- exchanges
+class TorchDistExchange:
+    """All-gather / all-reduce through torch.distributed (NCCL on GPUs, gloo
+    on CPU for the host-logic tests).  The all-gather is in place: the local
+    block already sits in its slot of the padded buffer."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather(self, full: torch.Tensor, stride_rows: int):
+        d = self.dist
+        mine = full[self.rank * stride_rows:(self.rank + 1) * stride_rows]
+        if d.get_backend(self.group) == "nccl":
+            d.all_gather_into_tensor(full, mine, group=self.group)
+        else:
+            parts = list(full.split(stride_rows))
+            d.all_gather(parts, mine.clone(), group=self.group)
+
+    def all_reduce(self, t: torch.Tensor):
+        self.dist.all_reduce(t, group=self.group)
+
+
+class LocalExchange:
+    """P virtual ranks in one process (one GPU): the exchanges copy slots
+    between the ranks' buffers.  Used to test the partitioned schedule."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.pending = {}
+
+    def all_gather_many(self, fulls, stride_rows):
+        for q, src in enumerate(fulls):
+            blk = src[q * stride_rows:(q + 1) * stride_rows]
+            for p, dst in enumerate(fulls):
+                if p != q:
+                    dst[q * stride_rows:(q + 1) * stride_rows].copy_(blk)
+
+    def all_reduce_many(self, ts):
+        tot = torch.stack(ts).sum(0)
+        for t in ts:
+            t.copy_(tot)
+
+
+# ------------------------------------------------------------ partition
+class RowPartition:
+    """Rank ``rank``'s share of graph ``g`` (global CSR/CSC on this device)."""
+
+    def __init__(self, g: CsrGraph, parts: int, rank: int, *, coalesced: bool = True,
+                 bounds: np.ndarray | None = None):
+        self.g, self.parts, self.rank = g, parts, rank
+        dev = g.device
+        self.bounds = partition_bounds(g.offsets, parts) if bounds is None else np.asarray(bounds)
+        self.stride = block_stride(self.bounds)
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.rows = self.hi - self.lo
+        self.d_bounds = torch.from_numpy(self.bounds.astype(np.int64)).to(dev)
+        cols_total = parts * self.stride
+        # canonical row degrees of the owned rows (every degree-norm uses them)
+        self.deg_offsets = (g.d_offsets[self.lo:self.hi + 1] - g.d_offsets[self.lo]).contiguous()
+        if coalesced:
+            A, AT = g.csr_coalesced(), g.csc_coalesced()
+        else:
+            A, AT = g.csr(), g.csc()
+        self.A = self._slice(A, cols_total, deg=self.deg_offsets)
+        self.AT = self._slice(AT, cols_total, deg=None)
+
+    def _slice(self, op: SparseOperand, cols_total: int, deg) -> SparseOperand:
+        lib = _lib.lib()
+        off = op.offsets[self.lo:self.hi + 1]
+        e0, e1 = int(off[0].item()), int(off[-1].item())
+        loc_off = (off - e0).contiguous()
+        cols = op.cols[e0:e1]
+        out = torch.empty(e1 - e0, dtype=torch.int32, device=cols.device)
+        with torch.cuda.device(cols.device):
+            _lib.check(lib.gnn_remap_ids(e1 - e0, cols.data_ptr() if e1 > e0 else None,
+                                         self.d_bounds.data_ptr(), self.parts, self.stride,
+                                         out.data_ptr() if e1 > e0 else None,
+                                         _lib.stream_handle(cols.device)), "remap_ids")
+        vals = op.vals[e0:e1].contiguous() if op.vals is not None else None
+        return SparseOperand(self.rows, cols_total, loc_off, out, vals=vals,
+                             deg_offsets=deg if deg is not None else None)
+
+    def local_rows(self, t: torch.Tensor) -> torch.Tensor:
+        return t[self.lo:self.hi]
+
+
+# ------------------------------------------------------------- trainer
+class DistGCNTrainer:
+    """One rank of the row-partitioned 2-layer GCN epoch (same math and
+    kernels as ``models.GCNTrainer``; see the module docstring).
+
+    Phases (exchanges between them):
+      A  H1[slot] = X_loc W1                         -> all-gather H1
+      B  Y1[slot] = relu(D^-1 A_loc H1 + b1)          -> all-gather Y1
+      C  P2 = D^-1 A_loc Y1; head (loss scaled 1/V): dP2[slot], dW2, db2
+                                                     -> all-gather dP2
+      D  dZ1 = (A^T_loc dP2) * [Y1 > 0]; dZ1n[slot] = D^-1 dZ1, db1
+                                                     -> all-gather dZ1n
+      E  dH1 = A^T_loc dZ1n; dW1 = X_loc^T dH1       -> all-reduce grads+loss
+      F  Adam (identical on every rank)
+    """
+
+    def __init__(self, part: RowPartition, in_feats: int, hidden: int, classes: int, *,
+                 lr=0.01, seed: int = 0):
+        from .kernels import HeadCall
+
+        self.part = part
+        g = part.g
+        dev = g.device
+        self.dev = dev
+        V, n, S, P = g.num_vertices, part.rows, part.stride, part.parts
+        self.V, self.F, self.Hd, self.C = V, in_feats, hidden, classes
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.W1 = torch.from_numpy(glorot(in_feats, hidden, seed, 0)).to(dev)
+        self.b1 = torch.zeros(hidden, **f32)
+        self.W2 = torch.from_numpy(glorot(hidden, classes, seed, 2)).to(dev)
+        self.b2 = torch.zeros(classes, **f32)
+        # one flat gradient buffer (+ loss) -> a single all-reduce
+        sizes = [in_feats * hidden, hidden, hidden * classes, classes, 1]
+        self.flat = torch.zeros(sum(sizes), **f32)
+        views = list(self.flat.split(sizes))
+        self.dW1 = views[0].view(in_feats, hidden)
+        self.db1, self.db2 = views[1], views[3]
+        self.dW2 = views[2].view(hidden, classes)
+        self.loss = views[4]
+        self.Fpad = -(-in_feats // 32) * 32
+        self._Xstore = torch.zeros(max(n, 1), self.Fpad, **f32)
+        self.X = self._Xstore[:n, :in_feats]
+        self.labels = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)[:n]
+        full = lambda: torch.zeros(P * S, hidden, **f32)  # noqa: E731
+        self.H1f, self.Y1f, self.dP2f, self.dZ1f = full(), full(), full(), full()
+        sl = slice(part.rank * S, part.rank * S + n)
+        self.H1, self.Y1 = self.H1f[sl], self.Y1f[sl]
+        self.dP2, self.dZ1n = self.dP2f[sl], self.dZ1f[sl]
+        e = lambda: torch.empty(max(n, 1), hidden, **f32)[:n]  # noqa: E731
+        self.P2, self.dZ1, self.dH1 = e(), e(), e()
+        A, AT = part.A, part.AT
+        N_, B_, R_, M_ = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        deg = part.deg_offsets
+        self.phases = []
+        if n > 0:
+            k_gemm1 = GemmCall(self.X, self.W1, self.H1)
+            k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
+            k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
+            k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
+                              self.db2, self.loss, deg_offsets=deg)
+            k_head.scale = 1.0 / V
+            k_bagg2 = SpmmCall(AT, self.dP2f, self.dZ1, flags=M_, mask=self.Y1)
+            k_norm1 = MaskNormColsumCall(self.dZ1, self.dZ1n, deg_offsets=deg, colsum=self.db1)
+            k_bagg1 = SpmmCall(AT, self.dZ1f, self.dH1)
+            k_dW1 = GemmCall(self.X, self.dH1, self.dW1, trans_a=True)
+            zero = lambda: None  # noqa: E731
+        else:  # a rank without rows still takes part in every exchange
+            k_gemm1 = k_agg1 = k_agg2 = k_bagg2 = k_norm1 = k_bagg1 = k_dW1 = lambda: None  # noqa: E731
+            k_head = None
+            zero = self.flat.zero_
+        self._head = k_head
+        self.phases = [
+            ("A", [("X.W1", k_gemm1)], ("gather", self.H1f)),
+            ("B", [("agg1", k_agg1)], ("gather", self.Y1f)),
+            ("C", [("agg2", k_agg2), ("head", self._run_head if n > 0 else zero)],
+             ("gather", self.dP2f)),
+            ("D", [("bagg2", k_bagg2), ("mask_norm_db1", k_norm1)], ("gather", self.dZ1f)),
+            ("E", [("bagg1", k_bagg1), ("X^T.dH1", k_dW1)], ("reduce", self.flat)),
+        ]
+        self.k_adam = AdamCall([self.W1, self.b1, self.W2, self.b2],
+                               [self.dW1, self.db1, self.dW2, self.db2], lr=lr)
+
+    def _run_head(self):
+        h = self._head
+        _lib.check(h.lib.gnn_gcn_head_scaled(
+            h.M, h.Din, h.C, h.P.data_ptr(), h.P.stride(0), h.W.data_ptr(), h.b.data_ptr(),
+            h.labels.data_ptr(), h.deg.data_ptr(), h.scale, h.dP.data_ptr(), h.dP.stride(0),
+            h.dW.data_ptr(), h.db.data_ptr(), h.loss.data_ptr(), h.ws.data_ptr(), h.ws.numel(),
+            _lib.stream_handle(h.dev)), "gcn_head")
+
+    def set_inputs(self, X_local, labels_local, non_blocking=False):
+        self.X.copy_(X_local, non_blocking=non_blocking)
+        self.labels.copy_(labels_local, non_blocking=non_blocking)
+
+    def step(self, ex: TorchDistExchange):
+        S = self.part.stride
+        for _, calls, (kind, buf) in self.phases:
+            for _, c in calls:
+                c()
+            if kind == "gather":
+                ex.all_gather(buf, S)
+            else:
+                ex.all_reduce(buf)
+        self.k_adam()
+        return self.loss
+
+    def params(self):
+        return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}
+
+    def grads(self):
+        return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
+
+
+def step_virtual(trainers, ex: LocalExchange, adam: bool = True):
+    """One epoch of P virtual ranks (``trainers[p]`` = rank p) in lockstep."""
+    S = trainers[0].part.stride
+    for i in range(len(trainers[0].phases)):
+        for t in trainers:
+            for _, c in t.phases[i][1]:
+                c()
+        kind = trainers[0].phases[i][2][0]
+        bufs = [t.phases[i][2][1] for t in trainers]
+        if kind == "gather":
+            ex.all_gather_many(bufs, S)
+        else:
+            ex.all_reduce_many(bufs)
+    if adam:
+        for t in trainers:
+            t.k_adam()
+    return trainers[0].loss

@@ -1,0 +1,81 @@
+"""GPU: the row-partitioned GCN schedule (paper_2605_29346_b200.dist) run as
+P virtual ranks on one B200 (exchanges = slot copies), against the float64
+single-process oracle and the single-GPU fused trainer; plus the device id
+remap against its host statement."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import graph as og
+from oracle import ops as oo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(cuda):
+    import paper_2605_29346_b200 as gb
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 2708, 10556, exponent=2.1), 42)
+    rng = np.random.default_rng(np.random.SeedSequence(0, spawn_key=(10,)))
+    X = rng.uniform(-1, 1, (2708, 64)).astype(np.float32)
+    y = np.random.default_rng(1).integers(0, 7, 2708)
+    return gb, g, X, y
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+@pytest.mark.parametrize("coalesced", [False, True])
+def test_virtual_ranks_match_oracle(env, P, coalesced):
+    from paper_2605_29346_b200.dist import DistGCNTrainer, LocalExchange, RowPartition, step_virtual
+
+    gb, g, X, y = env
+    V = g.num_vertices
+    parts = [RowPartition(g, P, r, coalesced=coalesced) for r in range(P)]
+    trs = [DistGCNTrainer(p, 64, 16, 7, seed=0) for p in parts]
+    for p, t in zip(parts, trs):
+        t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
+    step_virtual(trs, LocalExchange(P), adam=False)
+    torch.cuda.synchronize()
+    off, tgt = g.offsets, g.targets
+    t_off, t_rows, _ = og.transpose(V, V, off, tgt)
+    pr = {k: v.double().cpu().numpy() for k, v in trs[0].params().items()}
+    ref = oo.gcn2_step(off, tgt, t_off, t_rows, X, pr["W1"], pr["b1"], pr["W2"], pr["b2"], y)
+    for t in trs:
+        assert abs(t.loss.item() - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+        for k, gv in t.grads().items():
+            ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
+            assert ok, (P, k, worst)
+
+
+def test_virtual_ranks_train_like_single_gpu(env):
+    from paper_2605_29346_b200.dist import DistGCNTrainer, LocalExchange, RowPartition, step_virtual
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    gb, g, X, y = env
+    single = GCNTrainer(g, 64, 16, 7, seed=0, coalesced=True)
+    single.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+    parts = [RowPartition(g, 2, r) for r in range(2)]
+    trs = [DistGCNTrainer(p, 64, 16, 7, seed=0) for p in parts]
+    for p, t in zip(parts, trs):
+        t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
+    ex = LocalExchange(2)
+    for _ in range(5):
+        ls = single.step().item()
+        ld = step_virtual(trs, ex).item()
+        assert abs(ls - ld) <= 1e-4 * abs(ls)
+    for k, v in single.params().items():
+        assert torch.allclose(v, trs[0].params()[k], rtol=1e-4, atol=1e-6)
+        assert torch.equal(trs[0].params()[k], trs[1].params()[k])  # replicas stay identical
+
+
+def test_remap_kernel_matches_host(env):
+    from paper_2605_29346_b200.dist import RowPartition, remap_ids_host
+
+    gb, g, X, y = env
+    for P in (2, 4):
+        for r in range(P):
+            part = RowPartition(g, P, r, coalesced=False)
+            off, tgt = g.offsets, g.targets
+            ref = remap_ids_host(tgt[off[part.lo]:off[part.hi]], part.bounds, part.stride)
+            assert np.array_equal(part.A.cols.cpu().numpy(), ref)
