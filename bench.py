@@ -32,6 +32,14 @@ REDDIT = dict(V=232_965, E=114_615_892, F=602, H=16, C=41, exponent=2.1, seed=42
 L2_BYTES = 126 * 1024 * 1024
 
 
+def local_device() -> int:
+    """GPU of this rank: LOCAL_RANK (wrapped onto the visible devices, so a
+    gloo test run can put several ranks on one GPU)."""
+    import torch
+
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -112,6 +120,28 @@ class ClockSampler:
 def spmm_bytes(V, E, K):
     """SURVEY.md §8d official algorithmic bytes of one SpMMv: 8(V+1)+4E+4VK+4VK."""
     return 8 * (V + 1) + 4 * E + 8 * V * K
+
+
+def l2_read_gbs(lib, dev, mb=48, reps=200):
+    """Measured L2 -> SM read bandwidth (GB/s): an L2-resident buffer streamed
+    with 128-bit loads by every SM (gnn_read_probe)."""
+    import torch
+
+    n = mb * 2**20 // 4
+    buf = torch.rand(n, device=dev)
+    out = torch.zeros(1, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        lib.gnn_read_probe(buf.data_ptr(), n, reps, out.data_ptr(), st.cuda_stream)
+    ts = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        lib.gnn_read_probe(buf.data_ptr(), n, reps, out.data_ptr(), st.cuda_stream)
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return n * 4 * reps / (min(ts) * 1e-3) / 1e9
 
 
 def flush_l2(buf):
@@ -322,7 +352,11 @@ def run_ours(args, rank, world):
     t32 = k32["csr"]["ms"] if "csr" in k32 else k32["csr_coalesced"]["ms"]
     ach32 = spmm_bytes(V, E, 32) / (t32 * 1e-3) / 1e9
     # hierarchical bound: max(B_comp/BW_hbm, 4EK/BW_L2) with BW_L2 = 2x HBM (nominal)
-    hier32 = max(spmm_bytes(V, E, 32) / (hbm_peak * 1e9), 4 * E * 32 / (2 * hbm_peak * 1e9)) * 1e3
+    # hierarchical bound: max(B_comp/BW_hbm, 4*nnz*K/BW_L2), BW_L2 measured
+    # here by an L2-resident 128-bit read probe (libgnnb200 gnn_read_probe)
+    l2_gbs = l2_read_gbs(lib, dev)
+    nnz32 = g.operand("csr_coalesced" if "csr" not in k32 else "csr").nnz
+    hier32 = max(spmm_bytes(V, E, 32) / (hbm_peak * 1e9), 4 * nnz32 * 32 / (l2_gbs * 1e9)) * 1e3
 
     # BASELINE.md analytic footprint: canonical CSR+CSC (int64 offsets, int32 ids),
     # X, and the epoch's [V,hidden] activations/gradients
@@ -357,7 +391,8 @@ def run_ours(args, rank, world):
                      "bytes_per_launch": b16, "peak_source": peak_src},
         "spmmv_k32": {"ms": t32, "gbs": round(ach32, 1), "frac": round(ach32 / hbm_peak, 4),
                       "hierarchical_bound_ms": round(hier32, 4),
-                      "hierarchical_frac": round(hier32 / t32, 4), "layouts": k32},
+                      "hierarchical_frac": round(hier32 / t32, 4), "l2_read_gbs": round(l2_gbs, 1),
+                      "gather_bytes": 4 * nnz32 * 32, "layouts": k32},
         "kernels_ms": {k: round(v, 4) for k, v in kern_ms.items()},
         "peak_mb": {"train_phase": round(peak_train / 2**20, 1),
                     "allocated_before_train": round(base_alloc / 2**20, 1),
@@ -378,7 +413,110 @@ def run_ours(args, rank, world):
                                          y_h.numpy(), W1, b1, W2, b2)
         res["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "cores": 1,
                                "kind": "port", "sample": desc, **cpu_info()}
+    if not args.no_extras:
+        # the other BASELINE configs, measured in the same run (not the headline)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_models as bm
+
+        del tr
+        torch.cuda.empty_cache()
+        extras = {}
+        for name, fn in (("gin_reddit", bm.run_gin), ("gat_products", bm.run_gat),
+                         ("spmm_sweep_reddit", bm.run_sweep)):
+            try:
+                extras[name] = fn()
+            except Exception as exc:  # report, never hide
+                extras[name] = {"error": repr(exc)[:300]}
+            torch.cuda.empty_cache()
+        res["extras"] = extras
     return res
+
+
+# ------------------------------------------------- our arm, N > 1 ranks
+def run_dist(args, rank, world):
+    """Row-partitioned GCN epoch: every rank generates the same
+    graph on its GPU (bit-exact device generator), keeps its edge-balanced row
+    block of the CSR/CSC, and exchanges [V, hidden] blocks with in-place NCCL
+    all-gathers; one all-reduce of the weight gradients.  Strong scaling: the
+    whole Reddit-shape epoch is fixed, split over N GPUs."""
+    import torch
+
+    import paper_2605_29346_b200 as gb
+    from paper_2605_29346_b200 import _lib
+    from paper_2605_29346_b200.dist import DistGCNTrainer, RowPartition, TorchDistExchange
+
+    dev = torch.device("cuda", local_device())
+    torch.cuda.set_device(dev)
+    lib = _lib.lib()
+    P = REDDIT
+    V, E, F, Hd, C = P["V"], P["E"], P["F"], P["H"], P["C"]
+    g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=P["exponent"]), P["seed"],
+                    device=dev)
+    part = RowPartition(g, world, rank, coalesced=True)
+    g.drop_csc()
+    rng = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(10,)))
+    X_all = rng.random((V, F), dtype=np.float32) * 2 - 1
+    y_all = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(13,))).integers(0, C, V)
+    X_h = torch.from_numpy(np.ascontiguousarray(X_all[part.lo:part.hi])).pin_memory()
+    y_h = torch.from_numpy(np.ascontiguousarray(y_all[part.lo:part.hi])).pin_memory()
+    del X_all
+    torch.cuda.reset_peak_memory_stats(dev)
+    tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"])
+    tr.set_inputs(X_h, y_h)
+    ex = TorchDistExchange()
+    c0 = lib.gnn_launch_counter()
+    tr.step(ex)
+    torch.cuda.synchronize()
+    launches = lib.gnn_launch_counter() - c0
+    for _ in range(args.warmup):
+        tr.step(ex)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    with ClockSampler(dev.index) as clk:
+        st = torch.cuda.current_stream()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(args.steps):
+            tr.step(ex)
+        b.record(st)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    torch.distributed.barrier()
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    a.record(st)
+    for _ in range(args.steps):
+        tr.set_inputs(X_h, y_h, non_blocking=True)
+        tr.step(ex)
+        loss_h.copy_(tr.loss, non_blocking=True)
+    b.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / args.steps
+    t = torch.tensor([ms, e2e_ms], device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    return {
+        "metric": "gcn_epoch_ms", "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device power-law generator, bit-exact gsbench.generate seed 42; "
+                "X~U[-1,1) f32, labels uniform)",
+        "config": {"workload": "2-layer GCN full-graph epoch, Reddit-shape power-law graph, "
+                               "1D row partition (edge-balanced) + NCCL all-gathers",
+                   "V": V, "E": E, "K": F, "hidden": Hd, "classes": C, "layout": "coalesced",
+                   "optimizer": "adam", "parallelism": f"rowpart{world}",
+                   "rows_rank0": part.rows, "bounds": [int(x) for x in part.bounds],
+                   "l2": "inputs larger than L2: no flush needed"},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms",
+                "h2d_bytes_per_step": int(X_h.numel() * 4 + y_h.numel() * 8),
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches * args.steps),
+        "peak_mb": {"train_phase": round(torch.cuda.max_memory_allocated(dev) / 2**20, 1)},
+        "loss": float(tr.loss.item()), "clocks": clk.summary(),
+    }
 
 
 # -------------------------------------------------------- reference arm
@@ -436,6 +574,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--layout", choices=["canonical", "coalesced"], default="coalesced")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the GIN / GAT / SpMM-sweep lines of the other BASELINE configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -449,15 +589,14 @@ def main():
     if world > 1:
         import torch
 
-        torch.distributed.init_process_group("nccl")
-    res = run_ours(args, rank, world)
-    if world > 1:
-        import torch
-
-        t = torch.tensor([res["value"]], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        res["value"] = res["ms_per_step"] = round(float(t.item()), 4)
+        torch.cuda.set_device(local_device())
+        # NCCL over NVLink/NVSwitch; GNN_DIST_BACKEND=gloo lets the partitioned path be
+        # exercised with several ranks sharing one GPU (test only, not a bench number)
+        torch.distributed.init_process_group(os.environ.get("GNN_DIST_BACKEND", "nccl"))
+        res = run_dist(args, rank, world)
         torch.distributed.destroy_process_group()
+    else:
+        res = run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(res), flush=True)
 

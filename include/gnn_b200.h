@@ -62,6 +62,10 @@ const char *gnn_strerror(int status);
 int gnn_last_cuda_error(void);             /* cudaError_t of the last GNN_ERR_CUDA */
 int gnn_device_sm_count(void);             /* SMs of the current device */
 int64_t gnn_launch_counter(void);          /* kernels launched by this library so far */
+/* Diagnostic: every CTA reads buf[0:n_floats) `reps` times (128-bit, L2-cached
+ * loads) — with an L2-resident buffer this measures the L2 -> SM roof that
+ * bounds the SpMM's row gathers.  out receives nothing meaningful. */
+int gnn_read_probe(const float *buf, int64_t n_floats, int reps, float *out, gnn_stream_t stream);
 
 /* ------------------------------------------------------- graph builders */
 /* Stable counting sort of (src,dst) pairs into CSR: offsets[V+1] int64,

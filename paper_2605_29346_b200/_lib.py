@@ -97,6 +97,7 @@ SIGNATURES = {
     "gnn_last_cuda_error": (c_int, []),
     "gnn_device_sm_count": (c_int, []),
     "gnn_launch_counter": (c_i64, []),
+    "gnn_read_probe": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr]),
     "gnn_csr_from_edges_workspace": (c_sz, [c_i64, c_i64]),
     "gnn_csr_from_edges": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_subgraph_csr_workspace": (c_sz, [c_i64, c_i64]),
