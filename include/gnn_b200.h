@@ -244,6 +244,29 @@ int gnn_edge_softmax_bwd(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, i
 int gnn_segment_sum(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
                     const float *vals, float *out, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Fused GAT backward over the CSC (AT must carry the edge-ID array): one
+ * gather of dY per edge feeds both the SpMMve^T and the SDDMM
+ *   dWh[u,:]         = sum_{j in CSC row u} alpha[eid_j, head] * dY[row_j, :]
+ *   dalpha[eid_j, h] = < dY[row_j, head h], Wh[u, head h] >
+ * alpha / dalpha are [nnz, heads] in CSR edge order.  K % 4 == 0, F % 4 == 0,
+ * K <= 512, heads <= 8.  Deterministic. */
+size_t gnn_gat_bwd_csc_workspace(const gnn_spmm_plan_t *plan, int64_t K);
+int gnn_gat_bwd_csc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t heads,
+                    const float *alpha, const float *dY, int64_t ldy, const float *Wh, int64_t ldw,
+                    int64_t K, float *dWh, int64_t ldd, float *dalpha, void *ws, size_t ws_bytes,
+                    gnn_stream_t stream);
+
+/* The same for a head-MEAN output layer, whose concatenated-head gradient is
+ * dZ * scale broadcast to every head (scale = 1/heads): only dZ[v] (F floats)
+ * is gathered per edge, and all heads are produced from it:
+ *   dWh[u, h*F+f]    = scale * sum_j alpha[eid_j, h] * dZ[row_j, f]
+ *   dalpha[eid_j, h] = scale * < dZ[row_j, :], Wh[u, h*F:(h+1)*F] >
+ * Workspace: gnn_gat_bwd_csc_workspace(plan, heads*F).  F % 4 == 0, F <= 128. */
+int gnn_gat_bwd_csc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const float *alpha, const float *dZ, int64_t ldz, float scale,
+                         const float *Wh, int64_t ldw, int64_t F, float *dWh, int64_t ldd,
+                         float *dalpha, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
 /* GAT attention projections (Appendix A.6): el[v,h] = <Wh[v,h,:], a_l[h,:]>,
  * er[v,h] = <Wh[v,h,:], a_r[h,:]>; a_l/a_r are [heads, F]. */
 int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,

@@ -165,6 +165,17 @@ SIGNATURES = {
         c_int,
         [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_gat_bwd_csc_workspace": (c_sz, [C.POINTER(SpmmPlan), c_i64]),
+    "gnn_gat_bwd_csc": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_i64,
+         c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_gat_bwd_csc_mean": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, c_i64, C.c_float, c_ptr,
+         c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
     "gnn_gat_attn_proj": (
         c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "gnn_gat_attn_proj_bwd_workspace": (c_sz, [c_i64, c_i64]),

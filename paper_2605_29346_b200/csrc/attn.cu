@@ -305,7 +305,19 @@ __device__ __forceinline__ void warp_sum_reduce(float (&t)[HM]) {
     for (int h = 0; h < HM; ++h) t[h] += __shfl_xor_sync(kFull, t[h], o);
 }
 
-// Forward statistics + normalisation of one row piece [lo,hi) of row r.
+// Forward statistics + normalisation of one row piece [lo,hi) of row r:
+// pass 1 row max, pass 2 sum of exp(s - max), pass 3 (whole rows) writes
+// alpha — plain max / sum warp trees (an online (m,l) merge in the tree costs
+// two exponentials per level per head).  Scores are recomputed per pass; the
+// column ids and el rows are L1-resident after the first.
+template <int HM>
+__device__ __forceinline__ void warp_max_reduce(float (&t)[HM]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int h = 0; h < HM; ++h) t[h] = fmaxf(t[h], __shfl_xor_sync(kFull, t[h], o));
+}
+
 template <int HM, bool GAT>
 __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, int64_t lo, int64_t hi,
                                               bool whole, float *slot) {
@@ -322,9 +334,16 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
     float s[HM];
     load_scores<HM, GAT>(a, e, erow, s);
 #pragma unroll
-    for (int h = 0; h < HM; ++h) ml_merge(m[h], l[h], s[h], 1.f);
+    for (int h = 0; h < HM; ++h) m[h] = fmaxf(m[h], s[h]);
   }
-  warp_ml_reduce<HM>(m, l);
+  warp_max_reduce<HM>(m);
+  for (int64_t e = lo + lane; e < hi; e += 32) {
+    float s[HM];
+    load_scores<HM, GAT>(a, e, erow, s);
+#pragma unroll
+    for (int h = 0; h < HM; ++h) l[h] += __expf(s[h] - m[h]);
+  }
+  warp_sum_reduce<HM>(l);
   if (!whole) {
     if (lane == 0)
 #pragma unroll
@@ -343,12 +362,12 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
     load_scores<HM, GAT>(a, e, erow, s);
     if (HM == 4 && a.H == 4) {
       *reinterpret_cast<float4 *>(a.alpha + e * 4) =
-          make_float4(expf(s[0] - m[0]) * inv[0], expf(s[1] - m[1]) * inv[1],
-                      expf(s[2] - m[2]) * inv[2], expf(s[3] - m[3]) * inv[3]);
+          make_float4(__expf(s[0] - m[0]) * inv[0], __expf(s[1] - m[1]) * inv[1],
+                      __expf(s[2] - m[2]) * inv[2], __expf(s[3] - m[3]) * inv[3]);
     } else {
 #pragma unroll
       for (int h = 0; h < HM; ++h)
-        if (h < a.H) a.alpha[e * a.H + h] = expf(s[h] - m[h]) * inv[h];
+        if (h < a.H) a.alpha[e * a.H + h] = __expf(s[h] - m[h]) * inv[h];
     }
   }
 }
@@ -501,7 +520,7 @@ __global__ void __launch_bounds__(256) softmax_split_apply_kernel(SoftmaxArgs a)
       load_scores<HM, GAT>(a, e, erow, s);
 #pragma unroll
       for (int h = 0; h < HM; ++h)
-        if (h < a.H) a.alpha[e * a.H + h] = expf(s[h] - m[h]) * inv[h];
+        if (h < a.H) a.alpha[e * a.H + h] = __expf(s[h] - m[h]) * inv[h];
     }
   }
 }
@@ -763,6 +782,375 @@ __global__ void head_mean_bwd_kernel(int64_t V, int H, int64_t F, const float *_
   }
 }
 
+// Reduce 4 per-lane head partials over a G-lane group (G >= 4) with a
+// reduce-scatter butterfly: 2 + 1 shuffles leave each lane one head's
+// partial, then log2(G) - 2 more finish it.  Returns the head sum; *head is
+// the head this lane holds (complete on lanes with (gl & (G/4 - 1)) == 0).
+template <int G>
+__device__ __forceinline__ float reduce4_scatter(const float (&ph)[4], unsigned gmask, int gl,
+                                                 int *head) {
+  const bool b1 = (gl & (G / 2)) != 0, b2 = (gl & (G / 4)) != 0;
+  const float sa = b1 ? ph[0] : ph[2], sb = b1 ? ph[1] : ph[3];
+  const float k0 = (b1 ? ph[2] : ph[0]) + __shfl_xor_sync(gmask, sa, G / 2);
+  const float k1 = (b1 ? ph[3] : ph[1]) + __shfl_xor_sync(gmask, sb, G / 2);
+  float k = (b2 ? k1 : k0) + __shfl_xor_sync(gmask, b2 ? k0 : k1, G / 4);
+#pragma unroll
+  for (int o = G / 8; o > 0; o >>= 1) k += __shfl_xor_sync(gmask, k, o);
+  *head = (b1 ? 2 : 0) + (b2 ? 1 : 0);
+  return k;
+}
+
+// ----------------------------------------- fused GAT backward over the CSC
+// One pass over the CSC (in-edges of every vertex u, with the edge-ID array)
+// computes both products that need dY[v] of every edge (v -> u):
+//   dWh[u,:]          = sum_j alpha[eid_j, head(:)] * dY[v_j, :]      (SpMMve^T)
+//   dalpha[eid_j, h]  = < dY[v_j, head h], Wh[u, head h] >           (SDDMM)
+// so dY is gathered once instead of twice.  Warp per plan chunk of the CSC,
+// one row piece at a time; G lanes per edge x VPL float4 columns; NG = 32/G
+// edges per step, U steps in flight.  Edge indices are loaded 32 at a time by
+// the warp and broadcast by shuffle.  Split rows leave partials that
+// gat_bwd_finalize sums in fixed order.
+struct GatBwdArgs {
+  int64_t R, nnz, P, nwarps;
+  const int64_t *offsets;
+  const int32_t *rows;  // CSC "cols": source vertices v
+  const int32_t *eid;
+  const int32_t *chunk_row;
+  const int32_t *chunk_split;
+  const int32_t *split_rows;
+  int64_t num_split;
+  const int32_t *empty_rows;
+  int64_t num_empty;
+  int H;
+  int64_t F, K;
+  const float *alpha;  // [E, H] CSR order
+  const float *dY;
+  int64_t ldy;
+  const float *Wh;
+  int64_t ldw;
+  float *dWh;
+  int64_t ldd;
+  float *dalpha;       // [E, H] CSR order
+  float *slots;        // [nwarps][2][K]
+};
+
+template <int G, int VPL, int HM, bool POW2>
+__global__ void __launch_bounds__(256, (VPL == 1) ? 3 : 1) gat_bwd_csc_kernel(GatBwdArgs a, int LPH) {
+  constexpr int NG = 32 / G;
+  constexpr int U = VPL >= 3 ? 3 : 4;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (g * G));
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  const bool h4 = HM == 4 && a.H == 4;
+  int64_t col[VPL];
+  int hd[VPL];
+  bool cv[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    col[v] = (int64_t)(v * G + gl) * 4;
+    cv[v] = col[v] < a.K;
+    if (!cv[v]) col[v] = 0;
+    hd[v] = (int)(col[v] / a.F);
+  }
+  RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
+  while (true) {
+    const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if (hi > lo) {
+      const int64_t u = rw.r;
+      float4 self[VPL], acc[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        self[v] = ldg_f4(a.Wh + u * a.ldw + col[v]);
+        acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int nb = (int)min((int64_t)32, hi - b0);
+        int32_t myc = 0, mye = 0;
+        if (lane < nb) {
+          myc = a.rows[b0 + lane];
+          mye = a.eid[b0 + lane];
+        }
+        for (int k0 = 0; k0 < nb; k0 += NG * U) {
+          int32_t c[U], ee[U];
+          bool ok[U];
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+            const int k = k0 + t * NG + g;
+            ok[t] = k < nb;
+            c[t] = __shfl_sync(kFull, myc, k & 31);
+            ee[t] = __shfl_sync(kFull, mye, k & 31);
+          }
+          float4 x[U][VPL];
+          float wg[U][VPL];
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              x[t][v] = ok[t] ? ldg_f4(a.dY + (int64_t)c[t] * a.ldy + col[v])
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            // edge weights issued with the gathers (no second dependent latency)
+            if (h4) {
+              const float4 al = ok[t] ? ldg_f4(a.alpha + (int64_t)ee[t] * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int v = 0; v < VPL; ++v)
+                wg[t][v] = hd[v] == 0 ? al.x : hd[v] == 1 ? al.y : hd[v] == 2 ? al.z : al.w;
+            } else {
+#pragma unroll
+              for (int v = 0; v < VPL; ++v)
+                wg[t][v] = ok[t] ? __ldg(a.alpha + (int64_t)ee[t] * a.H + hd[v]) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+            // SpMMve^T accumulation
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) acc[v] = f4_fma(wg[t][v], x[t][v], acc[v]);
+            // SDDMM: per-head dots with the row's own Wh
+            if constexpr (POW2) {
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+                float p = x[t][v].x * self[v].x;
+                p = fmaf(x[t][v].y, self[v].y, p);
+                p = fmaf(x[t][v].z, self[v].z, p);
+                p = fmaf(x[t][v].w, self[v].w, p);
+                for (int o = 1; o < LPH; o <<= 1) p += __shfl_xor_sync(gmask, p, o);
+                if (ok[t] && cv[v] && (gl & (LPH - 1)) == 0)
+                  a.dalpha[(int64_t)ee[t] * a.H + hd[v]] = p;
+              }
+            } else {
+              float ph[HM];
+#pragma unroll
+              for (int h = 0; h < HM; ++h) ph[h] = 0.f;
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+                float p = x[t][v].x * self[v].x;
+                p = fmaf(x[t][v].y, self[v].y, p);
+                p = fmaf(x[t][v].z, self[v].z, p);
+                p = fmaf(x[t][v].w, self[v].w, p);
+                if (cv[v])
+#pragma unroll
+                  for (int h = 0; h < HM; ++h) ph[h] += h == hd[v] ? p : 0.f;
+              }
+              bool done = false;
+              if constexpr (HM == 4 && G >= 4) {
+                if (a.H == 4) {
+                  int hh;
+                  const float sum = reduce4_scatter<G>(ph, gmask, gl, &hh);
+                  if (ok[t] && (gl & (G / 4 - 1)) == 0) a.dalpha[(int64_t)ee[t] * 4 + hh] = sum;
+                  done = true;
+                }
+              }
+              if (!done) {
+#pragma unroll
+                for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+                  for (int h = 0; h < HM; ++h) ph[h] += __shfl_xor_sync(gmask, ph[h], o);
+                if (ok[t] && gl == 0)
+#pragma unroll
+                  for (int h = 0; h < HM; ++h)
+                    if (h < a.H) a.dalpha[(int64_t)ee[t] * a.H + h] = ph[h];
+              }
+            }
+          }
+        }
+      }
+      // combine the NG groups (fixed xor tree), then store row / partial
+#pragma unroll
+      for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          acc[v] = f4_add(acc[v], make_float4(__shfl_xor_sync(kFull, acc[v].x, o),
+                                              __shfl_xor_sync(kFull, acc[v].y, o),
+                                              __shfl_xor_sync(kFull, acc[v].z, o),
+                                              __shfl_xor_sync(kFull, acc[v].w, o)));
+      const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
+      float *dst = (carry || trail) ? a.slots + (w * 2 + (carry ? 0 : 1)) * a.K : a.dWh + u * a.ldd;
+      if (g == 0)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (cv[v]) *reinterpret_cast<float4 *>(dst + col[v]) = acc[v];
+    }
+    if (rw.re >= e1 || rw.r + 1 >= a.R) break;
+    rw.next();
+  }
+}
+
+// Head-mean output layer: dY of the concatenated heads is dZ / H broadcast
+// to every head, so the kernel gathers only dZ[v] (F floats, not H*F) and
+// produces all heads from it:
+//   dWh[u, h*F + f]  = scale * sum_j alpha[eid_j, h] * dZ[v_j, f]
+//   dalpha[eid_j, h] = scale * < dZ[v_j, :], Wh[u, h*F : (h+1)*F] >
+template <int G, int VPL, int HM>
+__global__ void __launch_bounds__(256, (VPL * HM <= 4) ? 3 : 1) gat_bwd_csc_mean_kernel(GatBwdArgs a, float scale) {
+  constexpr int NG = 32 / G;
+  constexpr int U = 4;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (g * G));
+  const int64_t e0 = w * a.P, e1 = min(e0 + a.P, a.nnz);
+  const bool h4 = HM == 4 && a.H == 4;
+  int64_t col[VPL];
+  bool cv[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    col[v] = (int64_t)(v * G + gl) * 4;
+    cv[v] = col[v] < a.F;
+    if (!cv[v]) col[v] = 0;
+  }
+  RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
+  while (true) {
+    const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if (hi > lo) {
+      const int64_t u = rw.r;
+      float4 self[HM][VPL], acc[HM][VPL];
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          self[h][v] = (h < a.H && cv[v]) ? ldg_f4(a.Wh + u * a.ldw + h * a.F + col[v])
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          acc[h][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+        const int nb = (int)min((int64_t)32, hi - b0);
+        int32_t myc = 0, mye = 0;
+        if (lane < nb) {
+          myc = a.rows[b0 + lane];
+          mye = a.eid[b0 + lane];
+        }
+        for (int k0 = 0; k0 < nb; k0 += NG * U) {
+          int32_t c[U], ee[U];
+          bool ok[U];
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+            const int k = k0 + t * NG + g;
+            ok[t] = k < nb;
+            c[t] = __shfl_sync(kFull, myc, k & 31);
+            ee[t] = __shfl_sync(kFull, mye, k & 31);
+          }
+          float4 x[U][VPL];
+          float wg[U][HM];
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              x[t][v] = (ok[t] && cv[v]) ? ldg_f4(a.dY + (int64_t)c[t] * a.ldy + col[v])
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (h4) {
+              const float4 al = ok[t] ? ldg_f4(a.alpha + (int64_t)ee[t] * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+              wg[t][0] = al.x;
+              wg[t][1] = al.y;
+              wg[t][2] = al.z;
+              wg[t][3] = al.w;
+            } else {
+#pragma unroll
+              for (int h = 0; h < HM; ++h)
+                wg[t][h] = (ok[t] && h < a.H) ? __ldg(a.alpha + (int64_t)ee[t] * a.H + h) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < U; ++t) {
+            float ph[HM];
+#pragma unroll
+            for (int h = 0; h < HM; ++h) {
+              float p = 0.f;
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+                acc[h][v] = f4_fma(wg[t][h], x[t][v], acc[h][v]);
+                p = fmaf(x[t][v].x, self[h][v].x, p);
+                p = fmaf(x[t][v].y, self[h][v].y, p);
+                p = fmaf(x[t][v].z, self[h][v].z, p);
+                p = fmaf(x[t][v].w, self[h][v].w, p);
+              }
+              ph[h] = p;
+            }
+            bool done = false;
+            if constexpr (HM == 4 && G >= 4) {
+              if (a.H == 4) {
+                int hh;
+                const float sum = reduce4_scatter<G>(ph, gmask, gl, &hh);
+                if (ok[t] && (gl & (G / 4 - 1)) == 0) a.dalpha[(int64_t)ee[t] * 4 + hh] = sum * scale;
+                done = true;
+              }
+            }
+            if (!done) {
+#pragma unroll
+              for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+                for (int h = 0; h < HM; ++h) ph[h] += __shfl_xor_sync(gmask, ph[h], o);
+              if (ok[t] && gl == 0)
+#pragma unroll
+                for (int h = 0; h < HM; ++h)
+                  if (h < a.H) a.dalpha[(int64_t)ee[t] * a.H + h] = ph[h] * scale;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            acc[h][v] = f4_add(acc[h][v], make_float4(__shfl_xor_sync(kFull, acc[h][v].x, o),
+                                                      __shfl_xor_sync(kFull, acc[h][v].y, o),
+                                                      __shfl_xor_sync(kFull, acc[h][v].z, o),
+                                                      __shfl_xor_sync(kFull, acc[h][v].w, o)));
+      const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
+      float *dst = (carry || trail) ? a.slots + (w * 2 + (carry ? 0 : 1)) * a.K : a.dWh + u * a.ldd;
+      if (g == 0)
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (h < a.H && cv[v]) {
+              const float4 r = acc[h][v];
+              *reinterpret_cast<float4 *>(dst + h * a.F + col[v]) =
+                  make_float4(r.x * scale, r.y * scale, r.z * scale, r.w * scale);
+            }
+    }
+    if (rw.re >= e1 || rw.r + 1 >= a.R) break;
+    rw.next();
+  }
+}
+
+// Split rows: sum the partials of row s (slot[wa][1], slot[wa+j][0]) in j order.
+__global__ void gat_bwd_finalize_kernel(GatBwdArgs a) {
+  const int64_t s = blockIdx.x;
+  if (s >= a.num_split) return;
+  const int64_t r = a.split_rows[s];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  for (int64_t c = threadIdx.x; c < a.K; c += blockDim.x) {
+    float t = 0.f;
+    for (int64_t j = 0; j <= wb - wa; ++j)
+      t += a.slots[((wa + j) * 2 + (j == 0 ? 1 : 0)) * a.K + c];
+    a.dWh[r * a.ldd + c] = t;
+  }
+}
+
+__global__ void gat_bwd_empty_kernel(GatBwdArgs a) {
+  const int64_t total = a.num_empty * a.K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    a.dWh[(int64_t)a.empty_rows[t / a.K] * a.ldd + t % a.K] = 0.f;
+}
+
+template <int G, int VPL>
+void launch_gat_bwd(const GatBwdArgs &a, bool pow2, int LPH, unsigned grid, cudaStream_t st) {
+  if (pow2)
+    gat_bwd_csc_kernel<G, VPL, 1, true><<<grid, 256, 0, st>>>(a, LPH);
+  else if (a.H <= 4)
+    gat_bwd_csc_kernel<G, VPL, 4, false><<<grid, 256, 0, st>>>(a, LPH);
+  else
+    gat_bwd_csc_kernel<G, VPL, 8, false><<<grid, 256, 0, st>>>(a, LPH);
+}
+
 }  // namespace
 }  // namespace gnn
 
@@ -907,6 +1295,185 @@ int gnn_segment_sum(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_
   if (heads <= 4) return launch_segsum<4>(a, e, st);
   if (heads <= 8) return launch_segsum<8>(a, e, st);
   return launch_segsum<16>(a, e, st);
+}
+
+size_t gnn_gat_bwd_csc_workspace(const gnn_spmm_plan_t *plan, int64_t K) {
+  if (!plan || K <= 0) return 0;
+  return sizeof(float) * (size_t)(plan->num_warps * 2 * K) + 256;
+}
+
+int gnn_gat_bwd_csc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t heads,
+                    const float *alpha, const float *dY, int64_t ldy, const float *Wh, int64_t ldw,
+                    int64_t K, float *dWh, int64_t ldd, float *dalpha, void *ws, size_t ws_bytes,
+                    gnn_stream_t stream) {
+  if (!AT || !plan || heads <= 0 || heads > 8 || K <= 0 || K % heads != 0 || !AT->offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  const int64_t F = K / heads;
+  if (K % 4 || F % 4 || ldy % 4 || ldw % 4 || ldd % 4 || ldy < K || ldw < K || ldd < K)
+    return GNN_ERR_UNSUPPORTED;
+  if (AT->num_rows > 0 && (!dWh || !Wh || !al16(Wh) || !al16(dWh))) return GNN_ERR_INVALID_ARGUMENT;
+  if (AT->nnz > 0 && (!AT->cols || !AT->eid || !alpha || !dY || !dalpha || !al16(dY)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (heads == 4 && (!al16(alpha) || !al16(dalpha))) return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  const int64_t q = K / 4;
+  if (q > 128) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_gat_bwd_csc_workspace(plan, K)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  GatBwdArgs a{};
+  a.R = AT->num_rows;
+  a.nnz = AT->nnz;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.offsets = AT->offsets;
+  a.rows = AT->cols;
+  a.eid = AT->eid;
+  a.chunk_row = plan->chunk_row;
+  a.chunk_split = plan->chunk_split;
+  a.split_rows = plan->split_rows;
+  a.num_split = plan->num_split;
+  a.empty_rows = plan->empty_rows;
+  a.num_empty = plan->num_empty;
+  a.H = (int)heads;
+  a.F = F;
+  a.K = K;
+  a.alpha = alpha;
+  a.dY = dY;
+  a.ldy = ldy;
+  a.Wh = Wh;
+  a.ldw = ldw;
+  a.dWh = dWh;
+  a.ldd = ldd;
+  a.dalpha = dalpha;
+  a.slots = static_cast<float *>(ws);
+  // lane layout: exact fits first (e.g. 48 float4 columns -> 16 lanes x 3)
+  int G, VPL;
+  if (q <= 32) {
+    G = 1;
+    while (G < q) G <<= 1;
+    VPL = 1;
+  } else if (q % 16 == 0 && q / 16 <= 4 && q % 32 != 0) {
+    G = 16;
+    VPL = (int)(q / 16);
+  } else {
+    G = 32;
+    VPL = (int)ceil_div(q, 32);
+  }
+  const int64_t lph = F / 4;
+  const bool pow2 = (lph & (lph - 1)) == 0 && lph <= G && (G * 4) % F == 0;
+  const int LPH = (int)lph;
+  if (a.nwarps > 0) {
+    const unsigned grid = grid_warps(a.nwarps, 256);
+    if (VPL == 1) {
+      switch (G) {
+        case 1: launch_gat_bwd<1, 1>(a, pow2, LPH, grid, st); break;
+        case 2: launch_gat_bwd<2, 1>(a, pow2, LPH, grid, st); break;
+        case 4: launch_gat_bwd<4, 1>(a, pow2, LPH, grid, st); break;
+        case 8: launch_gat_bwd<8, 1>(a, pow2, LPH, grid, st); break;
+        case 16: launch_gat_bwd<16, 1>(a, pow2, LPH, grid, st); break;
+        default: launch_gat_bwd<32, 1>(a, pow2, LPH, grid, st); break;
+      }
+    } else if (G == 16) {
+      if (VPL == 3)
+        launch_gat_bwd<16, 3>(a, pow2, LPH, grid, st);
+      else
+        launch_gat_bwd<16, 2>(a, pow2, LPH, grid, st);  // unreachable in practice (q%32 != 0)
+    } else {
+      if (VPL == 2)
+        launch_gat_bwd<32, 2>(a, pow2, LPH, grid, st);
+      else if (VPL == 3)
+        launch_gat_bwd<32, 3>(a, pow2, LPH, grid, st);
+      else
+        launch_gat_bwd<32, 4>(a, pow2, LPH, grid, st);
+    }
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_split > 0) {
+    gat_bwd_finalize_kernel<<<(unsigned)a.num_split, 128, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_empty > 0) {
+    gat_bwd_empty_kernel<<<grid_1d_a(a.num_empty * K, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+int gnn_gat_bwd_csc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t heads,
+                         const float *alpha, const float *dZ, int64_t ldz, float scale,
+                         const float *Wh, int64_t ldw, int64_t F, float *dWh, int64_t ldd,
+                         float *dalpha, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (!AT || !plan || heads <= 0 || heads > 8 || F <= 0 || !AT->offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  const int64_t K = heads * F;
+  if (F % 4 || ldz % 4 || ldw % 4 || ldd % 4 || ldz < F || ldw < K || ldd < K || F > 128)
+    return GNN_ERR_UNSUPPORTED;
+  if (AT->num_rows > 0 && (!dWh || !Wh || !al16(Wh) || !al16(dWh))) return GNN_ERR_INVALID_ARGUMENT;
+  if (AT->nnz > 0 && (!AT->cols || !AT->eid || !alpha || !dZ || !dalpha || !al16(dZ)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (heads == 4 && (!al16(alpha) || !al16(dalpha))) return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_gat_bwd_csc_workspace(plan, K)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  GatBwdArgs a{};
+  a.R = AT->num_rows;
+  a.nnz = AT->nnz;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.offsets = AT->offsets;
+  a.rows = AT->cols;
+  a.eid = AT->eid;
+  a.chunk_row = plan->chunk_row;
+  a.chunk_split = plan->chunk_split;
+  a.split_rows = plan->split_rows;
+  a.num_split = plan->num_split;
+  a.empty_rows = plan->empty_rows;
+  a.num_empty = plan->num_empty;
+  a.H = (int)heads;
+  a.F = F;
+  a.K = K;
+  a.alpha = alpha;
+  a.dY = dZ;
+  a.ldy = ldz;
+  a.Wh = Wh;
+  a.ldw = ldw;
+  a.dWh = dWh;
+  a.ldd = ldd;
+  a.dalpha = dalpha;
+  a.slots = static_cast<float *>(ws);
+  const int64_t q = F / 4;
+  if (a.nwarps > 0) {
+    const unsigned grid = grid_warps(a.nwarps, 256);
+    const bool h4 = heads <= 4;
+#define GNN_GBM(G, VPL)                                                                 \
+  (h4 ? gat_bwd_csc_mean_kernel<G, VPL, 4><<<grid, 256, 0, st>>>(a, scale)              \
+      : gat_bwd_csc_mean_kernel<G, VPL, 8><<<grid, 256, 0, st>>>(a, scale))
+    if (q <= 4)
+      GNN_GBM(4, 1);
+    else if (q <= 8)
+      GNN_GBM(8, 1);
+    else if (q <= 16)
+      GNN_GBM(16, 1);
+    else if (q <= 32)
+      GNN_GBM(32, 1);
+    else if (q <= 64)
+      GNN_GBM(32, 2);
+    else
+      GNN_GBM(32, 4);
+#undef GNN_GBM
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_split > 0) {
+    gat_bwd_finalize_kernel<<<(unsigned)a.num_split, 128, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_empty > 0) {
+    gat_bwd_empty_kernel<<<grid_1d_a(a.num_empty * K, 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
 }
 
 int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,

@@ -299,3 +299,53 @@ class SegmentSumCall:
                                             self.vals.data_ptr(), self.out.data_ptr(),
                                             self.ws.data_ptr(), self.ws.numel(),
                                             _lib.stream_handle(self.dev)), "segment_sum")
+
+
+class GatBwdCscCall:
+    """Fused GAT backward over the CSC (edge-ID view): dWh = SpMMve^T(alpha, dY)
+    and dalpha = SDDMM(dY, Wh) from one gather of dY per edge."""
+
+    def __init__(self, AT: SparseOperand, alpha, dY, Wh, dWh, dalpha, heads):
+        self.lib = _lib.lib()
+        self.dev = dY.device
+        self.view = AT.view(vals=alpha, eid=AT.eid)
+        self.plan = AT.plan()
+        self.K = int(dY.shape[1])
+        self.t = (alpha, dY, Wh, dWh, dalpha)
+        self.heads, self._op = heads, AT
+        self.ws = _lib.workspace(self.lib.gnn_gat_bwd_csc_workspace(C.byref(self.plan), self.K),
+                                 self.dev)
+
+    def __call__(self):
+        alpha, dY, Wh, dWh, dalpha = self.t
+        _lib.check(self.lib.gnn_gat_bwd_csc(
+            C.byref(self.view), C.byref(self.plan), self.heads, alpha.data_ptr(), dY.data_ptr(),
+            dY.stride(0), Wh.data_ptr(), Wh.stride(0), self.K, dWh.data_ptr(), dWh.stride(0),
+            dalpha.data_ptr(), self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+            "gat_bwd_csc")
+
+
+class GatBwdCscMeanCall:
+    """Fused GAT backward of a head-mean layer over the CSC: gathers dZ[v]
+    (F floats) once per edge and produces dWh (all heads) and dalpha."""
+
+    def __init__(self, AT: SparseOperand, alpha, dZ, Wh, dWh, dalpha, heads, scale=None):
+        self.lib = _lib.lib()
+        self.dev = dZ.device
+        self.view = AT.view(vals=alpha, eid=AT.eid)
+        self.plan = AT.plan()
+        self.F = int(dZ.shape[1])
+        self.heads = heads
+        self.scale = float(1.0 / heads if scale is None else scale)
+        self.t = (alpha, dZ, Wh, dWh, dalpha)
+        self._op = AT
+        self.ws = _lib.workspace(
+            self.lib.gnn_gat_bwd_csc_workspace(C.byref(self.plan), heads * self.F), self.dev)
+
+    def __call__(self):
+        alpha, dZ, Wh, dWh, dalpha = self.t
+        _lib.check(self.lib.gnn_gat_bwd_csc_mean(
+            C.byref(self.view), C.byref(self.plan), self.heads, alpha.data_ptr(), dZ.data_ptr(),
+            dZ.stride(0), self.scale, Wh.data_ptr(), Wh.stride(0), self.F, dWh.data_ptr(),
+            dWh.stride(0), dalpha.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+            _lib.stream_handle(self.dev)), "gat_bwd_csc_mean")

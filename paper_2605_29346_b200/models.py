@@ -283,8 +283,9 @@ class _GATAggregate(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dout):
-        from .kernels import (AttnProjBwdCall, ColsumCall, EdgeSoftmaxCall, HeadMeanCall,
-                              MaskNormColsumCall, SddmmCall, SegmentSumCall)
+        from .kernels import (AttnProjBwdCall, ColsumCall, EdgeSoftmaxCall, GatBwdCscCall,
+                              GatBwdCscMeanCall, HeadMeanCall, MaskNormColsumCall, SddmmCall,
+                              SegmentSumCall)
 
         Wh, a_l, a_r, alpha, el, er, out = ctx.saved_tensors
         g, H = ctx.g, ctx.heads
@@ -293,20 +294,29 @@ class _GATAggregate(torch.autograd.Function):
         dev = Wh.device
         dout = dout.contiguous()
         db = torch.empty(dout.shape[1], dtype=torch.float32, device=dev)
+        A, AT = g.csr(), g.csc(with_eid=True)
+        ds = torch.empty(A.nnz, H, dtype=torch.float32, device=dev)
+        fused_ok = F % 4 == 0 and H <= 8
         if ctx.relu:
             dY = torch.empty_like(dout)
             MaskNormColsumCall(dout, dY, mask=out, colsum=db)()
         else:
             ColsumCall(dout, db)()
-            if ctx.mean:
+            dY = dout
+            if ctx.mean and not (fused_ok and F <= 128):
                 dY = torch.empty(V, K, dtype=torch.float32, device=dev)
                 HeadMeanCall(dY, dout, H, F, backward=True)()
-            else:
-                dY = dout
-        A, AT = g.csr(), g.csc(with_eid=True)
-        dWh = spmm_raw(AT, dY, heads=H, vals=alpha, eid=AT.eid)  # SpMMve^T, alpha via edge-ID
-        ds = torch.empty(A.nnz, H, dtype=torch.float32, device=dev)
-        SddmmCall(A, dY, Wh, ds, heads=H)()                       # dalpha
+        if ctx.mean and fused_ok and F <= 128:
+            # gathers dZ[v] once per edge for every head (dY = dZ/H broadcast)
+            dWh = torch.empty_like(Wh)
+            GatBwdCscMeanCall(AT, alpha, dout, Wh, dWh, ds, H)()
+        elif K % 4 == 0 and fused_ok and K <= 512:
+            # SpMMve^T (alpha via edge-ID) + SDDMM (dalpha) from one gather of dY
+            dWh = torch.empty_like(Wh)
+            GatBwdCscCall(AT, alpha, dY, Wh, dWh, ds, H)()
+        else:
+            dWh = spmm_raw(AT, dY, heads=H, vals=alpha, eid=AT.eid)
+            SddmmCall(A, dY, Wh, ds, heads=H)()
         EdgeSoftmaxCall(A, H, ds, el=el, er=er, slope=ctx.slope, backward=True, alpha=alpha,
                         dalpha=ds)()                               # ds (in place)
         der = torch.empty(V, H, dtype=torch.float32, device=dev)
@@ -517,7 +527,7 @@ class GATTrainer(_FusedEpoch):
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
                  lr=0.01, slope=0.2, seed: int = 0):
         from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
-                              HeadMeanCall, SddmmCall, SegmentSumCall)
+                              GatBwdCscCall, GatBwdCscMeanCall, HeadMeanCall, SegmentSumCall)
 
         self.g = g
         dev = g.device
@@ -563,7 +573,7 @@ class GATTrainer(_FusedEpoch):
         self.Wh2, self.Yc2 = e(V, K2), e(V, K2)
         self.Z = torch.zeros(V, Cp, **f32)
         self.dZ = torch.zeros(V, Cp, **f32)  # pad column never written: stays 0
-        self.dYc2, self.dWh2 = e(V, K2), e(V, K2)
+        self.dWh2 = e(V, K2)
         self.ds = e(E, H)
         self.der, self.del_ = e(V, H), e(V, H)
         self.dY1, self.dY1m, self.dWh1 = e(V, K1), e(V, K1), e(V, K1)
@@ -584,9 +594,10 @@ class GATTrainer(_FusedEpoch):
         k["xent"] = XentCall(self.Z[:, :classes], self.labels, self.loss, dZ=self.dZ[:, :classes])
         # backward, layer 2
         k["db2"] = ColsumCall(self.dZ, self.db2)
-        k["mean2_bwd"] = HeadMeanCall(self.dYc2, self.dZ, H, Cp, backward=True)
-        k["bagg2"] = SpmmCall(AT, self.dYc2, self.dWh2, heads=H, vals=self.alpha2, eid=AT.eid)
-        k["sddmm2"] = SddmmCall(A, self.dYc2, self.Wh2, self.ds, heads=H)
+        # head-mean layer: the concatenated-head gradient is dZ/H broadcast, so the
+        # fused CSC kernel gathers dZ[v] (Cp floats) instead of H*Cp per edge
+        k["bagg2+sddmm2"] = GatBwdCscMeanCall(AT, self.alpha2, self.dZ, self.Wh2, self.dWh2,
+                                              self.ds, H)
         k["softmax2_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el2, er=self.er2, slope=slope,
                                             backward=True, alpha=self.alpha2, dalpha=self.ds)
         k["der2"] = SegmentSumCall(A, self.ds, self.der, H)
@@ -597,8 +608,7 @@ class GATTrainer(_FusedEpoch):
         k["dWh2.W2^T"] = GemmCall(self.dWh2, self.W2, self.dY1, trans_b=True)
         # backward, layer 1
         k["relu1_bwd"] = MaskNormColsumCall(self.dY1, self.dY1m, mask=self.Y1, colsum=self.db1)
-        k["bagg1"] = SpmmCall(AT, self.dY1m, self.dWh1, heads=H, vals=self.alpha1, eid=AT.eid)
-        k["sddmm1"] = SddmmCall(A, self.dY1m, self.Wh1, self.ds, heads=H)
+        k["bagg1+sddmm1"] = GatBwdCscCall(AT, self.alpha1, self.dY1m, self.Wh1, self.dWh1, self.ds, H)
         k["softmax1_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el1, er=self.er1, slope=slope,
                                             backward=True, alpha=self.alpha1, dalpha=self.ds)
         k["der1"] = SegmentSumCall(A, self.ds, self.der, H)
