@@ -61,31 +61,22 @@ namespace gnn {
 namespace {
 __global__ void __launch_bounds__(512) read_probe_kernel(const float4 *__restrict__ buf, int64_t n,
                                                          int reps, float *out) {
+  // grid-stride passes over an L2-resident buffer, L1 bypassed (ld.global.cg),
+  // 4 independent 128-bit loads in flight per thread
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int r = 0; r < reps; ++r) {
-    const int64_t shift = ((int64_t)blockIdx.x * 4099 + r * 7919) % n;
     int64_t i = t0;
-    for (; i + 3 * stride < n; i += 4 * stride) {  // 4 independent 128-bit loads in flight
-      int64_t j0 = i + shift, j1 = j0 + stride, j2 = j1 + stride, j3 = j2 + stride;
-      j0 -= j0 >= n ? n : 0;
-      j1 -= j1 >= n ? n : 0;
-      j2 -= j2 >= n ? n : 0;
-      j3 -= j3 >= n ? n : 0;
-      const float4 v0 = __ldcg(buf + j0), v1 = __ldcg(buf + j1), v2 = __ldcg(buf + j2),
-                   v3 = __ldcg(buf + j3);
-      a0 += v0.x + v0.w;
-      a1 += v1.x + v1.w;
-      a2 += v2.x + v2.w;
-      a3 += v3.x + v3.w;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+      const float4 v0 = __ldcg(buf + i), v1 = __ldcg(buf + i + stride),
+                   v2 = __ldcg(buf + i + 2 * stride), v3 = __ldcg(buf + i + 3 * stride);
+      a0 += v0.x;
+      a1 += v1.y;
+      a2 += v2.z;
+      a3 += v3.w;
     }
-    for (; i < n; i += stride) {
-      int64_t j = i + shift;
-      j -= j >= n ? n : 0;
-      const float4 v = __ldcg(buf + j);
-      a0 += v.y + v.z;
-    }
+    for (; i < n; i += stride) a0 += __ldcg(buf + i).x;
   }
   if (a0 + a1 + a2 + a3 == 123456.789f) *out = a0;  // never true; keeps the loads
 }

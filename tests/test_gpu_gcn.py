@@ -87,3 +87,26 @@ def test_autograd_layers_match_oracle(setup):
                    (model.layers[0].bias.grad, "b1"), (model.layers[1].bias.grad, "b2")):
         ok, worst = oo.close(got.cpu().numpy(), ref[k], ref["abs"][k])
         assert ok, (k, worst)
+
+
+def test_e2e_graph_matches_device_resident_epoch(setup):
+    """capture_e2e (chunked H2D overlapped with X W1, loss copied back) trains
+    exactly like the device-resident epoch."""
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    gb, g, _, X, y, (V, F, Hd, C) = setup
+    a = GCNTrainer(g, F, Hd, C, seed=0)
+    b = GCNTrainer(g, F, Hd, C, seed=0)
+    a.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+    Xp = torch.zeros(V, b.Fpad).pin_memory()
+    Xp[:, :F].copy_(torch.from_numpy(X))
+    yh = torch.from_numpy(y).pin_memory()
+    loss_h = torch.zeros(1).pin_memory()
+    b.capture_e2e(Xp, yh, loss_h, chunks=4)
+    for _ in range(3):
+        la = a.step().item()
+        b.run_e2e()
+        torch.cuda.synchronize()
+        assert la == loss_h.item()
+    for k in a.params():
+        assert torch.equal(a.params()[k], b.params()[k])
