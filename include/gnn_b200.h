@@ -184,12 +184,23 @@ typedef struct gnn_spmm_plan {
   int64_t num_groups;
   int64_t num_empty;
   const int32_t *empty_rows;       /* [num_empty] */
+  int64_t short_max;               /* rows with 1 <= deg <= short_max go to the short-row kernel */
+  int64_t num_short;
+  const int32_t *short_rows;       /* [num_short] */
 } gnn_spmm_plan_t;
 
 size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_per_warp);
 size_t gnn_spmm_plan_workspace(int64_t num_rows);
 int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t *plan_buf,
                         gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* Degree-binned plan for gnn_spmm: rows with 1 <= deg <= short_max (the
+ * power-law tail) are listed for a group-per-row kernel (32/G rows per warp
+ * in parallel) and skipped by the nnz-split kernel, so a warp never walks a
+ * run of tiny rows one by one.  short_max = 0 gives gnn_spmm_plan_build's
+ * plan (the form the edge-softmax / SDDMM / GAT kernels expect). */
+int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t edges_per_warp, int64_t short_max,
+                           int32_t *plan_buf, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
+                           gnn_stream_t stream);
 
 /* Y[num_rows,K] = epilogue(A . X), X[num_cols,K].  heads>=1 splits K into
  * `heads` slices scaled by their own edge value (vals is [nnz,heads]).

@@ -86,6 +86,9 @@ class SpmmPlan(C.Structure):
         ("num_groups", c_i64),
         ("num_empty", c_i64),
         ("empty_rows", c_ptr),
+        ("short_max", c_i64),
+        ("num_short", c_i64),
+        ("short_rows", c_ptr),
     ]
 
 
@@ -125,6 +128,10 @@ SIGNATURES = {
     "gnn_spmm_plan_build": (
         c_int,
         [C.POINTER(CsrView), c_i64, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_spmm_plan_build_ex": (
+        c_int,
+        [C.POINTER(CsrView), c_i64, c_i64, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
     ),
     "gnn_spmm_workspace": (c_sz, [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64]),
     "gnn_spmm": (

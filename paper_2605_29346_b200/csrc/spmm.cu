@@ -55,6 +55,7 @@ struct SpmmArgs {
   int stage;                 // StageMode
   int bulk_ok;
   int warp_smem;             // bytes of shared memory per warp
+  int64_t short_max;         // rows with 1 <= deg <= short_max: short-row kernel, skipped here
 };
 
 
@@ -427,11 +428,12 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
     const int32_t *bv = sval + b * kSub;
     while (true) {
       const int64_t lo = max(rs, s0), hi = min(re, s1);
-      if (hi > lo)
+      const bool is_short = re - rs <= a.short_max;  // owned by the short-row kernel
+      if (hi > lo && !is_short)
         seg_accumulate<G, VPL, VW, HAS_VALS>(a, lc, bc, bv, stage, s0, (int)(lo - s0),
                                              (int)(hi - s0), acc);
       if (re > s1) break;  // row continues in the next sub-chunk (or the next warp)
-      if (re > rs) {       // a row ends here
+      if (re > rs && !is_short) {  // a row ends here
         group_reduce<G, VPL, VW>(acc);
         if (rs < e0) {     // carry-in piece of a row owned by an earlier warp
           store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
@@ -456,7 +458,7 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
     }
     __syncwarp();  // buffer b fully consumed before issue(sc + 2) refills it
   }
-  if (!done && re > e1) {  // the range ends inside row r
+  if (!done && re > e1 && re - rs > a.short_max) {  // the range ends inside row r
     group_reduce<G, VPL, VW>(acc);
     if (rs < e0) {         // whole range inside one row: a carry-in piece
       store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
@@ -705,6 +707,71 @@ int launch_tma(const SpmmArgs &a, bool has_vals, const CUtensorMap &tm, cudaStre
   return GNN_OK;
 }
 
+// Short rows (1 <= deg <= short_max; the power-law tail): one lane group per
+// row instead of a whole warp walking rows one by one — NG rows per warp in
+// parallel, U edges of each in flight, fused epilogue per group.  Indices and
+// edge values are read straight from global (a short row is one or two
+// sectors).  Summation order is fixed per row: deterministic.
+template <int G, int VPL, int VW, bool HAS_VALS>
+__global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
+                                                              int64_t nrows) {
+  using V = VecT<VW>;
+  constexpr int NG = 32 / G;
+  constexpr int U = (VPL * VW >= 8) ? 4 : 8;
+  constexpr int KB = G * VPL * VW;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  const int64_t cbase = (int64_t)blockIdx.y * KB;
+  const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * NG + g;
+  if (i >= nrows) return;  // group-uniform
+  const int64_t r = rows[i];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const LaneCols<G, VPL, VW> lc(a, cbase);
+  const uint32_t ldxb = (uint32_t)a.ldx * 4u;
+  typename V::T acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
+  for (int64_t e = rs; e < re; e += U) {
+    int32_t c[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ok[u] = e + u < re;
+      c[u] = ok[u] ? __ldg(a.cols + e + u) : 0;
+    }
+    typename V::T x[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather<VW>(lc.xb[v], c[u], ldxb) : V::zero();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if constexpr (HAS_VALS) {
+        float w[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int64_t vi = ok[u] ? (a.eid ? (int64_t)__ldg(a.eid + e + u) : e + u) : 0;
+          w[v] = ok[u] ? __ldg(a.vals + vi * a.heads + lc.head[v]) : 0.f;
+        }
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::fma(w[v], x[u][v], acc[v]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = V::add(acc[v], x[u][v]);
+      }
+    }
+  }
+  float ns = 1.f, ps = 1.f;
+  if (a.epi.flags & GNN_EPI_NORM) ns = inv_deg(a.deg_offsets, r);
+  if (a.epi.flags & GNN_EPI_POSTNORM) ps = inv_deg(a.epi.post_deg_offsets, r);
+  float *dst = a.Y + r * a.ldy;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int64_t col = cbase + (int64_t)(v * G + gl) * VW;
+    if (col < a.K) V::st(dst + col, epi_vec<VW>(acc[v], r, col, a, ns, ps));
+  }
+}
+
 __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                        int64_t nrows) {
   const int64_t total = nrows * a.K;
@@ -728,11 +795,15 @@ __global__ void plan_chunk_rows_kernel(const int64_t *__restrict__ off, int64_t 
   }
 }
 __global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                  int64_t *fsplit, int64_t *fempty, int64_t *ngroups) {
+                                  int64_t short_max, int64_t *fsplit, int64_t *fempty,
+                                  int64_t *ngroups, int64_t *fshort) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t rs = off[r], re = off[r + 1];
     fempty[r] = re == rs ? 1 : 0;
+    fshort[r] = (re > rs && re - rs <= short_max) ? 1 : 0;
+    // split-row bookkeeping covers short rows too: a call that does not use the
+    // short-row kernel (wide K: one row per warp anyway) finishes them here
     const bool split = re > rs && rs / P != (re - 1) / P;
     fsplit[r] = split ? 1 : 0;
     ngroups[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kGroupPartials) : 0;
@@ -742,7 +813,8 @@ __global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, 
                                     const int64_t *__restrict__ us, const int64_t *__restrict__ ue,
                                     const int64_t *__restrict__ ug, int32_t *split_rows,
                                     int32_t *split_group_base, int32_t *chunk_split,
-                                    int32_t *empty_rows) {
+                                    int32_t *empty_rows, const int64_t *__restrict__ ush,
+                                    int32_t *short_rows) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     if (us[r + 1] != us[r]) {
@@ -754,6 +826,7 @@ __global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, 
       for (int64_t w = wa + 1; w <= wb; ++w) chunk_split[2 * w] = (int32_t)si;  // carry-ins
     }
     if (ue[r + 1] != ue[r]) empty_rows[ue[r]] = (int32_t)r;
+    if (ush[r + 1] != ush[r]) short_rows[ush[r]] = (int32_t)r;
     if (r == 0) split_group_base[us[R]] = (int32_t)ug[R];
   }
 }
@@ -784,9 +857,23 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+template <int G, int VPL, int VW>
+int launch_short(const SpmmArgs &a, bool has_vals, const gnn_spmm_plan_t *plan, cudaStream_t st) {
+  constexpr int KB = G * VPL * VW;
+  constexpr int NG = 32 / G;
+  const int64_t warps = ceil_div(plan->num_short, NG);
+  dim3 grid((unsigned)ceil_div(warps * 32, 256), (unsigned)ceil_div(a.K, KB));
+  if (has_vals)
+    spmm_short_rows_kernel<G, VPL, VW, true><<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
+  else
+    spmm_short_rows_kernel<G, VPL, VW, false><<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
 struct PlanLayout {
   int64_t nw;
-  int64_t o_chunk, o_csplit, o_split, o_sgb, o_empty, total;
+  int64_t o_chunk, o_csplit, o_split, o_sgb, o_empty, o_short, total;
 };
 PlanLayout plan_layout(int64_t R, int64_t nnz, int64_t P) {
   PlanLayout L;
@@ -801,6 +888,8 @@ PlanLayout plan_layout(int64_t R, int64_t nnz, int64_t P) {
   L.o_sgb = o;
   o += R + 1;
   L.o_empty = o;
+  o += R;
+  L.o_short = o;
   o += R;
   L.total = o;
   return L;
@@ -820,15 +909,20 @@ size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_pe
 
 size_t gnn_spmm_plan_workspace(int64_t num_rows) {
   WsCounter c;
-  for (int i = 0; i < 3; ++i) c.take<int64_t>(num_rows + 1);
-  c.used += 3 * (scan_i64_workspace(num_rows) + 256);
+  for (int i = 0; i < 4; ++i) c.take<int64_t>(num_rows + 1);
+  c.used += 4 * (scan_i64_workspace(num_rows) + 256);
   return c.used + 512;
 }
 
 int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_spmm_plan_t *plan,
                         void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  return gnn_spmm_plan_build_ex(A, P, 0, buf, plan, ws, ws_bytes, stream);
+}
+
+int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max, int32_t *buf,
+                           gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes, gnn_stream_t stream) {
   if (!A || !plan || !buf || P <= 0 || P % 4 != 0 || A->num_rows < 0 ||
-      !A->offsets)
+      !A->offsets || short_max < 0)
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 30))
     return GNN_ERR_UNSUPPORTED;
@@ -840,32 +934,37 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   int64_t *fs = ar.take<int64_t>(R + 1);
   int64_t *fe = ar.take<int64_t>(R + 1);
   int64_t *fg = ar.take<int64_t>(R + 1);
+  int64_t *fh = ar.take<int64_t>(R + 1);
   size_t sb = scan_i64_workspace(R);
   void *s1 = ar.take<char>((int64_t)sb);
   void *s2 = ar.take<char>((int64_t)sb);
   void *s3 = ar.take<char>((int64_t)sb);
+  void *s4 = ar.take<char>((int64_t)sb);
   if (!ar.ok()) return GNN_ERR_WORKSPACE;
   plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, A->nnz, P, L.nw,
                                                                  buf + L.o_chunk);
   GNN_LAUNCH_CHECK();
   if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, fs, fe, fg, fh);
     GNN_LAUNCH_CHECK();
   }
   GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
   GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
   GNN_TRY(exclusive_scan_i64(fg, fg, R, true, s3, sb, st));
+  GNN_TRY(exclusive_scan_i64(fh, fh, R, true, s4, sb, st));
   if (R > 0) {
     plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg,
                                                          buf + L.o_split, buf + L.o_sgb,
-                                                         buf + L.o_csplit, buf + L.o_empty);
+                                                         buf + L.o_csplit, buf + L.o_empty, fh,
+                                                         buf + L.o_short);
     GNN_LAUNCH_CHECK();
   }
-  int64_t h[3] = {0, 0, 0};
+  int64_t h[4] = {0, 0, 0, 0};
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[0], fs + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[1], fe + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], fg + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h[3], fh + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaStreamSynchronize(st));
   plan->edges_per_warp = P;
   plan->num_warps = L.nw;
@@ -877,6 +976,9 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t P, int32_t *buf, gnn_sp
   plan->num_groups = h[2];
   plan->num_empty = h[1];
   plan->empty_rows = buf + L.o_empty;
+  plan->short_max = short_max;
+  plan->num_short = h[3];
+  plan->short_rows = buf + L.o_short;
   return GNN_OK;
 }
 
@@ -958,6 +1060,12 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
   a.warp_smem = (int)(16 + 2 * kSub * 4 * (a.stage != STAGE_NONE ? 2 : 1));
+  // short-row kernel only where it runs several rows per warp (32/G >= 2)
+  {
+    const bool v4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
+                    (a.F % 4 == 0);
+    a.short_max = (v4 && K <= 64) ? plan->short_max : 0;
+  }
 
   if (a.nwarps > 0) {
     const bool hv = A->vals != nullptr;
@@ -970,7 +1078,7 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     int s;
     const bool tma_ok = vec4 && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
                         a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
-                        getenv("GNN_SPMM_TMA") != nullptr;
+                        plan->short_max == 0 && getenv("GNN_SPMM_TMA") != nullptr;
     CUtensorMap tm;
     const int kb = K <= 16 ? 16 : K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
     if (tma_ok && make_gather_map(&tm, X, A->num_cols, K, ldx, kb)) {
@@ -999,6 +1107,32 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
         s = launch_main<32, 4, 1>(a, hv, st);  // 128 columns per block-column
     }
     GNN_TRY(s);
+  }
+  if (plan->num_short > 0 && a.short_max > 0) {
+    // same lane layout as the main kernel for this K (see launch_main dispatch)
+    const bool hv = A->vals != nullptr;
+    bool vec4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
+                (a.F % 4 == 0);
+    if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
+    if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
+    if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
+    if (vec4) {
+      if (K <= 16)
+        GNN_TRY((launch_short<4, 1, 4>(a, hv, plan, st)));
+      else if (K <= 32)
+        GNN_TRY((launch_short<8, 1, 4>(a, hv, plan, st)));
+      else if (K <= 64)
+        GNN_TRY((launch_short<16, 1, 4>(a, hv, plan, st)));
+      else if (K <= 128)
+        GNN_TRY((launch_short<32, 1, 4>(a, hv, plan, st)));
+      else
+        GNN_TRY((launch_short<32, 2, 4>(a, hv, plan, st)));
+    } else {
+      if (K <= 32)
+        GNN_TRY((launch_short<32, 1, 1>(a, hv, plan, st)));
+      else
+        GNN_TRY((launch_short<32, 4, 1>(a, hv, plan, st)));
+    }
   }
   if (plan->num_empty > 0) {
     spmm_empty_rows_kernel<<<grid_1d(plan->num_empty * K, 256), 256, 0, st>>>(a, plan->empty_rows,

@@ -19,6 +19,7 @@ access, read-only, with the reference's dtypes (int64 / int32 / int64).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass
 from pathlib import Path
@@ -75,6 +76,10 @@ def _default_edges_per_warp(nnz: int, sms: int) -> int:
     return p
 
 
+# rows of degree <= this go to the SpMM's group-per-row kernel (power-law tail)
+SPMM_SHORT_MAX = int(os.environ.get("GNN_SPMM_SHORT", "32"))
+
+
 class SparseOperand:
     """One device sparse matrix in CSR layout (a graph's CSR, or its CSC which
     is the CSR of the transpose), plus cached SpMM schedules."""
@@ -110,29 +115,37 @@ class SparseOperand:
         v.deg_offsets = self.deg_offsets.data_ptr() if self.deg_offsets is not None else None
         return v
 
-    def plan(self, edges_per_warp: int | None = None) -> _lib.SpmmPlan:
+    def plan(self, edges_per_warp: int | None = None, short_max: int = 0) -> _lib.SpmmPlan:
+        """Chunk schedule shared by every edge kernel.  ``short_max`` > 0 gives
+        the degree-binned SpMM plan (rows of degree <= short_max handled by the
+        group-per-row kernel); the edge-softmax / SDDMM / GAT kernels use 0."""
         lib = _lib.lib()
         if edges_per_warp is None:
             with torch.cuda.device(self.device):
                 sms = lib.gnn_device_sm_count()
             edges_per_warp = _default_edges_per_warp(self.nnz, sms)
-        key = int(edges_per_warp)
+        key = (int(edges_per_warp), int(short_max))
         if key in self._plans:
             return self._plans[key][0]
         dev = self.device
         with torch.cuda.device(dev):
-            nint = lib.gnn_spmm_plan_buffer_ints(self.num_rows, self.nnz, key)
+            nint = lib.gnn_spmm_plan_buffer_ints(self.num_rows, self.nnz, key[0])
             buf = torch.empty(max(int(nint), 1), dtype=torch.int32, device=dev)
             ws = _lib.workspace(lib.gnn_spmm_plan_workspace(self.num_rows), dev)
             plan = _lib.SpmmPlan()
             view = self.view()
             _lib.check(
-                lib.gnn_spmm_plan_build(C.byref(view), key, buf.data_ptr(), C.byref(plan),
-                                        ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
+                lib.gnn_spmm_plan_build_ex(C.byref(view), key[0], key[1], buf.data_ptr(),
+                                           C.byref(plan), ws.data_ptr(), ws.numel(),
+                                           _lib.stream_handle(dev)),
                 "spmm plan",
             )
         self._plans[key] = (plan, buf)
         return plan
+
+    def spmm_plan(self, edges_per_warp: int | None = None) -> _lib.SpmmPlan:
+        """Plan for gnn_spmm: degree-binned with short_max = SPMM_SHORT_MAX."""
+        return self.plan(edges_per_warp, short_max=SPMM_SHORT_MAX)
 
     def nbytes(self) -> int:
         n = self.offsets.numel() * 8 + self.cols.numel() * 4

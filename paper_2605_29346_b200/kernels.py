@@ -25,7 +25,7 @@ class SpmmCall:
         self.K = int(X.shape[1])
         assert Y.shape[1] == self.K and X.stride(1) == 1 and Y.stride(1) == 1
         self.view = op.view(vals=vals, eid=eid)
-        self.plan = op.plan(edges_per_warp)
+        self.plan = op.spmm_plan(edges_per_warp)
         self.epi = _lib.Epilogue()
         self.epi.flags = flags
         self.epi.self_scale = float(self_scale)

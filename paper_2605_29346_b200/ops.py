@@ -45,7 +45,7 @@ def spmm_raw(op: SparseOperand, X: torch.Tensor, *, heads: int = 1, vals=None, e
         _check_features(out, op.num_rows, "spmm output")
     view = op.view(vals=vals, eid=eid)
     if plan is None:
-        plan = op.plan()
+        plan = op.spmm_plan()
     epi = _lib.Epilogue()
     epi.flags = flags
     epi.self_scale = float(self_scale)
