@@ -1,0 +1,57 @@
+"""CPU: the B200-fitted calibration (tools/fit_cost_model.py ->
+profiles/b200_cost_model.json) is a drop-in for the reference cost model's
+calibration file (execmodel.py:44-109): same keys, only the 'train' class
+refitted, loadable by gsbench's own CostModel.from_json when the reference
+tree is present (this container), and its predictions match the measured
+points it was fitted to within the stated error."""
+
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CAL = os.path.join(ROOT, "profiles", "b200_cost_model.json")
+REF_SRC = "/root/reference/pkg/src"
+
+
+def _load():
+    with open(CAL) as fh:
+        return json.load(fh)
+
+
+def test_calibration_has_reference_keys_and_train_refit():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from fit_cost_model import REFERENCE_DEFAULT
+
+    cal = _load()
+    assert set(cal) == set(REFERENCE_DEFAULT) | {"provenance"}
+    for k, v in REFERENCE_DEFAULT["kernel_coeffs"].items():
+        if k != "train":
+            assert cal["kernel_coeffs"][k] == v
+    tr = cal["kernel_coeffs"]["train"]
+    assert set(tr) == {"a", "b_v", "b_e", "b_f"}
+    assert all(x >= 0 for x in tr.values())
+    assert tr != REFERENCE_DEFAULT["kernel_coeffs"]["train"]
+    assert "B200" in cal["provenance"]
+
+
+def test_train_kernel_prediction_is_b200_scale():
+    """Reddit-shape full-graph train kernel: the reference's fitted coefficients
+    predict ~271 ms; the B200 fit must predict well under 10 ms."""
+    tr = _load()["kernel_coeffs"]["train"]
+    V, E, K = 232_965, 114_615_892, 602
+    us = tr["a"] + tr["b_v"] * V + tr["b_e"] * E + tr["b_f"] * V * K
+    assert 0 < us < 10_000
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference tree not mounted")
+def test_reference_cost_model_loads_b200_calibration():
+    sys.path.insert(0, REF_SRC)
+    from gsbench.execmodel import CostModel, KernelCoeffs
+
+    cm = CostModel.from_json(CAL)
+    c = cm.coeffs("train")
+    assert isinstance(c, KernelCoeffs)
+    assert c.a == pytest.approx(_load()["kernel_coeffs"]["train"]["a"])
