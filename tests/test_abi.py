@@ -63,7 +63,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.CsrView) == 64
     # uint32 + float + 6 pointer/int64 fields
     assert ctypes.sizeof(_lib.Epilogue) == 8 + 6 * 8
-    assert ctypes.sizeof(_lib.SpmmPlan) == 10 * 8
+    assert ctypes.sizeof(_lib.SpmmPlan) == 13 * 8
+    assert ctypes.sizeof(_lib.EdgeScores) == 4 * 8
 
 
 def test_graphgenspec_validation_mirrors_reference():
