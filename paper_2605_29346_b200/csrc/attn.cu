@@ -702,40 +702,45 @@ __global__ void attn_proj_kernel(int64_t V, int H, int64_t F, const float *__res
   }
 }
 
-// dWh[v,h,f] += del[v,h] a_l[h,f] + der[v,h] a_r[h,f]
-__global__ void attn_proj_bwd_dwh_kernel(int64_t V, int H, int64_t F, const float *__restrict__ del,
-                                         const float *__restrict__ der, const float *__restrict__ al,
-                                         const float *__restrict__ ar, float *dWh, int64_t ldd) {
-  const int64_t K = (int64_t)H * F;
-  const int64_t total = V * K;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = t / K, k = t % K;
-    const int64_t h = k / F;
-    float d = dWh[v * ldd + k];
-    d = fmaf(del[v * H + h], al[k], d);
-    d = fmaf(der[v * H + h], ar[k], d);
-    dWh[v * ldd + k] = d;
-  }
-}
-
-// da_l[k] = sum_v Wh[v,k] del[v,k/F] (and da_r): block partials over vertex
-// ranges (fixed order), then a fixed-order sum over blocks.
+// One streaming pass over the vertices: thread = column k (< K <= 512, two
+// passes of 256 for wider K), each CTA a contiguous vertex range, 4 rows in
+// flight.  dWh[v,k] += del[v,h(k)] a_l[k] + der[v,h(k)] a_r[k] (in place) and
+// the CTA's partial of da_l[k] = sum_v Wh[v,k] del[v,h(k)] (and da_r), summed
+// over CTAs in fixed order by attn_proj_bwd_da_final_kernel.
 constexpr int kProjBlocks = 1024;
-__global__ void attn_proj_bwd_da_partial_kernel(int64_t V, int H, int64_t F,
-                                                const float *__restrict__ Wh, int64_t ldw,
-                                                const float *__restrict__ del,
-                                                const float *__restrict__ der, float *part) {
+__global__ void __launch_bounds__(256) attn_proj_bwd_kernel(
+    int64_t V, int H, int64_t F, const float *__restrict__ Wh, int64_t ldw,
+    const float *__restrict__ del, const float *__restrict__ der, const float *__restrict__ al,
+    const float *__restrict__ ar, float *dWh, int64_t ldd, float *part) {
   const int64_t K = (int64_t)H * F;
   const int64_t per = ceil_div(V, gridDim.x);
   const int64_t v0 = blockIdx.x * per, v1 = min(v0 + per, V);
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
     const int64_t h = k / F;
+    const float alk = __ldg(al + k), ark = __ldg(ar + k);
     float sl = 0.f, sr = 0.f;
-    for (int64_t v = v0; v < v1; ++v) {
-      const float x = __ldg(Wh + v * ldw + k);
-      sl = fmaf(x, __ldg(del + v * H + h), sl);
-      sr = fmaf(x, __ldg(der + v * H + h), sr);
+    int64_t v = v0;
+    for (; v + 3 < v1; v += 4) {
+      float x[4], d[4], dl[4], dr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = __ldg(Wh + (v + u) * ldw + k);
+        d[u] = dWh[(v + u) * ldd + k];
+        dl[u] = __ldg(del + (v + u) * H + h);
+        dr[u] = __ldg(der + (v + u) * H + h);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sl = fmaf(x[u], dl[u], sl);
+        sr = fmaf(x[u], dr[u], sr);
+        dWh[(v + u) * ldd + k] = fmaf(dr[u], ark, fmaf(dl[u], alk, d[u]));
+      }
+    }
+    for (; v < v1; ++v) {
+      const float x = __ldg(Wh + v * ldw + k), dl = __ldg(del + v * H + h), dr = __ldg(der + v * H + h);
+      sl = fmaf(x, dl, sl);
+      sr = fmaf(x, dr, sr);
+      dWh[v * ldd + k] = fmaf(dr, ark, fmaf(dl, alk, dWh[v * ldd + k]));
     }
     part[(int64_t)blockIdx.x * 2 * K + k] = sl;
     part[(int64_t)blockIdx.x * 2 * K + K + k] = sr;
@@ -1507,11 +1512,9 @@ int gnn_gat_attn_proj_bwd(int64_t V, int64_t heads, int64_t F, const float *Wh, 
   float *part = static_cast<float *>(ws);
   const int nb = (int)(V < kProjBlocks ? (V > 0 ? V : 1) : kProjBlocks);
   if (V > 0) {
-    // partials read Wh before dWh is updated (they may not alias anyway)
-    attn_proj_bwd_da_partial_kernel<<<nb, 128, 0, st>>>(V, (int)heads, F, Wh, ldw, del, der, part);
-    GNN_LAUNCH_CHECK();
-    attn_proj_bwd_dwh_kernel<<<grid_1d_a(V * K, 256), 256, 0, st>>>(V, (int)heads, F, del, der,
-                                                                    a_l, a_r, dWh, ldd);
+    const int threads = (int)(K >= 256 ? 256 : ceil_div(K, 32) * 32);
+    attn_proj_bwd_kernel<<<nb, threads, 0, st>>>(V, (int)heads, F, Wh, ldw, del, der, a_l, a_r,
+                                                 dWh, ldd, part);
     GNN_LAUNCH_CHECK();
   } else {
     GNN_CUDA_TRY(cudaMemsetAsync(part, 0, sizeof(float) * 2 * K, st));

@@ -45,6 +45,7 @@ struct TcArgs {
   int64_t ldc;
   const float *bias;
   int relu;
+  int vec_store;  // C rows 16-byte aligned: 128-bit epilogue stores
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *tm, int c0, int c1,
@@ -255,7 +256,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
         tmem_ld16(taddr, v);
         tmem_ld16(taddr + NPAD, u);  // the B_lo half
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < p.M) {
+        if (row < p.M && p.vec_store && c0 + 16 <= p.N) {
+          // full 16-column slice: 4 x 128-bit stores instead of 16 scalar ones
+          float y[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            y[j] = __uint_as_float(v[j]) + __uint_as_float(u[j]);
+            if (p.bias) y[j] += __ldg(p.bias + c0 + j);
+            if (p.relu) y[j] = fmaxf(y[j], 0.f);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4 *>(crow + c0 + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+        } else if (row < p.M) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int64_t c = c0 + j;
@@ -657,6 +670,7 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
   p.ldc = ldc;
   p.bias = bias;
   p.relu = relu;
+  p.vec_store = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
   switch (npad) {
     case 16: return launch_tc<16>(ta, tbh, tbl, p, st);
     case 32: return launch_tc<32>(ta, tbh, tbl, p, st);
