@@ -354,7 +354,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
 // engine): column ids (+ edge values or edge ids).  Row accumulators carry
 // across sub-chunk boundaries in registers; only rows crossing the warp's
 // range boundaries produce partials (split rows, finished by split_arrive).
-constexpr int kSub = 256;
+constexpr int kSub = 512;
 
 template <int G, int VPL, int VW, bool HAS_VALS>
 __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
