@@ -66,6 +66,11 @@ int64_t gnn_launch_counter(void);          /* kernels launched by this library s
  * loads) — with an L2-resident buffer this measures the L2 -> SM roof that
  * bounds the SpMM's row gathers.  out receives nothing meaningful. */
 int gnn_read_probe(const float *buf, int64_t n_floats, int reps, float *out, gnn_stream_t stream);
+/* Strided 2-D copy (cudaMemcpyDefault: host<->device or device<->device),
+ * stream-ordered, no staging buffer — used to put [V, F] host features into
+ * the padded [V, Fpad] device layout the TMA-fed GEMMs need. */
+int gnn_memcpy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width,
+                 size_t height, gnn_stream_t stream);
 
 /* ------------------------------------------------------- graph builders */
 /* Stable counting sort of (src,dst) pairs into CSR: offsets[V+1] int64,

@@ -101,6 +101,7 @@ SIGNATURES = {
     "gnn_device_sm_count": (c_int, []),
     "gnn_launch_counter": (c_i64, []),
     "gnn_read_probe": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr]),
+    "gnn_memcpy2d": (c_int, [c_ptr, c_sz, c_ptr, c_sz, c_sz, c_sz, c_ptr]),
     "gnn_csr_from_edges_workspace": (c_sz, [c_i64, c_i64]),
     "gnn_csr_from_edges": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_subgraph_csr_workspace": (c_sz, [c_i64, c_i64]),
@@ -295,3 +296,18 @@ def stream_handle(device=None) -> int:
 def workspace(nbytes: int, device) -> torch.Tensor:
     """Scratch from torch's caching allocator, so peak-memory accounting sees it."""
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def copy_rows(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst[:] = src for 2-D fp32/int tensors with unit column stride and
+    possibly different row strides (host or device src), as one strided copy
+    (gnn_memcpy2d) — no transient contiguous device buffer."""
+    if dst.shape != src.shape or dst.dtype != src.dtype:
+        raise ValueError("copy_rows: shape/dtype mismatch")
+    if src.dim() != 2 or dst.stride(1) != 1 or src.stride(1) != 1:
+        dst.copy_(src)
+        return
+    es = dst.element_size()
+    check(load_library(False).gnn_memcpy2d(dst.data_ptr(), dst.stride(0) * es, src.data_ptr(),
+                                           src.stride(0) * es, dst.shape[1] * es, dst.shape[0],
+                                           stream_handle(dst.device)), "memcpy2d")

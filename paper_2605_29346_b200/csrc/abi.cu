@@ -93,3 +93,17 @@ extern "C" int gnn_read_probe(const float *buf, int64_t n_floats, int reps, floa
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
+
+// Strided 2-D copy between host (pinned or pageable) and device or device
+// and device, stream-ordered, no staging buffer: feature matrices go straight
+// into a padded-row-stride device layout (no transient contiguous copy).
+extern "C" int gnn_memcpy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width,
+                            size_t height, gnn_stream_t stream) {
+  using namespace gnn;
+  if ((height > 0 && width > 0) && (!dst || !src || dpitch < width || spitch < width))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (height == 0 || width == 0) return GNN_OK;
+  GNN_CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                 as_stream(stream)));
+  return GNN_OK;
+}

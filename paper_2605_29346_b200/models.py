@@ -180,7 +180,9 @@ class GCNTrainer:
     LAUNCHES_PER_STEP = None
 
     def set_inputs(self, X: torch.Tensor, labels: torch.Tensor, non_blocking: bool = False):
-        self.X.copy_(X, non_blocking=non_blocking)
+        # one strided copy into the padded-stride store (no transient [V, F] buffer);
+        # a pageable host source makes the copy synchronous, a pinned one async
+        _lib.copy_rows(self.X, X.to(torch.float32) if X.dtype != torch.float32 else X)
         self.labels.copy_(labels, non_blocking=non_blocking)
 
     def forward_backward(self):
@@ -521,7 +523,9 @@ class _FusedEpoch:
         raise NotImplementedError
 
     def set_inputs(self, X: torch.Tensor, labels: torch.Tensor, non_blocking: bool = False):
-        self.X.copy_(X, non_blocking=non_blocking)
+        # one strided copy into the padded-stride store (no transient [V, F] buffer);
+        # a pageable host source makes the copy synchronous, a pinned one async
+        _lib.copy_rows(self.X, X.to(torch.float32) if X.dtype != torch.float32 else X)
         self.labels.copy_(labels, non_blocking=non_blocking)
 
     def forward_backward(self):
