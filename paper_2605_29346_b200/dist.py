@@ -244,7 +244,7 @@ class DistGCNTrainer:
             _lib.stream_handle(h.dev)), "gcn_head")
 
     def set_inputs(self, X_local, labels_local, non_blocking=False):
-        self.X.copy_(X_local, non_blocking=non_blocking)
+        _lib.copy_rows(self.X, X_local)
         self.labels.copy_(labels_local, non_blocking=non_blocking)
 
     def step(self, ex: TorchDistExchange):
