@@ -492,17 +492,55 @@ def save_csr(graph: CsrGraph, path) -> None:
         fh.write(np.asarray(graph.targets, dtype="<i4").tobytes())
 
 
+def _stream_to_device(fh, dst: torch.Tensor, nbytes: int, chunk: int = 64 << 20) -> None:
+    """Read ``nbytes`` from ``fh`` straight into device tensor ``dst`` through
+    two pinned staging buffers: the read of chunk i+1 overlaps the H2D copy of
+    chunk i; no full host copy of the array ever exists."""
+    if nbytes == 0:
+        return
+    dev = dst.device
+    st = torch.cuda.current_stream(dev)
+    bufs = [torch.empty(min(chunk, nbytes), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    done = [None, None]
+    flat = dst.view(torch.uint8).reshape(-1)
+    pos = 0
+    k = 0
+    while pos < nbytes:
+        n = min(chunk, nbytes - pos)
+        b = bufs[k & 1]
+        if done[k & 1] is not None:
+            done[k & 1].synchronize()  # the copy that last used this buffer has landed
+        got = fh.readinto(memoryview(b.numpy())[:n])
+        if got != n:
+            raise ParseError(0, "truncated CSR1 file")
+        flat[pos:pos + n].copy_(b[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        done[k & 1] = ev
+        pos += n
+        k += 1
+    st.synchronize()
+
+
 def load_csr(path, device=None) -> CsrGraph:
-    """Read a "CSR1" file straight into device memory and validate it on
-    device (graph.py:212-220); ParseError on a bad magic."""
-    with open(path, "rb") as fh:
+    """Read a "CSR1" file (graph.py:212-220) straight into device memory —
+    the <i8 offsets and <i4 targets are streamed through pinned staging
+    buffers (read overlapped with H2D, no full host copy)
+    — and validate it on device; ParseError on a bad magic, the reference's
+    ValueError / RangeError on invariant violations."""
+    dev = _device(device)
+    with open(path, "rb", buffering=0) as fh:
         magic = fh.read(4)
         if magic != _CSR_MAGIC:
             raise ParseError(1, f"bad magic {magic!r}, expected {_CSR_MAGIC!r}")
         n, m = struct.unpack("<QQ", fh.read(16))
-        off = np.frombuffer(fh.read(8 * (n + 1)), dtype="<i8")
-        tgt = np.frombuffer(fh.read(4 * m), dtype="<i4")
-    return make_csr(int(n), off.astype(OFFSET_DTYPE), tgt.astype(TARGET_DTYPE), device=device)
+        n, m = int(n), int(m)
+        d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        d_tgt = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+        with torch.cuda.device(dev):
+            _stream_to_device(fh, d_off, 8 * (n + 1))
+            _stream_to_device(fh, d_tgt, 4 * m)
+    return make_csr(n, d_off, d_tgt, device=dev)
 
 
 # -------------------------------------------------------------- generators
