@@ -520,7 +520,7 @@ namespace gnn {
 namespace {
 
 constexpr int kHeadWarps = 4;
-constexpr int kHeadRowsPerWarp = 32;
+constexpr int kHeadRowsPerWarp = 128;
 
 // partials layout: float [nb][din*C + C] then double loss[nb] (8-byte aligned)
 inline int64_t head_float_slots(int64_t nb, int64_t din, int64_t C) {
