@@ -127,6 +127,35 @@ int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t stat
                           uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src,
                           int64_t *dst, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* --------------------------------------- sampled-block pipeline (ZeroGNN) */
+/* sample_hop (sampler.py:118-144), bit-exact with numpy's PCG64 Generator
+ * whose (state, inc) is given as 128-bit hi/lo words: active = frontier
+ * vertices of nonzero degree (order kept); draw j < A*fanout:
+ *   src[j] = frontier[active[j / fanout]],
+ *   dst[j] = targets[offsets[src] + floor(u_j * deg(src))],  u_j = stream position j.
+ * src/dst have capacity F*fanout; *count (device) receives A*fanout. */
+size_t gnn_sample_hop_workspace(int64_t F);
+int gnn_sample_hop(int64_t V, const int64_t *offsets, const int32_t *targets,
+                   const int64_t *frontier, int64_t F, int64_t fanout, uint64_t state_hi,
+                   uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src, int64_t *dst,
+                   int64_t *count, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* dedup_relabel (sampler.py:191-239): table[V] (global -> local, -1 unseen) is
+ * updated in place; destinations first seen in this hop get locals start,
+ * start+1, ... in first-occurrence order (new_globals, *new_count on device);
+ * src_local / dst_local are the relabelled draws; *error_flag = 1 when a
+ * source is not yet in the table (the reference's ValueError).  firstpos[V]
+ * is scratch that must hold INT32_MAX on entry and does on exit. */
+size_t gnn_dedup_relabel_workspace(int64_t n);
+int gnn_dedup_relabel(int64_t V, int32_t *table, int32_t *firstpos, const int64_t *src_g,
+                      const int64_t *dst_g, int64_t n, int64_t start, int32_t *src_local,
+                      int32_t *dst_local, int64_t *new_globals, int64_t *new_count,
+                      int32_t *error_flag, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* out[i] = table[ids[i]];  table[ids[i]] = start + i */
+int gnn_table_lookup(const int32_t *table, const int64_t *ids, int64_t n, int32_t *out,
+                     gnn_stream_t stream);
+int gnn_table_assign(int32_t *table, const int64_t *ids, int64_t n, int64_t start,
+                     gnn_stream_t stream);
+
 /* ----------------------------------------------------------- sparse ops */
 /* A device CSR (or CSC, which is the CSR of the transpose). */
 typedef struct gnn_csr_view {

@@ -124,6 +124,20 @@ SIGNATURES = {
         c_int,
         [c_i64, c_i64, c_ptr, c_u64, c_u64, c_u64, c_u64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_sample_hop_workspace": (c_sz, [c_i64]),
+    "gnn_sample_hop": (
+        c_int,
+        [c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_u64, c_u64, c_u64, c_u64, c_ptr, c_ptr,
+         c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_dedup_relabel_workspace": (c_sz, [c_i64]),
+    "gnn_dedup_relabel": (
+        c_int,
+        [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+         c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_table_lookup": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
+    "gnn_table_assign": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_spmm_plan_buffer_ints": (c_sz, [c_i64, c_i64, c_i64]),
     "gnn_spmm_plan_workspace": (c_sz, [c_i64]),
     "gnn_spmm_plan_build": (

@@ -777,3 +777,218 @@ extern "C" int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bound
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
+
+// ------------------------------------------- device sampled-block pipeline
+// sample_hop (sampler.py:118-144) bit-exact with numpy's
+// PCG64 stream (same jump-ahead as the generator above) and dedup_relabel
+// (sampler.py:191-239) with first-occurrence local ids, deterministic
+// (atomicMin of positions is order-independent).  Counts stay on device;
+// the Python layer reads them once per hop to size the next hop.
+namespace gnn {
+namespace {
+
+__global__ void sample_active_flags_kernel(const int64_t *__restrict__ offsets,
+                                           const int64_t *__restrict__ frontier, int64_t F,
+                                           int64_t *flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = frontier[i];
+    flags[i] = offsets[v + 1] > offsets[v] ? 1 : 0;
+  }
+}
+__global__ void sample_active_scatter_kernel(const int64_t *__restrict__ pos, int64_t F,
+                                             int64_t fanout, int64_t *active, int64_t *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (pos[i + 1] != pos[i]) active[pos[i]] = i;
+    if (i == 0) *count = pos[F] * fanout;
+  }
+}
+__global__ void __launch_bounds__(256) sample_draw_kernel(
+    const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
+    const int64_t *__restrict__ frontier, const int64_t *__restrict__ active,
+    const int64_t *__restrict__ count, int64_t cap, int64_t fanout, U128 state0, U128 inc,
+    int64_t *src, int64_t *dst) {
+  const int64_t n = *count;
+  const int64_t nchunks = ceil_div(n, kGenChunk);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = c * kGenChunk, p1 = min(p0 + kGenChunk, n);
+    U128 s = pcg_advance(state0, inc, (uint64_t)p0);
+    for (int64_t p = p0; p < p1; ++p) {
+      s = u128_add(u128_mul(s, kPcgMult), inc);
+      const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+      const int64_t v = frontier[active[p / fanout]];
+      const int64_t base = offsets[v];
+      const int64_t pick = (int64_t)(u * (double)(offsets[v + 1] - base));  // numpy astype(int64)
+      src[p] = v;
+      dst[p] = targets[base + pick];
+    }
+  }
+}
+
+__global__ void relabel_src_kernel(const int32_t *__restrict__ table, const int64_t *__restrict__ g,
+                                   int64_t n, int32_t *out, int32_t *err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = table[g[i]];
+    out[i] = l;
+    if (l < 0) *err = 1;
+  }
+}
+__global__ void fresh_first_kernel(const int32_t *__restrict__ table, const int64_t *__restrict__ g,
+                                   int64_t n, int32_t *firstpos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (table[g[i]] < 0) atomicMin(firstpos + g[i], (int32_t)i);
+}
+__global__ void first_flags_kernel(const int32_t *__restrict__ table, const int32_t *__restrict__ firstpos,
+                                   const int64_t *__restrict__ g, int64_t n, int64_t *flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (table[g[i]] < 0 && firstpos[g[i]] == (int32_t)i) ? 1 : 0;
+}
+__global__ void assign_new_kernel(const int64_t *__restrict__ rank, const int64_t *__restrict__ g,
+                                  int64_t n, int64_t start, int32_t *table, int32_t *firstpos,
+                                  int64_t *new_globals, int64_t *new_count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (rank[i + 1] != rank[i]) {
+      const int64_t v = g[i];
+      new_globals[rank[i]] = v;
+      table[v] = (int32_t)(start + rank[i]);
+      firstpos[v] = INT32_MAX;  // restore the scratch for the next hop
+    }
+    if (i == 0) *new_count = rank[n];
+  }
+}
+__global__ void lookup_kernel(const int32_t *__restrict__ table, const int64_t *__restrict__ ids,
+                              int64_t n, int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = table[ids[i]];
+}
+__global__ void assign_seq_kernel(int32_t *table, const int64_t *__restrict__ ids, int64_t n,
+                                  int64_t start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    table[ids[i]] = (int32_t)(start + i);
+}
+unsigned grid_for(int64_t n) {
+  int64_t b = ceil_div(n > 0 ? n : 1, 256), cap = (int64_t)sm_count() * 16;
+  return (unsigned)(b < cap ? b : cap);
+}
+
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+size_t gnn_sample_hop_workspace(int64_t F) {
+  using namespace gnn;
+  WsCounter c;
+  c.take<int64_t>(F + 1);  // flags / positions
+  c.take<int64_t>(F);      // active indices
+  c.used += scan_i64_workspace(F) + 256;
+  return c.used + 256;
+}
+
+int gnn_sample_hop(int64_t V, const int64_t *offsets, const int32_t *targets,
+                   const int64_t *frontier, int64_t F, int64_t fanout, uint64_t state_hi,
+                   uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src, int64_t *dst,
+                   int64_t *count, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  using namespace gnn;
+  if (V < 0 || F < 0 || fanout < 0 || !offsets || !count || (F > 0 && !frontier))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (F * fanout > 0 && (!src || !dst || !targets)) return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_sample_hop_workspace(F)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  if (F == 0 || fanout == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  int64_t *pos = ar.take<int64_t>(F + 1);
+  int64_t *active = ar.take<int64_t>(F);
+  size_t sb = scan_i64_workspace(F);
+  void *sws = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  sample_active_flags_kernel<<<grid_for(F), 256, 0, st>>>(offsets, frontier, F, pos);
+  GNN_LAUNCH_CHECK();
+  GNN_TRY(exclusive_scan_i64(pos, pos, F, true, sws, sb, st));
+  sample_active_scatter_kernel<<<grid_for(F), 256, 0, st>>>(pos, F, fanout, active, count);
+  GNN_LAUNCH_CHECK();
+  const U128 s0{state_hi, state_lo}, inc{inc_hi, inc_lo};
+  sample_draw_kernel<<<grid_for(ceil_div(F * fanout, kGenChunk)), 256, 0, st>>>(
+      offsets, targets, frontier, active, count, F * fanout, fanout, s0, inc, src, dst);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_dedup_relabel_workspace(int64_t n) {
+  using namespace gnn;
+  WsCounter c;
+  c.take<int64_t>(n + 1);
+  c.used += scan_i64_workspace(n) + 256;
+  return c.used + 256;
+}
+
+int gnn_dedup_relabel(int64_t V, int32_t *table, int32_t *firstpos, const int64_t *src_g,
+                      const int64_t *dst_g, int64_t n, int64_t start, int32_t *src_local,
+                      int32_t *dst_local, int64_t *new_globals, int64_t *new_count,
+                      int32_t *error_flag, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  using namespace gnn;
+  if (V < 0 || n < 0 || start < 0 || !table || !firstpos || !new_count || !error_flag)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (n >= ((int64_t)1 << 31) || start + n >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (n > 0 && (!src_g || !dst_g || !src_local || !dst_local || !new_globals))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_dedup_relabel_workspace(n)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  GNN_CUDA_TRY(cudaMemsetAsync(error_flag, 0, sizeof(int32_t), st));
+  if (n == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(new_count, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  int64_t *rank = ar.take<int64_t>(n + 1);
+  size_t sb = scan_i64_workspace(n);
+  void *sws = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  const unsigned gr = grid_for(n);
+  relabel_src_kernel<<<gr, 256, 0, st>>>(table, src_g, n, src_local, error_flag);
+  GNN_LAUNCH_CHECK();
+  fresh_first_kernel<<<gr, 256, 0, st>>>(table, dst_g, n, firstpos);
+  GNN_LAUNCH_CHECK();
+  first_flags_kernel<<<gr, 256, 0, st>>>(table, firstpos, dst_g, n, rank);
+  GNN_LAUNCH_CHECK();
+  GNN_TRY(exclusive_scan_i64(rank, rank, n, true, sws, sb, st));
+  assign_new_kernel<<<gr, 256, 0, st>>>(rank, dst_g, n, start, table, firstpos, new_globals,
+                                        new_count);
+  GNN_LAUNCH_CHECK();
+  lookup_kernel<<<gr, 256, 0, st>>>(table, dst_g, n, dst_local);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_table_lookup(const int32_t *table, const int64_t *ids, int64_t n, int32_t *out,
+                     gnn_stream_t stream) {
+  using namespace gnn;
+  if (n < 0 || (n > 0 && (!table || !ids || !out))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GNN_OK;
+  lookup_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(table, ids, n, out);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_table_assign(int32_t *table, const int64_t *ids, int64_t n, int64_t start,
+                     gnn_stream_t stream) {
+  using namespace gnn;
+  if (n < 0 || start < 0 || (n > 0 && (!table || !ids))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GNN_OK;
+  assign_seq_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(table, ids, n, start);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+"""Device sampled-block pipeline: the reference's
+per-iteration sampler (``gsbench/sampler.py``) with the same names, argument
+meaning, RNG contract and exceptions, running on libgnnb200 kernels:
+
+  * ``sample_hop``      sampler.py:118-144 — draws bit-exact with numpy's PCG64
+                        stream (device jump-ahead), ``pick = floor(u * deg)``;
+  * ``SubgraphBuilder`` sampler.py:146-188 — device global->local table;
+  * ``dedup_relabel``   sampler.py:191-239 — first-occurrence local ids
+                        (deterministic: atomicMin of positions + stable scan);
+  * ``build_subgraph_csr`` sampler.py:242-256 — device stable CSR build;
+  * ``sample_minibatch`` sampler.py:259-296 — one count read per hop (to size
+                        the next frontier); everything else stays on device.
+
+Results (``HopBlock`` / ``SampledSubgraph`` / ``IterationMetadata``) hold
+numpy arrays like the reference's, copied from device once per mini-batch;
+``sample_minibatch(..., on_device=True)`` keeps them as device tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError
+from .graph import CsrGraph
+from .graph import build_subgraph_csr as _device_subgraph_csr
+
+LOCAL_DTYPE = np.int32
+SeedLike = Union[int, np.random.SeedSequence, None]
+_INT32_MAX = 2**31 - 1
+
+
+@dataclass(frozen=True)
+class SampleConfig:
+    """Mini-batch size B and per-hop fanouts F_1..F_N (sampler.py:29-47)."""
+
+    batch_size: int
+    fanouts: tuple
+    seed: int = 0
+
+    def __post_init__(self):
+        object.__setattr__(self, "fanouts", tuple(int(f) for f in self.fanouts))
+        if self.batch_size < 1:
+            raise ConfigError("batch_size must be >= 1")
+        if len(self.fanouts) < 1:
+            raise ConfigError("at least one hop is required")
+        if any(f < 0 for f in self.fanouts):
+            raise ConfigError("fanouts must be nonnegative")
+
+    @property
+    def num_hops(self) -> int:
+        return len(self.fanouts)
+
+
+@dataclass
+class HopBlock:
+    hop_index: int
+    src_local: object
+    dst_unique_local: object
+    edge_src: object
+    edge_dst: object
+    raw_draw_count: int
+
+
+@dataclass
+class SampledSubgraph:
+    hops: list
+    local_to_global: object
+
+    @property
+    def num_local_vertices(self) -> int:
+        return int(self.local_to_global.shape[0])
+
+
+@dataclass(frozen=True)
+class IterationMetadata:
+    batch_size: int
+    per_hop_vertex_counts: tuple
+    per_hop_edge_counts: tuple
+    total_unique_vertices: int
+    total_edges: int
+
+    @property
+    def num_hops(self) -> int:
+        return len(self.per_hop_vertex_counts)
+
+
+def _as_seed_sequence(rng: SeedLike, default_seed: int) -> np.random.SeedSequence:
+    if rng is None:
+        return np.random.SeedSequence(default_seed)
+    if isinstance(rng, np.random.SeedSequence):
+        return rng
+    return np.random.SeedSequence(int(rng))
+
+
+def hop_state(base: np.random.SeedSequence, hop: int) -> tuple[int, int]:
+    """(state, inc) of the hop's PCG64 stream: sampler.py:99-107 appends the
+    1-based hop index to the base spawn key."""
+    if base.entropy is None:
+        raise ConfigError("entropy-less seed sequences cannot be re-derived on device")
+    child = np.random.SeedSequence(base.entropy, spawn_key=tuple(base.spawn_key) + (hop,))
+    st = np.random.PCG64(child).state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+def _i64(x, dev) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=torch.int64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).to(dev)
+
+
+def sample_hop(graph: CsrGraph, frontier, fanout: int, state: tuple[int, int]):
+    """Device sample_hop: (src, dst) int64 device tensors of the hop's draws,
+    bit-exact with sampler.py:118-144 for the PCG64 stream ``state``."""
+    lib = _lib.lib()
+    dev = graph.device
+    fr = _i64(frontier, dev)
+    F = int(fr.numel())
+    cap = F * int(fanout)
+    src = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    dst = torch.empty_like(src)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    s, inc = state
+    mask = (1 << 64) - 1
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(lib.gnn_sample_hop_workspace(F), dev)
+        _lib.check(lib.gnn_sample_hop(graph.num_vertices, graph.d_offsets.data_ptr(),
+                                      graph._device_targets().data_ptr(),
+                                      fr.data_ptr() if F else None, F, int(fanout), s >> 64,
+                                      s & mask, inc >> 64, inc & mask, src.data_ptr(),
+                                      dst.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      _lib.stream_handle(dev)), "sample_hop")
+    n = int(count.item())  # one read per hop: sizes the next hop
+    return src[:n], dst[:n]
+
+
+class SubgraphBuilder:
+    """Device twin of sampler.py:146-188: seeds take locals 0..B-1; the
+    global->local table is an int32 device array over the base graph."""
+
+    def __init__(self, num_vertices: int, seeds, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        s = np.asarray(seeds.cpu() if isinstance(seeds, torch.Tensor) else seeds, dtype=np.int64)
+        if s.size == 0:
+            raise ConfigError("seed batch must be non-empty")
+        if np.unique(s).size != s.size:
+            raise ConfigError("seed vertices must be distinct")
+        if s.min() < 0 or s.max() >= num_vertices:
+            raise ConfigError("seed vertex id out of range")
+        self.dev = dev
+        self.num_vertices = num_vertices
+        self.table = torch.full((num_vertices,), -1, dtype=torch.int32, device=dev)
+        self.firstpos = torch.full((num_vertices,), _INT32_MAX, dtype=torch.int32, device=dev)
+        seeds_d = torch.from_numpy(s).to(dev)
+        lib = _lib.lib()
+        with torch.cuda.device(dev):
+            _lib.check(lib.gnn_table_assign(self.table.data_ptr(), seeds_d.data_ptr(), s.size, 0,
+                                            _lib.stream_handle(dev)), "table_assign")
+        self._chunks = [seeds_d]
+        self._size = int(s.size)
+        self.hops: list[HopBlock] = []
+
+    @property
+    def num_local_vertices(self) -> int:
+        return self._size
+
+    def add_hop(self, hop_index: int, frontier, src_global, dst_global) -> HopBlock:
+        block = dedup_relabel(src_global, dst_global, self, hop_index, frontier=frontier)
+        self.hops.append(block)
+        return block
+
+    def finish(self) -> SampledSubgraph:
+        l2g = torch.cat(self._chunks) if len(self._chunks) > 1 else self._chunks[0]
+        return SampledSubgraph(hops=self.hops, local_to_global=l2g)
+
+
+def dedup_relabel(src_global, dst_global, builder: SubgraphBuilder, hop_index: int,
+                  frontier=None) -> HopBlock:
+    """sampler.py:191-239 on device: ValueError when a draw's source is not
+    yet in the subgraph; first-seen destinations get fresh locals in
+    first-occurrence order."""
+    lib = _lib.lib()
+    dev = builder.dev
+    sg = _i64(src_global, dev)
+    dg = _i64(dst_global, dev)
+    n = int(sg.numel())
+    src_l = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+    dst_l = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+    new_g = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    start = builder._size
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(lib.gnn_dedup_relabel_workspace(n), dev)
+        _lib.check(lib.gnn_dedup_relabel(
+            builder.num_vertices, builder.table.data_ptr(), builder.firstpos.data_ptr(),
+            sg.data_ptr() if n else None, dg.data_ptr() if n else None, n, start,
+            src_l.data_ptr() if n else None, dst_l.data_ptr() if n else None, new_g.data_ptr(),
+            cnt.data_ptr(), err.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
+            "dedup_relabel")
+    k = int(cnt.item())
+    if int(err.item()):
+        raise ValueError("hop source vertex not present in subgraph")
+    new_g = new_g[:k]
+    if k:
+        builder._chunks.append(new_g)
+        builder._size = start + k
+    new_locals = torch.arange(start, start + k, dtype=torch.int32, device=dev)
+    if frontier is not None:
+        fr = _i64(frontier, dev)
+        fl = torch.empty(max(fr.numel(), 1), dtype=torch.int32, device=dev)[:fr.numel()]
+        if fr.numel():
+            with torch.cuda.device(dev):
+                _lib.check(lib.gnn_table_lookup(builder.table.data_ptr(), fr.data_ptr(),
+                                                fr.numel(), fl.data_ptr(),
+                                                _lib.stream_handle(dev)), "table_lookup")
+    else:  # the draw sources, unique in first-occurrence order (host fallback path)
+        u, pos = np.unique(src_l.cpu().numpy(), return_index=True)
+        fl = torch.from_numpy(u[np.argsort(pos, kind="stable")].astype(LOCAL_DTYPE)).to(dev)
+    return HopBlock(hop_index=hop_index, src_local=fl, dst_unique_local=new_locals,
+                    edge_src=src_l, edge_dst=dst_l, raw_draw_count=n)
+
+
+def build_subgraph_csr(edge_src, edge_dst, num_local_src: int):
+    """sampler.py:242-256 on device (stable CSR of a sampled block)."""
+    return _device_subgraph_csr(edge_src, edge_dst, num_local_src)
+
+
+def _to_host(sg: SampledSubgraph) -> SampledSubgraph:
+    hops = [HopBlock(b.hop_index, b.src_local.cpu().numpy(), b.dst_unique_local.cpu().numpy(),
+                     b.edge_src.cpu().numpy(), b.edge_dst.cpu().numpy(), b.raw_draw_count)
+            for b in sg.hops]
+    l2g = sg.local_to_global.cpu().numpy()
+    l2g.setflags(write=False)
+    return SampledSubgraph(hops=hops, local_to_global=l2g)
+
+
+def sample_minibatch(graph: CsrGraph, config: SampleConfig, seed_vertices, rng: SeedLike = None,
+                     on_device: bool = False):
+    """sampler.py:259-296 on device: hop h's frontier is hop h-1's new
+    destinations (hop 1: the seeds); deterministic for fixed (seeds, rng)."""
+    seeds = np.asarray(seed_vertices.cpu() if isinstance(seed_vertices, torch.Tensor)
+                       else seed_vertices, dtype=np.int64)
+    if seeds.size != config.batch_size:
+        raise ConfigError(f"expected {config.batch_size} seed vertices, got {seeds.size}")
+    base = _as_seed_sequence(rng, config.seed)
+    builder = SubgraphBuilder(graph.num_vertices, seeds, device=graph.device)
+    vc, ec = [], []
+    frontier = builder._chunks[0]
+    for hop, fanout in enumerate(config.fanouts, 1):
+        src, dst = sample_hop(graph, frontier, fanout, hop_state(base, hop))
+        block = builder.add_hop(hop, frontier, src, dst)
+        vc.append(builder.num_local_vertices)
+        ec.append(block.raw_draw_count)
+        frontier = (builder._chunks[-1] if block.dst_unique_local.numel()
+                    else torch.empty(0, dtype=torch.int64, device=graph.device))
+    sg = builder.finish()
+    meta = IterationMetadata(batch_size=int(seeds.size), per_hop_vertex_counts=tuple(vc),
+                             per_hop_edge_counts=tuple(ec),
+                             total_unique_vertices=builder.num_local_vertices,
+                             total_edges=int(sum(ec)))
+    return (sg if on_device else _to_host(sg)), meta
+
+
+def gather_indices(subgraph: SampledSubgraph):
+    """sampler.py:299-305: feature rows = every sampled vertex, label rows =
+    the seed batch."""
+    batch = subgraph.hops[0].src_local.shape[0] if subgraph.hops else 0
+    l2g = subgraph.local_to_global
+    feat = l2g.clone() if isinstance(l2g, torch.Tensor) else np.array(l2g, copy=True)
+    return feat, feat[:batch].clone() if isinstance(feat, torch.Tensor) else feat[:batch].copy()
