@@ -483,7 +483,7 @@ def run_ours(args, rank, world):
         torch.cuda.empty_cache()
         extras = {}
         for name, fn in (("gin_reddit", bm.run_gin), ("gat_products", bm.run_gat),
-                         ("spmm_sweep_reddit", bm.run_sweep)):
+                         ("spmm_sweep_reddit", bm.run_sweep), ("sampling", bm.run_sampling)):
             try:
                 extras[name] = fn()
             except Exception as exc:  # report, never hide

@@ -144,9 +144,43 @@ def run_sweep():
     return out
 
 
+def run_sampling():
+    """Reference default sampling config (configs/default.json: power-law
+    n=1e5, m=2e7, exponent 2.1; B=256, fanouts [10,10]) — device
+    sample_minibatch vs the reference algorithm on the host (oracle port)."""
+    from oracle import sampler as osm
+    from paper_2605_29346_b200.sampling import SampleConfig, sample_minibatch
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 100_000, 20_000_000, exponent=2.1), 42)
+    off, tgt = g.offsets, g.targets
+    out = {}
+    for B, fan, reps in ((256, (10, 10), 20), (8192, (25, 10), 5)):
+        cfg = SampleConfig(B, fan)
+        rng = np.random.default_rng(0)
+        batches = [rng.choice(100_000, B, replace=False) for _ in range(reps)]
+        for s in batches[:2]:
+            sample_minibatch(g, cfg, s, 1, on_device=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i, s in enumerate(batches):
+            sample_minibatch(g, cfg, s, i, on_device=True)
+        torch.cuda.synchronize()
+        dev_ms = (time.perf_counter() - t0) * 1e3 / reps
+        t0 = time.perf_counter()
+        for i, s in enumerate(batches):
+            osm.sample_minibatch(off, tgt, s, cfg.fanouts, i)
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / reps
+        out[f"B{B}_F{'x'.join(map(str, fan))}"] = {"device_ms": round(dev_ms, 3),
+                                                  "cpu_reference_port_ms": round(cpu_ms, 3)}
+    return {"item": "sample_minibatch_ms",
+            "workload": "reference default graph (configs/default.json: power-law 1e5/2e7, "
+                        "exponent 2.1)", **out,
+            "note": "wall clock per mini-batch incl. the per-hop count reads (host-synchronous API)"}
+
+
 if __name__ == "__main__":
     for item in sys.argv[1:] or ["gin", "gat", "sweep"]:
-        r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep}[item]()
+        r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep, "sampling": run_sampling}[item]()
         for x in (r if isinstance(r, list) else [r]):
             print(json.dumps(x), flush=True)
         torch.cuda.empty_cache()
