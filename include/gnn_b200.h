@@ -156,6 +156,32 @@ int gnn_table_lookup(const int32_t *table, const int64_t *ids, int64_t n, int32_
 int gnn_table_assign(int32_t *table, const int64_t *ids, int64_t n, int64_t start,
                      gnn_stream_t stream);
 
+/* Device-resident-count forms (ZeroGNN DRMB): sizes are
+ * read from device scalars (F_dev, n_dev, size_dev), buffers are provisioned
+ * for a capacity envelope, grids cover the capacity with early exit
+ * (PAPER.md:1472-1474), and the PCG64 (state, inc) words come from device
+ * memory (rng_state[4] = state_hi, state_lo, inc_hi, inc_lo) — no host sync
+ * anywhere, so a whole mini-batch can be captured and replayed.
+ * gnn_dedup_relabel_dev reads the builder size from *size_dev and adds the
+ * hop's new-vertex count to it. */
+size_t gnn_sample_hop_dev_workspace(int64_t F_cap);
+int gnn_sample_hop_dev(int64_t V, const int64_t *offsets, const int32_t *targets,
+                       const int64_t *frontier, const int64_t *F_dev, int64_t F_cap, int64_t fanout,
+                       const uint64_t *rng_state, int64_t *src, int64_t *dst, int64_t *count,
+                       void *ws, size_t ws_bytes, gnn_stream_t stream);
+size_t gnn_dedup_relabel_dev_workspace(int64_t n_cap);
+int gnn_dedup_relabel_dev(int64_t V, int32_t *table, int32_t *firstpos, const int64_t *src_g,
+                          const int64_t *dst_g, const int64_t *n_dev, int64_t n_cap,
+                          int64_t *size_dev, int32_t *src_local, int32_t *dst_local,
+                          int64_t *new_globals, int64_t *new_count, int32_t *error_flag, void *ws,
+                          size_t ws_bytes, gnn_stream_t stream);
+int gnn_table_lookup_dev(const int32_t *table, const int64_t *ids, const int64_t *n_dev,
+                         int64_t n_cap, int32_t *out, gnn_stream_t stream);
+/* table[ids[i]] = value for i < *n_dev (n_dev NULL: i < n_cap) — resets the
+ * builder table between replayed mini-batches. */
+int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int64_t *n_dev, int64_t n_cap,
+                       int32_t value, gnn_stream_t stream);
+
 /* ----------------------------------------------------------- sparse ops */
 /* A device CSR (or CSC, which is the CSR of the transpose). */
 typedef struct gnn_csr_view {

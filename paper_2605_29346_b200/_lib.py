@@ -136,6 +136,20 @@ SIGNATURES = {
         [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
          c_ptr, c_sz, c_ptr],
     ),
+    "gnn_sample_hop_dev_workspace": (c_sz, [c_i64]),
+    "gnn_sample_hop_dev": (
+        c_int,
+        [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz,
+         c_ptr],
+    ),
+    "gnn_dedup_relabel_dev_workspace": (c_sz, [c_i64]),
+    "gnn_dedup_relabel_dev": (
+        c_int,
+        [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+         c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_table_lookup_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
+    "gnn_table_fill_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, C.c_int32, c_ptr]),
     "gnn_table_lookup": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "gnn_table_assign": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_spmm_plan_buffer_ints": (c_sz, [c_i64, c_i64, c_i64]),

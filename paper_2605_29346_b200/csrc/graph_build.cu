@@ -992,3 +992,220 @@ int gnn_table_assign(int32_t *table, const int64_t *ids, int64_t n, int64_t star
 }
 
 }  // extern "C"
+
+// ----------------- device-resident counts: capturable sampling (ZeroGNN DRMB)
+// The same pipeline with every size on device: buffers are provisioned for a
+// worst-case envelope (capacity), grids cover the capacity and threads past
+// the live count exit early, and nothing synchronises
+// the host, so a whole mini-batch is one CUDA graph replay.
+namespace gnn {
+namespace {
+
+__global__ void sample_active_flags_dev_kernel(const int64_t *__restrict__ offsets,
+                                               const int64_t *__restrict__ frontier,
+                                               const int64_t *__restrict__ F_dev, int64_t cap,
+                                               int64_t *flags) {
+  const int64_t F = *F_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = 0;
+    if (i < F) {
+      const int64_t v = frontier[i];
+      f = offsets[v + 1] > offsets[v] ? 1 : 0;
+    }
+    flags[i] = f;
+  }
+}
+__global__ void relabel_src_dev_kernel(const int32_t *__restrict__ table,
+                                       const int64_t *__restrict__ g, const int64_t *__restrict__ n_dev,
+                                       int64_t cap, int32_t *out, int32_t *err) {
+  const int64_t n = *n_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < min(n, cap);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = table[g[i]];
+    out[i] = l;
+    if (l < 0) *err = 1;
+  }
+}
+__global__ void fresh_first_dev_kernel(const int32_t *__restrict__ table,
+                                       const int64_t *__restrict__ g, const int64_t *__restrict__ n_dev,
+                                       int64_t cap, int32_t *firstpos) {
+  const int64_t n = *n_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < min(n, cap);
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (table[g[i]] < 0) atomicMin(firstpos + g[i], (int32_t)i);
+}
+__global__ void first_flags_dev_kernel(const int32_t *__restrict__ table,
+                                       const int32_t *__restrict__ firstpos,
+                                       const int64_t *__restrict__ g, const int64_t *__restrict__ n_dev,
+                                       int64_t cap, int64_t *flags) {
+  const int64_t n = *n_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i < n && table[g[i]] < 0 && firstpos[g[i]] == (int32_t)i) ? 1 : 0;
+}
+__global__ void assign_new_dev_kernel(const int64_t *__restrict__ rank, const int64_t *__restrict__ g,
+                                      const int64_t *__restrict__ n_dev, int64_t cap,
+                                      const int64_t *__restrict__ size_dev, int32_t *table,
+                                      int32_t *firstpos, int64_t *new_globals, int64_t *new_count) {
+  const int64_t n = min(*n_dev, cap), start = *size_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (rank[i + 1] != rank[i]) {
+      const int64_t v = g[i];
+      new_globals[rank[i]] = v;
+      table[v] = (int32_t)(start + rank[i]);
+      firstpos[v] = INT32_MAX;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *new_count = rank[cap];
+}
+__global__ void lookup_dev_kernel(const int32_t *__restrict__ table, const int64_t *__restrict__ ids,
+                                  const int64_t *__restrict__ n_dev, int64_t cap, int32_t *out) {
+  const int64_t n = min(*n_dev, cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = table[ids[i]];
+}
+__global__ void size_add_kernel(int64_t *size_dev, const int64_t *__restrict__ add) {
+  *size_dev += *add;
+}
+__global__ void sample_draw_dev_kernel(const int64_t *__restrict__ offsets,
+                                       const int32_t *__restrict__ targets,
+                                       const int64_t *__restrict__ frontier,
+                                       const int64_t *__restrict__ active,
+                                       const int64_t *__restrict__ count, int64_t fanout,
+                                       const uint64_t *__restrict__ rng, int64_t *src, int64_t *dst) {
+  const U128 state0{rng[0], rng[1]}, inc{rng[2], rng[3]};
+  const int64_t n = *count;
+  const int64_t nchunks = ceil_div(n, kGenChunk);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = c * kGenChunk, p1 = min(p0 + kGenChunk, n);
+    U128 s = pcg_advance(state0, inc, (uint64_t)p0);
+    for (int64_t p = p0; p < p1; ++p) {
+      s = u128_add(u128_mul(s, kPcgMult), inc);
+      const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+      const int64_t v = frontier[active[p / fanout]];
+      const int64_t base = offsets[v];
+      const int64_t pick = (int64_t)(u * (double)(offsets[v + 1] - base));
+      src[p] = v;
+      dst[p] = targets[base + pick];
+    }
+  }
+}
+
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+size_t gnn_sample_hop_dev_workspace(int64_t F_cap) { return gnn_sample_hop_workspace(F_cap); }
+
+int gnn_sample_hop_dev(int64_t V, const int64_t *offsets, const int32_t *targets,
+                       const int64_t *frontier, const int64_t *F_dev, int64_t F_cap, int64_t fanout,
+                       const uint64_t *rng_state, int64_t *src, int64_t *dst, int64_t *count,
+                       void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  using namespace gnn;
+  if (V < 0 || F_cap < 0 || fanout < 0 || !offsets || !F_dev || !count || !rng_state)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (F_cap * fanout > 0 && (!src || !dst || !targets || !frontier)) return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_sample_hop_dev_workspace(F_cap)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  if (F_cap == 0 || fanout == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  int64_t *pos = ar.take<int64_t>(F_cap + 1);
+  int64_t *active = ar.take<int64_t>(F_cap);
+  size_t sb = scan_i64_workspace(F_cap);
+  void *sws = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  sample_active_flags_dev_kernel<<<grid_for(F_cap), 256, 0, st>>>(offsets, frontier, F_dev, F_cap,
+                                                                   pos);
+  GNN_LAUNCH_CHECK();
+  GNN_TRY(exclusive_scan_i64(pos, pos, F_cap, true, sws, sb, st));
+  sample_active_scatter_kernel<<<grid_for(F_cap), 256, 0, st>>>(pos, F_cap, fanout, active, count);
+  GNN_LAUNCH_CHECK();
+  sample_draw_dev_kernel<<<grid_for(ceil_div(F_cap * fanout, kGenChunk)), 256, 0, st>>>(
+      offsets, targets, frontier, active, count, fanout, rng_state, src, dst);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_dedup_relabel_dev_workspace(int64_t n_cap) { return gnn_dedup_relabel_workspace(n_cap); }
+
+int gnn_dedup_relabel_dev(int64_t V, int32_t *table, int32_t *firstpos, const int64_t *src_g,
+                          const int64_t *dst_g, const int64_t *n_dev, int64_t n_cap,
+                          int64_t *size_dev, int32_t *src_local, int32_t *dst_local,
+                          int64_t *new_globals, int64_t *new_count, int32_t *error_flag, void *ws,
+                          size_t ws_bytes, gnn_stream_t stream) {
+  using namespace gnn;
+  if (V < 0 || n_cap < 0 || !table || !firstpos || !n_dev || !size_dev || !new_count || !error_flag)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (n_cap >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (n_cap > 0 && (!src_g || !dst_g || !src_local || !dst_local || !new_globals))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_dedup_relabel_dev_workspace(n_cap)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  if (n_cap == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(new_count, 0, sizeof(int64_t), st));
+    return GNN_OK;
+  }
+  WsArena ar(ws, ws_bytes);
+  int64_t *rank = ar.take<int64_t>(n_cap + 1);
+  size_t sb = scan_i64_workspace(n_cap);
+  void *sws = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  const unsigned gr = grid_for(n_cap);
+  relabel_src_dev_kernel<<<gr, 256, 0, st>>>(table, src_g, n_dev, n_cap, src_local, error_flag);
+  GNN_LAUNCH_CHECK();
+  fresh_first_dev_kernel<<<gr, 256, 0, st>>>(table, dst_g, n_dev, n_cap, firstpos);
+  GNN_LAUNCH_CHECK();
+  first_flags_dev_kernel<<<gr, 256, 0, st>>>(table, firstpos, dst_g, n_dev, n_cap, rank);
+  GNN_LAUNCH_CHECK();
+  GNN_TRY(exclusive_scan_i64(rank, rank, n_cap, true, sws, sb, st));
+  assign_new_dev_kernel<<<gr, 256, 0, st>>>(rank, dst_g, n_dev, n_cap, size_dev, table, firstpos,
+                                            new_globals, new_count);
+  GNN_LAUNCH_CHECK();
+  lookup_dev_kernel<<<gr, 256, 0, st>>>(table, dst_g, n_dev, n_cap, dst_local);
+  GNN_LAUNCH_CHECK();
+  size_add_kernel<<<1, 1, 0, st>>>(size_dev, new_count);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_table_lookup_dev(const int32_t *table, const int64_t *ids, const int64_t *n_dev,
+                         int64_t n_cap, int32_t *out, gnn_stream_t stream) {
+  using namespace gnn;
+  if (n_cap < 0 || !n_dev || (n_cap > 0 && (!table || !ids || !out))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n_cap == 0) return GNN_OK;
+  lookup_dev_kernel<<<grid_for(n_cap), 256, 0, as_stream(stream)>>>(table, ids, n_dev, n_cap, out);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"
+
+namespace gnn {
+namespace {
+__global__ void fill_dev_kernel(int32_t *table, const int64_t *__restrict__ ids,
+                                const int64_t *__restrict__ n_dev, int64_t cap, int32_t value) {
+  const int64_t n = n_dev ? min(*n_dev, cap) : cap;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    table[ids[i]] = value;
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int64_t *n_dev,
+                                  int64_t n_cap, int32_t value, gnn_stream_t stream) {
+  using namespace gnn;
+  if (n_cap < 0 || (n_cap > 0 && (!table || !ids))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n_cap == 0) return GNN_OK;
+  fill_dev_kernel<<<grid_for(n_cap), 256, 0, as_stream(stream)>>>(table, ids, n_dev, n_cap, value);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}

@@ -274,3 +274,143 @@ def gather_indices(subgraph: SampledSubgraph):
     l2g = subgraph.local_to_global
     feat = l2g.clone() if isinstance(l2g, torch.Tensor) else np.array(l2g, copy=True)
     return feat, feat[:batch].clone() if isinstance(feat, torch.Tensor) else feat[:batch].copy()
+
+
+class DeviceSampler:
+    """Host-sync-free, replayable ``sample_minibatch`` (ZeroGNN's device-
+    resident metadata + capture/replay; the
+    reference models it in execmodel.py:430-490).  Every buffer is
+    provisioned for the worst-case envelope of ``config`` (hop h: frontier ≤
+    B·Π_{i<h} F_i, draws ≤ frontier·F_h); counts live in device scalars;
+    kernels cover the capacity and exit early past the live count.  One
+    mini-batch = one CUDA graph replay that also copies the seeds and the
+    per-hop PCG64 states in from pinned host memory.  ``result()`` reads the
+    sampled blocks back (bit-exact with ``sample_minibatch``)."""
+
+    def __init__(self, graph: CsrGraph, config: SampleConfig):
+        lib = _lib.lib()
+        self.lib, self.g, self.cfg = lib, graph, config
+        dev = graph.device
+        self.dev = dev
+        B, H = config.batch_size, config.num_hops
+        i64 = dict(dtype=torch.int64, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.table = torch.full((graph.num_vertices,), -1, **i32)
+        self.firstpos = torch.full((graph.num_vertices,), _INT32_MAX, **i32)
+        self.size = torch.zeros(1, **i64)
+        self.err = torch.zeros(1, **i32)
+        self.seeds = torch.zeros(B, **i64)
+        self.B_dev = torch.full((1,), B, **i64)
+        self.rng = torch.zeros(H, 4, dtype=torch.int64, device=dev)  # uint64 words
+        self.seeds_h = torch.zeros(B, dtype=torch.int64).pin_memory()
+        self.rng_h = torch.zeros(H, 4, dtype=torch.int64).pin_memory()
+        self.hops = []
+        f_cap = B
+        for h, fan in enumerate(config.fanouts):
+            n_cap = f_cap * fan
+            hop = dict(
+                f_cap=f_cap, n_cap=n_cap, fanout=fan,
+                src=torch.empty(max(n_cap, 1), **i64), dst=torch.empty(max(n_cap, 1), **i64),
+                count=torch.zeros(1, **i64), new_count=torch.zeros(1, **i64),
+                src_local=torch.empty(max(n_cap, 1), **i32),
+                dst_local=torch.empty(max(n_cap, 1), **i32),
+                new_globals=torch.empty(max(n_cap, 1), **i64),
+                frontier_local=torch.empty(max(f_cap, 1), **i32),
+                ws_s=_lib.workspace(lib.gnn_sample_hop_dev_workspace(f_cap), dev),
+                ws_d=_lib.workspace(lib.gnn_dedup_relabel_dev_workspace(n_cap), dev))
+            self.hops.append(hop)
+            f_cap = n_cap
+        self.graph = None
+
+    def _launch(self):
+        lib, g, st = self.lib, self.g, _lib.stream_handle(self.dev)
+        B = self.cfg.batch_size
+        self.seeds.copy_(self.seeds_h, non_blocking=True)
+        self.rng.copy_(self.rng_h, non_blocking=True)
+        _lib.check(lib.gnn_table_assign(self.table.data_ptr(), self.seeds.data_ptr(), B, 0, st),
+                   "table_assign")
+        self.size.fill_(B)
+        frontier, f_dev = self.seeds, self.B_dev
+        tgt = g._device_targets()
+        for h, hop in enumerate(self.hops):
+            _lib.check(lib.gnn_sample_hop_dev(
+                g.num_vertices, g.d_offsets.data_ptr(), tgt.data_ptr(), frontier.data_ptr(),
+                f_dev.data_ptr(), hop["f_cap"], hop["fanout"], self.rng[h].data_ptr(),
+                hop["src"].data_ptr(), hop["dst"].data_ptr(), hop["count"].data_ptr(),
+                hop["ws_s"].data_ptr(), hop["ws_s"].numel(), st), "sample_hop_dev")
+            _lib.check(lib.gnn_dedup_relabel_dev(
+                g.num_vertices, self.table.data_ptr(), self.firstpos.data_ptr(),
+                hop["src"].data_ptr(), hop["dst"].data_ptr(), hop["count"].data_ptr(),
+                hop["n_cap"], self.size.data_ptr(), hop["src_local"].data_ptr(),
+                hop["dst_local"].data_ptr(), hop["new_globals"].data_ptr(),
+                hop["new_count"].data_ptr(), self.err.data_ptr(), hop["ws_d"].data_ptr(),
+                hop["ws_d"].numel(), st), "dedup_relabel_dev")
+            _lib.check(lib.gnn_table_lookup_dev(self.table.data_ptr(), frontier.data_ptr(),
+                                                f_dev.data_ptr(), hop["f_cap"],
+                                                hop["frontier_local"].data_ptr(), st),
+                       "table_lookup_dev")
+            frontier, f_dev = hop["new_globals"], hop["new_count"]
+        # reset the table for the next mini-batch (seeds + every hop's new vertices)
+        _lib.check(lib.gnn_table_fill_dev(self.table.data_ptr(), self.seeds.data_ptr(), None, B,
+                                          -1, st), "table_fill_dev")
+        for hop in self.hops:
+            _lib.check(lib.gnn_table_fill_dev(self.table.data_ptr(), hop["new_globals"].data_ptr(),
+                                              hop["new_count"].data_ptr(), hop["n_cap"], -1, st),
+                       "table_fill_dev")
+
+    def _stage(self, seeds, rng: SeedLike):
+        s = np.asarray(seeds, dtype=np.int64)
+        if s.size != self.cfg.batch_size:
+            raise ConfigError(f"expected {self.cfg.batch_size} seed vertices, got {s.size}")
+        base = _as_seed_sequence(rng, self.cfg.seed)
+        self.seeds_h.copy_(torch.from_numpy(s))
+        words = []
+        for h in range(1, self.cfg.num_hops + 1):
+            st, inc = hop_state(base, h)
+            words.append([st >> 64, st & ((1 << 64) - 1), inc >> 64, inc & ((1 << 64) - 1)])
+        self.rng_h.copy_(torch.from_numpy(np.array(words, dtype=np.uint64).view(np.int64)))
+
+    def capture(self):
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self._launch()
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self._launch()
+        self.graph = graph
+        return graph
+
+    def run(self, seeds, rng: SeedLike = None):
+        """One mini-batch: stage seeds + RNG states in pinned memory, replay."""
+        self._stage(seeds, rng)
+        if self.graph is None:
+            self._launch()
+        else:
+            self.graph.replay()
+
+    def result(self):
+        """(SampledSubgraph, IterationMetadata) with host arrays (synchronises)."""
+        torch.cuda.synchronize(self.dev)
+        if int(self.err.item()):
+            raise ValueError("hop source vertex not present in subgraph")
+        B = self.cfg.batch_size
+        chunks = [self.seeds.cpu().numpy()]
+        hops, vc, ec = [], [], []
+        size = B
+        for h, hop in enumerate(self.hops):
+            n, k = int(hop["count"].item()), int(hop["new_count"].item())
+            f = B if h == 0 else int(self.hops[h - 1]["new_count"].item())
+            new_l = np.arange(size, size + k, dtype=LOCAL_DTYPE)
+            size += k
+            chunks.append(hop["new_globals"][:k].cpu().numpy())
+            hops.append(HopBlock(h + 1, hop["frontier_local"][:f].cpu().numpy(), new_l,
+                                 hop["src_local"][:n].cpu().numpy(),
+                                 hop["dst_local"][:n].cpu().numpy(), n))
+            vc.append(size)
+            ec.append(n)
+        l2g = np.concatenate(chunks)
+        meta = IterationMetadata(B, tuple(vc), tuple(ec), size, int(sum(ec)))
+        return SampledSubgraph(hops=hops, local_to_global=l2g), meta
