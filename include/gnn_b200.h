@@ -182,6 +182,12 @@ int gnn_table_lookup_dev(const int32_t *table, const int64_t *ids, const int64_t
 int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int64_t *n_dev, int64_t n_cap,
                        int32_t value, gnn_stream_t stream);
 
+/* Feature gather of a sampled mini-batch (the pipeline's "gather" kernel,
+ * execmodel.py:306-314; rows = gather_indices, sampler.py:299-305):
+ * out[i, :] = X[ids[i], :]. */
+int gnn_gather_rows(const float *X, int64_t ldx, const int64_t *ids, int64_t n, int64_t K,
+                    float *out, int64_t ldo, gnn_stream_t stream);
+
 /* ----------------------------------------------------------- sparse ops */
 /* A device CSR (or CSC, which is the CSR of the transpose). */
 typedef struct gnn_csr_view {

@@ -150,6 +150,7 @@ SIGNATURES = {
     ),
     "gnn_table_lookup_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "gnn_table_fill_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, C.c_int32, c_ptr]),
+    "gnn_gather_rows": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "gnn_table_lookup": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "gnn_table_assign": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_spmm_plan_buffer_ints": (c_sz, [c_i64, c_i64, c_i64]),

@@ -1209,3 +1209,51 @@ extern "C" int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int6
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
+
+// Feature gather of a sampled mini-batch (the reference pipeline's "gather"
+// kernel class, execmodel.py:306-314): out[i, :] = X[ids[i], :].
+namespace gnn {
+namespace {
+__global__ void gather_rows_vec_kernel(const float4 *__restrict__ X, int64_t ldx4,
+                                       const int64_t *__restrict__ ids, int64_t n, int64_t K4,
+                                       float4 *out, int64_t ldo4) {
+  const int64_t total = n * K4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / K4, k = t % K4;
+    out[i * ldo4 + k] = __ldg(X + ids[i] * ldx4 + k);
+  }
+}
+__global__ void gather_rows_kernel(const float *__restrict__ X, int64_t ldx,
+                                   const int64_t *__restrict__ ids, int64_t n, int64_t K,
+                                   float *out, int64_t ldo) {
+  const int64_t total = n * K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / K, k = t % K;
+    out[i * ldo + k] = __ldg(X + ids[i] * ldx + k);
+  }
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" int gnn_gather_rows(const float *X, int64_t ldx, const int64_t *ids, int64_t n,
+                               int64_t K, float *out, int64_t ldo, gnn_stream_t stream) {
+  using namespace gnn;
+  if (n < 0 || K < 0 || ldx < K || ldo < K || (n > 0 && K > 0 && (!X || !ids || !out)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (n == 0 || K == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  const bool v4 = K % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(X) & 15u) == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  if (v4) {
+    gather_rows_vec_kernel<<<grid_for(n * K / 4), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(X), ldx / 4, ids, n, K / 4,
+        reinterpret_cast<float4 *>(out), ldo / 4);
+  } else {
+    gather_rows_kernel<<<grid_for(n * K), 256, 0, st>>>(X, ldx, ids, n, K, out, ldo);
+  }
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}

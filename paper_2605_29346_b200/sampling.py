@@ -414,3 +414,17 @@ class DeviceSampler:
         l2g = np.concatenate(chunks)
         meta = IterationMetadata(B, tuple(vc), tuple(ec), size, int(sum(ec)))
         return SampledSubgraph(hops=hops, local_to_global=l2g), meta
+
+
+def gather_features(X: torch.Tensor, ids: torch.Tensor, out: torch.Tensor | None = None):
+    """out[i] = X[ids[i]] on libgnnb200 (the mini-batch feature gather)."""
+    lib = _lib.lib()
+    ids = ids.to(device=X.device, dtype=torch.int64).contiguous()
+    n, K = int(ids.numel()), int(X.shape[1])
+    if out is None:
+        out = torch.empty(n, K, dtype=torch.float32, device=X.device)
+    with torch.cuda.device(X.device):
+        _lib.check(lib.gnn_gather_rows(X.data_ptr(), X.stride(0), ids.data_ptr() if n else None,
+                                       n, K, out.data_ptr(), out.stride(0),
+                                       _lib.stream_handle(X.device)), "gather_rows")
+    return out

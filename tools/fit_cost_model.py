@@ -1,5 +1,6 @@
 """measure the B200 path and fit the
-reference cost model's ``train`` kernel class.
+reference cost model's ``train`` kernel class (and, from the device sampling
+pipeline, the ``sample`` / ``relabel`` / ``build`` / ``gather`` classes).
 
 The reference models each of the 2*layers GNN training kernels of an
 iteration as KernelCoeffs(a, b_v, b_e, b_f) with device time
@@ -24,8 +25,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
-import paper_2605_29346_b200 as gb
-from paper_2605_29346_b200 import _lib
+import paper_2605_29346_b200 as gb  # noqa: E402
+from paper_2605_29346_b200 import _lib  # noqa: E402
 from paper_2605_29346_b200.kernels import GemmCall, SpmmCall
 
 HIDDEN = 16
@@ -98,6 +99,107 @@ def nnls(Amat, y):
         active.remove(min(neg, key=lambda i: x[i]))
 
 
+def timed_us(fn, reps=20):
+    """Device time (us) of fn() replayed from a CUDA graph."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fn()
+    for _ in range(3):
+        graph.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        graph.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / reps
+
+
+def pipeline_points():
+    """(class, [1, V, E, V*K], us) measurements of the sampling-pipeline
+    kernel classes on the device pipeline (sampling.py / graph_build.cu):
+    sample (gnn_sample_hop_dev), relabel (gnn_dedup_relabel_dev), build
+    (gnn_subgraph_csr), gather (gnn_gather_rows)."""
+    from paper_2605_29346_b200.sampling import DeviceSampler, SampleConfig
+
+    lib = _lib.lib()
+    pts = []
+    g = gb.generate(gb.GraphGenSpec("power-law", 100_000, 20_000_000, exponent=2.1), 42)
+    for B, fan in ((64, 10), (256, 10), (1024, 25), (4096, 25), (16384, 25)):
+        ds = DeviceSampler(g, SampleConfig(B, (fan,)))
+        ds._stage(np.random.default_rng(B).choice(100_000, B, replace=False), 1)
+        hop = ds.hops[0]
+        st = lambda: _lib.stream_handle(g.device)  # noqa: E731
+        tgt = g._device_targets()
+
+        def sample():
+            _lib.check(lib.gnn_sample_hop_dev(
+                g.num_vertices, g.d_offsets.data_ptr(), tgt.data_ptr(), ds.seeds.data_ptr(),
+                ds.B_dev.data_ptr(), hop["f_cap"], fan, ds.rng[0].data_ptr(), hop["src"].data_ptr(),
+                hop["dst"].data_ptr(), hop["count"].data_ptr(), hop["ws_s"].data_ptr(),
+                hop["ws_s"].numel(), st()))
+
+        ds.seeds.copy_(ds.seeds_h)
+        ds.rng.copy_(ds.rng_h)
+        sample()
+        torch.cuda.synchronize()
+        E = int(hop["count"].item())
+        pts.append(("sample", [1.0, 0, E, 0], timed_us(sample)))
+        table = ds.table
+
+        def relabel():
+            lib.gnn_table_assign(table.data_ptr(), ds.seeds.data_ptr(), B, 0, st())
+            ds.size.fill_(B)
+            _lib.check(lib.gnn_dedup_relabel_dev(
+                g.num_vertices, table.data_ptr(), ds.firstpos.data_ptr(), hop["src"].data_ptr(),
+                hop["dst"].data_ptr(), hop["count"].data_ptr(), hop["n_cap"], ds.size.data_ptr(),
+                hop["src_local"].data_ptr(), hop["dst_local"].data_ptr(),
+                hop["new_globals"].data_ptr(), hop["new_count"].data_ptr(), ds.err.data_ptr(),
+                hop["ws_d"].data_ptr(), hop["ws_d"].numel(), st()))
+            lib.gnn_table_fill_dev(table.data_ptr(), ds.seeds.data_ptr(), None, B, -1, st())
+            lib.gnn_table_fill_dev(table.data_ptr(), hop["new_globals"].data_ptr(),
+                                   hop["new_count"].data_ptr(), hop["n_cap"], -1, st())
+
+        pts.append(("relabel", [1.0, 0, E, 0], timed_us(relabel)))
+        relabel()
+        torch.cuda.synchronize()
+        n_loc = B + int(hop["new_count"].item())
+        es = hop["src_local"][:E].to(torch.int64)
+        ed = hop["dst_local"][:E].to(torch.int64)
+        off = torch.empty(n_loc + 1, dtype=torch.int64, device="cuda")
+        tg = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+        wsb = _lib.workspace(lib.gnn_subgraph_csr_workspace(n_loc, E), g.device)
+
+        def build():
+            # gnn_subgraph_csr synchronises once (error report); time the kernels directly
+            _lib.check(lib.gnn_subgraph_csr(n_loc, E, es.data_ptr(), ed.data_ptr(), off.data_ptr(),
+                                            tg.data_ptr(), wsb.data_ptr(), wsb.numel(), st()))
+
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(2):
+            build()
+        a.record()
+        for _ in range(10):
+            build()
+        b.record()
+        torch.cuda.synchronize()
+        pts.append(("build", [1.0, 0, E, 0], a.elapsed_time(b) * 1e3 / 10))
+        for K in (100, 602):
+            X = torch.rand(100_000, K, device="cuda")
+            ids = torch.from_numpy(np.random.default_rng(K).integers(0, 100_000, n_loc)).cuda()
+            outb = torch.empty(n_loc, K, device="cuda")
+            pts.append(("gather", [1.0, n_loc, 0, n_loc * K], timed_us(
+                lambda: lib.gnn_gather_rows(X.data_ptr(), K, ids.data_ptr(), n_loc, K,
+                                            outb.data_ptr(), K, st()))))
+    return pts
+
+
 def main(out):
     rows, ys = [], []
     for V in (2_000, 20_000, 200_000):
@@ -117,9 +219,28 @@ def main(out):
     rel = np.abs(pred - y) / y
     cal = json.loads(json.dumps(REFERENCE_DEFAULT))
     cal["kernel_coeffs"]["train"] = {"a": coef[0], "b_v": coef[1], "b_e": coef[2], "b_f": coef[3]}
+    # sampling-pipeline classes from the device pipeline (same affine form;
+    # terms the reference's KernelSpec does not feed stay 0)
+    pts = pipeline_points()
+    fits = {}
+    for cls in ("sample", "relabel", "build", "gather"):
+        P = [(r, t) for c, r, t in pts if c == cls]
+        A2 = np.array([r for r, _ in P], dtype=np.float64)
+        y2 = np.array([t for _, t in P])
+        used = [0] + [i for i in (1, 2, 3) if np.any(A2[:, i])]
+        c2 = np.zeros(4)
+        c2[used] = nnls(A2[:, used] / y2[:, None], np.ones_like(y2))
+        r2 = np.abs(A2 @ c2 - y2) / y2
+        fits[cls] = {"max_rel_err": float(r2.max()), "points": len(P)}
+        cal["kernel_coeffs"][cls] = {k: float(v) for k, v in zip(("a", "b_v", "b_e", "b_f"), c2)
+                                     if v != 0.0 or k == "a"}
+        print(json.dumps({"class": cls, "coeffs": cal["kernel_coeffs"][cls], **fits[cls]}))
     cal["provenance"] = (
-        "Time unit: microseconds. Host constants and non-train kernel coefficients: the "
-        "reference calibration/default.json unchanged. 'train' fitted by "
+        "Time unit: microseconds. Host constants and the pre/scan classes: the reference "
+        "calibration/default.json unchanged. 'sample', 'relabel', 'build', 'gather' fitted to "
+        "B200 measurements of the device sampling pipeline (gnn_sample_hop_dev, "
+        "gnn_dedup_relabel_dev, gnn_subgraph_csr, gnn_gather_rows; reference default graph, "
+        "B 64..16384, fanout 10/25). 'train' fitted by "
         "tools/fit_cost_model.py (non-negative least squares, relative weighting) to "
         f"{len(y)} B200 measurements of one GCN layer fwd+bwd / 2 on libgnnb200 "
         "(tcgen05 X.W, fused-norm SpMMv, CSC SpMMv, weight-gradient GEMM; CUDA-graph replay) "
