@@ -134,3 +134,13 @@ def test_replayed_device_sampler_matches_oracle(gb, fanouts):
             for got, key in ((b.src_local, "frontier_local"), (b.dst_unique_local, "new_unique_local"),
                              (b.edge_src, "edge_src"), (b.edge_dst, "edge_dst")):
                 assert np.array_equal(got, h[key]), (it, key)
+
+
+@pytest.mark.parametrize("K", [100, 602, 3])
+def test_gather_features(gb, K):
+    from paper_2605_29346_b200.sampling import gather_features
+
+    X = torch.rand(5000, K, device="cuda")
+    ids = torch.from_numpy(np.random.default_rng(K).integers(0, 5000, 777)).cuda()
+    out = gather_features(X, ids)
+    assert torch.equal(out, X[ids])
