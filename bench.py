@@ -566,7 +566,7 @@ def run_dist(args, rank, world):
         "data": "synthetic (device power-law generator, bit-exact gsbench.generate seed 42; "
                 "X~U[-1,1) f32, labels uniform)",
         "config": {"workload": "2-layer GCN full-graph epoch, Reddit-shape power-law graph, "
-                               "1D row partition (edge-balanced) + NCCL all-gathers",
+                               "1D row partition (cost-balanced: deg + 170 per row) + NCCL all-gathers",
                    "V": V, "E": E, "K": F, "hidden": Hd, "classes": C, "layout": "coalesced",
                    "optimizer": "adam", "parallelism": f"rowpart{world}",
                    "rows_rank0": part.rows, "bounds": [int(x) for x in part.bounds],

@@ -32,16 +32,26 @@ from .models import glorot
 
 
 # ----------------------------------------------------------- host logic
-def partition_bounds(offsets: np.ndarray, parts: int) -> np.ndarray:
-    """Row boundaries [P+1] of contiguous blocks holding ~E/P edges each
-    (searchsorted on the CSR offsets; every block non-empty when V >= P)."""
+# Per-row cost of the GCN epoch in edge-equivalents: the SpMMs cost ~15 ps per
+# (canonical) edge, the row-proportional work (X.W1 and X^T.dH1 at 602
+# features, the fused head, mask/norm) ~2.6 ns per row on B200 (bench.py
+# kernels_ms, Reddit shape) -> ~170 edges.  Balancing deg(r) + ROW_COST keeps
+# both the sparse and the dense work even across ranks.
+ROW_COST = 170
+
+
+def partition_bounds(offsets: np.ndarray, parts: int, row_cost: float = 0.0) -> np.ndarray:
+    """Row boundaries [P+1] of contiguous blocks of ~equal cost
+    sum_r (deg(r) + row_cost); row_cost = 0 balances edges only
+    (searchsorted on the cumulative cost; every block non-empty when V >= P)."""
     offsets = np.asarray(offsets, dtype=np.int64)
     V = offsets.size - 1
-    E = int(offsets[-1])
     if parts <= 0:
         raise ValueError("parts must be positive")
-    targets = (E * np.arange(parts + 1, dtype=np.float64) / parts).astype(np.int64)
-    b = np.searchsorted(offsets, targets, side="left").astype(np.int64)
+    cum = offsets.astype(np.float64) + row_cost * np.arange(V + 1, dtype=np.float64)
+    total = cum[-1]
+    targets = total * np.arange(parts + 1, dtype=np.float64) / parts
+    b = np.searchsorted(cum, targets, side="left").astype(np.int64)
     b[0], b[-1] = 0, V
     b = np.maximum.accumulate(np.minimum(b, V))
     # keep every block non-empty in rows when possible (P <= V)
@@ -118,7 +128,8 @@ class RowPartition:
                  bounds: np.ndarray | None = None):
         self.g, self.parts, self.rank = g, parts, rank
         dev = g.device
-        self.bounds = partition_bounds(g.offsets, parts) if bounds is None else np.asarray(bounds)
+        self.bounds = (partition_bounds(g.offsets, parts, ROW_COST) if bounds is None
+                       else np.asarray(bounds))
         self.stride = block_stride(self.bounds)
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
         self.rows = self.hi - self.lo

@@ -142,3 +142,17 @@ def test_partitioned_gcn_exchange_matches_single_process(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert err < 1e-12, err
+
+
+def test_partition_bounds_row_cost_balances_rows_and_edges():
+    from paper_2605_29346_b200.dist import ROW_COST
+
+    off, _ = _graph(V=5000, E=200_000)
+    for P in (2, 4, 8):
+        b = partition_bounds(off, P, ROW_COST)
+        cost = (off[b[1:]] - off[b[:-1]]) + ROW_COST * np.diff(b)
+        ideal = (off[-1] + ROW_COST * (off.size - 1)) / P
+        assert np.all(np.abs(cost - ideal) <= np.diff(off).max() + ROW_COST + 1)
+        # the edge-only split starves the first block of rows on a power-law graph
+        b0 = partition_bounds(off, P)
+        assert np.diff(b).max() <= np.diff(b0).max()
