@@ -356,22 +356,26 @@ def run_ours(args, rank, world):
     loss_val = float(tr.loss.item())
 
     # ---- e2e: host buffers in, loss out, copies inside the timed region.  The
-    # host X is laid out with the trainer's 128-byte row stride (608 floats), so
-    # each of the 8 row blocks is one contiguous H2D copy that overlaps the
-    # X W1 GEMM of the blocks before it (GCNTrainer.capture_e2e).
+    # host X is laid out with the trainer's 128-byte row stride (608 floats) so
+    # it copies as one contiguous block.  Inputs are double-buffered: each step
+    # (one CUDA graph) trains on one device buffer while the copy stream loads
+    # the next step's X / labels into the other; the first step's copy (prime)
+    # is inside the timed region too.
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
     Xp_h = torch.zeros(V, tr.Fpad, dtype=torch.float32).pin_memory()
     Xp_h[:, :F].copy_(X_h)
-    tr.capture_e2e(Xp_h, y_h, loss_h)
-    for _ in range(2):
-        tr.run_e2e()
+    tr.capture_e2e_pipelined(Xp_h, y_h, loss_h)
+    tr.prime_e2e()
+    for k in range(2):
+        tr.run_e2e_pipelined(k)
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(st)
-    for _ in range(args.steps):
-        tr.run_e2e()
+    tr.prime_e2e()
+    for k in range(args.steps):
+        tr.run_e2e_pipelined(k)
     b.record(st)
     torch.cuda.synchronize()
     e2e_ms = a.elapsed_time(b) / args.steps
@@ -434,9 +438,10 @@ def run_ours(args, rank, world):
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms",
                 "h2d_bytes_per_step": int(Xp_h.numel() * 4 + y_h.numel() * 8),
                 "d2h_bytes_per_step": 4, "loss_read_back": e2e_loss,
-                "how": "one CUDA graph per step: X (8 row blocks, row stride 608) and labels "
-                       "copied from pinned host memory, X.W1 per block as it lands, rest of "
-                       "the epoch, loss copied back"},
+                "how": "one CUDA graph per step trains on one device input buffer while a copy "
+                       "stream loads the next step's X (row stride 608) and labels from pinned "
+                       "host memory into the other; loss copied back every step; the first "
+                       "step's copy is inside the timed region"},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"kernel": "spmm width-16 (4 per epoch, avg, timed in-epoch)", "bound": "hbm",
                      "achieved": round(ach16, 1), "peak": hbm_peak, "unit": "GB/s",

@@ -306,6 +306,72 @@ class GCNTrainer:
     def run_e2e(self):
         self.graph_e2e.replay()
 
+    # ---- end-to-end, double-buffered inputs: step k's H2D of the NEXT
+    # step's inputs runs under step k's compute
+    def capture_e2e_pipelined(self, X_host: torch.Tensor, labels_host: torch.Tensor,
+                              loss_host: torch.Tensor):
+        """Two CUDA graphs over two device input buffers: graph b trains on
+        buffer b while a copy stream loads the next step's X / labels from the
+        pinned host buffers into buffer 1-b; the loss is read back each step.
+        Steady-state step time = max(H2D, epoch) instead of their sum.  Call
+        ``prime_e2e()`` once (loads buffer 0), then ``run_e2e_pipelined(k)``
+        for k = 0, 1, 2, ..."""
+        assert X_host.is_pinned() and labels_host.is_pinned() and loss_host.is_pinned()
+        assert X_host.shape[1] == self.Fpad, "host X must use the device row stride (Fpad)"
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self._Xstore_b = torch.empty(self.V, self.Fpad, **f32)
+        self.labels_b = torch.empty_like(self.labels)
+        X_b = self._Xstore_b[:, :self.F]
+        stores = [(self._Xstore, self.X, self.labels), (self._Xstore_b, X_b, self.labels_b)]
+        self._pipe_host = (X_host, labels_host, loss_host)
+        copy = torch.cuda.Stream(self.dev)
+        main = torch.cuda.Stream(self.dev)
+        graphs, keep = [], []
+        for b in (0, 1):
+            _, Xb, lab_b = stores[b]
+            nxt_store, _, nxt_lab = stores[1 - b]
+            k_g1 = GemmCall(Xb, self.W1, self.H1)
+            k_dw = GemmCall(Xb, self.dH1, self.dW1, trans_a=True)
+            k_hd = HeadCall(self.P2, self.W2, self.b2, lab_b, self.dP2, self.dW2, self.db2,
+                            self.loss, deg_offsets=self.g.d_offsets)
+            sched = [k_g1, self.k_agg1, self.k_agg2, k_hd, self.k_bagg2, self.k_norm1,
+                     self.k_bagg1, k_dw]
+            keep.append((k_g1, k_dw, k_hd))
+
+            def body(adam=True, sched=sched, nxt_store=nxt_store, nxt_lab=nxt_lab):
+                cur = torch.cuda.current_stream(self.dev)
+                copy.wait_stream(cur)  # buffer 1-b is free: the previous step finished
+                with torch.cuda.stream(copy):
+                    nxt_store.copy_(X_host, non_blocking=True)
+                    nxt_lab.copy_(labels_host, non_blocking=True)
+                for call in sched:
+                    call()
+                if adam:
+                    self.k_adam()
+                loss_host.copy_(self.loss, non_blocking=True)
+                cur.wait_stream(copy)
+
+            main.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(main):
+                body(adam=False)  # warm-up outside capture (no parameter update)
+            torch.cuda.current_stream(self.dev).wait_stream(main)
+            torch.cuda.synchronize(self.dev)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                body()
+            graphs.append(gr)
+        self._pipe = (graphs, keep, copy, main)
+        return graphs
+
+    def prime_e2e(self):
+        """Load buffer 0 from the pinned host inputs (stream-ordered)."""
+        X_host, labels_host, _ = self._pipe_host
+        self._Xstore.copy_(X_host, non_blocking=True)
+        self.labels.copy_(labels_host, non_blocking=True)
+
+    def run_e2e_pipelined(self, k: int):
+        self._pipe[0][k & 1].replay()
+
     def params(self):
         return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}
 

@@ -110,3 +110,27 @@ def test_e2e_graph_matches_device_resident_epoch(setup):
         assert la == loss_h.item()
     for k in a.params():
         assert torch.equal(a.params()[k], b.params()[k])
+
+
+def test_e2e_pipelined_matches_device_resident_epoch(setup):
+    """Double-buffered e2e graphs (next step's inputs loaded under this step's
+    compute) train exactly like the device-resident epoch."""
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    gb, g, _, X, y, (V, F, Hd, C) = setup
+    a = GCNTrainer(g, F, Hd, C, seed=0)
+    b = GCNTrainer(g, F, Hd, C, seed=0)
+    a.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+    Xp = torch.zeros(V, b.Fpad).pin_memory()
+    Xp[:, :F].copy_(torch.from_numpy(X))
+    yh = torch.from_numpy(y).pin_memory()
+    loss_h = torch.zeros(1).pin_memory()
+    b.capture_e2e_pipelined(Xp, yh, loss_h)
+    b.prime_e2e()
+    for k in range(4):
+        la = a.step().item()
+        b.run_e2e_pipelined(k)
+        torch.cuda.synchronize()
+        assert la == loss_h.item(), k
+    for k2 in a.params():
+        assert torch.equal(a.params()[k2], b.params()[k2])
