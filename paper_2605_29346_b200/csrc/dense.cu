@@ -127,12 +127,21 @@ GemmShape gemm_shape(int64_t M, int64_t N, int64_t Kd) {
   return g;
 }
 
-constexpr int kColsumRows = 4096;
+// Rows per CTA of the column-sum style reductions: enough CTAs to fill every
+// SM ~4 times (a fixed 2-4K-row block left a Reddit-size [V,64] pass on ~60-110
+// CTAs), at most 4096 rows so the partial buffer stays small.
+int64_t reduce_rows_per_block(int64_t M) {
+  const int64_t target = 4 * (int64_t)sm_count();
+  int64_t r = ceil_div(M > 0 ? M : 1, target);
+  r = ceil_div(r, 64) * 64;
+  return r < 64 ? 64 : (r > 4096 ? 4096 : r);
+}
+
 __global__ void colsum_partial_kernel(int64_t M, int64_t N, const float *__restrict__ X,
-                                      int64_t ldx, float *partials) {
-  // block b sums rows [b*kColsumRows, ...) for every column; threads stride columns
-  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
-  const int64_t r1 = min(M, r0 + kColsumRows);
+                                      int64_t ldx, float *partials, int64_t rpb) {
+  // block b sums rows [b*rpb, ...) for every column; threads stride columns
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = min(M, r0 + rpb);
   for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
     float s = 0.f;
     for (int64_t r = r0; r < r1; ++r) s += X[r * ldx + c];
@@ -143,14 +152,16 @@ __global__ void colsum_partial_kernel(int64_t M, int64_t N, const float *__restr
 template <int NCOL>
 __global__ void __launch_bounds__(256) colsum_narrow_kernel(int64_t M, int64_t N,
                                                             const float *__restrict__ X,
-                                                            int64_t ldx, float *partials) {
+                                                            int64_t ldx, float *partials,
+                                                            int64_t rpb) {
   constexpr int SLOTS = 256 / NCOL;
   __shared__ float red[SLOTS][NCOL];
   const int c = threadIdx.x % NCOL, s = threadIdx.x / NCOL;
-  const int64_t r0 = (int64_t)blockIdx.x * kColsumRows;
-  const int64_t r1 = min(M, r0 + kColsumRows);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = min(M, r0 + rpb);
   float acc = 0.f;
   if (c < N)
+#pragma unroll 4
     for (int64_t r = r0 + s; r < r1; r += SLOTS) acc += X[r * ldx + c];
   red[s][c] = acc;
   __syncthreads();
@@ -230,7 +241,7 @@ using namespace gnn;
 extern "C" {
 
 size_t gnn_colsum_workspace(int64_t M, int64_t N) {
-  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, kColsumRows) * (N > 0 ? N : 1)) + 256;
+  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, reduce_rows_per_block(M)) * (N > 0 ? N : 1)) + 256;
 }
 
 int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, void *ws,
@@ -244,14 +255,15 @@ int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, vo
     GNN_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * N, st));
     return GNN_OK;
   }
-  int64_t nb = ceil_div(M, kColsumRows);
+  const int64_t rpb = reduce_rows_per_block(M);
+  int64_t nb = ceil_div(M, rpb);
   float *partials = static_cast<float *>(ws);
   if (N <= 16)
-    colsum_narrow_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+    colsum_narrow_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials, rpb);
   else if (N <= 64)
-    colsum_narrow_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+    colsum_narrow_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials, rpb);
   else
-    colsum_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials);
+    colsum_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials, rpb);
   GNN_LAUNCH_CHECK();
   colsum_final_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, out);
   GNN_LAUNCH_CHECK();
@@ -297,7 +309,6 @@ int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int 
 namespace gnn {
 namespace {
 
-constexpr int kRowBlock = 2048;  // rows per CTA for the partial column sums
 
 __device__ __forceinline__ float inv_deg_of(const int64_t *off, int64_t r) {
   int64_t d = off[r + 1] - off[r];
@@ -310,16 +321,17 @@ template <int NCOL>
 __global__ void __launch_bounds__(256) mask_norm_colsum_kernel(
     int64_t M, int64_t N, const float *__restrict__ X, int64_t ldx, const float *__restrict__ mask,
     int64_t ldm, const int64_t *__restrict__ deg_offsets, float *out, int64_t ldo,
-    float *partials) {
+    float *partials, int64_t rpb) {
   constexpr int SLOTS = 256 / NCOL;
   __shared__ float red[SLOTS][NCOL];
   const int s = threadIdx.x / NCOL;
-  const int64_t r0 = (int64_t)blockIdx.x * kRowBlock;
-  const int64_t r1 = min(M, r0 + kRowBlock);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = min(M, r0 + rpb);
   for (int64_t c0 = 0; c0 < N; c0 += NCOL) {
     const int64_t c = c0 + threadIdx.x % NCOL;
     float acc = 0.f;
     if (c < N) {
+#pragma unroll 4
       for (int64_t r = r0 + s; r < r1; r += SLOTS) {
         float v = X[r * ldx + c];
         if (mask && !(mask[r * ldm + c] > 0.f)) v = 0.f;
@@ -440,7 +452,7 @@ __global__ void step_increment_kernel(int64_t *step) { *step += 1; }
 extern "C" {
 
 size_t gnn_mask_norm_colsum_workspace(int64_t M, int64_t N) {
-  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, kRowBlock) * (N > 0 ? N : 1)) + 256;
+  return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, reduce_rows_per_block(M)) * (N > 0 ? N : 1)) + 256;
 }
 
 int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
@@ -454,17 +466,18 @@ int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, cons
     if (colsum) GNN_CUDA_TRY(cudaMemsetAsync(colsum, 0, sizeof(float) * N, st));
     return GNN_OK;
   }
-  const int64_t nb = ceil_div(M, kRowBlock);
+  const int64_t rpb = reduce_rows_per_block(M);
+  const int64_t nb = ceil_div(M, rpb);
   float *partials = colsum ? static_cast<float *>(ws) : nullptr;
   if (N <= 16)
     mask_norm_colsum_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                             deg_offsets, out, ldo, partials);
+                                                             deg_offsets, out, ldo, partials, rpb);
   else if (N <= 64)
     mask_norm_colsum_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                             deg_offsets, out, ldo, partials);
+                                                             deg_offsets, out, ldo, partials, rpb);
   else
     mask_norm_colsum_kernel<256><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                              deg_offsets, out, ldo, partials);
+                                                              deg_offsets, out, ldo, partials, rpb);
   GNN_LAUNCH_CHECK();
   if (colsum) {
     sum_partials_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, colsum);

@@ -826,8 +826,21 @@ class GINTrainer(_FusedEpoch):
         k["Y1.W2a"] = GemmCall(self.Y1, self.W2a, self.H2)
         k["agg2"] = SpmmCall(A, self.H2, self.U2, flags=S | Bf | R, self_x=self.H2, self_scale=s1,
                              bias=self.b2a)
-        k["head"] = HeadCall(self.U2, self.W2b, self.b2b, self.labels, self.dU2, self.dW2b,
-                             self.db2b, self.loss)
+        if hidden <= 32:  # fused output layer: weights of <= 32 x C live in registers
+            k["head"] = HeadCall(self.U2, self.W2b, self.b2b, self.labels, self.dU2, self.dW2b,
+                                 self.db2b, self.loss)
+        else:  # wide hidden: the output layer as tensor-core GEMMs + one softmax-CE kernel
+            from .kernels import ColsumCall
+
+            Cp = -(-classes // 4) * 4
+            self.Z2 = torch.zeros(V, Cp, **f32)
+            self.dZ2 = torch.zeros(V, Cp, **f32)
+            Z2, dZ2 = self.Z2[:, :classes], self.dZ2[:, :classes]
+            k["head.Z"] = GemmCall(self.U2, self.W2b, Z2, bias=self.b2b)
+            k["head.xent"] = XentCall(Z2, self.labels, self.loss, dZ=dZ2)
+            k["head.dW"] = GemmCall(self.U2, dZ2, self.dW2b, trans_a=True)
+            k["head.db"] = ColsumCall(dZ2, self.db2b)
+            k["head.dP"] = GemmCall(dZ2, self.W2b, self.dU2, trans_b=True)
         k["relu_bwd_U2"] = MaskNormColsumCall(self.dU2, self.dU2, mask=self.U2, colsum=self.db2a)
         k["bagg2"] = SpmmCall(AT, self.dU2, self.dH2, flags=S, self_x=self.dU2, self_scale=s1)
         k["Y1^T.dH2"] = GemmCall(self.Y1, self.dH2, self.dW2a, trans_a=True)
