@@ -362,12 +362,73 @@ __global__ void sum_partials_kernel(int64_t nb, int64_t N, const float *__restri
 
 // One warp per row: numerically stable log-softmax cross-entropy; writes
 // dlogits = (softmax - onehot) * scale and a per-CTA partial of the loss.
+// Warp per row; the row's logits are loaded once into registers (NPL per
+// lane, C <= 32*NPL) and max, sum, loss and dZ are computed from them (one
+// memory round trip per row instead of three).
+template <int NPL>
 __global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t C,
                                                            const float *__restrict__ Z,
                                                            int64_t ldz,
                                                            const int64_t *__restrict__ labels,
                                                            float scale, float *dZ, int64_t ldd,
                                                            float *loss_partials) {
+  __shared__ float wl[8];
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  float lsum = 0.f;
+  const int64_t rows_per_cta = 8 * 16;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  for (int64_t r = r0 + warp; r < min(M, r0 + rows_per_cta); r += 8) {
+    const float *z = Z + r * ldz;
+    const int64_t y = __ldg(labels + r);
+    float v[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int64_t c = lane + 32 * j;
+      v[j] = c < C ? __ldg(z + c) : -INFINITY;
+    }
+    float mx = v[0];
+#pragma unroll
+    for (int j = 1; j < NPL; ++j) mx = fmaxf(mx, v[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    float se = 0.f, zy = 0.f;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int64_t c = lane + 32 * j;
+      if (c < C) se += expf(v[j] - mx);
+      if (c == y) zy = v[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      se += __shfl_xor_sync(kFull, se, o);
+      zy += __shfl_xor_sync(kFull, zy, o);
+    }
+    const float lse = mx + logf(se);
+    if (lane == 0) lsum += lse - zy;
+    if (dZ) {
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) {
+        const int64_t c = lane + 32 * j;
+        if (c < C) dZ[r * ldd + c] = (expf(v[j] - lse) - (c == y ? 1.f : 0.f)) * scale;
+      }
+    }
+  }
+  if (lane == 0) wl[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += wl[k];
+    loss_partials[blockIdx.x] = t;
+  }
+}
+
+// wide C (> 256): three passes over global memory
+__global__ void __launch_bounds__(256) softmax_xent_wide_kernel(int64_t M, int64_t C,
+                                                                const float *__restrict__ Z,
+                                                                int64_t ldz,
+                                                                const int64_t *__restrict__ labels,
+                                                                float scale, float *dZ, int64_t ldd,
+                                                                float *loss_partials) {
   __shared__ float wl[8];
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   float lsum = 0.f;
@@ -499,8 +560,21 @@ int gnn_softmax_xent(int64_t M, int64_t C, const float *Z, int64_t ldz, const in
   cudaStream_t st = as_stream(stream);
   const int64_t nb = ceil_div(M, 128);
   float *partials = static_cast<float *>(ws);
-  softmax_xent_kernel<<<(unsigned)nb, 256, 0, st>>>(M, C, Z, ldz, labels, grad_scale, dZ, ldd,
-                                                    partials);
+#define GNN_XENT(NPL)                                                                      \
+  softmax_xent_kernel<NPL><<<(unsigned)nb, 256, 0, st>>>(M, C, Z, ldz, labels, grad_scale, dZ, \
+                                                         ldd, partials)
+  if (C <= 32)
+    GNN_XENT(1);
+  else if (C <= 64)
+    GNN_XENT(2);
+  else if (C <= 128)
+    GNN_XENT(4);
+  else if (C <= 256)
+    GNN_XENT(8);
+  else
+    softmax_xent_wide_kernel<<<(unsigned)nb, 256, 0, st>>>(M, C, Z, ldz, labels, grad_scale, dZ,
+                                                           ldd, partials);
+#undef GNN_XENT
   GNN_LAUNCH_CHECK();
   loss_final_kernel<<<1, 256, 0, st>>>(nb, partials, 1.0f / (float)M, loss);
   GNN_LAUNCH_CHECK();
