@@ -518,7 +518,11 @@ def run_dist(args, rank, world):
     V, E, F, Hd, C = P["V"], P["E"], P["F"], P["H"], P["C"]
     g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=P["exponent"]), P["seed"],
                     device=dev)
-    part = RowPartition(g, world, rank, coalesced=True)
+    # exchange: NCCL all-gathers (default) or, with GNN_DIST_EXCHANGE=peer, the
+    # peer-memory form (gnn_spmm_peer reads every rank's block in place through
+    # torch symmetric memory; phase boundaries are device-side barriers)
+    mode = os.environ.get("GNN_DIST_EXCHANGE", "nccl")
+    part = RowPartition(g, world, rank, coalesced=True, pow2_stride=(mode == "peer"))
     g.drop_csc()
     rng = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(10,)))
     X_all = rng.random((V, F), dtype=np.float32) * 2 - 1
@@ -527,9 +531,16 @@ def run_dist(args, rank, world):
     y_h = torch.from_numpy(np.ascontiguousarray(y_all[part.lo:part.hi])).pin_memory()
     del X_all
     torch.cuda.reset_peak_memory_stats(dev)
-    tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"])
+    if mode == "peer":
+        from paper_2605_29346_b200.dist import PeerExchange
+
+        ex = PeerExchange()
+        tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"], peer=True, alloc=lambda r, w, d: ex.alloc(r, w, d))
+        tr.bind_peers(ex.peer_ptrs(tr))
+    else:
+        ex = TorchDistExchange()
+        tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"])
     tr.set_inputs(X_h, y_h)
-    ex = TorchDistExchange()
     c0 = lib.gnn_launch_counter()
     tr.step(ex)
     torch.cuda.synchronize()
@@ -571,7 +582,9 @@ def run_dist(args, rank, world):
         "data": "synthetic (device power-law generator, bit-exact gsbench.generate seed 42; "
                 "X~U[-1,1) f32, labels uniform)",
         "config": {"workload": "2-layer GCN full-graph epoch, Reddit-shape power-law graph, "
-                               "1D row partition (cost-balanced: deg + 170 per row) + NCCL all-gathers",
+                               "1D row partition (cost-balanced: deg + 170 per row) + "
+                               + ("peer-memory SpMM (symmetric memory, NVLink loads)"
+                                  if mode == "peer" else "NCCL all-gathers"),
                    "V": V, "E": E, "K": F, "hidden": Hd, "classes": C, "layout": "coalesced",
                    "optimizer": "adam", "parallelism": f"rowpart{world}",
                    "rows_rank0": part.rows, "bounds": [int(x) for x in part.bounds],

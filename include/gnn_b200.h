@@ -276,6 +276,18 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
              const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
              const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Row-partitioned multi-GPU form of gnn_spmm (fused with the
+ * exchange): instead of all-gathering the feature blocks first, the kernel
+ * reads every gathered row in place from the rank that owns it — column id c
+ * lives at row (c & (2^part_rows_log2 - 1)) of parts[c >> part_rows_log2],
+ * where parts[] are peer-mapped device pointers (NVLink / NVSwitch P2P loads,
+ * e.g. from torch symmetric memory) or local buffers.  heads = 1, K <= 64,
+ * fp32 rows 16-byte aligned; nparts <= 8. */
+int gnn_spmm_peer(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, const float *const *parts,
+                  int64_t nparts, int64_t part_rows_log2, int64_t ldx, float *Y, int64_t ldy,
+                  int64_t K, const gnn_epilogue_t *epi, void *ws, size_t ws_bytes,
+                  gnn_stream_t stream);
+
 /* X[v,:] /= deg(v) in place (deg 0 -> row zeroed). */
 int gnn_degree_norm_inplace(int64_t num_rows, const int64_t *offsets, float *X, int64_t ldx,
                             int64_t K, gnn_stream_t stream);

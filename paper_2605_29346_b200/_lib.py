@@ -181,6 +181,11 @@ SIGNATURES = {
             c_ptr,
         ],
     ),
+    "gnn_spmm_peer": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_i64,
+         C.POINTER(Epilogue), c_ptr, c_sz, c_ptr],
+    ),
     "gnn_degree_norm_inplace": (c_int, [c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_sddmm": (
         c_int,

@@ -26,6 +26,8 @@
 namespace gnn {
 namespace {
 
+constexpr int kMaxParts = 8;  // one NVLink / NVSwitch box
+
 struct SpmmArgs {
   int64_t R, nnz;
   const int64_t *offsets;
@@ -56,6 +58,11 @@ struct SpmmArgs {
   int bulk_ok;
   int warp_smem;             // bytes of shared memory per warp
   int64_t short_max;         // rows with 1 <= deg <= short_max: short-row kernel, skipped here
+  // peer mode (row-partitioned multi-GPU): column id c lives in part c >> pshift
+  // at row c & pmask of xt[part] — the owning rank's block, read in place over
+  // NVLink through peer-mapped pointers instead of an all-gathered copy
+  const float *xt[kMaxParts];
+  uint32_t pshift, pmask;
 };
 
 
@@ -140,9 +147,9 @@ enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
 
 // Lane-invariant part of the gather: per-vector base pointers (column offset
 // folded in; columns past K are clamped to column 0 and simply not stored).
-template <int G, int VPL, int VW>
+template <int G, int VPL, int VW, bool PEER = false>
 struct LaneCols {
-  const char *xb[VPL];
+  const char *xb[VPL];  // PEER: byte offset of the lane's column (no base)
   int head[VPL];
   __device__ __forceinline__ LaneCols(const SpmmArgs &a, int64_t cbase) {
     const int gl = (int)lane_id() % G;
@@ -150,7 +157,8 @@ struct LaneCols {
     for (int v = 0; v < VPL; ++v) {
       int64_t col = cbase + (int64_t)(v * G + gl) * VW;
       if (col >= a.K) col = 0;
-      xb[v] = reinterpret_cast<const char *>(a.X + col);
+      xb[v] = PEER ? reinterpret_cast<const char *>(col * 4)
+                   : reinterpret_cast<const char *>(a.X + col);
       head[v] = (int)(col / a.F);
     }
   }
@@ -160,14 +168,31 @@ template <int VW>
 __device__ __forceinline__ typename VecT<VW>::T gather(const char *xb, int32_t c, uint32_t ldxb) {
   return VecT<VW>::ld(reinterpret_cast<const float *>(xb + (uint64_t)(uint32_t)c * ldxb));
 }
+// peer mode: part base from the kernel-parameter pointer table
+template <int VW>
+__device__ __forceinline__ typename VecT<VW>::T gather_peer(const SpmmArgs &a, const char *colb,
+                                                            int32_t c, uint32_t ldxb) {
+  const uint32_t cu = (uint32_t)c;
+  const char *base = reinterpret_cast<const char *>(a.xt[cu >> a.pshift]);
+  return VecT<VW>::ld(reinterpret_cast<const float *>(
+      base + reinterpret_cast<uintptr_t>(colb) + (uint64_t)(cu & a.pmask) * ldxb));
+}
+template <int VW, bool PEER>
+__device__ __forceinline__ typename VecT<VW>::T gather_x(const SpmmArgs &a, const char *xb,
+                                                         int32_t c, uint32_t ldxb) {
+  if constexpr (PEER)
+    return gather_peer<VW>(a, xb, c, ldxb);
+  else
+    return gather<VW>(xb, c, ldxb);
+}
 
 // acc[v] += sum over this group's edges of w_e * X[c_e, cols of v] for the
 // buffer-local edge range [is, ie); group g takes is+g, is+g+NG, ...  Full
 // blocks of U edges per group run unpredicated; the remainder is one
 // predicated block, so a piece costs a single gather latency.  The order is
 // fixed by (G, U, piece bounds): deterministic.
-template <int G, int VPL, int VW, bool HAS_VALS>
-__device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols<G, VPL, VW> &lc,
+template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
+__device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols<G, VPL, VW, PEER> &lc,
                                                const int32_t *scol, const void *sval, int stage,
                                                int64_t ebase, int is, int ie,
                                                typename VecT<VW>::T (&acc)[VPL]) {
@@ -191,7 +216,7 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) x[u][v] = gather<VW>(lc.xb[v], c[u], ldxb);
+      for (int v = 0; v < VPL; ++v) x[u][v] = gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb);
     if constexpr (HAS_VALS) {
       float w[U][VPL];
 #pragma unroll
@@ -221,7 +246,7 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather<VW>(lc.xb[v], c[u], ldxb) : V::zero();
+      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb) : V::zero();
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -356,7 +381,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
 // range boundaries produce partials (split rows, finished by split_arrive).
 constexpr int kSub = 512;
 
-template <int G, int VPL, int VW, bool HAS_VALS>
+template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
 __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
@@ -411,7 +436,7 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
   int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
   int bi = 0;
   int64_t re = shfl_i64(obuf, 0);
-  const LaneCols<G, VPL, VW> lc(a, cbase);
+  const LaneCols<G, VPL, VW, PEER> lc(a, cbase);
   typename V::T acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
@@ -430,7 +455,7 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
       const int64_t lo = max(rs, s0), hi = min(re, s1);
       const bool is_short = re - rs <= a.short_max;  // owned by the short-row kernel
       if (hi > lo && !is_short)
-        seg_accumulate<G, VPL, VW, HAS_VALS>(a, lc, bc, bv, stage, s0, (int)(lo - s0),
+        seg_accumulate<G, VPL, VW, HAS_VALS, PEER>(a, lc, bc, bv, stage, s0, (int)(lo - s0),
                                              (int)(hi - s0), acc);
       if (re > s1) break;  // row continues in the next sub-chunk (or the next warp)
       if (re > rs && !is_short) {  // a row ends here
@@ -712,7 +737,7 @@ int launch_tma(const SpmmArgs &a, bool has_vals, const CUtensorMap &tm, cudaStre
 // parallel, U edges of each in flight, fused epilogue per group.  Indices and
 // edge values are read straight from global (a short row is one or two
 // sectors).  Summation order is fixed per row: deterministic.
-template <int G, int VPL, int VW, bool HAS_VALS>
+template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
 __global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                                               int64_t nrows) {
   using V = VecT<VW>;
@@ -726,7 +751,7 @@ __global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const 
   if (i >= nrows) return;  // group-uniform
   const int64_t r = rows[i];
   const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
-  const LaneCols<G, VPL, VW> lc(a, cbase);
+  const LaneCols<G, VPL, VW, PEER> lc(a, cbase);
   const uint32_t ldxb = (uint32_t)a.ldx * 4u;
   typename V::T acc[VPL];
 #pragma unroll
@@ -743,7 +768,7 @@ __global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const 
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather<VW>(lc.xb[v], c[u], ldxb) : V::zero();
+      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb) : V::zero();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if constexpr (HAS_VALS) {
@@ -837,14 +862,15 @@ unsigned grid_1d(int64_t n, int threads) {
   return (unsigned)(b < cap ? b : cap);
 }
 
-template <int G, int VPL, int VW>
+template <int G, int VPL, int VW, bool PEER = false>
 int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
   const size_t smem = (size_t)a.warp_smem * 8;
   // Shared memory only holds the staged index chunks; give the rest of the
   // unified L1/shared array to L1 so hot feature rows stay cached.
-  auto kern = has_vals ? spmm_main_kernel<G, VPL, VW, true> : spmm_main_kernel<G, VPL, VW, false>;
+  auto kern = has_vals ? spmm_main_kernel<G, VPL, VW, true, PEER>
+                       : spmm_main_kernel<G, VPL, VW, false, PEER>;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int per_sm_kb = (int)((smem * 3 + 1023) / 1024);  // 3 resident CTAs (persistent grid)
   const int carve = per_sm_kb * 100 / 228 + 1;
@@ -857,16 +883,18 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int G, int VPL, int VW>
+template <int G, int VPL, int VW, bool PEER = false>
 int launch_short(const SpmmArgs &a, bool has_vals, const gnn_spmm_plan_t *plan, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   constexpr int NG = 32 / G;
   const int64_t warps = ceil_div(plan->num_short, NG);
   dim3 grid((unsigned)ceil_div(warps * 32, 256), (unsigned)ceil_div(a.K, KB));
   if (has_vals)
-    spmm_short_rows_kernel<G, VPL, VW, true><<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
+    spmm_short_rows_kernel<G, VPL, VW, true, PEER><<<grid, 256, 0, st>>>(a, plan->short_rows,
+                                                                         plan->num_short);
   else
-    spmm_short_rows_kernel<G, VPL, VW, false><<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
+    spmm_short_rows_kernel<G, VPL, VW, false, PEER><<<grid, 256, 0, st>>>(a, plan->short_rows,
+                                                                          plan->num_short);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -1003,9 +1031,11 @@ size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, 
   return spmm_ws_layout(plan, K, &a, &b, &c);
 }
 
-int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
-             const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
-             const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                     const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
+                     const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream,
+                     const float *const *parts, int64_t nparts, int64_t part_log2) {
+  const bool peer = parts != nullptr;
   if (!A || !plan || !Y || K <= 0 || heads <= 0 || K % heads != 0 || ldy < K ||
       (A->nnz > 0 && (!X || ldx < K || !A->cols)) || !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
@@ -1039,6 +1069,11 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
   a.ldy = ldy;
   a.K = K;
   a.epi = e;
+  if (peer) {
+    for (int64_t q = 0; q < nparts; ++q) a.xt[q] = parts[q];
+    a.pshift = (uint32_t)part_log2;
+    a.pmask = (uint32_t)((1ull << part_log2) - 1);
+  }
   a.P = plan->edges_per_warp;
   a.nwarps = plan->num_warps;
   a.chunk_row = plan->chunk_row;
@@ -1078,7 +1113,7 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     int s;
     const bool tma_ok = vec4 && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
                         a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
-                        plan->short_max == 0 && getenv("GNN_SPMM_TMA") != nullptr;
+                        plan->short_max == 0 && !peer && getenv("GNN_SPMM_TMA") != nullptr;
     CUtensorMap tm;
     const int kb = K <= 16 ? 16 : K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
     if (tma_ok && make_gather_map(&tm, X, A->num_cols, K, ldx, kb)) {
@@ -1089,6 +1124,14 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
         case 128: s = launch_tma<128>(a, hv, tm, st); break;
         default: s = launch_tma<256>(a, hv, tm, st); break;
       }
+    } else if (peer) {
+      if (!vec4 || K > 64) return GNN_ERR_UNSUPPORTED;
+      if (K <= 16)
+        s = launch_main<4, 1, 4, true>(a, hv, st);
+      else if (K <= 32)
+        s = launch_main<8, 1, 4, true>(a, hv, st);
+      else
+        s = launch_main<16, 1, 4, true>(a, hv, st);
     } else if (vec4) {
       if (K <= 16)
         s = launch_main<4, 1, 4>(a, hv, st);
@@ -1116,7 +1159,14 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
     if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
     if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
-    if (vec4) {
+    if (peer) {
+      if (K <= 16)
+        GNN_TRY((launch_short<4, 1, 4, true>(a, hv, plan, st)));
+      else if (K <= 32)
+        GNN_TRY((launch_short<8, 1, 4, true>(a, hv, plan, st)));
+      else
+        GNN_TRY((launch_short<16, 1, 4, true>(a, hv, plan, st)));
+    } else if (vec4) {
       if (K <= 16)
         GNN_TRY((launch_short<4, 1, 4>(a, hv, plan, st)));
       else if (K <= 32)
@@ -1140,6 +1190,26 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
     GNN_LAUNCH_CHECK();
   }
   return GNN_OK;
+}
+
+int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+             const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
+             const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  return spmm_impl(A, plan, heads, X, ldx, Y, ldy, K, epi, ws, ws_bytes, stream, nullptr, 0, 0);
+}
+
+int gnn_spmm_peer(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, const float *const *parts,
+                  int64_t nparts, int64_t part_rows_log2, int64_t ldx, float *Y, int64_t ldy,
+                  int64_t K, const gnn_epilogue_t *epi, void *ws, size_t ws_bytes,
+                  gnn_stream_t stream) {
+  if (!parts || nparts <= 0 || nparts > kMaxParts || part_rows_log2 < 0 || part_rows_log2 > 30)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if ((nparts << part_rows_log2) > ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  for (int64_t q = 0; q < nparts; ++q)
+    if (!parts[q] || !aligned16(parts[q])) return GNN_ERR_INVALID_ARGUMENT;
+  if (A && A->num_cols > (nparts << part_rows_log2)) return GNN_ERR_INVALID_ARGUMENT;
+  return spmm_impl(A, plan, 1, parts[0], ldx, Y, ldy, K, epi, ws, ws_bytes, stream, parts, nparts,
+                   part_rows_log2);
 }
 
 __global__ void degree_norm_kernel(int64_t R, const int64_t *__restrict__ off, float *X,

@@ -99,6 +99,56 @@ class TorchDistExchange:
         self.dist.all_reduce(t, group=self.group)
 
 
+class PeerExchange:
+    """Peer-memory form of the exchange (one process per GPU): every rank's
+    exchanged blocks live in torch symmetric memory, mapped into every peer
+    over NVLink / NVSwitch; the aggregation kernels (gnn_spmm_peer) read the
+    rows they need straight from the owner, so a phase boundary is only a
+    device-side barrier — no all-gather copy.  Gradients still use one NCCL
+    all-reduce.
+
+    Opt-in (bench: GNN_DIST_EXCHANGE=peer), not the default: an aggregation
+    re-reads every source row ~deg times, so in-place remote gathers move
+    nnz*K*4 bytes over NVLink (Reddit, K=16: 4.4 GB, ~5 ms at 900 GB/s) where
+    the all-gather moves each remote row once (V*K*4 = 15 MB) and the gathers
+    then hit local L2/HBM.  Peer loads pay off for single-use operands (GEMM
+    tiles), not for SpMM's high-reuse gathers."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.dist, self.symm, self.group = dist, symm, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.group_name = (group or dist.group.WORLD).group_name
+        if hasattr(symm, "enable_symm_mem_for_group"):
+            symm.enable_symm_mem_for_group(self.group_name)
+        self.handles = []
+        self.ptrs = {}
+
+    def alloc(self, rows: int, width: int, device) -> torch.Tensor:
+        """A [rows, width] fp32 block in symmetric memory (collective: every
+        rank allocates its blocks in the same order); its peers' pointers are
+        recorded under ptrs[id(tensor)]."""
+        t = self.symm.empty(rows, width, dtype=torch.float32, device=device)
+        t.zero_()
+        h = self.symm.rendezvous(t, self.group_name)
+        self.handles.append(h)
+        self.ptrs[t.data_ptr()] = [int(p) for p in h.buffer_ptrs]
+        return t
+
+    def peer_ptrs(self, trainer) -> dict:
+        return {n: self.ptrs[b.data_ptr()] for n, b in trainer.blocks().items()}
+
+    def barrier(self):
+        # device-side barrier over the group, stream-ordered (no host sync)
+        self.handles[0].barrier(channel=0, timeout_ms=60_000)
+
+    def all_reduce(self, t: torch.Tensor):
+        self.dist.all_reduce(t, group=self.group)
+
+
 class LocalExchange:
     """P virtual ranks in one process (one GPU): the exchanges copy slots
     between the ranks' buffers.  Used to test the partitioned schedule."""
@@ -125,12 +175,15 @@ class RowPartition:
     """Rank ``rank``'s share of graph ``g`` (global CSR/CSC on this device)."""
 
     def __init__(self, g: CsrGraph, parts: int, rank: int, *, coalesced: bool = True,
-                 bounds: np.ndarray | None = None):
+                 bounds: np.ndarray | None = None, pow2_stride: bool = False):
         self.g, self.parts, self.rank = g, parts, rank
         dev = g.device
         self.bounds = (partition_bounds(g.offsets, parts, ROW_COST) if bounds is None
                        else np.asarray(bounds))
         self.stride = block_stride(self.bounds)
+        if pow2_stride:  # peer mode: owner = id >> log2(stride), row = id & (stride - 1)
+            self.stride = 1 << max(0, (self.stride - 1).bit_length())
+        self.stride_log2 = self.stride.bit_length() - 1 if pow2_stride else None
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
         self.rows = self.hi - self.lo
         self.d_bounds = torch.from_numpy(self.bounds.astype(np.int64)).to(dev)
@@ -181,10 +234,15 @@ class DistGCNTrainer:
     """
 
     def __init__(self, part: RowPartition, in_feats: int, hidden: int, classes: int, *,
-                 lr=0.01, seed: int = 0):
+                 lr=0.01, seed: int = 0, peer: bool = False, alloc=None):
+        """``peer``: exchanged blocks are read in place by gnn_spmm_peer (see
+        PeerExchange / bind_peers) instead of being all-gathered; ``alloc``
+        (rows, width, device) -> tensor provides the block storage (torch
+        symmetric memory for real ranks, plain tensors for virtual ones)."""
         from .kernels import HeadCall
 
         self.part = part
+        self.peer = peer
         g = part.g
         dev = g.device
         self.dev = dev
@@ -207,9 +265,17 @@ class DistGCNTrainer:
         self._Xstore = torch.zeros(max(n, 1), self.Fpad, **f32)
         self.X = self._Xstore[:n, :in_feats]
         self.labels = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)[:n]
-        full = lambda: torch.zeros(P * S, hidden, **f32)  # noqa: E731
-        self.H1f, self.Y1f, self.dP2f, self.dZ1f = full(), full(), full(), full()
-        sl = slice(part.rank * S, part.rank * S + n)
+        if peer:
+            if part.stride_log2 is None:
+                raise ValueError("peer mode needs RowPartition(..., pow2_stride=True)")
+            mk = alloc or (lambda r, w, d: torch.zeros(r, w, dtype=torch.float32, device=d))
+            # local blocks only; peers' blocks are read in place
+            self.H1f, self.Y1f, self.dP2f, self.dZ1f = (mk(S, hidden, dev) for _ in range(4))
+            sl = slice(0, n)
+        else:
+            full = lambda: torch.zeros(P * S, hidden, **f32)  # noqa: E731
+            self.H1f, self.Y1f, self.dP2f, self.dZ1f = full(), full(), full(), full()
+            sl = slice(part.rank * S, part.rank * S + n)
         self.H1, self.Y1 = self.H1f[sl], self.Y1f[sl]
         self.dP2, self.dZ1n = self.dP2f[sl], self.dZ1f[sl]
         e = lambda: torch.empty(max(n, 1), hidden, **f32)[:n]  # noqa: E731
@@ -218,16 +284,25 @@ class DistGCNTrainer:
         N_, B_, R_, M_ = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
         deg = part.deg_offsets
         self.phases = []
+        self._lazy = {}  # peer mode: aggregation calls built by bind_peers()
         if n > 0:
             k_gemm1 = GemmCall(self.X, self.W1, self.H1)
-            k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
-            k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
+            if peer:
+                k_agg1 = self._deferred("agg1")
+                k_agg2 = self._deferred("agg2")
+            else:
+                k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
+                k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
             k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
                               self.db2, self.loss, deg_offsets=deg)
             k_head.scale = 1.0 / V
-            k_bagg2 = SpmmCall(AT, self.dP2f, self.dZ1, flags=M_, mask=self.Y1)
+            if peer:
+                k_bagg2 = self._deferred("bagg2")
+                k_bagg1 = self._deferred("bagg1")
+            else:
+                k_bagg2 = SpmmCall(AT, self.dP2f, self.dZ1, flags=M_, mask=self.Y1)
+                k_bagg1 = SpmmCall(AT, self.dZ1f, self.dH1)
             k_norm1 = MaskNormColsumCall(self.dZ1, self.dZ1n, deg_offsets=deg, colsum=self.db1)
-            k_bagg1 = SpmmCall(AT, self.dZ1f, self.dH1)
             k_dW1 = GemmCall(self.X, self.dH1, self.dW1, trans_a=True)
             zero = lambda: None  # noqa: E731
         else:  # a rank without rows still takes part in every exchange
@@ -246,6 +321,34 @@ class DistGCNTrainer:
         self.k_adam = AdamCall([self.W1, self.b1, self.W2, self.b2],
                                [self.dW1, self.db1, self.dW2, self.db2], lr=lr)
 
+    def _deferred(self, name):
+        def call():
+            self._lazy[name]()
+        return call
+
+    def blocks(self) -> dict:
+        """The exchanged blocks of this rank (peer mode: what peers read)."""
+        return {"H1": self.H1f, "Y1": self.Y1f, "dP2": self.dP2f, "dZ1": self.dZ1f}
+
+    def bind_peers(self, ptrs: dict) -> None:
+        """Peer mode: ``ptrs[name][q]`` = device pointer of rank q's block
+        ``name`` (peer-mapped for real ranks); builds the gnn_spmm_peer calls."""
+        from .kernels import PeerSpmmCall
+
+        if self.part.rows == 0:
+            return
+        part, hd = self.part, self.Hd
+        lg, ld = part.stride_log2, hd
+        N_, B_, R_, M_ = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        self._lazy = {
+            "agg1": PeerSpmmCall(part.A, ptrs["H1"], lg, ld, hd, self.Y1, flags=N_ | B_ | R_,
+                                 bias=self.b1),
+            "agg2": PeerSpmmCall(part.A, ptrs["Y1"], lg, ld, hd, self.P2, flags=N_),
+            "bagg2": PeerSpmmCall(part.AT, ptrs["dP2"], lg, ld, hd, self.dZ1, flags=M_,
+                                  mask=self.Y1),
+            "bagg1": PeerSpmmCall(part.AT, ptrs["dZ1"], lg, ld, hd, self.dH1),
+        }
+
     def _run_head(self):
         h = self._head
         _lib.check(h.lib.gnn_gcn_head_scaled(
@@ -258,13 +361,16 @@ class DistGCNTrainer:
         _lib.copy_rows(self.X, X_local)
         self.labels.copy_(labels_local, non_blocking=non_blocking)
 
-    def step(self, ex: TorchDistExchange):
+    def step(self, ex):
         S = self.part.stride
         for _, calls, (kind, buf) in self.phases:
             for _, c in calls:
                 c()
             if kind == "gather":
-                ex.all_gather(buf, S)
+                if self.peer:
+                    ex.barrier()  # the block is complete on every rank; peers read it in place
+                else:
+                    ex.all_gather(buf, S)
             else:
                 ex.all_reduce(buf)
         self.k_adam()
@@ -277,8 +383,20 @@ class DistGCNTrainer:
         return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
 
 
+def bind_virtual_peers(trainers) -> None:
+    """Peer mode with P virtual ranks on one GPU: every rank reads the other
+    ranks' blocks directly (same device), exactly as real ranks read peer-
+    mapped NVLink memory."""
+    names = ("H1", "Y1", "dP2", "dZ1")
+    ptrs = {n: [t.blocks()[n].data_ptr() for t in trainers] for n in names}
+    for t in trainers:
+        t.bind_peers(ptrs)
+
+
 def step_virtual(trainers, ex: LocalExchange, adam: bool = True):
-    """One epoch of P virtual ranks (``trainers[p]`` = rank p) in lockstep."""
+    """One epoch of P virtual ranks (``trainers[p]`` = rank p) in lockstep.
+    Peer-mode trainers need no exchange: phase order on the one stream is the
+    barrier."""
     S = trainers[0].part.stride
     for i in range(len(trainers[0].phases)):
         for t in trainers:
@@ -287,7 +405,8 @@ def step_virtual(trainers, ex: LocalExchange, adam: bool = True):
         kind = trainers[0].phases[i][2][0]
         bufs = [t.phases[i][2][1] for t in trainers]
         if kind == "gather":
-            ex.all_gather_many(bufs, S)
+            if not trainers[0].peer:
+                ex.all_gather_many(bufs, S)
         else:
             ex.all_reduce_many(bufs)
     if adam:

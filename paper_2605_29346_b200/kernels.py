@@ -349,3 +349,34 @@ class GatBwdCscMeanCall:
             dZ.stride(0), self.scale, Wh.data_ptr(), Wh.stride(0), self.F, dWh.data_ptr(),
             dWh.stride(0), dalpha.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
             _lib.stream_handle(self.dev)), "gat_bwd_csc_mean")
+
+
+class PeerSpmmCall:
+    """gnn_spmm_peer: Y = epilogue(op . X) where X is row-partitioned across
+    ``parts`` (device pointers, one per rank; rows of part q are the global
+    columns [q << log2, (q+1) << log2)) and every gathered row is read in place
+    from its owner — peer-mapped NVLink memory on a multi-GPU box."""
+
+    def __init__(self, op: SparseOperand, part_ptrs, part_rows_log2: int, ldx: int, K: int,
+                 Y: torch.Tensor, *, flags=0, bias=None, mask=None, keep=()):
+        self.lib = _lib.lib()
+        self.dev = Y.device
+        self.view = op.view()
+        self.plan = op.spmm_plan()
+        self.parts = (C.c_void_p * len(part_ptrs))(*[int(p) for p in part_ptrs])
+        self.nparts, self.log2, self.ldx, self.K, self.Y = len(part_ptrs), part_rows_log2, ldx, K, Y
+        self.epi = _lib.Epilogue()
+        self.epi.flags = flags
+        if bias is not None:
+            self.epi.bias = bias.data_ptr()
+        if mask is not None:
+            self.epi.mask, self.epi.ld_mask = mask.data_ptr(), mask.stride(0)
+        self._keep = (op, bias, mask, keep)
+        self.ws = _lib.workspace(self.lib.gnn_spmm_workspace(C.byref(self.view), C.byref(self.plan),
+                                                             K), self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_spmm_peer(
+            C.byref(self.view), C.byref(self.plan), self.parts, self.nparts, self.log2, self.ldx,
+            self.Y.data_ptr(), self.Y.stride(0), self.K, C.byref(self.epi), self.ws.data_ptr(),
+            self.ws.numel(), _lib.stream_handle(self.dev)), "spmm_peer")

@@ -79,3 +79,36 @@ def test_remap_kernel_matches_host(env):
             off, tgt = g.offsets, g.targets
             ref = remap_ids_host(tgt[off[part.lo]:off[part.hi]], part.bounds, part.stride)
             assert np.array_equal(part.A.cols.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_peer_mode_virtual_ranks_match_oracle(env, P):
+    """Peer mode (gnn_spmm_peer reads every rank's block in place, no
+    all-gather) with P virtual ranks on one GPU: same gradients as the
+    single-process oracle and bit-identical to the all-gather mode."""
+    from paper_2605_29346_b200.dist import (DistGCNTrainer, LocalExchange, RowPartition,
+                                            bind_virtual_peers, step_virtual)
+
+    gb, g, X, y = env
+    V = g.num_vertices
+    parts = [RowPartition(g, P, r, pow2_stride=True) for r in range(P)]
+    trs = [DistGCNTrainer(p, 64, 16, 7, seed=0, peer=True) for p in parts]
+    bind_virtual_peers(trs)
+    gparts = [RowPartition(g, P, r) for r in range(P)]
+    gtrs = [DistGCNTrainer(p, 64, 16, 7, seed=0) for p in gparts]
+    for p, t, gt in zip(parts, trs, gtrs):
+        t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
+        gt.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
+    step_virtual(trs, LocalExchange(P), adam=False)
+    step_virtual(gtrs, LocalExchange(P), adam=False)
+    torch.cuda.synchronize()
+    off, tgt = g.offsets, g.targets
+    t_off, t_rows, _ = og.transpose(V, V, off, tgt)
+    pr = {k: v.double().cpu().numpy() for k, v in trs[0].params().items()}
+    ref = oo.gcn2_step(off, tgt, t_off, t_rows, X, pr["W1"], pr["b1"], pr["W2"], pr["b2"], y)
+    for t, gt in zip(trs, gtrs):
+        assert abs(t.loss.item() - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+        for k, gv in t.grads().items():
+            ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
+            assert ok, (P, k, worst)
+            assert torch.equal(gv, gt.grads()[k]), k  # same kernels, same summation order
