@@ -539,7 +539,13 @@ def run_dist(args, rank, world):
         tr.bind_peers(ex.peer_ptrs(tr))
     else:
         ex = TorchDistExchange()
-        tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"])
+        # overlap the all-gathers with the own-slot part of each aggregation
+        # (GNN_DIST_OVERLAP=0 turns it off; no use with a single rank)
+        overlap = world > 1 and os.environ.get("GNN_DIST_OVERLAP", "1") != "0"
+        tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"], overlap=overlap)
+        if overlap:  # the trainer holds the own-slot / other-slot parts; drop the unsplit slices
+            part.A = part.AT = None
+            torch.cuda.empty_cache()
     tr.set_inputs(X_h, y_h)
     c0 = lib.gnn_launch_counter()
     tr.step(ex)
@@ -584,7 +590,9 @@ def run_dist(args, rank, world):
         "config": {"workload": "2-layer GCN full-graph epoch, Reddit-shape power-law graph, "
                                "1D row partition (cost-balanced: deg + 170 per row) + "
                                + ("peer-memory SpMM (symmetric memory, NVLink loads)"
-                                  if mode == "peer" else "NCCL all-gathers"),
+                                  if mode == "peer" else "NCCL all-gathers"
+                                  + (" overlapped with own-slot aggregation"
+                                     if mode != "peer" and tr.overlap else "")),
                    "V": V, "E": E, "K": F, "hidden": Hd, "classes": C, "layout": "coalesced",
                    "optimizer": "adam", "parallelism": f"rowpart{world}",
                    "rows_rank0": part.rows, "bounds": [int(x) for x in part.bounds],

@@ -86,17 +86,24 @@ class TorchDistExchange:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def all_gather(self, full: torch.Tensor, stride_rows: int):
+    def all_gather(self, full: torch.Tensor, stride_rows: int, async_op: bool = False):
         d = self.dist
         mine = full[self.rank * stride_rows:(self.rank + 1) * stride_rows]
         if d.get_backend(self.group) == "nccl":
-            d.all_gather_into_tensor(full, mine, group=self.group)
-        else:
-            parts = list(full.split(stride_rows))
-            d.all_gather(parts, mine.clone(), group=self.group)
+            return d.all_gather_into_tensor(full, mine, group=self.group, async_op=async_op)
+        parts = list(full.split(stride_rows))
+        return d.all_gather(parts, mine.clone(), group=self.group, async_op=async_op)
 
     def all_reduce(self, t: torch.Tensor):
         self.dist.all_reduce(t, group=self.group)
+
+    def all_gather_start(self, full: torch.Tensor, stride_rows: int):
+        """Launch the in-place all-gather (NCCL's own stream, ordered after the
+        producer kernels) and return its work handle."""
+        return self.all_gather(full, stride_rows, async_op=True)
+
+    def all_gather_wait(self, handle):
+        handle.wait()  # NCCL: the current stream waits on the collective, no host sync
 
 
 class PeerExchange:
@@ -213,6 +220,28 @@ class RowPartition:
         return SparseOperand(self.rows, cols_total, loc_off, out, vals=vals,
                              deg_offsets=deg if deg is not None else None)
 
+    def split_local_remote(self, op: SparseOperand):
+        """(local, remote) parts of a sliced operand: entries whose column is
+        in this rank's own slot vs the others (order within a row kept).  The
+        local part can aggregate while the all-gather of the other slots is
+        still in flight (SURVEY §8e pipelining)."""
+        dev = op.offsets.device
+        R = op.num_rows
+        lo, hi = self.rank * self.stride, (self.rank + 1) * self.stride
+        deg = (op.offsets[1:] - op.offsets[:-1])
+        rows = torch.repeat_interleave(torch.arange(R, device=dev), deg)
+        is_loc = (op.cols >= lo) & (op.cols < hi)
+        out = []
+        for sel in (is_loc, ~is_loc):
+            idx = torch.nonzero(sel).squeeze(1)  # keeps row-major, in-row order
+            cnt = torch.bincount(rows[idx], minlength=R)
+            off = torch.zeros(R + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(cnt, 0, out=off[1:])
+            vals = op.vals[idx].contiguous() if op.vals is not None else None
+            out.append(SparseOperand(R, op.num_cols, off, op.cols[idx].contiguous(), vals=vals,
+                                     deg_offsets=op.deg_offsets))
+        return out[0], out[1]
+
     def local_rows(self, t: torch.Tensor) -> torch.Tensor:
         return t[self.lo:self.hi]
 
@@ -234,15 +263,27 @@ class DistGCNTrainer:
     """
 
     def __init__(self, part: RowPartition, in_feats: int, hidden: int, classes: int, *,
-                 lr=0.01, seed: int = 0, peer: bool = False, alloc=None):
+                 lr=0.01, seed: int = 0, peer: bool = False, alloc=None,
+                 overlap: bool = False):
         """``peer``: exchanged blocks are read in place by gnn_spmm_peer (see
         PeerExchange / bind_peers) instead of being all-gathered; ``alloc``
         (rows, width, device) -> tensor provides the block storage (torch
-        symmetric memory for real ranks, plain tensors for virtual ones)."""
+        symmetric memory for real ranks, plain tensors for virtual ones).
+
+        ``overlap`` (all-gather mode): every aggregation is split by source
+        owner — the entries whose column is this rank's own slot aggregate
+        while the all-gather of the other slots is in flight (on a comm
+        stream), then the remote entries finish the row with the local partial
+        as the SELF term (NORM distributes: acc_loc/d + acc_rem/d).  Same
+        math, different fp32 summation order (tolerance, not bit-exact, vs
+        the unsplit schedule)."""
         from .kernels import HeadCall
 
         self.part = part
         self.peer = peer
+        if overlap and peer:
+            raise ValueError("overlap applies to the all-gather exchange, not peer mode")
+        self.overlap = overlap
         g = part.g
         dev = g.device
         self.dev = dev
@@ -285,12 +326,31 @@ class DistGCNTrainer:
         deg = part.deg_offsets
         self.phases = []
         self._lazy = {}  # peer mode: aggregation calls built by bind_peers()
+        # overlap: pre[name] runs before the pending all-gather is waited on
+        pre = {k: [] for k in ("agg1", "agg2", "bagg2", "bagg1")}
+        if n > 0 and overlap:
+            S_ = _lib.EPI_SELF
+            self.tmp = e()
+            A_l, A_r = part.split_local_remote(A)
+            AT_l, AT_r = part.split_local_remote(AT)
+            self.split_nnz = {"A": (A_l.nnz, A_r.nnz), "AT": (AT_l.nnz, AT_r.nnz)}
+            t = self.tmp
+            pre["agg1"] = [("agg1.local", SpmmCall(A_l, self.H1f, t, flags=N_))]
+            k_agg1 = SpmmCall(A_r, self.H1f, self.Y1, flags=N_ | S_ | B_ | R_, bias=self.b1,
+                              self_x=t)
+            pre["agg2"] = [("agg2.local", SpmmCall(A_l, self.Y1f, t, flags=N_))]
+            k_agg2 = SpmmCall(A_r, self.Y1f, self.P2, flags=N_ | S_, self_x=t)
+            pre["bagg2"] = [("bagg2.local", SpmmCall(AT_l, self.dP2f, t))]
+            k_bagg2_ov = SpmmCall(AT_r, self.dP2f, self.dZ1, flags=S_ | M_, self_x=t,
+                                  mask=self.Y1)
+            pre["bagg1"] = [("bagg1.local", SpmmCall(AT_l, self.dZ1f, t))]
+            k_bagg1_ov = SpmmCall(AT_r, self.dZ1f, self.dH1, flags=S_, self_x=t)
         if n > 0:
             k_gemm1 = GemmCall(self.X, self.W1, self.H1)
             if peer:
                 k_agg1 = self._deferred("agg1")
                 k_agg2 = self._deferred("agg2")
-            else:
+            elif not overlap:
                 k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
                 k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
             k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
@@ -299,6 +359,8 @@ class DistGCNTrainer:
             if peer:
                 k_bagg2 = self._deferred("bagg2")
                 k_bagg1 = self._deferred("bagg1")
+            elif overlap:
+                k_bagg2, k_bagg1 = k_bagg2_ov, k_bagg1_ov
             else:
                 k_bagg2 = SpmmCall(AT, self.dP2f, self.dZ1, flags=M_, mask=self.Y1)
                 k_bagg1 = SpmmCall(AT, self.dZ1f, self.dH1)
@@ -310,13 +372,15 @@ class DistGCNTrainer:
             k_head = None
             zero = self.flat.zero_
         self._head = k_head
+        # (name, calls before the previous exchange is waited on, calls after, exchange)
         self.phases = [
-            ("A", [("X.W1", k_gemm1)], ("gather", self.H1f)),
-            ("B", [("agg1", k_agg1)], ("gather", self.Y1f)),
-            ("C", [("agg2", k_agg2), ("head", self._run_head if n > 0 else zero)],
+            ("A", [], [("X.W1", k_gemm1)], ("gather", self.H1f)),
+            ("B", pre["agg1"], [("agg1", k_agg1)], ("gather", self.Y1f)),
+            ("C", pre["agg2"], [("agg2", k_agg2), ("head", self._run_head if n > 0 else zero)],
              ("gather", self.dP2f)),
-            ("D", [("bagg2", k_bagg2), ("mask_norm_db1", k_norm1)], ("gather", self.dZ1f)),
-            ("E", [("bagg1", k_bagg1), ("X^T.dH1", k_dW1)], ("reduce", self.flat)),
+            ("D", pre["bagg2"], [("bagg2", k_bagg2), ("mask_norm_db1", k_norm1)],
+             ("gather", self.dZ1f)),
+            ("E", pre["bagg1"], [("bagg1", k_bagg1), ("X^T.dH1", k_dW1)], ("reduce", self.flat)),
         ]
         self.k_adam = AdamCall([self.W1, self.b1, self.W2, self.b2],
                                [self.dW1, self.db1, self.dW2, self.db2], lr=lr)
@@ -363,12 +427,20 @@ class DistGCNTrainer:
 
     def step(self, ex):
         S = self.part.stride
-        for _, calls, (kind, buf) in self.phases:
+        pending = None
+        for _, pre, calls, (kind, buf) in self.phases:
+            for _, c in pre:  # own-slot aggregation, overlapping the all-gather
+                c()
+            if pending is not None:
+                ex.all_gather_wait(pending)
+                pending = None
             for _, c in calls:
                 c()
             if kind == "gather":
                 if self.peer:
                     ex.barrier()  # the block is complete on every rank; peers read it in place
+                elif self.overlap:
+                    pending = ex.all_gather_start(buf, S)
                 else:
                     ex.all_gather(buf, S)
             else:
@@ -398,13 +470,22 @@ def step_virtual(trainers, ex: LocalExchange, adam: bool = True):
     Peer-mode trainers need no exchange: phase order on the one stream is the
     barrier."""
     S = trainers[0].part.stride
+    pending = None
     for i in range(len(trainers[0].phases)):
-        for t in trainers:
+        for t in trainers:  # overlap: own-slot parts run before the slots land
             for _, c in t.phases[i][1]:
                 c()
-        kind = trainers[0].phases[i][2][0]
-        bufs = [t.phases[i][2][1] for t in trainers]
-        if kind == "gather":
+        if pending is not None:
+            ex.all_gather_many(pending, S)
+            pending = None
+        for t in trainers:
+            for _, c in t.phases[i][2]:
+                c()
+        kind = trainers[0].phases[i][3][0]
+        bufs = [t.phases[i][3][1] for t in trainers]
+        if kind == "gather" and trainers[0].overlap:
+            pending = bufs
+        elif kind == "gather":
             if not trainers[0].peer:
                 ex.all_gather_many(bufs, S)
         else:

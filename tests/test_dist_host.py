@@ -63,7 +63,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -93,13 +93,31 @@ def _worker(rank, world, port, q):
 
         H1f, Y1f, dP2f, dZ1f = full(), full(), full(), full()
         sl = slice(rank * S, rank * S + (hi - lo))
+
+        def exchange_agg(o, c, buf, norm=False, deg_off=None):
+            """All-gather buf, then aggregate.  overlap: the own-slot entries
+            aggregate before the async all-gather is waited on (the
+            DistGCNTrainer(overlap=True) schedule), remote entries after."""
+            if not overlap:
+                ex.all_gather(buf, S)
+                return oo.spmm(o, c, buf.numpy(), norm=norm)
+            h = ex.all_gather_start(buf, S)
+            own = (c >= rank * S) & (c < (rank + 1) * S)
+            rows = np.repeat(np.arange(o.size - 1), np.diff(o))
+            parts = []
+            for sel in (own, ~own):
+                oo_ = np.concatenate([[0], np.cumsum(np.bincount(rows[sel], minlength=o.size - 1))])
+                parts.append((oo_, c[sel]))
+            acc = oo.spmm(parts[0][0], parts[0][1], buf.numpy().copy())  # own slot only
+            ex.all_gather_wait(h)
+            acc = acc + oo.spmm(parts[1][0], parts[1][1], buf.numpy())
+            return acc * inv if norm else acc
+
         H1f[sl] = torch.from_numpy(X[lo:hi] @ W1)
-        ex.all_gather(H1f, S)
-        Z1 = oo.spmm(loff, lcols, H1f.numpy(), norm=True) + b1
+        Z1 = exchange_agg(loff, lcols, H1f, norm=True) + b1
         Y1 = np.maximum(Z1, 0)
         Y1f[sl] = torch.from_numpy(Y1)
-        ex.all_gather(Y1f, S)
-        P2 = oo.spmm(loff, lcols, Y1f.numpy(), norm=True)
+        P2 = exchange_agg(loff, lcols, Y1f, norm=True)
         Z2 = P2 @ W2 + b2
         # mean over the GLOBAL vertex count (gnn_gcn_head_scaled with 1/V)
         z = Z2 - Z2.max(1, keepdims=True)
@@ -111,12 +129,10 @@ def _worker(rank, world, port, q):
         dW2 = P2.T @ dZ2
         db2 = dZ2.sum(0)
         dP2f[sl] = torch.from_numpy((dZ2 @ W2.T) * inv)
-        ex.all_gather(dP2f, S)
-        dZ1 = oo.spmm(ltoff, lrows, dP2f.numpy()) * (Y1 > 0)
+        dZ1 = exchange_agg(ltoff, lrows, dP2f) * (Y1 > 0)
         db1 = dZ1.sum(0)
         dZ1f[sl] = torch.from_numpy(dZ1 * inv)
-        ex.all_gather(dZ1f, S)
-        dH1 = oo.spmm(ltoff, lrows, dZ1f.numpy())
+        dH1 = exchange_agg(ltoff, lrows, dZ1f)
         dW1 = X[lo:hi].T @ dH1
         flat = torch.from_numpy(np.concatenate([dW1.ravel(), db1, dW2.ravel(), db2, [loss]]))
         ex.all_reduce(flat)
@@ -129,12 +145,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_partitioned_gcn_exchange_matches_single_process(world):
+@pytest.mark.parametrize("world,overlap", [(2, False), (2, True), (3, True)])
+def test_partitioned_gcn_exchange_matches_single_process(world, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     err = q.get(timeout=120)

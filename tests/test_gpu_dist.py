@@ -25,14 +25,15 @@ def env(cuda):
 
 
 @pytest.mark.parametrize("P", [1, 2, 3, 5])
-@pytest.mark.parametrize("coalesced", [False, True])
-def test_virtual_ranks_match_oracle(env, P, coalesced):
+@pytest.mark.parametrize("coalesced,overlap", [(False, False), (True, False), (True, True),
+                                               (False, True)])
+def test_virtual_ranks_match_oracle(env, P, coalesced, overlap):
     from paper_2605_29346_b200.dist import DistGCNTrainer, LocalExchange, RowPartition, step_virtual
 
     gb, g, X, y = env
     V = g.num_vertices
     parts = [RowPartition(g, P, r, coalesced=coalesced) for r in range(P)]
-    trs = [DistGCNTrainer(p, 64, 16, 7, seed=0) for p in parts]
+    trs = [DistGCNTrainer(p, 64, 16, 7, seed=0, overlap=overlap) for p in parts]
     for p, t in zip(parts, trs):
         t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
     step_virtual(trs, LocalExchange(P), adam=False)
@@ -112,3 +113,29 @@ def test_peer_mode_virtual_ranks_match_oracle(env, P):
             ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
             assert ok, (P, k, worst)
             assert torch.equal(gv, gt.grads()[k]), k  # same kernels, same summation order
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_split_local_remote_partitions_rows(env, P):
+    """Own-slot / other-slot split: per row, the two parts are a stable
+    partition of the row's entries (multiplicities carried along)."""
+    from paper_2605_29346_b200.dist import RowPartition
+
+    gb, g, X, y = env
+    for r in range(P):
+        part = RowPartition(g, P, r)
+        for op in (part.A, part.AT):
+            loc, rem = part.split_local_remote(op)
+            assert loc.nnz + rem.nnz == op.nnz
+            off = op.offsets.cpu().numpy(); cols = op.cols.cpu().numpy()
+            vals = op.vals.cpu().numpy() if op.vals is not None else None
+            lo_, hi_ = r * part.stride, (r + 1) * part.stride
+            parts_ = [(x.offsets.cpu().numpy(), x.cols.cpu().numpy(),
+                       x.vals.cpu().numpy() if x.vals is not None else None) for x in (loc, rem)]
+            for v in range(op.num_rows):
+                row = cols[off[v]:off[v + 1]]
+                own = (row >= lo_) & (row < hi_)
+                for (o, c, vv), sel in zip(parts_, (own, ~own)):
+                    assert np.array_equal(c[o[v]:o[v + 1]], row[sel])
+                    if vals is not None:
+                        assert np.array_equal(vv[o[v]:o[v + 1]], vals[off[v]:off[v + 1]][sel])
