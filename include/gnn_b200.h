@@ -117,6 +117,14 @@ int gnn_csr_coalesce(int64_t num_rows, int64_t nnz, const int64_t *offsets, cons
                      int64_t *out_offsets, int32_t *out_cols, float *out_mult, int64_t *out_nnz,
                      void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Packed-weight operand for gnn_spmm (see gnn_csr_view_t.col_bits):
+ * out[j] = cols[j] | (uint32)weights[j] << col_bits.  GNN_ERR_RANGE (one
+ * sync) if a column needs more than col_bits bits or a weight is not an
+ * integer in [0, 2^(32-col_bits)) — the caller keeps the float form then. */
+size_t gnn_csr_pack_weights_workspace(void);
+int gnn_csr_pack_weights(int64_t nnz, const int32_t *cols, const float *weights, int32_t col_bits,
+                         int32_t *out, void *ws, size_t ws_bytes, gnn_stream_t stream);
+
 /* Chung-Lu power-law edge draws of graph.py:256-261, bit-exact: numpy PCG64
  * (state,inc given as 128-bit hi/lo words of the SeedSequence-seeded
  * generator) position k -> double (raw>>11)*2^-53; src uses positions
@@ -199,6 +207,20 @@ typedef struct gnn_csr_view {
   const float *vals;          /* [nnz*heads] edge values, or NULL (SpMMv: implicit 1, no |E| tensor) */
   const int32_t *eid;         /* [nnz] or NULL: edge value of entry j is vals[eid[j]] (SpMMve^T) */
   const int64_t *deg_offsets; /* degree source for GNN_EPI_NORM, NULL = offsets */
+  /* 0, or (gnn_spmm / gnn_spmm_peer only; vals == NULL, heads == 1) the
+   * packed-weight form built by gnn_csr_pack_weights: entry j is column
+   * cols[j] & (2^col_bits - 1) with edge value (float)(cols[j] >> col_bits)
+   * — the coalesced multigraph operand (multiplicities) in 4 bytes per edge.
+   * Every other entry point rejects col_bits != 0. */
+  int32_t col_bits;
+  int32_t reserved_;
+  /* NULL, or (gnn_spmm / gnn_spmm_peer only) a row-permuted operand: operand
+   * row i produces output row row_ids[i], and every per-row epilogue input
+   * (deg_offsets, self_x, mask, bias row, post_deg_offsets) is indexed by
+   * row_ids[i].  Used for the degree-sorted form (rows longest-first), whose
+   * long rows form a prefix the nnz-split kernel covers alone.  NORM then
+   * requires deg_offsets (indexed by output row). */
+  const int32_t *row_ids;
 } gnn_csr_view_t;
 
 /* Epilogue applied per output row v, in this order:
@@ -241,7 +263,7 @@ typedef struct gnn_epilogue {
  * plan may serve concurrent calls on different streams. */
 typedef struct gnn_spmm_plan {
   int64_t edges_per_warp;          /* multiple of 4, <= 2048 */
-  int64_t num_warps;               /* ceil(nnz / edges_per_warp) */
+  int64_t num_warps;               /* ceil(main_nnz / edges_per_warp) */
   const int32_t *chunk_row;        /* [num_warps+1] */
   const int32_t *chunk_split;      /* [2*num_warps] split index of carry-in / trailing row or -1 */
   int64_t num_split;
@@ -252,7 +274,12 @@ typedef struct gnn_spmm_plan {
   const int32_t *empty_rows;       /* [num_empty] */
   int64_t short_max;               /* rows with 1 <= deg <= short_max go to the short-row kernel */
   int64_t num_short;
-  const int32_t *short_rows;       /* [num_short] */
+  const int32_t *short_rows;       /* [num_short], longest first */
+  int64_t main_nnz;                /* edges the nnz-split kernel covers: nnz, or — for a
+                                      permuted operand (row_ids) whose rows of degree >
+                                      short_max form a prefix (degree-sorted) — that
+                                      prefix's edge count; gnn_spmm then needs the
+                                      short-row kernel (K <= 64, 16-byte rows) */
 } gnn_spmm_plan_t;
 
 size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_per_warp);

@@ -19,6 +19,8 @@ import torch
 from .errors import ExtensionMissing, RangeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgnnb200.so")
+# experiment builds (tools/): GNN_LIB_PATH selects another in-tree build of the library
+LIB_PATH = os.environ.get("GNN_LIB_PATH", LIB_PATH)
 
 GNN_OK = 0
 GNN_ERR_INVALID_ARGUMENT = 1
@@ -54,6 +56,9 @@ class CsrView(C.Structure):
         ("vals", c_ptr),
         ("eid", c_ptr),
         ("deg_offsets", c_ptr),
+        ("col_bits", C.c_int32),
+        ("reserved_", C.c_int32),
+        ("row_ids", c_ptr),
     ]
 
 
@@ -89,6 +94,7 @@ class SpmmPlan(C.Structure):
         ("short_max", c_i64),
         ("num_short", c_i64),
         ("short_rows", c_ptr),
+        ("main_nnz", c_i64),
     ]
 
 
@@ -119,6 +125,8 @@ SIGNATURES = {
         c_int,
         [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, C.POINTER(c_i64), c_ptr, c_sz, c_ptr],
     ),
+    "gnn_csr_pack_weights_workspace": (c_sz, []),
+    "gnn_csr_pack_weights": (c_int, [c_i64, c_ptr, c_ptr, C.c_int32, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_generate_powerlaw_workspace": (c_sz, [c_i64]),
     "gnn_generate_powerlaw": (
         c_int,

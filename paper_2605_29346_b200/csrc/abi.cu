@@ -28,7 +28,7 @@ int sm_count() {
 
 extern "C" {
 
-int gnn_abi_version(void) { return 2; }
+int gnn_abi_version(void) { return 3; }
 
 const char *gnn_strerror(int s) {
   switch (s) {

@@ -650,7 +650,7 @@ size_t softmax_ws_layout(const gnn_spmm_plan_t *plan, int64_t H, size_t *o_stat)
 
 int softmax_common(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
                    const gnn_edge_scores_t *sc, void *ws, size_t ws_bytes, SoftmaxArgs &a) {
-  if (!A || !plan || heads <= 0 || heads > 16 || !A->offsets || (A->nnz > 0 && !A->cols))
+  if ((A && (A->col_bits || A->row_ids)) || !A || !plan || heads <= 0 || heads > 16 || !A->offsets || (A->nnz > 0 && !A->cols))
     return GNN_ERR_INVALID_ARGUMENT;
   if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
@@ -1166,7 +1166,7 @@ extern "C" {
 int gnn_sddmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads, const float *X,
               int64_t ldx, const float *Y, int64_t ldy, int64_t K, float *out,
               gnn_stream_t stream) {
-  if (!A || !plan || heads <= 0 || K <= 0 || K % heads != 0 || !A->offsets)
+  if ((A && (A->col_bits || A->row_ids)) || !A || !plan || heads <= 0 || K <= 0 || K % heads != 0 || !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->nnz > 0 && (!A->cols || !X || !Y || !out || ldx < K || ldy < K))
     return GNN_ERR_INVALID_ARGUMENT;
@@ -1311,7 +1311,7 @@ int gnn_gat_bwd_csc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64
                     const float *alpha, const float *dY, int64_t ldy, const float *Wh, int64_t ldw,
                     int64_t K, float *dWh, int64_t ldd, float *dalpha, void *ws, size_t ws_bytes,
                     gnn_stream_t stream) {
-  if (!AT || !plan || heads <= 0 || heads > 8 || K <= 0 || K % heads != 0 || !AT->offsets)
+  if ((AT && (AT->col_bits || AT->row_ids)) || !AT || !plan || heads <= 0 || heads > 8 || K <= 0 || K % heads != 0 || !AT->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
   const int64_t F = K / heads;
   if (K % 4 || F % 4 || ldy % 4 || ldw % 4 || ldd % 4 || ldy < K || ldw < K || ldd < K)
@@ -1409,7 +1409,7 @@ int gnn_gat_bwd_csc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, 
                          const float *alpha, const float *dZ, int64_t ldz, float scale,
                          const float *Wh, int64_t ldw, int64_t F, float *dWh, int64_t ldd,
                          float *dalpha, void *ws, size_t ws_bytes, gnn_stream_t stream) {
-  if (!AT || !plan || heads <= 0 || heads > 8 || F <= 0 || !AT->offsets)
+  if ((AT && (AT->col_bits || AT->row_ids)) || !AT || !plan || heads <= 0 || heads > 8 || F <= 0 || !AT->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
   const int64_t K = heads * F;
   if (F % 4 || ldz % 4 || ldw % 4 || ldd % 4 || ldz < F || ldw < K || ldd < K || F > 128)

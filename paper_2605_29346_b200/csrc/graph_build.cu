@@ -716,6 +716,40 @@ int gnn_csr_coalesce(int64_t R, int64_t nnz, const int64_t *offsets, const int32
   return GNN_OK;
 }
 
+__global__ void pack_weights_kernel(const int32_t *__restrict__ cols, const float *__restrict__ w,
+                                    int64_t nnz, int col_bits, int32_t *out, int *flag) {
+  const uint32_t cmax = 1u << col_bits;  // col_bits <= 31
+  const float wmax = (float)(1ull << (32 - col_bits));
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)cols[j];
+    const float x = w[j];
+    if (c >= cmax || !(x >= 0.f) || x >= wmax || x != truncf(x)) {
+      atomicOr(flag, 1);
+      continue;
+    }
+    out[j] = (int32_t)(c | ((uint32_t)x << col_bits));
+  }
+}
+
+size_t gnn_csr_pack_weights_workspace(void) { return 256; }
+int gnn_csr_pack_weights(int64_t nnz, const int32_t *cols, const float *weights, int32_t col_bits,
+                         int32_t *out, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (nnz < 0 || col_bits < 1 || col_bits > 31 || (nnz > 0 && (!cols || !weights || !out)) || !ws)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < sizeof(int)) return GNN_ERR_WORKSPACE;
+  if (nnz == 0) return GNN_OK;
+  cudaStream_t st = as_stream(stream);
+  int *flag = static_cast<int *>(ws);
+  GNN_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  pack_weights_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, weights, nnz, col_bits, out, flag);
+  GNN_LAUNCH_CHECK();
+  int h = 0;
+  GNN_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  return h ? GNN_ERR_RANGE : GNN_OK;
+}
+
 size_t gnn_generate_powerlaw_workspace(int64_t n) {
   (void)n;
   return sizeof(int32_t) * (size_t)(kGuide + 1) + 256;

@@ -55,6 +55,9 @@ struct SpmmArgs {
   float *l2;                   // [num_groups][K] level-2 partials
   float *slots;                // [nwarps][2][K]
   int stage;                 // StageMode
+  const int32_t *row_ids;    // row-permuted operand: operand row i -> output row row_ids[i]
+  int col_bits;              // packed weights (WM_PACKED): column id = cols[j] & col_mask,
+  uint32_t col_mask;         //   edge weight = float(cols[j] >> col_bits)
   int bulk_ok;
   int warp_smem;             // bytes of shared memory per warp
   int64_t short_max;         // rows with 1 <= deg <= short_max: short-row kernel, skipped here
@@ -96,6 +99,9 @@ struct VecT<1> {
   static __device__ __forceinline__ T shfl_xor(T v, int o) { return __shfl_xor_sync(kFull, v, o); }
 };
 
+__device__ __forceinline__ int64_t out_row(const SpmmArgs &a, int64_t r) {
+  return a.row_ids ? (int64_t)a.row_ids[r] : r;
+}
 __device__ __forceinline__ float inv_deg(const int64_t *off, int64_t r) {
   int64_t d = off[r + 1] - off[r];
   return d > 0 ? 1.0f / (float)d : 0.0f;
@@ -144,6 +150,19 @@ __device__ __forceinline__ typename VecT<VW>::T epi_vec(typename VecT<VW>::T y, 
 // only waits on the feature loads.  U edges per group are in flight per
 // iteration (U*32/G per warp).
 enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
+// Where an edge's weight comes from (compile-time, so the gather loop carries
+// no per-edge mode test):
+//   WM_NONE    implicit 1 (SpMMv)
+//   WM_GLOBAL  vals[(e)*heads + head] read from global (multi-head SpMMve)
+//   WM_SVALS   vals staged in the shared ring with the column ids (heads == 1)
+//   WM_SEID    edge ids staged in the ring, vals[eid*heads + head] (SpMMve^T)
+//   WM_PACKED  small integer weight in the high bits of the column id (the
+//              coalesced multigraph operand: one 4-byte word per edge)
+enum WeightMode : int { WM_NONE = 0, WM_GLOBAL = 1, WM_SVALS = 2, WM_SEID = 3, WM_PACKED = 4 };
+template <int WM>
+constexpr int stage_of() {
+  return WM == WM_SVALS ? STAGE_VALS : WM == WM_SEID ? STAGE_EID : STAGE_NONE;
+}
 
 // Lane-invariant part of the gather: per-vector base pointers (column offset
 // folded in; columns past K are clamped to column 0 and simply not stored).
@@ -191,38 +210,45 @@ __device__ __forceinline__ typename VecT<VW>::T gather_x(const SpmmArgs &a, cons
 // blocks of U edges per group run unpredicated; the remainder is one
 // predicated block, so a piece costs a single gather latency.  The order is
 // fixed by (G, U, piece bounds): deterministic.
-template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
+template <int G, int VPL, int VW, int WM, bool PEER = false>
 __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols<G, VPL, VW, PEER> &lc,
-                                               const int32_t *scol, const void *sval, int stage,
+                                               const int32_t *scol, const void *sval,
                                                int64_t ebase, int is, int ie,
                                                typename VecT<VW>::T (&acc)[VPL]) {
   using V = VecT<VW>;
+  constexpr bool HAS_VALS = WM != WM_NONE;
   constexpr int NG = 32 / G;
   constexpr int U = (VPL * VW >= 8) ? 4 : 8;
   const int g = (int)lane_id() / G;
   const uint32_t ldxb = (uint32_t)a.ldx * 4u;
-  auto weight = [&](int i, int v) -> float {
-    if (stage == STAGE_VALS) return static_cast<const float *>(sval)[i];
+  // packed: p -> (column, weight); otherwise the weight of ring entry i
+  auto weight = [&](int i, int v, int32_t p) -> float {
+    if constexpr (WM == WM_PACKED) return (float)((uint32_t)p >> a.col_bits);
+    if constexpr (WM == WM_SVALS) return static_cast<const float *>(sval)[i];
     const int64_t vi =
-        stage == STAGE_EID ? (int64_t) static_cast<const int32_t *>(sval)[i] : ebase + i;
+        WM == WM_SEID ? (int64_t) static_cast<const int32_t *>(sval)[i] : ebase + i;
     return __ldg(a.vals + vi * a.heads + lc.head[v]);
+  };
+  auto col = [&](int32_t p) -> int32_t {
+    if constexpr (WM == WM_PACKED) return (int32_t)((uint32_t)p & a.col_mask);
+    return p;
   };
   int i = is + g;
   for (; i + (U - 1) * NG < ie; i += NG * U) {
-    int32_t c[U];
+    int32_t p[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = scol[i + u * NG];
+    for (int u = 0; u < U; ++u) p[u] = scol[i + u * NG];
     typename V::T x[U][VPL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) x[u][v] = gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb);
+      for (int v = 0; v < VPL; ++v) x[u][v] = gather_x<VW, PEER>(a, lc.xb[v], col(p[u]), ldxb);
     if constexpr (HAS_VALS) {
       float w[U][VPL];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) w[u][v] = weight(i + u * NG, v);
+        for (int v = 0; v < VPL; ++v) w[u][v] = weight(i + u * NG, v, p[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -235,24 +261,25 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
     }
   }
   if (i < ie) {  // one predicated block: < U edges left for this group
-    int32_t c[U];
+    int32_t p[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       ok[u] = i + u * NG < ie;
-      c[u] = ok[u] ? scol[i + u * NG] : 0;
+      p[u] = ok[u] ? scol[i + u * NG] : 0;
     }
     typename V::T x[U][VPL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb) : V::zero();
+      for (int v = 0; v < VPL; ++v)
+        x[u][v] = ok[u] ? gather_x<VW, PEER>(a, lc.xb[v], col(p[u]), ldxb) : V::zero();
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         if constexpr (HAS_VALS)
-          acc[v] = V::fma(ok[u] ? weight(i + u * NG, v) : 0.f, x[u][v], acc[v]);
+          acc[v] = V::fma(ok[u] ? weight(i + u * NG, v, p[u]) : 0.f, x[u][v], acc[v]);
         else
           acc[v] = V::add(acc[v], x[u][v]);
       }
@@ -334,6 +361,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
   const int lane = (int)lane_id();
   const int64_t r = a.split_rows[s];
   const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t orow = out_row(a, r);
   const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
   const int64_t np = wb - wa + 1;
   const int64_t gi = j / kGroupPartials;
@@ -347,15 +375,15 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
   if (lane == 0) old = atom_add_release_gpu(&a.cnt1[(gbase + gi) * a.ncb + blockIdx.y], 1);
   old = __shfl_sync(kFull, old, 0);
   if (old != m - 1) return;
-  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, r) : 1.f;
-  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
+  const float ns = (a.epi.flags & GNN_EPI_NORM) ? inv_deg(a.deg_offsets, orow) : 1.f;
+  const float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, orow) : 1.f;
   const int64_t j0 = gi * kGroupPartials;
   for (int64_t c = cbase + lane; c < cend; c += 32) {
     float t = 0.f;
 #pragma unroll 8
     for (int k = 0; k < m; ++k) t += ld_relaxed_gpu(partial_ptr(a, wa, j0 + k) + c);
     if (ng == 1)
-      a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+      a.Y[orow * a.ldy + c] = epi_scalar(t, orow, c, a, ns, ps);
     else
       a.l2[(gbase + gi) * a.K + c] = t;
   }
@@ -368,7 +396,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
     float t = 0.f;
 #pragma unroll 8
     for (int64_t g2 = 0; g2 < ng; ++g2) t += ld_relaxed_gpu(a.l2 + (gbase + g2) * a.K + c);
-    a.Y[r * a.ldy + c] = epi_scalar(t, r, c, a, ns, ps);
+    a.Y[orow * a.ldy + c] = epi_scalar(t, orow, c, a, ns, ps);
   }
 }
 
@@ -381,8 +409,11 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
 // range boundaries produce partials (split rows, finished by split_arrive).
 constexpr int kSub = 512;
 
-template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
-__global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
+template <int G, int VPL, int VW, int WM, bool PEER = false>
+#ifndef GNN_SPMM_MINB
+#define GNN_SPMM_MINB 4  // resident CTAs per SM (8 warps each) the register budget targets (64 regs)
+#endif
+__global__ void __launch_bounds__(256, GNN_SPMM_MINB) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
   extern __shared__ __align__(16) uint8_t spmm_smem[];
@@ -390,7 +421,7 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
   const int lane = (int)lane_id();
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= a.nwarps) return;
-  const int stage = a.stage;
+  constexpr int stage = stage_of<WM>();
   uint8_t *wbase = spmm_smem + (size_t)warp * a.warp_smem;
   uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);           // [2]
   int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);       // [2][kSub]
@@ -455,7 +486,7 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
       const int64_t lo = max(rs, s0), hi = min(re, s1);
       const bool is_short = re - rs <= a.short_max;  // owned by the short-row kernel
       if (hi > lo && !is_short)
-        seg_accumulate<G, VPL, VW, HAS_VALS, PEER>(a, lc, bc, bv, stage, s0, (int)(lo - s0),
+        seg_accumulate<G, VPL, VW, WM, PEER>(a, lc, bc, bv, s0, (int)(lo - s0),
                                              (int)(hi - s0), acc);
       if (re > s1) break;  // row continues in the next sub-chunk (or the next warp)
       if (re > rs && !is_short) {  // a row ends here
@@ -464,7 +495,8 @@ __global__ void __launch_bounds__(256, 3) spmm_main_kernel(SpmmArgs a) {
           store_row<G, VPL, VW>(a, a.slots + (w * 2 + 0) * a.K, cbase, acc, false, r);
           split_arrive(a, a.chunk_split[2 * w], w - rs / a.P, cbase, KB);
         } else {
-          store_row<G, VPL, VW>(a, a.Y + r * a.ldy, cbase, acc, true, r);
+          const int64_t orow = out_row(a, r);
+          store_row<G, VPL, VW>(a, a.Y + orow * a.ldy, cbase, acc, true, orow);
         }
 #pragma unroll
         for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
@@ -734,35 +766,61 @@ int launch_tma(const SpmmArgs &a, bool has_vals, const CUtensorMap &tm, cudaStre
 
 // Short rows (1 <= deg <= short_max; the power-law tail): one lane group per
 // row instead of a whole warp walking rows one by one — NG rows per warp in
-// parallel, U edges of each in flight, fused epilogue per group.  Indices and
-// edge values are read straight from global (a short row is one or two
-// sectors).  Summation order is fixed per row: deterministic.
-template <int G, int VPL, int VW, bool HAS_VALS, bool PEER = false>
-__global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
-                                                              int64_t nrows) {
+// parallel, U edges of each in flight, fused epilogue per group.  The group's
+// lanes load its column ids cooperatively (consecutive words, then a shuffle
+// broadcast: one L1 request per G ids instead of G), in 32-bit row-relative
+// arithmetic; the loop runs to the warp's longest row (the list is longest
+// first, so neighbours are near-equal) so every shuffle is warp-converged.
+// Summation order is fixed per row: deterministic.
+template <int G, int VPL, int VW, int WM, bool PEER = false>
+__global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
+                                                                 int64_t nrows) {
   using V = VecT<VW>;
   constexpr int NG = 32 / G;
   constexpr int U = (VPL * VW >= 8) ? 4 : 8;
+  constexpr int KL = (U + G - 1) / G;  // ids each lane loads per block
   constexpr int KB = G * VPL * VW;
   const int lane = (int)lane_id();
   const int g = lane / G, gl = lane % G;
+  const int gbase = lane & ~(G - 1);
   const int64_t cbase = (int64_t)blockIdx.y * KB;
   const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * NG + g;
-  if (i >= nrows) return;  // group-uniform
-  const int64_t r = rows[i];
-  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const bool valid = i < nrows;
+  const int64_t r = valid ? rows[i] : 0;
+  const int64_t rs = valid ? a.offsets[r] : 0;
+  const int n = valid ? (int)(a.offsets[r + 1] - rs) : 0;  // deg <= short_max
+  int nmax = n;
+#pragma unroll
+  for (int o = 16; o >= G; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
+  const int32_t *cp = a.cols + rs;
   const LaneCols<G, VPL, VW, PEER> lc(a, cbase);
   const uint32_t ldxb = (uint32_t)a.ldx * 4u;
+  const int cbits = a.col_bits;
+  const uint32_t cmask = a.col_mask;
   typename V::T acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
-  for (int64_t e = rs; e < re; e += U) {
+  for (int e = 0; e < nmax; e += U) {
+    int32_t mine[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      const int j = gl + k * G;
+      mine[k] = (j < U && e + j < n) ? __ldg(cp + e + j) : 0;
+    }
     int32_t c[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ok[u] = e + u < re;
-      c[u] = ok[u] ? __ldg(a.cols + e + u) : 0;
+      ok[u] = e + u < n;
+      c[u] = __shfl_sync(kFull, mine[u / G], gbase + u % G);
+    }
+    float pw[U];  // packed weights
+    if constexpr (WM == WM_PACKED) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pw[u] = (float)((uint32_t)c[u] >> cbits);
+        c[u] = (int32_t)((uint32_t)c[u] & cmask);
+      }
     }
     typename V::T x[U][VPL];
 #pragma unroll
@@ -771,12 +829,16 @@ __global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const 
       for (int v = 0; v < VPL; ++v) x[u][v] = ok[u] ? gather_x<VW, PEER>(a, lc.xb[v], c[u], ldxb) : V::zero();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if constexpr (HAS_VALS) {
+      if constexpr (WM != WM_NONE) {
         float w[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
-          const int64_t vi = ok[u] ? (a.eid ? (int64_t)__ldg(a.eid + e + u) : e + u) : 0;
-          w[v] = ok[u] ? __ldg(a.vals + vi * a.heads + lc.head[v]) : 0.f;
+          if constexpr (WM == WM_PACKED) {
+            w[v] = pw[u];  // 0 for the padding entries (c = 0)
+          } else {
+            const int64_t vi = ok[u] ? (WM == WM_SEID ? (int64_t)__ldg(a.eid + rs + e + u) : rs + e + u) : 0;
+            w[v] = ok[u] ? __ldg(a.vals + vi * a.heads + lc.head[v]) : 0.f;
+          }
         }
 #pragma unroll
         for (int v = 0; v < VPL; ++v) acc[v] = V::fma(w[v], x[u][v], acc[v]);
@@ -786,14 +848,16 @@ __global__ void __launch_bounds__(256) spmm_short_rows_kernel(SpmmArgs a, const 
       }
     }
   }
+  if (!valid) return;
+  const int64_t orow = out_row(a, r);
   float ns = 1.f, ps = 1.f;
-  if (a.epi.flags & GNN_EPI_NORM) ns = inv_deg(a.deg_offsets, r);
-  if (a.epi.flags & GNN_EPI_POSTNORM) ps = inv_deg(a.epi.post_deg_offsets, r);
-  float *dst = a.Y + r * a.ldy;
+  if (a.epi.flags & GNN_EPI_NORM) ns = inv_deg(a.deg_offsets, orow);
+  if (a.epi.flags & GNN_EPI_POSTNORM) ps = inv_deg(a.epi.post_deg_offsets, orow);
+  float *dst = a.Y + orow * a.ldy;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int64_t col = cbase + (int64_t)(v * G + gl) * VW;
-    if (col < a.K) V::st(dst + col, epi_vec<VW>(acc[v], r, col, a, ns, ps));
+    if (col < a.K) V::st(dst + col, epi_vec<VW>(acc[v], orow, col, a, ns, ps));
   }
 }
 
@@ -803,7 +867,7 @@ __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ r
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / a.K, c = t % a.K;
-    int64_t r = rows[i];
+    int64_t r = out_row(a, rows[i]);
     float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
     a.Y[r * a.ldy + c] = epi_scalar(0.f, r, c, a, 0.f, ps);
   }
@@ -819,17 +883,28 @@ __global__ void plan_chunk_rows_kernel(const int64_t *__restrict__ off, int64_t 
                                          : (int32_t)(upper_bound_dev(off, 0, R + 1, e) - 1);
   }
 }
+// Do the rows of degree > short_max form a prefix (a degree-sorted operand)?
+// info[0] |= 1 on a long row after a non-long one; info[1] = long-row count.
+__global__ void plan_long_prefix_kernel(const int64_t *__restrict__ off, int64_t R,
+                                        int64_t short_max, unsigned long long *info) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const bool lg = off[r + 1] - off[r] > short_max;
+    if (lg) atomicAdd(info + 1, 1ull);
+    if (lg && r > 0 && off[r] - off[r - 1] <= short_max) atomicOr(info, 1ull);
+  }
+}
 __global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                  int64_t short_max, int64_t *fsplit, int64_t *fempty,
-                                  int64_t *ngroups, int64_t *fshort) {
+                                  int64_t short_max, int64_t main_nnz, int64_t *fsplit,
+                                  int64_t *fempty, int64_t *ngroups, int64_t *fshort) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t rs = off[r], re = off[r + 1];
     fempty[r] = re == rs ? 1 : 0;
     fshort[r] = (re > rs && re - rs <= short_max) ? 1 : 0;
-    // split-row bookkeeping covers short rows too: a call that does not use the
-    // short-row kernel (wide K: one row per warp anyway) finishes them here
-    const bool split = re > rs && rs / P != (re - 1) / P;
+    // split-row bookkeeping covers short rows too (inside the nnz-split range):
+    // a call that does not use the short-row kernel (wide K) finishes them here
+    const bool split = re > rs && re <= main_nnz && rs / P != (re - 1) / P;
     fsplit[r] = split ? 1 : 0;
     ngroups[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kGroupPartials) : 0;
   }
@@ -856,23 +931,68 @@ __global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, 
   }
 }
 
+// Degree order of the short-row list (longest first): the NG rows a warp of
+// the group-per-row kernel runs side by side then have near-equal lengths,
+// so no group idles behind a longer neighbour.  Counting sort on min(deg, R);
+// the order among equal degrees is arbitrary (each row's result does not
+// depend on where it is scheduled).
+__global__ void short_hist_kernel(const int64_t *__restrict__ off, int64_t R,
+                                  const int32_t *__restrict__ rows, int64_t n, int64_t *hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows[i];
+    const int64_t d = min(off[r + 1] - off[r], R);
+    atomicAdd(reinterpret_cast<unsigned long long *>(hist + (R - d)), 1ull);
+  }
+}
+__global__ void short_scatter_kernel(const int64_t *__restrict__ off, int64_t R,
+                                     const int32_t *__restrict__ rows, int64_t n, int64_t *cursor,
+                                     int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rows[i];
+    const int64_t d = min(off[r + 1] - off[r], R);
+    const int64_t pos =
+        (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(cursor + (R - d)), 1ull);
+    out[pos] = r;
+  }
+}
+
 unsigned grid_1d(int64_t n, int threads) {
   int64_t b = ceil_div(n > 0 ? n : 1, threads);
   int64_t cap = (int64_t)sm_count() * 32;
   return (unsigned)(b < cap ? b : cap);
 }
 
+template <int G, int VPL, int VW, int WM, bool PEER>
+struct MainKernel {
+  static constexpr auto fn = spmm_main_kernel<G, VPL, VW, WM, PEER>;
+};
+template <int G, int VPL, int VW, int WM, bool PEER>
+struct ShortKernel {
+  static constexpr auto fn = spmm_short_rows_kernel<G, VPL, VW, WM, PEER>;
+};
+template <template <int, int, int, int, bool> class K, int G, int VPL, int VW, bool PEER>
+auto pick_wm(int wm) {
+  switch (wm) {
+    case WM_GLOBAL: return K<G, VPL, VW, WM_GLOBAL, PEER>::fn;
+    case WM_SVALS: return K<G, VPL, VW, WM_SVALS, PEER>::fn;
+    case WM_SEID: return K<G, VPL, VW, WM_SEID, PEER>::fn;
+    case WM_PACKED: return K<G, VPL, VW, WM_PACKED, PEER>::fn;
+    default: return K<G, VPL, VW, WM_NONE, PEER>::fn;
+  }
+}
+
 template <int G, int VPL, int VW, bool PEER = false>
-int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
+int launch_main(const SpmmArgs &a, int wm, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   dim3 grid((unsigned)ceil_div(a.nwarps * 32, 256), (unsigned)ceil_div(a.K, KB));
   const size_t smem = (size_t)a.warp_smem * 8;
   // Shared memory only holds the staged index chunks; give the rest of the
   // unified L1/shared array to L1 so hot feature rows stay cached.
-  auto kern = has_vals ? spmm_main_kernel<G, VPL, VW, true, PEER>
-                       : spmm_main_kernel<G, VPL, VW, false, PEER>;
+  auto kern = pick_wm<MainKernel, G, VPL, VW, PEER>(wm);
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm_kb = (int)((smem * 3 + 1023) / 1024);  // 3 resident CTAs (persistent grid)
+  const int per_sm_kb = (int)((smem * GNN_SPMM_MINB + 1023) / 1024);  // resident CTAs
   const int carve = per_sm_kb * 100 / 228 + 1;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     carve > 100 ? 100 : carve));
@@ -883,18 +1003,41 @@ int launch_main(const SpmmArgs &a, bool has_vals, cudaStream_t st) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Per-thread, per-device side stream + fork/join events for the concurrent
+// short-row launch (GNN_SPMM_CONCURRENT=0 serialises it on the caller's stream).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream &side_stream() {
+  static thread_local SideStream ss[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream &x = ss[dev & 63];
+  if (!x.s) {
+    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return x;
+}
+bool spmm_concurrent() {
+  static const bool on = [] {
+    const char *e = getenv("GNN_SPMM_CONCURRENT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int G, int VPL, int VW, bool PEER = false>
-int launch_short(const SpmmArgs &a, bool has_vals, const gnn_spmm_plan_t *plan, cudaStream_t st) {
+int launch_short(const SpmmArgs &a, int wm, const gnn_spmm_plan_t *plan, cudaStream_t st) {
   constexpr int KB = G * VPL * VW;
   constexpr int NG = 32 / G;
   const int64_t warps = ceil_div(plan->num_short, NG);
   dim3 grid((unsigned)ceil_div(warps * 32, 256), (unsigned)ceil_div(a.K, KB));
-  if (has_vals)
-    spmm_short_rows_kernel<G, VPL, VW, true, PEER><<<grid, 256, 0, st>>>(a, plan->short_rows,
-                                                                         plan->num_short);
-  else
-    spmm_short_rows_kernel<G, VPL, VW, false, PEER><<<grid, 256, 0, st>>>(a, plan->short_rows,
-                                                                          plan->num_short);
+  // the short kernel reads vals / eid straight from global: SVALS == GLOBAL there
+  auto kern = pick_wm<ShortKernel, G, VPL, VW, PEER>(wm == WM_SVALS ? WM_GLOBAL : wm);
+  kern<<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -937,8 +1080,9 @@ size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_pe
 
 size_t gnn_spmm_plan_workspace(int64_t num_rows) {
   WsCounter c;
-  for (int i = 0; i < 4; ++i) c.take<int64_t>(num_rows + 1);
-  c.used += 4 * (scan_i64_workspace(num_rows) + 256);
+  for (int i = 0; i < 5; ++i) c.take<int64_t>(num_rows + 1);
+  c.take<int32_t>(num_rows + 1);
+  c.used += 5 * (scan_i64_workspace(num_rows) + 256);
   return c.used + 512;
 }
 
@@ -957,7 +1101,6 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   if (ws_bytes < gnn_spmm_plan_workspace(A->num_rows)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
   const int64_t R = A->num_rows;
-  const PlanLayout L = plan_layout(R, A->nnz, P);
   WsArena ar(ws, ws_bytes);
   int64_t *fs = ar.take<int64_t>(R + 1);
   int64_t *fe = ar.take<int64_t>(R + 1);
@@ -968,13 +1111,35 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   void *s2 = ar.take<char>((int64_t)sb);
   void *s3 = ar.take<char>((int64_t)sb);
   void *s4 = ar.take<char>((int64_t)sb);
+  int64_t *dh = ar.take<int64_t>(R + 1);   // short rows: degree histogram -> cursors
+  int32_t *srt = ar.take<int32_t>(R + 1);  // short rows in degree order
+  void *s5 = ar.take<char>((int64_t)sb);
   if (!ar.ok()) return GNN_ERR_WORKSPACE;
-  plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, A->nnz, P, L.nw,
+  // long rows a prefix (degree-sorted operand)?  then the nnz-split kernel
+  // covers only their edges and never walks the short tail
+  int64_t main_nnz = A->nnz;
+  if (short_max > 0 && R > 0 && A->row_ids) {  // only a permuted (sorted) operand opts in
+    unsigned long long *info = reinterpret_cast<unsigned long long *>(dh);
+    GNN_CUDA_TRY(cudaMemsetAsync(info, 0, 2 * sizeof(unsigned long long), st));
+    plan_long_prefix_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, short_max, info);
+    GNN_LAUNCH_CHECK();
+    unsigned long long hi[2] = {1, 0};
+    GNN_CUDA_TRY(cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, st));
+    GNN_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hi[0] == 0) {
+      GNN_CUDA_TRY(cudaMemcpyAsync(&main_nnz, A->offsets + hi[1], sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, st));
+      GNN_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
+  const PlanLayout L = plan_layout(R, main_nnz, P);
+  plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, main_nnz, P, L.nw,
                                                                  buf + L.o_chunk);
   GNN_LAUNCH_CHECK();
   if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, fs, fe, fg, fh);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, main_nnz, fs,
+                                                       fe, fg, fh);
     GNN_LAUNCH_CHECK();
   }
   GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
@@ -994,6 +1159,16 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], fg + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaMemcpyAsync(&h[3], fh + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h[3] > 1) {  // longest-first order of the short rows
+    int32_t *sr = buf + L.o_short;
+    GNN_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(int64_t) * (R + 1), st));
+    short_hist_kernel<<<grid_1d(h[3], 256), 256, 0, st>>>(A->offsets, R, sr, h[3], dh);
+    GNN_LAUNCH_CHECK();
+    GNN_TRY(exclusive_scan_i64(dh, dh, R, true, s5, sb, st));
+    short_scatter_kernel<<<grid_1d(h[3], 256), 256, 0, st>>>(A->offsets, R, sr, h[3], dh, srt);
+    GNN_LAUNCH_CHECK();
+    GNN_CUDA_TRY(cudaMemcpyAsync(sr, srt, sizeof(int32_t) * h[3], cudaMemcpyDeviceToDevice, st));
+  }
   plan->edges_per_warp = P;
   plan->num_warps = L.nw;
   plan->chunk_row = buf + L.o_chunk;
@@ -1005,6 +1180,7 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   plan->num_empty = h[1];
   plan->empty_rows = buf + L.o_empty;
   plan->short_max = short_max;
+  plan->main_nnz = main_nnz;
   plan->num_short = h[3];
   plan->short_rows = buf + L.o_short;
   return GNN_OK;
@@ -1040,10 +1216,16 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
       (A->nnz > 0 && (!X || ldx < K || !A->cols)) || !A->offsets)
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->eid && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
-  if (heads > 1 && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->edges_per_warp % 4 != 0 ||
-      plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+  const bool packed = A->col_bits != 0;
+  if (packed && (A->col_bits < 1 || A->col_bits > 31 || A->vals || heads != 1))
     return GNN_ERR_INVALID_ARGUMENT;
+  if (packed && A->num_cols > ((int64_t)1 << A->col_bits)) return GNN_ERR_INVALID_ARGUMENT;
+  if (heads > 1 && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->edges_per_warp % 4 != 0 || plan->main_nnz < 0 ||
+      plan->main_nnz > A->nnz || plan->num_warps != ceil_div(plan->main_nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->row_ids && (epi ? epi->flags & GNN_EPI_NORM : 0) && !A->deg_offsets)
+    return GNN_ERR_INVALID_ARGUMENT;  // NORM of a permuted operand needs output-row degrees
   gnn_epilogue_t e{};
   if (epi) e = *epi;
   if (((e.flags & GNN_EPI_SELF) && (!e.self_x || e.ld_self < K)) ||
@@ -1055,7 +1237,8 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
 
   SpmmArgs a{};
   a.R = A->num_rows;
-  a.nnz = A->nnz;
+  a.nnz = plan->main_nnz;  // the nnz-split kernel's edge range
+  a.row_ids = A->row_ids;
   a.offsets = A->offsets;
   a.cols = A->cols;
   a.vals = A->vals;
@@ -1092,6 +1275,11 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
     GNN_CUDA_TRY(cudaMemsetAsync(
         a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split) * a.ncb, st));
   a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
+  const int wm = packed ? WM_PACKED
+                        : !A->vals ? WM_NONE
+                                   : (A->eid ? WM_SEID : (heads == 1 ? WM_SVALS : WM_GLOBAL));
+  a.col_bits = packed ? A->col_bits : 0;
+  a.col_mask = packed ? (uint32_t)((1ull << A->col_bits) - 1) : 0xffffffffu;
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
   a.warp_smem = (int)(16 + 2 * kSub * 4 * (a.stage != STAGE_NONE ? 2 : 1));
@@ -1101,7 +1289,60 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
                     (a.F % 4 == 0);
     a.short_max = (v4 && K <= 64) ? plan->short_max : 0;
   }
+  // a plan whose nnz-split range stops before the short tail needs the short-row kernel
+  if (plan->main_nnz < A->nnz && a.short_max == 0) return GNN_ERR_UNSUPPORTED;
 
+  // The group-per-row tail and the nnz-split kernel write disjoint rows: run
+  // them concurrently (side stream forked / joined with events — also inside
+  // CUDA-graph capture), so the latency-bound nnz-split kernel and the
+  // L1-bound short kernel share the SMs.
+  auto launch_short_rows = [&](cudaStream_t ss) -> int {
+    // same lane layout as the main kernel for this K (see launch_main dispatch)
+    bool vec4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
+                (a.F % 4 == 0);
+    if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
+    if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
+    if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
+    if (peer) {
+      if (K <= 16)
+        GNN_TRY((launch_short<4, 1, 4, true>(a, wm, plan, ss)));
+      else if (K <= 32)
+        GNN_TRY((launch_short<8, 1, 4, true>(a, wm, plan, ss)));
+      else
+        GNN_TRY((launch_short<16, 1, 4, true>(a, wm, plan, ss)));
+    } else if (vec4) {
+      if (K <= 16)
+        GNN_TRY((launch_short<4, 1, 4>(a, wm, plan, ss)));
+      else if (K <= 32)
+        GNN_TRY((launch_short<8, 1, 4>(a, wm, plan, ss)));
+      else if (K <= 64)
+        GNN_TRY((launch_short<16, 1, 4>(a, wm, plan, ss)));
+      else if (K <= 128)
+        GNN_TRY((launch_short<32, 1, 4>(a, wm, plan, ss)));
+      else
+        GNN_TRY((launch_short<32, 2, 4>(a, wm, plan, ss)));
+    } else {
+      if (K <= 32)
+        GNN_TRY((launch_short<32, 1, 1>(a, wm, plan, ss)));
+      else
+        GNN_TRY((launch_short<32, 4, 1>(a, wm, plan, ss)));
+    }
+      return GNN_OK;
+  };
+  const bool run_short = plan->num_short > 0 && a.short_max > 0;
+  const bool concurrent = run_short && a.nwarps > 0 && spmm_concurrent();
+  SideStream *side = nullptr;
+  if (run_short) {
+    if (concurrent) {
+      side = &side_stream();
+      GNN_CUDA_TRY(cudaEventRecord(side->fork, st));
+      GNN_CUDA_TRY(cudaStreamWaitEvent(side->s, side->fork, 0));
+      GNN_TRY(launch_short_rows(side->s));
+      GNN_CUDA_TRY(cudaEventRecord(side->join, side->s));
+    } else {
+      GNN_TRY(launch_short_rows(st));
+    }
+  }
   if (a.nwarps > 0) {
     const bool hv = A->vals != nullptr;
     // float4 path needs 16B-aligned rows and heads that do not straddle a vector
@@ -1111,7 +1352,7 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
     if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
     if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
     int s;
-    const bool tma_ok = vec4 && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
+    const bool tma_ok = vec4 && !packed && !A->row_ids && plan->main_nnz == A->nnz && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
                         a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
                         plan->short_max == 0 && !peer && getenv("GNN_SPMM_TMA") != nullptr;
     CUtensorMap tm;
@@ -1127,63 +1368,31 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
     } else if (peer) {
       if (!vec4 || K > 64) return GNN_ERR_UNSUPPORTED;
       if (K <= 16)
-        s = launch_main<4, 1, 4, true>(a, hv, st);
+        s = launch_main<4, 1, 4, true>(a, wm, st);
       else if (K <= 32)
-        s = launch_main<8, 1, 4, true>(a, hv, st);
+        s = launch_main<8, 1, 4, true>(a, wm, st);
       else
-        s = launch_main<16, 1, 4, true>(a, hv, st);
+        s = launch_main<16, 1, 4, true>(a, wm, st);
     } else if (vec4) {
       if (K <= 16)
-        s = launch_main<4, 1, 4>(a, hv, st);
+        s = launch_main<4, 1, 4>(a, wm, st);
       else if (K <= 32)
-        s = launch_main<8, 1, 4>(a, hv, st);
+        s = launch_main<8, 1, 4>(a, wm, st);
       else if (K <= 64)
-        s = launch_main<16, 1, 4>(a, hv, st);
+        s = launch_main<16, 1, 4>(a, wm, st);
       else if (K <= 128)
-        s = launch_main<32, 1, 4>(a, hv, st);
+        s = launch_main<32, 1, 4>(a, wm, st);
       else
-        s = launch_main<32, 2, 4>(a, hv, st);  // 256 columns per block-column
+        s = launch_main<32, 2, 4>(a, wm, st);  // 256 columns per block-column
     } else {
       if (K <= 32)
-        s = launch_main<32, 1, 1>(a, hv, st);
+        s = launch_main<32, 1, 1>(a, wm, st);
       else
-        s = launch_main<32, 4, 1>(a, hv, st);  // 128 columns per block-column
+        s = launch_main<32, 4, 1>(a, wm, st);  // 128 columns per block-column
     }
     GNN_TRY(s);
   }
-  if (plan->num_short > 0 && a.short_max > 0) {
-    // same lane layout as the main kernel for this K (see launch_main dispatch)
-    const bool hv = A->vals != nullptr;
-    bool vec4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
-                (a.F % 4 == 0);
-    if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
-    if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
-    if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
-    if (peer) {
-      if (K <= 16)
-        GNN_TRY((launch_short<4, 1, 4, true>(a, hv, plan, st)));
-      else if (K <= 32)
-        GNN_TRY((launch_short<8, 1, 4, true>(a, hv, plan, st)));
-      else
-        GNN_TRY((launch_short<16, 1, 4, true>(a, hv, plan, st)));
-    } else if (vec4) {
-      if (K <= 16)
-        GNN_TRY((launch_short<4, 1, 4>(a, hv, plan, st)));
-      else if (K <= 32)
-        GNN_TRY((launch_short<8, 1, 4>(a, hv, plan, st)));
-      else if (K <= 64)
-        GNN_TRY((launch_short<16, 1, 4>(a, hv, plan, st)));
-      else if (K <= 128)
-        GNN_TRY((launch_short<32, 1, 4>(a, hv, plan, st)));
-      else
-        GNN_TRY((launch_short<32, 2, 4>(a, hv, plan, st)));
-    } else {
-      if (K <= 32)
-        GNN_TRY((launch_short<32, 1, 1>(a, hv, plan, st)));
-      else
-        GNN_TRY((launch_short<32, 4, 1>(a, hv, plan, st)));
-    }
-  }
+  if (side) GNN_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
   if (plan->num_empty > 0) {
     spmm_empty_rows_kernel<<<grid_1d(plan->num_empty * K, 256), 256, 0, st>>>(a, plan->empty_rows,
                                                                             plan->num_empty);

@@ -209,16 +209,16 @@ class RowPartition:
         off = op.offsets[self.lo:self.hi + 1]
         e0, e1 = int(off[0].item()), int(off[-1].item())
         loc_off = (off - e0).contiguous()
-        cols = op.cols[e0:e1]
+        cols, vals = op.entries(e0, e1)
         out = torch.empty(e1 - e0, dtype=torch.int32, device=cols.device)
         with torch.cuda.device(cols.device):
             _lib.check(lib.gnn_remap_ids(e1 - e0, cols.data_ptr() if e1 > e0 else None,
                                          self.d_bounds.data_ptr(), self.parts, self.stride,
                                          out.data_ptr() if e1 > e0 else None,
                                          _lib.stream_handle(cols.device)), "remap_ids")
-        vals = op.vals[e0:e1].contiguous() if op.vals is not None else None
+        vals = vals.contiguous() if vals is not None else None
         return SparseOperand(self.rows, cols_total, loc_off, out, vals=vals,
-                             deg_offsets=deg if deg is not None else None)
+                             deg_offsets=deg if deg is not None else None, mult=op.mult)
 
     def split_local_remote(self, op: SparseOperand):
         """(local, remote) parts of a sliced operand: entries whose column is
@@ -230,16 +230,17 @@ class RowPartition:
         lo, hi = self.rank * self.stride, (self.rank + 1) * self.stride
         deg = (op.offsets[1:] - op.offsets[:-1])
         rows = torch.repeat_interleave(torch.arange(R, device=dev), deg)
-        is_loc = (op.cols >= lo) & (op.cols < hi)
+        cols, vals_all = op.entries()
+        is_loc = (cols >= lo) & (cols < hi)
         out = []
         for sel in (is_loc, ~is_loc):
             idx = torch.nonzero(sel).squeeze(1)  # keeps row-major, in-row order
             cnt = torch.bincount(rows[idx], minlength=R)
             off = torch.zeros(R + 1, dtype=torch.int64, device=dev)
             torch.cumsum(cnt, 0, out=off[1:])
-            vals = op.vals[idx].contiguous() if op.vals is not None else None
-            out.append(SparseOperand(R, op.num_cols, off, op.cols[idx].contiguous(), vals=vals,
-                                     deg_offsets=op.deg_offsets))
+            vals = vals_all[idx].contiguous() if vals_all is not None else None
+            out.append(SparseOperand(R, op.num_cols, off, cols[idx].contiguous(), vals=vals,
+                                     deg_offsets=op.deg_offsets, mult=op.mult))
         return out[0], out[1]
 
     def local_rows(self, t: torch.Tensor) -> torch.Tensor:

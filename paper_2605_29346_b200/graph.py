@@ -77,23 +77,179 @@ def _default_edges_per_warp(nnz: int, sms: int) -> int:
 
 
 # rows of degree <= this go to the SpMM's group-per-row kernel (power-law tail)
-SPMM_SHORT_MAX = int(os.environ.get("GNN_SPMM_SHORT", "32"))
+SPMM_SHORT_MAX = int(os.environ.get("GNN_SPMM_SHORT", "512"))
+
+
+# GNN_SPMM_SORT=0 keeps gnn_spmm on the operand's own row order
+SPMM_SORT = os.environ.get("GNN_SPMM_SORT", "1") != "0"
+
+
+def _al16(t) -> bool:
+    return t is None or (t.data_ptr() % 16 == 0 and (t.dim() < 2 or t.stride(0) % 4 == 0))
+
+
+def spmm_operand(op: "SparseOperand", X, Y, *, heads=1, vals=None, eid=None, self_x=None,
+                 mask=None, bias=None) -> "SparseOperand":
+    """The operand form gnn_spmm should run on: the degree-sorted one
+    (``by_degree``) where its group-per-row tail applies — topology or
+    multiplicity weights only, K <= 64 in float4 lanes — else ``op``."""
+    K = int(X.shape[1])
+    if (not SPMM_SORT or SPMM_SHORT_MAX <= 0 or heads != 1 or vals is not None
+            or eid is not None or (op._vals is not None and not op.mult) or op.nnz == 0
+            or K > 64 or K % 4 or not all(_al16(t) for t in (X, Y, self_x, mask, bias))):
+        return op
+    return op.by_degree()
+
+
+# GNN_SPMM_PACK=0 keeps multiplicity-weighted operands in the float form
+SPMM_PACK = os.environ.get("GNN_SPMM_PACK", "1") != "0"
 
 
 class SparseOperand:
     """One device sparse matrix in CSR layout (a graph's CSR, or its CSC which
-    is the CSR of the transpose), plus cached SpMM schedules."""
+    is the CSR of the transpose), plus cached SpMM schedules.
 
-    def __init__(self, num_rows, num_cols, offsets, cols, vals=None, eid=None, deg_offsets=None):
+    ``mult=True`` marks ``vals`` as integer multiplicities (the coalesced
+    multigraph forms); such an operand is stored packed when it fits — column
+    id in the low ``col_bits`` bits, multiplicity above (gnn_csr_pack_weights)
+    — one 4-byte word per edge instead of 8.  ``cols`` / ``vals`` then
+    unpack on demand (setup-time consumers); the SpMM reads the packed words."""
+
+    def __init__(self, num_rows, num_cols, offsets, cols, vals=None, eid=None, deg_offsets=None,
+                 mult: bool = False, row_ids=None):
         self.num_rows = int(num_rows)
         self.num_cols = int(num_cols)
         self.nnz = int(cols.numel())
         self.offsets = offsets
-        self.cols = cols
-        self.vals = vals
+        self._cols = cols
+        self._vals = vals
         self.eid = eid
         self.deg_offsets = deg_offsets
+        self.mult = bool(mult)
+        self.row_ids = row_ids  # permuted operand: row i -> output row row_ids[i]
+        self._sorted = None
+        self.col_bits = 0
+        self.packed = None
+        self._plain = None
         self._plans = {}
+        if mult and vals is not None and eid is None and SPMM_PACK and self.nnz > 0:
+            self._try_pack()
+
+    def _try_pack(self):
+        bits = max(1, (self.num_cols - 1).bit_length())
+        if bits > 24:  # < 256 per word: hub pairs would expand too much
+            return
+        maxw = (1 << (32 - bits)) - 1
+        cols, vals, offsets = self._cols, self._vals, self.offsets
+        reps = torch.div(vals.to(torch.int64) + (maxw - 1), maxw, rounding_mode="floor")
+        reps.clamp_(min=1)
+        if int(reps.max().item()) > 1:
+            # a multiplicity above the word's weight field (hub pairs of a
+            # power-law multigraph: Reddit's top pair repeats ~2e5 times) is
+            # split into several entries of the same column; the SpMM sums
+            # them (same value, fp32 rounding of the split product)
+            n2 = int(reps.sum().item())
+            idx = torch.repeat_interleave(torch.arange(self.nnz, device=cols.device), reps,
+                                          output_size=n2)
+            first = torch.cumsum(reps, 0) - reps
+            pos = torch.arange(n2, device=cols.device) - first[idx]
+            r = reps[idx]
+            w = torch.where(pos < r - 1, torch.full_like(pos, maxw),
+                            vals[idx].to(torch.int64) - maxw * (r - 1))
+            extra = torch.zeros(self.nnz + 1, dtype=torch.int64, device=cols.device)
+            torch.cumsum(reps - 1, 0, out=extra[1:])
+            offsets = offsets + extra[offsets]
+            cols, vals = cols[idx].contiguous(), w.to(torch.float32)
+            del idx, first, pos, r, w, extra
+        lib = _lib.lib()
+        dev = self.device
+        out = torch.empty(cols.numel(), dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            ws = _lib.workspace(lib.gnn_csr_pack_weights_workspace(), dev)
+            rc = lib.gnn_csr_pack_weights(cols.numel(), cols.data_ptr(), vals.data_ptr(),
+                                          bits, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                          _lib.stream_handle(dev))
+        if rc != 0:  # not representable: keep the float form
+            return
+        self.packed, self.col_bits, self.offsets = out, bits, offsets
+        self.nnz = int(out.numel())
+        self._cols = self._vals = None
+
+    def by_degree(self) -> "SparseOperand":
+        """Degree-sorted form for gnn_spmm (cached): rows longest-first with
+        ``row_ids`` mapping each back to its output row; the nnz-split kernel
+        then covers only the long-row prefix and the group-per-row kernel the
+        contiguous, length-ordered tail (SPMM_SHORT_MAX).  Same entries per
+        row, same order within a row: results are bit-identical."""
+        if self.row_ids is not None:
+            return self
+        if self._sorted is None:
+            dev = self.device
+            deg = self.offsets[1:] - self.offsets[:-1]
+            order = torch.sort(deg, descending=True, stable=True).indices
+            sdeg = deg[order]
+            off = torch.zeros(self.num_rows + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(sdeg, 0, out=off[1:])
+            # shift[i] = old start - new start of sorted row i: entry j of the
+            # new array comes from j + shift[row(j)] (gathered in slabs of rows
+            # to bound the int64 temporaries)
+            shift = self.offsets[order] - off[:-1]
+            words = self.packed if self.packed is not None else self._cols
+            cols = torch.empty_like(words)
+            vals = (torch.empty_like(self._vals) if (self.packed is None and self._vals is not None)
+                    else None)
+            slab = int(os.environ.get("GNN_SORT_SLAB", 1 << 24))
+            r0 = 0
+            while r0 < self.num_rows:
+                e0 = int(off[r0].item())
+                if e0 >= self.nnz:  # only empty rows left
+                    break
+                e1 = min(self.nnz, e0 + slab)
+                r1 = int(torch.searchsorted(off, e1, right=True).item()) - 1
+                r1 = min(max(r1, r0 + 1), self.num_rows)
+                e1 = int(off[r1].item())
+                row = torch.repeat_interleave(torch.arange(r0, r1, device=dev), sdeg[r0:r1],
+                                              output_size=e1 - e0)
+                src = torch.arange(e0, e1, device=dev) + shift[row]
+                cols[e0:e1] = words[src]
+                if vals is not None:
+                    vals[e0:e1] = self._vals[src]
+                del row, src
+                r0 = r1
+            del shift
+            deg_off = self.deg_offsets if self.deg_offsets is not None else self.offsets
+            if self.packed is not None:
+                op = SparseOperand(self.num_rows, self.num_cols, off, cols,
+                                   deg_offsets=deg_off, row_ids=order.to(torch.int32))
+                op.packed, op.col_bits, op._cols, op.mult = op._cols, self.col_bits, None, True
+            else:
+                op = SparseOperand(self.num_rows, self.num_cols, off, cols, vals=vals,
+                                   deg_offsets=deg_off, row_ids=order.to(torch.int32))
+            self._sorted = op
+        return self._sorted
+
+    def entries(self, e0: int = 0, e1: int | None = None):
+        """(cols, vals) of entries [e0, e1) in plain form (vals None if none)."""
+        e1 = self.nnz if e1 is None else e1
+        if self.packed is None:
+            v = self._vals[e0:e1] if self._vals is not None else None
+            return self._cols[e0:e1], v
+        pk = self.packed[e0:e1]
+        w = torch.bitwise_right_shift(pk, self.col_bits) & ((1 << (32 - self.col_bits)) - 1)
+        return pk & ((1 << self.col_bits) - 1), w.to(torch.float32)
+
+    @property
+    def cols(self) -> torch.Tensor:
+        if self.packed is None:
+            return self._cols
+        return self.packed & ((1 << self.col_bits) - 1)
+
+    @property
+    def vals(self):
+        if self.packed is None:
+            return self._vals
+        w = torch.bitwise_right_shift(self.packed, self.col_bits) & ((1 << (32 - self.col_bits)) - 1)
+        return w.to(torch.float32)
 
     @property
     def device(self):
@@ -105,7 +261,21 @@ class SparseOperand:
         v.num_cols = self.num_cols
         v.nnz = self.nnz
         v.offsets = self.offsets.data_ptr()
-        v.cols = self.cols.data_ptr() if self.nnz else None
+        v.row_ids = self.row_ids.data_ptr() if self.row_ids is not None else None
+        if self.packed is not None and vals is None:
+            # packed multiplicities: the SpMM decodes column + weight per word
+            v.cols = self.packed.data_ptr()
+            v.col_bits = self.col_bits
+            v.vals = None
+            v.eid = None
+            v.deg_offsets = self.deg_offsets.data_ptr() if self.deg_offsets is not None else None
+            return v
+        if self.packed is not None:  # explicit edge values over a packed operand
+            if self._plain is None:
+                self._plain = self.cols
+            v.cols = self._plain.data_ptr()
+        else:
+            v.cols = self.cols.data_ptr() if self.nnz else None
         vv = vals if vals is not None else self.vals
         v.vals = vv.data_ptr() if vv is not None else None
         ee = eid if eid is not None else self.eid
@@ -148,9 +318,9 @@ class SparseOperand:
         return self.plan(edges_per_warp, short_max=SPMM_SHORT_MAX)
 
     def nbytes(self) -> int:
-        n = self.offsets.numel() * 8 + self.cols.numel() * 4
-        if self.vals is not None:
-            n += self.vals.numel() * self.vals.element_size()
+        n = self.offsets.numel() * 8 + self.nnz * 4
+        if self._vals is not None:
+            n += self._vals.numel() * self._vals.element_size()
         if self.eid is not None:
             n += self.eid.numel() * 4
         for _, buf in self._plans.values():
@@ -277,7 +447,7 @@ class CsrGraph:
             del s_off, s_cols
             object.__setattr__(self, "_csr_co", SparseOperand(
                 self.num_vertices, self.num_vertices, off, cols, vals=mult,
-                deg_offsets=self.d_offsets))
+                deg_offsets=self.d_offsets, mult=True))
         return self._csr_co
 
     def csc_coalesced(self) -> SparseOperand:
@@ -286,7 +456,7 @@ class CsrGraph:
             off, cols, mult = _coalesce(self.num_vertices, csc.offsets, csc.cols)
             object.__setattr__(self, "_csc_co", SparseOperand(
                 self.num_vertices, self.num_vertices, off, cols, vals=mult,
-                deg_offsets=csc.offsets))
+                deg_offsets=csc.offsets, mult=True))
         return self._csc_co
 
     def operand(self, kind: str) -> SparseOperand:

@@ -13,7 +13,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from .graph import SparseOperand
+from .graph import SparseOperand, spmm_operand
 
 
 class SpmmCall:
@@ -24,6 +24,8 @@ class SpmmCall:
         self.dev = X.device
         self.K = int(X.shape[1])
         assert Y.shape[1] == self.K and X.stride(1) == 1 and Y.stride(1) == 1
+        op = spmm_operand(op, X, Y, heads=heads, vals=vals, eid=eid, self_x=self_x, mask=mask,
+                          bias=bias)
         self.view = op.view(vals=vals, eid=eid)
         self.plan = op.spmm_plan(edges_per_warp)
         self.epi = _lib.Epilogue()

@@ -17,7 +17,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from .graph import CsrGraph, SparseOperand
+from .graph import CsrGraph, SparseOperand, spmm_operand
 
 
 def _check_features(X: torch.Tensor, rows: int, what: str):
@@ -43,9 +43,11 @@ def spmm_raw(op: SparseOperand, X: torch.Tensor, *, heads: int = 1, vals=None, e
         out = torch.empty(op.num_rows, K, dtype=torch.float32, device=dev)
     else:
         _check_features(out, op.num_rows, "spmm output")
-    view = op.view(vals=vals, eid=eid)
     if plan is None:
+        op = spmm_operand(op, X, out, heads=heads, vals=vals, eid=eid, self_x=self_x, mask=mask,
+                          bias=bias)
         plan = op.spmm_plan()
+    view = op.view(vals=vals, eid=eid)
     epi = _lib.Epilogue()
     epi.flags = flags
     epi.self_scale = float(self_scale)

@@ -60,10 +60,10 @@ def test_status_mapping_to_reference_exceptions():
 
 def test_struct_layouts_match_header():
     # 8 x 8-byte fields
-    assert ctypes.sizeof(_lib.CsrView) == 64
+    assert ctypes.sizeof(_lib.CsrView) == 80  # 8 x 8 + col_bits + reserved + row_ids
     # uint32 + float + 6 pointer/int64 fields
     assert ctypes.sizeof(_lib.Epilogue) == 8 + 6 * 8
-    assert ctypes.sizeof(_lib.SpmmPlan) == 13 * 8
+    assert ctypes.sizeof(_lib.SpmmPlan) == 14 * 8
     assert ctypes.sizeof(_lib.EdgeScores) == 4 * 8
 
 

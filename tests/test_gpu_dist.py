@@ -86,7 +86,7 @@ def test_remap_kernel_matches_host(env):
 def test_peer_mode_virtual_ranks_match_oracle(env, P):
     """Peer mode (gnn_spmm_peer reads every rank's block in place, no
     all-gather) with P virtual ranks on one GPU: same gradients as the
-    single-process oracle and bit-identical to the all-gather mode."""
+    single-process oracle and the all-gather mode."""
     from paper_2605_29346_b200.dist import (DistGCNTrainer, LocalExchange, RowPartition,
                                             bind_virtual_peers, step_virtual)
 
@@ -112,7 +112,9 @@ def test_peer_mode_virtual_ranks_match_oracle(env, P):
         for k, gv in t.grads().items():
             ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
             assert ok, (P, k, worst)
-            assert torch.equal(gv, gt.grads()[k]), k  # same kernels, same summation order
+            # the gather mode aggregates over the degree-sorted operands (other
+            # fp32 summation order on long rows), so equal to rounding only
+            assert torch.allclose(gv, gt.grads()[k], rtol=1e-4, atol=1e-7), k
 
 
 @pytest.mark.parametrize("P", [2, 3])

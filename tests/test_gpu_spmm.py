@@ -181,3 +181,142 @@ def test_reddit_shape_spmmv_properties(gb):
             ref = Xh[seg].astype(np.float64).sum(0) / len(seg)
             ra = np.abs(Xh[seg]).astype(np.float64).sum(0) / len(seg)
             assert np.all(np.abs(Y[r] - ref) <= RTOL * np.maximum(np.abs(ref), ra)), (r, coalesced)
+
+
+@pytest.mark.parametrize("gname", ["cora_pl", "pl_10k", "mega"])
+@pytest.mark.parametrize("K", [4, 16, 32, 64, 130])
+def test_packed_multiplicity_operand_bit_identical(gb, graphs, gname, K):
+    """The coalesced operands are stored packed (column | multiplicity <<
+    col_bits, gnn_csr_pack_weights); the SpMM over the packed words equals the
+    SpMM over the float-multiplicity form bit for bit (same order, same
+    weights), with every epilogue path."""
+    from paper_2605_29346_b200 import _lib
+    from paper_2605_29346_b200.graph import SparseOperand
+    from paper_2605_29346_b200.ops import spmm_raw
+
+    g = graphs[gname]
+    for co in (g.csr_coalesced(), g.csc_coalesced()):
+        assert co.packed is not None and co.col_bits == max(1, (g.num_vertices - 1).bit_length())
+        cols, vals = co.entries()
+        plain = SparseOperand(co.num_rows, co.num_cols, co.offsets, cols, vals=vals,
+                              deg_offsets=co.deg_offsets)
+        assert plain.packed is None
+        rng = np.random.default_rng(K)
+        X = torch.from_numpy(rng.uniform(-1, 1, (g.num_vertices, K)).astype(np.float32)).cuda()
+        b = torch.from_numpy(rng.uniform(-1, 1, K).astype(np.float32)).cuda()
+        for flags in (0, _lib.EPI_NORM | _lib.EPI_BIAS | _lib.EPI_RELU):
+            Ys = []
+            for op in (co, plain):  # row order for both (a given plan skips the sorted form)
+                Ys.append(spmm_raw(op, X, plan=op.spmm_plan(), flags=flags, bias=b))
+            assert torch.equal(Ys[0], Ys[1]), (gname, K, flags)
+
+
+def test_pack_weights_range_checks(gb):
+    from paper_2605_29346_b200 import _lib
+
+    lib = _lib.lib()
+    ws = _lib.workspace(lib.gnn_csr_pack_weights_workspace(), torch.device("cuda"))
+    out = torch.empty(3, dtype=torch.int32, device="cuda")
+
+    def pack(cols, w, bits):
+        c = torch.tensor(cols, dtype=torch.int32, device="cuda")
+        v = torch.tensor(w, dtype=torch.float32, device="cuda")
+        return lib.gnn_csr_pack_weights(3, c.data_ptr(), v.data_ptr(), bits, out.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), None)
+
+    assert pack([0, 5, 7], [1, 2, 3], 3) == 0
+    assert out.tolist() == [0 | 1 << 3, 5 | 2 << 3, 7 | 3 << 3]
+    assert pack([0, 8, 7], [1, 2, 3], 3) == _lib.GNN_ERR_RANGE      # column needs 4 bits
+    assert pack([0, 1, 2], [1, 2.5, 3], 3) == _lib.GNN_ERR_RANGE    # not an integer weight
+    assert pack([0, 1, 2], [1, 2, 1 << 29], 3) == _lib.GNN_ERR_RANGE  # weight overflows 29 bits
+    assert pack([0, 1, 2], [1, -1, 3], 3) == _lib.GNN_ERR_RANGE
+    assert pack([0, 1, 2], [1, 2, 3], 0) == _lib.GNN_ERR_INVALID_ARGUMENT
+
+
+def test_packed_operand_splits_large_multiplicities(gb):
+    """A multiplicity above the packed word's weight field (2^(32-col_bits)-1)
+    is split into several entries of the same column; the SpMM result stays
+    within the A.8 tolerance of the oracle."""
+    V = 1 << 20  # 20 column bits -> weights up to 4095 per word
+    rng = np.random.default_rng(3)
+    src = np.concatenate([np.zeros(10_000, np.int64), np.full(5000, 7), rng.integers(0, V, 50_000)])
+    dst = np.concatenate([np.full(10_000, 5), np.full(5000, 5), rng.integers(0, V, 50_000)])
+    g = gb.csr_from_edges(V, src, dst)
+    co = g.csr_coalesced()
+    assert co.packed is not None and co.col_bits == 20
+    cols, vals = co.entries()
+    o = co.offsets.cpu().numpy()
+    c0, w0 = cols[o[0]:o[1]].cpu().numpy(), vals[o[0]:o[1]].cpu().numpy()
+    assert sorted(w0[c0 == 5].tolist()) == [1810.0, 4095.0, 4095.0]  # 10000 = 2*4095 + 1810
+    c7, w7 = cols[o[7]:o[8]].cpu().numpy(), vals[o[7]:o[8]].cpu().numpy()
+    assert sorted(w7[c7 == 5].tolist()) == [905.0, 4095.0]
+    off, tgt = g.offsets, g.targets
+    X = rng.uniform(-1, 1, (V, 16)).astype(np.float32)
+    Y = gb.spmmv(g, torch.from_numpy(X).cuda(), norm=True, coalesced=True)
+    assert_close(Y, oo.spmm(off, tgt, X, norm=True), oo.spmm(off, tgt, np.abs(X), norm=True),
+                 "split multiplicities")
+    ct = g.csc_coalesced()
+    t_off, t_rows, _ = og.transpose(V, V, off, tgt)
+    Yt = gb.spmmv(g, torch.from_numpy(X).cuda(), transpose=True, coalesced=True)
+    assert_close(Yt, oo.spmm(t_off, t_rows, X), oo.spmm(t_off, t_rows, np.abs(X)), "csc split")
+    assert ct.packed is not None
+
+
+@pytest.mark.parametrize("gname", ["cora_pl", "pl_10k", "ur_5k", "mega"])
+@pytest.mark.parametrize("K", [4, 16, 32, 64])
+def test_degree_sorted_operand_matches_row_order(gb, graphs, gname, K):
+    """gnn_spmm over the degree-sorted operand (rows longest-first, row_ids
+    back to output rows; the nnz-split kernel covers only the long-row prefix)
+    equals the SpMM over the operand in row order — bit for bit on the short
+    tail, to fp32 rounding on the long rows — for every epilogue (per-row
+    inputs indexed by output row)."""
+    from paper_2605_29346_b200 import _lib
+    from paper_2605_29346_b200.graph import SPMM_SHORT_MAX
+    from paper_2605_29346_b200.ops import spmm_raw
+
+    g = graphs[gname]
+    V = g.num_vertices
+    rng = np.random.default_rng(K + 7)
+    X = torch.from_numpy(rng.uniform(-1, 1, (V, K)).astype(np.float32)).cuda()
+    S = torch.from_numpy(rng.uniform(-1, 1, (V, K)).astype(np.float32)).cuda()
+    M = torch.from_numpy(rng.uniform(-1, 1, (V, K)).astype(np.float32)).cuda()
+    b = torch.from_numpy(rng.uniform(-1, 1, K).astype(np.float32)).cuda()
+    N_, S_, B_, R_, M_, P_ = (_lib.EPI_NORM, _lib.EPI_SELF, _lib.EPI_BIAS, _lib.EPI_RELU,
+                              _lib.EPI_MASK, _lib.EPI_POSTNORM)
+    for op in (g.csr(), g.csc(), g.csr_coalesced(), g.csc_coalesced()):
+        so = op.by_degree()
+        assert so.row_ids is not None and so.nnz == op.nnz
+        plan = so.spmm_plan()
+        long_rows = int((so.offsets[1:] - so.offsets[:-1] > SPMM_SHORT_MAX).sum().item())
+        assert plan.main_nnz == int(so.offsets[long_rows].item())
+        deg = op.deg_offsets if op.deg_offsets is not None else op.offsets
+        for flags in (0, N_ | B_ | R_, S_ | M_, N_ | S_ | P_):
+            kw = dict(flags=flags, bias=b, self_x=S, self_scale=0.5, mask=M,
+                      post_deg_offsets=g.d_offsets)
+            Y0 = spmm_raw(op, X, plan=op.spmm_plan(), **kw)  # row order (plan given: no sorting)
+            Y1 = spmm_raw(so, X, plan=plan, **kw)
+            # the long rows' fp32 partial-sum order follows their position in
+            # the edge array (warp ranges), so equal up to rounding only
+            tol = 1e-5 * (Y0.abs() + Y0.abs().max() * 1e-2)
+            assert bool(((Y0 - Y1).abs() <= tol).all()), (gname, K, flags)
+            # rows of the short tail run the same group-per-row kernel: bit-identical
+            short = (op.offsets[1:] - op.offsets[:-1]) <= SPMM_SHORT_MAX
+            assert torch.equal(Y0[short], Y1[short]), (gname, K, flags)
+        ref_deg = deg  # NORM of the sorted operand uses output-row degrees
+        assert so.deg_offsets is ref_deg or torch.equal(so.deg_offsets, ref_deg)
+
+
+def test_degree_sorted_plan_needs_short_kernel(gb, graphs):
+    """A sorted operand's plan stops the nnz-split range at the short tail, so
+    a call that cannot use the short-row kernel (K > 64) is refused."""
+    from paper_2605_29346_b200.ops import spmm_raw
+
+    g = graphs["pl_10k"]
+    so = g.csr().by_degree()
+    plan = so.spmm_plan()
+    assert plan.main_nnz < so.nnz
+    X = torch.ones(g.num_vertices, 128, device="cuda")
+    with pytest.raises(ValueError):
+        spmm_raw(so, X, plan=plan)
+    Y = spmm_raw(g.csr(), X)  # the row-order operand still runs at K=128
+    assert torch.equal(Y[:, 0].cpu(), torch.from_numpy(np.diff(g.offsets).astype(np.float32)))
