@@ -412,6 +412,14 @@ def run_ours(args, rank, world):
     nnz32 = g.operand("csr_coalesced" if "csr" not in k32 else "csr").nnz
     hier32 = max(spmm_bytes(V, E, 32) / (hbm_peak * 1e9), 4 * nnz32 * 32 / (l2_gbs * 1e9)) * 1e3
 
+    # width-16 gathers: one 64-byte feature row per stored (coalesced) entry
+    gather16 = 4 * Hd * g.csr_coalesced().nnz if args.layout == "coalesced" else 4 * Hd * E
+    traffic16 = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                         "r1_spmm16_traffic.json")
+    if os.path.exists(tpath) and args.layout == "coalesced":
+        with open(tpath) as f:
+            traffic16 = json.load(f)["traffic_bytes_per_launch"]
     # BASELINE.md analytic footprint: canonical CSR+CSC (int64 offsets, int32 ids),
     # X, and the epoch's [V,hidden] activations/gradients
     analytic = (g.d_offsets.numel() * 8 + E * 4) * 2 + V * F * 4 + V * 6 * Hd * 4
@@ -445,8 +453,14 @@ def run_ours(args, rank, world):
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"kernel": "spmm width-16 (4 per epoch, avg, timed in-epoch)", "bound": "hbm",
                      "achieved": round(ach16, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(ach16 / hbm_peak, 4), "traffic": None,
-                     "bytes_per_launch": b16, "peak_source": peak_src},
+                     "frac": round(ach16 / hbm_peak, 4), "traffic": traffic16,
+                     "traffic_source": "profiles/r1_spmm16_traffic.json (ncu --set full)",
+                     "bytes_per_launch": b16, "peak_source": peak_src,
+                     # the binding unit is the L2->SM gather return, not HBM
+                     "gather_bytes_per_launch": gather16,
+                     "gather_tbs": round(gather16 / (avg_spmm * 1e-3) / 1e12, 2),
+                     "l2_read_tbs": round(l2_gbs / 1e3, 2),
+                     "gather_frac_of_l2_roof": round(gather16 / (avg_spmm * 1e-3) / (l2_gbs * 1e9), 4)},
         "spmmv_k32": {"ms": t32, "gbs": round(ach32, 1), "frac": round(ach32 / hbm_peak, 4),
                       "hierarchical_bound_ms": round(hier32, 4),
                       "hierarchical_frac": round(hier32 / t32, 4), "l2_read_gbs": round(l2_gbs, 1),
