@@ -770,13 +770,184 @@ __global__ void gcn_head_reduce_kernel(int64_t nb, int din, int C, const float *
   }
 }
 
+// Thread-per-row form (din <= 32): each thread owns one row end to end —
+// logits (W, b broadcast from shared memory), softmax-CE, dz, dP = dz W^T *
+// rowscale — with no cross-lane traffic; the CTA then forms its dW / db
+// partials from the staged P and dz tiles in fixed row order.  The warp-per-
+// row kernel above serialises ~150 dependent shuffle/FMA steps per row on
+// 12 warps per SM; here 256 independent rows per CTA keep every lane busy.
+constexpr int kHeadRowsPerCta = 256;
+
+template <int DIN, int CM>
+__global__ void __launch_bounds__(kHeadRowsPerCta, 2) gcn_head_rows_kernel(
+    int64_t M, int din, int C, const float *__restrict__ P, int64_t ldp,
+    const float *__restrict__ W, const float *__restrict__ b, const int64_t *__restrict__ labels,
+    const int64_t *__restrict__ deg_offsets, float scale, float *dP, int64_t lddp,
+    float *partials, double *lpart) {
+  constexpr int T = kHeadRowsPerCta;
+  constexpr int C4 = CM / 4;
+  constexpr int LDD = CM + 4;            // dz tile row stride (16-byte rows)
+  extern __shared__ __align__(16) float hsm[];
+  float *Ws = hsm;                       // [DIN][CM] zero padded
+  float *bs = Ws + DIN * CM;             // [CM]
+  float *Ps = bs + CM;                   // [T][DIN + 1]
+  float *Ds = Ps + T * (DIN + 1);        // [T][LDD]
+  __shared__ double lred[T / 32];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < DIN * CM; i += T) {
+    const int k = i / CM, c = i % CM;
+    Ws[i] = (k < din && c < C) ? W[k * C + c] : 0.f;
+  }
+  for (int c = tid; c < CM; c += T) bs[c] = c < C ? b[c] : 0.f;
+  __syncthreads();
+  const float4 *W4 = reinterpret_cast<const float4 *>(Ws);
+  const int64_t r = (int64_t)blockIdx.x * T + tid;
+  const bool valid = r < M;
+  float p[DIN];
+#pragma unroll
+  for (int k = 0; k < DIN; ++k) p[k] = (valid && k < din) ? __ldg(P + r * ldp + k) : 0.f;
+  float z[CM];
+#pragma unroll
+  for (int c = 0; c < CM; ++c) z[c] = bs[c];
+#pragma unroll
+  for (int k = 0; k < DIN; ++k)
+#pragma unroll
+    for (int q = 0; q < C4; ++q) {
+      const float4 w = W4[k * C4 + q];  // broadcast: every lane reads the same word
+      z[4 * q] = fmaf(p[k], w.x, z[4 * q]);
+      z[4 * q + 1] = fmaf(p[k], w.y, z[4 * q + 1]);
+      z[4 * q + 2] = fmaf(p[k], w.z, z[4 * q + 2]);
+      z[4 * q + 3] = fmaf(p[k], w.w, z[4 * q + 3]);
+    }
+  const int y = valid ? (int)__ldg(labels + r) : -1;
+  float mx = -INFINITY, zy = 0.f;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) {
+    if (c < C) mx = fmaxf(mx, z[c]);
+    if (c == y) zy = z[c];
+  }
+  float se = 0.f;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) {
+    z[c] = c < C ? __expf(z[c] - mx) : 0.f;  // z now holds e_c
+    se += z[c];
+  }
+  const float inv = 1.f / se;
+  double lrow = 0.0;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) z[c] = valid ? (z[c] * inv - (c == y ? 1.f : 0.f)) * scale : 0.f;
+  float4 *D4 = reinterpret_cast<float4 *>(Ds + tid * LDD);
+#pragma unroll
+  for (int q = 0; q < C4; ++q) D4[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
+  if (valid) lrow = (double)(mx + logf(se) - zy);
+  float rs = 1.f;
+  if (valid && deg_offsets) {
+    const int64_t dg = __ldg(deg_offsets + r + 1) - __ldg(deg_offsets + r);
+    rs = dg > 0 ? 1.f / (float)dg : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < DIN; ++k) {
+    Ps[tid * (DIN + 1) + k] = p[k];
+    float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+    for (int q = 0; q < C4; ++q) {
+      const float4 w = W4[k * C4 + q];
+      t0 = fmaf(z[4 * q], w.x, t0);
+      t1 = fmaf(z[4 * q + 1], w.y, t1);
+      t0 = fmaf(z[4 * q + 2], w.z, t0);
+      t1 = fmaf(z[4 * q + 3], w.w, t1);
+    }
+    if (valid && k < din) dP[r * lddp + k] = (t0 + t1) * rs;
+  }
+  // loss: fixed-order block reduction (warp butterfly, then warps in order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lrow += __shfl_xor_sync(kFull, lrow, o);
+  if ((tid & 31) == 0) lred[tid >> 5] = lrow;
+  __syncthreads();
+  // dW[k][4q..4q+3] = sum_i P[i][k] dz[i][4q..]; db (item k == din) = sum_i dz[i][4q..]
+  const int64_t NPF = (int64_t)din * C + C;
+  float *out = partials + (int64_t)blockIdx.x * NPF;
+  const int items = (din + 1) * C4;
+  for (int it = tid; it < items; it += T) {
+    const int k = it / C4, q = it % C4;
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < din) {
+      for (int i = 0; i < T; ++i) {
+        const float pk = Ps[i * (DIN + 1) + k];
+        const float4 d = reinterpret_cast<const float4 *>(Ds + i * LDD)[q];
+        t.x = fmaf(pk, d.x, t.x);
+        t.y = fmaf(pk, d.y, t.y);
+        t.z = fmaf(pk, d.z, t.z);
+        t.w = fmaf(pk, d.w, t.w);
+      }
+    } else {
+      for (int i = 0; i < T; ++i) {
+        const float4 d = reinterpret_cast<const float4 *>(Ds + i * LDD)[q];
+        t.x += d.x;
+        t.y += d.y;
+        t.z += d.z;
+        t.w += d.w;
+      }
+    }
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * q + j;
+      if (c < C) out[(int64_t)k * C + c] = tv[j];
+    }
+  }
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < T / 32; ++w2) t += lred[w2];
+    lpart[blockIdx.x] = t;
+  }
+}
+
+template <int DIN, int CM>
+size_t head_rows_smem() {
+  return sizeof(float) * (size_t)(DIN * CM + CM + kHeadRowsPerCta * (DIN + 1) +
+                                  kHeadRowsPerCta * (CM + 4));
+}
+
+// warp per output: lanes stride the CTA partials, fixed-order butterfly
+__global__ void gcn_head_reduce_warp_kernel(int64_t nb, int din, int C,
+                                            const float *__restrict__ partials,
+                                            const double *__restrict__ lpart, float *dW, float *db,
+                                            float *loss, float loss_scale) {
+  const int64_t NPF = (int64_t)din * C + C;
+  const int lane = (int)lane_id();
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i <= NPF;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (i < NPF) {
+      float t = 0.f;
+      for (int64_t b2 = lane; b2 < nb; b2 += 32) t += partials[b2 * NPF + i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+      if (lane == 0) {
+        if (i < (int64_t)din * C)
+          dW[i] = t;
+        else
+          db[i - (int64_t)din * C] = t;
+      }
+    } else {
+      double t = 0.0;
+      for (int64_t b2 = lane; b2 < nb; b2 += 32) t += lpart[b2];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+      if (lane == 0) *loss = (float)(t * (double)loss_scale);
+    }
+  }
+}
+
 }  // namespace
 }  // namespace gnn
 
 extern "C" {
 
 size_t gnn_gcn_head_workspace(int64_t M, int64_t Din, int64_t C) {
-  const int64_t nb = ceil_div(M > 0 ? M : 1, (int64_t)kHeadWarps * kHeadRowsPerWarp);
+  const int64_t nb1 = ceil_div(M > 0 ? M : 1, (int64_t)kHeadWarps * kHeadRowsPerWarp);
+  const int64_t nb2 = ceil_div(M > 0 ? M : 1, (int64_t)kHeadRowsPerCta);
+  const int64_t nb = nb1 > nb2 ? nb1 : nb2;
   return sizeof(float) * (size_t)head_float_slots(nb, Din, C) + sizeof(double) * (size_t)nb + 512;
 }
 
@@ -790,10 +961,44 @@ int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64
     return GNN_ERR_INVALID_ARGUMENT;
   if (ws_bytes < gnn_gcn_head_workspace(M, Din, C)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
-  const int64_t nb = ceil_div(M, (int64_t)kHeadWarps * kHeadRowsPerWarp);
-  float *partials = static_cast<float *>(ws);
-  double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
   const float scale = grad_scale;
+  float *partials = static_cast<float *>(ws);
+  static const bool rows_form = [] {
+    const char *e = getenv("GNN_HEAD_ROWS");
+    return !(e && e[0] == '0');
+  }();
+  if (Din <= 32 && rows_form) {  // thread-per-row form
+    const int64_t nb = ceil_div(M, (int64_t)kHeadRowsPerCta);
+    double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
+#define GNN_HEAD_ROWS(DN, CMX)                                                                  \
+  do {                                                                                          \
+    const size_t sm = head_rows_smem<DN, CMX>();                                                \
+    GNN_CUDA_TRY(cudaFuncSetAttribute(gcn_head_rows_kernel<DN, CMX>,                            \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
+    gcn_head_rows_kernel<DN, CMX><<<(unsigned)nb, kHeadRowsPerCta, sm, st>>>(                   \
+        M, (int)Din, (int)C, P, ldp, W, b, labels, deg_offsets, scale, dP, lddp, partials, lpart); \
+  } while (0)
+    if (Din <= 16) {
+      if (C <= 16) GNN_HEAD_ROWS(16, 16);
+      else if (C <= 32) GNN_HEAD_ROWS(16, 32);
+      else if (C <= 48) GNN_HEAD_ROWS(16, 48);
+      else GNN_HEAD_ROWS(16, 64);
+    } else {
+      if (C <= 16) GNN_HEAD_ROWS(32, 16);
+      else if (C <= 32) GNN_HEAD_ROWS(32, 32);
+      else if (C <= 48) GNN_HEAD_ROWS(32, 48);
+      else GNN_HEAD_ROWS(32, 64);
+    }
+#undef GNN_HEAD_ROWS
+    GNN_LAUNCH_CHECK();
+    const int64_t outs = Din * C + C + 1;
+    gcn_head_reduce_warp_kernel<<<(unsigned)ceil_div(outs * 32, 256), 256, 0, st>>>(
+        nb, (int)Din, (int)C, partials, lpart, dW, db, loss, grad_scale);
+    GNN_LAUNCH_CHECK();
+    return GNN_OK;
+  }
+  const int64_t nb = ceil_div(M, (int64_t)kHeadWarps * kHeadRowsPerWarp);
+  double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
 #define GNN_HEAD(DN)                                                                            \
   gcn_head_kernel<DN><<<(unsigned)nb, 128, 0, st>>>(M, (int)Din, (int)C, P, ldp, W, b, labels, \
                                                     deg_offsets, scale, dP, lddp, partials, lpart)

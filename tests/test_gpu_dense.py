@@ -107,3 +107,48 @@ def test_weight_gradient_gemm_tn_shapes(M, N, K):
     ra = np.abs(A).astype(np.float64).T @ np.abs(B).astype(np.float64)
     ok, worst = oo.close(C.cpu().numpy(), ref, ra)
     assert ok, worst
+
+
+@pytest.mark.parametrize("M,Din,C", [(1, 16, 7), (1000, 16, 41), (4097, 16, 16), (777, 32, 47),
+                                     (300, 8, 64), (513, 24, 33), (2000, 64, 41)])
+@pytest.mark.parametrize("with_deg", [False, True])
+def test_gcn_head_matches_float64(gb, M, Din, C, with_deg):
+    """Fused output layer (gnn_gcn_head_scaled): loss, dP (with the 1/deg
+    row scale), dW, db against a float64 torch statement of softmax-CE;
+    tolerance 1e-5 of the quantity's own absolute scale (Appendix A.8)."""
+    from paper_2605_29346_b200 import _lib
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(M + Din + C)
+    P = torch.from_numpy(rng.uniform(-2, 2, (M, Din)).astype(np.float32)).cuda()
+    W = torch.from_numpy(rng.uniform(-1, 1, (Din, C)).astype(np.float32)).cuda()
+    b = torch.from_numpy(rng.uniform(-1, 1, C).astype(np.float32)).cuda()
+    y = torch.from_numpy(rng.integers(0, C, M)).cuda()
+    deg = torch.from_numpy(np.concatenate([[0], np.cumsum(rng.integers(0, 5, M))])).cuda()
+    scale = 1.0 / M
+    dP = torch.empty(M, Din, device="cuda")
+    dW = torch.empty(Din, C, device="cuda")
+    db = torch.empty(C, device="cuda")
+    loss = torch.empty(1, device="cuda")
+    ws = _lib.workspace(lib.gnn_gcn_head_workspace(M, Din, C), torch.device("cuda"))
+    _lib.check(lib.gnn_gcn_head_scaled(M, Din, C, P.data_ptr(), Din, W.data_ptr(), b.data_ptr(),
+                                       y.data_ptr(), deg.data_ptr() if with_deg else None, scale,
+                                       dP.data_ptr(), Din, dW.data_ptr(), db.data_ptr(),
+                                       loss.data_ptr(), ws.data_ptr(), ws.numel(), None), "head")
+    torch.cuda.synchronize()
+    Pd, Wd, bd = P.double(), W.double(), b.double()
+    z = Pd @ Wd + bd
+    lse = torch.logsumexp(z, 1)
+    ref_loss = (lse - z.gather(1, y[:, None])[:, 0]).sum() * scale
+    dz = (torch.softmax(z, 1) - torch.nn.functional.one_hot(y, C).double()) * scale
+    d = (deg[1:] - deg[:-1]).double()
+    rs = torch.where(d > 0, 1.0 / d.clamp(min=1), torch.zeros_like(d)) if with_deg else torch.ones_like(d)
+    ref_dP = (dz @ Wd.T) * rs[:, None]
+    ref_dW, ref_db = Pd.T @ dz, dz.sum(0)
+    # absolute-value statement of dz = p - onehot: |p| + onehot (A.8 ref_abs)
+    dza = (torch.softmax(z, 1) + torch.nn.functional.one_hot(y, C).double()) * scale
+    assert abs(loss.item() - ref_loss.item()) <= 1e-5 * abs(ref_loss.item())
+    for got, ref, abs_scale in ((dP, ref_dP, (dza @ Wd.abs().T) * rs[:, None]),
+                                (dW, ref_dW, Pd.abs().T @ dza), (db, ref_db, dza.sum(0))):
+        err = (got.double() - ref).abs()
+        assert bool((err <= 1e-5 * (abs_scale + ref.abs()) + 1e-12).all()), float(err.max())
