@@ -184,6 +184,8 @@ class SparseOperand:
         if self.row_ids is not None:
             return self
         if self._sorted is None:
+            if getattr(self, "_released", False):
+                raise RuntimeError("row-order storage of this operand was released")
             dev = self.device
             deg = self.offsets[1:] - self.offsets[:-1]
             order = torch.sort(deg, descending=True, stable=True).indices
@@ -228,6 +230,17 @@ class SparseOperand:
             self._sorted = op
         return self._sorted
 
+    def release_row_order(self) -> None:
+        """Keep only the degree-sorted form (built now if needed) and free the
+        row-order index arrays: for trainers whose every use of this operand is
+        a gnn_spmm (which runs on the sorted form) — halves its footprint.
+        Afterwards ``cols`` / ``vals`` / ``entries`` / ``view`` are unavailable."""
+        so = self.by_degree()
+        if so is self:
+            return
+        self.packed = self._cols = self._vals = self._plain = None
+        self._released = True
+
     def entries(self, e0: int = 0, e1: int | None = None):
         """(cols, vals) of entries [e0, e1) in plain form (vals None if none)."""
         e1 = self.nnz if e1 is None else e1
@@ -256,6 +269,9 @@ class SparseOperand:
         return self.offsets.device
 
     def view(self, vals=None, eid=None) -> _lib.CsrView:
+        if getattr(self, "_released", False):
+            raise RuntimeError("row-order storage of this operand was released "
+                               "(release_row_order): use by_degree()")
         v = _lib.CsrView()
         v.num_rows = self.num_rows
         v.num_cols = self.num_cols

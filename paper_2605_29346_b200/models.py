@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .graph import CsrGraph
+from .graph import SPMM_SHORT_MAX, SPMM_SORT, CsrGraph
 from .kernels import AdamCall, GemmCall, HeadCall, MaskNormColsumCall, SpmmCall, XentCall
 from .ops import colsum, gemm, linear, spmm_raw
 
@@ -158,6 +158,10 @@ class GCNTrainer:
                 g.drop_csc()
             if release_canonical:  # canonical CSR stays on the host only
                 g.release_device_targets()
+                if hidden <= 64 and hidden % 4 == 0 and SPMM_SORT and SPMM_SHORT_MAX > 0:
+                    # every aggregation runs on the degree-sorted forms: keep only those
+                    A.release_row_order()
+                    AT.release_row_order()
         else:
             A, AT = g.csr(), g.csc()
         self.A, self.AT = A, AT

@@ -134,3 +134,26 @@ def test_e2e_pipelined_matches_device_resident_epoch(setup):
         assert la == loss_h.item(), k
     for k2 in a.params():
         assert torch.equal(a.params()[k2], b.params()[k2])
+
+
+def test_trainer_with_released_row_order_operands(setup):
+    """release_canonical=True keeps only the degree-sorted coalesced operands
+    on the device (the row-order arrays are freed); the epoch is unchanged —
+    bit-identical to the trainer that still holds both forms."""
+    import paper_2605_29346_b200 as gbm
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    gb, g0, (off, tgt, t_off, t_rows), X, y, (V, F, Hd, C) = setup
+    g = gbm.generate(gbm.GraphGenSpec("power-law", V, 10556, exponent=2.1), 42)
+    a = GCNTrainer(g0, F, Hd, C, seed=0, coalesced=True)
+    b = GCNTrainer(g, F, Hd, C, seed=0, coalesced=True, release_canonical=True)
+    assert getattr(g.csr_coalesced(), "_released", False) and g.csr_coalesced().packed is None
+    with pytest.raises(RuntimeError):
+        g.csr_coalesced().view()
+    for t in (a, b):
+        t.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+        t.forward_backward()
+    torch.cuda.synchronize()
+    assert torch.equal(a.loss, b.loss)
+    for k, v in a.grads().items():
+        assert torch.equal(v, b.grads()[k]), k
