@@ -988,8 +988,11 @@ __global__ void __launch_bounds__(256, (VPL == 1) ? 3 : 1) gat_bwd_csc_kernel(Ga
 // produces all heads from it:
 //   dWh[u, h*F + f]  = scale * sum_j alpha[eid_j, h] * dZ[v_j, f]
 //   dalpha[eid_j, h] = scale * < dZ[v_j, :], Wh[u, h*F : (h+1)*F] >
+#ifndef GNN_GATM_MINB
+#define GNN_GATM_MINB 3
+#endif
 template <int G, int VPL, int HM>
-__global__ void __launch_bounds__(256, (VPL * HM <= 4) ? 3 : 1) gat_bwd_csc_mean_kernel(GatBwdArgs a, float scale) {
+__global__ void __launch_bounds__(256, (VPL * HM <= 4) ? GNN_GATM_MINB : 1) gat_bwd_csc_mean_kernel(GatBwdArgs a, float scale) {
   constexpr int NG = 32 / G;
   constexpr int U = 4;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

@@ -354,6 +354,10 @@ class DistGCNTrainer:
             elif not overlap:
                 k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
                 k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
+            if hidden > HeadCall.FUSED_MAX or classes > HeadCall.FUSED_MAX:
+                raise NotImplementedError(
+                    "row-partitioned GCN: the 1/V_global-scaled output layer is the fused "
+                    f"kernel (hidden, classes <= {HeadCall.FUSED_MAX})")
             k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
                               self.db2, self.loss, deg_offsets=deg)
             k_head.scale = 1.0 / V

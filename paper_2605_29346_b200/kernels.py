@@ -136,7 +136,14 @@ class AdamCall:
 
 
 class HeadCall:
-    """Fused output layer: logits, mean cross-entropy, dP (degree-normed), dW, db."""
+    """Fused output layer: logits, mean cross-entropy, dP (degree-normed), dW, db.
+
+    The fused kernel (gnn_gcn_head) covers Din, C <= 64; wider layers (e.g. the
+    172 classes of the papers100M shape) run the same math as library calls:
+    Z = P W + b, softmax-CE (dZ scaled 1/M), dW = P^T dZ, db = colsum(dZ),
+    dP = (dZ W^T) / deg."""
+
+    FUSED_MAX = 64
 
     def __init__(self, P, W, b, labels, dP, dW, db, loss, deg_offsets=None):
         self.lib = _lib.lib()
@@ -145,10 +152,27 @@ class HeadCall:
         self.C = W.shape[1]
         self.P, self.W, self.b, self.labels, self.dP = P, W, b, labels, dP
         self.dW, self.db, self.loss, self.deg = dW, db, loss, deg_offsets
+        self.fused = self.Din <= self.FUSED_MAX and self.C <= self.FUSED_MAX
+        if not self.fused:
+            f32 = dict(dtype=torch.float32, device=self.dev)
+            self.Z = torch.empty(self.M, self.C, **f32)
+            self.dZ = torch.empty(self.M, self.C, **f32)
+            self._parts = [GemmCall(P, W, self.Z, bias=b),
+                           XentCall(self.Z, labels, loss, dZ=self.dZ, grad_scale=1.0 / self.M),
+                           GemmCall(P, self.dZ, dW, trans_a=True),
+                           ColsumCall(self.dZ, db),
+                           GemmCall(self.dZ, W, dP, trans_b=True)]
+            if deg_offsets is not None:
+                self._parts.append(MaskNormColsumCall(dP, dP, deg_offsets=deg_offsets))
+            return
         self.ws = _lib.workspace(self.lib.gnn_gcn_head_workspace(self.M, self.Din, self.C),
                                  self.dev)
 
     def __call__(self):
+        if not self.fused:
+            for c in self._parts:
+                c()
+            return
         _lib.check(self.lib.gnn_gcn_head(
             self.M, self.Din, self.C, self.P.data_ptr(), self.P.stride(0), self.W.data_ptr(),
             self.b.data_ptr(), self.labels.data_ptr(),

@@ -157,3 +157,31 @@ def test_trainer_with_released_row_order_operands(setup):
     assert torch.equal(a.loss, b.loss)
     for k, v in a.grads().items():
         assert torch.equal(v, b.grads()[k]), k
+
+
+def test_trainer_wide_output_layer_matches_oracle(cuda):
+    """More classes than the fused output kernel covers (C > 64, e.g. the 172
+    of the papers100M shape): HeadCall runs GEMM + softmax-CE + colsum + GEMMs
+    + degree norm; the epoch still matches the float64 oracle."""
+    import paper_2605_29346_b200 as gb
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    V, E, F, Hd, C = 3000, 20000, 64, 16, 172
+    g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=2.1), 7)
+    off, tgt = g.offsets, g.targets
+    t_off, t_rows, _ = og.transpose(V, V, off, tgt)
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (V, F)).astype(np.float32)
+    y = rng.integers(0, C, V)
+    for coalesced in (False, True):
+        tr = GCNTrainer(g, F, Hd, C, seed=0, coalesced=coalesced)
+        assert not tr.k_head.fused
+        tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+        tr.forward_backward()
+        torch.cuda.synchronize()
+        p = {k: v.cpu().numpy().astype(np.float64) for k, v in tr.params().items()}
+        ref = oo.gcn2_step(off, tgt, t_off, t_rows, X, p["W1"], p["b1"], p["W2"], p["b2"], y)
+        assert abs(tr.loss.item() - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+        for k, gv in tr.grads().items():
+            ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
+            assert ok, (coalesced, k, worst)
