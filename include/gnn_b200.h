@@ -303,6 +303,19 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
              const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
              const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Four attention heads over ONE shared feature row (GAT output layer in the
+ * aggregate-then-transform order): Y[v, 4i+h] = scale * sum_e vals[e*4+h] *
+ * X[col_e, i], i < F; Y is [num_rows, 4F] (head-minor, so Y viewed as
+ * [num_rows*F, 4] rows line up with W[F, 4*C] viewed as [4F, C] rows: the
+ * head mean of sum_e alpha_eh (X W_h)[col_e] is then one GEMM Y . W).  vals
+ * [nnz*4] in CSR edge order (16-byte aligned), no eid / packed / row_ids;
+ * a plan with short_max = 0 (the nnz-split kernel covers every row).  Gathers
+ * F floats per edge instead of 4C. */
+int gnn_spmm_shared_heads(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, const float *X,
+                          int64_t ldx, int64_t F, float *Y, int64_t ldy, float scale,
+                          const gnn_epilogue_t *epi, void *ws, size_t ws_bytes,
+                          gnn_stream_t stream);
+
 /* Row-partitioned multi-GPU form of gnn_spmm (fused with the
  * exchange): instead of all-gathering the feature blocks first, the kernel
  * reads every gathered row in place from the rank that owns it — column id c

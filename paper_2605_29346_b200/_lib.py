@@ -189,6 +189,9 @@ SIGNATURES = {
             c_ptr,
         ],
     ),
+    "gnn_spmm_shared_heads": (c_int, [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_ptr, c_i64,
+                                      c_i64, c_ptr, c_i64, C.c_float, C.POINTER(Epilogue), c_ptr,
+                                      c_sz, c_ptr]),
     "gnn_spmm_peer": (
         c_int,
         [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_i64,

@@ -56,6 +56,8 @@ struct SpmmArgs {
   float *slots;                // [nwarps][2][K]
   int stage;                 // StageMode
   const int32_t *row_ids;    // row-permuted operand: operand row i -> output row row_ids[i]
+  int xdiv;                  // X column of output column c is c / xdiv (4: shared heads)
+  float wscale;              // WM_SHARED4: scale on the edge weights
   int col_bits;              // packed weights (WM_PACKED): column id = cols[j] & col_mask,
   uint32_t col_mask;         //   edge weight = float(cols[j] >> col_bits)
   int bulk_ok;
@@ -158,7 +160,10 @@ enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
 //   WM_SEID    edge ids staged in the ring, vals[eid*heads + head] (SpMMve^T)
 //   WM_PACKED  small integer weight in the high bits of the column id (the
 //              coalesced multigraph operand: one 4-byte word per edge)
-enum WeightMode : int { WM_NONE = 0, WM_GLOBAL = 1, WM_SVALS = 2, WM_SEID = 3, WM_PACKED = 4 };
+//   WM_SHARED4 four heads over ONE shared feature row: output column 4i+h =
+//              sum_e vals[e*4+h] * X[col_e, i] (gnn_spmm_shared_heads)
+enum WeightMode : int { WM_NONE = 0, WM_GLOBAL = 1, WM_SVALS = 2, WM_SEID = 3, WM_PACKED = 4,
+                        WM_SHARED4 = 5 };
 template <int WM>
 constexpr int stage_of() {
   return WM == WM_SVALS ? STAGE_VALS : WM == WM_SEID ? STAGE_EID : STAGE_NONE;
@@ -176,8 +181,9 @@ struct LaneCols {
     for (int v = 0; v < VPL; ++v) {
       int64_t col = cbase + (int64_t)(v * G + gl) * VW;
       if (col >= a.K) col = 0;
-      xb[v] = PEER ? reinterpret_cast<const char *>(col * 4)
-                   : reinterpret_cast<const char *>(a.X + col);
+      const int64_t xc = a.xdiv > 1 ? col / a.xdiv : col;
+      xb[v] = PEER ? reinterpret_cast<const char *>(xc * 4)
+                   : reinterpret_cast<const char *>(a.X + xc);
       head[v] = (int)(col / a.F);
     }
   }
@@ -234,6 +240,45 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
     return p;
   };
   int i = is + g;
+  if constexpr (WM == WM_SHARED4) {
+    // every head of a lane's float4 reads the same X element: one scalar gather,
+    // the 4 head weights as one float4
+    const float ws = a.wscale;
+    for (; i < ie; i += NG * U) {
+      int32_t c[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ok[u] = i + u * NG < ie;
+        c[u] = ok[u] ? scol[i + u * NG] : 0;
+      }
+      float xs[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          xs[u][v] = ok[u] ? __ldg(reinterpret_cast<const float *>(lc.xb[v] + (uint64_t)(uint32_t)c[u] * ldxb))
+                           : 0.f;
+      float4 w4[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 t = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w4[u] = make_float4(t.x * ws, t.y * ws, t.z * ws, t.w * ws);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          if constexpr (VW == 4) {
+            acc[v].x = fmaf(w4[u].x, xs[u][v], acc[v].x);
+            acc[v].y = fmaf(w4[u].y, xs[u][v], acc[v].y);
+            acc[v].z = fmaf(w4[u].z, xs[u][v], acc[v].z);
+            acc[v].w = fmaf(w4[u].w, xs[u][v], acc[v].w);
+          }
+        }
+    }
+    return;
+  }
   for (; i + (U - 1) * NG < ie; i += NG * U) {
     int32_t p[U];
 #pragma unroll
@@ -979,6 +1024,7 @@ auto pick_wm(int wm) {
     case WM_SVALS: return K<G, VPL, VW, WM_SVALS, PEER>::fn;
     case WM_SEID: return K<G, VPL, VW, WM_SEID, PEER>::fn;
     case WM_PACKED: return K<G, VPL, VW, WM_PACKED, PEER>::fn;
+    case WM_SHARED4: return K<G, VPL, VW, WM_SHARED4, PEER>::fn;
     default: return K<G, VPL, VW, WM_NONE, PEER>::fn;
   }
 }
@@ -1210,10 +1256,16 @@ size_t gnn_spmm_workspace(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, 
 static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
                      const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
                      const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream,
-                     const float *const *parts, int64_t nparts, int64_t part_log2) {
+                     const float *const *parts, int64_t nparts, int64_t part_log2,
+                     float shared_scale = 0.f) {
   const bool peer = parts != nullptr;
+  const bool shared = shared_scale != 0.f;  // four heads over one shared X row
+  const int64_t xw = shared ? K / 4 : K;    // X columns read
   if (!A || !plan || !Y || K <= 0 || heads <= 0 || K % heads != 0 || ldy < K ||
-      (A->nnz > 0 && (!X || ldx < K || !A->cols)) || !A->offsets)
+      (A->nnz > 0 && (!X || ldx < xw || !A->cols)) || !A->offsets)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (shared && (heads != 4 || K % 4 != 0 || !A->vals || A->eid || A->col_bits || A->row_ids ||
+                 peer || plan->main_nnz != A->nnz || !aligned16(A->vals)))
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->eid && !A->vals) return GNN_ERR_INVALID_ARGUMENT;
   const bool packed = A->col_bits != 0;
@@ -1275,9 +1327,12 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
     GNN_CUDA_TRY(cudaMemsetAsync(
         a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split) * a.ncb, st));
   a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
-  const int wm = packed ? WM_PACKED
-                        : !A->vals ? WM_NONE
-                                   : (A->eid ? WM_SEID : (heads == 1 ? WM_SVALS : WM_GLOBAL));
+  const int wm = shared ? WM_SHARED4
+                 : packed ? WM_PACKED
+                          : !A->vals ? WM_NONE
+                                     : (A->eid ? WM_SEID : (heads == 1 ? WM_SVALS : WM_GLOBAL));
+  a.xdiv = shared ? 4 : 1;
+  a.wscale = shared ? shared_scale : 1.f;
   a.col_bits = packed ? A->col_bits : 0;
   a.col_mask = packed ? (uint32_t)((1ull << A->col_bits) - 1) : 0xffffffffu;
   a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
@@ -1287,7 +1342,7 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
   {
     const bool v4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
                     (a.F % 4 == 0);
-    a.short_max = (v4 && K <= 64) ? plan->short_max : 0;
+    a.short_max = (v4 && K <= 64 && !shared) ? plan->short_max : 0;
   }
   // a plan whose nnz-split range stops before the short tail needs the short-row kernel
   if (plan->main_nnz < A->nnz && a.short_max == 0) return GNN_ERR_UNSUPPORTED;
@@ -1351,8 +1406,9 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
     if (vec4 && (e.flags & GNN_EPI_SELF)) vec4 = e.ld_self % 4 == 0 && aligned16(e.self_x);
     if (vec4 && (e.flags & GNN_EPI_MASK)) vec4 = e.ld_mask % 4 == 0 && aligned16(e.mask);
     if (vec4 && (e.flags & GNN_EPI_BIAS)) vec4 = aligned16(e.bias);
+    if (shared && !vec4) return GNN_ERR_UNSUPPORTED;
     int s;
-    const bool tma_ok = vec4 && !packed && !A->row_ids && plan->main_nnz == A->nnz && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
+    const bool tma_ok = vec4 && !packed && !shared && !A->row_ids && plan->main_nnz == A->nnz && (a.stage == STAGE_NONE || a.stage == STAGE_VALS) && a.heads == 1 &&
                         a.P % 4 == 0 && aligned16(A->cols) && (!hv || aligned16(A->vals)) &&
                         plan->short_max == 0 && !peer && getenv("GNN_SPMM_TMA") != nullptr;
     CUtensorMap tm;
@@ -1405,6 +1461,15 @@ int gnn_spmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads
              const float *X, int64_t ldx, float *Y, int64_t ldy, int64_t K,
              const gnn_epilogue_t *epi, void *ws, size_t ws_bytes, gnn_stream_t stream) {
   return spmm_impl(A, plan, heads, X, ldx, Y, ldy, K, epi, ws, ws_bytes, stream, nullptr, 0, 0);
+}
+
+int gnn_spmm_shared_heads(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, const float *X,
+                          int64_t ldx, int64_t F, float *Y, int64_t ldy, float scale,
+                          const gnn_epilogue_t *epi, void *ws, size_t ws_bytes,
+                          gnn_stream_t stream) {
+  if (F <= 0 || scale == 0.f) return GNN_ERR_INVALID_ARGUMENT;
+  return spmm_impl(A, plan, 4, X, ldx, Y, ldy, 4 * F, epi, ws, ws_bytes, stream, nullptr, 0, 0,
+                   scale);
 }
 
 int gnn_spmm_peer(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, const float *const *parts,

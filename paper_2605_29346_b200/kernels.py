@@ -53,6 +53,30 @@ class SpmmCall:
                                      _lib.stream_handle(self.dev)), "spmm")
 
 
+class SharedHeadsCall:
+    """Y[:, 4i+h] = scale * sum_e vals[e, h] X[col_e, i] (gnn_spmm_shared_heads):
+    four heads aggregated over one shared feature row."""
+
+    def __init__(self, op: SparseOperand, X, vals, Y, scale=1.0):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.F = int(X.shape[1])
+        assert Y.shape[1] == 4 * self.F and vals.shape[-1] == 4
+        self.view = op.view(vals=vals)
+        self.plan = op.plan()
+        self.X, self.Y, self.scale = X, Y, float(scale)
+        self.epi = _lib.Epilogue()
+        self._keep = (op, vals)
+        nbytes = self.lib.gnn_spmm_workspace(C.byref(self.view), C.byref(self.plan), 4 * self.F)
+        self.ws = _lib.workspace(nbytes, self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_spmm_shared_heads(
+            C.byref(self.view), C.byref(self.plan), self.X.data_ptr(), self.X.stride(0), self.F,
+            self.Y.data_ptr(), self.Y.stride(0), self.scale, C.byref(self.epi), self.ws.data_ptr(),
+            self.ws.numel(), _lib.stream_handle(self.dev)), "spmm_shared_heads")
+
+
 class GemmCall:
     """C = op(A) op(B) (+bias)(relu)."""
 

@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import numpy as np
 import torch
 
@@ -664,7 +666,8 @@ class GATTrainer(_FusedEpoch):
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
                  lr=0.01, slope=0.2, seed: int = 0):
         from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
-                              GatBwdCscCall, GatBwdCscMeanCall, HeadMeanCall, SegmentSumCall)
+                              GatBwdCscCall, GatBwdCscMeanCall, HeadMeanCall, SegmentSumCall,
+                              SharedHeadsCall)
 
         self.g = g
         dev = g.device
@@ -707,7 +710,12 @@ class GATTrainer(_FusedEpoch):
         self.Wh1, self.Y1 = e(V, K1), e(V, K1)
         self.el1, self.er1, self.el2, self.er2 = e(V, H), e(V, H), e(V, H), e(V, H)
         self.alpha1, self.alpha2 = e(E, H), e(E, H)
-        self.Wh2, self.Yc2 = e(V, K2), e(V, K2)
+        # layer-2 aggregation order: with 4 heads, aggregate the shared Y1 row
+        # (K1 floats per edge) for every head and transform once after
+        # (gnn_spmm_shared_heads + one GEMM) instead of gathering Wh2 (H*Cp)
+        self.shared2 = H == 4 and os.environ.get("GNN_GAT_SHARED", "1") != "0"
+        self.Wh2 = e(V, K2)
+        self.Yc2 = e(V, K1 * H) if self.shared2 else e(V, K2)
         self.Z = torch.zeros(V, Cp, **f32)
         self.dZ = torch.zeros(V, Cp, **f32)  # pad column never written: stays 0
         self.dWh2 = e(V, K2)
@@ -726,8 +734,13 @@ class GATTrainer(_FusedEpoch):
         k["Y1.W2"] = GemmCall(self.Y1, self.W2, self.Wh2)
         k["proj2"] = AttnProjCall(self.Wh2, self.al2, self.ar2, self.el2, self.er2, H)
         k["softmax2"] = EdgeSoftmaxCall(A, H, self.alpha2, el=self.el2, er=self.er2, slope=slope)
-        k["agg2"] = SpmmCall(A, self.Wh2, self.Yc2, heads=H, vals=self.alpha2)
-        k["mean2"] = HeadMeanCall(self.Yc2, self.Z, H, Cp, bias=self.b2)
+        if self.shared2:
+            k["agg2"] = SharedHeadsCall(A, self.Y1, self.alpha2, self.Yc2, scale=1.0 / H)
+            # rows 4i+h of W2 viewed [K1*H, Cp] = W2[i, h*Cp:(h+1)*Cp]: the head mean
+            k["mean2"] = GemmCall(self.Yc2, self.W2.view(K1 * H, Cp), self.Z, bias=self.b2)
+        else:
+            k["agg2"] = SpmmCall(A, self.Wh2, self.Yc2, heads=H, vals=self.alpha2)
+            k["mean2"] = HeadMeanCall(self.Yc2, self.Z, H, Cp, bias=self.b2)
         k["xent"] = XentCall(self.Z[:, :classes], self.labels, self.loss, dZ=self.dZ[:, :classes])
         # backward, layer 2
         k["db2"] = ColsumCall(self.dZ, self.db2)

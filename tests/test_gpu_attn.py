@@ -310,3 +310,29 @@ def test_gat_bwd_csc_mean_fused(gb, graphs, gname, H, F):
     assert_close(dWh, ref, ra, "mean dWh")
     assert_close(dal, oo.sddmm(off, tgt, dY, Wh, H), oo.sddmm(off, tgt, np.abs(dY), np.abs(Wh), H),
                  "mean dalpha")
+
+
+@pytest.mark.parametrize("gname", ["cora_pl", "pl_10k", "mega"])
+@pytest.mark.parametrize("F", [4, 16, 64])
+def test_spmm_shared_heads(gb, graphs, gname, F):
+    """gnn_spmm_shared_heads: Y[v, 4i+h] = s * sum_e alpha[e,h] X[col_e, i]
+    (four heads over one shared row) against the float64 statement."""
+    from paper_2605_29346_b200.kernels import SharedHeadsCall
+
+    g = graphs[gname]
+    off, tgt = g.offsets, g.targets
+    V = g.num_vertices
+    rng = np.random.default_rng(F)
+    X = rng.uniform(-1, 1, (V, F)).astype(np.float32)
+    al = rng.uniform(0, 1, (tgt.size, 4)).astype(np.float32)
+    Y = torch.empty(V, 4 * F, device="cuda")
+    SharedHeadsCall(g.csr(), torch.from_numpy(X).cuda(), torch.from_numpy(al).cuda(), Y,
+                    scale=0.25)()
+    rows = np.repeat(np.arange(V), np.diff(off))
+    ref = np.zeros((V, F, 4))
+    ra = np.zeros((V, F, 4))
+    for h in range(4):
+        np.add.at(ref[:, :, h], rows, al[:, h:h + 1].astype(np.float64) * X[tgt])
+        np.add.at(ra[:, :, h], rows, np.abs(al[:, h:h + 1].astype(np.float64) * X[tgt]))
+    ok, worst = oo.close(Y.cpu().numpy(), 0.25 * ref.reshape(V, 4 * F), 0.25 * ra.reshape(V, 4 * F))
+    assert ok, worst
