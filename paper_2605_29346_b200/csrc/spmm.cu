@@ -243,30 +243,34 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
   if constexpr (WM == WM_SHARED4) {
     // every head of a lane's float4 reads the same X element: one scalar gather,
     // the 4 head weights as one float4
+#ifndef GNN_SH4_U
+#define GNN_SH4_U 4
+#endif
+    constexpr int US = GNN_SH4_U;  // edges in flight per group (scalar gathers: cheap registers)
     const float ws = a.wscale;
-    for (; i < ie; i += NG * U) {
-      int32_t c[U];
-      bool ok[U];
+    for (; i < ie; i += NG * US) {
+      int32_t c[US];
+      bool ok[US];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < US; ++u) {
         ok[u] = i + u * NG < ie;
         c[u] = ok[u] ? scol[i + u * NG] : 0;
       }
-      float xs[U][VPL];
+      float xs[US][VPL];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < US; ++u)
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
           xs[u][v] = ok[u] ? __ldg(reinterpret_cast<const float *>(lc.xb[v] + (uint64_t)(uint32_t)c[u] * ldxb))
                            : 0.f;
-      float4 w4[U];
+      float4 w4[US];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < US; ++u) {
         const float4 t = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
         w4[u] = make_float4(t.x * ws, t.y * ws, t.z * ws, t.w * ws);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < US; ++u)
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
           if constexpr (VW == 4) {
