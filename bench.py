@@ -660,7 +660,8 @@ def run_reference(args):
     finally:
         pool.close()
     v = statistics.mean(times)
-    return {"metric": "gcn_epoch_ms", "value": round(v, 1), "unit": "ms", "n_gpus": 0,
+    return {"metric": "gcn_epoch_ms", "value": round(v, 1), "unit": "ms", "n_gpus": args.gpus,
+            "device": "cpu (the reference path is host code; n_gpus = the run's N)",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 1),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gsbench power-law restatement, seed 42)",

@@ -171,13 +171,17 @@ __global__ void __launch_bounds__(256) colsum_narrow_kernel(int64_t M, int64_t N
     partials[(int64_t)blockIdx.x * N + c] = t;
   }
 }
+// warp per column, fixed-order butterfly (see sum_partials_kernel)
 __global__ void colsum_final_kernel(int64_t nb, int64_t N, const float *__restrict__ partials,
                                     float *out) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
-       c += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = (int)(threadIdx.x & 31);
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < N;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     float s = 0.f;
-    for (int64_t b = 0; b < nb; ++b) s += partials[b * N + c];
-    out[c] = s;
+    for (int64_t b = lane; b < nb; b += 32) s += partials[b * N + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
   }
 }
 
@@ -265,7 +269,7 @@ int gnn_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, float *out, vo
   else
     colsum_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, partials, rpb);
   GNN_LAUNCH_CHECK();
-  colsum_final_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, out);
+  colsum_final_kernel<<<(unsigned)ceil_div(N * 32, (int64_t)256), 256, 0, st>>>(nb, N, partials, out);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -350,13 +354,19 @@ __global__ void __launch_bounds__(256) mask_norm_colsum_kernel(
   }
 }
 
+// out[c] = sum_b partials[b*N + c]: one warp per column, lanes stride the
+// partials, fixed-order butterfly (deterministic).  A thread-per-column loop
+// over ~500 partials was a 46 us chain of dependent loads for N = 16.
 __global__ void sum_partials_kernel(int64_t nb, int64_t N, const float *__restrict__ partials,
                                     float *out) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < N;
-       c += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = (int)(threadIdx.x & 31);
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < N;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     float s = 0.f;
-    for (int64_t b = 0; b < nb; ++b) s += partials[b * N + c];
-    out[c] = s;
+    for (int64_t b = lane; b < nb; b += 32) s += partials[b * N + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
   }
 }
 
@@ -541,7 +551,8 @@ int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, cons
                                                               deg_offsets, out, ldo, partials, rpb);
   GNN_LAUNCH_CHECK();
   if (colsum) {
-    sum_partials_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(nb, N, partials, colsum);
+    sum_partials_kernel<<<(unsigned)ceil_div(N * 32, (int64_t)256), 256, 0, st>>>(nb, N, partials,
+                                                                                colsum);
     GNN_LAUNCH_CHECK();
   }
   return GNN_OK;

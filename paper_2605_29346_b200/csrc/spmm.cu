@@ -460,9 +460,9 @@ constexpr int kSub = 512;
 
 template <int G, int VPL, int VW, int WM, bool PEER = false>
 #ifndef GNN_SPMM_MINB
-#define GNN_SPMM_MINB 4  // resident CTAs per SM (8 warps each) the register budget targets (64 regs)
+#define GNN_SPMM_MINB 4  // resident CTAs per SM for column blocks <= 16 wide (64 regs); wider: 3
 #endif
-__global__ void __launch_bounds__(256, GNN_SPMM_MINB) spmm_main_kernel(SpmmArgs a) {
+__global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
   extern __shared__ __align__(16) uint8_t spmm_smem[];
@@ -1042,7 +1042,8 @@ int launch_main(const SpmmArgs &a, int wm, cudaStream_t st) {
   // unified L1/shared array to L1 so hot feature rows stay cached.
   auto kern = pick_wm<MainKernel, G, VPL, VW, PEER>(wm);
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int per_sm_kb = (int)((smem * GNN_SPMM_MINB + 1023) / 1024);  // resident CTAs
+  constexpr int minb = (KB <= 16) ? GNN_SPMM_MINB : 3;  // resident CTAs (see the kernel)
+  const int per_sm_kb = (int)((smem * minb + 1023) / 1024);
   const int carve = per_sm_kb * 100 / 228 + 1;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     carve > 100 ? 100 : carve));

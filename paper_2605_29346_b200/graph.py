@@ -76,8 +76,12 @@ def _default_edges_per_warp(nnz: int, sms: int) -> int:
     return p
 
 
-# rows of degree <= this go to the SpMM's group-per-row kernel (power-law tail)
+# rows of degree <= this go to the SpMM's group-per-row kernel (power-law tail):
+# a degree-sorted operand hands it a contiguous, length-ordered tail (512); a
+# row-order operand keeps it to the shortest rows (its nnz-split kernel walks
+# every row anyway, and staged edge values beat the tail's global loads)
 SPMM_SHORT_MAX = int(os.environ.get("GNN_SPMM_SHORT", "512"))
+SPMM_SHORT_ROWORDER = int(os.environ.get("GNN_SPMM_SHORT_ROWORDER", "32"))
 
 
 # GNN_SPMM_SORT=0 keeps gnn_spmm on the operand's own row order
@@ -330,8 +334,10 @@ class SparseOperand:
         return plan
 
     def spmm_plan(self, edges_per_warp: int | None = None) -> _lib.SpmmPlan:
-        """Plan for gnn_spmm: degree-binned with short_max = SPMM_SHORT_MAX."""
-        return self.plan(edges_per_warp, short_max=SPMM_SHORT_MAX)
+        """Plan for gnn_spmm: degree-binned, short_max = SPMM_SHORT_MAX for the
+        degree-sorted form, SPMM_SHORT_ROWORDER otherwise."""
+        return self.plan(edges_per_warp, short_max=SPMM_SHORT_MAX if self.row_ids is not None
+                         else SPMM_SHORT_ROWORDER)
 
     def nbytes(self) -> int:
         n = self.offsets.numel() * 8 + self.nnz * 4

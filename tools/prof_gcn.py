@@ -24,9 +24,14 @@ tr = GCNTrainer(g, 602, 16, 41, seed=42, coalesced=a.layout == "coalesced")
 X = torch.rand(V, 602) * 2 - 1
 y = torch.randint(0, 41, (V,))
 tr.set_inputs(X, y)
+tr.step()  # warm (plans, workspaces)
+torch.cuda.synchronize()
+# ncu --profile-from-start off: only the epochs below are captured
+torch.cuda.profiler.start()
 for _ in range(a.epochs):
     tr.step()
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 for K in a.spmm_k:
     Xk = torch.rand(V, K, device="cuda")
     Yk = torch.empty_like(Xk)
