@@ -247,7 +247,6 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
 #define GNN_SH4_U 4
 #endif
     constexpr int US = GNN_SH4_U;  // edges in flight per group (scalar gathers: cheap registers)
-    const float ws = a.wscale;
     for (; i < ie; i += NG * US) {
       int32_t c[US];
       bool ok[US];
@@ -263,12 +262,10 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
         for (int v = 0; v < VPL; ++v)
           xs[u][v] = ok[u] ? __ldg(reinterpret_cast<const float *>(lc.xb[v] + (uint64_t)(uint32_t)c[u] * ldxb))
                            : 0.f;
-      float4 w4[US];
+      float4 w4[US];  // (the scale is applied once at the row's final store)
 #pragma unroll
-      for (int u = 0; u < US; ++u) {
-        const float4 t = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        w4[u] = make_float4(t.x * ws, t.y * ws, t.z * ws, t.w * ws);
-      }
+      for (int u = 0; u < US; ++u)
+        w4[u] = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < US; ++u)
 #pragma unroll
@@ -362,7 +359,15 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, float *dst, int64_t
     int64_t col = cbase + (int64_t)(v * G + gl) * VW;
     if (col < a.K) {
       typename V::T y = acc[v];
-      if (final_row) y = epi_vec<VW>(y, r, col, a, ns, ps);
+      if (final_row) {
+        if constexpr (VW == 4) {
+          const float w = a.wscale;  // shared-heads scale, applied once per row
+          y = make_float4(y.x * w, y.y * w, y.z * w, y.w * w);
+        } else {
+          y *= a.wscale;
+        }
+        y = epi_vec<VW>(y, r, col, a, ns, ps);
+      }
       V::st(dst + col, y);
     }
   }
@@ -432,7 +437,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
 #pragma unroll 8
     for (int k = 0; k < m; ++k) t += ld_relaxed_gpu(partial_ptr(a, wa, j0 + k) + c);
     if (ng == 1)
-      a.Y[orow * a.ldy + c] = epi_scalar(t, orow, c, a, ns, ps);
+      a.Y[orow * a.ldy + c] = epi_scalar(t * a.wscale, orow, c, a, ns, ps);
     else
       a.l2[(gbase + gi) * a.K + c] = t;
   }
@@ -445,7 +450,7 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
     float t = 0.f;
 #pragma unroll 8
     for (int64_t g2 = 0; g2 < ng; ++g2) t += ld_relaxed_gpu(a.l2 + (gbase + g2) * a.K + c);
-    a.Y[orow * a.ldy + c] = epi_scalar(t, orow, c, a, ns, ps);
+    a.Y[orow * a.ldy + c] = epi_scalar(t * a.wscale, orow, c, a, ns, ps);
   }
 }
 
