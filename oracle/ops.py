@@ -126,9 +126,12 @@ def cross_entropy(logits, labels):
     return loss, p / n
 
 
-def gcn2_step(offsets, cols, t_offsets, t_cols, X, W1, b1, W2, b2, labels):
+def gcn2_step(offsets, cols, t_offsets, t_cols, X, W1, b1, W2, b2, labels, loss_rows=None):
     """2-layer GCN forward + backward (Appendix A.4): returns loss, logits and
-    the parameter gradients, all float64."""
+    the parameter gradients, all float64.  ``loss_rows`` = B restricts the
+    mean cross-entropy to the first B rows (the seed vertices of a sampled
+    mini-batch subgraph, sampler.py:299-305: labels = the seed batch); the
+    other rows get zero logit gradient."""
     X = np.asarray(X, dtype=np.float64)
     H1 = X @ W1
     P1 = spmm(offsets, cols, H1, norm=True)
@@ -136,7 +139,12 @@ def gcn2_step(offsets, cols, t_offsets, t_cols, X, W1, b1, W2, b2, labels):
     Y1 = np.maximum(Z1, 0.0)
     H2 = Y1 @ W2
     Z2 = spmm(offsets, cols, H2, norm=True) + b2
-    loss, dZ2 = cross_entropy(Z2, labels)
+    if loss_rows is None:
+        loss, dZ2 = cross_entropy(Z2, labels)
+    else:
+        loss, dz = cross_entropy(Z2[:loss_rows], np.asarray(labels)[:loss_rows])
+        dZ2 = np.zeros_like(Z2)
+        dZ2[:loss_rows] = dz
     db2 = dZ2.sum(axis=0)
     dH2 = spmm(t_offsets, t_cols, degree_norm(offsets, dZ2))
     dW2 = Y1.T @ dH2

@@ -385,6 +385,91 @@ class GCNTrainer:
         return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
 
 
+# ======================================================= sampled mini-batch
+class SampledGCNTrainer:
+    """Mini-batch 2-layer GCN on sampled subgraphs — the regime the
+    reference's sampler and execution model describe (sampler.py:259-305,
+    execmodel.py:430-490): per step the seed batch's F-fanout neighbourhood is
+    drawn on device (``sample_minibatch``, bit-exact with the reference's
+    PCG64 stream), the union of the hop edges (frontier -> drawn neighbour,
+    local ids; seeds are locals 0..B-1) forms the local subgraph A_s, the
+    feature rows of every sampled vertex are gathered (``gather_features``),
+    and the epoch math of ``GCNTrainer`` runs on A_s with the mean
+    cross-entropy over the B seeds only (loss rows = the seed batch,
+    sampler.py:299-305); Adam updates the shared weights.  Everything runs on
+    libgnnb200 kernels; per-step calls are rebuilt because the subgraph size
+    changes with every batch."""
+
+    def __init__(self, g: CsrGraph, X: torch.Tensor, labels: torch.Tensor, in_feats: int,
+                 hidden: int, classes: int, config, *, lr=0.01, seed: int = 0):
+        self.g, self.X, self.labels, self.cfg = g, X, labels, config
+        dev = g.device
+        self.dev = dev
+        self.F, self.Hd, self.C = in_feats, hidden, classes
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.W1 = torch.from_numpy(glorot(in_feats, hidden, seed, 0)).to(dev)
+        self.b1 = torch.zeros(hidden, **f32)
+        self.W2 = torch.from_numpy(glorot(hidden, classes, seed, 2)).to(dev)
+        self.b2 = torch.zeros(classes, **f32)
+        self.dW1, self.db1 = torch.empty_like(self.W1), torch.empty_like(self.b1)
+        self.dW2, self.db2 = torch.empty_like(self.W2), torch.empty_like(self.b2)
+        self.loss = torch.zeros(1, **f32)
+        self.k_adam = AdamCall([self.W1, self.b1, self.W2, self.b2],
+                               [self.dW1, self.db1, self.dW2, self.db2], lr=lr)
+        self.last = None
+
+    def subgraph(self, seeds, rng=None):
+        """(local CsrGraph A_s, local->global ids, B) of one sampled batch."""
+        from .graph import csr_from_edges
+        from .sampling import sample_minibatch
+
+        sg, _ = sample_minibatch(self.g, self.cfg, seeds, rng, on_device=True)
+        n = sg.num_local_vertices
+        es = torch.cat([h.edge_src for h in sg.hops]) if sg.hops else torch.empty(0)
+        ed = torch.cat([h.edge_dst for h in sg.hops]) if sg.hops else torch.empty(0)
+        A = csr_from_edges(n, es.to(torch.int64), ed.to(torch.int64), device=self.dev)
+        return A, sg.local_to_global, self.cfg.batch_size
+
+    def forward_backward(self, A: CsrGraph, l2g: torch.Tensor, B: int):
+        from .sampling import gather_features
+
+        n = A.num_vertices
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        Xs = gather_features(self.X, l2g)
+        ys = self.labels[l2g[:B]]
+        e = lambda k: torch.empty(n, k, **f32)  # noqa: E731
+        H1, Y1, P2, dZ1, dH1 = e(self.Hd), e(self.Hd), e(self.Hd), e(self.Hd), e(self.Hd)
+        dP2 = torch.zeros(n, self.Hd, **f32)  # rows >= B: no loss, zero gradient
+        op, opT = A.csr(), A.csc()
+        deg = A.d_offsets
+        N_, B_, R_, M_ = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        calls = [GemmCall(Xs, self.W1, H1),
+                 SpmmCall(op, H1, Y1, flags=N_ | B_ | R_, bias=self.b1),
+                 SpmmCall(op, Y1, P2, flags=N_),
+                 HeadCall(P2[:B], self.W2, self.b2, ys, dP2[:B], self.dW2, self.db2, self.loss,
+                          deg_offsets=deg[:B + 1]),
+                 SpmmCall(opT, dP2, dZ1, flags=M_, mask=Y1),
+                 MaskNormColsumCall(dZ1, dZ1, deg_offsets=deg, colsum=self.db1),
+                 SpmmCall(opT, dZ1, dH1),
+                 GemmCall(Xs, dH1, self.dW1, trans_a=True)]
+        for c in calls:
+            c()
+        self.last = (A, l2g, B)
+        return self.loss
+
+    def step(self, seeds, rng=None):
+        A, l2g, B = self.subgraph(seeds, rng)
+        self.forward_backward(A, l2g, B)
+        self.k_adam()
+        return self.loss
+
+    def params(self):
+        return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}
+
+    def grads(self):
+        return {"W1": self.dW1, "b1": self.db1, "W2": self.dW2, "b2": self.db2}
+
+
 # ===================================================================== GAT
 class _GATAggregate(torch.autograd.Function):
     """Appendix A.6 aggregation of one GAT layer, given Wh = X W:
