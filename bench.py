@@ -506,7 +506,8 @@ def run_ours(args, rank, world):
         torch.cuda.empty_cache()
         extras = {}
         for name, fn in (("gin_reddit", bm.run_gin), ("gat_products", bm.run_gat),
-                         ("spmm_sweep_reddit", bm.run_sweep), ("sampling", bm.run_sampling)):
+                         ("spmm_sweep_reddit", bm.run_sweep), ("sampling", bm.run_sampling),
+                         ("minibatch_gcn_reddit", bm.run_minibatch)):
             try:
                 extras[name] = fn()
             except Exception as exc:  # report, never hide

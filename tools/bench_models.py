@@ -3,6 +3,8 @@
   gin      2-layer GIN epoch, Reddit shape (K=602 -> 64 -> 41)        [BASELINE configs[2]]
   gat      2-layer GAT epoch, products shape (K=100 -> 4x16 -> 4x47)   [BASELINE configs[3]]
   sweep    SpMMv / SpMMve K sweep 16..256, Reddit shape               [BASELINE configs[1]]
+  sampling device sample_minibatch / DeviceSampler vs the reference sampler (host)
+  minibatch sampled mini-batch GCN training step, Reddit shape (SampledGCNTrainer)
 
 Prints one JSON object per item: device-timed ms (CUDA-graph replay), per-
 kernel ms inside eager epochs, peak memory.  Usage:
@@ -194,9 +196,45 @@ def run_sampling():
                     "seed / RNG-state H2D copies, no host sync"}
 
 
+def run_minibatch():
+    """Sampled mini-batch GCN training (SampledGCNTrainer) on the Reddit shape:
+    B=1024 seeds, fanouts (25, 10), K=602 -> 16 -> 41 — sampling, subgraph
+    CSR/CSC build, feature gather, the epoch kernels on the subgraph and Adam,
+    wall clock per step."""
+    from paper_2605_29346_b200.models import SampledGCNTrainer
+    from paper_2605_29346_b200.sampling import SampleConfig
+
+    V, E = REDDIT["V"], REDDIT["E"]
+    g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=2.1), 42)
+    X = torch.rand(V, 602, device="cuda") * 2 - 1
+    y = torch.randint(0, 41, (V,), device="cuda")
+    B, fan = 1024, (25, 10)
+    tr = SampledGCNTrainer(g, X, y, 602, 16, 41, SampleConfig(B, fan), seed=42)
+    rng = np.random.default_rng(0)
+    batches = [rng.choice(V, B, replace=False) for _ in range(12)]
+    for i, s in enumerate(batches[:2]):
+        tr.step(s, rng=i)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sizes = []
+    for i, s in enumerate(batches[2:]):
+        tr.step(s, rng=100 + i)
+        sizes.append((tr.last[0].num_vertices, tr.last[0].num_edges))
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / (len(batches) - 2)
+    return {"item": "minibatch_gcn_step_ms", "ms": round(ms, 3),
+            "workload": f"Reddit shape, B={B}, fanouts {fan}, GCN 602->16->41, Adam",
+            "mean_subgraph_vertices": int(np.mean([v for v, _ in sizes])),
+            "mean_subgraph_edges": int(np.mean([e for _, e in sizes])),
+            "loss": float(tr.loss.item()),
+            "note": "wall clock per step incl. device sampling, subgraph build, gather, "
+                    "kernels rebuilt per batch (no graph replay yet)"}
+
+
 if __name__ == "__main__":
     for item in sys.argv[1:] or ["gin", "gat", "sweep"]:
-        r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep, "sampling": run_sampling}[item]()
+        r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep, "sampling": run_sampling,
+             "minibatch": run_minibatch}[item]()
         for x in (r if isinstance(r, list) else [r]):
             print(json.dumps(x), flush=True)
         torch.cuda.empty_cache()
