@@ -84,8 +84,11 @@ SPMM_SHORT_MAX = int(os.environ.get("GNN_SPMM_SHORT", "512"))
 SPMM_SHORT_ROWORDER = int(os.environ.get("GNN_SPMM_SHORT_ROWORDER", "32"))
 
 
-# GNN_SPMM_SORT=0 keeps gnn_spmm on the operand's own row order
+# GNN_SPMM_SORT=0 keeps gnn_spmm on the operand's own row order; operands
+# below SPMM_SORT_MIN_NNZ entries stay in row order (building the sorted copy
+# costs more than it saves on a small, e.g. per-mini-batch, subgraph)
 SPMM_SORT = os.environ.get("GNN_SPMM_SORT", "1") != "0"
+SPMM_SORT_MIN_NNZ = int(os.environ.get("GNN_SPMM_SORT_MIN_NNZ", str(1 << 20)))
 
 
 def _al16(t) -> bool:
@@ -98,9 +101,12 @@ def spmm_operand(op: "SparseOperand", X, Y, *, heads=1, vals=None, eid=None, sel
     (``by_degree``) where its group-per-row tail applies — topology or
     multiplicity weights only, K <= 64 in float4 lanes — else ``op``."""
     K = int(X.shape[1])
+    if getattr(op, "_released", False):  # only the sorted form is left
+        return op.by_degree()
     if (not SPMM_SORT or SPMM_SHORT_MAX <= 0 or heads != 1 or vals is not None
             or eid is not None or (op._vals is not None and not op.mult) or op.nnz == 0
-            or K > 64 or K % 4 or not all(_al16(t) for t in (X, Y, self_x, mask, bias))):
+            or op.nnz < SPMM_SORT_MIN_NNZ or K > 64 or K % 4
+            or not all(_al16(t) for t in (X, Y, self_x, mask, bias))):
         return op
     return op.by_degree()
 

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .graph import SPMM_SHORT_MAX, SPMM_SORT, CsrGraph
+from .graph import SPMM_SHORT_MAX, SPMM_SORT, SPMM_SORT_MIN_NNZ, CsrGraph
 from .kernels import AdamCall, GemmCall, HeadCall, MaskNormColsumCall, SpmmCall, XentCall
 from .ops import colsum, gemm, linear, spmm_raw
 
@@ -160,7 +160,8 @@ class GCNTrainer:
                 g.drop_csc()
             if release_canonical:  # canonical CSR stays on the host only
                 g.release_device_targets()
-                if hidden <= 64 and hidden % 4 == 0 and SPMM_SORT and SPMM_SHORT_MAX > 0:
+                if (hidden <= 64 and hidden % 4 == 0 and SPMM_SORT and SPMM_SHORT_MAX > 0
+                        and min(A.nnz, AT.nnz) >= SPMM_SORT_MIN_NNZ):
                     # every aggregation runs on the degree-sorted forms: keep only those
                     A.release_row_order()
                     AT.release_row_order()

@@ -30,12 +30,19 @@ def setup(cuda):
     return gb, g, (off, tgt, t_off, t_rows), X, y, (V, F, Hd, C)
 
 
-@pytest.mark.parametrize("coalesced", [False, True])
-def test_trainer_matches_oracle(setup, coalesced):
+@pytest.mark.parametrize("coalesced,sort_all", [(False, False), (True, False), (False, True),
+                                               (True, True)])
+def test_trainer_matches_oracle(setup, coalesced, sort_all, monkeypatch):
+    """sort_all: the degree-sorted SpMM operands even at this small size (the
+    default keeps operands under SPMM_SORT_MIN_NNZ entries in row order)."""
+    import paper_2605_29346_b200.graph as G
     from paper_2605_29346_b200.models import GCNTrainer
 
+    if sort_all:
+        monkeypatch.setattr(G, "SPMM_SORT_MIN_NNZ", 0)
     gb, g, (off, tgt, t_off, t_rows), X, y, (V, F, Hd, C) = setup
     tr = GCNTrainer(g, F, Hd, C, seed=0, coalesced=coalesced)
+    assert (tr.k_agg1.view.row_ids is not None) == sort_all
     tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
     tr.forward_backward()
     torch.cuda.synchronize()
@@ -136,13 +143,17 @@ def test_e2e_pipelined_matches_device_resident_epoch(setup):
         assert torch.equal(a.params()[k2], b.params()[k2])
 
 
-def test_trainer_with_released_row_order_operands(setup):
+def test_trainer_with_released_row_order_operands(setup, monkeypatch):
     """release_canonical=True keeps only the degree-sorted coalesced operands
     on the device (the row-order arrays are freed); the epoch is unchanged —
     bit-identical to the trainer that still holds both forms."""
     import paper_2605_29346_b200 as gbm
+    import paper_2605_29346_b200.graph as G
+    import paper_2605_29346_b200.models as Mo
     from paper_2605_29346_b200.models import GCNTrainer
 
+    monkeypatch.setattr(G, "SPMM_SORT_MIN_NNZ", 0)
+    monkeypatch.setattr(Mo, "SPMM_SORT_MIN_NNZ", 0)
     gb, g0, (off, tgt, t_off, t_rows), X, y, (V, F, Hd, C) = setup
     g = gbm.generate(gbm.GraphGenSpec("power-law", V, 10556, exponent=2.1), 42)
     a = GCNTrainer(g0, F, Hd, C, seed=0, coalesced=True)
