@@ -547,14 +547,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
                  : "memory");
 }
 
+// Split-K reduction: 8 lanes per output stride the splits (independent
+// loads in flight instead of one dependent chain), fixed-order butterfly.
 __global__ void tn_reduce_kernel(int64_t M, int64_t N, int splits, const float *__restrict__ partials,
                                  float *C, int64_t ldc) {
   const int64_t total = M * N;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  const int sub = (int)(threadIdx.x & 7);
+  const unsigned mask8 = 0xffu << (threadIdx.x & 24);  // this output's 8 lanes
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; t < total;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 3) {
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += partials[(int64_t)z * total + t];
-    C[(t / N) * ldc + (t % N)] = s;
+    for (int z = sub; z < splits; z += 8) s += partials[(int64_t)z * total + t];
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(mask8, s, o, 8);
+    if (sub == 0) C[(t / N) * ldc + (t % N)] = s;
   }
 }
 
@@ -748,7 +754,7 @@ int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, con
     case 64: GNN_TRY(launch_tn<64>(ta, tb, p, st)); break;
     default: GNN_TRY(launch_tn<128>(ta, tb, p, st)); break;
   }
-  tn_reduce_kernel<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(M, N, splits, p.partials, C, ldc);
+  tn_reduce_kernel<<<(unsigned)ceil_div(M * N * 8, 256), 256, 0, st>>>(M, N, splits, p.partials, C, ldc);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
