@@ -37,3 +37,31 @@ def test_by_degree_keeps_rows(monkeypatch, slab):
         a, b = int(so.offsets[i]), int(so.offsets[i + 1])
         assert torch.equal(so.cols[a:b], cols[off[r]:off[r + 1]])
         assert torch.equal(so.vals[a:b], vals[off[r]:off[r + 1]])
+
+
+def test_spmm_operand_selection(monkeypatch):
+    """Which form gnn_spmm runs on: the degree-sorted copy only for topology /
+    multiplicity weights, K <= 64 in float4 lanes, operands above the size
+    threshold; a released operand always resolves to its sorted form."""
+    monkeypatch.setattr(G, "SPMM_SORT_MIN_NNZ", 100)
+    rng = np.random.default_rng(1)
+    R = 300
+    deg = rng.integers(0, 9, R)
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(deg)])).long()
+    nnz = int(off[-1])
+    cols = torch.from_numpy(rng.integers(0, R, nnz)).int()
+    plain = G.SparseOperand(R, R, off, cols)
+    X16, Y16 = torch.zeros(R, 16), torch.zeros(R, 16)
+    assert G.spmm_operand(plain, X16, Y16).row_ids is not None
+    assert G.spmm_operand(plain, torch.zeros(R, 128), torch.zeros(R, 128)) is plain  # K > 64
+    assert G.spmm_operand(plain, torch.zeros(R, 6), torch.zeros(R, 6)) is plain      # K % 4
+    assert G.spmm_operand(plain, X16, Y16, heads=2) is plain
+    assert G.spmm_operand(plain, X16, Y16, vals=torch.ones(nnz)) is plain           # edge values
+    weighted = G.SparseOperand(R, R, off, cols, vals=torch.rand(nnz))
+    assert G.spmm_operand(weighted, X16, Y16) is weighted  # general values: CSR edge order
+    monkeypatch.setattr(G, "SPMM_SORT_MIN_NNZ", nnz + 1)
+    assert G.spmm_operand(plain, X16, Y16) is plain  # small operand: row order
+    plain.release_row_order()
+    assert G.spmm_operand(plain, X16, Y16) is plain.by_degree()
+    with pytest.raises(RuntimeError):
+        plain.view()
