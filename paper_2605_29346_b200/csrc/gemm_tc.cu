@@ -17,6 +17,7 @@
 //   warps 4-7   split warps: A -> A_hi (in place) + A_lo (second buffer)
 //   warps 8-11  epilogue warpgroup: tcgen05.ld (32x32b) -> bias/relu -> global
 // TMEM holds two accumulators so the epilogue of tile i overlaps tile i+1.
+#include <algorithm>
 #include <cuda.h>
 
 #include <cstdio>
@@ -700,10 +701,28 @@ static void tn_plan(int64_t M, int64_t N, int64_t K, int64_t &mtiles, int64_t &n
   mtiles = ceil_div(M, kTcM);
   ntiles = ceil_div(N, tn_nb(N));
   nkb = (int)ceil_div(K, kTcBK);
-  int64_t want = 2 * (int64_t)sm_count();  // units
-  int64_t sp = ceil_div(want, mtiles * ntiles);
-  if (sp > nkb) sp = nkb;
-  kbps = (int)ceil_div(nkb, sp);
+  // Units = (m-tile, n-tile, k-split) on a persistent grid of min(units, SMs)
+  // CTAs: pick the split count that minimises the busiest CTA's k-blocks
+  // (e.g. 602x16 over 233K rows: 60 splits -> 300 units on 148 SMs leaves 4
+  // CTAs with 3 units = 1.48x the balanced time; 59 splits -> 295 units, at
+  // most 2 per CTA).  Each unit also pays ~2 k-blocks of pipeline fill and
+  // accumulator handoff; ties go to fewer splits (smaller partial buffer).
+  const int64_t sms = sm_count();
+  const int64_t tiles = mtiles * ntiles;
+  int64_t best_sp = 1, best_cost = -1;
+  const int64_t max_sp = std::min<int64_t>(nkb, 4 * sms);
+  for (int64_t sp = 1; sp <= max_sp; ++sp) {
+    const int64_t kb_each = ceil_div((int64_t)nkb, sp);
+    const int64_t sp_real = ceil_div((int64_t)nkb, kb_each);
+    const int64_t units = tiles * sp_real;
+    const int64_t grid = units < sms ? units : sms;
+    const int64_t cost = ceil_div(units, grid) * (kb_each + 2);  // +2: per-unit fill / handoff
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_sp = sp;
+    }
+  }
+  kbps = (int)ceil_div((int64_t)nkb, best_sp);
   splits = (int)ceil_div(nkb, kbps);
 }
 

@@ -7,7 +7,7 @@ set -euo pipefail
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
 src=$root/paper_2605_29346_b200/csrc
-out=$root/build_var/$name
+out=${GNN_VARIANT_DIR:-$root/build_var}/$name
 mkdir -p "$out"
 objs=()
 for f in "$src"/*.cu; do
