@@ -70,10 +70,10 @@ def _default_edges_per_warp(nnz: int, sms: int) -> int:
     enough to amortise row-bound loads and split-row arrivals, short enough for
     ~56k warps of parallelism); smaller graphs shrink it so every SM still
     gets several waves."""
-    p = 2048
+    p = int(os.environ.get("GNN_SPMM_P", "2048"))
     while p > 256 and nnz // p < sms * 64:
         p //= 2
-    return p
+    return p // 4 * 4
 
 
 # rows of degree <= this go to the SpMM's group-per-row kernel (power-law tail):
