@@ -356,6 +356,10 @@ def run_ours(args, rank, world):
     if world > 1:
         torch.distributed.barrier()
     peak_train = torch.cuda.max_memory_allocated(dev)
+    # SURVEY §8d cross-check: the driver's view (cudaMemGetInfo) of device memory in use
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    dev_used = total_b - free_b
+    torch_reserved = torch.cuda.memory_reserved(dev)
     loss_val = float(tr.loss.item())
 
     # ---- e2e: host buffers in, loss out, copies inside the timed region.  The
@@ -474,6 +478,8 @@ def run_ours(args, rank, world):
                     "analytic_graph_plus_tensors": round(analytic / 2**20, 1),
                     "train_over_analytic": round(peak_train / analytic, 3),
                     "setup_peak_incl_device_build": round(setup_peak / 2**20, 1),
+                    "cudaMemGetInfo_used_mb": round(dev_used / 2**20, 1),
+                    "torch_reserved_mb": round(torch_reserved / 2**20, 1),
                     "note": "train phase: resident degree-sorted coalesced CSR+CSC (packed column + "
                             "multiplicity words, row_ids), X at "
                             "row stride 608, activations, workspaces; analytic = canonical "
