@@ -325,6 +325,7 @@ def run_ours(args, rank, world):
                            .integers(0, C, V)).pin_memory()
 
     setup_peak = torch.cuda.max_memory_allocated(dev)
+    torch.cuda.empty_cache()  # return the setup temporaries (radix-sort scratch) to the driver
     torch.cuda.reset_peak_memory_stats(dev)
     base_alloc = torch.cuda.memory_allocated(dev)
     tr = GCNTrainer(g, F, Hd, C, seed=P["seed"], coalesced=args.layout == "coalesced")

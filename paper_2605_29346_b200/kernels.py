@@ -9,6 +9,7 @@ CUDA graph (no allocation, no host sync inside).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -167,7 +168,7 @@ class HeadCall:
     Z = P W + b, softmax-CE (dZ scaled 1/M), dW = P^T dZ, db = colsum(dZ),
     dP = (dZ W^T) / deg."""
 
-    FUSED_MAX = 64
+    FUSED_MAX = int(os.environ.get("GNN_HEAD_FUSED_MAX", "64"))
 
     def __init__(self, P, W, b, labels, dP, dW, db, loss, deg_offsets=None):
         self.lib = _lib.lib()
