@@ -354,13 +354,9 @@ class DistGCNTrainer:
             elif not overlap:
                 k_agg1 = SpmmCall(A, self.H1f, self.Y1, flags=N_ | B_ | R_, bias=self.b1)
                 k_agg2 = SpmmCall(A, self.Y1f, self.P2, flags=N_)
-            if hidden > HeadCall.FUSED_MAX or classes > HeadCall.FUSED_MAX:
-                raise NotImplementedError(
-                    "row-partitioned GCN: the 1/V_global-scaled output layer is the fused "
-                    f"kernel (hidden, classes <= {HeadCall.FUSED_MAX})")
+            # loss and dZ scaled 1/V_global: the all-reduce sums to the single-GPU mean
             k_head = HeadCall(self.P2, self.W2, self.b2, self.labels, self.dP2, self.dW2,
-                              self.db2, self.loss, deg_offsets=deg)
-            k_head.scale = 1.0 / V
+                              self.db2, self.loss, deg_offsets=deg, scale=1.0 / V)
             if peer:
                 k_bagg2 = self._deferred("bagg2")
                 k_bagg1 = self._deferred("bagg1")
@@ -381,7 +377,7 @@ class DistGCNTrainer:
         self.phases = [
             ("A", [], [("X.W1", k_gemm1)], ("gather", self.H1f)),
             ("B", pre["agg1"], [("agg1", k_agg1)], ("gather", self.Y1f)),
-            ("C", pre["agg2"], [("agg2", k_agg2), ("head", self._run_head if n > 0 else zero)],
+            ("C", pre["agg2"], [("agg2", k_agg2), ("head", k_head if n > 0 else zero)],
              ("gather", self.dP2f)),
             ("D", pre["bagg2"], [("bagg2", k_bagg2), ("mask_norm_db1", k_norm1)],
              ("gather", self.dZ1f)),
@@ -417,14 +413,6 @@ class DistGCNTrainer:
                                   mask=self.Y1),
             "bagg1": PeerSpmmCall(part.AT, ptrs["dZ1"], lg, ld, hd, self.dH1),
         }
-
-    def _run_head(self):
-        h = self._head
-        _lib.check(h.lib.gnn_gcn_head_scaled(
-            h.M, h.Din, h.C, h.P.data_ptr(), h.P.stride(0), h.W.data_ptr(), h.b.data_ptr(),
-            h.labels.data_ptr(), h.deg.data_ptr(), h.scale, h.dP.data_ptr(), h.dP.stride(0),
-            h.dW.data_ptr(), h.db.data_ptr(), h.loss.data_ptr(), h.ws.data_ptr(), h.ws.numel(),
-            _lib.stream_handle(h.dev)), "gcn_head")
 
     def set_inputs(self, X_local, labels_local, non_blocking=False):
         _lib.copy_rows(self.X, X_local)

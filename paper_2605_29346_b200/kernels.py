@@ -163,18 +163,22 @@ class AdamCall:
 class HeadCall:
     """Fused output layer: logits, mean cross-entropy, dP (degree-normed), dW, db.
 
-    The fused kernel (gnn_gcn_head) covers Din, C <= 64; wider layers (e.g. the
-    172 classes of the papers100M shape) run the same math as library calls:
-    Z = P W + b, softmax-CE (dZ scaled 1/M), dW = P^T dZ, db = colsum(dZ),
-    dP = (dZ W^T) / deg."""
+    The fused kernel (gnn_gcn_head_scaled) covers Din, C <= 64; wider layers
+    (e.g. the 172 classes of the papers100M shape) run the same math as
+    library calls: Z = P W + b, softmax-CE (dZ scaled), dW = P^T dZ,
+    db = colsum(dZ), dP = (dZ W^T) / deg.  ``scale`` multiplies the summed
+    loss and dZ: 1/M (the default) is the mean over these rows; a row-
+    partitioned rank passes 1/V_global so the all-reduced loss and gradients
+    equal the single-GPU mean."""
 
     FUSED_MAX = int(os.environ.get("GNN_HEAD_FUSED_MAX", "64"))
 
-    def __init__(self, P, W, b, labels, dP, dW, db, loss, deg_offsets=None):
+    def __init__(self, P, W, b, labels, dP, dW, db, loss, deg_offsets=None, scale=None):
         self.lib = _lib.lib()
         self.dev = P.device
         self.M, self.Din = P.shape
         self.C = W.shape[1]
+        self.scale = float(1.0 / self.M if scale is None else scale)
         self.P, self.W, self.b, self.labels, self.dP = P, W, b, labels, dP
         self.dW, self.db, self.loss, self.deg = dW, db, loss, deg_offsets
         self.fused = self.Din <= self.FUSED_MAX and self.C <= self.FUSED_MAX
@@ -183,7 +187,7 @@ class HeadCall:
             self.Z = torch.empty(self.M, self.C, **f32)
             self.dZ = torch.empty(self.M, self.C, **f32)
             self._parts = [GemmCall(P, W, self.Z, bias=b),
-                           XentCall(self.Z, labels, loss, dZ=self.dZ, grad_scale=1.0 / self.M),
+                           XentCall(self.Z, labels, loss, dZ=self.dZ, grad_scale=self.scale),
                            GemmCall(P, self.dZ, dW, trans_a=True),
                            ColsumCall(self.dZ, db),
                            GemmCall(self.dZ, W, dP, trans_b=True)]
@@ -197,13 +201,16 @@ class HeadCall:
         if not self.fused:
             for c in self._parts:
                 c()
+            if self.scale * self.M != 1.0:  # softmax_xent's loss is the mean over M rows
+                self.loss.mul_(self.scale * self.M)
             return
-        _lib.check(self.lib.gnn_gcn_head(
+        _lib.check(self.lib.gnn_gcn_head_scaled(
             self.M, self.Din, self.C, self.P.data_ptr(), self.P.stride(0), self.W.data_ptr(),
             self.b.data_ptr(), self.labels.data_ptr(),
-            self.deg.data_ptr() if self.deg is not None else None, self.dP.data_ptr(),
-            self.dP.stride(0), self.dW.data_ptr(), self.db.data_ptr(), self.loss.data_ptr(),
-            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "gcn_head")
+            self.deg.data_ptr() if self.deg is not None else None, self.scale,
+            self.dP.data_ptr(), self.dP.stride(0), self.dW.data_ptr(), self.db.data_ptr(),
+            self.loss.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+            _lib.stream_handle(self.dev)), "gcn_head")
 
 
 class ColsumCall:

@@ -141,3 +141,31 @@ def test_split_local_remote_partitions_rows(env, P):
                     assert np.array_equal(c[o[v]:o[v + 1]], row[sel])
                     if vals is not None:
                         assert np.array_equal(vv[o[v]:o[v + 1]], vals[off[v]:off[v + 1]][sel])
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_virtual_ranks_wide_output_layer(env, P):
+    """More classes than the fused head takes (library-call head, loss and dZ
+    scaled 1/V_global per rank): the all-reduced loss and gradients still
+    equal the single-process oracle."""
+    from paper_2605_29346_b200.dist import DistGCNTrainer, LocalExchange, RowPartition, step_virtual
+
+    gb, g, X, _ = env
+    V, C = g.num_vertices, 100
+    y = np.random.default_rng(2).integers(0, C, V)
+    parts = [RowPartition(g, P, r) for r in range(P)]
+    trs = [DistGCNTrainer(p, 64, 16, C, seed=0, overlap=P > 1) for p in parts]
+    assert not trs[0]._head.fused
+    for p, t in zip(parts, trs):
+        t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
+    step_virtual(trs, LocalExchange(P), adam=False)
+    torch.cuda.synchronize()
+    off, tgt = g.offsets, g.targets
+    t_off, t_rows, _ = og.transpose(V, V, off, tgt)
+    pr = {k: v.double().cpu().numpy() for k, v in trs[0].params().items()}
+    ref = oo.gcn2_step(off, tgt, t_off, t_rows, X, pr["W1"], pr["b1"], pr["W2"], pr["b2"], y)
+    for t in trs:
+        assert abs(t.loss.item() - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+        for k, gv in t.grads().items():
+            ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
+            assert ok, (P, k, worst)
