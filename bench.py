@@ -671,7 +671,7 @@ def run_reference(args):
     return {"metric": "gcn_epoch_ms", "value": round(v, 1), "unit": "ms", "n_gpus": args.gpus,
             "device": "cpu (the reference path is host code; n_gpus = the run's N)",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 1),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gsbench power-law restatement, seed 42)",
             "config": {"workload": "2-layer GCN full-graph epoch, Reddit-shape power-law graph",
                        "V": V, "E": E, "K": F, "hidden": Hd, "classes": C},
