@@ -78,6 +78,24 @@ class SharedHeadsCall:
             self.ws.numel(), _lib.stream_handle(self.dev)), "spmm_shared_heads")
 
 
+class ParallelCall:
+    """Two independent launches: ``side`` on a forked stream, ``main`` on the
+    current one, joined before returning (fork/join events; capturable into
+    the epoch's CUDA graph as two branches)."""
+
+    def __init__(self, main, side, dev):
+        self.main, self.side = main, side
+        self.stream = torch.cuda.Stream(dev)
+
+    def __call__(self):
+        cur = torch.cuda.current_stream(self.stream.device)
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            self.side()
+        self.main()
+        cur.wait_stream(self.stream)
+
+
 class GemmCall:
     """C = op(A) op(B) (+bias)(relu)."""
 

@@ -853,6 +853,24 @@ class GATTrainer(_FusedEpoch):
                                          self.dWh1, self.dal1, self.dar1, H)
         k["X^T.dWh1"] = GemmCall(self.X, self.dWh1, self.dW1, trans_a=True)
         k["adam"] = AdamCall(plist, self.grads_, lr=lr)
+        if os.environ.get("GNN_GAT_CONCURRENT", "1") != "0":
+            # independent pairs run as two graph branches: the CSR row sums
+            # (der) beside the CSC column sums (del, random edge-id gathers),
+            # and the two weight-gradient-side GEMMs of layer 2
+            from .kernels import ParallelCall
+
+            out = {}
+            for name, call in k.items():
+                if name in ("del2", "del1", "dWh2.W2^T"):
+                    continue
+                if name in ("der2", "der1"):
+                    dl = "del" + name[-1]
+                    out[name + "|" + dl] = ParallelCall(call, k[dl], dev)
+                elif name == "Y1^T.dWh2":
+                    out[name + "|dWh2.W2^T"] = ParallelCall(call, k["dWh2.W2^T"], dev)
+                else:
+                    out[name] = call
+            k = out
         self.k = k
 
     def schedule(self):
