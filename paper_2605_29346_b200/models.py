@@ -670,6 +670,29 @@ class GIN(torch.nn.Module):
 
 
 # ======================================================= fused trainers (2)
+def _parallelize(k: dict, pairs: dict, dev) -> dict:
+    """Schedule rewrite: each ``main`` name in ``pairs`` becomes one
+    ParallelCall running its listed (mutually independent) side launches on a
+    forked stream, at main's position; the side entries leave the list."""
+    from .kernels import ParallelCall
+
+    sides = {n for v in pairs.values() for n in v}
+    out = {}
+    for name, call in k.items():
+        if name in sides:
+            continue
+        if name in pairs:
+            calls = [k[n] for n in pairs[name]]
+
+            def side(calls=calls):
+                for c in calls:
+                    c()
+            out["|".join([name] + pairs[name])] = ParallelCall(call, side, dev)
+        else:
+            out[name] = call
+    return out
+
+
 class _FusedEpoch:
     """Shared driver of the fused full-graph trainers: ``schedule()`` lists
     the epoch's pre-bound launches; ``step()`` runs them eagerly,
@@ -857,20 +880,8 @@ class GATTrainer(_FusedEpoch):
             # independent pairs run as two graph branches: the CSR row sums
             # (der) beside the CSC column sums (del, random edge-id gathers),
             # and the two weight-gradient-side GEMMs of layer 2
-            from .kernels import ParallelCall
-
-            out = {}
-            for name, call in k.items():
-                if name in ("del2", "del1", "dWh2.W2^T"):
-                    continue
-                if name in ("der2", "der1"):
-                    dl = "del" + name[-1]
-                    out[name + "|" + dl] = ParallelCall(call, k[dl], dev)
-                elif name == "Y1^T.dWh2":
-                    out[name + "|dWh2.W2^T"] = ParallelCall(call, k["dWh2.W2^T"], dev)
-                else:
-                    out[name] = call
-            k = out
+            k = _parallelize(k, {"der2": ["del2"], "der1": ["del1"],
+                                 "Y1^T.dWh2": ["dWh2.W2^T"]}, dev)
         self.k = k
 
     def schedule(self):
