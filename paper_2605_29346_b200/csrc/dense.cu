@@ -354,6 +354,48 @@ __global__ void __launch_bounds__(256) mask_norm_colsum_kernel(
   }
 }
 
+// float4 form (N % 4 == 0, 16-byte rows): a thread owns 4 columns of a row,
+// so the row's 1/deg is computed once per 4 values instead of per value.
+template <int C4P>
+__global__ void __launch_bounds__(256) mask_norm_colsum_vec_kernel(
+    int64_t M, int64_t N, const float *__restrict__ X, int64_t ldx, const float *__restrict__ mask,
+    int64_t ldm, const int64_t *__restrict__ deg_offsets, float *out, int64_t ldo,
+    float *partials, int64_t rpb) {
+  constexpr int SLOTS = 256 / C4P;
+  __shared__ float4 red[SLOTS][C4P];
+  const int s = threadIdx.x / C4P, q = threadIdx.x % C4P;
+  const int64_t n4 = N / 4;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = min(M, r0 + rpb);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (q < n4) {
+#pragma unroll 4
+    for (int64_t r = r0 + s; r < r1; r += SLOTS) {
+      float4 v = *reinterpret_cast<const float4 *>(X + r * ldx + 4 * q);
+      if (mask) {
+        const float4 m = *reinterpret_cast<const float4 *>(mask + r * ldm + 4 * q);
+        v = make_float4(m.x > 0.f ? v.x : 0.f, m.y > 0.f ? v.y : 0.f, m.z > 0.f ? v.z : 0.f,
+                        m.w > 0.f ? v.w : 0.f);
+      }
+      acc = make_float4(acc.x + v.x, acc.y + v.y, acc.z + v.z, acc.w + v.w);
+      if (out) {
+        const float w = deg_offsets ? inv_deg_of(deg_offsets, r) : 1.f;
+        *reinterpret_cast<float4 *>(out + r * ldo + 4 * q) = make_float4(v.x * w, v.y * w, v.z * w, v.w * w);
+      }
+    }
+  }
+  red[s][q] = acc;
+  __syncthreads();
+  if (s == 0 && q < n4 && partials) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < SLOTS; ++k) {
+      const float4 a = red[k][q];
+      t = make_float4(t.x + a.x, t.y + a.y, t.z + a.z, t.w + a.w);
+    }
+    *reinterpret_cast<float4 *>(partials + (int64_t)blockIdx.x * N + 4 * q) = t;
+  }
+}
+
 // out[c] = sum_b partials[b*N + c]: one warp per column, lanes stride the
 // partials, fixed-order butterfly (deterministic).  A thread-per-column loop
 // over ~500 partials was a 46 us chain of dependent loads for N = 16.
@@ -540,7 +582,21 @@ int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, cons
   const int64_t rpb = reduce_rows_per_block(M);
   const int64_t nb = ceil_div(M, rpb);
   float *partials = colsum ? static_cast<float *>(ws) : nullptr;
-  if (N <= 16)
+  const auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool vec = N % 4 == 0 && N <= 64 && ldx % 4 == 0 && al16(X) &&
+                   (!mask || (ldm % 4 == 0 && al16(mask))) && (!out || (ldo % 4 == 0 && al16(out))) &&
+                   (!partials || al16(partials));
+  if (vec) {
+    if (N <= 16)
+      mask_norm_colsum_vec_kernel<4><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                                   deg_offsets, out, ldo, partials, rpb);
+    else if (N <= 32)
+      mask_norm_colsum_vec_kernel<8><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                                   deg_offsets, out, ldo, partials, rpb);
+    else
+      mask_norm_colsum_vec_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
+                                                                    deg_offsets, out, ldo, partials, rpb);
+  } else if (N <= 16)
     mask_norm_colsum_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
                                                              deg_offsets, out, ldo, partials, rpb);
   else if (N <= 64)

@@ -152,3 +152,35 @@ def test_gcn_head_matches_float64(gb, M, Din, C, with_deg):
                                 (dW, ref_dW, Pd.abs().T @ dza), (db, ref_db, dza.sum(0))):
         err = (got.double() - ref).abs()
         assert bool((err <= 1e-5 * (abs_scale + ref.abs()) + 1e-12).all()), float(err.max())
+
+
+@pytest.mark.parametrize("N", [4, 12, 16, 41, 64, 100])
+@pytest.mark.parametrize("with_mask,with_deg", [(True, True), (False, True), (True, False)])
+def test_mask_norm_colsum(gb, N, with_mask, with_deg):
+    """gnn_mask_norm_colsum (float4 and scalar forms): out = mask(X) / deg,
+    colsum = column sums of mask(X), in place allowed."""
+    from paper_2605_29346_b200 import _lib
+    from paper_2605_29346_b200.kernels import MaskNormColsumCall
+
+    rng = np.random.default_rng(N)
+    M = 50_001
+    X = torch.from_numpy(rng.uniform(-1, 1, (M, N)).astype(np.float32)).cuda()
+    Mk = torch.from_numpy(rng.uniform(-1, 1, (M, N)).astype(np.float32)).cuda()
+    deg = torch.from_numpy(np.concatenate([[0], np.cumsum(rng.integers(0, 4, M))])).cuda()
+    out = torch.empty_like(X)
+    cs = torch.empty(N, device="cuda")
+    MaskNormColsumCall(X, out, mask=Mk if with_mask else None,
+                       deg_offsets=deg if with_deg else None, colsum=cs)()
+    torch.cuda.synchronize()
+    x = X.double().cpu().numpy()
+    v = np.where(Mk.cpu().numpy() > 0, x, 0.0) if with_mask else x
+    d = np.diff(deg.cpu().numpy()).astype(np.float64)
+    w = np.divide(1.0, d, out=np.zeros_like(d), where=d > 0) if with_deg else np.ones(M)
+    assert np.allclose(out.cpu().numpy(), v * w[:, None], rtol=1e-6, atol=0)
+    ok, worst = oo.close(cs.cpu().numpy(), v.sum(0), np.abs(v).sum(0))
+    assert ok, worst
+    # in place
+    Y = X.clone()
+    MaskNormColsumCall(Y, Y, mask=Mk if with_mask else None,
+                       deg_offsets=deg if with_deg else None)()
+    assert torch.equal(Y, out)
