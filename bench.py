@@ -370,6 +370,9 @@ def run_ours(args, rank, world):
     # the next step's X / labels into the other; the first step's copy (prime)
     # is inside the timed region too.
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    # pinned host X at the device row stride (608): one linear DMA per step.
+    # (A [V, 602] host array works too — one 2-D DMA into the padded rows — but
+    # pitched H2D runs at ~16 GB/s here vs ~53 GB/s linear.)
     Xp_h = torch.zeros(V, tr.Fpad, dtype=torch.float32).pin_memory()
     Xp_h[:, :F].copy_(X_h)
     tr.capture_e2e_pipelined(Xp_h, y_h, loss_h)

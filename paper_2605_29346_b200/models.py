@@ -324,7 +324,10 @@ class GCNTrainer:
         ``prime_e2e()`` once (loads buffer 0), then ``run_e2e_pipelined(k)``
         for k = 0, 1, 2, ..."""
         assert X_host.is_pinned() and labels_host.is_pinned() and loss_host.is_pinned()
-        assert X_host.shape[1] == self.Fpad, "host X must use the device row stride (Fpad)"
+        # host X either already [V, Fpad] (one linear DMA: ~53 GB/s on the B200
+        # box) or [V, F] (one 2-D DMA into the padded rows: correct, but pitched
+        # H2D measured ~16 GB/s — keep the host copy at the device stride)
+        assert X_host.shape[1] in (self.F, self.Fpad)
         f32 = dict(dtype=torch.float32, device=self.dev)
         self._Xstore_b = torch.empty(self.V, self.Fpad, **f32)
         self.labels_b = torch.empty_like(self.labels)
@@ -349,7 +352,7 @@ class GCNTrainer:
                 cur = torch.cuda.current_stream(self.dev)
                 copy.wait_stream(cur)  # buffer 1-b is free: the previous step finished
                 with torch.cuda.stream(copy):
-                    nxt_store.copy_(X_host, non_blocking=True)
+                    self._load_x(nxt_store, X_host)
                     nxt_lab.copy_(labels_host, non_blocking=True)
                 for call in sched:
                     call()
@@ -370,10 +373,16 @@ class GCNTrainer:
         self._pipe = (graphs, keep, copy, main)
         return graphs
 
+    def _load_x(self, store, X_host):
+        if X_host.shape[1] == self.Fpad:
+            store.copy_(X_host, non_blocking=True)
+        else:
+            _lib.copy_rows(store[:, :self.F], X_host)
+
     def prime_e2e(self):
         """Load buffer 0 from the pinned host inputs (stream-ordered)."""
         X_host, labels_host, _ = self._pipe_host
-        self._Xstore.copy_(X_host, non_blocking=True)
+        self._load_x(self._Xstore, X_host)
         self.labels.copy_(labels_host, non_blocking=True)
 
     def run_e2e_pipelined(self, k: int):

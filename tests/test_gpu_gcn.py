@@ -119,17 +119,22 @@ def test_e2e_graph_matches_device_resident_epoch(setup):
         assert torch.equal(a.params()[k], b.params()[k])
 
 
-def test_e2e_pipelined_matches_device_resident_epoch(setup):
+@pytest.mark.parametrize("padded", [True, False])
+def test_e2e_pipelined_matches_device_resident_epoch(setup, padded):
     """Double-buffered e2e graphs (next step's inputs loaded under this step's
-    compute) train exactly like the device-resident epoch."""
+    compute) train exactly like the device-resident epoch; the host X is
+    either at the device row stride or the user's [V, F] array (2-D DMA)."""
     from paper_2605_29346_b200.models import GCNTrainer
 
     gb, g, _, X, y, (V, F, Hd, C) = setup
     a = GCNTrainer(g, F, Hd, C, seed=0)
     b = GCNTrainer(g, F, Hd, C, seed=0)
     a.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
-    Xp = torch.zeros(V, b.Fpad).pin_memory()
-    Xp[:, :F].copy_(torch.from_numpy(X))
+    if padded:
+        Xp = torch.zeros(V, b.Fpad).pin_memory()
+        Xp[:, :F].copy_(torch.from_numpy(X))
+    else:
+        Xp = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()
     yh = torch.from_numpy(y).pin_memory()
     loss_h = torch.zeros(1).pin_memory()
     b.capture_e2e_pipelined(Xp, yh, loss_h)
