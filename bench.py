@@ -556,7 +556,10 @@ def run_dist(args, rank, world):
     rng = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(10,)))
     X_all = rng.random((V, F), dtype=np.float32) * 2 - 1
     y_all = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(13,))).integers(0, C, V)
-    X_h = torch.from_numpy(np.ascontiguousarray(X_all[part.lo:part.hi])).pin_memory()
+    # this rank's rows, pinned at the device row stride (one linear H2D per step)
+    Fpad = -(-F // 32) * 32
+    X_h = torch.zeros(part.rows, Fpad, dtype=torch.float32).pin_memory()
+    X_h[:, :F].copy_(torch.from_numpy(X_all[part.lo:part.hi]))
     y_h = torch.from_numpy(np.ascontiguousarray(y_all[part.lo:part.hi])).pin_memory()
     del X_all
     torch.cuda.reset_peak_memory_stats(dev)
