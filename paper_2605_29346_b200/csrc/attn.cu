@@ -746,6 +746,55 @@ __global__ void __launch_bounds__(256) attn_proj_bwd_kernel(
     part[(int64_t)blockIdx.x * 2 * K + K + k] = sr;
   }
 }
+// float4 form (F % 4 == 0, 16-byte rows): row groups of K/4 lanes, each lane
+// 4 consecutive columns of one head; 16-byte loads / stores of Wh and dWh keep
+// more bytes in flight than the column-per-thread form above (which ran the
+// products-shape layer-2 pass at ~2.5 TB/s).  Per-block partials of
+// da = sum_v d{l,r}[v,h] * Wh[v,:] are reduced over the row groups in fixed
+// order.
+__global__ void __launch_bounds__(256) attn_proj_bwd_vec_kernel(
+    int64_t V, int H, int64_t F, const float *__restrict__ Wh, int64_t ldw,
+    const float *__restrict__ del, const float *__restrict__ der, const float *__restrict__ al,
+    const float *__restrict__ ar, float *dWh, int64_t ldd, float *part) {
+  __shared__ float4 red[2][256];
+  const int64_t K = (int64_t)H * F;
+  const int K4 = (int)(K / 4);
+  const int groups = (int)blockDim.x / K4;  // row groups per block
+  const int q = (int)threadIdx.x % K4, rg = (int)threadIdx.x / K4;
+  const int64_t per = ceil_div(V, gridDim.x);
+  const int64_t v0 = blockIdx.x * per, v1 = min(v0 + per, V);
+  float4 sl = make_float4(0.f, 0.f, 0.f, 0.f), sr = sl;
+  if (rg < groups) {
+    const int64_t k = 4 * (int64_t)q;
+    const int64_t h = k / F;
+    const float4 alk = *reinterpret_cast<const float4 *>(al + k);
+    const float4 ark = *reinterpret_cast<const float4 *>(ar + k);
+#pragma unroll 2
+    for (int64_t v = v0 + rg; v < v1; v += groups) {
+      const float4 x = ldg_f4(Wh + v * ldw + k);
+      float4 *dp = reinterpret_cast<float4 *>(dWh + v * ldd + k);
+      const float4 d = *dp;
+      const float dl = __ldg(del + v * H + h), dr = __ldg(der + v * H + h);
+      sl = make_float4(fmaf(x.x, dl, sl.x), fmaf(x.y, dl, sl.y), fmaf(x.z, dl, sl.z), fmaf(x.w, dl, sl.w));
+      sr = make_float4(fmaf(x.x, dr, sr.x), fmaf(x.y, dr, sr.y), fmaf(x.z, dr, sr.z), fmaf(x.w, dr, sr.w));
+      *dp = make_float4(fmaf(dr, ark.x, fmaf(dl, alk.x, d.x)), fmaf(dr, ark.y, fmaf(dl, alk.y, d.y)),
+                        fmaf(dr, ark.z, fmaf(dl, alk.z, d.z)), fmaf(dr, ark.w, fmaf(dl, alk.w, d.w)));
+    }
+  }
+  red[0][threadIdx.x] = sl;
+  red[1][threadIdx.x] = sr;
+  __syncthreads();
+  if (rg == 0) {
+    float4 tl = make_float4(0.f, 0.f, 0.f, 0.f), tr = tl;
+    for (int g = 0; g < groups; ++g) {
+      const float4 a = red[0][g * K4 + q], b = red[1][g * K4 + q];
+      tl = make_float4(tl.x + a.x, tl.y + a.y, tl.z + a.z, tl.w + a.w);
+      tr = make_float4(tr.x + b.x, tr.y + b.y, tr.z + b.z, tr.w + b.w);
+    }
+    *reinterpret_cast<float4 *>(part + (int64_t)blockIdx.x * 2 * K + 4 * q) = tl;
+    *reinterpret_cast<float4 *>(part + (int64_t)blockIdx.x * 2 * K + K + 4 * q) = tr;
+  }
+}
 __global__ void attn_proj_bwd_da_final_kernel(int64_t K, int nb, const float *__restrict__ part,
                                               float *dal, float *dar) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 2 * K;
@@ -1514,7 +1563,13 @@ int gnn_gat_attn_proj_bwd(int64_t V, int64_t heads, int64_t F, const float *Wh, 
   const int64_t K = heads * F;
   float *part = static_cast<float *>(ws);
   const int nb = (int)(V < kProjBlocks ? (V > 0 ? V : 1) : kProjBlocks);
-  if (V > 0) {
+  const bool vec = F % 4 == 0 && K / 4 <= 256 && ldw % 4 == 0 && ldd % 4 == 0 && al16(Wh) &&
+                   al16(dWh) && al16(a_l) && al16(a_r) && al16(part);
+  if (V > 0 && vec) {
+    attn_proj_bwd_vec_kernel<<<nb, 256, 0, st>>>(V, (int)heads, F, Wh, ldw, del, der, a_l, a_r,
+                                                 dWh, ldd, part);
+    GNN_LAUNCH_CHECK();
+  } else if (V > 0) {
     const int threads = (int)(K >= 256 ? 256 : ceil_div(K, 32) * 32);
     attn_proj_bwd_kernel<<<nb, threads, 0, st>>>(V, (int)heads, F, Wh, ldw, del, der, a_l, a_r,
                                                  dWh, ldd, part);
