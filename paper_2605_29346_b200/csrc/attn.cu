@@ -702,6 +702,43 @@ __global__ void attn_proj_kernel(int64_t V, int H, int64_t F, const float *__res
   }
 }
 
+// float4 form (F % 4 == 0, 16-byte rows): 4 lanes per (vertex, head), each
+// summing every 4th float4 of the head's F features, then a 4-lane butterfly;
+// a warp's loads cover 8 head rows contiguously (the thread-per-(v, h) form
+// above issues one scattered 4-byte load per feature).
+__global__ void attn_proj_vec_kernel(int64_t V, int H, int64_t F, const float *__restrict__ Wh,
+                                     int64_t ldw, const float *__restrict__ al,
+                                     const float *__restrict__ ar, float *el, float *er) {
+  const int64_t total = V * H;
+  const int gl = (int)(threadIdx.x & 3);
+  const unsigned gmask = 0xfu << (threadIdx.x & 28);
+  const int64_t F4 = F / 4;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2; t < total;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 2) {
+    const int64_t v = t / H;
+    const int h = (int)(t % H);
+    const float4 *x = reinterpret_cast<const float4 *>(Wh + v * ldw + h * F);
+    const float4 *a4 = reinterpret_cast<const float4 *>(al + h * F);
+    const float4 *r4 = reinterpret_cast<const float4 *>(ar + h * F);
+    float sl = 0.f, sr = 0.f;
+    for (int64_t j = gl; j < F4; j += 4) {
+      const float4 xv = ldg_f4(reinterpret_cast<const float *>(x + j));
+      const float4 a = __ldg(a4 + j), b = __ldg(r4 + j);
+      sl = fmaf(xv.x, a.x, fmaf(xv.y, a.y, fmaf(xv.z, a.z, fmaf(xv.w, a.w, sl))));
+      sr = fmaf(xv.x, b.x, fmaf(xv.y, b.y, fmaf(xv.z, b.z, fmaf(xv.w, b.w, sr))));
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
+      sl += __shfl_xor_sync(gmask, sl, o, 4);
+      sr += __shfl_xor_sync(gmask, sr, o, 4);
+    }
+    if (gl == 0) {
+      el[t] = sl;
+      er[t] = sr;
+    }
+  }
+}
+
 // One streaming pass over the vertices: thread = column k (< K <= 512, two
 // passes of 256 for wider K), each CTA a contiguous vertex range, 4 rows in
 // flight.  dWh[v,k] += del[v,h(k)] a_l[k] + der[v,h(k)] a_r[k] (in place) and
@@ -1540,6 +1577,12 @@ int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int6
   if (V == 0) return GNN_OK;
   if (!Wh || !a_l || !a_r || !el || !er) return GNN_ERR_INVALID_ARGUMENT;
   cudaStream_t st = as_stream(stream);
+  if (F % 4 == 0 && ldw % 4 == 0 && al16(Wh) && al16(a_l) && al16(a_r)) {
+    attn_proj_vec_kernel<<<grid_1d_a(V * heads * 4, 256), 256, 0, st>>>(V, (int)heads, F, Wh, ldw,
+                                                                         a_l, a_r, el, er);
+    GNN_LAUNCH_CHECK();
+    return GNN_OK;
+  }
   attn_proj_kernel<<<grid_1d_a(V * heads, 256), 256, 0, st>>>(V, (int)heads, F, Wh, ldw, a_l, a_r,
                                                               el, er);
   GNN_LAUNCH_CHECK();
