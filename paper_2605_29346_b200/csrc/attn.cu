@@ -330,6 +330,43 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
     m[h] = kNegInf;
     l[h] = 0.f;
   }
+  if (whole && hi - lo <= 32) {
+    // one edge per lane: the scores stay in registers for all three passes
+    // (the general path below re-derives them per pass); same accumulation
+    // order as the general path, so results are identical.  (Two edges per
+    // lane for rows <= 64 measured slower: registers.)
+    const int64_t e = lo + lane;
+    const bool ok = e < hi;
+    float sv[HM];
+    if (ok) {
+      load_scores<HM, GAT>(a, e, erow, sv);
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h) sv[h] = kNegInf;
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) m[h] = sv[h];
+    warp_max_reduce<HM>(m);
+    float ex[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+      ex[h] = ok ? __expf(sv[h] - m[h]) : 0.f;
+      l[h] = ex[h];
+    }
+    warp_sum_reduce<HM>(l);
+    if (ok) {
+      if (HM == 4 && a.H == 4) {
+        *reinterpret_cast<float4 *>(a.alpha + e * 4) =
+            make_float4(ex[0] * (1.f / l[0]), ex[1] * (1.f / l[1]), ex[2] * (1.f / l[2]),
+                        ex[3] * (1.f / l[3]));
+      } else {
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+          if (h < a.H) a.alpha[e * a.H + h] = ex[h] * (1.f / l[h]);
+      }
+    }
+    return;
+  }
   for (int64_t e = lo + lane; e < hi; e += 32) {
     float s[HM];
     load_scores<HM, GAT>(a, e, erow, s);
@@ -406,6 +443,39 @@ __device__ __forceinline__ void softmax_bwd_piece(const SoftmaxArgs &a, int64_t 
   float S[HM];
 #pragma unroll
   for (int h = 0; h < HM; ++h) S[h] = 0.f;
+  if (whole && hi - lo <= 32 && HM == 4 && a.H == 4) {
+    // one edge per lane: alpha / dalpha stay in registers for the apply
+    const int64_t e = lo + lane;
+    const bool ok = e < hi;
+    const float4 al = ok ? *reinterpret_cast<const float4 *>(a.alpha_in + e * 4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 da = ok ? *reinterpret_cast<const float4 *>(a.dalpha + e * 4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float alv[4] = {al.x, al.y, al.z, al.w}, dav[4] = {da.x, da.y, da.z, da.w};
+#pragma unroll
+    for (int h = 0; h < HM; ++h) S[h] = fmaf(alv[h < 4 ? h : 0], dav[h < 4 ? h : 0], 0.f);
+    warp_sum_reduce<HM>(S);
+    if (ok) {
+      float pre[4] = {1.f, 1.f, 1.f, 1.f};
+      if constexpr (GAT) {
+        const float4 l4 = ldg_f4(a.el + (int64_t)a.cols[e] * 4);
+        const float er0 = __ldg(a.er + r * 4), er1 = __ldg(a.er + r * 4 + 1),
+                    er2 = __ldg(a.er + r * 4 + 2), er3 = __ldg(a.er + r * 4 + 3);
+        pre[0] = l4.x + er0;
+        pre[1] = l4.y + er1;
+        pre[2] = l4.z + er2;
+        pre[3] = l4.w + er3;
+      }
+      float d[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        d[h] = alv[h] * (dav[h] - S[h < HM ? h : 0]);
+        if constexpr (GAT) d[h] = pre[h] > 0.f ? d[h] : a.slope * d[h];
+      }
+      *reinterpret_cast<float4 *>(a.ds + e * 4) = make_float4(d[0], d[1], d[2], d[3]);
+    }
+    return;
+  }
   for (int64_t e = lo + lane; e < hi; e += 32) {
 #pragma unroll
     for (int h = 0; h < HM; ++h)
