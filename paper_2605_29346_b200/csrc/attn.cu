@@ -297,12 +297,38 @@ __device__ __forceinline__ void warp_ml_reduce(float (&m)[HM], float (&l)[HM]) {
     }
 }
 
+// All-reduce of 4 per-head values over the warp in 10 shuffles instead of
+// 20: transpose-butterfly (after the bit-16 and bit-8 steps each lane holds
+// one head, reduced over the lanes that differ in those bits), a 3-step tree
+// over the remaining 8 lanes, then a broadcast of each head from lane 8h.
+// Deterministic (fixed pairing); every lane ends with all four totals.
+template <bool MAX>
+__device__ __forceinline__ void warp_allreduce4(float (&t)[4]) {
+  auto op = [](float x, float y) { return MAX ? fmaxf(x, y) : x + y; };
+  const int lane = (int)lane_id();
+  const bool u16 = (lane & 16) != 0, u8 = (lane & 8) != 0;
+  float a0 = u16 ? t[2] : t[0], a1 = u16 ? t[3] : t[1];
+  const float b0 = u16 ? t[0] : t[2], b1 = u16 ? t[1] : t[3];
+  a0 = op(a0, __shfl_xor_sync(kFull, b0, 16));
+  a1 = op(a1, __shfl_xor_sync(kFull, b1, 16));
+  float k = u8 ? a1 : a0;
+  k = op(k, __shfl_xor_sync(kFull, u8 ? a0 : a1, 8));
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) k = op(k, __shfl_xor_sync(kFull, k, o));
+#pragma unroll
+  for (int h = 0; h < 4; ++h) t[h] = __shfl_sync(kFull, k, 8 * h);
+}
+
 template <int HM>
 __device__ __forceinline__ void warp_sum_reduce(float (&t)[HM]) {
+  if constexpr (HM == 4) {
+    warp_allreduce4<false>(t);
+  } else {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int h = 0; h < HM; ++h) t[h] += __shfl_xor_sync(kFull, t[h], o);
+      for (int h = 0; h < HM; ++h) t[h] += __shfl_xor_sync(kFull, t[h], o);
+  }
 }
 
 // Forward statistics + normalisation of one row piece [lo,hi) of row r:
@@ -312,10 +338,14 @@ __device__ __forceinline__ void warp_sum_reduce(float (&t)[HM]) {
 // column ids and el rows are L1-resident after the first.
 template <int HM>
 __device__ __forceinline__ void warp_max_reduce(float (&t)[HM]) {
+  if constexpr (HM == 4) {
+    warp_allreduce4<true>(t);
+  } else {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int h = 0; h < HM; ++h) t[h] = fmaxf(t[h], __shfl_xor_sync(kFull, t[h], o));
+      for (int h = 0; h < HM; ++h) t[h] = fmaxf(t[h], __shfl_xor_sync(kFull, t[h], o));
+  }
 }
 
 template <int HM, bool GAT>
