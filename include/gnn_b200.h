@@ -58,6 +58,9 @@ typedef enum gnn_status {
 
 /* ---------------------------------------------------------------- misc */
 int gnn_abi_version(void);                 /* bumped on any signature change */
+/* "src:<sha256[:16] of the library's sources> git:<sha> sm_100a" — the
+ * provenance smoke() and bench.py check against the shipped sources. */
+const char *gnn_build_id(void);
 const char *gnn_strerror(int status);
 int gnn_last_cuda_error(void);             /* cudaError_t of the last GNN_ERR_CUDA */
 int gnn_device_sm_count(void);             /* SMs of the current device */

@@ -102,6 +102,7 @@ class SpmmPlan(C.Structure):
 # test suite checks that every declared symbol is exported.
 SIGNATURES = {
     "gnn_abi_version": (c_int, []),
+    "gnn_build_id": (C.c_char_p, []),
     "gnn_strerror": (C.c_char_p, [c_int]),
     "gnn_last_cuda_error": (c_int, []),
     "gnn_device_sm_count": (c_int, []),
@@ -295,8 +296,28 @@ def load_library(require_cuda: bool = True):
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            _check_provenance(lib)
             _lib = lib
     return _lib
+
+
+def build_id() -> str:
+    """The loaded library's embedded provenance string (gnn_build_id)."""
+    return load_library(False).gnn_build_id().decode()
+
+
+def _check_provenance(lib) -> None:
+    """Refuse a library not built from the sources next to it: the embedded
+    source hash must equal buildinfo.source_hash() of the shipped csrc/ and
+    include/ (GNN_ALLOW_STALE=1 skips the check, for debugging only)."""
+    from . import buildinfo
+
+    bid = lib.gnn_build_id().decode()
+    want = buildinfo.source_hash()
+    if f"src:{want} " not in bid + " " and os.environ.get("GNN_ALLOW_STALE") != "1":
+        raise ExtensionMissing(
+            f"{LIB_PATH} is stale: built from sources {bid!r}, the tree has src:{want}; "
+            "rebuild with __graft_entry__.build()")
 
 
 def lib():

@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t C,
       zy += __shfl_xor_sync(kFull, zy, o);
     }
     const float lse = mx + logf(se);
-    if (lane == 0) lsum += lse - zy;
+    // a label outside [0, C) poisons the loss (NaN) instead of reading past the row
+    if (lane == 0) lsum += (y >= 0 && y < C) ? lse - zy : NAN;
     if (dZ) {
 #pragma unroll
       for (int j = 0; j < NPL; ++j) {
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(256) softmax_xent_wide_kernel(int64_t M, int64
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
     const float lse = mx + logf(se);
     const int64_t y = labels[r];
-    if (lane == 0) lsum += lse - z[y];
+    if (lane == 0) lsum += (y >= 0 && y < C) ? lse - z[y] : NAN;  // bad label -> NaN loss, no OOB read
     if (dZ) {
       for (int64_t c = lane; c < C; c += 32) {
         float p = expf(z[c] - lse);
@@ -759,7 +760,7 @@ __global__ void __launch_bounds__(128) gcn_head_kernel(
     const float inv = 1.f / se;
     const int y = (int)__ldg(labels + r);
     const float zy = __shfl_sync(kFull, y < 32 ? z0 : z1, y & 31);
-    if (lane == 0) lsum += (double)(mx + logf(se) - zy);
+    if (lane == 0) lsum += (y >= 0 && y < C) ? (double)(mx + logf(se) - zy) : (double)NAN;
     const float d0 = v0 ? (e0 * inv - (lane == y ? 1.f : 0.f)) * scale : 0.f;
     const float d1 = v1 ? (e1 * inv - (lane + 32 == y ? 1.f : 0.f)) * scale : 0.f;
     ab0 += d0;
@@ -906,7 +907,7 @@ __global__ void __launch_bounds__(kHeadRowsPerCta, 2) gcn_head_rows_kernel(
   float4 *D4 = reinterpret_cast<float4 *>(Ds + tid * LDD);
 #pragma unroll
   for (int q = 0; q < C4; ++q) D4[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
-  if (valid) lrow = (double)(mx + logf(se) - zy);
+  if (valid) lrow = (y >= 0 && y < C) ? (double)(mx + logf(se) - zy) : (double)NAN;
   float rs = 1.f;
   if (valid && deg_offsets) {
     const int64_t dg = __ldg(deg_offsets + r + 1) - __ldg(deg_offsets + r);

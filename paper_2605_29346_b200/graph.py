@@ -708,9 +708,17 @@ def _stream_to_device(fh, dst: torch.Tensor, nbytes: int, chunk: int = 64 << 20)
         b = bufs[k & 1]
         if done[k & 1] is not None:
             done[k & 1].synchronize()  # the copy that last used this buffer has landed
-        got = fh.readinto(memoryview(b.numpy())[:n])
+        view = memoryview(b.numpy())[:n]
+        got = 0
+        while got < n:  # raw readinto may return short counts (pipes, FUSE, network FS)
+            r = fh.readinto(view[got:])
+            if not r:
+                break
+            got += r
         if got != n:
-            raise ParseError(0, "truncated CSR1 file")
+            # the reference's load_csr hits make_csr's shape check on a short
+            # array (graph.py:218-220, 95-96): ValueError, not ParseError
+            raise ValueError("truncated CSR1 file: offsets/targets shorter than the header says")
         flat[pos:pos + n].copy_(b[:n], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(st)
@@ -731,7 +739,7 @@ def load_csr(path, device=None) -> CsrGraph:
         magic = fh.read(4)
         if magic != _CSR_MAGIC:
             raise ParseError(1, f"bad magic {magic!r}, expected {_CSR_MAGIC!r}")
-        n, m = struct.unpack("<QQ", fh.read(16))
+        n, m = struct.unpack("<QQ", fh.read(16))  # struct.error on a short header, as the reference
         n, m = int(n), int(m)
         d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         d_tgt = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]

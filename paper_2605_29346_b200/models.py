@@ -148,7 +148,7 @@ class GCNTrainer:
         self.Fpad = -(-in_feats // 32) * 32
         self._Xstore = torch.empty(V, self.Fpad, **f32)
         self.X = self._Xstore[:, :in_feats]
-        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        self.labels = torch.zeros(V, dtype=torch.int64, device=dev)
         e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
         self.H1, self.Y1, self.P2 = e(hidden), e(hidden), e(hidden)
         self.dP2, self.dZ1, self.dH1 = e(hidden), e(hidden), e(hidden)
@@ -330,7 +330,7 @@ class GCNTrainer:
         assert X_host.shape[1] in (self.F, self.Fpad)
         f32 = dict(dtype=torch.float32, device=self.dev)
         self._Xstore_b = torch.empty(self.V, self.Fpad, **f32)
-        self.labels_b = torch.empty_like(self.labels)
+        self.labels_b = torch.zeros_like(self.labels)
         X_b = self._Xstore_b[:, :self.F]
         stores = [(self._Xstore, self.X, self.labels), (self._Xstore_b, X_b, self.labels_b)]
         self._pipe_host = (X_host, labels_host, loss_host)
@@ -819,7 +819,7 @@ class GATTrainer(_FusedEpoch):
         self.Fpad = -(-in_feats // 32) * 32
         self._Xstore = torch.zeros(V, self.Fpad, **f32)
         self.X = self._Xstore[:, :in_feats]
-        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        self.labels = torch.zeros(V, dtype=torch.int64, device=dev)
         # ---- activations / state tensors
         A, AT = g.csr(), g.csc(with_eid=True)
         self.A, self.AT = A, AT
@@ -947,7 +947,7 @@ class GINTrainer(_FusedEpoch):
         self.Fpad = -(-in_feats // 32) * 32
         self._Xstore = torch.zeros(V, self.Fpad, **f32)
         self.X = self._Xstore[:, :in_feats]
-        self.labels = torch.empty(V, dtype=torch.int64, device=dev)
+        self.labels = torch.zeros(V, dtype=torch.int64, device=dev)
         e = lambda k: torch.empty(V, k, **f32)  # noqa: E731
         self.H1, self.U1, self.Y1, self.H2, self.U2 = (e(hidden) for _ in range(5))
         self.dU2, self.dH2, self.dY1, self.dU1, self.dH1 = (e(hidden) for _ in range(5))

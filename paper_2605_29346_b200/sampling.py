@@ -114,9 +114,28 @@ def _i64(x, dev) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).to(dev)
 
 
-def sample_hop(graph: CsrGraph, frontier, fanout: int, state: tuple[int, int]):
-    """Device sample_hop: (src, dst) int64 device tensors of the hop's draws,
-    bit-exact with sampler.py:118-144 for the PCG64 stream ``state``."""
+def _pcg64_words(rng) -> tuple[int, int]:
+    """(state, inc) of a numpy PCG64 stream: a ``np.random.Generator`` over
+    PCG64 (the reference's argument, sampler.py:118-123) or a raw
+    ``(state, inc)`` tuple."""
+    if isinstance(rng, np.random.Generator):
+        bg = rng.bit_generator
+        if not isinstance(bg, np.random.PCG64):
+            raise ConfigError("device sample_hop reproduces numpy's PCG64 stream only")
+        st = bg.state["state"]
+        return int(st["state"]), int(st["inc"])
+    s, inc = rng
+    return int(s), int(inc)
+
+
+def sample_hop(graph: CsrGraph, frontier, fanout: int, rng):
+    """Device sample_hop (sampler.py:118-144): (src, dst) int64 device tensors
+    of the hop's draws, bit-exact with the reference for the same generator.
+
+    ``rng`` is the reference's ``np.random.Generator`` (PCG64): the draws use
+    its current stream position and, like ``rng.random(n)`` in the reference,
+    the generator is advanced past the n doubles consumed.  A raw PCG64
+    ``(state, inc)`` tuple is accepted too (used by the device pipeline)."""
     lib = _lib.lib()
     dev = graph.device
     fr = _i64(frontier, dev)
@@ -125,7 +144,7 @@ def sample_hop(graph: CsrGraph, frontier, fanout: int, state: tuple[int, int]):
     src = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     dst = torch.empty_like(src)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
-    s, inc = state
+    s, inc = _pcg64_words(rng)
     mask = (1 << 64) - 1
     with torch.cuda.device(dev):
         ws = _lib.workspace(lib.gnn_sample_hop_workspace(F), dev)
@@ -136,7 +155,23 @@ def sample_hop(graph: CsrGraph, frontier, fanout: int, state: tuple[int, int]):
                                       dst.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
                                       _lib.stream_handle(dev)), "sample_hop")
     n = int(count.item())  # one read per hop: sizes the next hop
+    if isinstance(rng, np.random.Generator) and n:
+        rng.bit_generator.advance(n)  # the reference consumed n doubles (sampler.py:142)
     return src[:n], dst[:n]
+
+
+def _check_seeds(seeds, num_vertices: int) -> np.ndarray:
+    """The reference's seed-batch checks (sampler.py:153-160): non-empty,
+    distinct, inside [0, V) — ConfigError otherwise."""
+    s = np.asarray(seeds.cpu() if isinstance(seeds, torch.Tensor) else seeds, dtype=np.int64)
+    s = s.reshape(-1)
+    if s.size == 0:
+        raise ConfigError("seed batch must be non-empty")
+    if np.unique(s).size != s.size:
+        raise ConfigError("seed vertices must be distinct")
+    if s.min() < 0 or s.max() >= num_vertices:
+        raise ConfigError("seed vertex id out of range")
+    return s
 
 
 class SubgraphBuilder:
@@ -145,13 +180,7 @@ class SubgraphBuilder:
 
     def __init__(self, num_vertices: int, seeds, device=None):
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        s = np.asarray(seeds.cpu() if isinstance(seeds, torch.Tensor) else seeds, dtype=np.int64)
-        if s.size == 0:
-            raise ConfigError("seed batch must be non-empty")
-        if np.unique(s).size != s.size:
-            raise ConfigError("seed vertices must be distinct")
-        if s.min() < 0 or s.max() >= num_vertices:
-            raise ConfigError("seed vertex id out of range")
+        s = _check_seeds(seeds, num_vertices)
         self.dev = dev
         self.num_vertices = num_vertices
         self.table = torch.full((num_vertices,), -1, dtype=torch.int32, device=dev)
@@ -304,6 +333,7 @@ class DeviceSampler:
         self.rng = torch.zeros(H, 4, dtype=torch.int64, device=dev)  # uint64 words
         self.seeds_h = torch.zeros(B, dtype=torch.int64).pin_memory()
         self.rng_h = torch.zeros(H, 4, dtype=torch.int64).pin_memory()
+        self._inflight = None  # event after the last replay's staging copies
         self.hops = []
         f_cap = B
         for h, fan in enumerate(config.fanouts):
@@ -325,6 +355,7 @@ class DeviceSampler:
     def _launch(self):
         lib, g, st = self.lib, self.g, _lib.stream_handle(self.dev)
         B = self.cfg.batch_size
+        self.err.zero_()  # an error flag never sticks to later batches
         self.seeds.copy_(self.seeds_h, non_blocking=True)
         self.rng.copy_(self.rng_h, non_blocking=True)
         _lib.check(lib.gnn_table_assign(self.table.data_ptr(), self.seeds.data_ptr(), B, 0, st),
@@ -359,10 +390,15 @@ class DeviceSampler:
                        "table_fill_dev")
 
     def _stage(self, seeds, rng: SeedLike):
-        s = np.asarray(seeds, dtype=np.int64)
+        s = np.asarray(seeds.cpu() if isinstance(seeds, torch.Tensor) else seeds, dtype=np.int64)
         if s.size != self.cfg.batch_size:
             raise ConfigError(f"expected {self.cfg.batch_size} seed vertices, got {s.size}")
+        s = _check_seeds(s, self.g.num_vertices)  # out-of-range ids would index offsets[] OOB
         base = _as_seed_sequence(rng, self.cfg.seed)
+        if self._inflight is not None:
+            # the previous replay's H2D copies read these pinned buffers: wait for them
+            self._inflight.synchronize()
+            self._inflight = None
         self.seeds_h.copy_(torch.from_numpy(s))
         words = []
         for h in range(1, self.cfg.num_hops + 1):
@@ -390,6 +426,9 @@ class DeviceSampler:
             self._launch()
         else:
             self.graph.replay()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self._inflight = ev
 
     def result(self):
         """(SampledSubgraph, IterationMetadata) with host arrays (synchronises)."""
