@@ -200,3 +200,46 @@ def test_sampled_gcn_training_lowers_the_loss(cuda):
         seeds = rng.choice(3000, 128, replace=False)
         losses.append(tr.step(seeds, rng=it).item())
     assert np.mean(losses[-5:]) < np.mean(losses[:5]) - 0.1, losses
+
+
+def test_sample_hop_takes_reference_generator(gb):
+    """sample_hop(graph, frontier, fanout, rng) with the reference's own
+    np.random.Generator (sampler.py:118-123): same draws as gsbench's
+    sample_hop (oracle restatement), and the generator ends at the same
+    stream position, so consecutive calls keep matching."""
+    from paper_2605_29346_b200.sampling import sample_hop
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 20_000, 400_000, exponent=2.1), 3)
+    off, tgt = g.offsets, g.targets
+    frontier = np.random.default_rng(0).choice(20_000, 300, replace=False)
+    r_dev = np.random.default_rng(77)
+    r_ref = np.random.default_rng(77)
+    for fan in (5, 3):
+        s, d = sample_hop(g, frontier, fan, r_dev)
+        rs, rd = osm.sample_hop(off, tgt, frontier, fan, r_ref)
+        assert np.array_equal(s.cpu().numpy(), rs) and np.array_equal(d.cpu().numpy(), rd)
+        assert r_dev.bit_generator.state == r_ref.bit_generator.state
+
+
+def test_device_sampler_rejects_bad_seeds(gb):
+    """ConfigError (as SubgraphBuilder / the reference) for duplicate or
+    out-of-range seeds — never an out-of-bounds device access; a replay after
+    a rejected batch still matches the oracle."""
+    from paper_2605_29346_b200.errors import ConfigError
+    from paper_2605_29346_b200.sampling import DeviceSampler, SampleConfig
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 5_000, 100_000, exponent=2.1), 9)
+    ds = DeviceSampler(g, SampleConfig(8, (4,)))
+    ds.capture()
+    with pytest.raises(ConfigError):
+        ds.run(np.array([1, 2, 3, 4, 5, 6, 7, 7]))
+    with pytest.raises(ConfigError):
+        ds.run(np.array([1, 2, 3, 4, 5, 6, 7, 5_000]))
+    with pytest.raises(ConfigError):
+        ds.run(np.array([-1, 2, 3, 4, 5, 6, 7, 8]))
+    seeds = np.arange(10, 18)
+    for it in range(3):  # back-to-back replays without a sync in between
+        ds.run(seeds + it, 5 + it)
+    sg, _ = ds.result()
+    l2g, *_ = osm.sample_minibatch(g.offsets, g.targets, seeds + 2, (4,), 7)
+    assert np.array_equal(sg.local_to_global, l2g)
