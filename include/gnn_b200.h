@@ -138,6 +138,32 @@ int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t stat
                           uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t *src,
                           int64_t *dst, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* Row-block build of the power-law graph for the 1D row partition (SURVEY
+ * §8e), without materialising the whole graph: the bit-exact edge stream of
+ * gnn_generate_powerlaw is regenerated in `chunk`-edge pieces and, in stream
+ * order, (src-lo, dst) of every edge with src in [lo,hi) is appended to
+ * r_key/r_val and (dst-lo, src) of every edge with dst in [lo,hi) to
+ * c_key/c_val (either pair may be NULL to skip it); count[2] (device)
+ * receives the two totals.  At most `capacity` pairs are written per output
+ * (the caller sizes it, e.g. the expected block size plus a margin, and
+ * re-runs with count's exact totals if count exceeds it).  Stable sorts of these pairs (gnn_sort_pairs) give rows
+ * lo..hi-1 of csr_from_edges (graph.py:106-114) and of its transpose. */
+size_t gnn_powerlaw_block_workspace(int64_t n, int64_t chunk);
+int gnn_powerlaw_block(int64_t n, int64_t m, const double *cdf, uint64_t state_hi,
+                       uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t lo, int64_t hi,
+                       int64_t chunk, int64_t capacity, int32_t *r_key, int32_t *r_val,
+                       int32_t *c_key, int32_t *c_val, int64_t *count, void *ws, size_t ws_bytes,
+                       gnn_stream_t stream);
+/* Stable LSD radix sort of int32 (key, val) pairs, keys in [0, key_limit). */
+size_t gnn_sort_pairs_workspace(int64_t n, int64_t key_limit);
+int gnn_sort_pairs(int64_t n, int64_t key_limit, const int32_t *keys, const int32_t *vals,
+                   int32_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes,
+                   gnn_stream_t stream);
+/* offsets[R+1] from sorted int32 row keys in [0, R) (= the CSR offsets). */
+size_t gnn_offsets_from_keys_workspace(int64_t R);
+int gnn_offsets_from_keys(int64_t n, int64_t R, const int32_t *sorted_keys, int64_t *offsets,
+                          void *ws, size_t ws_bytes, gnn_stream_t stream);
+
 /* --------------------------------------- sampled-block pipeline (ZeroGNN) */
 /* sample_hop (sampler.py:118-144), bit-exact with numpy's PCG64 Generator
  * whose (state, inc) is given as 128-bit hi/lo words: active = frontier
@@ -486,6 +512,17 @@ typedef struct gnn_adam_param {
 int gnn_adam_step(int nparams, const void *param_table /* device gnn_adam_param_t[nparams] */,
                   float lr, float beta1, float beta2, float eps, float weight_decay,
                   int64_t *step /* device */, gnn_stream_t stream);
+
+/* ------------------------------------------ synthetic input synthesis */
+/* X[r, k] (rows [row0, row0+rows) of a global [V, cols] matrix, row stride
+ * ldx) ~ U[-1, 1) as a hash of (seed, global index): partition-independent,
+ * so every rank of a row partition fills exactly the rows one GPU would.
+ * Labels likewise uniform in [0, classes).  Used for shapes whose inputs do
+ * not fit the host (papers100M: X = 56.9 GB). */
+int gnn_fill_uniform(float *X, int64_t ldx, int64_t rows, int64_t cols, int64_t row0,
+                     uint64_t seed, gnn_stream_t stream);
+int gnn_fill_labels(int64_t *y, int64_t n, int64_t row0, int64_t classes, uint64_t seed,
+                    gnn_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -133,6 +133,18 @@ SIGNATURES = {
         c_int,
         [c_i64, c_i64, c_ptr, c_u64, c_u64, c_u64, c_u64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_powerlaw_block_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_powerlaw_block": (
+        c_int,
+        [c_i64, c_i64, c_ptr, c_u64, c_u64, c_u64, c_u64, c_i64, c_i64, c_i64, c_i64, c_ptr,
+         c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_fill_uniform": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr]),
+    "gnn_fill_labels": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_u64, c_ptr]),
+    "gnn_sort_pairs_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_sort_pairs": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
+    "gnn_offsets_from_keys_workspace": (c_sz, [c_i64]),
+    "gnn_offsets_from_keys": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_sample_hop_workspace": (c_sz, [c_i64]),
     "gnn_sample_hop": (
         c_int,

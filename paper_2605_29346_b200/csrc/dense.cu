@@ -1007,6 +1007,207 @@ __global__ void gcn_head_reduce_warp_kernel(int64_t nb, int din, int C,
   }
 }
 
+// Wide output layer (C > 64, e.g. the 172 classes of the papers100M shape):
+// the [M, C] logits never exist in memory.  Thread per row, classes in
+// chunks of 32: pass 1 forms each chunk's logits from the row's P (registers)
+// and W (shared memory) and keeps an online max / sum; pass 2 recomputes the
+// chunk, forms dz, accumulates dP = dz W^T, and stages dz in shared memory
+// where each warp forms its 32 rows' share of dW = P^T dz (lane = class, DIN
+// register accumulators), reduced across warps in fixed order into per-thread
+// CTA accumulators.  Persistent grid: partials are [grid][din*C + C] and the
+// fixed-order warp reduce of the narrow head finishes dW / db / loss.
+constexpr int kWideT = 256;
+constexpr int kWideWarps = kWideT / 32;
+
+template <int DIN, int NCH>
+size_t head_wide_smem() {
+  constexpr int CP = NCH * 32;
+  return sizeof(float) * (size_t)(DIN * CP + CP + kWideT * (DIN + 4) + kWideT * 33 +
+                                  kWideWarps * (DIN + 1) * 32 + (DIN + 1) * CP);
+}
+
+template <int DIN, int NCH>
+__global__ void __launch_bounds__(kWideT, 1) gcn_head_wide_kernel(
+    int64_t M, int din, int C, const float *__restrict__ P, int64_t ldp,
+    const float *__restrict__ W, const float *__restrict__ b, const int64_t *__restrict__ labels,
+    const int64_t *__restrict__ deg_offsets, float scale, float *dP, int64_t lddp,
+    float *partials, double *lpart) {
+  constexpr int T = kWideT, CP = NCH * 32, LDP = DIN + 4, KR = DIN * 32 / T;
+  extern __shared__ __align__(16) float hw[];
+  float *Ws = hw;                    // [DIN][CP]
+  float *bs = Ws + DIN * CP;         // [CP]
+  float *Ps = bs + CP;               // [T][LDP]
+  float *Ds = Ps + T * LDP;          // [T][33]
+  float *St = Ds + T * 33;           // [warps][DIN+1][32]
+  float *Acc = St + kWideWarps * (DIN + 1) * 32;  // [DIN+1][CP] CTA dW / db (row DIN) partials
+  __shared__ double lred[kWideWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < DIN * CP; i += T) {
+    const int k = i / CP, c = i % CP;
+    Ws[i] = (k < din && c < C) ? W[(int64_t)k * C + c] : 0.f;
+  }
+  for (int c = tid; c < CP; c += T) bs[c] = c < C ? b[c] : 0.f;
+  for (int i = tid; i < (DIN + 1) * CP; i += T) Acc[i] = 0.f;
+  __syncthreads();
+  double lsum = 0.0;
+  const float4 *W4 = reinterpret_cast<const float4 *>(Ws);
+  for (int64_t r0 = (int64_t)blockIdx.x * T; r0 < M; r0 += (int64_t)gridDim.x * T) {
+    const int64_t r = r0 + tid;
+    const bool valid = r < M;
+    float p[DIN];
+#pragma unroll
+    for (int k = 0; k < DIN; ++k) p[k] = (valid && k < din) ? __ldg(P + r * ldp + k) : 0.f;
+#pragma unroll
+    for (int k = 0; k < DIN; k += 4)
+      *reinterpret_cast<float4 *>(Ps + tid * LDP + k) = make_float4(p[k], p[k + 1], p[k + 2], p[k + 3]);
+    const int64_t y = valid ? __ldg(labels + r) : -1;
+    // ---- pass 1: online max / sum of exp over the class chunks
+    float mx = -INFINITY, se = 0.f, zy = 0.f;
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+      float z[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = bs[ch * 32 + j];
+#pragma unroll
+      for (int k = 0; k < DIN; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 w = W4[(k * CP + ch * 32) / 4 + q];
+          z[4 * q] = fmaf(p[k], w.x, z[4 * q]);
+          z[4 * q + 1] = fmaf(p[k], w.y, z[4 * q + 1]);
+          z[4 * q + 2] = fmaf(p[k], w.z, z[4 * q + 2]);
+          z[4 * q + 3] = fmaf(p[k], w.w, z[4 * q + 3]);
+        }
+      float cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = ch * 32 + j;
+        if (c < C) cm = fmaxf(cm, z[j]);
+        if (c == y) zy = z[j];
+      }
+      const float nm = fmaxf(mx, cm);
+      float add = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (ch * 32 + j < C) add += __expf(z[j] - nm);
+      se = se * __expf(mx - nm) + add;
+      mx = nm;
+    }
+    const float inv = 1.f / se;
+    if (valid) lsum += (y >= 0 && y < C) ? (double)(mx + logf(se) - zy) : (double)NAN;
+    float rs = 1.f;
+    if (valid && deg_offsets) {
+      const int64_t dg = __ldg(deg_offsets + r + 1) - __ldg(deg_offsets + r);
+      rs = dg > 0 ? 1.f / (float)dg : 0.f;
+    }
+    float dp[DIN];
+#pragma unroll
+    for (int k = 0; k < DIN; ++k) dp[k] = 0.f;
+    // ---- pass 2: dz per chunk, dP, and this chunk's dW / db partials
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+      float z[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = bs[ch * 32 + j];
+#pragma unroll
+      for (int k = 0; k < DIN; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 w = W4[(k * CP + ch * 32) / 4 + q];
+          z[4 * q] = fmaf(p[k], w.x, z[4 * q]);
+          z[4 * q + 1] = fmaf(p[k], w.y, z[4 * q + 1]);
+          z[4 * q + 2] = fmaf(p[k], w.z, z[4 * q + 2]);
+          z[4 * q + 3] = fmaf(p[k], w.w, z[4 * q + 3]);
+        }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = ch * 32 + j;
+        z[j] = (valid && c < C) ? (__expf(z[j] - mx) * inv - (c == y ? 1.f : 0.f)) * scale : 0.f;
+        Ds[tid * 33 + j] = z[j];
+      }
+#pragma unroll
+      for (int k = 0; k < DIN; ++k) {
+        float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 w = W4[(k * CP + ch * 32) / 4 + q];
+          t0 = fmaf(z[4 * q], w.x, t0);
+          t1 = fmaf(z[4 * q + 1], w.y, t1);
+          t0 = fmaf(z[4 * q + 2], w.z, t0);
+          t1 = fmaf(z[4 * q + 3], w.w, t1);
+        }
+        dp[k] += t0 + t1;
+      }
+      __syncthreads();
+      // warp's 32 rows: lane = class column, DIN accumulators (+ db)
+      float a[DIN];
+#pragma unroll
+      for (int k = 0; k < DIN; ++k) a[k] = 0.f;
+      float ab = 0.f;
+#pragma unroll 4
+      for (int i = warp * 32; i < warp * 32 + 32; ++i) {
+        const float d = Ds[i * 33 + lane];
+        ab += d;
+#pragma unroll
+        for (int k = 0; k < DIN; k += 4) {
+          const float4 pv = *reinterpret_cast<const float4 *>(Ps + i * LDP + k);
+          a[k] = fmaf(pv.x, d, a[k]);
+          a[k + 1] = fmaf(pv.y, d, a[k + 1]);
+          a[k + 2] = fmaf(pv.z, d, a[k + 2]);
+          a[k + 3] = fmaf(pv.w, d, a[k + 3]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DIN; ++k) St[(warp * (DIN + 1) + k) * 32 + lane] = a[k];
+      St[(warp * (DIN + 1) + DIN) * 32 + lane] = ab;
+      __syncthreads();
+      // fixed-order cross-warp sum into the CTA accumulators (each (k, class)
+      // item has one owning thread: deterministic, no atomics)
+#pragma unroll
+      for (int q = 0; q < KR; ++q) {
+        const int k = warp + kWideWarps * q;
+        float t = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < kWideWarps; ++w2) t += St[(w2 * (DIN + 1) + k) * 32 + lane];
+        Acc[k * CP + ch * 32 + lane] += t;
+      }
+      if (warp == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < kWideWarps; ++w2) t += St[(w2 * (DIN + 1) + DIN) * 32 + lane];
+        Acc[DIN * CP + ch * 32 + lane] += t;
+      }
+      __syncthreads();
+    }
+    if (valid) {
+#pragma unroll
+      for (int k = 0; k < DIN; ++k)
+        if (k < din) dP[r * lddp + k] = dp[k] * rs;
+    }
+  }
+  const int64_t NPF = (int64_t)din * C + C;
+  float *out = partials + (int64_t)blockIdx.x * NPF;
+  for (int i = tid; i < (din + 1) * C; i += T) {
+    const int k = i / C, c = i % C;
+    out[i] = Acc[(k < din ? k : DIN) * CP + c];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+  if (lane == 0) lred[warp] = lsum;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < kWideWarps; ++w2) t += lred[w2];
+    lpart[blockIdx.x] = t;
+  }
+}
+
+int64_t head_wide_grid(int64_t M) {
+  const int64_t g = (int64_t)sm_count();
+  const int64_t need = ceil_div(M > 0 ? M : 1, (int64_t)kWideT);
+  return need < g ? need : g;
+}
+
 }  // namespace
 }  // namespace gnn
 
@@ -1015,7 +1216,8 @@ extern "C" {
 size_t gnn_gcn_head_workspace(int64_t M, int64_t Din, int64_t C) {
   const int64_t nb1 = ceil_div(M > 0 ? M : 1, (int64_t)kHeadWarps * kHeadRowsPerWarp);
   const int64_t nb2 = ceil_div(M > 0 ? M : 1, (int64_t)kHeadRowsPerCta);
-  const int64_t nb = nb1 > nb2 ? nb1 : nb2;
+  int64_t nb = nb1 > nb2 ? nb1 : nb2;
+  if (C > 64) nb = head_wide_grid(M);  // persistent wide head
   return sizeof(float) * (size_t)head_float_slots(nb, Din, C) + sizeof(double) * (size_t)nb + 512;
 }
 
@@ -1024,13 +1226,48 @@ int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64
                         const int64_t *deg_offsets, float grad_scale, float *dP, int64_t lddp,
                         float *dW, float *db, float *loss, void *ws, size_t ws_bytes,
                         gnn_stream_t stream) {
-  if (M <= 0 || Din <= 0 || Din > 64 || C <= 0 || C > 64 || !P || ldp < Din || !W || !b ||
-      !labels || !dP || lddp < Din || !dW || !db || !loss)
+  if (M <= 0 || Din <= 0 || Din > 64 || C <= 0 || C > 256 || (C > 64 && Din > 32) || !P ||
+      ldp < Din || !W || !b || !labels || !dP || lddp < Din || !dW || !db || !loss)
     return GNN_ERR_INVALID_ARGUMENT;
   if (ws_bytes < gnn_gcn_head_workspace(M, Din, C)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);
   const float scale = grad_scale;
   float *partials = static_cast<float *>(ws);
+  if (C > 64) {  // wide head: logits never materialised
+    const int64_t nb = head_wide_grid(M);
+    double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
+    const int nch = (int)ceil_div(C, (int64_t)32);
+#define GNN_HEAD_WIDE(DN, NC)                                                                   \
+  do {                                                                                          \
+    const size_t sm = head_wide_smem<DN, NC>();                                                 \
+    GNN_CUDA_TRY(cudaFuncSetAttribute(gcn_head_wide_kernel<DN, NC>,                             \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
+    gcn_head_wide_kernel<DN, NC><<<(unsigned)nb, kWideT, sm, st>>>(                             \
+        M, (int)Din, (int)C, P, ldp, W, b, labels, deg_offsets, scale, dP, lddp, partials, lpart); \
+  } while (0)
+#define GNN_HEAD_WIDE_D(DN)                  \
+  switch (nch) {                             \
+    case 3: GNN_HEAD_WIDE(DN, 3); break;     \
+    case 4: GNN_HEAD_WIDE(DN, 4); break;     \
+    case 5: GNN_HEAD_WIDE(DN, 5); break;     \
+    case 6: GNN_HEAD_WIDE(DN, 6); break;     \
+    case 7: GNN_HEAD_WIDE(DN, 7); break;     \
+    default: GNN_HEAD_WIDE(DN, 8); break;    \
+  }
+    if (Din <= 16) {
+      GNN_HEAD_WIDE_D(16);
+    } else {
+      GNN_HEAD_WIDE_D(32);
+    }
+#undef GNN_HEAD_WIDE_D
+#undef GNN_HEAD_WIDE
+    GNN_LAUNCH_CHECK();
+    const int64_t outs = Din * C + C + 1;
+    gcn_head_reduce_warp_kernel<<<(unsigned)ceil_div(outs * 32, 256), 256, 0, st>>>(
+        nb, (int)Din, (int)C, partials, lpart, dW, db, loss, grad_scale);
+    GNN_LAUNCH_CHECK();
+    return GNN_OK;
+  }
   static const bool rows_form = [] {
     const char *e = getenv("GNN_HEAD_ROWS");
     return !(e && e[0] == '0');
@@ -1091,6 +1328,70 @@ int gnn_gcn_head(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp,
   if (M <= 0) return GNN_ERR_INVALID_ARGUMENT;
   return gnn_gcn_head_scaled(M, Din, C, P, ldp, W, b, labels, deg_offsets, 1.0f / (float)M, dP,
                              lddp, dW, db, loss, ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- synthetic input synthesis
+// Partition-independent synthetic features / labels for shapes too large to
+// draw on the host (papers100M: X is 56.9 GB): element (r, k) of the global
+// [V, K] matrix is a function of (seed, r*K + k) only, so every rank fills
+// its row block [row0, row0+rows) with exactly the rows a single GPU would.
+namespace gnn {
+namespace {
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void fill_uniform_kernel(float *X, int64_t ldx, int64_t rows, int64_t cols,
+                                    int64_t row0, uint64_t seed) {
+  const uint64_t key = splitmix64(seed);
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, k = i - r * cols;
+    const uint64_t h = splitmix64(key ^ (uint64_t)((row0 + r) * cols + k));
+    // 24 random bits -> U[-1, 1) on a 2^-23 grid (exact in fp32)
+    X[r * ldx + k] = (float)(int32_t)(h >> 40) * (1.0f / 8388608.0f) - 1.0f;
+  }
+}
+__global__ void fill_labels_kernel(int64_t *y, int64_t n, int64_t row0, int64_t classes,
+                                   uint64_t seed) {
+  const uint64_t key = splitmix64(seed ^ 0xC1A55E5ull);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (int64_t)((splitmix64(key ^ (uint64_t)(row0 + i)) >> 11) % (uint64_t)classes);
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+int gnn_fill_uniform(float *X, int64_t ldx, int64_t rows, int64_t cols, int64_t row0,
+                     uint64_t seed, gnn_stream_t stream) {
+  using namespace gnn;
+  if (rows < 0 || cols < 0 || ldx < cols || row0 < 0 || (rows * cols > 0 && !X))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (rows * cols == 0) return GNN_OK;
+  const int64_t blocks = ceil_div(rows * cols, (int64_t)256), cap = (int64_t)sm_count() * 32;
+  fill_uniform_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, as_stream(stream)>>>(
+      X, ldx, rows, cols, row0, seed);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_fill_labels(int64_t *y, int64_t n, int64_t row0, int64_t classes, uint64_t seed,
+                    gnn_stream_t stream) {
+  using namespace gnn;
+  if (n < 0 || row0 < 0 || classes < 1 || (n > 0 && !y)) return GNN_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GNN_OK;
+  const int64_t blocks = ceil_div(n, (int64_t)256), cap = (int64_t)sm_count() * 32;
+  fill_labels_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, as_stream(stream)>>>(
+      y, n, row0, classes, seed);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
 }
 
 }  // extern "C"

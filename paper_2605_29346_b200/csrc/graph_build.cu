@@ -618,12 +618,255 @@ __global__ void __launch_bounds__(256) powerlaw_kernel(const double *__restrict_
   }
 }
 
+// ------------------------------------------- row-block power-law build
+// The per-rank build of the row-partitioned path: rank p never
+// materialises the whole graph.  It regenerates the bit-exact edge stream of
+// graph.py:256-261 chunk by chunk (edge i: src = draw i, dst = draw m+i) and
+// keeps, in stream order, (src-lo, dst) for src in [lo,hi) (its CSR rows) and
+// (dst-lo, src) for dst in [lo,hi) (its CSC rows).  Stable sorts of those
+// pairs then give the block of the reference's CSR / transposed CSR exactly.
+__global__ void __launch_bounds__(256) powerlaw_pairs_kernel(
+    const double *__restrict__ cdf, int64_t m, const int32_t *__restrict__ guide, U128 state0,
+    U128 inc, int64_t e0, int64_t e1, int32_t *src, int32_t *dst) {
+  const int64_t nchunks = ceil_div(e1 - e0, kGenChunk);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < 2 * nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_dst = c >= nchunks;
+    const int64_t q0 = e0 + (is_dst ? c - nchunks : c) * kGenChunk;
+    const int64_t q1 = min(q0 + kGenChunk, e1);
+    U128 s = pcg_advance(state0, inc, (uint64_t)(is_dst ? m + q0 : q0));
+    int32_t *out = is_dst ? dst : src;
+    for (int64_t q = q0; q < q1; ++q) {
+      s = u128_add(u128_mul(s, kPcgMult), inc);
+      const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+      const int64_t b = (int64_t)(u * (double)kGuide);
+      out[q - e0] = (int32_t)upper_bound_dev(cdf, (int64_t)guide[b], (int64_t)guide[b + 1], u);
+    }
+  }
+}
+
+constexpr int kSelThreads = 256;
+constexpr int kSelItems = 16;
+constexpr int kSelTile = kSelThreads * kSelItems;
+
+__device__ __forceinline__ int64_t sel_warp_incl(int64_t v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t n = __shfl_up_sync(kFull, v, o);
+    if ((int)lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+// exclusive block prefix of (a, b) per thread; totals in *ta / *tb
+__device__ __forceinline__ void sel_block_scan(int64_t &a, int64_t &b, int64_t *ta, int64_t *tb) {
+  __shared__ int64_t wa[kSelThreads / 32 + 1], wb[kSelThreads / 32 + 1];
+  const int w = threadIdx.x >> 5;
+  const int64_t ia = sel_warp_incl(a), ib = sel_warp_incl(b);
+  if (lane_id() == 31) {
+    wa[w] = ia;
+    wb[w] = ib;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t ra = 0, rb = 0;
+    for (int k = 0; k < kSelThreads / 32; ++k) {
+      const int64_t xa = wa[k], xb = wb[k];
+      wa[k] = ra;
+      wb[k] = rb;
+      ra += xa;
+      rb += xb;
+    }
+    wa[kSelThreads / 32] = ra;
+    wb[kSelThreads / 32] = rb;
+  }
+  __syncthreads();
+  a = wa[w] + ia - a;
+  b = wb[w] + ib - b;
+  *ta = wa[kSelThreads / 32];
+  *tb = wb[kSelThreads / 32];
+}
+
+// pass 1: kept counts per tile, [2][ntiles] (row 0: src in block, row 1: dst in block)
+__global__ void __launch_bounds__(kSelThreads) block_select_count_kernel(
+    int64_t n, const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t lo,
+    int64_t hi, int64_t ntiles, int64_t *tilecnt) {
+  const int64_t base = (int64_t)blockIdx.x * kSelTile + (int64_t)threadIdx.x * kSelItems;
+  int64_t a = 0, b = 0;
+#pragma unroll
+  for (int j = 0; j < kSelItems; ++j) {
+    const int64_t i = base + j;
+    if (i < n) {
+      const int64_t s = src[i], d = dst[i];
+      a += (s >= lo && s < hi);
+      b += (d >= lo && d < hi);
+    }
+  }
+  int64_t ta, tb;
+  sel_block_scan(a, b, &ta, &tb);
+  if (threadIdx.x == 0) {
+    tilecnt[blockIdx.x] = ta;
+    tilecnt[ntiles + 1 + blockIdx.x] = tb;
+  }
+}
+
+// pass 2: append the kept pairs in stream order after the running counts
+__global__ void __launch_bounds__(kSelThreads) block_select_write_kernel(
+    int64_t n, const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t lo,
+    int64_t hi, int64_t ntiles, const int64_t *__restrict__ tilebase,
+    const int64_t *__restrict__ count, int64_t cap, int32_t *r_key, int32_t *r_val, int32_t *c_key,
+    int32_t *c_val) {
+  const int64_t base = (int64_t)blockIdx.x * kSelTile + (int64_t)threadIdx.x * kSelItems;
+  int32_t sv[kSelItems], dv[kSelItems];
+  int64_t a = 0, b = 0;
+#pragma unroll
+  for (int j = 0; j < kSelItems; ++j) {
+    const int64_t i = base + j;
+    sv[j] = i < n ? src[i] : -1;
+    dv[j] = i < n ? dst[i] : -1;
+    a += (sv[j] >= lo && sv[j] < hi);
+    b += (dv[j] >= lo && dv[j] < hi);
+  }
+  int64_t ta, tb;
+  sel_block_scan(a, b, &ta, &tb);
+  int64_t pa = count[0] + tilebase[blockIdx.x] + a;
+  int64_t pb = count[1] + tilebase[ntiles + 1 + blockIdx.x] + b;
+#pragma unroll
+  for (int j = 0; j < kSelItems; ++j) {
+    if (sv[j] >= lo && sv[j] < hi) {
+      if (r_key && pa < cap) {  // past capacity: counted, not written (caller re-runs)
+        r_key[pa] = (int32_t)(sv[j] - lo);
+        r_val[pa] = dv[j];
+      }
+      ++pa;
+    }
+    if (dv[j] >= lo && dv[j] < hi) {
+      if (c_key && pb < cap) {
+        c_key[pb] = (int32_t)(dv[j] - lo);
+        c_val[pb] = sv[j];
+      }
+      ++pb;
+    }
+  }
+}
+
+__global__ void block_count_add_kernel(int64_t *count, const int64_t *__restrict__ tilebase,
+                                       int64_t ntiles) {
+  if (threadIdx.x == 0) {
+    count[0] += tilebase[ntiles];
+    count[1] += tilebase[2 * ntiles + 1];
+  }
+}
+
 }  // namespace
 }  // namespace gnn
 
 using namespace gnn;
 
 extern "C" {
+
+size_t gnn_powerlaw_block_workspace(int64_t n, int64_t chunk) {
+  (void)n;
+  WsCounter c;
+  c.take<int32_t>(kGuide + 1);
+  c.take<int32_t>(chunk);  // src chunk
+  c.take<int32_t>(chunk);  // dst chunk
+  const int64_t ntiles = ceil_div(chunk > 0 ? chunk : 1, kSelTile);
+  c.take<int64_t>(2 * (ntiles + 1));  // tile counts -> bases (two scans)
+  c.used += 2 * scan_i64_workspace(ntiles) + 256;
+  return c.used + 1024;
+}
+
+int gnn_powerlaw_block(int64_t n, int64_t m, const double *cdf, uint64_t state_hi,
+                       uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t lo, int64_t hi,
+                       int64_t chunk, int64_t capacity, int32_t *r_key, int32_t *r_val,
+                       int32_t *c_key, int32_t *c_val, int64_t *count, void *ws, size_t ws_bytes,
+                       gnn_stream_t stream) {
+  if (capacity < 0 || n < 1 || m < 0 || !cdf || lo < 0 || hi < lo || hi > n || chunk < kSelTile || !count ||
+      (!r_key) != (!r_val) || (!c_key) != (!c_val))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (n >= ((int64_t)1 << 31)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_powerlaw_block_workspace(n, chunk)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  WsArena ar(ws, ws_bytes);
+  int32_t *guide = ar.take<int32_t>(kGuide + 1);
+  int32_t *cs = ar.take<int32_t>(chunk);
+  int32_t *cd = ar.take<int32_t>(chunk);
+  const int64_t ntiles_max = ceil_div(chunk, kSelTile);
+  int64_t *tiles = ar.take<int64_t>(2 * (ntiles_max + 1));
+  const size_t sws_bytes = scan_i64_workspace(ntiles_max);
+  void *sws0 = ar.take<char>((int64_t)sws_bytes);
+  void *sws1 = ar.take<char>((int64_t)sws_bytes);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  GNN_CUDA_TRY(cudaMemsetAsync(count, 0, 2 * sizeof(int64_t), st));
+  if (m == 0) return GNN_OK;
+  guide_kernel<<<grid_for(kGuide + 1, 256), 256, 0, st>>>(cdf, n, guide);
+  GNN_LAUNCH_CHECK();
+  const U128 s0{state_hi, state_lo}, inc{inc_hi, inc_lo};
+  for (int64_t e0 = 0; e0 < m; e0 += chunk) {
+    const int64_t e1 = e0 + chunk < m ? e0 + chunk : m;
+    const int64_t len = e1 - e0, ntiles = ceil_div(len, kSelTile);
+    powerlaw_pairs_kernel<<<grid_for(2 * ceil_div(len, kGenChunk), 256), 256, 0, st>>>(
+        cdf, m, guide, s0, inc, e0, e1, cs, cd);
+    GNN_LAUNCH_CHECK();
+    block_select_count_kernel<<<(unsigned)ntiles, kSelThreads, 0, st>>>(len, cs, cd, lo, hi,
+                                                                        ntiles, tiles);
+    GNN_LAUNCH_CHECK();
+    GNN_TRY(exclusive_scan_i64(tiles, tiles, ntiles, true, sws0, sws_bytes, st));
+    GNN_TRY(exclusive_scan_i64(tiles + ntiles + 1, tiles + ntiles + 1, ntiles, true, sws1,
+                               sws_bytes, st));
+    block_select_write_kernel<<<(unsigned)ntiles, kSelThreads, 0, st>>>(
+        len, cs, cd, lo, hi, ntiles, tiles, count, capacity, r_key, r_val, c_key, c_val);
+    GNN_LAUNCH_CHECK();
+    block_count_add_kernel<<<1, 32, 0, st>>>(count, tiles, ntiles);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
+// Stable LSD radix sort of int32 (key, val) pairs by key in [0, key_limit)
+// (the building block of the block CSR / CSC / coalesced orders).
+size_t gnn_sort_pairs_workspace(int64_t n, int64_t key_limit) {
+  WsCounter c;
+  sort_ws_count(c, n, key_limit > 0 ? key_limit : 1, 1);
+  return c.used + 1024;
+}
+
+int gnn_sort_pairs(int64_t n, int64_t key_limit, const int32_t *keys, const int32_t *vals,
+                   int32_t *keys_out, int32_t *vals_out, void *ws, size_t ws_bytes,
+                   gnn_stream_t stream) {
+  if (n < 0 || key_limit < 1 || key_limit > ((int64_t)1 << 31) ||
+      (n > 0 && (!keys || !vals || !keys_out || !vals_out)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (n >= ((int64_t)1 << 32)) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_sort_pairs_workspace(n, key_limit)) return GNN_ERR_WORKSPACE;
+  if (n == 0) return GNN_OK;
+  WsArena ar(ws, ws_bytes);
+  SortIO io{};
+  io.n = n;
+  io.key_limit = key_limit;
+  io.key = SrcDesc{SRC_I32, keys};
+  io.nvals = 1;
+  io.val[0] = SrcDesc{SRC_I32, vals};
+  io.keys_sorted = keys_out;
+  io.vals_sorted[0] = vals_out;
+  return stable_sort(io, nullptr, ar, as_stream(stream));
+}
+
+// offsets[R+1] of sorted int32 keys in [0, R) (run lengths -> exclusive scan)
+size_t gnn_offsets_from_keys_workspace(int64_t R) {
+  WsCounter c;
+  offsets_ws_count(c, R);
+  return c.used + 1024;
+}
+
+int gnn_offsets_from_keys(int64_t n, int64_t R, const int32_t *sorted_keys, int64_t *offsets,
+                          void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (n < 0 || R < 0 || !offsets || (n > 0 && !sorted_keys)) return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_offsets_from_keys_workspace(R)) return GNN_ERR_WORKSPACE;
+  WsArena ar(ws, ws_bytes);
+  return offsets_from_sorted(sorted_keys, n, R, offsets, ar, as_stream(stream));
+}
 
 size_t gnn_csr_from_edges_workspace(int64_t V, int64_t E) { return edges_ws(V, E); }
 int gnn_csr_from_edges(int64_t V, int64_t E, const int64_t *src, const int64_t *dst,

@@ -44,7 +44,7 @@ def partition_bounds(offsets: np.ndarray, parts: int, row_cost: float = 0.0) -> 
     """Row boundaries [P+1] of contiguous blocks of ~equal cost
     sum_r (deg(r) + row_cost); row_cost = 0 balances edges only
     (searchsorted on the cumulative cost; every block non-empty when V >= P)."""
-    offsets = np.asarray(offsets, dtype=np.int64)
+    offsets = np.asarray(offsets)
     V = offsets.size - 1
     if parts <= 0:
         raise ValueError("parts must be positive")
@@ -59,6 +59,19 @@ def partition_bounds(offsets: np.ndarray, parts: int, row_cost: float = 0.0) -> 
         for p in range(1, parts):
             b[p] = min(max(b[p], b[p - 1] + 1), V - (parts - p))
     return b
+
+
+def expected_bounds(spec, parts: int, row_cost: float = 0.0) -> np.ndarray:
+    """Row bounds for the power-law generator WITHOUT building the graph: the
+    expected out-degree prefix of graph.py:256-261 is m * cdf (every edge's
+    source is a draw from that CDF), so blocks of equal expected cost are
+    found from the CDF alone.  Realised block sums differ from expectation by
+    O(sqrt) — a fraction of a percent at the papers100M shape."""
+    from .graph import powerlaw_cdf
+
+    cdf = powerlaw_cdf(spec.num_vertices, spec.exponent)
+    cum = np.concatenate([[0.0], spec.edge_count() * cdf])
+    return partition_bounds(cum, parts, row_cost)
 
 
 def remap_ids_host(ids: np.ndarray, bounds: np.ndarray, stride: int) -> np.ndarray:
@@ -156,6 +169,24 @@ class PeerExchange:
         self.dist.all_reduce(t, group=self.group)
 
 
+class NullExchange:
+    """The exchange of a single rank (N=1): every slot is already local."""
+
+    world, rank = 1, 0
+
+    def all_gather(self, full, stride_rows, async_op=False):
+        return None
+
+    def all_gather_start(self, full, stride_rows):
+        return None
+
+    def all_gather_wait(self, handle):
+        pass
+
+    def all_reduce(self, t):
+        pass
+
+
 class LocalExchange:
     """P virtual ranks in one process (one GPU): the exchanges copy slots
     between the ranks' buffers.  Used to test the partitioned schedule."""
@@ -183,17 +214,10 @@ class RowPartition:
 
     def __init__(self, g: CsrGraph, parts: int, rank: int, *, coalesced: bool = True,
                  bounds: np.ndarray | None = None, pow2_stride: bool = False):
-        self.g, self.parts, self.rank = g, parts, rank
-        dev = g.device
-        self.bounds = (partition_bounds(g.offsets, parts, ROW_COST) if bounds is None
-                       else np.asarray(bounds))
-        self.stride = block_stride(self.bounds)
-        if pow2_stride:  # peer mode: owner = id >> log2(stride), row = id & (stride - 1)
-            self.stride = 1 << max(0, (self.stride - 1).bit_length())
-        self.stride_log2 = self.stride.bit_length() - 1 if pow2_stride else None
-        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
-        self.rows = self.hi - self.lo
-        self.d_bounds = torch.from_numpy(self.bounds.astype(np.int64)).to(dev)
+        self.g = g
+        self._setup(g.num_vertices, g.device, parts, rank,
+                    partition_bounds(g.offsets, parts, ROW_COST) if bounds is None else bounds,
+                    pow2_stride)
         cols_total = parts * self.stride
         # canonical row degrees of the owned rows (every degree-norm uses them)
         self.deg_offsets = (g.d_offsets[self.lo:self.hi + 1] - g.d_offsets[self.lo]).contiguous()
@@ -203,6 +227,51 @@ class RowPartition:
             A, AT = g.csr(), g.csc()
         self.A = self._slice(A, cols_total, deg=self.deg_offsets)
         self.AT = self._slice(AT, cols_total, deg=None)
+
+    def _setup(self, num_vertices, device, parts, rank, bounds, pow2_stride):
+        self.num_vertices, self.device = int(num_vertices), device
+        self.parts, self.rank = parts, rank
+        self.bounds = np.asarray(bounds, dtype=np.int64)
+        self.stride = block_stride(self.bounds)
+        if pow2_stride:  # peer mode: owner = id >> log2(stride), row = id & (stride - 1)
+            self.stride = 1 << max(0, (self.stride - 1).bit_length())
+        self.stride_log2 = self.stride.bit_length() - 1 if pow2_stride else None
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.rows = self.hi - self.lo
+        self.d_bounds = torch.from_numpy(self.bounds).to(device)
+
+    @classmethod
+    def from_block(cls, block, parts: int, rank: int, bounds, *,
+                   pow2_stride: bool = False) -> "RowPartition":
+        """Partition from this rank's own RowBlock (graph.powerlaw_row_block):
+        the per-rank build, no global graph anywhere.  ``block`` must hold
+        rows [bounds[rank], bounds[rank+1]) with coalesced forms."""
+        self = cls.__new__(cls)
+        self.g = None
+        self._setup(block.num_vertices, block.device, parts, rank, bounds, pow2_stride)
+        if (block.lo, block.hi) != (self.lo, self.hi):
+            raise ValueError("row block does not match the partition bounds")
+        cols_total = parts * self.stride
+        self.deg_offsets = block.deg_offsets
+        self.A = self._remap(block.csr_coalesced(), cols_total, deg=self.deg_offsets)
+        self.AT = self._remap(block.csc_coalesced(), cols_total, deg=None)
+        return self
+
+    def _remap(self, op: SparseOperand, cols_total: int, deg) -> SparseOperand:
+        """Block operand with global column ids -> exchange-buffer positions."""
+        lib = _lib.lib()
+        cols, vals = op.entries()
+        nnz = int(cols.numel())
+        out = torch.empty(max(nnz, 1), dtype=torch.int32, device=cols.device)[:nnz]
+        with torch.cuda.device(cols.device):
+            _lib.check(lib.gnn_remap_ids(nnz, cols.data_ptr() if nnz else None,
+                                         self.d_bounds.data_ptr(), self.parts, self.stride,
+                                         out.data_ptr() if nnz else None,
+                                         _lib.stream_handle(cols.device)), "remap_ids")
+        vals = vals.contiguous() if vals is not None else None
+        del cols
+        return SparseOperand(self.rows, cols_total, op.offsets, out, vals=vals,
+                             deg_offsets=deg, mult=op.mult)
 
     def _slice(self, op: SparseOperand, cols_total: int, deg) -> SparseOperand:
         lib = _lib.lib()
@@ -285,10 +354,9 @@ class DistGCNTrainer:
         if overlap and peer:
             raise ValueError("overlap applies to the all-gather exchange, not peer mode")
         self.overlap = overlap
-        g = part.g
-        dev = g.device
+        dev = part.device
         self.dev = dev
-        V, n, S, P = g.num_vertices, part.rows, part.stride, part.parts
+        V, n, S, P = part.num_vertices, part.rows, part.stride, part.parts
         self.V, self.F, self.Hd, self.C = V, in_feats, hidden, classes
         f32 = dict(dtype=torch.float32, device=dev)
         self.W1 = torch.from_numpy(glorot(in_feats, hidden, seed, 0)).to(dev)

@@ -126,7 +126,7 @@ class SparseOperand:
     unpack on demand (setup-time consumers); the SpMM reads the packed words."""
 
     def __init__(self, num_rows, num_cols, offsets, cols, vals=None, eid=None, deg_offsets=None,
-                 mult: bool = False, row_ids=None):
+                 mult: bool = False, row_ids=None, pack: bool = True):
         self.num_rows = int(num_rows)
         self.num_cols = int(num_cols)
         self.nnz = int(cols.numel())
@@ -142,17 +142,21 @@ class SparseOperand:
         self.packed = None
         self._plain = None
         self._plans = {}
-        if mult and vals is not None and eid is None and SPMM_PACK and self.nnz > 0:
+        if pack and mult and vals is not None and eid is None and SPMM_PACK and self.nnz > 0:
             self._try_pack()
 
     def _try_pack(self):
         bits = max(1, (self.num_cols - 1).bit_length())
-        if bits > 24:  # < 256 per word: hub pairs would expand too much
+        if bits > 28:  # < 16 per word
             return
         maxw = (1 << (32 - bits)) - 1
         cols, vals, offsets = self._cols, self._vals, self.offsets
         reps = torch.div(vals.to(torch.int64) + (maxw - 1), maxw, rounding_mode="floor")
         reps.clamp_(min=1)
+        if bits > 24 and int(reps.sum().item()) > 1.05 * self.nnz:
+            # a narrow weight field (>= 2^25 columns, e.g. papers100M) splits
+            # hub pairs into too many words: keep the float form
+            return
         if int(reps.max().item()) > 1:
             # a multiplicity above the word's weight field (hub pairs of a
             # power-law multigraph: Reddit's top pair repeats ~2e5 times) is
@@ -851,3 +855,200 @@ def generate(spec: GraphGenSpec, seed: int, device=None) -> CsrGraph:
     g = csr_from_edges(n, src, dst, device=dev)
     del src, dst
     return g
+
+
+# ------------------------------------------------ row-block (per-rank) build
+def _sort_pairs(keys: torch.Tensor, vals: torch.Tensor, key_limit: int):
+    """Stable device radix sort of int32 (key, val) pairs by key (gnn_sort_pairs)."""
+    lib = _lib.lib()
+    dev = keys.device
+    n = int(keys.numel())
+    ko = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+    vo = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(lib.gnn_sort_pairs_workspace(n, max(int(key_limit), 1)), dev)
+        _lib.check(lib.gnn_sort_pairs(n, max(int(key_limit), 1), keys.data_ptr() if n else None,
+                                      vals.data_ptr() if n else None, ko.data_ptr() if n else None,
+                                      vo.data_ptr() if n else None, ws.data_ptr(), ws.numel(),
+                                      _lib.stream_handle(dev)), "sort_pairs")
+        del ws
+    return ko, vo
+
+
+def _offsets_from_keys(sorted_keys: torch.Tensor, R: int) -> torch.Tensor:
+    lib = _lib.lib()
+    dev = sorted_keys.device
+    n = int(sorted_keys.numel())
+    off = torch.empty(R + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(lib.gnn_offsets_from_keys_workspace(R), dev)
+        _lib.check(lib.gnn_offsets_from_keys(n, R, sorted_keys.data_ptr() if n else None,
+                                             off.data_ptr(), ws.data_ptr(), ws.numel(),
+                                             _lib.stream_handle(dev)), "offsets_from_keys")
+    return off
+
+
+class RowBlock:
+    """Rows [lo, hi) of a graph's CSR and of its transposed CSR (CSC), built
+    on device without the rest of the graph (SURVEY §8e per-rank build).
+
+    ``csr_offsets`` / ``csr_targets``: rows lo..hi-1 of csr_from_edges
+    (graph.py:106-114), local row ids, global column ids; ``csc_offsets`` /
+    ``csc_rows``: rows lo..hi-1 of the transposed CSR (in-edges of the owned
+    vertices, source ids ascending, stream order within equal sources) —
+    both bit-exact with the reference's arrays sliced to the block.
+    ``csr_coalesced()`` / ``csc_coalesced()`` are the multiplicity-weighted
+    unique-pair forms the trainers aggregate over; ``deg_offsets`` the
+    canonical out-degree prefix of the block rows (every degree-norm)."""
+
+    def __init__(self, num_vertices, num_edges, lo, hi, deg_offsets, csr=None, csc=None,
+                 csr_co=None, csc_co=None, in_deg_offsets=None):
+        self.num_vertices, self.num_edges = int(num_vertices), int(num_edges)
+        self.lo, self.hi, self.rows = int(lo), int(hi), int(hi) - int(lo)
+        self.deg_offsets = deg_offsets
+        self.in_deg_offsets = in_deg_offsets
+        self.csr_offsets, self.csr_targets = csr if csr is not None else (None, None)
+        self.csc_offsets, self.csc_rows = csc if csc is not None else (None, None)
+        self._csr_co, self._csc_co = csr_co, csc_co
+
+    @property
+    def device(self):
+        return self.deg_offsets.device
+
+    def csr_coalesced(self) -> SparseOperand:
+        return self._csr_co
+
+    def csc_coalesced(self) -> SparseOperand:
+        return self._csc_co
+
+    def nbytes(self) -> int:
+        n = 0
+        for t in (self.deg_offsets, self.in_deg_offsets, self.csr_offsets, self.csr_targets,
+                  self.csc_offsets, self.csc_rows):
+            if t is not None:
+                n += t.numel() * t.element_size()
+        for op in (self._csr_co, self._csc_co):
+            if op is not None:
+                n += op.nbytes()
+        return n
+
+
+def _block_capacity(spec: GraphGenSpec, lo: int, hi: int, cdf: np.ndarray) -> int:
+    """Expected edges with an endpoint draw in [lo, hi) plus a 6-sigma margin
+    (the block builder re-runs with the exact count if a block exceeds it)."""
+    m = spec.edge_count()
+    p = float(cdf[hi - 1] - (cdf[lo - 1] if lo > 0 else 0.0)) if hi > lo else 0.0
+    mu = m * p
+    return int(min(m, mu + 6.0 * np.sqrt(max(mu, 1.0)) + 8192))
+
+
+def powerlaw_row_block(spec: GraphGenSpec, seed: int, lo: int, hi: int, device=None, *,
+                       canonical: bool = False, coalesced: bool = True,
+                       chunk: int = 1 << 26, pack: bool = True) -> RowBlock:
+    """Build rows [lo, hi) of ``generate(spec, seed)`` (power-law) and of its
+    transpose on device.  The bit-exact edge stream of graph.py:256-261 is
+    regenerated in ``chunk``-edge pieces (gnn_powerlaw_block), keeping in
+    stream order the edges with src (CSR) or dst (CSC) in the block; stable
+    radix sorts then give the block's rows exactly as the reference's CSR and
+    transposed CSR hold them.  Memory is O(block), not O(E): a rank of the
+    row partition never holds the whole papers100M graph.  ``pack=False``
+    keeps the coalesced forms unpacked (a partition re-packs after its id
+    remap)."""
+    if spec.kind != "power-law":
+        raise ConfigError("row-block build covers the power-law generator")
+    lib = _lib.lib()
+    dev = _device(device)
+    n, m = spec.num_vertices, spec.edge_count()
+    if not 0 <= lo <= hi <= n:
+        raise ValueError("block bounds outside [0, V]")
+    R = hi - lo
+    cdf_h = powerlaw_cdf(n, spec.exponent)
+    cdf = torch.from_numpy(cdf_h).to(dev)
+    state, inc = pcg64_seed_state(seed)
+    mask = (1 << 64) - 1
+    chunk = max(int(chunk), 4096)
+    cap = _block_capacity(spec, lo, hi, cdf_h)
+    i32 = dict(dtype=torch.int32, device=dev)
+    count = torch.zeros(2, dtype=torch.int64, device=dev)
+    for _attempt in range(2):
+        rk, rv = torch.empty(max(cap, 1), **i32), torch.empty(max(cap, 1), **i32)
+        ck, cv = torch.empty(max(cap, 1), **i32), torch.empty(max(cap, 1), **i32)
+        with torch.cuda.device(dev):
+            ws = _lib.workspace(lib.gnn_powerlaw_block_workspace(n, chunk), dev)
+            _lib.check(lib.gnn_powerlaw_block(n, m, cdf.data_ptr(), state >> 64, state & mask,
+                                              inc >> 64, inc & mask, lo, hi, chunk, cap,
+                                              rk.data_ptr(), rv.data_ptr(), ck.data_ptr(),
+                                              cv.data_ptr(), count.data_ptr(), ws.data_ptr(),
+                                              ws.numel(), _lib.stream_handle(dev)),
+                       "powerlaw_block")
+            del ws
+        nr, nc = (int(x) for x in count.tolist())
+        if max(nr, nc) <= cap:
+            break
+        del rk, rv, ck, cv
+        cap = max(nr, nc)  # rare: the block exceeded the 6-sigma margin; exact re-run
+    del cdf
+    rk, rv, ck, cv = rk[:nr], rv[:nr], ck[:nc], cv[:nc]
+    # ---- CSR rows: stable by row (stream order within a row) = the canonical block
+    csr = None
+    if canonical:
+        k1, t1 = _sort_pairs(rk, rv, R)
+        csr = (_offsets_from_keys(k1, R), t1)
+        del k1
+    csr_co = None
+    if coalesced:
+        # (row, col) order: stable by col, then stable by row; then run-length coalesce
+        c1, r1 = _sort_pairs(rv, rk, n)
+        del rk, rv
+        r2, c2 = _sort_pairs(r1, c1, R)
+        del c1, r1
+        deg_off = _offsets_from_keys(r2, R)
+        del r2
+        off, cols, mult = _coalesce(R, deg_off, c2)
+        del c2
+        csr_co = SparseOperand(R, n, off, cols, vals=mult, deg_offsets=deg_off, mult=True,
+                               pack=pack)
+    else:
+        deg_off = csr[0] if csr is not None else _offsets_from_keys(_sort_pairs(rk, rv, R)[0], R)
+        del rk, rv
+    if csr is not None:
+        deg_off = csr[0]
+        if csr_co is not None:
+            csr_co.deg_offsets = deg_off
+    # ---- CSC rows: stable by source then by destination = the transposed CSR
+    s1, d1 = _sort_pairs(cv, ck, n)
+    del ck, cv
+    d2, s2 = _sort_pairs(d1, s1, R)
+    del s1, d1
+    in_off = _offsets_from_keys(d2, R)
+    del d2
+    csc = (in_off, s2) if canonical else None
+    csc_co = None
+    if coalesced:
+        off, rows, mult = _coalesce(R, in_off, s2)
+        csc_co = SparseOperand(R, n, off, rows, vals=mult, deg_offsets=in_off, mult=True,
+                               pack=pack)
+    del s2
+    return RowBlock(n, m, lo, hi, deg_off, csr=csr, csc=csc, csr_co=csr_co, csc_co=csc_co,
+                    in_deg_offsets=in_off)
+
+
+def fill_uniform(X: torch.Tensor, row0: int, seed: int) -> torch.Tensor:
+    """X[i, k] = U[-1, 1) hash of (seed, (row0 + i) * K + k) in place
+    (gnn_fill_uniform): rows of a global synthetic feature matrix, identical
+    however the rows are partitioned."""
+    lib = _lib.lib()
+    with torch.cuda.device(X.device):
+        _lib.check(lib.gnn_fill_uniform(X.data_ptr(), X.stride(0), X.shape[0], X.shape[1], row0,
+                                        seed & ((1 << 64) - 1), _lib.stream_handle(X.device)),
+                   "fill_uniform")
+    return X
+
+
+def fill_labels(y: torch.Tensor, row0: int, classes: int, seed: int) -> torch.Tensor:
+    lib = _lib.lib()
+    with torch.cuda.device(y.device):
+        _lib.check(lib.gnn_fill_labels(y.data_ptr(), y.numel(), row0, classes,
+                                       seed & ((1 << 64) - 1), _lib.stream_handle(y.device)),
+                   "fill_labels")
+    return y

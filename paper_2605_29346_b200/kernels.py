@@ -181,10 +181,11 @@ class AdamCall:
 class HeadCall:
     """Fused output layer: logits, mean cross-entropy, dP (degree-normed), dW, db.
 
-    The fused kernel (gnn_gcn_head_scaled) covers Din, C <= 64; wider layers
-    (e.g. the 172 classes of the papers100M shape) run the same math as
-    library calls: Z = P W + b, softmax-CE (dZ scaled), dW = P^T dZ,
-    db = colsum(dZ), dP = (dZ W^T) / deg.  ``scale`` multiplies the summed
+    The fused kernel (gnn_gcn_head_scaled) covers Din, C <= 64 and, with the
+    wide form (class chunks, online softmax, logits never stored), Din <= 32
+    with C <= 256 — the 172 classes of the papers100M shape; other shapes run
+    the same math as library calls: Z = P W + b, softmax-CE (dZ scaled),
+    dW = P^T dZ, db = colsum(dZ), dP = (dZ W^T) / deg.  ``scale`` multiplies the summed
     loss and dZ: 1/M (the default) is the mean over these rows; a row-
     partitioned rank passes 1/V_global so the all-reduced loss and gradients
     equal the single-GPU mean."""
@@ -199,7 +200,8 @@ class HeadCall:
         self.scale = float(1.0 / self.M if scale is None else scale)
         self.P, self.W, self.b, self.labels, self.dP = P, W, b, labels, dP
         self.dW, self.db, self.loss, self.deg = dW, db, loss, deg_offsets
-        self.fused = self.Din <= self.FUSED_MAX and self.C <= self.FUSED_MAX
+        self.fused = ((self.Din <= self.FUSED_MAX and self.C <= self.FUSED_MAX)
+                      or (self.FUSED_MAX > 0 and self.Din <= 32 and 64 < self.C <= 256))
         if not self.fused:
             f32 = dict(dtype=torch.float32, device=self.dev)
             self.Z = torch.empty(self.M, self.C, **f32)

@@ -110,7 +110,11 @@ def test_weight_gradient_gemm_tn_shapes(M, N, K):
 
 
 @pytest.mark.parametrize("M,Din,C", [(1, 16, 7), (1000, 16, 41), (4097, 16, 16), (777, 32, 47),
-                                     (300, 8, 64), (513, 24, 33), (2000, 64, 41)])
+                                     (300, 8, 64), (513, 24, 33), (2000, 64, 41),
+                                     # wide form (C > 64: class chunks, online softmax), incl.
+                                     # more row tiles than CTAs of the persistent grid
+                                     (1000, 16, 172), (90_001, 16, 172), (513, 32, 100),
+                                     (5, 8, 65), (3000, 16, 256), (2049, 12, 97)])
 @pytest.mark.parametrize("with_deg", [False, True])
 def test_gcn_head_matches_float64(gb, M, Din, C, with_deg):
     """Fused output layer (gnn_gcn_head_scaled): loss, dP (with the 1/deg

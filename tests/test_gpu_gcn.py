@@ -175,12 +175,18 @@ def test_trainer_with_released_row_order_operands(setup, monkeypatch):
         assert torch.equal(v, b.grads()[k]), k
 
 
-def test_trainer_wide_output_layer_matches_oracle(cuda):
-    """More classes than the fused output kernel covers (C > 64, e.g. the 172
-    of the papers100M shape): HeadCall runs GEMM + softmax-CE + colsum + GEMMs
-    + degree norm; the epoch still matches the float64 oracle."""
+@pytest.mark.parametrize("fused", [True, False])
+def test_trainer_wide_output_layer_matches_oracle(cuda, fused, monkeypatch):
+    """172 classes (the papers100M shape): the fused wide output layer (class
+    chunks, online softmax, no [V, C] logits) and, with the fused head turned
+    off, the library-call composition (GEMM + softmax-CE + colsum + GEMMs +
+    degree norm); the epoch matches the float64 oracle either way."""
     import paper_2605_29346_b200 as gb
+    from paper_2605_29346_b200.kernels import HeadCall
     from paper_2605_29346_b200.models import GCNTrainer
+
+    if not fused:
+        monkeypatch.setattr(HeadCall, "FUSED_MAX", 0)
 
     V, E, F, Hd, C = 3000, 20000, 64, 16, 172
     g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=2.1), 7)
@@ -191,7 +197,7 @@ def test_trainer_wide_output_layer_matches_oracle(cuda):
     y = rng.integers(0, C, V)
     for coalesced in (False, True):
         tr = GCNTrainer(g, F, Hd, C, seed=0, coalesced=coalesced)
-        assert not tr.k_head.fused
+        assert tr.k_head.fused == fused
         tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
         tr.forward_backward()
         torch.cuda.synchronize()

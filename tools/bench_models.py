@@ -5,6 +5,8 @@
   sweep    SpMMv / SpMMve K sweep 16..256, Reddit shape               [BASELINE configs[1]]
   sampling device sample_minibatch / DeviceSampler vs the reference sampler (host)
   minibatch sampled mini-batch GCN training step, Reddit shape (SampledGCNTrainer)
+  papers100m 2-layer GCN epoch, ogbn-papers100M shape (V=111M, E=1.6B, K=128 -> 16 -> 172),
+           row-partitioned over the N ranks of the run, per-rank block build [configs[4]]
 
 Prints one JSON object per item: device-timed ms (CUDA-graph replay), per-
 kernel ms inside eager epochs, peak memory.  Usage:
@@ -25,6 +27,11 @@ from paper_2605_29346_b200 import _lib
 from paper_2605_29346_b200.kernels import SpmmCall
 
 REDDIT = dict(V=232_965, E=114_615_892)
+PAPERS100M = dict(V=111_059_956, E=1_615_685_872, F=128, H=16, C=172, seed=42)
+# row-proportional cost of the papers100M epoch in edge-equivalents (X.W1 and
+# X^T.dH1 stream 512 B per row, the 172-class head ~0.3 ns per row, vs ~15 ps
+# per edge for each of the four SpMMs)
+PAPERS100M_ROW_COST = 40.0
 PRODUCTS = dict(V=2_449_029, E=123_718_280)
 
 
@@ -231,10 +238,103 @@ def run_minibatch():
                     "kernels rebuilt per batch (no graph replay yet)"}
 
 
+
+
+def run_papers100m(rank=0, world=1, steps=10, warmup=3, scale=None):
+    """2-layer GCN epoch on the ogbn-papers100M-shaped power-law graph
+    (BASELINE configs[4]), row-partitioned over the run's ranks.  Every rank
+    builds only its own block (graph.powerlaw_row_block: the bit-exact edge
+    stream regenerated and filtered, no whole graph anywhere), fills its rows
+    of the synthetic [V, 128] features / labels on device (hash-based,
+    partition independent), and trains with DistGCNTrainer (N=1: one block,
+    no exchange; N>1: NCCL all-gathers of the [V, 16] blocks overlapped with
+    the own-slot aggregation + one gradient all-reduce).  Output layer: the
+    fused 172-class head (logits never stored).  ``scale`` (or
+    GNN_C5_SCALE) shrinks V and E for smoke runs."""
+    from paper_2605_29346_b200.dist import (DistGCNTrainer, NullExchange, RowPartition,
+                                            TorchDistExchange, expected_bounds)
+
+    scale = float(os.environ.get("GNN_C5_SCALE", "1")) if scale is None else scale
+    P = PAPERS100M
+    V, E = int(P["V"] * scale), int(P["E"] * scale)
+    F, Hd, C = P["F"], P["H"], P["C"]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    spec = gb.GraphGenSpec("power-law", V, E, exponent=2.1)
+    bounds = expected_bounds(spec, world, PAPERS100M_ROW_COST)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    t0 = time.perf_counter()
+    blk = gb.graph.powerlaw_row_block(spec, P["seed"], lo, hi, pack=False)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    build_peak = torch.cuda.max_memory_allocated(dev)
+    nnz_csr, nnz_csc = blk.csr_coalesced().nnz, blk.csc_coalesced().nnz
+    deg_edges = int(blk.deg_offsets[-1].item())
+    part = RowPartition.from_block(blk, world, rank, bounds)
+    del blk
+    torch.cuda.synchronize()
+    t_part = time.perf_counter() - t0 - t_build
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats(dev)
+    overlap = world > 1
+    tr = DistGCNTrainer(part, F, Hd, C, seed=P["seed"], overlap=overlap)
+    if overlap:
+        part.A = part.AT = None
+    else:  # every aggregation runs on the degree-sorted forms: keep only those
+        part.A.release_row_order()
+        part.AT.release_row_order()
+    torch.cuda.empty_cache()
+    gb.graph.fill_uniform(tr.X, lo, P["seed"])
+    gb.graph.fill_labels(tr.labels, lo, C, P["seed"])
+    ex = NullExchange() if world == 1 else TorchDistExchange()
+    lib = _lib.lib()
+    c0 = lib.gnn_launch_counter()
+    tr.step(ex)
+    torch.cuda.synchronize()
+    launches = lib.gnn_launch_counter() - c0
+    for _ in range(warmup):
+        tr.step(ex)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(steps):
+        tr.step(ex)
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    peak = torch.cuda.max_memory_allocated(dev)
+    t = torch.tensor([ms, peak / 2**20, build_peak / 2**20, t_build], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    # analytic per-rank footprint: block CSR+CSC (coalesced, packed words + int64
+    # offsets), X rows, 4 exchanged [V,16] buffers (+ 3 local [rows,16])
+    rows = hi - lo
+    analytic = (8 * 2 * (rows + 1) + 4 * (nnz_csr + nnz_csc) + 4 * rows * F
+                + 4 * Hd * (4 * world * part.stride + 3 * rows))
+    return {"item": "gcn_papers100m_epoch_ms",
+            "workload": "2-layer GCN full-graph epoch, ogbn-papers100M-shaped power-law graph "
+                        f"(V={V}, E={E}, K={F} -> {Hd} -> {C}), row-partitioned over {world} "
+                        "rank(s), per-rank block build",
+            "scale": scale, "n_gpus": world, "ms": round(float(t[0]), 3),
+            "steps": steps, "warmup": warmup, "timing": "CUDA events, max over ranks",
+            "loss": float(tr.loss.item()), "launches_per_step": int(launches),
+            "rank0_rows": rows, "rank0_edges": deg_edges, "rank0_unique_pairs_csr": nnz_csr,
+            "rank0_unique_pairs_csc": nnz_csc,
+            "peak_mb_train": round(float(t[1]), 1), "peak_mb_build": round(float(t[2]), 1),
+            "rank0_analytic_mb": round(analytic / 2**20, 1),
+            "build_s": round(float(t[3]), 2), "partition_s": round(t_part, 2),
+            "inputs": "X / labels hashed on device (gnn_fill_uniform / gnn_fill_labels)",
+            "exchange": "none (one rank)" if world == 1 else "NCCL all-gather, own-slot overlap"}
+
+
 if __name__ == "__main__":
     for item in sys.argv[1:] or ["gin", "gat", "sweep"]:
         r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep, "sampling": run_sampling,
-             "minibatch": run_minibatch}[item]()
+             "minibatch": run_minibatch, "papers100m": run_papers100m}[item]()
         for x in (r if isinstance(r, list) else [r]):
             print(json.dumps(x), flush=True)
         torch.cuda.empty_cache()
