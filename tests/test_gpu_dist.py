@@ -144,18 +144,22 @@ def test_split_local_remote_partitions_rows(env, P):
 
 
 @pytest.mark.parametrize("P", [1, 3])
-def test_virtual_ranks_wide_output_layer(env, P):
-    """More classes than the fused head takes (library-call head, loss and dZ
+@pytest.mark.parametrize("fused", [True, False])
+def test_virtual_ranks_wide_output_layer(env, P, fused, monkeypatch):
+    """100 classes: the fused wide head and the library-call head (loss and dZ
     scaled 1/V_global per rank): the all-reduced loss and gradients still
     equal the single-process oracle."""
     from paper_2605_29346_b200.dist import DistGCNTrainer, LocalExchange, RowPartition, step_virtual
+    from paper_2605_29346_b200.kernels import HeadCall
 
+    if not fused:
+        monkeypatch.setattr(HeadCall, "FUSED_MAX", 0)
     gb, g, X, _ = env
     V, C = g.num_vertices, 100
     y = np.random.default_rng(2).integers(0, C, V)
     parts = [RowPartition(g, P, r) for r in range(P)]
     trs = [DistGCNTrainer(p, 64, 16, C, seed=0, overlap=P > 1) for p in parts]
-    assert not trs[0]._head.fused
+    assert trs[0]._head.fused == fused
     for p, t in zip(parts, trs):
         t.set_inputs(torch.from_numpy(X[p.lo:p.hi]), torch.from_numpy(y[p.lo:p.hi]))
     step_virtual(trs, LocalExchange(P), adam=False)
