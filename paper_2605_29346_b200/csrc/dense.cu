@@ -1202,6 +1202,135 @@ __global__ void __launch_bounds__(kWideT, 1) gcn_head_wide_kernel(
   }
 }
 
+// Lane-per-class form of the wide head (Din <= 16): a warp owns a row at a
+// time and lane l owns classes l, l+32, ..., l+32(NJ-1); W[k][class] (16 x NJ)
+// and the warp's dW partials (16 x NJ) live in registers for the whole
+// kernel, so per row the only traffic is the row of P (one 64-byte load),
+// its label and its row of dP.  The thread-per-row form above reloads W from
+// shared memory for every logit and is bound by those loads.
+template <int NJ>
+__global__ void __launch_bounds__(kWideT, 1) gcn_head_lanes_kernel(
+    int64_t M, int din, int C, const float *__restrict__ P, int64_t ldp,
+    const float *__restrict__ W, const float *__restrict__ b, const int64_t *__restrict__ labels,
+    const int64_t *__restrict__ deg_offsets, float scale, float *dP, int64_t lddp,
+    float *partials, double *lpart) {
+  constexpr int CP = NJ * 32;
+  extern __shared__ __align__(16) float hl[];  // [warps][17][CP] warp partials (dW rows, db)
+  __shared__ double lred[kWideWarps];
+  const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+  float w[16][NJ], acc[16][NJ], bb[NJ], accb[NJ];
+  bool ok[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int c = lane + 32 * j;
+    ok[j] = c < C;
+    bb[j] = ok[j] ? b[c] : 0.f;
+    accb[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      w[k][j] = (ok[j] && k < din) ? W[(int64_t)k * C + c] : 0.f;
+      acc[k][j] = 0.f;
+    }
+  }
+  double lsum = 0.0;
+  const int64_t nw = (int64_t)gridDim.x * kWideWarps;
+  // software pipeline: the next row's P / label / degree are loaded while
+  // this row computes (one HBM round trip per row would otherwise bound it)
+  int64_t r = (int64_t)blockIdx.x * kWideWarps + warp;
+  float pl_n = 0.f;
+  int64_t y_n = 0, dg_n = 0;
+  if (r < M) {
+    pl_n = lane < din ? __ldg(P + r * ldp + lane) : 0.f;
+    y_n = __ldg(labels + r);
+    if (deg_offsets) dg_n = __ldg(deg_offsets + r + 1) - __ldg(deg_offsets + r);
+  }
+  for (; r < M; r += nw) {
+    const float pl = pl_n;
+    const int64_t y = y_n, dg = dg_n;
+    const int64_t rn = r + nw;
+    if (rn < M) {
+      pl_n = lane < din ? __ldg(P + rn * ldp + lane) : 0.f;
+      y_n = __ldg(labels + rn);
+      if (deg_offsets) dg_n = __ldg(deg_offsets + rn + 1) - __ldg(deg_offsets + rn);
+    }
+    float p[16], z[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) z[j] = bb[j];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      p[k] = __shfl_sync(kFull, pl, k);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) z[j] = fmaf(p[k], w[k][j], z[j]);
+    }
+    float mx = -INFINITY, zsel = 0.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      if (ok[j]) mx = fmaxf(mx, z[j]);
+      if (j == (int)(y >> 5)) zsel = z[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    float se = 0.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      z[j] = ok[j] ? __expf(z[j] - mx) : 0.f;
+      se += z[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
+    const float zy = __shfl_sync(kFull, zsel, (int)(y & 31));
+    if (lane == 0) lsum += (y >= 0 && y < C) ? (double)(mx + logf(se) - zy) : (double)NAN;
+    const float inv = 1.f / se;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = lane + 32 * j;
+      z[j] = ok[j] ? (z[j] * inv - (c == y ? 1.f : 0.f)) * scale : 0.f;  // z = dz now
+      accb[j] += z[j];
+    }
+    float part[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        t = fmaf(z[j], w[k][j], t);
+        acc[k][j] = fmaf(p[k], z[j], acc[k][j]);
+      }
+      part[k] = t;
+    }
+    const float dpv = butterfly_reduce<16>(part);  // lanes 2k, 2k+1: dP[k]
+    const float rs = deg_offsets ? (dg > 0 ? 1.f / (float)dg : 0.f) : 1.f;
+    const int k = lane >> 1;
+    if ((lane & 1) == 0 && k < din) dP[r * lddp + k] = dpv * rs;
+  }
+  // CTA reduction in fixed warp order
+  float *st = hl + (int64_t)warp * 17 * CP;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) st[k * CP + lane + 32 * j] = acc[k][j];
+    st[16 * CP + lane + 32 * j] = accb[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+  if (lane == 0) lred[warp] = lsum;
+  __syncthreads();
+  const int64_t NPF = (int64_t)din * C + C;
+  float *out = partials + (int64_t)blockIdx.x * NPF;
+  for (int i = threadIdx.x; i < (din + 1) * C; i += kWideT) {
+    const int kk = i / C, c = i % C;
+    const int row = kk < din ? kk : 16;
+    float t = 0.f;
+    for (int w2 = 0; w2 < kWideWarps; ++w2) t += hl[((int64_t)w2 * 17 + row) * CP + c];
+    out[i] = t;
+  }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < kWideWarps; ++w2) t += lred[w2];
+    lpart[blockIdx.x] = t;
+  }
+}
+
 int64_t head_wide_grid(int64_t M) {
   const int64_t g = (int64_t)sm_count();
   const int64_t need = ceil_div(M > 0 ? M : 1, (int64_t)kWideT);
@@ -1254,7 +1383,32 @@ int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64
     case 7: GNN_HEAD_WIDE(DN, 7); break;     \
     default: GNN_HEAD_WIDE(DN, 8); break;    \
   }
-    if (Din <= 16) {
+    // lane-per-class form: opt-in (GNN_HEAD_LANES=1); measured slower at the
+    // papers100M shape (171 vs 148 ms: 8 warps/SM at 255 registers cannot hide
+    // its shuffle-reduction chains), see DESIGN.md
+    static const bool lanes_form = [] {
+      const char *e = getenv("GNN_HEAD_LANES");
+      return e && e[0] == '1';
+    }();
+    if (Din <= 16 && lanes_form) {
+#define GNN_HEAD_LANES(NJ)                                                                      \
+  do {                                                                                          \
+    const size_t sm = sizeof(float) * (size_t)kWideWarps * 17 * (NJ * 32);                      \
+    GNN_CUDA_TRY(cudaFuncSetAttribute(gcn_head_lanes_kernel<NJ>,                                \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
+    gcn_head_lanes_kernel<NJ><<<(unsigned)nb, kWideT, sm, st>>>(                                \
+        M, (int)Din, (int)C, P, ldp, W, b, labels, deg_offsets, scale, dP, lddp, partials, lpart); \
+  } while (0)
+      switch (nch) {
+        case 3: GNN_HEAD_LANES(3); break;
+        case 4: GNN_HEAD_LANES(4); break;
+        case 5: GNN_HEAD_LANES(5); break;
+        case 6: GNN_HEAD_LANES(6); break;
+        case 7: GNN_HEAD_LANES(7); break;
+        default: GNN_HEAD_LANES(8); break;
+      }
+#undef GNN_HEAD_LANES
+    } else if (Din <= 16) {
       GNN_HEAD_WIDE_D(16);
     } else {
       GNN_HEAD_WIDE_D(32);

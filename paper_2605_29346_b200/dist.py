@@ -515,6 +515,39 @@ class DistGCNTrainer:
         self.k_adam()
         return self.loss
 
+    def timed_step(self, ex) -> dict:
+        """One epoch with CUDA events around every launch and exchange on the
+        current stream (exchanges unoverlapped, so each is timed alone);
+        returns {name: ms}."""
+        st = torch.cuda.current_stream(self.dev)
+        S = self.part.stride
+        marks = []
+
+        def mark(name, fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            marks.append((name, a, b))
+
+        torch.cuda.synchronize(self.dev)
+        for _, pre, calls, (kind, buf) in self.phases:
+            for name, c in list(pre) + list(calls):
+                mark(name, c)
+            if kind == "gather":
+                if self.peer:
+                    mark("barrier", ex.barrier)
+                else:
+                    mark("all_gather", lambda: ex.all_gather(buf, S))
+            else:
+                mark("all_reduce", lambda: ex.all_reduce(buf))
+        mark("adam", self.k_adam)
+        torch.cuda.synchronize(self.dev)
+        out = {}
+        for name, a, b in marks:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
     def params(self):
         return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}
 

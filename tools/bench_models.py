@@ -307,6 +307,8 @@ def run_papers100m(rank=0, world=1, steps=10, warmup=3, scale=None):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     peak = torch.cuda.max_memory_allocated(dev)
+    per = [tr.timed_step(ex) for _ in range(3)]
+    kern = {k: round(statistics.median(p[k] for p in per), 3) for k in per[0]}
     t = torch.tensor([ms, peak / 2**20, build_peak / 2**20, t_build], device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -322,6 +324,7 @@ def run_papers100m(rank=0, world=1, steps=10, warmup=3, scale=None):
             "scale": scale, "n_gpus": world, "ms": round(float(t[0]), 3),
             "steps": steps, "warmup": warmup, "timing": "CUDA events, max over ranks",
             "loss": float(tr.loss.item()), "launches_per_step": int(launches),
+            "rank0_kernels_ms": kern,
             "rank0_rows": rows, "rank0_edges": deg_edges, "rank0_unique_pairs_csr": nnz_csr,
             "rank0_unique_pairs_csc": nnz_csc,
             "peak_mb_train": round(float(t[1]), 1), "peak_mb_build": round(float(t[2]), 1),
