@@ -517,7 +517,8 @@ def run_ours(args, rank, world):
         extras = {}
         for name, fn in (("gin_reddit", bm.run_gin), ("gat_products", bm.run_gat),
                          ("spmm_sweep_reddit", bm.run_sweep), ("sampling", bm.run_sampling),
-                         ("minibatch_gcn_reddit", bm.run_minibatch)):
+                         ("minibatch_gcn_reddit", bm.run_minibatch),
+                         ("gcn_papers100m", lambda: bm.run_papers100m(0, 1, steps=10, warmup=3))):
             try:
                 extras[name] = fn()
             except Exception as exc:  # report, never hide
@@ -529,11 +530,11 @@ def run_ours(args, rank, world):
 
 # ------------------------------------------------- our arm, N > 1 ranks
 def run_dist(args, rank, world):
-    """Row-partitioned GCN epoch: every rank generates the same
-    graph on its GPU (bit-exact device generator), keeps its edge-balanced row
-    block of the CSR/CSC, and exchanges [V, hidden] blocks with in-place NCCL
-    all-gathers; one all-reduce of the weight gradients.  Strong scaling: the
-    whole Reddit-shape epoch is fixed, split over N GPUs."""
+    """Row-partitioned GCN epoch: every rank builds only its own
+    cost-balanced row block of the CSR/CSC (bit-exact edge stream regenerated
+    and filtered on its GPU) and exchanges [V, hidden] blocks with in-place
+    NCCL all-gathers; one all-reduce of the weight gradients.  Strong
+    scaling: the whole Reddit-shape epoch is fixed, split over N GPUs."""
     import torch
 
     import paper_2605_29346_b200 as gb
@@ -545,14 +546,23 @@ def run_dist(args, rank, world):
     lib = _lib.lib()
     P = REDDIT
     V, E, F, Hd, C = P["V"], P["E"], P["F"], P["H"], P["C"]
-    g = gb.generate(gb.GraphGenSpec("power-law", V, E, exponent=P["exponent"]), P["seed"],
-                    device=dev)
+    # per-rank build: this rank regenerates the bit-exact edge stream and keeps
+    # only its rows of the CSR and CSC (graph.powerlaw_row_block) — no rank
+    # ever holds the whole graph; bounds from the expected degree prefix
+    from paper_2605_29346_b200.dist import ROW_COST, expected_bounds
+
+    spec = gb.GraphGenSpec("power-law", V, E, exponent=P["exponent"])
+    bounds = expected_bounds(spec, world, ROW_COST)
+    blk = gb.graph.powerlaw_row_block(spec, P["seed"], int(bounds[rank]), int(bounds[rank + 1]),
+                                      pack=False)
     # exchange: NCCL all-gathers (default) or, with GNN_DIST_EXCHANGE=peer, the
     # peer-memory form (gnn_spmm_peer reads every rank's block in place through
     # torch symmetric memory; phase boundaries are device-side barriers)
     mode = os.environ.get("GNN_DIST_EXCHANGE", "nccl")
-    part = RowPartition(g, world, rank, coalesced=True, pow2_stride=(mode == "peer"))
-    g.drop_csc()
+    part = RowPartition.from_block(blk, world, rank, bounds, pow2_stride=(mode == "peer"))
+    del blk
+    g = None
+    torch.cuda.empty_cache()
     rng = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(10,)))
     X_all = rng.random((V, F), dtype=np.float32) * 2 - 1
     y_all = np.random.default_rng(np.random.SeedSequence(P["seed"], spawn_key=(13,))).integers(0, C, V)
@@ -613,6 +623,22 @@ def run_dist(args, rank, world):
     t = torch.tensor([ms, e2e_ms], device=dev)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms, e2e_ms = float(t[0]), float(t[1])
+    loss_val = float(tr.loss.item())
+    peak_mb = round(torch.cuda.max_memory_allocated(dev) / 2**20, 1)
+    clocks = clk.summary()
+    extras = {}
+    if not args.no_extras:
+        # BASELINE configs[4]: the papers100M-shaped epoch, row-partitioned over
+        # these N ranks (per-rank block build; every rank runs it)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_models as bm
+
+        del tr, part, g
+        torch.cuda.empty_cache()
+        try:
+            extras["gcn_papers100m"] = bm.run_papers100m(rank, world, steps=10, warmup=3)
+        except Exception as exc:  # report, never hide
+            extras["gcn_papers100m"] = {"error": repr(exc)[:300]}
     return {
         "metric": "gcn_epoch_ms", "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -633,8 +659,12 @@ def run_dist(args, rank, world):
                 "h2d_bytes_per_step": int(X_h.numel() * 4 + y_h.numel() * 8),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches * args.steps),
-        "peak_mb": {"train_phase": round(torch.cuda.max_memory_allocated(dev) / 2**20, 1)},
-        "loss": float(tr.loss.item()), "clocks": clk.summary(),
+        "peak_mb": {"train_phase": peak_mb},
+        "loss": loss_val, "clocks": clocks,
+        "dist": {"backend": torch.distributed.get_backend(), "world_size": world,
+                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                 "nccl_log": "NCCL_DEBUG=INFO (INIT) on stderr: nranks per communicator"},
+        "extras": extras,
     }
 
 
@@ -714,6 +744,11 @@ def main():
         import torch
 
         torch.cuda.set_device(local_device())
+        # NCCL's init log (nranks, rings / NVLS) on stderr, so the scaling run can
+        # verify the communicator size; stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         # NCCL over NVLink/NVSwitch; GNN_DIST_BACKEND=gloo lets the partitioned path be
         # exercised with several ranks sharing one GPU (test only, not a bench number)
         torch.distributed.init_process_group(os.environ.get("GNN_DIST_BACKEND", "nccl"))
