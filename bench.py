@@ -626,6 +626,8 @@ def run_dist(args, rank, world):
     loss_val = float(tr.loss.item())
     peak_mb = round(torch.cuda.max_memory_allocated(dev) / 2**20, 1)
     clocks = clk.summary()
+    overlapped = mode != "peer" and tr.overlap
+    rows_rank0, bounds_l = part.rows, [int(x) for x in part.bounds]
     extras = {}
     if not args.no_extras:
         # BASELINE configs[4]: the papers100M-shaped epoch, row-partitioned over
@@ -650,10 +652,10 @@ def run_dist(args, rank, world):
                                + ("peer-memory SpMM (symmetric memory, NVLink loads)"
                                   if mode == "peer" else "NCCL all-gathers"
                                   + (" overlapped with own-slot aggregation"
-                                     if mode != "peer" and tr.overlap else "")),
+                                     if overlapped else "")),
                    "V": V, "E": E, "K": F, "hidden": Hd, "classes": C, "layout": "coalesced",
                    "optimizer": "adam", "parallelism": f"rowpart{world}",
-                   "rows_rank0": part.rows, "bounds": [int(x) for x in part.bounds],
+                   "rows_rank0": rows_rank0, "bounds": bounds_l,
                    "l2": "inputs larger than L2: no flush needed"},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms",
                 "h2d_bytes_per_step": int(X_h.numel() * 4 + y_h.numel() * 8),
