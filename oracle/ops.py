@@ -13,6 +13,8 @@ SURVEY.md §8c).  Semantics follow SURVEY.md Appendix A:
 
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 
 _CHUNK = 1 << 24  # gathered elements per block (bounds oracle memory)
@@ -31,8 +33,31 @@ def _row_blocks(offsets, K):
         r0 = r1
 
 
+_POOL = None  # oracle.parallel.ForkSpmmPool while inside parallel(pool)
+
+
+@contextlib.contextmanager
+def parallel(pool):
+    """Run every eligible spmm() on ``pool`` (oracle.parallel.ForkSpmmPool):
+    same per-row float64 sums, all host cores."""
+    global _POOL
+    prev, _POOL = _POOL, pool
+    try:
+        yield pool
+    finally:
+        _POOL = prev
+
+
 def spmm(offsets, cols, X, vals=None, heads=1, norm=False, deg_offsets=None):
     """Y[v] = sum_{e in row v} w_e * X[cols_e] (w_e = vals[e, head] or 1)."""
+    if _POOL is not None and vals is None and deg_offsets is None:
+        name = _POOL.lookup(offsets, cols, X)
+        if name is not None:
+            return _POOL.spmm(name, X, norm=norm)
+    return _spmm_serial(offsets, cols, X, vals, heads, norm, deg_offsets)
+
+
+def _spmm_serial(offsets, cols, X, vals=None, heads=1, norm=False, deg_offsets=None):
     offsets = np.asarray(offsets, dtype=np.int64)
     X = np.asarray(X, dtype=np.float64)
     R = offsets.size - 1
@@ -268,19 +293,30 @@ def gat_layer_bwd(offsets, cols, c, dout, absmode=False):
 
 
 # ------------------------------------------------------------------- GIN
-def gin_layer_fwd(offsets, cols, X, W1, b1, W2, b2, eps=0.0, relu_out=False):
+def gin_layer_fwd(offsets, cols, X, W1, b1, W2, b2, eps=0.0, relu_out=False,
+                  transform_first=False):
     """Appendix A.5: Z = MLP((1+eps) X + A X), MLP = Linear -> ReLU -> Linear
-    (SpMMv without norm, PAPER.md:2320-2321 class B)."""
+    (SpMMv without norm, PAPER.md:2320-2321 class B).
+
+    ``transform_first``: evaluate Hs W1 as (1+eps) (X W1) + A (X W1) — the same
+    value in exact arithmetic (A is linear), float64 rounding apart — so a
+    wide input (Reddit K=602) is aggregated at the hidden width; Hs itself is
+    then never formed (the backward takes dW1 = X^T ((1+eps) dU + A^T dU))."""
     X = np.asarray(X, dtype=np.float64)
-    Hs = (1.0 + eps) * X + spmm(offsets, cols, X)
-    U = Hs @ W1 + b1
+    if transform_first:
+        XW = X @ W1
+        Hs = None
+        U = (1.0 + eps) * XW + spmm(offsets, cols, XW) + b1
+    else:
+        Hs = (1.0 + eps) * X + spmm(offsets, cols, X)
+        U = Hs @ W1 + b1
     Ur = np.maximum(U, 0.0)
     Z = Ur @ W2 + b2
     out = np.maximum(Z, 0.0) if relu_out else Z
     return out, dict(X=X, Hs=Hs, U=U, Ur=Ur, Z=Z, W1=W1, W2=W2, eps=eps, relu_out=relu_out)
 
 
-def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False):
+def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False, need_dx=True):
     A = np.abs if absmode else (lambda t: t)
     dZ = A(np.asarray(dout, np.float64))
     if c["relu_out"]:
@@ -289,9 +325,16 @@ def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False):
     dW2 = A(c["Ur"]).T @ dZ
     dU = (dZ @ A(np.asarray(c["W2"], np.float64)).T) * (c["U"] > 0)
     db1 = dU.sum(axis=0)
-    dW1 = A(c["Hs"]).T @ dU
-    dHs = dU @ A(np.asarray(c["W1"], np.float64)).T
-    dX = (1.0 + c["eps"]) * dHs + spmm(t_offsets, t_cols, dHs)
+    W1 = A(np.asarray(c["W1"], np.float64))
+    eps = abs(c["eps"]) if absmode else c["eps"]
+    if c["Hs"] is None:  # transform_first: Hs^T dU = X^T ((1+eps) dU + A^T dU)
+        dXW = (1.0 + eps) * dU + spmm(t_offsets, t_cols, dU)
+        dW1 = A(c["X"]).T @ dXW
+        dX = dXW @ W1.T if need_dx else None
+    else:
+        dW1 = A(c["Hs"]).T @ dU
+        dHs = dU @ W1.T
+        dX = (1.0 + eps) * dHs + spmm(t_offsets, t_cols, dHs) if need_dx else None
     return {"W1": dW1, "b1": db1, "W2": dW2, "b2": db2, "X": dX}
 
 
@@ -316,16 +359,20 @@ def gat2_step(offsets, cols, X, p, labels, heads, slope=0.2):
             "abs": absd}
 
 
-def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0):
-    """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients."""
+def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform_first=False):
+    """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients.
+    ``transform_first`` applies each layer's first Linear before its
+    aggregation (see gin_layer_fwd)."""
+    tf = transform_first
     h1, c1 = gin_layer_fwd(offsets, cols, X, p["W1a"], p["b1a"], p["W1b"], p["b1b"], eps,
-                           relu_out=True)
-    Z, c2 = gin_layer_fwd(offsets, cols, h1, p["W2a"], p["b2a"], p["W2b"], p["b2b"], eps)
+                           relu_out=True, transform_first=tf)
+    Z, c2 = gin_layer_fwd(offsets, cols, h1, p["W2a"], p["b2a"], p["W2b"], p["b2b"], eps,
+                          transform_first=tf)
     loss, dZ = cross_entropy(Z, labels)
     g2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ)
-    g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"])
+    g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"], need_dx=False)
     a2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ, absmode=True)
-    a1 = gin_layer_bwd(t_offsets, t_cols, c1, a2["X"], absmode=True)
+    a1 = gin_layer_bwd(t_offsets, t_cols, c1, a2["X"], absmode=True, need_dx=False)
     grads, absd = {}, {}
     for k, n in {"W1": "W{}a", "b1": "b{}a", "W2": "W{}b", "b2": "b{}b"}.items():
         grads[n.format(1)], grads[n.format(2)] = g1[k], g2[k]
