@@ -316,14 +316,39 @@ def gin_layer_fwd(offsets, cols, X, W1, b1, W2, b2, eps=0.0, relu_out=False,
     return out, dict(X=X, Hs=Hs, U=U, Ur=Ur, Z=Z, W1=W1, W2=W2, eps=eps, relu_out=relu_out)
 
 
+def gin2_forward(offsets, cols, X, p, eps=0.0, transform_first=False):
+    """Forward caches (c1, c2) of gin2_step (each with its layer output "out")."""
+    tf = transform_first
+    h1, c1 = gin_layer_fwd(offsets, cols, X, p["W1a"], p["b1a"], p["W1b"], p["b1b"], eps,
+                           relu_out=True, transform_first=tf)
+    Z, c2 = gin_layer_fwd(offsets, cols, h1, p["W2a"], p["b2a"], p["W2b"], p["b2b"], eps,
+                          transform_first=tf)
+    c1["out"], c2["out"] = h1, Z
+    return c1, c2
+
+
+def gin2_forward_abs(offsets, cols, X, p, eps=0.0):
+    """Appendix A.8 ref_abs scales of the three ReLU pre-activations of
+    gin2_forward(transform_first=True): the same contractions on absolute
+    values (|X| |W1a| aggregated, and so on through the layers)."""
+    e = 1.0 + abs(eps)
+    A = lambda k: np.abs(np.asarray(p[k], np.float64))  # noqa: E731
+    XW = np.abs(np.asarray(X, np.float64)) @ A("W1a")
+    U1 = e * XW + spmm(offsets, cols, XW) + A("b1a")
+    Z1 = U1 @ A("W1b") + A("b1b")
+    HW = Z1 @ A("W2a")
+    U2 = e * HW + spmm(offsets, cols, HW) + A("b2a")
+    return {"U1": U1, "Z1": Z1, "U2": U2}
+
+
 def gin_layer_bwd(t_offsets, t_cols, c, dout, absmode=False, need_dx=True):
     A = np.abs if absmode else (lambda t: t)
     dZ = A(np.asarray(dout, np.float64))
     if c["relu_out"]:
-        dZ = dZ * (c["Z"] > 0)
+        dZ = dZ * c.get("mask_Z", c["Z"] > 0)
     db2 = dZ.sum(axis=0)
     dW2 = A(c["Ur"]).T @ dZ
-    dU = (dZ @ A(np.asarray(c["W2"], np.float64)).T) * (c["U"] > 0)
+    dU = (dZ @ A(np.asarray(c["W2"], np.float64)).T) * c.get("mask_U", c["U"] > 0)
     db1 = dU.sum(axis=0)
     W1 = A(np.asarray(c["W1"], np.float64))
     eps = abs(c["eps"]) if absmode else c["eps"]
@@ -359,15 +384,23 @@ def gat2_step(offsets, cols, X, p, labels, heads, slope=0.2):
             "abs": absd}
 
 
-def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform_first=False):
+def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform_first=False,
+              masks=None, forward=None):
     """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients.
     ``transform_first`` applies each layer's first Linear before its
-    aggregation (see gin_layer_fwd)."""
-    tf = transform_first
-    h1, c1 = gin_layer_fwd(offsets, cols, X, p["W1a"], p["b1a"], p["W1b"], p["b1b"], eps,
-                           relu_out=True, transform_first=tf)
-    Z, c2 = gin_layer_fwd(offsets, cols, h1, p["W2a"], p["b2a"], p["W2b"], p["b2b"], eps,
-                          transform_first=tf)
+    aggregation (see gin_layer_fwd).  ``forward`` = (c1, c2) reuses caches of
+    gin2_forward.  ``masks`` = {"U1", "Z1", "U2": bool [V, w]} sets the ReLU
+    branch the backward takes for those pre-activations (the caller passes
+    the device's branches for units whose pre-activation lies within the
+    forward tolerance of zero, where either branch is a correct result)."""
+    c1, c2 = forward if forward is not None else gin2_forward(
+        offsets, cols, X, p, eps, transform_first)
+    h1, Z = c1["out"], c2["out"]
+    for name, (c, key) in {"U1": (c1, "mask_U"), "Z1": (c1, "mask_Z"),
+                           "U2": (c2, "mask_U")}.items():
+        c.pop(key, None)
+        if masks and name in masks:
+            c[key] = masks[name]
     loss, dZ = cross_entropy(Z, labels)
     g2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ)
     g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"], need_dx=False)

@@ -68,7 +68,7 @@ def test_reddit_spmmv_every_row(reddit, coalesced):
 @pytest.mark.parametrize("coalesced", [False, True])
 def test_reddit_gcn_epoch_matches_oracle(reddit, coalesced):
     """One full-graph GCN epoch (602 -> 16 -> 41, BASELINE configs[2]): loss
-    and all four gradients elementwise, then one Adam step's parameters."""
+    and all four gradients elementwise."""
     from paper_2605_29346_b200.models import GCNTrainer
 
     r = reddit
@@ -85,11 +85,20 @@ def test_reddit_gcn_epoch_matches_oracle(reddit, coalesced):
 
 def test_reddit_gin_epoch_matches_oracle(reddit):
     """One full-graph GIN epoch (hidden 64, eps 0.1; BASELINE configs[2]) at
-    the benchmark's own input scale (X ~ U[-1,1), no rescaling): loss and all
-    eight gradients elementwise.  The oracle applies each layer's first Linear
-    before its aggregation (gin2_step(transform_first=True)), the order the
-    trainer computes in — equal in exact arithmetic, and the Appendix A.8
-    ref_abs scale is then that of the contractions actually performed."""
+    the benchmark's own input scale (X ~ U[-1,1), no rescaling): every ReLU
+    pre-activation (forward), the loss and all eight gradients elementwise.
+
+    * The oracle applies each layer's first Linear before its aggregation
+      (gin2_step(transform_first=True)), the order the trainer computes in —
+      equal in exact arithmetic, and the A.8 ref_abs scale is then that of
+      the contractions actually performed.
+    * ReLU branches: a unit whose oracle pre-activation lies within the A.8
+      forward tolerance of zero (|u_ref| <= 1e-5 * u_abs) may take either
+      branch on the device; the oracle's backward follows the device's branch
+      for exactly those units (and the test asserts every disagreement is of
+      that kind).  A flipped unit at a hub row otherwise moves a bias
+      gradient by ~1e-5 of its scale: the derivative of ReLU is not defined
+      within rounding of its kink."""
     from paper_2605_29346_b200.models import GINTrainer
 
     r = reddit
@@ -99,6 +108,19 @@ def test_reddit_gin_epoch_matches_oracle(reddit):
     tr.forward_backward()
     torch.cuda.synchronize()
     with oo.parallel(r["pool"]):
+        fwd = oo.gin2_forward(r["off"], r["tgt"], r["X"], p, eps=0.1, transform_first=True)
+        scale = oo.gin2_forward_abs(r["off"], r["tgt"], r["X"], p, eps=0.1)
+        masks = {}
+        for name, ref, dev in (("U1", fwd[0]["U"], tr.U1), ("Z1", fwd[0]["Z"], tr.Y1),
+                               ("U2", fwd[1]["U"], tr.U2)):
+            got = dev.cpu().numpy()
+            ok, worst = oo.close(got, np.maximum(ref, 0.0), scale[name], RTOL)
+            assert ok, (name, worst)  # forward values
+            m = got > 0
+            flip = m != (ref > 0)
+            assert np.all(np.abs(ref[flip]) <= RTOL * scale[name][flip]), name
+            assert flip.sum() <= 1e-5 * flip.size, (name, int(flip.sum()))
+            masks[name] = m
         ref = oo.gin2_step(r["off"], r["tgt"], r["t_off"], r["t_rows"], r["X"], p, r["y"],
-                           eps=0.1, transform_first=True)
+                           eps=0.1, transform_first=True, forward=fwd, masks=masks)
     _check_grads(tr, ref, list(p))
