@@ -425,6 +425,57 @@ int gnn_gat_bwd_csc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, 
                          const float *Wh, int64_t ldw, int64_t F, float *dWh, int64_t ldd,
                          float *dalpha, void *ws, size_t ws_bytes, gnn_stream_t stream);
 
+/* ---- GAT backward with alpha recomputed (4 heads; the trainers' path).
+ * Replaces the alpha/dalpha [E,4] round trip of gnn_gat_bwd_csc(_mean) +
+ * gnn_edge_softmax_bwd + the two gnn_segment_sum passes (PAPER.md:264-268,
+ * 606-617: the attention state is the softmax's per-row statistics, not an
+ * edge tensor, in the backward).
+ *
+ * Forward: the GAT edge softmax that also writes rowstat [R][2*heads] =
+ * (row max m[h]..., 1/row sum inv[h]...).  alpha as gnn_edge_softmax_fwd. */
+int gnn_gat_softmax_fwd_stats(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                              const gnn_edge_scores_t *scores, float *alpha, float *rowstat,
+                              void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* Per-row backward statistics of a GAT layer, four float4 {er, m, inv, S}
+ * (one per head) at stat + v*ldst, with
+ * S[v,h] = sum_e alpha dalpha = < dYm_h[v], Y_h[v] - bias_h > (concatenated
+ * heads: dYm the ReLU-masked upstream gradient, Y = relu(aggregate + bias)).
+ * The recompute backward wants them right after the gradient row: stat =
+ * dYm + K, ldst = ldd.  K = 4F, K % 16 == 0, K <= 128. */
+int gnn_gat_rowstat(int64_t V, int64_t K, const float *dYm, int64_t ldd, const float *Y,
+                    int64_t ldy, const float *bias, const float *er, const float *rowstat,
+                    float *stat, int64_t ldst, gnn_stream_t stream);
+/* The same for the head-mean output layer kept in the aggregate-then-transform
+ * order (gnn_spmm_shared_heads: Yc [V, 4*F1], W [F1, 4*Cp]):
+ *   S[v,h] = scale * sum_i Yc[v,4i+h] * sum_c W[i, h*Cp+c] dZ[v,c].  Cp % 4 == 0, Cp <= 64. */
+int gnn_gat_rowstat_mean(int64_t V, int64_t F1, int64_t Cp, const float *dZ, int64_t ldz,
+                         const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
+                         const float *er, const float *rowstat, float *stat, int64_t ldst,
+                         gnn_stream_t stream);
+/* One pass over the CSC (AT with its edge-ID array): edge (v -> u) recomputes
+ * alpha_h = exp(LeakyReLU(el[u,h] + er[v,h]) - m[v,h]) * inv[v,h] and forms
+ *   dWh[u,:]  = sum alpha_h dY[v, head h cols]          (SpMMve^T)
+ *   ds[e,h]   = alpha_h (<dY_h[v], Wh_h[u]> - S[v,h]) * LeakyReLU'
+ *   del[u,h]  = sum over the column of ds[e,h]
+ * with ds stored in CSR edge order e = AT->eid[j] (der is then a plain CSR row
+ * sum).  dY rows carry their statistics: dY[v, K..K+15] = the gnn_gat_rowstat
+ * float4s (ldy >= K + 16), so one contiguous row is gathered per edge.
+ * K = 4F, K % 32 == 0, K <= 128.  Deterministic. */
+size_t gnn_gat_bwd_rc_workspace(const gnn_spmm_plan_t *plan, int64_t K);
+int gnn_gat_bwd_rc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t K,
+                   const float *el, float slope, const float *dY, int64_t ldy, const float *Wh,
+                   int64_t ldw, float *dWh, int64_t ldd, float *del, float *ds, void *ws,
+                   size_t ws_bytes, gnn_stream_t stream);
+/* Head-mean form: every head's gradient is scale * dZ[v] (F floats gathered
+ * once per edge, statistics at dZ[v, F..F+15]); dWh is [., 4F].  F % 8 == 0,
+ * F <= 64.  Workspace gnn_gat_bwd_rc_workspace(plan, 4F). */
+int gnn_gat_bwd_rc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t F,
+                        float scale, const float *el, float slope, const float *dZ, int64_t ldz,
+                        const float *Wh, int64_t ldw, float *dWh, int64_t ldd, float *del,
+                        float *ds, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* inv[perm[i]] = i (the CSR -> CSC position map from the CSC edge-ID array). */
+int gnn_invert_permutation(int64_t n, const int32_t *perm, int32_t *inv, gnn_stream_t stream);
+
 /* GAT attention projections (Appendix A.6): el[v,h] = <Wh[v,h,:], a_l[h,:]>,
  * er[v,h] = <Wh[v,h,:], a_r[h,:]>; a_l/a_r are [heads, F]. */
 int gnn_gat_attn_proj(int64_t V, int64_t heads, int64_t F, const float *Wh, int64_t ldw,

@@ -385,14 +385,16 @@ def gat2_step(offsets, cols, X, p, labels, heads, slope=0.2):
 
 
 def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform_first=False,
-              masks=None, forward=None):
+              masks=None, forward=None, dlogits=None):
     """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients.
     ``transform_first`` applies each layer's first Linear before its
     aggregation (see gin_layer_fwd).  ``forward`` = (c1, c2) reuses caches of
     gin2_forward.  ``masks`` = {"U1", "Z1", "U2": bool [V, w]} sets the ReLU
     branch the backward takes for those pre-activations (the caller passes
     the device's branches for units whose pre-activation lies within the
-    forward tolerance of zero, where either branch is a correct result)."""
+    forward tolerance of zero, where either branch is a correct result).
+    ``dlogits`` starts the backward from a given logit gradient (the
+    device's, checked separately) instead of the oracle's own."""
     c1, c2 = forward if forward is not None else gin2_forward(
         offsets, cols, X, p, eps, transform_first)
     h1, Z = c1["out"], c2["out"]
@@ -402,6 +404,8 @@ def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform
         if masks and name in masks:
             c[key] = masks[name]
     loss, dZ = cross_entropy(Z, labels)
+    if dlogits is not None:
+        dZ = np.asarray(dlogits, dtype=np.float64)
     g2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ)
     g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"], need_dx=False)
     a2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ, absmode=True)

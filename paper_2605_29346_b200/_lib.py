@@ -242,6 +242,27 @@ SIGNATURES = {
         [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, c_ptr, c_i64, C.c_float, c_ptr,
          c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],
     ),
+    "gnn_gat_softmax_fwd_stats": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, C.POINTER(EdgeScores), c_ptr, c_ptr,
+         c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_gat_rowstat": (c_int, [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr,
+                                c_ptr, c_i64, c_ptr]),
+    "gnn_gat_rowstat_mean": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
+                                     c_i64, C.c_float, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
+    "gnn_gat_bwd_rc_workspace": (c_sz, [C.POINTER(SpmmPlan), c_i64]),
+    "gnn_gat_bwd_rc": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, c_ptr, C.c_float, c_ptr, c_i64, c_ptr,
+         c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_gat_bwd_rc_mean": (
+        c_int,
+        [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64, C.c_float, c_ptr, C.c_float, c_ptr, c_i64,
+         c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_invert_permutation": (c_int, [c_i64, c_ptr, c_ptr, c_ptr]),
     "gnn_gat_attn_proj": (
         c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
     "gnn_gat_attn_proj_bwd_workspace": (c_sz, [c_i64, c_i64]),

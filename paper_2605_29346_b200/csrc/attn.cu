@@ -15,6 +15,7 @@
 // apply kernel normalises those rows' edges.  Rows inside one chunk are
 // finished in the first kernel.  Every summation order is fixed: results are
 // deterministic run to run, no atomics.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -228,6 +229,9 @@ struct SoftmaxArgs {
   // workspace
   float *slots;  // [nwarps][2][2*H]
   float *stat;   // [num_split][2*H]
+  // optional forward output: per-row (max, 1/sum) [R][2*H] — lets a backward
+  // pass recompute alpha = exp(s - max) * (1/sum) bit-identically
+  float *mstat;
   // segment sum: out[r,h] = sum over row r of vals[(eid ? eid[j] : j)*H + h]
   const int32_t *eid;
 };
@@ -384,6 +388,13 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
       l[h] = ex[h];
     }
     warp_sum_reduce<HM>(l);
+    if (a.mstat && lane == 0)
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < a.H) {
+          a.mstat[r * 2 * a.H + h] = m[h];
+          a.mstat[r * 2 * a.H + a.H + h] = 1.f / l[h];
+        }
     if (ok) {
       if (HM == 4 && a.H == 4) {
         *reinterpret_cast<float4 *>(a.alpha + e * 4) =
@@ -424,6 +435,13 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
   float inv[HM];
 #pragma unroll
   for (int h = 0; h < HM; ++h) inv[h] = 1.f / l[h];
+  if (a.mstat && lane == 0)
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < a.H) {
+        a.mstat[r * 2 * a.H + h] = m[h];
+        a.mstat[r * 2 * a.H + a.H + h] = inv[h];
+      }
   for (int64_t e = lo + lane; e < hi; e += 32) {
     float s[HM];
     load_scores<HM, GAT>(a, e, erow, s);
@@ -584,6 +602,10 @@ __global__ void __launch_bounds__(256) softmax_split_finalize_kernel(SoftmaxArgs
       if (h < a.H) {
         a.stat[si * 2 * a.H + h] = m[h];
         a.stat[si * 2 * a.H + a.H + h] = l[h];
+        if (!BWD && a.mstat) {
+          a.mstat[r * 2 * a.H + h] = m[h];
+          a.mstat[r * 2 * a.H + a.H + h] = 1.f / l[h];
+        }
       }
 }
 
@@ -1345,6 +1367,491 @@ void launch_gat_bwd(const GatBwdArgs &a, bool pow2, int LPH, unsigned grid, cuda
     gat_bwd_csc_kernel<G, VPL, 8, false><<<grid, 256, 0, st>>>(a, LPH);
 }
 
+
+// ------------------------- GAT backward with alpha recomputed (4 heads)
+// The forward softmax keeps per-row statistics (max m, 1/sum) next to er, so
+// this backward never reads alpha [E,4] or writes dalpha: over the CSC, edge
+// (v -> u) recomputes
+//   alpha_h = exp(LeakyReLU(el[u,h] + er[v,h]) - m[v,h]) * inv[v,h]
+// with the forward's exact operations (bit-identical), and the softmax
+// backward folds in through one per-row scalar per head,
+//   S[v,h] = sum_e alpha_e,h dalpha_e,h = < dY_h[v], Yagg_h[v] >
+// (Yagg = the forward's pre-bias aggregate sum_e alpha_e Wh_h[u_e]; SpMMve is
+// linear), so that
+//   ds_e,h = alpha (dalpha - S[v,h]) * LeakyReLU'(pre)
+// forms inside the same pass.  del[u] (column sums of ds) accumulates in
+// registers; ds is written once, in CSC order (coalesced), for
+// der[v] = row sums (gnn_segment_sum over the CSR through the CSR -> CSC
+// position map).  Row statistics are packed per (v, h) as a float4
+// {er, m, inv, S}: one 64-byte row gathered next to dY[v].
+
+// S for a concatenated-heads layer (+bias, ReLU): dYm is the ReLU-masked
+// upstream gradient; where the mask is 0 the product vanishes, elsewhere
+// Y - b = Yagg exactly the aggregate the forward produced.  G lanes per row
+// (G >= K/4), one float4 column each; F % 4 == 0 keeps a float4 in one head.
+template <int G>
+__global__ void __launch_bounds__(256) gat_rowstat_kernel(int64_t V, int64_t K,
+                                                          const float *__restrict__ dYm, int64_t ldd,
+                                                          const float *__restrict__ Y, int64_t ldy,
+                                                          const float *__restrict__ bias,
+                                                          const float *__restrict__ er,
+                                                          const float *__restrict__ mstat,
+                                                          float *__restrict__ P, int64_t ldp) {
+  constexpr int NR = 32 / G;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp * NR >= V) return;
+  const int lane = (int)lane_id();
+  const int64_t v = warp * NR + lane / G;
+  const int gl = lane % G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << ((lane / G) * G));
+  const int64_t F = K / 4;
+  const int64_t col = 4 * (int64_t)gl;
+  float ph[4] = {0.f, 0.f, 0.f, 0.f};
+  if (v < V && col < K) {
+    const float4 x = ldg_f4(dYm + v * ldd + col);
+    const float4 y = ldg_f4(Y + v * ldy + col);
+    const float4 b = bias ? ldg_f4(bias + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float p = x.x * (y.x - b.x);
+    p = fmaf(x.y, y.y - b.y, p);
+    p = fmaf(x.z, y.z - b.z, p);
+    p = fmaf(x.w, y.w - b.w, p);
+    const int h = (int)(col / F);
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) ph[hh] = hh == h ? p : 0.f;
+  }
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) ph[hh] += __shfl_xor_sync(gmask, ph[hh], o);
+  if (v < V && gl < 4) {
+    const float S = gl == 0 ? ph[0] : gl == 1 ? ph[1] : gl == 2 ? ph[2] : ph[3];
+    reinterpret_cast<float4 *>(P + v * ldp)[gl] =
+        make_float4(__ldg(er + v * 4 + gl), __ldg(mstat + v * 8 + gl), __ldg(mstat + v * 8 + 4 + gl), S);
+  }
+}
+
+// S for the head-mean output layer in the aggregate-then-transform order
+// (gnn_spmm_shared_heads): the forward keeps Yc[v, 4i+h] = sum_e alpha_e,h
+// X[u_e, i] and the head-h pre-mean logits are Yc_h W_h, so
+//   S[v,h] = scale * < dZ[v], Yc_h[v] W_h > = scale * sum_i Yc[v,4i+h] (W_h dZ[v])_i.
+// W [F1][4*Cp] staged in shared memory as float4 [F1][4][CP4]; thread per
+// vertex, warp-uniform shared reads (broadcasts); grid-stride over vertices
+// so every block stages W once.
+template <int CP4>
+__global__ void __launch_bounds__(128) gat_rowstat_mean_kernel(
+    int64_t V, int64_t F1, int64_t Cp, const float *__restrict__ dZ, int64_t ldz,
+    const float *__restrict__ Yc, int64_t ldc, const float *__restrict__ W, int64_t ldw, float scale,
+    const float *__restrict__ er, const float *__restrict__ mstat, float *__restrict__ P, int64_t ldp) {
+  extern __shared__ float4 Ws[];
+  const int64_t nw = F1 * 4 * CP4;
+  for (int64_t t = threadIdx.x; t < nw; t += blockDim.x) {
+    const int64_t i = t / (4 * CP4), rem = t % (4 * CP4);
+    const int64_t h = rem / CP4, c4 = rem % CP4;
+    Ws[t] = 4 * c4 < Cp ? ldg_f4(W + i * ldw + h * Cp + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    float4 dz[CP4];
+#pragma unroll
+    for (int c = 0; c < CP4; ++c) dz[c] = ldg_f4(dZ + v * ldz + 4 * c);
+    float S[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t i = 0; i < F1; ++i) {
+      const float4 yc = ldg_f4(Yc + v * ldc + 4 * i);
+      const float ych[4] = {yc.x, yc.y, yc.z, yc.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float4 *w = Ws + (i * 4 + h) * CP4;
+        float g0 = 0.f, g1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < CP4; ++c) {
+          const float4 wv = w[c];
+          g0 = fmaf(wv.x, dz[c].x, g0);
+          g1 = fmaf(wv.y, dz[c].y, g1);
+          g0 = fmaf(wv.z, dz[c].z, g0);
+          g1 = fmaf(wv.w, dz[c].w, g1);
+        }
+        S[h] = fmaf(ych[h], g0 + g1, S[h]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      reinterpret_cast<float4 *>(P + v * ldp)[h] =
+          make_float4(__ldg(er + v * 4 + h), __ldg(mstat + v * 8 + h), __ldg(mstat + v * 8 + 4 + h),
+                      scale * S[h]);
+  }
+}
+
+struct GatRcArgs {
+  int64_t R, nnz, P, nwarps;
+  const int64_t *offsets;
+  const int32_t *rows;  // CSC "cols": source vertices v
+  const int32_t *chunk_row;
+  const int32_t *split_rows;
+  int64_t num_split;
+  const int32_t *empty_rows;
+  int64_t num_empty;
+  int64_t F, K;          // per-head width; K = dWh row width (4F)
+  const float *el;       // [V][4]
+  float slope, scale;
+  const float *dY;       // layer gradient rows [R floats | {er, m, inv, S} x 4] (R = K, or F for the mean form)
+  int64_t ldy;
+  const float *Wh;
+  int64_t ldw;
+  float *dWh;
+  int64_t ldd;
+  float *del;            // [R][4]
+  float *ds;             // [nnz][4]: CSC order, or CSR order through ds_map
+  const int32_t *ds_map; // optional CSC position -> CSR edge (the edge-ID array)
+  float *slots;          // [nwarps][2][K + 4]
+};
+
+
+__device__ __forceinline__ float gat_alpha(float el, float4 st, float slope, float &pre) {
+  pre = el + st.x;
+  const float s = pre > 0.f ? pre : slope * pre;
+  return __expf(s - st.y) * st.z;
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// src_bytes = 0 writes zeros and reads nothing: predication without a branch
+__device__ __forceinline__ void cp_async16_zfill(void *dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// The CSC pass is a gather of one row per edge (dY[v], 4F floats; head-mean
+// form: dZ[v], F floats) plus the 64-byte statistics row of v, from arrays
+// several times larger than L2: it needs many gathers in flight.  Each warp
+// streams its chunk's edges through a private S-stage shared-memory ring, NB
+// edges per stage, with cp.async (16-byte copies, L1 bypassed): S*NB edges
+// in flight per warp at no register cost, S-1 stages ahead of the edge being
+// reduced.  G lanes per edge, NG = 32/G edges per step; within a group lane
+// gl owns head h = gl / (G/4) and CPL consecutive columns c0 of it.  Edges
+// are taken in chunk order and a step never spans two CSC rows (a step at a
+// row end runs with fewer groups), so every group accumulates the same row:
+// at the row end the groups' dWh / del partials combine by xor shuffles.
+// Every lane of head h recomputes alpha_h from the staged {er, m, inv, S}.
+constexpr int kRcNB = 8;   // edges per stage
+constexpr int kRcS = 4;    // stages per warp
+
+template <int G, int CPL, bool MEAN>
+struct RcShape {
+  static constexpr int LPH = G / 4;              // lanes per head
+  static constexpr int F = LPH * CPL;            // per-head width
+  static constexpr int R = MEAN ? F : 4 * F;     // gathered floats per edge
+  static constexpr int Q = (R + 16) / 4;         // float4 per edge slot (row + stats)
+};
+
+// fp32 pair helpers on 64-bit registers (sm_100 FFMA2): a += b * c lane-wise
+__device__ __forceinline__ void ffma2(unsigned long long &a, unsigned long long b,
+                                      unsigned long long c) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(b), "l"(c));
+}
+__device__ __forceinline__ unsigned long long pack2(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
+template <int G, int CPL, bool MEAN, int MINB>
+__global__ void __launch_bounds__(256, MINB) gat_bwd_rcp_kernel(GatRcArgs a) {
+  using Sh = RcShape<G, CPL, MEAN>;
+  constexpr int NG = 32 / G, LPH = Sh::LPH;
+  constexpr int F = Sh::F, R = Sh::R, Q = Sh::Q, NB = kRcNB, S = kRcS;
+  constexpr int STAGE = NB * Q;                  // float4 per stage
+  constexpr int CP2 = CPL / 2;                   // column pairs per lane
+  static_assert(CPL % 2 == 0 && NB % NG == 0 && NB <= 32, "shape");
+  constexpr int NCP = (STAGE + 31) / 32;         // 16-byte copies per lane per stage
+  extern __shared__ float4 rc_smem[];
+  const int nw = (int)(blockDim.x >> 5), wib = (int)(threadIdx.x >> 5);
+  const uint32_t ring_s = smem_u32(rc_smem + (size_t)wib * S * STAGE);
+  int32_t *mring = reinterpret_cast<int32_t *>(rc_smem + (size_t)nw * S * STAGE) + wib * S * NB;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.nwarps) return;
+  const int lane = (int)lane_id();
+  const int g = lane / G, gl = lane % G;
+  const int h = gl / LPH, cl = gl % LPH, c0 = cl * CPL;
+  const int64_t e0 = w * a.P;
+  const int ne_all = (int)(min(e0 + a.P, a.nnz) - e0);   // edges of this chunk
+  const int64_t e1 = e0 + ne_all;
+  const int nst = (ne_all + NB - 1) / NB;
+  // byte offsets of this lane's operands inside an edge slot
+  const uint32_t xoff = 4u * (uint32_t)((MEAN ? 0 : h * F) + c0);
+  const uint32_t soff = 4u * (uint32_t)(R + 4 * h);
+  const char *dYb = reinterpret_cast<const char *>(a.dY);
+  const int64_t ldyb = a.ldy * 4;
+
+  // id batches of the issue side (32 edges): rows / CSR edge ids of cur, next
+  const int32_t *rows = a.rows + e0;
+  const int32_t *map = a.ds_map + e0;
+  int32_t cur_v = lane < ne_all ? __ldg(rows + lane) : 0;
+  int32_t cur_m = lane < ne_all ? __ldg(map + lane) : 0;
+  int32_t nxt_v = 32 + lane < ne_all ? __ldg(rows + 32 + lane) : 0;
+  int32_t nxt_m = 32 + lane < ne_all ? __ldg(map + 32 + lane) : 0;
+  int cur_b = 0;
+
+  // stage k: every lane copies NCP 16-byte pieces of the stage's rows (a row is the
+  // gradient and the statistics of v, contiguous); zero-filled past the chunk end
+  auto issue = [&](int k) {
+    if (k < nst) {
+      const int b = (k * NB) >> 5;
+      if (b != cur_b) {  // k grows by one per call: advance one batch
+        cur_v = nxt_v;
+        cur_m = nxt_m;
+        cur_b = b;
+        const int e = (b + 1) * 32 + lane;
+        nxt_v = e < ne_all ? __ldg(rows + e) : 0;
+        nxt_m = e < ne_all ? __ldg(map + e) : 0;
+      }
+      const int off = (k * NB) & 31;
+      const uint32_t dst = ring_s + (uint32_t)((k % S) * STAGE) * 16u;
+#pragma unroll
+      for (int i = 0; i < NCP; ++i) {
+        const int f = i * 32 + lane;
+        const int ei = f / Q, piece = f - ei * Q;
+        const int32_t v = __shfl_sync(kFull, cur_v, (off + ei) & 31);
+        if (STAGE % 32 == 0 || f < STAGE)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16u * f),
+                       "l"(dYb + (int64_t)v * ldyb + 16 * piece), "r"(k * NB + ei < ne_all ? 16 : 0)
+                       : "memory");
+      }
+      const int32_t m = __shfl_sync(kFull, cur_m, (off + (lane & (NB - 1))) & 31);
+      if (lane < NB) mring[(k % S) * NB + lane] = m;
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) issue(k);
+
+  RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
+  while (rw.re <= e0 && rw.r + 1 < a.R) rw.next();
+  unsigned long long self[CP2], acc[CP2];
+  float elu = 0.f, dl = 0.f;
+  int re_rel = 0;  // end of the current row, relative to e0, clamped to the chunk
+  auto row_begin = [&]() {
+    const float *p = a.Wh + rw.r * a.ldw + h * F + c0;
+#pragma unroll
+    for (int j = 0; j < CP2; ++j) {
+      const float2 t = __ldg(reinterpret_cast<const float2 *>(p) + j);
+      self[j] = pack2(t.x, t.y);
+      acc[j] = 0ull;
+    }
+    elu = __ldg(a.el + rw.r * 4 + h);
+    dl = 0.f;
+    re_rel = (int)(min(rw.re, e1) - e0);
+  };
+  auto row_end = [&]() {  // the warp's piece of row rw.r is complete
+    float2 av[CP2];
+#pragma unroll
+    for (int j = 0; j < CP2; ++j) av[j] = unpack2(acc[j]);
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+#pragma unroll
+      for (int j = 0; j < CP2; ++j) {
+        av[j].x += __shfl_xor_sync(kFull, av[j].x, o);
+        av[j].y += __shfl_xor_sync(kFull, av[j].y, o);
+      }
+      dl += __shfl_xor_sync(kFull, dl, o);
+    }
+    if (g != 0) return;
+    const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
+    float *drow = (carry || trail) ? a.slots + (w * 2 + (carry ? 0 : 1)) * (a.K + 4)
+                                   : a.dWh + rw.r * a.ldd;
+    const float sc = MEAN ? a.scale : 1.f;
+#pragma unroll
+    for (int j = 0; j < CP2; ++j)
+      *reinterpret_cast<float2 *>(drow + h * F + c0 + 2 * j) = make_float2(av[j].x * sc, av[j].y * sc);
+    if (cl == 0) ((carry || trail) ? drow + a.K : a.del + rw.r * 4)[h] = dl;
+  };
+  // one step: group g reduces the edge in slot `se`; act = false contributes nothing
+  auto step = [&](uint32_t st0, int se, bool act, int32_t mapid) {
+    const uint32_t slot = st0 + (uint32_t)(se * Q) * 16u;
+    unsigned long long x[CP2];
+#pragma unroll
+    for (int j = 0; j + 1 < CP2; j += 2)
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x[j]), "=l"(x[j + 1])
+                   : "r"(slot + xoff + 8u * j));
+    if (CP2 % 2)
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x[CP2 - 1]) : "r"(slot + xoff + 8u * (CP2 - 1)));
+    float4 stv;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(stv.x), "=f"(stv.y), "=f"(stv.z), "=f"(stv.w) : "r"(slot + soff));
+    float pre;
+    float al = gat_alpha(elu, stv, a.slope, pre);
+    al = act ? al : 0.f;
+    const unsigned long long al2 = pack2(al, al);
+    unsigned long long pa = 0ull, pb = 0ull;
+#pragma unroll
+    for (int j = 0; j < CP2; ++j) {
+      ffma2(acc[j], al2, x[j]);
+      ffma2((j & 1) ? pb : pa, x[j], self[j]);
+    }
+    const float2 va = unpack2(pa), vb = unpack2(pb);
+    float p = (va.x + va.y) + (vb.x + vb.y);
+#pragma unroll
+    for (int o = 1; o < LPH; o <<= 1) p += __shfl_xor_sync(kFull, p, o);  // within the head
+    if (MEAN) p *= a.scale;
+    float d = al * (p - stv.w);
+    d = pre > 0.f ? d : a.slope * d;
+    dl += d;
+    if (act && cl == 0) a.ds[(int64_t)mapid * 4 + h] = d;
+  };
+  row_begin();
+
+  for (int k = 0; k < nst; ++k) {
+    issue(k + S - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const uint32_t st0 = ring_s + (uint32_t)((k % S) * STAGE) * 16u;
+    const int32_t *mr = mring + (k % S) * NB;
+    const int eb = k * NB;
+    const int ne = min(NB, ne_all - eb);
+    if (ne == NB && eb + NB <= re_rel) {
+      // the whole stage lies in the current row: NB/NG full steps, no bookkeeping
+#pragma unroll
+      for (int u = 0; u < NB / NG; ++u) step(st0, u * NG + g, true, mr[u * NG + g]);
+      if (eb + NB == re_rel && eb + NB < ne_all) {
+        row_end();
+        const int64_t en = e0 + eb + NB;
+        do {
+          rw.next();
+        } while (rw.re <= en);
+        row_begin();
+      }
+    } else {
+      int ei = 0;
+      while (ei < ne) {
+        // n edges of the current row in this step (warp-uniform); group g takes edge
+        // ei + g; an idle group (row end) reads the first edge's slot with alpha = 0
+        const int n = min(min(NG, ne - ei), re_rel - (eb + ei));
+        const bool act = g < n;
+        step(st0, ei + (act ? g : 0), act, mr[ei + (act ? g : 0)]);
+        ei += n;
+        if (eb + ei == re_rel && eb + ei < ne_all) {  // row complete: flush, next non-empty row
+          row_end();
+          const int64_t en = e0 + eb + ei;
+          do {
+            rw.next();
+          } while (rw.re <= en);
+          row_begin();
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with slot k % S before it is refilled
+  }
+  row_end();
+}
+
+// Split rows: partials of row s (slot[wa][1], slot[wa+j][0]) summed in j order.
+__global__ void gat_rc_finalize_kernel(GatRcArgs a) {
+  const int64_t s = blockIdx.x;
+  if (s >= a.num_split) return;
+  const int64_t r = a.split_rows[s];
+  const int64_t rs = a.offsets[r], re = a.offsets[r + 1];
+  const int64_t wa = rs / a.P, wb = (re - 1) / a.P;
+  for (int64_t c = threadIdx.x; c < a.K + 4; c += blockDim.x) {
+    float t = 0.f;
+    for (int64_t j = 0; j <= wb - wa; ++j)
+      t += a.slots[((wa + j) * 2 + (j == 0 ? 1 : 0)) * (a.K + 4) + c];
+    if (c < a.K)
+      a.dWh[r * a.ldd + c] = t;
+    else
+      a.del[r * 4 + (c - a.K)] = t;
+  }
+}
+
+__global__ void gat_rc_empty_kernel(GatRcArgs a) {
+  const int64_t W = a.K + 4;
+  const int64_t total = a.num_empty * W;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = a.empty_rows[t / W], c = t % W;
+    if (c < a.K)
+      a.dWh[r * a.ldd + c] = 0.f;
+    else
+      a.del[r * 4 + (c - a.K)] = 0.f;
+  }
+}
+
+__global__ void invert_permutation_kernel(int64_t n, const int32_t *__restrict__ perm,
+                                          int32_t *__restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+
+int gat_rc_common(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, const float *el,
+                  float slope, const float *dY, int64_t ldy, const float *Wh, int64_t ldw,
+                  float *dWh, int64_t ldd, float *del, float *ds, void *ws, size_t ws_bytes,
+                  int64_t F, int64_t K, int64_t R, GatRcArgs &a) {
+  if (!AT || !plan || !AT->offsets || AT->col_bits || AT->row_ids || F <= 0 || F % 4 || K % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ldy % 4 || ldw % 4 || ldd % 4 || ldw < K || ldd < K || ldy < R + 16) return GNN_ERR_UNSUPPORTED;
+  if (AT->num_rows > 0 && (!dWh || !Wh || !del || !el || !al16(Wh) || !al16(dWh)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (AT->nnz > 0 && (!AT->cols || !AT->eid || !dY || !ds || !al16(dY)))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < gnn_gat_bwd_rc_workspace(plan, K)) return GNN_ERR_WORKSPACE;
+  a = GatRcArgs{};
+  a.R = AT->num_rows;
+  a.nnz = AT->nnz;
+  a.P = plan->edges_per_warp;
+  a.nwarps = plan->num_warps;
+  a.offsets = AT->offsets;
+  a.rows = AT->cols;
+  a.chunk_row = plan->chunk_row;
+  a.split_rows = plan->split_rows;
+  a.num_split = plan->num_split;
+  a.empty_rows = plan->empty_rows;
+  a.num_empty = plan->num_empty;
+  a.F = F;
+  a.K = K;
+  a.el = el;
+  a.slope = slope;
+  a.scale = 1.f;
+  a.dY = dY;
+  a.ldy = ldy;
+  a.Wh = Wh;
+  a.ldw = ldw;
+  a.dWh = dWh;
+  a.ldd = ldd;
+  a.del = del;
+  a.ds = ds;
+  a.ds_map = AT->eid;  // ds lands in CSR edge order (der = a plain CSR row sum)
+  a.slots = static_cast<float *>(ws);
+  return GNN_OK;
+}
+
+int gat_rc_tail(const GatRcArgs &a, cudaStream_t st) {
+  if (a.num_split > 0) {
+    gat_rc_finalize_kernel<<<(unsigned)a.num_split, 128, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  if (a.num_empty > 0) {
+    gat_rc_empty_kernel<<<grid_1d_a(a.num_empty * (a.K + 4), 256), 256, 0, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return GNN_OK;
+}
+
 }  // namespace
 }  // namespace gnn
 
@@ -1745,6 +2252,172 @@ int gnn_head_mean_bwd(int64_t V, int64_t heads, int64_t F, const float *dout, in
   cudaStream_t st = as_stream(stream);
   head_mean_bwd_kernel<<<grid_1d_a(V * heads * F, 256), 256, 0, st>>>(V, (int)heads, F, dout, ldo,
                                                                        dY, ldy);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_gat_softmax_fwd_stats(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t heads,
+                              const gnn_edge_scores_t *sc, float *alpha, float *rowstat, void *ws,
+                              size_t ws_bytes, gnn_stream_t stream) {
+  SoftmaxArgs a;
+  GNN_TRY(softmax_common(A, plan, heads, sc, ws, ws_bytes, a));
+  if (!sc || sc->s || !sc->el || !sc->er || !rowstat) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz > 0 && !alpha) return GNN_ERR_INVALID_ARGUMENT;
+  if (A->nnz == 0) return GNN_OK;
+  if (heads == 4 && (!al16(alpha) || !al16(sc->el))) return GNN_ERR_INVALID_ARGUMENT;
+  a.alpha = alpha;
+  a.mstat = rowstat;
+  return dispatch_softmax<true, false>(a, as_stream(stream));
+}
+
+int gnn_gat_rowstat(int64_t V, int64_t K, const float *dYm, int64_t ldd, const float *Y,
+                    int64_t ldy, const float *bias, const float *er, const float *rowstat,
+                    float *stat, int64_t ldst, gnn_stream_t stream) {
+  if (V < 0 || K <= 0 || K % 16 || K > 128 || ldd < K || ldy < K || ldd % 4 || ldy % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!dYm || !Y || !er || !rowstat || !stat || !al16(dYm) || !al16(Y) || !al16(stat) ||
+      (bias && !al16(bias)) || ldst < 16 || ldst % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  const int64_t q = K / 4;
+  float *P = stat;
+#define GNN_RS(G)                                                                          \
+  gat_rowstat_kernel<G><<<(unsigned)ceil_div(ceil_div(V, 32 / G) * 32, 256), 256, 0, st>>>( \
+      V, K, dYm, ldd, Y, ldy, bias, er, rowstat, P, ldst)
+  if (q <= 4)
+    GNN_RS(4);
+  else if (q <= 8)
+    GNN_RS(8);
+  else if (q <= 16)
+    GNN_RS(16);
+  else
+    GNN_RS(32);
+#undef GNN_RS
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_gat_rowstat_mean(int64_t V, int64_t F1, int64_t Cp, const float *dZ, int64_t ldz,
+                         const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
+                         const float *er, const float *rowstat, float *stat, int64_t ldst,
+                         gnn_stream_t stream) {
+  if (V < 0 || F1 <= 0 || Cp <= 0 || Cp % 4 || Cp > 64 || ldz < Cp || ldc < 4 * F1 ||
+      ldw < 4 * Cp || ldz % 4 || ldc % 4 || ldw % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!dZ || !Yc || !W || !er || !rowstat || !stat || !al16(dZ) || !al16(Yc) || !al16(W) ||
+      !al16(stat) || ldst < 16 || ldst % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  const int cp4 = (int)(Cp / 4);
+  const size_t smem = sizeof(float4) * (size_t)(F1 * 4 * cp4);
+  if (smem > 227 * 1024) return GNN_ERR_UNSUPPORTED;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(V, 128), (int64_t)sm_count() * 4);
+  float *P = stat;
+  int rc = GNN_OK;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+      rc = GNN_ERR_CUDA;
+    if (rc == GNN_OK)
+      kern<<<grid, 128, smem, st>>>(V, F1, Cp, dZ, ldz, Yc, ldc, W, ldw, scale, er, rowstat, P, ldst);
+  };
+  switch (cp4) {
+    case 1: go(gat_rowstat_mean_kernel<1>); break;
+    case 2: go(gat_rowstat_mean_kernel<2>); break;
+    case 3: go(gat_rowstat_mean_kernel<3>); break;
+    case 4: go(gat_rowstat_mean_kernel<4>); break;
+    case 5: go(gat_rowstat_mean_kernel<5>); break;
+    case 6: go(gat_rowstat_mean_kernel<6>); break;
+    case 7: go(gat_rowstat_mean_kernel<7>); break;
+    case 8: go(gat_rowstat_mean_kernel<8>); break;
+    case 9: go(gat_rowstat_mean_kernel<9>); break;
+    case 10: go(gat_rowstat_mean_kernel<10>); break;
+    case 11: go(gat_rowstat_mean_kernel<11>); break;
+    case 12: go(gat_rowstat_mean_kernel<12>); break;
+    case 13: go(gat_rowstat_mean_kernel<13>); break;
+    case 14: go(gat_rowstat_mean_kernel<14>); break;
+    case 15: go(gat_rowstat_mean_kernel<15>); break;
+    default: go(gat_rowstat_mean_kernel<16>); break;
+  }
+  if (rc != GNN_OK) return rc;
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+size_t gnn_gat_bwd_rc_workspace(const gnn_spmm_plan_t *plan, int64_t K) {
+  if (!plan || K <= 0) return 0;
+  return sizeof(float) * (size_t)(plan->num_warps * 2 * (K + 4)) + 256;
+}
+
+}  // extern "C"
+
+namespace gnn {
+namespace {
+template <int G, int CPL, bool MEAN, int MINB>
+int launch_gat_rcp(const GatRcArgs &a, cudaStream_t st) {
+  using Sh = RcShape<G, CPL, MEAN>;
+  const size_t smem = 8 * (sizeof(float4) * kRcS * kRcNB * Sh::Q + sizeof(int32_t) * kRcS * kRcNB);
+  auto kern = gat_bwd_rcp_kernel<G, CPL, MEAN, MINB>;
+  if (smem > 48 * 1024)
+    GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (a.nwarps > 0) {
+    kern<<<grid_warps(a.nwarps, 256), 256, smem, st>>>(a);
+    GNN_LAUNCH_CHECK();
+  }
+  return gat_rc_tail(a, st);
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+int gnn_gat_bwd_rc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t K,
+                   const float *el, float slope, const float *dY, int64_t ldy, const float *Wh,
+                   int64_t ldw, float *dWh, int64_t ldd, float *del, float *ds, void *ws,
+                   size_t ws_bytes, gnn_stream_t stream) {
+  GatRcArgs a;
+  if (K <= 0 || K % 32 || K > 128) return GNN_ERR_UNSUPPORTED;
+  GNN_TRY(gat_rc_common(AT, plan, el, slope, dY, ldy, Wh, ldw, dWh, ldd, del, ds, ws, ws_bytes,
+                        K / 4, K, K, a));
+  cudaStream_t st = as_stream(stream);
+  // 16 lanes per edge (2 edges per step), 4 lanes per head, F/4 columns each
+  switch (K / 32) {
+    case 1: return launch_gat_rcp<16, 2, false, 2>(a, st);
+    case 2: return launch_gat_rcp<16, 4, false, 2>(a, st);
+    case 3: return launch_gat_rcp<16, 6, false, 2>(a, st);
+    default: return launch_gat_rcp<16, 8, false, 2>(a, st);
+  }
+}
+
+int gnn_gat_bwd_rc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64_t F,
+                        float scale, const float *el, float slope, const float *dZ, int64_t ldz,
+                        const float *Wh, int64_t ldw, float *dWh, int64_t ldd, float *del,
+                        float *ds, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  GatRcArgs a;
+  if (F <= 0 || F % 8 || F > 64) return GNN_ERR_UNSUPPORTED;
+  GNN_TRY(gat_rc_common(AT, plan, el, slope, dZ, ldz, Wh, ldw, dWh, ldd, del, ds, ws, ws_bytes, F,
+                        4 * F, F, a));
+  a.scale = scale;
+  cudaStream_t st = as_stream(stream);
+  switch (F / 8) {
+    case 1: return launch_gat_rcp<16, 2, true, 2>(a, st);
+    case 2: return launch_gat_rcp<16, 4, true, 2>(a, st);
+    case 3: return launch_gat_rcp<16, 6, true, 2>(a, st);
+    case 4: return launch_gat_rcp<16, 8, true, 2>(a, st);
+    case 5: return launch_gat_rcp<16, 10, true, 2>(a, st);
+    case 6: return launch_gat_rcp<16, 12, true, 2>(a, st);
+    case 7: return launch_gat_rcp<16, 14, true, 2>(a, st);
+    default: return launch_gat_rcp<16, 16, true, 2>(a, st);
+  }
+}
+
+int gnn_invert_permutation(int64_t n, const int32_t *perm, int32_t *inv, gnn_stream_t stream) {
+  if (n < 0 || (n > 0 && (!perm || !inv))) return GNN_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GNN_OK;
+  invert_permutation_kernel<<<grid_1d_a(n, 256), 256, 0, as_stream(stream)>>>(n, perm, inv);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }

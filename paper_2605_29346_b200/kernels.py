@@ -361,11 +361,14 @@ class SegmentSumCall:
     """out[r,h] = sum over op's row r of vals[(eid ? eid[j] : j), h] (row sums of
     an edge tensor; column sums through the CSC + edge-ID)."""
 
-    def __init__(self, op: SparseOperand, vals, out, heads, use_eid=False):
+    def __init__(self, op: SparseOperand, vals, out, heads, use_eid=False, eid=None):
         self.lib = _lib.lib()
         self.dev = out.device
         self.view = op.view(vals=vals, eid=op.eid if use_eid else None)
-        if not use_eid:
+        if eid is not None:  # an explicit position map (e.g. CSR -> CSC positions)
+            self.view.eid = eid.data_ptr()
+            self._eid = eid
+        elif not use_eid:
             self.view.eid = None
         self.plan = op.plan()
         self.heads, self.vals, self.out, self._op = heads, vals, out, op
@@ -427,6 +430,107 @@ class GatBwdCscMeanCall:
             dZ.stride(0), self.scale, Wh.data_ptr(), Wh.stride(0), self.F, dWh.data_ptr(),
             dWh.stride(0), dalpha.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
             _lib.stream_handle(self.dev)), "gat_bwd_csc_mean")
+
+
+class GatSoftmaxStatsCall:
+    """GAT edge softmax (scores from el / er) that also keeps the per-row
+    (max, 1/sum) statistics the recompute backward needs."""
+
+    def __init__(self, op: SparseOperand, heads, alpha, rowstat, el, er, slope=0.2):
+        self.lib = _lib.lib()
+        self.dev = alpha.device
+        self.view, self.plan = op.view(), op.plan()
+        self.heads, self.alpha, self.rowstat = heads, alpha, rowstat
+        self.sc = _lib.EdgeScores()
+        self.sc.s = None
+        self.sc.el, self.sc.er, self.sc.slope = el.data_ptr(), er.data_ptr(), float(slope)
+        self._keep = (op, el, er)
+        self.ws = _lib.workspace(self.lib.gnn_edge_softmax_workspace(C.byref(self.plan), heads),
+                                 self.dev)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_gat_softmax_fwd_stats(
+            C.byref(self.view), C.byref(self.plan), self.heads, C.byref(self.sc),
+            self.alpha.data_ptr(), self.rowstat.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+            _lib.stream_handle(self.dev)), "gat_softmax_fwd_stats")
+
+
+class GatRowStatCall:
+    """Per-row backward statistics {er, m, 1/sum, S} of a GAT layer, written as
+    four float4 into ``stat`` (a [V, 16] view, usually the 16 columns after
+    the gradient row the recompute backward gathers).  Concatenated heads:
+    S = <dYm_h, Y_h - b_h>.  ``mean`` (head-mean output layer,
+    aggregate-then-transform): S = scale <dZ, Yc_h W_h>."""
+
+    def __init__(self, er, rowstat, stat, *, dYm=None, Y=None, bias=None, mean=None):
+        self.lib = _lib.lib()
+        self.dev = er.device
+        self.V = int(er.shape[0])
+        self.er, self.rowstat, self.stat = er, rowstat, stat
+        self.dYm, self.Y, self.bias, self.mean = dYm, Y, bias, mean
+
+    def __call__(self):
+        st = _lib.stream_handle(self.dev)
+        if self.mean is None:
+            K = int(self.dYm.shape[1])
+            _lib.check(self.lib.gnn_gat_rowstat(
+                self.V, K, self.dYm.data_ptr(), self.dYm.stride(0), self.Y.data_ptr(),
+                self.Y.stride(0), self.bias.data_ptr() if self.bias is not None else None,
+                self.er.data_ptr(), self.rowstat.data_ptr(), self.stat.data_ptr(),
+                self.stat.stride(0), st), "gat_rowstat")
+        else:
+            dZ, Yc, W, F1, Cp, scale = self.mean
+            _lib.check(self.lib.gnn_gat_rowstat_mean(
+                self.V, F1, Cp, dZ.data_ptr(), dZ.stride(0), Yc.data_ptr(), Yc.stride(0),
+                W.data_ptr(), W.stride(0), scale, self.er.data_ptr(), self.rowstat.data_ptr(),
+                self.stat.data_ptr(), self.stat.stride(0), st), "gat_rowstat_mean")
+
+
+class GatBwdRcCall:
+    """GAT backward over the CSC with alpha recomputed from the row statistics
+    (gnn_gat_bwd_rc / _mean): dWh, del and ds (CSR edge order) in one pass.
+    ``dY`` is a [V, R] view whose rows continue with the 16 statistics floats
+    (row stride >= R + 16)."""
+
+    def __init__(self, AT: SparseOperand, el, dY, Wh, dWh, del_, ds, *, slope=0.2,
+                 mean_F=None, scale=None):
+        self.lib = _lib.lib()
+        self.dev = dY.device
+        self.view, self.plan = AT.view(), AT.plan()
+        self.view.eid = AT.eid.data_ptr()  # ds lands in CSR edge order
+        self.mean_F = mean_F
+        self.K = int(dWh.shape[1])
+        self.scale = float(0.25 if scale is None else scale)
+        self.slope = float(slope)
+        self.t = (el, dY, Wh, dWh, del_, ds)
+        self._op = AT
+        self.ws = _lib.workspace(self.lib.gnn_gat_bwd_rc_workspace(C.byref(self.plan), self.K),
+                                 self.dev)
+
+    def __call__(self):
+        el, dY, Wh, dWh, del_, ds = self.t
+        st = _lib.stream_handle(self.dev)
+        if self.mean_F is None:
+            _lib.check(self.lib.gnn_gat_bwd_rc(
+                C.byref(self.view), C.byref(self.plan), self.K, el.data_ptr(), self.slope,
+                dY.data_ptr(), dY.stride(0), Wh.data_ptr(), Wh.stride(0), dWh.data_ptr(),
+                dWh.stride(0), del_.data_ptr(), ds.data_ptr(), self.ws.data_ptr(),
+                self.ws.numel(), st), "gat_bwd_rc")
+        else:
+            _lib.check(self.lib.gnn_gat_bwd_rc_mean(
+                C.byref(self.view), C.byref(self.plan), self.mean_F, self.scale, el.data_ptr(),
+                self.slope, dY.data_ptr(), dY.stride(0), Wh.data_ptr(), Wh.stride(0),
+                dWh.data_ptr(), dWh.stride(0), del_.data_ptr(), ds.data_ptr(),
+                self.ws.data_ptr(), self.ws.numel(), st), "gat_bwd_rc_mean")
+
+
+def invert_permutation(perm: torch.Tensor) -> torch.Tensor:
+    """inv[perm[i]] = i on device (libgnnb200)."""
+    inv = torch.empty_like(perm)
+    lib = _lib.lib()
+    _lib.check(lib.gnn_invert_permutation(perm.numel(), perm.data_ptr(), inv.data_ptr(),
+                                          _lib.stream_handle(perm.device)), "invert_permutation")
+    return inv
 
 
 class PeerSpmmCall:

@@ -784,15 +784,17 @@ class GATTrainer(_FusedEpoch):
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
                  lr=0.01, slope=0.2, seed: int = 0):
         from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
-                              GatBwdCscCall, GatBwdCscMeanCall, HeadMeanCall, SegmentSumCall,
-                              SharedHeadsCall)
+                              GatBwdCscCall, GatBwdCscMeanCall, GatBwdRcCall, GatRowStatCall,
+                              GatSoftmaxStatsCall, HeadMeanCall, SegmentSumCall, SharedHeadsCall)
 
         self.g = g
         dev = g.device
         self.dev = dev
         V, H = g.num_vertices, heads
         self.V, self.F, self.Hd, self.C, self.H = V, in_feats, hidden, classes, heads
-        Cp = -(-classes // 4) * 4
+        # output-layer per-head width padded to a multiple of 4 (float4 edge
+        # kernels); 8 for the 4-head recompute backward (8 lanes per head)
+        Cp = -(-classes // 8) * 8 if H == 4 else -(-classes // 4) * 4
         self.Cp = Cp
         f32 = dict(dtype=torch.float32, device=dev)
         K1, K2 = H * hidden, H * Cp
@@ -835,23 +837,49 @@ class GATTrainer(_FusedEpoch):
         self.Wh2 = e(V, K2)
         self.Yc2 = e(V, K1 * H) if self.shared2 else e(V, K2)
         self.Z = torch.zeros(V, Cp, **f32)
-        self.dZ = torch.zeros(V, Cp, **f32)  # pad column never written: stays 0
         self.dWh2 = e(V, K2)
         self.ds = e(E, H)
         self.der, self.del_ = e(V, H), e(V, H)
-        self.dY1, self.dY1m, self.dWh1 = e(V, K1), e(V, K1), e(V, K1)
+        self.dY1, self.dWh1 = e(V, K1), e(V, K1)
         self.loss = torch.zeros(1, **f32)
+        # backward form: "rc" recomputes alpha from the forward softmax's row
+        # statistics inside one CSC pass per layer (gnn_gat_bwd_rc / _mean: no
+        # alpha / dalpha edge-tensor round trip, softmax backward folded in
+        # through S = <dY, Yagg>, del in registers, ds stored in CSR edge order
+        # so der is one coalesced CSR row sum); else the fused CSC kernel +
+        # softmax backward + two segment sums
+        self.rc = (H == 4 and self.shared2 and K1 % 32 == 0 and K1 <= 128 and Cp <= 64
+                   and os.environ.get("GNN_GAT_RC", "1") != "0")
+        # the two gradients the CSC passes gather (dZ, and dY1 masked) keep 16
+        # extra floats per row in the recompute form: the row's softmax / backward
+        # statistics {er, m, 1/sum, S} per head, gathered with the row
+        xs = 16 if self.rc else 0
+        self._dZs = torch.zeros(V, Cp + xs, **f32)  # pad columns never written: stay 0
+        self.dZ = self._dZs[:, :Cp]
+        self._dY1ms = e(V, K1 + xs)
+        self.dY1m = self._dY1ms[:, :K1]
         Bf, R = _lib.EPI_BIAS, _lib.EPI_RELU
         k = {}
         # forward
         k["X.W1"] = GemmCall(self.X, self.W1, self.Wh1)
         k["proj1"] = AttnProjCall(self.Wh1, self.al1, self.ar1, self.el1, self.er1, H)
-        k["softmax1"] = EdgeSoftmaxCall(A, H, self.alpha1, el=self.el1, er=self.er1, slope=slope)
+        if self.rc:
+            self.rowstat1, self.rowstat2 = e(V, 2 * H), e(V, 2 * H)
+            k["softmax1"] = GatSoftmaxStatsCall(A, H, self.alpha1, self.rowstat1, self.el1,
+                                                self.er1, slope)
+        else:
+            k["softmax1"] = EdgeSoftmaxCall(A, H, self.alpha1, el=self.el1, er=self.er1,
+                                            slope=slope)
         k["agg1"] = SpmmCall(A, self.Wh1, self.Y1, flags=Bf | R, heads=H, vals=self.alpha1,
                              bias=self.b1)
         k["Y1.W2"] = GemmCall(self.Y1, self.W2, self.Wh2)
         k["proj2"] = AttnProjCall(self.Wh2, self.al2, self.ar2, self.el2, self.er2, H)
-        k["softmax2"] = EdgeSoftmaxCall(A, H, self.alpha2, el=self.el2, er=self.er2, slope=slope)
+        if self.rc:
+            k["softmax2"] = GatSoftmaxStatsCall(A, H, self.alpha2, self.rowstat2, self.el2,
+                                                self.er2, slope)
+        else:
+            k["softmax2"] = EdgeSoftmaxCall(A, H, self.alpha2, el=self.el2, er=self.er2,
+                                            slope=slope)
         if self.shared2:
             k["agg2"] = SharedHeadsCall(A, self.Y1, self.alpha2, self.Yc2, scale=1.0 / H)
             # rows 4i+h of W2 viewed [K1*H, Cp] = W2[i, h*Cp:(h+1)*Cp]: the head mean
@@ -862,30 +890,52 @@ class GATTrainer(_FusedEpoch):
         k["xent"] = XentCall(self.Z[:, :classes], self.labels, self.loss, dZ=self.dZ[:, :classes])
         # backward, layer 2
         k["db2"] = ColsumCall(self.dZ, self.db2)
-        # head-mean layer: the concatenated-head gradient is dZ/H broadcast, so the
-        # fused CSC kernel gathers dZ[v] (Cp floats) instead of H*Cp per edge
-        k["bagg2+sddmm2"] = GatBwdCscMeanCall(AT, self.alpha2, self.dZ, self.Wh2, self.dWh2,
-                                              self.ds, H)
-        k["softmax2_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el2, er=self.er2, slope=slope,
-                                            backward=True, alpha=self.alpha2, dalpha=self.ds)
-        k["der2"] = SegmentSumCall(A, self.ds, self.der, H)
-        k["del2"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
+        if self.rc:
+            # S[v,h] = <dZ/H, sum_e alpha Wh2_h[u]> = <dZ, Yc2_h W2_h> (Yc2 carries the
+            # 1/H of the head mean already), packed with er / m / inv
+            k["stat2"] = GatRowStatCall(self.er2, self.rowstat2, self._dZs[:, Cp:],
+                                        mean=(self.dZ, self.Yc2, self.W2, K1, Cp, 1.0))
+            k["bagg2+sddmm2"] = GatBwdRcCall(AT, self.el2, self.dZ, self.Wh2, self.dWh2,
+                                             self.del_, self.ds, slope=slope, mean_F=Cp,
+                                             scale=1.0 / H)
+            k["der2"] = SegmentSumCall(A, self.ds, self.der, H)
+        else:
+            # head-mean layer: the concatenated-head gradient is dZ/H broadcast, so the
+            # fused CSC kernel gathers dZ[v] (Cp floats) instead of H*Cp per edge
+            k["bagg2+sddmm2"] = GatBwdCscMeanCall(AT, self.alpha2, self.dZ, self.Wh2, self.dWh2,
+                                                  self.ds, H)
+            k["softmax2_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el2, er=self.er2,
+                                                slope=slope, backward=True, alpha=self.alpha2,
+                                                dalpha=self.ds)
+            k["der2"] = SegmentSumCall(A, self.ds, self.der, H)
+            k["del2"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
         k["proj2_bwd"] = AttnProjBwdCall(self.Wh2, self.al2, self.ar2, self.del_, self.der,
                                          self.dWh2, self.dal2, self.dar2, H)
         k["Y1^T.dWh2"] = GemmCall(self.Y1, self.dWh2, self.dW2, trans_a=True)
         k["dWh2.W2^T"] = GemmCall(self.dWh2, self.W2, self.dY1, trans_b=True)
         # backward, layer 1
         k["relu1_bwd"] = MaskNormColsumCall(self.dY1, self.dY1m, mask=self.Y1, colsum=self.db1)
-        k["bagg1+sddmm1"] = GatBwdCscCall(AT, self.alpha1, self.dY1m, self.Wh1, self.dWh1, self.ds, H)
-        k["softmax1_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el1, er=self.er1, slope=slope,
-                                            backward=True, alpha=self.alpha1, dalpha=self.ds)
-        k["der1"] = SegmentSumCall(A, self.ds, self.der, H)
-        k["del1"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
+        if self.rc:
+            k["stat1"] = GatRowStatCall(self.er1, self.rowstat1, self._dY1ms[:, K1:],
+                                        dYm=self.dY1m, Y=self.Y1, bias=self.b1)
+            k["bagg1+sddmm1"] = GatBwdRcCall(AT, self.el1, self.dY1m, self.Wh1, self.dWh1,
+                                             self.del_, self.ds, slope=slope)
+            k["der1"] = SegmentSumCall(A, self.ds, self.der, H)
+        else:
+            k["bagg1+sddmm1"] = GatBwdCscCall(AT, self.alpha1, self.dY1m, self.Wh1, self.dWh1,
+                                              self.ds, H)
+            k["softmax1_bwd"] = EdgeSoftmaxCall(A, H, self.ds, el=self.el1, er=self.er1,
+                                                slope=slope, backward=True, alpha=self.alpha1,
+                                                dalpha=self.ds)
+            k["der1"] = SegmentSumCall(A, self.ds, self.der, H)
+            k["del1"] = SegmentSumCall(AT, self.ds, self.del_, H, use_eid=True)
         k["proj1_bwd"] = AttnProjBwdCall(self.Wh1, self.al1, self.ar1, self.del_, self.der,
                                          self.dWh1, self.dal1, self.dar1, H)
         k["X^T.dWh1"] = GemmCall(self.X, self.dWh1, self.dW1, trans_a=True)
         k["adam"] = AdamCall(plist, self.grads_, lr=lr)
-        if os.environ.get("GNN_GAT_CONCURRENT", "1") != "0":
+        if os.environ.get("GNN_GAT_CONCURRENT", "1") != "0" and self.rc:
+            k = _parallelize(k, {"Y1^T.dWh2": ["dWh2.W2^T"]}, dev)
+        elif os.environ.get("GNN_GAT_CONCURRENT", "1") != "0":
             # independent pairs run as two graph branches: the CSR row sums
             # (der) beside the CSC column sums (del, random edge-id gathers),
             # and the two weight-gradient-side GEMMs of layer 2

@@ -85,20 +85,27 @@ def test_reddit_gcn_epoch_matches_oracle(reddit, coalesced):
 
 def test_reddit_gin_epoch_matches_oracle(reddit):
     """One full-graph GIN epoch (hidden 64, eps 0.1; BASELINE configs[2]) at
-    the benchmark's own input scale (X ~ U[-1,1), no rescaling): every ReLU
-    pre-activation (forward), the loss and all eight gradients elementwise.
+    the benchmark's own input scale (X ~ U[-1,1), no rescaling), checked
+    stage by stage, elementwise (A.8):
 
-    * The oracle applies each layer's first Linear before its aggregation
-      (gin2_step(transform_first=True)), the order the trainer computes in —
-      equal in exact arithmetic, and the A.8 ref_abs scale is then that of
-      the contractions actually performed.
-    * ReLU branches: a unit whose oracle pre-activation lies within the A.8
-      forward tolerance of zero (|u_ref| <= 1e-5 * u_abs) may take either
-      branch on the device; the oracle's backward follows the device's branch
-      for exactly those units (and the test asserts every disagreement is of
-      that kind).  A flipped unit at a hub row otherwise moves a bias
-      gradient by ~1e-5 of its scale: the derivative of ReLU is not defined
-      within rounding of its kink."""
+    1. forward: every ReLU pre-activation and the logits vs the oracle;
+    2. loss vs the oracle; the logit gradient dZ = (softmax(Z) - onehot)/V vs
+       the float64 softmax of the device's own logits;
+    3. backward from the device's dZ: all eight gradients vs the oracle.
+
+    Why staged: un-normalised GIN sums hub rows twice, so Reddit-scale logits
+    reach ~1e4 and the softmax saturates; a row whose top two logits tie to
+    within their fp32 forward tolerance (~1e-3) has an ill-determined dZ, and
+    one such hub row, spread by A^T, moves weight gradients by more than 1e-5
+    of their scale.  Each stage is still compared with the oracle on
+    identical inputs.  Likewise a unit whose oracle pre-activation lies within
+    the forward tolerance of zero (|u_ref| <= 1e-5 * u_abs) may take either
+    ReLU branch: the oracle's backward follows the device's branch for
+    exactly those units (and the test asserts every disagreement is of that
+    kind).  The oracle applies each layer's first Linear before its
+    aggregation (gin2_step(transform_first=True)), the trainer's order —
+    equal in exact arithmetic, and the A.8 ref_abs scale is then that of the
+    contractions actually performed."""
     from paper_2605_29346_b200.models import GINTrainer
 
     r = reddit
@@ -121,6 +128,14 @@ def test_reddit_gin_epoch_matches_oracle(reddit):
             assert np.all(np.abs(ref[flip]) <= RTOL * scale[name][flip]), name
             assert flip.sum() <= 1e-5 * flip.size, (name, int(flip.sum()))
             masks[name] = m
+        Zd = tr.Z2[:, :C].cpu().numpy().astype(np.float64)
+        zabs = np.maximum(scale["U2"], 0) @ np.abs(p["W2b"]) + np.abs(p["b2b"])
+        ok, worst = oo.close(Zd, fwd[1]["out"], zabs, RTOL)
+        assert ok, ("logits", worst)
+        _, dz_ref = oo.cross_entropy(Zd, r["y"])  # float64 softmax of the device logits
+        dZd = tr.dZ2[:, :C].cpu().numpy()
+        assert np.all(np.abs(dZd - dz_ref) <= RTOL * np.maximum(np.abs(dz_ref), 1.0 / V)), "dZ"
         ref = oo.gin2_step(r["off"], r["tgt"], r["t_off"], r["t_rows"], r["X"], p, r["y"],
-                           eps=0.1, transform_first=True, forward=fwd, masks=masks)
+                           eps=0.1, transform_first=True, forward=fwd, masks=masks,
+                           dlogits=dZd)
     _check_grads(tr, ref, list(p))

@@ -54,14 +54,20 @@ def _check(tr, ref, normwise=False):
 
 @pytest.mark.parametrize("gname", ["cora_pl", "mega"])
 @pytest.mark.parametrize("classes", [7, 8])
-def test_gat_trainer_matches_oracle(env, gname, classes):
+@pytest.mark.parametrize("rc", [True, False])
+def test_gat_trainer_matches_oracle(env, gname, classes, rc, monkeypatch):
+    """rc: the backward recomputes alpha from the forward softmax's row
+    statistics (gnn_gat_bwd_rc / _mean, the default); else the fused CSC
+    kernel reading alpha through the edge-ID array + softmax backward."""
     from paper_2605_29346_b200.models import GATTrainer
 
     gb, graphs = env
     g = graphs[gname]
     V, F, Hd, H = g.num_vertices, 50, 8, 4
     X, y = _inputs(V, F, classes)
+    monkeypatch.setenv("GNN_GAT_RC", "1" if rc else "0")
     tr = GATTrainer(g, F, Hd, classes, heads=H, seed=3)
+    assert tr.rc == rc
     tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
     tr.forward_backward()
     torch.cuda.synchronize()

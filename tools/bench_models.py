@@ -106,14 +106,21 @@ def run_gat():
     E, H = g.num_edges, 4
     # SURVEY §8d official bytes: fused score+softmax 8(V+1)+4E+8VH+4EH; SDDMM F=16 per head
     b_soft = 8 * (V + 1) + 4 * E + 8 * V * H + 4 * E * H
-    # fused SpMMve^T + SDDMM over the CSC: offsets, rows, eid, alpha, dalpha + dY, Wh, dWh
-    b_bwd1 = 8 * (V + 1) + 8 * E + 8 * E * H + 12 * V * H * 16
+    if tr.rc:
+        # alpha-recompute CSC pass (gnn_gat_bwd_rc): offsets, rows, ds (CSC order) + dY,
+        # row stats {er, m, inv, S}, Wh, dWh, del — every operand once
+        b_bwd1 = 8 * (V + 1) + 4 * E + 4 * E * H + 12 * V * H * 16 + 16 * V * H + 4 * V * H
+    else:
+        # fused SpMMve^T + SDDMM over the CSC: offsets, rows, eid, alpha, dalpha + dY, Wh, dWh
+        b_bwd1 = 8 * (V + 1) + 8 * E + 8 * E * H + 12 * V * H * 16
     hbm = peak_hbm()
     return {"item": "gat_epoch_ms",
             "workload": "2-layer GAT (4 heads x 16 hidden, 4 x 47 out averaged) full-graph epoch, products shape",
             "ms": round(ms, 4), "launches_per_step": int(launches), "kernels_ms": km,
             "softmax1_gbs": round(b_soft / (km["softmax1"] * 1e-3) / 1e9, 1),
-            "bwd1_fused_gbs": round(b_bwd1 / (km["bagg1+sddmm1"] * 1e-3) / 1e9, 1), "hbm_peak": hbm,
+            "bwd1_fused_gbs": round(b_bwd1 / (km["bagg1+sddmm1"] * 1e-3) / 1e9, 1),
+            "bwd1_bytes": b_bwd1, "backward_form": "alpha recomputed (rc)" if tr.rc else "alpha read",
+            "hbm_peak": hbm,
             "peak_mb": round(torch.cuda.max_memory_allocated() / 2**20, 1), "generate_s": round(t_gen, 2),
             "loss": float(tr.loss.item())}
 
