@@ -1542,7 +1542,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // at the row end the groups' dWh / del partials combine by xor shuffles.
 // Every lane of head h recomputes alpha_h from the staged {er, m, inv, S}.
 constexpr int kRcNB = 8;   // edges per stage
-constexpr int kRcS = 4;    // stages per warp
+// stages per warp: as deep as two 8-warp blocks per SM allow (~110 KB each)
+template <int Q>
+constexpr int rc_stages() {
+  return (110 * 1024) / (8 * kRcNB * Q * 16) < 4 ? 4 : (110 * 1024) / (8 * kRcNB * Q * 16);
+}
 
 template <int G, int CPL, bool MEAN>
 struct RcShape {
@@ -1572,7 +1576,7 @@ template <int G, int CPL, bool MEAN, int MINB>
 __global__ void __launch_bounds__(256, MINB) gat_bwd_rcp_kernel(GatRcArgs a) {
   using Sh = RcShape<G, CPL, MEAN>;
   constexpr int NG = 32 / G, LPH = Sh::LPH;
-  constexpr int F = Sh::F, R = Sh::R, Q = Sh::Q, NB = kRcNB, S = kRcS;
+  constexpr int F = Sh::F, R = Sh::R, Q = Sh::Q, NB = kRcNB, S = rc_stages<Sh::Q>();
   constexpr int STAGE = NB * Q;                  // float4 per stage
   constexpr int CP2 = CPL / 2;                   // column pairs per lane
   static_assert(CPL % 2 == 0 && NB % NG == 0 && NB <= 32, "shape");
@@ -2359,7 +2363,8 @@ namespace {
 template <int G, int CPL, bool MEAN, int MINB>
 int launch_gat_rcp(const GatRcArgs &a, cudaStream_t st) {
   using Sh = RcShape<G, CPL, MEAN>;
-  const size_t smem = 8 * (sizeof(float4) * kRcS * kRcNB * Sh::Q + sizeof(int32_t) * kRcS * kRcNB);
+  constexpr int S = rc_stages<Sh::Q>();
+  const size_t smem = 8 * (sizeof(float4) * S * kRcNB * Sh::Q + sizeof(int32_t) * S * kRcNB);
   auto kern = gat_bwd_rcp_kernel<G, CPL, MEAN, MINB>;
   if (smem > 48 * 1024)
     GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
