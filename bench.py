@@ -479,6 +479,8 @@ def run_ours(args, rank, world):
         for name, fn in (("gin_reddit", bm.run_gin), ("gat_products", bm.run_gat),
                          ("spmm_sweep_reddit", bm.run_sweep), ("sampling", bm.run_sampling),
                          ("minibatch_gcn_reddit", bm.run_minibatch),
+                         ("gcn_reddit_variants", bm.run_variants),
+                         ("csr_csc_build_reddit", bm.run_build),
                          ("gcn_papers100m", lambda: bm.run_papers100m(0, 1, steps=10, warmup=3))):
             try:
                 extras[name] = fn()

@@ -5,6 +5,9 @@
   sweep    SpMMv / SpMMve K sweep 16..256, Reddit shape               [BASELINE configs[1]]
   sampling device sample_minibatch / DeviceSampler vs the reference sampler (host)
   minibatch sampled mini-batch GCN training step, Reddit shape (SampledGCNTrainer)
+  build    device CSR / CSC(+eid) builders at the Reddit shape vs the reference port
+  variants GCN epoch + SpMMv K=32 on the canonical layout, the uniform-random control,
+           seeds 43 / 44
   papers100m 2-layer GCN epoch, ogbn-papers100M shape (V=111M, E=1.6B, K=128 -> 16 -> 172),
            row-partitioned over the N ranks of the run, per-rank block build [configs[4]]
 
@@ -247,6 +250,126 @@ def run_minibatch():
 
 
 
+def run_build(reps=5):
+    """Device CSR / CSC builders in isolation on the Reddit shape (BASELINE
+    configs[1] graph): csr_from_edges from the device int64 (src, dst) stream
+    (reference graph.py:106-114) and the transposed build with the edge-ID
+    array, CUDA-event medians; roofline on SURVEY §8d's
+    algorithmic bytes (CSR 16E + 4E + 8(V+1); CSC+eid 8(V+1) + 4E + 8(V+1) +
+    4E + 4E).  Beside them the reference algorithm (oracle numpy port, one
+    host thread like the reference) on a bounded sample: the first 1/8 of the
+    same edge stream, whole V."""
+    from oracle import graph as og
+
+    V, E = REDDIT["V"], REDDIT["E"]
+    hbm = peak_hbm()
+    src, dst = gb.graph.powerlaw_edges_device(V, E, 2.1, 42)
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            r = fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+            del r
+        return statistics.median(ts[1:])
+
+    t_csr = timed(lambda: gb.csr_from_edges(V, src, dst, device="cuda"))
+    g = gb.csr_from_edges(V, src, dst, device="cuda")
+
+    def csc():
+        g.drop_csc()
+        return g.csc(with_eid=True)
+
+    t_csc = timed(csc)
+    b_csr = 16 * E + 4 * E + 8 * (V + 1)
+    b_csc = 8 * (V + 1) + 4 * E + 8 * (V + 1) + 4 * E + 4 * E
+    ns = E // 8
+    hs, hd = src[:ns].cpu().numpy(), dst[:ns].cpu().numpy()
+    del src, dst
+    t0 = time.perf_counter()
+    off, tgt = og.csr_from_edges(V, hs, hd)
+    c_csr = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    og.transpose(V, V, off, tgt)
+    c_csc = time.perf_counter() - t0
+    return {"item": "csr_csc_build", "V": V, "E": E,
+            "csr_from_edges": {"ms": round(t_csr, 3), "bytes": b_csr,
+                               "gbs": round(b_csr / (t_csr * 1e-3) / 1e9, 1),
+                               "frac": round(b_csr / (t_csr * 1e-3) / 1e9 / hbm, 4)},
+            "csc_with_eid": {"ms": round(t_csc, 3), "bytes": b_csc,
+                             "gbs": round(b_csc / (t_csc * 1e-3) / 1e9, 1),
+                             "frac": round(b_csc / (t_csc * 1e-3) / 1e9 / hbm, 4)},
+            "cpu_reference_port": {"sample": f"first {ns} edges of the stream (1/8), V={V}",
+                                   "csr_from_edges_ms": round(c_csr * 1e3, 1),
+                                   "transpose_ms": round(c_csc * 1e3, 1), "threads": 1}}
+
+
+def run_variants():
+    """Simple-graph and seed controls of the headline: the GCN
+    epoch (device-timed CUDA-graph replay, 602 -> 16 -> 41, Adam) and SpMMv
+    K=32 (degree-norm fused, L2 flushed between reps, median of 15) on
+      * the canonical layout of the seed-42 power-law graph (every stored edge
+        gathered: what a simple graph without duplicate pairs gets);
+      * the uniform-random control (reference pkg/tests/conftest.py:40-42),
+        generated with the reference's own stream (host draws, device CSR);
+      * seeds 43 and 44 (reference configs/default.json:3-6).
+    The headline itself runs on the coalesced layout of seed 42."""
+    from paper_2605_29346_b200.models import GCNTrainer
+
+    V, E = REDDIT["V"], REDDIT["E"]
+    hbm = peak_hbm()
+    flush = torch.empty(64 * 2**20, device="cuda")
+    out = []
+    for name, kind, seed, coalesced in (("powerlaw_s42_canonical", "power-law", 42, False),
+                                        ("uniform_s42", "uniform-random", 42, True),
+                                        ("powerlaw_s43", "power-law", 43, True),
+                                        ("powerlaw_s44", "power-law", 44, True)):
+        t0 = time.perf_counter()
+        g = gb.generate(gb.GraphGenSpec(kind, V, E, exponent=2.1), seed, device="cuda")
+        torch.cuda.synchronize()
+        t_gen = time.perf_counter() - t0
+        nnz = g.csr_coalesced().nnz if coalesced else E
+        X = torch.rand(V, 602, device="cuda") * 2 - 1
+        y = torch.randint(0, 41, (V,), device="cuda")
+        tr = GCNTrainer(g, 602, 16, 41, seed=seed, coalesced=coalesced)
+        tr.set_inputs(X, y)
+        tr.step()
+        ms = time_graph(tr)
+        km = kernel_ms(tr)
+        del tr
+        X32 = torch.rand(V, 32, device="cuda") * 2 - 1
+        Y32 = torch.empty_like(X32)
+        call = SpmmCall(g.operand("csr_coalesced" if coalesced else "csr"), X32, Y32,
+                        flags=_lib.EPI_NORM)
+        ts = []
+        for _ in range(15):
+            flush.add_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            call()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t32 = statistics.median(ts[3:])
+        b32 = 8 * (V + 1) + 4 * E + 8 * V * 32
+        out.append({"item": "gcn_epoch_variant", "graph": name, "layout":
+                    "coalesced" if coalesced else "canonical", "unique_pairs": int(nnz),
+                    "duplicate_frac": round(1 - g.csr_coalesced().nnz / E, 4),
+                    "epoch_ms": round(ms, 4), "kernels_ms": km,
+                    "spmmv_k32": {"ms": round(t32, 4), "gbs": round(b32 / (t32 * 1e-3) / 1e9, 1),
+                                  "frac": round(b32 / (t32 * 1e-3) / 1e9 / hbm, 4),
+                                  "gather_tbs": round(4 * nnz * 32 / (t32 * 1e-3) / 1e12, 2)},
+                    "generate_s": round(t_gen, 2)})
+        del call, g, X, y, X32, Y32
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_papers100m(rank=0, world=1, steps=10, warmup=3, scale=None):
     """2-layer GCN epoch on the ogbn-papers100M-shaped power-law graph
     (BASELINE configs[4]), row-partitioned over the run's ranks.  Every rank
@@ -344,7 +467,8 @@ def run_papers100m(rank=0, world=1, steps=10, warmup=3, scale=None):
 if __name__ == "__main__":
     for item in sys.argv[1:] or ["gin", "gat", "sweep"]:
         r = {"gin": run_gin, "gat": run_gat, "sweep": run_sweep, "sampling": run_sampling,
-             "minibatch": run_minibatch, "papers100m": run_papers100m}[item]()
+             "minibatch": run_minibatch, "papers100m": run_papers100m,
+             "variants": run_variants, "build": run_build}[item]()
         for x in (r if isinstance(r, list) else [r]):
             print(json.dumps(x), flush=True)
         torch.cuda.empty_cache()
