@@ -385,7 +385,7 @@ def gat2_step(offsets, cols, X, p, labels, heads, slope=0.2):
 
 
 def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform_first=False,
-              masks=None, forward=None, dlogits=None):
+              masks=None, forward=None, dlogits=None, fwd_abs=None):
     """2-layer GIN (ReLU between layers), mean cross-entropy, all gradients.
     ``transform_first`` applies each layer's first Linear before its
     aggregation (see gin_layer_fwd).  ``forward`` = (c1, c2) reuses caches of
@@ -394,7 +394,13 @@ def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform
     the device's branches for units whose pre-activation lies within the
     forward tolerance of zero, where either branch is a correct result).
     ``dlogits`` starts the backward from a given logit gradient (the
-    device's, checked separately) instead of the oracle's own."""
+    device's, checked separately) instead of the oracle's own.
+    ``fwd_abs`` = gin2_forward_abs(...) makes the A.8 scales of the weight
+    gradients follow "the same op on |inputs|" through the forward too: the
+    activations a weight gradient contracts (relu(U1), Y1, relu(U2)) enter
+    the abs pass at their forward abs scale (masked by the taken ReLU branch)
+    instead of at |activation|, so a forward value that is small only through
+    cancellation carries its forward tolerance into the gradient's bound."""
     c1, c2 = forward if forward is not None else gin2_forward(
         offsets, cols, X, p, eps, transform_first)
     h1, Z = c1["out"], c2["out"]
@@ -408,8 +414,17 @@ def gin2_step(offsets, cols, t_offsets, t_cols, X, p, labels, eps=0.0, transform
         dZ = np.asarray(dlogits, dtype=np.float64)
     g2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ)
     g1 = gin_layer_bwd(t_offsets, t_cols, c1, g2["X"], need_dx=False)
-    a2 = gin_layer_bwd(t_offsets, t_cols, c2, dZ, absmode=True)
-    a1 = gin_layer_bwd(t_offsets, t_cols, c1, a2["X"], absmode=True, need_dx=False)
+    ca1, ca2 = c1, c2
+    if fwd_abs is not None:
+        m = lambda c, key, v: c.get(key, v > 0)  # noqa: E731
+        ca1 = dict(c1, Ur=fwd_abs["U1"] * m(c1, "mask_U", c1["U"]))
+        ca2 = dict(c2, Ur=fwd_abs["U2"] * m(c2, "mask_U", c2["U"]),
+                   X=fwd_abs["Z1"] * m(c1, "mask_Z", c1["Z"]))
+        if ca2["Hs"] is not None:  # aggregate-first: Hs = (1+eps) X + A X on the abs scale
+            e = 1.0 + abs(eps)
+            ca2["Hs"] = e * ca2["X"] + spmm(offsets, cols, ca2["X"])
+    a2 = gin_layer_bwd(t_offsets, t_cols, ca2, dZ, absmode=True)
+    a1 = gin_layer_bwd(t_offsets, t_cols, ca1, a2["X"], absmode=True, need_dx=False)
     grads, absd = {}, {}
     for k, n in {"W1": "W{}a", "b1": "b{}a", "W2": "W{}b", "b2": "b{}b"}.items():
         grads[n.format(1)], grads[n.format(2)] = g1[k], g2[k]

@@ -318,6 +318,15 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo, uint32
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
+// The tensor cores' fp32 accumulation rounds each MMA's sum toward zero, so a
+// long chain of MMAs into one TMEM accumulator drifts when every product has
+// the same sign (GIN's U1^T dY1 at 233K rows: 400 MMAs per split, 3.9e-5 of
+// sum |terms| measured, 1e-5 required).  Each unit therefore accumulates
+// kTnChunk k-blocks (16 MMA pairs) per TMEM pass and the epilogue warps add
+// the chunk into fp32 registers (round-to-nearest), double-buffered so the
+// next chunk's MMAs run under the read-out.
+constexpr int kTnChunk = 2;
+
 template <int NB>
 constexpr int tn_stages() {
   return NB <= 32 ? 5 : (NB <= 64 ? 4 : 3);
@@ -432,10 +441,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
         int kb0, kb1, m0, n0;
         int64_t sp;
         unit_of(u, kb0, kb1, m0, n0, sp);
-        mbar_wait(acc_empty + ab, aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(ab * kAcc);
+        uint32_t d = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
+          const int kc = (kb - kb0) % kTnChunk;  // k-block within this accumulation chunk
+          if (kc == 0) {
+            mbar_wait(acc_empty + ab, aph ^ 1);
+            tc_fence_after();
+            d = tmem + (uint32_t)(ab * kAcc);
+          }
           mbar_wait(split + s, ph);
           tc_fence_after();
           const uint32_t a_hi = smem_u32(sa + (size_t)s * kTcM * kTcBK);
@@ -446,19 +459,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
             const uint64_t ah = mn_desc(a_hi + k * 1024, 4096, 512, 1);
             const uint64_t al = mn_desc(a_lo + k * 1024, 4096, 512, 1);
             const uint64_t bc = mn_desc(b_hl + k * 1024, 4096, 512, 1);  // [hi atoms | lo atoms]
-            tc_mma_tf32(d, ah, bc, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            tc_mma_tf32(d, ah, bc, idesc, (kc != 0 || k != 0) ? 1u : 0u);
             tc_mma_tf32(d, al, bc, idesc, 1);
           }
           tc_commit(empty + s);
-          if (kb == kb1 - 1) tc_commit(acc_full + ab);
+          if (kc == kTnChunk - 1 || kb == kb1 - 1) {
+            tc_commit(acc_full + ab);
+            if (++ab == 2) {
+              ab = 0;
+              aph ^= 1;
+            }
+          }
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
-        }
-        if (++ab == 2) {
-          ab = 0;
-          aph ^= 1;
         }
       }
     }
@@ -514,29 +529,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
       int kb0, kb1, m0, n0;
       int64_t sp;
       unit_of(u, kb0, kb1, m0, n0, sp);
-      mbar_wait(acc_full + ab, aph);
-      tc_fence_after();
       const int64_t m = (int64_t)m0 + q * 32 + lane;
-      float *dst = p.partials + (sp * p.M + m) * p.N;
-#pragma unroll 1
-      for (int c0 = 0; c0 < NB; c0 += 16) {
-        uint32_t v[16], w[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
-        tmem_ld16(taddr, v);
-        tmem_ld16(taddr + NB, w);  // B_lo half
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (m < p.M) {
+      float acc[NB];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (n0 + c0 + j < p.N) dst[n0 + c0 + j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
+      for (int j = 0; j < NB; ++j) acc[j] = 0.f;
+      const int nchunks = (kb1 - kb0 + kTnChunk - 1) / kTnChunk;
+#pragma unroll 1
+      for (int ch = 0; ch < nchunks; ++ch) {
+        mbar_wait(acc_full + ab, aph);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < NB; c0 += 16) {
+          uint32_t v[16], w[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
+          tmem_ld16(taddr, v);
+          tmem_ld16(taddr + NB, w);  // B_lo half
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(v[j]) + __uint_as_float(w[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty + ab);
-      if (++ab == 2) {
-        ab = 0;
-        aph ^= 1;
+      if (m < p.M) {
+        float *dst = p.partials + (sp * p.M + m) * p.N;
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (n0 + j < p.N) dst[n0 + j] = acc[j];
       }
     }
   }
