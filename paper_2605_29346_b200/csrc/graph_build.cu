@@ -45,9 +45,11 @@ struct PassArgs {
   long long *minmax;       // [4] kmin,kmax,v0min,v0max, or null
 };
 
-__device__ __forceinline__ int64_t load_src_raw(const SrcDesc &s, int64_t i) {
-  if (s.kind == SRC_I64) return static_cast<const int64_t *>(s.p)[i];
-  if (s.kind == SRC_I32) return static_cast<const int32_t *>(s.p)[i];
+
+template <int KIND>
+__device__ __forceinline__ int64_t load_src(const void *p, int64_t i) {
+  if constexpr (KIND == SRC_I64) return static_cast<const int64_t *>(p)[i];
+  if constexpr (KIND == SRC_I32) return static_cast<const int32_t *>(p)[i];
   return i;
 }
 
@@ -69,7 +71,49 @@ __device__ __forceinline__ void block_minmax(long long lo, long long hi, long lo
   }
 }
 
+// CTA-wide min / max, then ONE pair of global atomics per CTA (per-warp
+// atomics on the same two words serialise at the L2 slice).  All threads call.
+template <int NW>
+__device__ __forceinline__ void cta_minmax(long long lo, long long hi, long long *dst) {
+  __shared__ long long red[2][NW];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFull, lo, o));
+    hi = max(hi, __shfl_xor_sync(kFull, hi, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if (lane_id() == 0) {
+    red[0][w] = lo;
+    red[1][w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < NW; ++i) {
+      lo = min(lo, red[0][i]);
+      hi = max(hi, red[1][i]);
+    }
+    if (lo != LLONG_MAX) atomicMin(dst, lo);
+    if (hi != LLONG_MIN) atomicMax(dst + 1, hi);
+  }
+}
+
+// Lanes of the warp holding the same BITS-bit digit as this lane (and valid):
+// one ballot per digit bit (a short fixed sequence; MATCH.ANY measured slow).
 template <int BITS>
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
+  unsigned peers = __ballot_sync(kFull, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bb = __ballot_sync(kFull, bit);
+    peers &= bit ? bb : ~bb;
+  }
+  return peers;
+}
+
+// Per-tile digit histogram (per-warp shared-memory counters; warp-aggregated
+// adds via ballots or MATCH.ANY measured slower even with power-law keys).
+template <int BITS, int KK>
 __global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(PassArgs a) {
   constexpr int R = 1 << BITS;
   extern __shared__ uint32_t smem_u32[];
@@ -80,18 +124,23 @@ __global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(PassArgs a) {
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * kRsTile + (int64_t)w * 32 * kRsRounds + lane_id();
   long long kmin = LLONG_MAX, kmax = LLONG_MIN;
-#pragma unroll 4
-  for (int r = 0; r < kRsRounds; ++r) {
-    int64_t i = base + (int64_t)r * 32;
-    if (i < a.n) {
-      int64_t raw = load_src_raw(a.key, i);
-      kmin = min(kmin, (long long)raw);
-      kmax = max(kmax, (long long)raw);
-      int32_t k = clamp_key(raw, a.key_limit);
-      atomicAdd(&wh[w * R + ((k >> a.shift) & (R - 1))], 1u);
-    }
+  int64_t raw[kRsRounds];
+#pragma unroll
+  for (int r = 0; r < kRsRounds; ++r) {  // all loads in flight first
+    const int64_t i = base + (int64_t)r * 32;
+    raw[r] = i < a.n ? load_src<KK>(a.key.p, i) : 0;
   }
-  if (a.minmax) block_minmax(kmin, kmax, a.minmax);
+#pragma unroll
+  for (int r = 0; r < kRsRounds; ++r) {
+    const int64_t i = base + (int64_t)r * 32;
+    const bool valid = i < a.n;
+    if (valid) {
+      kmin = min(kmin, (long long)raw[r]);
+      kmax = max(kmax, (long long)raw[r]);
+    }
+    if (valid) atomicAdd(&wh[w * R + ((clamp_key(raw[r], a.key_limit) >> a.shift) & (R - 1))], 1u);
+  }
+  if (a.minmax) cta_minmax<kRsWarps>(kmin, kmax, a.minmax);
   __syncthreads();
   for (int d = threadIdx.x; d < R; d += kRsThreads) {
     uint32_t s = 0;
@@ -101,83 +150,189 @@ __global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(PassArgs a) {
   }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(PassArgs a) {
+// Block-wide exclusive scan of v over the kScT threads (returns the prefix).
+constexpr int kScT = 512;  // scatter CTA: 16 warps x 8 rounds of 32 = one 4096-item tile
+constexpr int kScW = kScT / 32;
+constexpr int kScRounds = kRsTile / kScT;
+static_assert(kScRounds * kScT == kRsTile, "scatter and histogram tiles must match");
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *sw /*[kScW]*/) {
+  const unsigned lane = lane_id();
+  const int w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if ((int)lane >= o) x += y;
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  uint32_t wsum = 0;
+#pragma unroll
+  for (int ww = 0; ww < kScW; ++ww) wsum += ww < w ? sw[ww] : 0u;
+  __syncthreads();
+  return wsum + x - v;
+}
+
+// Stable scatter of one tile: items are ranked in original order (warp-major
+// rounds of 32 consecutive items, ballot-built digit peers, warp-private
+// running counts), placed at their tile-local digit-sorted position in shared
+// memory, and written out from there: consecutive threads then write
+// consecutive addresses of one digit run (coalesced), instead of one
+// scattered 4-byte store per item per array.  The
+// tile's global loads (keys, values, its scanned digit bases) are all issued
+// before the ranking, so a tile pays one memory latency (16 warps/CTA, 2
+// CTAs/SM resident for digits <= 9 bits).
+// Source kinds are compile-time (KK key, V0K value 0, V1K value 1 or -1).
+template <int BITS, int KK, int V0K, int V1K>
+__global__ void __launch_bounds__(kScT, BITS >= 10 ? 1 : 2) rs_scatter_kernel(PassArgs a) {
   constexpr int R = 1 << BITS;
+  constexpr int DPT = R >= kScT ? R / kScT : 1;  // digits per thread in the scans
   extern __shared__ uint32_t smem_u32[];
-  uint32_t *wc = smem_u32;  // [kRsWarps][R] running counts, then bases
+  uint32_t *wc = smem_u32;                 // [kScW][R] running counts, then warp bases
+  int64_t *gdelta = reinterpret_cast<int64_t *>(wc + kScW * R);  // [R] global - local
+  int32_t *skey = reinterpret_cast<int32_t *>(gdelta + R);        // [kRsTile]
+  int32_t *sv0 = skey + kRsTile;
+  int32_t *sv1 = sv0 + kRsTile;
+  __shared__ uint32_t sw[kScW];
   const int w = threadIdx.x >> 5;
   const unsigned lane = lane_id();
-  for (int i = threadIdx.x; i < kRsWarps * R; i += kRsThreads) wc[i] = 0;
-  __syncthreads();
+  for (int i = threadIdx.x; i < kScW * R; i += kScT) wc[i] = 0;
   const int64_t tile = blockIdx.x;
-  const int64_t base = tile * kRsTile + (int64_t)w * 32 * kRsRounds + lane;
+  const int64_t t0 = tile * kRsTile;
+  const int tn = (int)min((int64_t)kRsTile, a.n - t0);
+  const int64_t base = t0 + (int64_t)w * 32 * kScRounds + lane;
 
-  int32_t key[kRsRounds];
-  uint32_t rank[kRsRounds];
+  // every global load of the tile in flight at once: keys, values, and this
+  // tile's scanned digit bases (independent of the ranking)
+  int32_t key[kScRounds], v0[kScRounds], v1[kScRounds];
+  uint32_t rank[kScRounds];
+  long long vmin = LLONG_MAX, vmax = LLONG_MIN;
 #pragma unroll
-  for (int r = 0; r < kRsRounds; ++r) {
-    int64_t i = base + (int64_t)r * 32;
-    bool valid = i < a.n;
-    key[r] = valid ? clamp_key(load_src_raw(a.key, i), a.key_limit) : 0;
-    unsigned d = valid ? ((unsigned)(key[r] >> a.shift) & (R - 1)) : (unsigned)R;
-    unsigned peers = __match_any_sync(kFull, d);
-    unsigned lt = __popc(peers & lanemask_lt());
-    uint32_t cnt = valid ? wc[w * R + d] : 0u;
+  for (int r = 0; r < kScRounds; ++r) {
+    const int64_t i = base + (int64_t)r * 32;
+    const bool valid = i < a.n;
+    key[r] = valid ? clamp_key(load_src<KK>(a.key.p, i), a.key_limit) : 0;
+    const int64_t x0 = valid ? load_src<V0K>(a.val[0].p, i) : 0;
+    if (valid) {
+      vmin = min(vmin, (long long)x0);
+      vmax = max(vmax, (long long)x0);
+    }
+    v0[r] = static_cast<int32_t>(x0);
+    if constexpr (V1K >= 0) v1[r] = valid ? static_cast<int32_t>(load_src<V1K>(a.val[1].p, i)) : 0;
+  }
+  uint32_t gcnt[DPT];
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    gcnt[j] = d < R ? a.counts[(int64_t)d * a.ntiles + tile] : 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kScRounds; ++r) {
+    const bool valid = base + (int64_t)r * 32 < a.n;
+    const unsigned d = (unsigned)(key[r] >> a.shift) & (R - 1);
+#ifdef GNN_RS_MATCH
+    const unsigned peers = __match_any_sync(kFull, valid ? d : (unsigned)R);
+#else
+    const unsigned peers = digit_peers<BITS>(d, valid);
+#endif
+    const unsigned lt = __popc(peers & lanemask_lt());
+    const uint32_t cnt = valid ? wc[w * R + d] : 0u;
     rank[r] = cnt + lt;
     __syncwarp();
     if (valid && lt == 0) wc[w * R + d] = cnt + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < R; d += kRsThreads) {
-    uint32_t run = a.counts[(int64_t)d * a.ntiles + tile];
+  // tile totals per digit -> tile-local digit starts (block scan over digits)
+  uint32_t tot[DPT];
+  uint32_t my = 0;
 #pragma unroll
-    for (int ww = 0; ww < kRsWarps; ++ww) {
-      uint32_t c = wc[ww * R + d];
-      wc[ww * R + d] = run;
-      run += c;
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    uint32_t t = 0;
+    if (d < R) {
+#pragma unroll
+      for (int ww = 0; ww < kScW; ++ww) t += wc[ww * R + d];
+    }
+    tot[j] = t;
+    my += t;
+  }
+  uint32_t run = block_excl_scan(my, sw);
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    if (d < R) {
+      gdelta[d] = (int64_t)gcnt[j] - (int64_t)run;
+      uint32_t wr = run;  // warp-local starts within the digit's tile run
+#pragma unroll
+      for (int ww = 0; ww < kScW; ++ww) {
+        const uint32_t c = wc[ww * R + d];
+        wc[ww * R + d] = wr;
+        wr += c;
+      }
+    }
+    run += tot[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kScRounds; ++r) {
+    if (base + (int64_t)r * 32 < a.n) {
+      const unsigned d = (unsigned)(key[r] >> a.shift) & (R - 1);
+      const uint32_t lp = wc[w * R + d] + rank[r];
+      skey[lp] = key[r];
+      sv0[lp] = v0[r];
+      if constexpr (V1K >= 0) sv1[lp] = v1[r];
     }
   }
   __syncthreads();
-  long long vmin = LLONG_MAX, vmax = LLONG_MIN;
-#pragma unroll
-  for (int r = 0; r < kRsRounds; ++r) {
-    int64_t i = base + (int64_t)r * 32;
-    if (i < a.n) {
-      unsigned d = (unsigned)(key[r] >> a.shift) & (R - 1);
-      int64_t pos = (int64_t)wc[w * R + d] + rank[r];
-      a.key_out[pos] = key[r];
-      int64_t v0 = load_src_raw(a.val[0], i);
-      vmin = min(vmin, (long long)v0);
-      vmax = max(vmax, (long long)v0);
-      a.val_out[0][pos] = static_cast<int32_t>(v0);
-      if (a.nvals > 1) a.val_out[1][pos] = static_cast<int32_t>(load_src_raw(a.val[1], i));
-    }
+  for (int j = threadIdx.x; j < tn; j += kScT) {
+    const int32_t k = skey[j];
+    const int64_t pos = gdelta[(unsigned)(k >> a.shift) & (R - 1)] + j;
+    a.key_out[pos] = k;
+    a.val_out[0][pos] = sv0[j];
+    if constexpr (V1K >= 0) a.val_out[1][pos] = sv1[j];
   }
-  if (a.minmax) block_minmax(vmin, vmax, a.minmax + 2);
+  if (a.minmax) cta_minmax<kScW>(vmin, vmax, a.minmax + 2);
 }
 
-template <int BITS>
-int launch_pass(const PassArgs &a, cudaStream_t st, void *scan_ws, size_t scan_ws_bytes) {
+template <int BITS, int KK, int V0K, int V1K>
+int launch_pass_k(const PassArgs &a, cudaStream_t st, void *scan_ws, size_t scan_ws_bytes) {
   constexpr int R = 1 << BITS;
-  const size_t smem = sizeof(uint32_t) * kRsWarps * R;
+  const size_t smem_h = sizeof(uint32_t) * kRsWarps * R;
+  const size_t smem_s = sizeof(uint32_t) * kScW * R + sizeof(int64_t) * R + sizeof(int32_t) * 3 * kRsTile;
   static bool attr_set = false;  // idempotent; benign race
   if (!attr_set) {
-    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_hist_kernel<BITS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<BITS>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_hist_kernel<BITS, KK>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
+    GNN_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<BITS, KK, V0K, V1K>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
     attr_set = true;
   }
-  rs_hist_kernel<BITS><<<(unsigned)a.ntiles, kRsThreads, smem, st>>>(a);
+  rs_hist_kernel<BITS, KK><<<(unsigned)a.ntiles, kRsThreads, smem_h, st>>>(a);
   GNN_LAUNCH_CHECK();
   GNN_TRY(exclusive_scan_u32(a.counts, a.counts, (int64_t)R * a.ntiles, scan_ws, scan_ws_bytes, st));
-  PassArgs b = a;
-  b.minmax = a.minmax ? a.minmax : nullptr;
-  rs_scatter_kernel<BITS><<<(unsigned)a.ntiles, kRsThreads, smem, st>>>(b);
+  rs_scatter_kernel<BITS, KK, V0K, V1K><<<(unsigned)a.ntiles, kScT, smem_s, st>>>(a);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
+}
+
+// source-kind combinations the builders use: (i64 key, i64 val) csr_from_edges
+// pass 0; (i32, i32) later passes / sort_pairs; (i32, i32, iota) the CSC pass 0
+// (edge ids); (i32, i32, i32) its later passes
+template <int BITS>
+int launch_pass(const PassArgs &a, cudaStream_t st, void *scan_ws, size_t scan_ws_bytes) {
+  const int kk = a.key.kind, v0 = a.val[0].kind, v1 = a.nvals > 1 ? a.val[1].kind : -1;
+  if (kk == SRC_I64 && v0 == SRC_I64 && v1 < 0)
+    return launch_pass_k<BITS, SRC_I64, SRC_I64, -1>(a, st, scan_ws, scan_ws_bytes);
+  if (kk == SRC_I32 && v0 == SRC_I32 && v1 < 0)
+    return launch_pass_k<BITS, SRC_I32, SRC_I32, -1>(a, st, scan_ws, scan_ws_bytes);
+  if (kk == SRC_I32 && v0 == SRC_I32 && v1 == SRC_IOTA)
+    return launch_pass_k<BITS, SRC_I32, SRC_I32, SRC_IOTA>(a, st, scan_ws, scan_ws_bytes);
+  if (kk == SRC_I32 && v0 == SRC_I32 && v1 == SRC_I32)
+    return launch_pass_k<BITS, SRC_I32, SRC_I32, SRC_I32>(a, st, scan_ws, scan_ws_bytes);
+  return GNN_ERR_UNSUPPORTED;
 }
 
 int launch_pass_bits(int bits, const PassArgs &a, cudaStream_t st, void *sws, size_t sws_bytes) {
@@ -285,20 +440,29 @@ int stable_sort(const SortIO &io, long long *minmax, WsArena &ar, cudaStream_t s
 }
 
 // ------------------------------------------------ offsets from sorted keys
-__global__ void run_start_kernel(const int32_t *__restrict__ keys, int64_t n, int64_t *rstart) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) rstart[k] = i;
+// offsets[k] = first position whose key is >= k (= bincount -> cumsum of
+// graph.py:110-112 for sorted keys), streaming: position i with key boundary
+// (key[i-1], key[i]] writes offsets[key[i-1]+1 .. key[i]] = i, so empty keys
+// in the gap get the same start; the head (k <= key[0]) gets 0 and the tail
+// (k > key[n-1]) n.  A thread fills at most kGapRun entries of a gap; entries
+// of longer gaps stay at the -1 pre-fill and a second pass binary-searches
+// them (so one huge gap never serialises on one thread).
+constexpr int64_t kGapRun = 64;
+__global__ void offsets_from_keys_kernel(const int32_t *__restrict__ keys, int64_t n, int64_t V,
+                                         int64_t *offsets) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += stride) {
+    const int64_t lo = i == 0 ? -1 : (int64_t)keys[i - 1];  // previous key (-1: before the head)
+    const int64_t hi = i == n ? V : (int64_t)keys[i];       // this key (V: past the tail)
+    const int64_t top = min(hi, lo + kGapRun);
+    for (int64_t k = lo + 1; k <= top; ++k) offsets[k] = i;
   }
 }
-__global__ void run_end_kernel(const int32_t *__restrict__ keys, int64_t n,
-                               const int64_t *rstart, int64_t *deg) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t k = keys[i];
-    if (i == n - 1 || keys[i + 1] != k) deg[k] = i + 1 - rstart[k];
-  }
+__global__ void offsets_fill_gaps_kernel(const int32_t *__restrict__ keys, int64_t n, int64_t V,
+                                         int64_t *offsets) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= V; k += stride)
+    if (offsets[k] < 0) offsets[k] = lower_bound_dev(keys, (int64_t)0, n, (int32_t)min(k, (int64_t)INT32_MAX));
 }
 
 unsigned grid_for(int64_t n, int threads) {
@@ -307,26 +471,22 @@ unsigned grid_for(int64_t n, int threads) {
   return (unsigned)(b < cap ? b : cap);
 }
 
-void offsets_ws_count(WsCounter &c, int64_t V) {
-  c.take<int64_t>(V);
-  c.used += scan_i64_workspace(V) + 256;
-}
+void offsets_ws_count(WsCounter &c, int64_t V) { (void)c, (void)V; }
 
-// offsets[V+1] = [0, cumsum(run lengths of sorted keys per key value)]
+// offsets[V+1] of sorted keys in [0, V)
 int offsets_from_sorted(const int32_t *keys, int64_t n, int64_t V, int64_t *offsets, WsArena &ar,
                         cudaStream_t st) {
-  int64_t *rstart = ar.take<int64_t>(V);
-  size_t sws_bytes = scan_i64_workspace(V);
-  void *sws = ar.take<char>((int64_t)sws_bytes);
-  if (!ar.ok()) return GNN_ERR_WORKSPACE;
-  if (V > 0) GNN_CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * V, st));
-  if (n > 0) {
-    run_start_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys, n, rstart);
-    GNN_LAUNCH_CHECK();
-    run_end_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys, n, rstart, offsets);
-    GNN_LAUNCH_CHECK();
+  (void)ar;
+  if (n == 0) {
+    GNN_CUDA_TRY(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (V + 1), st));
+    return GNN_OK;
   }
-  return exclusive_scan_i64(offsets, offsets, V, true, sws, sws_bytes, st);
+  GNN_CUDA_TRY(cudaMemsetAsync(offsets, 0xff, sizeof(int64_t) * (V + 1), st));
+  offsets_from_keys_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, V, offsets);
+  GNN_LAUNCH_CHECK();
+  offsets_fill_gaps_kernel<<<grid_for(V + 1, 256), 256, 0, st>>>(keys, n, V, offsets);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
 }
 
 __global__ void init_minmax_kernel(long long *mm) {
@@ -390,6 +550,7 @@ int build_from_edges(int mode, int64_t V, int64_t E, const int64_t *src, const i
 // rows_of_edge[e] = r with offsets[r] <= e < offsets[r+1]; one tile of edges
 // per block, offsets of the tile's row span staged in shared memory.
 constexpr int kExpTile = 4096;
+constexpr int kExpRun = 16;  // consecutive edges per thread: one search, then a forward walk
 __global__ void __launch_bounds__(256) expand_rows_kernel(const int64_t *__restrict__ offsets,
                                                           int64_t num_rows, int64_t nnz,
                                                           int32_t *rows) {
@@ -408,13 +569,29 @@ __global__ void __launch_bounds__(256) expand_rows_kernel(const int64_t *__restr
   if (staged)
     for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) soff[i] = offsets[r0 + i];
   __syncthreads();
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    int64_t r;
-    if (staged)
-      r = r0 + upper_bound_dev(soff, 0, cnt, e) - 1;
-    else
-      r = upper_bound_dev(offsets, r0, r1 + 2, e) - 1;
-    rows[e] = (int32_t)r;
+  // thread t: edges e0 + t*kExpRun + [0, kExpRun), consecutive, row index walks forward
+  const int64_t s0 = e0 + (int64_t)threadIdx.x * kExpRun;
+  if (s0 >= e1) return;
+  int64_t r = staged ? upper_bound_dev(soff, 0, cnt, s0) - 1 : upper_bound_dev(offsets, r0, r1 + 2, s0) - 1 - r0;
+  int64_t rend = staged ? soff[r + 1] : offsets[r0 + r + 1];
+  int32_t out[kExpRun];
+#pragma unroll
+  for (int k = 0; k < kExpRun; ++k) {
+    const int64_t e = s0 + k;
+    while (e >= rend && e < e1) {  // empty rows are skipped by the same walk
+      ++r;
+      rend = staged ? soff[r + 1] : offsets[r0 + r + 1];
+    }
+    out[k] = (int32_t)(r0 + r);
+  }
+  if (s0 + kExpRun <= e1 && ((reinterpret_cast<uintptr_t>(rows + s0) & 15u) == 0)) {
+#pragma unroll
+    for (int k = 0; k < kExpRun; k += 4)
+      *reinterpret_cast<int4 *>(rows + s0 + k) = make_int4(out[k], out[k + 1], out[k + 2], out[k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kExpRun; ++k)
+      if (s0 + k < e1) rows[s0 + k] = out[k];
   }
 }
 

@@ -228,3 +228,41 @@ def test_csr1_streamed_ingest_chunks(gb, tmp_path):
     dst = torch.empty(raw.size, dtype=torch.int32, device="cuda")
     _stream_to_device(io.BytesIO(raw.tobytes()), dst, raw.nbytes, chunk=1000)
     assert np.array_equal(dst.cpu().numpy(), raw)
+
+
+@pytest.mark.parametrize("case", ["uniform", "gaps", "one_key", "skew"])
+def test_sort_pairs_and_offsets_match_numpy(gb, case):
+    """gnn_sort_pairs (stable LSD radix: ballot-ranked, shared-memory staged
+    scatter) and gnn_offsets_from_keys (run boundaries + binary-searched long
+    gaps) vs numpy's stable argsort and bincount -> cumsum (graph.py:110-114),
+    bit-exact, including empty keys at the head, in long interior gaps and at
+    the tail, and key ranges needing 1, 2 and 3 radix passes."""
+    import torch
+    from paper_2605_29346_b200.graph import _offsets_from_keys, _sort_pairs
+
+    rng = np.random.default_rng(7)
+    n = 300_001
+    if case == "uniform":
+        R = 3_000_000  # 22 bits: two 11-bit passes
+        k = rng.integers(0, R, n)
+    elif case == "gaps":
+        R = 1 << 27  # three 9-bit passes; keys in a few clusters, huge empty gaps
+        k = np.concatenate([rng.integers(1000, 1100, n // 3), rng.integers(5_000_000, 5_000_050, n // 3),
+                            rng.integers(R - 300, R - 200, n - 2 * (n // 3))])
+        rng.shuffle(k)
+    elif case == "one_key":
+        R = 100_000
+        k = np.full(n, 777)
+    else:
+        R = 232_965  # Reddit rows: 2 passes of 9 bits, power-law skew
+        k = np.minimum((rng.pareto(1.1, n) * 10).astype(np.int64), R - 1)
+    v = rng.integers(-2**31, 2**31 - 1, n)
+    kt = torch.from_numpy(k.astype(np.int32)).cuda()
+    vt = torch.from_numpy(v.astype(np.int32)).cuda()
+    ko, vo = _sort_pairs(kt, vt, R)
+    order = np.argsort(k, kind="stable")
+    assert eq(ko.cpu().numpy(), k[order])
+    assert eq(vo.cpu().numpy(), v.astype(np.int32)[order])
+    off = _offsets_from_keys(ko, R).cpu().numpy()
+    ref = np.concatenate([[0], np.cumsum(np.bincount(k, minlength=R))])
+    assert eq(off, ref)
