@@ -187,6 +187,10 @@ __global__ void colsum_final_kernel(int64_t nb, int64_t N, const float *__restri
 
 }  // namespace
 
+// fused tensor-core wide output layer (head_tc.cu)
+int gcn_head_tc(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, const float *W,
+                const float *b, const int64_t *labels, const int64_t *deg_offsets, float scale,
+                float *dP, int64_t lddp, float *partials, double *lpart, int64_t nb, cudaStream_t st);
 // tcgen05 tensor-core path (gemm_tc.cu)
 bool gemm_tc_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int trans_a);
 size_t gemm_tc_workspace(int64_t N, int64_t K);
@@ -1365,6 +1369,17 @@ int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64
   if (C > 64) {  // wide head: logits never materialised
     const int64_t nb = head_wide_grid(M);
     double *lpart = reinterpret_cast<double *>(partials + head_float_slots(nb, Din, C));
+    // tensor-core form (head_tc.cu) where it applies, else the SIMT kernels below
+    const int tc = gcn_head_tc(M, Din, C, P, ldp, W, b, labels, deg_offsets, scale, dP, lddp,
+                               partials, lpart, nb, st);
+    if (tc == GNN_OK) {
+      const int64_t outs = Din * C + C + 1;
+      gcn_head_reduce_warp_kernel<<<(unsigned)ceil_div(outs * 32, 256), 256, 0, st>>>(
+          nb, (int)Din, (int)C, partials, lpart, dW, db, loss, grad_scale);
+      GNN_LAUNCH_CHECK();
+      return GNN_OK;
+    }
+    if (tc != GNN_ERR_UNSUPPORTED) return tc;
     const int nch = (int)ceil_div(C, (int64_t)32);
 #define GNN_HEAD_WIDE(DN, NC)                                                                   \
   do {                                                                                          \

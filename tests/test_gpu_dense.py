@@ -116,11 +116,18 @@ def test_weight_gradient_gemm_tn_shapes(M, N, K):
                                      (1000, 16, 172), (90_001, 16, 172), (513, 32, 100),
                                      (5, 8, 65), (3000, 16, 256), (2049, 12, 97)])
 @pytest.mark.parametrize("with_deg", [False, True])
-def test_gcn_head_matches_float64(gb, M, Din, C, with_deg):
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_gcn_head_matches_float64(gb, M, Din, C, with_deg, tc, monkeypatch):
     """Fused output layer (gnn_gcn_head_scaled): loss, dP (with the 1/deg
     row scale), dW, db against a float64 torch statement of softmax-CE;
-    tolerance 1e-5 of the quantity's own absolute scale (Appendix A.8)."""
+    tolerance 1e-5 of the quantity's own absolute scale (Appendix A.8).
+    tc="1": C in (64, 176], Din <= 16 with 16-byte rows take the tcgen05 head
+    (head_tc.cu); "0" forces the SIMT wide kernel."""
     from paper_2605_29346_b200 import _lib
+
+    if tc == "0" and C <= 64:
+        pytest.skip("narrow head: one form")
+    monkeypatch.setenv("GNN_HEAD_TC", tc)
 
     lib = _lib.lib()
     rng = np.random.default_rng(M + Din + C)
