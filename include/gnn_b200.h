@@ -224,6 +224,10 @@ int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int64_t *n_dev,
  * out[i, :] = X[ids[i], :]. */
 int gnn_gather_rows(const float *X, int64_t ldx, const int64_t *ids, int64_t n, int64_t K,
                     float *out, int64_t ldo, gnn_stream_t stream);
+/* gnn_gather_rows over the first *n_dev of n_cap rows (device count; rows at
+ * or past it untouched): the feature gather of a replayed mini-batch. */
+int gnn_gather_rows_dev(const float *X, int64_t ldx, const int64_t *ids, const int64_t *n_dev,
+                        int64_t n_cap, int64_t K, float *out, int64_t ldo, gnn_stream_t stream);
 
 /* ----------------------------------------------------------- sparse ops */
 /* A device CSR (or CSC, which is the CSR of the transpose). */
@@ -309,6 +313,14 @@ typedef struct gnn_spmm_plan {
                                       short_max form a prefix (degree-sorted) — that
                                       prefix's edge count; gnn_spmm then needs the
                                       short-row kernel (K <= 64, 16-byte rows) */
+  const int64_t *dev_counts;       /* NULL, or (gnn_spmm_plan_build_dev) device
+                                      [num_split, num_empty, num_groups, num_short]
+                                      of this batch; the host fields above then hold
+                                      capacities and the kernels stop at the device
+                                      counts (a capturable, host-sync-free plan) */
+  const int64_t *row_limit;        /* NULL, or (device) rows >= *row_limit are not computed
+                                      (their outputs left untouched): the live rows of a
+                                      capacity-sized operand */
 } gnn_spmm_plan_t;
 
 size_t gnn_spmm_plan_buffer_ints(int64_t num_rows, int64_t nnz, int64_t edges_per_warp);
@@ -323,6 +335,18 @@ int gnn_spmm_plan_build(const gnn_csr_view_t *A, int64_t edges_per_warp, int32_t
 int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t edges_per_warp, int64_t short_max,
                            int32_t *plan_buf, gnn_spmm_plan_t *plan, void *ws, size_t ws_bytes,
                            gnn_stream_t stream);
+
+/* Host-sync-free plan for an operand whose row structure changes from call
+ * to call inside one fixed-size buffer (sampled mini-batch subgraphs replayed
+ * as one CUDA graph): same schedule as
+ * gnn_spmm_plan_build_ex (row-order operands only: A->row_ids must be NULL;
+ * short rows in row order), counts written to counts_dev[4] on device, host
+ * counts set to capacities; row_limit_dev (nullable) = the live row count.
+ * Only gnn_spmm accepts such a plan. */
+int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t edges_per_warp, int64_t short_max,
+                            int32_t *plan_buf, gnn_spmm_plan_t *plan, int64_t *counts_dev,
+                            const int64_t *row_limit_dev, void *ws, size_t ws_bytes,
+                            gnn_stream_t stream);
 
 /* Y[num_rows,K] = epilogue(A . X), X[num_cols,K].  heads>=1 splits K into
  * `heads` slices scaled by their own edge value (vals is [nnz,heads]).
@@ -503,6 +527,13 @@ size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a);
 int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
              const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
              int relu, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* gnn_gemm over the live rows *rows_dev of a capacity-sized operand (tiles of
+ * C rows past it skipped; for A^T B the contraction rows past it are zeroed):
+ * tensor-core paths only (GNN_ERR_UNSUPPORTED otherwise). */
+int gnn_gemm_rows_dev(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+                      const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc,
+                      const float *bias, int relu, const int64_t *rows_dev, void *ws,
+                      size_t ws_bytes, gnn_stream_t stream);
 
 /* out[N] = sum over rows of X[M,N] (deterministic two-level reduction). */
 size_t gnn_colsum_workspace(int64_t M, int64_t N);
@@ -517,6 +548,11 @@ size_t gnn_mask_norm_colsum_workspace(int64_t M, int64_t N);
 int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
                          int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
                          float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* gnn_mask_norm_colsum over the first *m_dev of M rows (device count). */
+int gnn_mask_norm_colsum_dev(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+                             int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
+                             float *colsum, const int64_t *m_dev, void *ws, size_t ws_bytes,
+                             gnn_stream_t stream);
 
 /* Mean softmax cross-entropy over M rows of C logits: *loss (device) and,
  * if dZ != NULL, dZ = (softmax(Z) - onehot(labels)) * grad_scale. */
@@ -547,6 +583,14 @@ int gnn_gcn_head_scaled(int64_t M, int64_t Din, int64_t C, const float *P, int64
 /* Remap global vertex ids to positions in a row-partitioned, padded exchange
  * buffer: owner p = max{q : bounds[q] <= id}; out = p * block_stride + (id - bounds[p]).
  * bounds[0..P] nondecreasing (SURVEY §8e 1D row partition). */
+/* Replayable subgraph assembly (device counts, no host sync):
+ * dst[*off_in + i] = src[i] for i < min(*count, cap) (off_in NULL: 0), then
+ * *off_out = *off_in + count; and dst[*from .. cap) = value.  elem_bytes 4 or 8. */
+int gnn_append_dev(void *dst, int64_t elem_bytes, const void *src, const int64_t *count,
+                   int64_t cap, const int64_t *off_in, int64_t *off_out, gnn_stream_t stream);
+int gnn_fill_tail_dev(void *dst, int64_t elem_bytes, const int64_t *from, int64_t cap,
+                      int64_t value, gnn_stream_t stream);
+
 int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bounds, int64_t P,
                   int64_t block_stride, int32_t *out, gnn_stream_t stream);
 

@@ -95,6 +95,8 @@ class SpmmPlan(C.Structure):
         ("num_short", c_i64),
         ("short_rows", c_ptr),
         ("main_nnz", c_i64),
+        ("dev_counts", c_ptr),
+        ("row_limit", c_ptr),
     ]
 
 
@@ -141,6 +143,8 @@ SIGNATURES = {
     ),
     "gnn_fill_uniform": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr]),
     "gnn_fill_labels": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_u64, c_ptr]),
+    "gnn_append_dev": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr]),
+    "gnn_fill_tail_dev": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_sort_pairs_workspace": (c_sz, [c_i64, c_i64]),
     "gnn_sort_pairs": (c_int, [c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_offsets_from_keys_workspace": (c_sz, [c_i64]),
@@ -172,6 +176,7 @@ SIGNATURES = {
     "gnn_table_lookup_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "gnn_table_fill_dev": (c_int, [c_ptr, c_ptr, c_ptr, c_i64, C.c_int32, c_ptr]),
     "gnn_gather_rows": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "gnn_gather_rows_dev": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "gnn_table_lookup": (c_int, [c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "gnn_table_assign": (c_int, [c_ptr, c_ptr, c_i64, c_i64, c_ptr]),
     "gnn_spmm_plan_buffer_ints": (c_sz, [c_i64, c_i64, c_i64]),
@@ -183,6 +188,11 @@ SIGNATURES = {
     "gnn_spmm_plan_build_ex": (
         c_int,
         [C.POINTER(CsrView), c_i64, c_i64, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_sz, c_ptr],
+    ),
+    "gnn_spmm_plan_build_dev": (
+        c_int,
+        [C.POINTER(CsrView), c_i64, c_i64, c_ptr, C.POINTER(SpmmPlan), c_ptr, c_ptr, c_ptr, c_sz,
+         c_ptr],
     ),
     "gnn_spmm_workspace": (c_sz, [C.POINTER(CsrView), C.POINTER(SpmmPlan), c_i64]),
     "gnn_spmm": (
@@ -274,6 +284,8 @@ SIGNATURES = {
     "gnn_head_mean": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "gnn_head_mean_bwd": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "gnn_gemm_workspace": (c_sz, [c_i64, c_i64, c_i64, c_int]),
+    "gnn_gemm_rows_dev": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_int, c_ptr, c_i64, c_int,
+                                  c_ptr, c_i64, c_ptr, c_int, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_gemm": (
         c_int,
         [c_i64, c_i64, c_i64, c_ptr, c_i64, c_int, c_ptr, c_i64, c_int, c_ptr, c_i64, c_ptr,
@@ -282,6 +294,8 @@ SIGNATURES = {
     "gnn_colsum_workspace": (c_sz, [c_i64, c_i64]),
     "gnn_colsum": (c_int, [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_mask_norm_colsum_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_mask_norm_colsum_dev": (c_int, [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
+                                         c_i64, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_mask_norm_colsum": (
         c_int,
         [c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_sz, c_ptr],

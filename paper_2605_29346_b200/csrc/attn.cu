@@ -774,7 +774,7 @@ int softmax_common(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t
                    const gnn_edge_scores_t *sc, void *ws, size_t ws_bytes, SoftmaxArgs &a) {
   if ((A && (A->col_bits || A->row_ids)) || !A || !plan || heads <= 0 || heads > 16 || !A->offsets || (A->nnz > 0 && !A->cols))
     return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+  if (plan->dev_counts || plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   if (ws_bytes < gnn_edge_softmax_workspace(plan, heads)) return GNN_ERR_WORKSPACE;
   a = SoftmaxArgs{};
@@ -1811,7 +1811,7 @@ int gat_rc_common(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, const f
     return GNN_ERR_INVALID_ARGUMENT;
   if (AT->nnz > 0 && (!AT->cols || !AT->eid || !dY || !ds || !al16(dY)))
     return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+  if (plan->dev_counts || plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   if (ws_bytes < gnn_gat_bwd_rc_workspace(plan, K)) return GNN_ERR_WORKSPACE;
   a = GatRcArgs{};
@@ -1870,7 +1870,7 @@ int gnn_sddmm(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64_t head
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->nnz > 0 && (!A->cols || !X || !Y || !out || ldx < K || ldy < K))
     return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
+  if (plan->dev_counts || plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(A->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   if (A->nnz == 0) return GNN_OK;
   cudaStream_t st = as_stream(stream);
@@ -2020,7 +2020,7 @@ int gnn_gat_bwd_csc(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, int64
   if (AT->nnz > 0 && (!AT->cols || !AT->eid || !alpha || !dY || !dalpha || !al16(dY)))
     return GNN_ERR_INVALID_ARGUMENT;
   if (heads == 4 && (!al16(alpha) || !al16(dalpha))) return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+  if (plan->dev_counts || plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   const int64_t q = K / 4;
   if (q > 128) return GNN_ERR_UNSUPPORTED;
@@ -2118,7 +2118,7 @@ int gnn_gat_bwd_csc_mean(const gnn_csr_view_t *AT, const gnn_spmm_plan_t *plan, 
   if (AT->nnz > 0 && (!AT->cols || !AT->eid || !alpha || !dZ || !dalpha || !al16(dZ)))
     return GNN_ERR_INVALID_ARGUMENT;
   if (heads == 4 && (!al16(alpha) || !al16(dalpha))) return GNN_ERR_INVALID_ARGUMENT;
-  if (plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
+  if (plan->dev_counts || plan->edges_per_warp <= 0 || plan->num_warps != ceil_div(AT->nnz, plan->edges_per_warp))
     return GNN_ERR_INVALID_ARGUMENT;
   if (ws_bytes < gnn_gat_bwd_csc_workspace(plan, K)) return GNN_ERR_WORKSPACE;
   cudaStream_t st = as_stream(stream);

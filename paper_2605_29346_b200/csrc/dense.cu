@@ -196,13 +196,14 @@ bool gemm_tc_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
 size_t gemm_tc_workspace(int64_t N, int64_t K);
 int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
             int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias, int relu, void *ws,
-            size_t ws_bytes, cudaStream_t st);
+            size_t ws_bytes, cudaStream_t st, const int64_t *rows_dev = nullptr);
 
 bool gemm_tc_tn_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                           const float *B, int64_t ldb);
 size_t gemm_tc_tn_workspace(int64_t M, int64_t N, int64_t K);
 int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
-               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
+               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
+               const int64_t *rows_dev = nullptr);
 
 // SIMT fallback (transposed A, unaligned strides, small M).
 int gemm_simt(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
@@ -284,30 +285,49 @@ size_t gnn_gemm_workspace(int64_t M, int64_t N, int64_t Kd, int trans_a) {
   return a > b ? a : b;
 }
 
-int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
-             const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
-             int relu, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+// rows_dev: live row count on device (the rows of C for the plain form, the
+// contraction rows for A^T B); tensor-core paths only.
+static int gemm_impl(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+                     const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc,
+                     const float *bias, int relu, void *ws, size_t ws_bytes, cudaStream_t st,
+                     const int64_t *rows_dev) {
   if (M < 0 || N < 0 || Kd < 0 || (M > 0 && N > 0 && (!C || ldc < N)) ||
       (M > 0 && Kd > 0 && (!A || (trans_a ? lda < M : lda < Kd))) ||
       (N > 0 && Kd > 0 && (!B || (trans_b ? ldb < Kd : ldb < N))))
     return GNN_ERR_INVALID_ARGUMENT;
   if (M == 0 || N == 0) return GNN_OK;
-  cudaStream_t st = as_stream(stream);
   if (gemm_tc_supported(M, N, Kd, A, lda, trans_a))
-    return gemm_tc(M, N, Kd, A, lda, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes, st);
+    return gemm_tc(M, N, Kd, A, lda, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes, st, rows_dev);
   if (N > 128 && gemm_tc_supported(M, 128, Kd, A, lda, trans_a)) {
     // wide outputs (e.g. GAT's heads x classes): 128-column slabs, A re-streamed per slab
     for (int64_t n0 = 0; n0 < N; n0 += 128) {
       const int64_t nb = N - n0 < 128 ? N - n0 : 128;
       GNN_TRY(gemm_tc(M, nb, Kd, A, lda, trans_b ? B + n0 * ldb : B + n0, ldb, trans_b, C + n0,
-                      ldc, bias ? bias + n0 : nullptr, relu, ws, ws_bytes, st));
+                      ldc, bias ? bias + n0 : nullptr, relu, ws, ws_bytes, st, rows_dev));
     }
     return GNN_OK;
   }
   if (trans_a && !trans_b && !bias && !relu && gemm_tc_tn_supported(M, N, Kd, A, lda, B, ldb))
-    return gemm_tc_tn(M, N, Kd, A, lda, B, ldb, C, ldc, ws, ws_bytes, st);
+    return gemm_tc_tn(M, N, Kd, A, lda, B, ldb, C, ldc, ws, ws_bytes, st, rows_dev);
+  if (rows_dev) return GNN_ERR_UNSUPPORTED;
   return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
                    st);
+}
+
+int gnn_gemm(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+             const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias,
+             int relu, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  return gemm_impl(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
+                   as_stream(stream), nullptr);
+}
+
+int gnn_gemm_rows_dev(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda, int trans_a,
+                      const float *B, int64_t ldb, int trans_b, float *C, int64_t ldc,
+                      const float *bias, int relu, const int64_t *rows_dev, void *ws,
+                      size_t ws_bytes, gnn_stream_t stream) {
+  if (!rows_dev) return GNN_ERR_INVALID_ARGUMENT;
+  return gemm_impl(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
+                   as_stream(stream), rows_dev);
 }
 
 }  // extern "C"
@@ -329,7 +349,8 @@ template <int NCOL>
 __global__ void __launch_bounds__(256) mask_norm_colsum_kernel(
     int64_t M, int64_t N, const float *__restrict__ X, int64_t ldx, const float *__restrict__ mask,
     int64_t ldm, const int64_t *__restrict__ deg_offsets, float *out, int64_t ldo,
-    float *partials, int64_t rpb) {
+    float *partials, int64_t rpb, const int64_t *m_dev = nullptr) {
+  if (m_dev) M = min(M, *m_dev);  // live rows (replayed mini-batch)
   constexpr int SLOTS = 256 / NCOL;
   __shared__ float red[SLOTS][NCOL];
   const int s = threadIdx.x / NCOL;
@@ -364,7 +385,8 @@ template <int C4P>
 __global__ void __launch_bounds__(256) mask_norm_colsum_vec_kernel(
     int64_t M, int64_t N, const float *__restrict__ X, int64_t ldx, const float *__restrict__ mask,
     int64_t ldm, const int64_t *__restrict__ deg_offsets, float *out, int64_t ldo,
-    float *partials, int64_t rpb) {
+    float *partials, int64_t rpb, const int64_t *m_dev = nullptr) {
+  if (m_dev) M = min(M, *m_dev);  // live rows (replayed mini-batch)
   constexpr int SLOTS = 256 / C4P;
   __shared__ float4 red[SLOTS][C4P];
   const int s = threadIdx.x / C4P, q = threadIdx.x % C4P;
@@ -573,9 +595,10 @@ size_t gnn_mask_norm_colsum_workspace(int64_t M, int64_t N) {
   return sizeof(float) * (size_t)(ceil_div(M > 0 ? M : 1, reduce_rows_per_block(M)) * (N > 0 ? N : 1)) + 256;
 }
 
-int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+static int mask_norm_colsum_impl(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
                          int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
-                         float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+                         float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream,
+                                 const int64_t *m_dev) {
   if (M < 0 || N <= 0 || ldx < N || (mask && ldm < N) || (out && ldo < N) || (M > 0 && !X))
     return GNN_ERR_INVALID_ARGUMENT;
   if (colsum && ws_bytes < gnn_mask_norm_colsum_workspace(M, N)) return GNN_ERR_WORKSPACE;
@@ -594,22 +617,22 @@ int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, cons
   if (vec) {
     if (N <= 16)
       mask_norm_colsum_vec_kernel<4><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                                   deg_offsets, out, ldo, partials, rpb);
+                                                                   deg_offsets, out, ldo, partials, rpb, m_dev);
     else if (N <= 32)
       mask_norm_colsum_vec_kernel<8><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                                   deg_offsets, out, ldo, partials, rpb);
+                                                                   deg_offsets, out, ldo, partials, rpb, m_dev);
     else
       mask_norm_colsum_vec_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                                    deg_offsets, out, ldo, partials, rpb);
+                                                                    deg_offsets, out, ldo, partials, rpb, m_dev);
   } else if (N <= 16)
     mask_norm_colsum_kernel<16><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                             deg_offsets, out, ldo, partials, rpb);
+                                                             deg_offsets, out, ldo, partials, rpb, m_dev);
   else if (N <= 64)
     mask_norm_colsum_kernel<64><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                             deg_offsets, out, ldo, partials, rpb);
+                                                             deg_offsets, out, ldo, partials, rpb, m_dev);
   else
     mask_norm_colsum_kernel<256><<<(unsigned)nb, 256, 0, st>>>(M, N, X, ldx, mask, ldm,
-                                                              deg_offsets, out, ldo, partials, rpb);
+                                                              deg_offsets, out, ldo, partials, rpb, m_dev);
   GNN_LAUNCH_CHECK();
   if (colsum) {
     sum_partials_kernel<<<(unsigned)ceil_div(N * 32, (int64_t)256), 256, 0, st>>>(nb, N, partials,
@@ -617,6 +640,22 @@ int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, cons
     GNN_LAUNCH_CHECK();
   }
   return GNN_OK;
+}
+
+int gnn_mask_norm_colsum(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+                         int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
+                         float *colsum, void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  return mask_norm_colsum_impl(M, N, X, ldx, mask, ldm, deg_offsets, out, ldo, colsum, ws, ws_bytes,
+                               stream, nullptr);
+}
+
+int gnn_mask_norm_colsum_dev(int64_t M, int64_t N, const float *X, int64_t ldx, const float *mask,
+                             int64_t ldm, const int64_t *deg_offsets, float *out, int64_t ldo,
+                             float *colsum, const int64_t *m_dev, void *ws, size_t ws_bytes,
+                             gnn_stream_t stream) {
+  if (!m_dev) return GNN_ERR_INVALID_ARGUMENT;
+  return mask_norm_colsum_impl(M, N, X, ldx, mask, ldm, deg_offsets, out, ldo, colsum, ws, ws_bytes,
+                               stream, m_dev);
 }
 
 size_t gnn_softmax_xent_workspace(int64_t M) {

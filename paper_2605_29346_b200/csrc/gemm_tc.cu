@@ -48,6 +48,7 @@ struct TcArgs {
   const float *bias;
   int relu;
   int vec_store;  // C rows 16-byte aligned: 128-bit epilogue stores
+  const int64_t *rows_dev;  // live rows on device (tiles past them skipped), or null
 };
 
 template <int NPAD>
@@ -77,6 +78,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
   const int warp = threadIdx.x >> 5;
   const int lane = (int)lane_id();
   constexpr uint32_t kTxBytes = (uint32_t)(kA + 2 * kB);
+  // every role walks the same tile sequence: live tiles only when rows_dev is set
+  const int64_t mtiles = p.rows_dev ? min(p.mtiles, ceil_div(*p.rows_dev, (int64_t)kTcM)) : p.mtiles;
   constexpr int kAcc = 2 * NPAD;  // accumulator width: [hi half | lo half]
   constexpr int kTmemCols = (2 * kAcc) <= 32 ? 32 : (2 * kAcc) <= 64 ? 64 : (2 * kAcc) <= 128 ? 128 : (2 * kAcc) <= 256 ? 256 : 512;
 
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+      for (int64_t t = blockIdx.x; t < mtiles; t += gridDim.x) {
         const int m0 = (int)(t * kTcM);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(empty + s, ph ^ 1);
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       uint32_t ph = 0;
       int ab = 0;
       uint32_t aph = 0;
-      for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+      for (int64_t t = blockIdx.x; t < mtiles; t += gridDim.x) {
         mbar_wait(acc_empty + ab, aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(ab * kAcc);
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
     const int tid = threadIdx.x - 128;
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+    for (int64_t t = blockIdx.x; t < mtiles; t += gridDim.x) {
       for (int kb = 0; kb < p.nkb; ++kb) {
         mbar_wait(full + s, ph);
         float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
     const int q = warp & 3;
     int ab = 0;
     uint32_t aph = 0;
-    for (int64_t t = blockIdx.x; t < p.mtiles; t += gridDim.x) {
+    for (int64_t t = blockIdx.x; t < mtiles; t += gridDim.x) {
       mbar_wait(acc_full + ab, aph);
       tc_fence_after();
       const int64_t row = t * kTcM + q * 32 + lane;
@@ -291,6 +294,7 @@ struct TnArgs {
   int splits;
   int64_t mtiles, ntiles;
   float *partials;    // [splits][M][N]
+  const int64_t *rows_dev;  // live contraction rows on device, or null
 };
 
 template <int NB>
@@ -316,6 +320,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
   constexpr int kAcc = 2 * NB;                 // [hi | lo] accumulator columns
   constexpr int kTmemCols = 2 * kAcc < 32 ? 32 : 2 * kAcc;  // two accumulators
   const int64_t units = p.mtiles * p.ntiles * p.splits;
+  // live contraction rows: k-blocks past them are skipped, and the rows of the
+  // last live block past them are zeroed (a capacity buffer's tail is stale)
+  const int64_t klive = p.rows_dev ? min(p.K, *p.rows_dev) : p.K;
+  const int nkb_live = (int)ceil_div(klive, (int64_t)kTcBK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -349,8 +357,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
     sp = u / (p.mtiles * p.ntiles);
     m0 = (int)(mt * kTcM);
     n0 = (int)(nt * NB);
-    kb0 = (int)(sp * p.kb_per_split);
-    kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
+    // the splits share the live k-blocks evenly (all of them without rows_dev)
+    const int kbps = p.rows_dev ? (nkb_live + p.splits - 1) / p.splits : p.kb_per_split;
+    kb1 = min(min(p.nkb_total, (int)sp * kbps + kbps), nkb_live);
+    kb0 = min((int)sp * kbps, kb1);
   };
 
   if (warp == 0) {
@@ -437,9 +447,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_tn_kernel(
         mbar_wait(full + s, ph);
         float4 *a4 = reinterpret_cast<float4 *>(sa + (size_t)s * kTcM * kTcBK);
         float4 *l4 = reinterpret_cast<float4 *>(salo + (size_t)s * kTcM * kTcBK);
+        // rows of this block past the live count (kTcBK rows of 128 B per atom)
+        const int live_rows = (int)min((int64_t)kTcBK, klive - (int64_t)kb * kTcBK);
 #pragma unroll 4
         for (int i = tid; i < kTcM * kTcBK / 4; i += 128) {
-          const float4 x = a4[i];
+          float4 x = a4[i];
+          if (((i & 255) >> 3) >= live_rows) {  // row (i % 256) / 8 of atom i / 256
+            x = make_float4(0.f, 0.f, 0.f, 0.f);
+            a4[i] = x;
+          }
           float4 h;
           h.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
           h.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
@@ -625,7 +641,7 @@ size_t gemm_tc_workspace(int64_t N, int64_t K) {
 
 int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
             int64_t ldb, int trans_b, float *C, int64_t ldc, const float *bias, int relu, void *ws,
-            size_t ws_bytes, cudaStream_t st) {
+            size_t ws_bytes, cudaStream_t st, const int64_t *rows_dev) {
   const int npad = tc_npad(N);
   const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
   if (ws_bytes < gemm_tc_workspace(N, K)) return GNN_ERR_WORKSPACE;
@@ -650,6 +666,7 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
   p.bias = bias;
   p.relu = relu;
   p.vec_store = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0);
+  p.rows_dev = rows_dev;
   switch (npad) {
     case 16: return launch_tc<16>(ta, tbh, tbl, p, st);
     case 32: return launch_tc<32>(ta, tbh, tbl, p, st);
@@ -719,7 +736,8 @@ static int launch_tn(const CUtensorMap &ta, const CUtensorMap &tb, const TnArgs 
 }
 
 int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
-               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st) {
+               int64_t ldb, float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
+               const int64_t *rows_dev) {
   TnArgs p{};
   int kbps, splits, nkb;
   int64_t mtiles, ntiles;
@@ -734,6 +752,7 @@ int gemm_tc_tn(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, con
   p.mtiles = mtiles;
   p.ntiles = ntiles;
   p.partials = static_cast<float *>(ws);
+  p.rows_dev = rows_dev;
   CUtensorMap ta, tb;
   // A [K rows, M cols] and B [K rows, N cols]: boxes of 32 cols x 32 rows (OOB zero-filled)
   // MN-major tf32 operands: the only legal smem layout is SWIZZLE_128B_BASE32B

@@ -771,6 +771,9 @@ __global__ void guide_kernel(const double *__restrict__ cdf, int64_t n, int32_t 
 }
 
 constexpr int kGenChunk = 64;
+// sampling draws: shorter chunks (a mini-batch hop is ~1e4-1e6 draws, each a
+// chain of dependent gathers): more threads in flight per jump-ahead
+constexpr int kDrawChunk = 8;
 __global__ void __launch_bounds__(256) powerlaw_kernel(const double *__restrict__ cdf, int64_t n,
                                                        int64_t m, const int32_t *__restrict__ guide,
                                                        U128 state0, U128 inc, int64_t *src,
@@ -1194,6 +1197,27 @@ int gnn_generate_powerlaw(int64_t n, int64_t m, const double *cdf, uint64_t stat
 
 }  // extern "C"
 
+// --------------------------------- device-count concatenation (replayable)
+// dst[off_in .. off_in + count) = src[0 .. count), *off_out = off_in + count,
+// with count and off_in on device (*off_in = 0 when off_in is null): the
+// sampled-subgraph assembly of a replayed mini-batch.
+template <typename T>
+__global__ void append_dev_kernel(T *dst, const T *__restrict__ src, const int64_t *count,
+                                  int64_t cap, const int64_t *off_in, int64_t *off_out) {
+  const int64_t n = min(*count, cap);
+  const int64_t o = off_in ? *off_in : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[o + i] = src[i];
+  if (off_out && blockIdx.x == 0 && threadIdx.x == 0) *off_out = o + n;
+}
+template <typename T>
+__global__ void fill_tail_dev_kernel(T *dst, const int64_t *from, int64_t cap, T value) {
+  for (int64_t i = *from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = value;
+}
+
 // ------------------------------------------------ row-partition id remap
 namespace gnn {
 namespace {
@@ -1217,7 +1241,39 @@ __global__ void remap_ids_kernel(int64_t n, const int32_t *__restrict__ ids,
 }  // namespace
 }  // namespace gnn
 
-extern "C" int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bounds, int64_t P,
+extern "C" int gnn_append_dev(void *dst, int64_t elem_bytes, const void *src, const int64_t *count,
+                   int64_t cap, const int64_t *off_in, int64_t *off_out, gnn_stream_t stream) {
+  if (!dst || !src || !count || cap < 0 || (elem_bytes != 4 && elem_bytes != 8))
+    return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = grid_for(cap > 0 ? cap : 1, 256);
+  if (elem_bytes == 4)
+    append_dev_kernel<int32_t><<<grid, 256, 0, st>>>(static_cast<int32_t *>(dst),
+                                                     static_cast<const int32_t *>(src), count, cap,
+                                                     off_in, off_out);
+  else
+    append_dev_kernel<int64_t><<<grid, 256, 0, st>>>(static_cast<int64_t *>(dst),
+                                                     static_cast<const int64_t *>(src), count, cap,
+                                                     off_in, off_out);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_fill_tail_dev(void *dst, int64_t elem_bytes, const int64_t *from, int64_t cap,
+                      int64_t value, gnn_stream_t stream) {
+  if (!dst || !from || cap < 0 || (elem_bytes != 4 && elem_bytes != 8)) return GNN_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = grid_for(cap > 0 ? cap : 1, 256);
+  if (elem_bytes == 4)
+    fill_tail_dev_kernel<int32_t><<<grid, 256, 0, st>>>(static_cast<int32_t *>(dst), from, cap,
+                                                        (int32_t)value);
+  else
+    fill_tail_dev_kernel<int64_t><<<grid, 256, 0, st>>>(static_cast<int64_t *>(dst), from, cap, value);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+int gnn_remap_ids(int64_t n, const int32_t *ids, const int64_t *bounds, int64_t P,
                              int64_t block_stride, int32_t *out, gnn_stream_t stream) {
   using namespace gnn;
   if (n < 0 || P <= 0 || block_stride <= 0 || (n > 0 && (!ids || !bounds || !out)))
@@ -1264,10 +1320,10 @@ __global__ void __launch_bounds__(256) sample_draw_kernel(
     const int64_t *__restrict__ count, int64_t cap, int64_t fanout, U128 state0, U128 inc,
     int64_t *src, int64_t *dst) {
   const int64_t n = *count;
-  const int64_t nchunks = ceil_div(n, kGenChunk);
+  const int64_t nchunks = ceil_div(n, kDrawChunk);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p0 = c * kGenChunk, p1 = min(p0 + kGenChunk, n);
+    const int64_t p0 = c * kDrawChunk, p1 = min(p0 + kDrawChunk, n);
     U128 s = pcg_advance(state0, inc, (uint64_t)p0);
     for (int64_t p = p0; p < p1; ++p) {
       s = u128_add(u128_mul(s, kPcgMult), inc);
@@ -1373,7 +1429,7 @@ int gnn_sample_hop(int64_t V, const int64_t *offsets, const int32_t *targets,
   sample_active_scatter_kernel<<<grid_for(F), 256, 0, st>>>(pos, F, fanout, active, count);
   GNN_LAUNCH_CHECK();
   const U128 s0{state_hi, state_lo}, inc{inc_hi, inc_lo};
-  sample_draw_kernel<<<grid_for(ceil_div(F * fanout, kGenChunk)), 256, 0, st>>>(
+  sample_draw_kernel<<<grid_for(ceil_div(F * fanout, kDrawChunk)), 256, 0, st>>>(
       offsets, targets, frontier, active, count, F * fanout, fanout, s0, inc, src, dst);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
@@ -1532,10 +1588,10 @@ __global__ void sample_draw_dev_kernel(const int64_t *__restrict__ offsets,
                                        const uint64_t *__restrict__ rng, int64_t *src, int64_t *dst) {
   const U128 state0{rng[0], rng[1]}, inc{rng[2], rng[3]};
   const int64_t n = *count;
-  const int64_t nchunks = ceil_div(n, kGenChunk);
+  const int64_t nchunks = ceil_div(n, kDrawChunk);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p0 = c * kGenChunk, p1 = min(p0 + kGenChunk, n);
+    const int64_t p0 = c * kDrawChunk, p1 = min(p0 + kDrawChunk, n);
     U128 s = pcg_advance(state0, inc, (uint64_t)p0);
     for (int64_t p = p0; p < p1; ++p) {
       s = u128_add(u128_mul(s, kPcgMult), inc);
@@ -1582,7 +1638,7 @@ int gnn_sample_hop_dev(int64_t V, const int64_t *offsets, const int32_t *targets
   GNN_TRY(exclusive_scan_i64(pos, pos, F_cap, true, sws, sb, st));
   sample_active_scatter_kernel<<<grid_for(F_cap), 256, 0, st>>>(pos, F_cap, fanout, active, count);
   GNN_LAUNCH_CHECK();
-  sample_draw_dev_kernel<<<grid_for(ceil_div(F_cap * fanout, kGenChunk)), 256, 0, st>>>(
+  sample_draw_dev_kernel<<<grid_for(ceil_div(F_cap * fanout, kDrawChunk)), 256, 0, st>>>(
       offsets, targets, frontier, active, count, fanout, rng_state, src, dst);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
@@ -1668,9 +1724,12 @@ extern "C" int gnn_table_fill_dev(int32_t *table, const int64_t *ids, const int6
 // kernel class, execmodel.py:306-314): out[i, :] = X[ids[i], :].
 namespace gnn {
 namespace {
+// n_dev (optional): the live row count on device; rows at or past it are not
+// written (replayed mini-batches over a capacity-sized buffer)
 __global__ void gather_rows_vec_kernel(const float4 *__restrict__ X, int64_t ldx4,
                                        const int64_t *__restrict__ ids, int64_t n, int64_t K4,
-                                       float4 *out, int64_t ldo4) {
+                                       float4 *out, int64_t ldo4, const int64_t *n_dev) {
+  if (n_dev) n = min(n, *n_dev);
   const int64_t total = n * K4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1678,9 +1737,21 @@ __global__ void gather_rows_vec_kernel(const float4 *__restrict__ X, int64_t ldx
     out[i * ldo4 + k] = __ldg(X + ids[i] * ldx4 + k);
   }
 }
+__global__ void gather_rows_v2_kernel(const float2 *__restrict__ X, int64_t ldx2,
+                                      const int64_t *__restrict__ ids, int64_t n, int64_t K2,
+                                      float2 *out, int64_t ldo2, const int64_t *n_dev) {
+  if (n_dev) n = min(n, *n_dev);
+  const int64_t total = n * K2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / K2, k = t % K2;
+    out[i * ldo2 + k] = __ldg(X + ids[i] * ldx2 + k);
+  }
+}
 __global__ void gather_rows_kernel(const float *__restrict__ X, int64_t ldx,
                                    const int64_t *__restrict__ ids, int64_t n, int64_t K,
-                                   float *out, int64_t ldo) {
+                                   float *out, int64_t ldo, const int64_t *n_dev) {
+  if (n_dev) n = min(n, *n_dev);
   const int64_t total = n * K;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1691,23 +1762,43 @@ __global__ void gather_rows_kernel(const float *__restrict__ X, int64_t ldx,
 }  // namespace
 }  // namespace gnn
 
-extern "C" int gnn_gather_rows(const float *X, int64_t ldx, const int64_t *ids, int64_t n,
-                               int64_t K, float *out, int64_t ldo, gnn_stream_t stream) {
-  using namespace gnn;
+namespace gnn {
+namespace {
+int gather_rows_impl(const float *X, int64_t ldx, const int64_t *ids, int64_t n, int64_t K,
+                     float *out, int64_t ldo, const int64_t *n_dev, cudaStream_t st) {
   if (n < 0 || K < 0 || ldx < K || ldo < K || (n > 0 && K > 0 && (!X || !ids || !out)))
     return GNN_ERR_INVALID_ARGUMENT;
   if (n == 0 || K == 0) return GNN_OK;
-  cudaStream_t st = as_stream(stream);
   const bool v4 = K % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(X) & 15u) == 0 &&
                   (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
   if (v4) {
     gather_rows_vec_kernel<<<grid_for(n * K / 4), 256, 0, st>>>(
         reinterpret_cast<const float4 *>(X), ldx / 4, ids, n, K / 4,
-        reinterpret_cast<float4 *>(out), ldo / 4);
+        reinterpret_cast<float4 *>(out), ldo / 4, n_dev);
+  } else if (K % 2 == 0 && ldx % 2 == 0 && ldo % 2 == 0 &&
+             (reinterpret_cast<uintptr_t>(X) & 7u) == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0) {
+    // 8-byte vectors (e.g. Reddit's 602 features: rows of 2408 B)
+    gather_rows_v2_kernel<<<grid_for(n * K / 2), 256, 0, st>>>(
+        reinterpret_cast<const float2 *>(X), ldx / 2, ids, n, K / 2,
+        reinterpret_cast<float2 *>(out), ldo / 2, n_dev);
   } else {
-    gather_rows_kernel<<<grid_for(n * K), 256, 0, st>>>(X, ldx, ids, n, K, out, ldo);
+    gather_rows_kernel<<<grid_for(n * K), 256, 0, st>>>(X, ldx, ids, n, K, out, ldo, n_dev);
   }
   GNN_LAUNCH_CHECK();
   return GNN_OK;
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" int gnn_gather_rows(const float *X, int64_t ldx, const int64_t *ids, int64_t n,
+                               int64_t K, float *out, int64_t ldo, gnn_stream_t stream) {
+  return gnn::gather_rows_impl(X, ldx, ids, n, K, out, ldo, nullptr, gnn::as_stream(stream));
+}
+
+extern "C" int gnn_gather_rows_dev(const float *X, int64_t ldx, const int64_t *ids,
+                                   const int64_t *n_dev, int64_t n_cap, int64_t K, float *out,
+                                   int64_t ldo, gnn_stream_t stream) {
+  if (!n_dev) return GNN_ERR_INVALID_ARGUMENT;
+  return gnn::gather_rows_impl(X, ldx, ids, n_cap, K, out, ldo, n_dev, gnn::as_stream(stream));
 }

@@ -30,6 +30,8 @@ constexpr int kMaxParts = 8;  // one NVLink / NVSwitch box
 
 struct SpmmArgs {
   int64_t R, nnz;
+  const int64_t *dev_counts;  // device-count plan: [split, empty, groups, short] (else null)
+  const int64_t *row_limit;   // rows >= *row_limit not computed (else null)
   const int64_t *offsets;
   const int32_t *cols;
   const float *vals;
@@ -513,10 +515,15 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
       }
     }
   };
+  // a warp whose first row is past the live rows has nothing to do (checked
+  // before any bulk copy is in flight)
+  const int64_t r_first = a.chunk_row[w];
+  const int64_t rlim = a.row_limit ? min(a.R, *a.row_limit) : a.R;
+  if (r_first >= rlim) return;
   issue(0);
 
   // row bounds: 32 row ends per batched load
-  int64_t r = a.chunk_row[w];
+  int64_t r = r_first;
   int64_t rs = a.offsets[r];
   int64_t obuf = a.offsets[min(r + 1 + lane, a.R)];
   int bi = 0;
@@ -527,12 +534,17 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
   for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
   bool done = false;
 
+  int last_issued = 0, last_waited = -1;
   for (int sc = 0; sc < nsub && !done; ++sc) {
     const int b = sc & 1;
     const int64_t s0 = e0 + (int64_t)sc * kSub;
     const int64_t s1 = min(s0 + kSub, e1);
-    if (sc + 1 < nsub) issue(sc + 1);
+    if (sc + 1 < nsub) {
+      issue(sc + 1);
+      last_issued = sc + 1;
+    }
     mbar_wait(bar + b, (uint32_t)((sc >> 1) & 1));
+    last_waited = sc;
     __syncwarp();
     const int32_t *bc = scol + b * kSub;
     const int32_t *bv = sval + b * kSub;
@@ -557,18 +569,42 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
       }
       ++r;
       rs = re;
-      if (rs >= e1 || r >= a.R) {
+      if (rs >= e1 || r >= rlim) {
         done = true;
         break;
       }
       if (++bi == 32) {
         obuf = a.offsets[min(r + 1 + lane, a.R)];
         bi = 0;
+        // a whole window of empty rows (their epilogue is the plan's empty-row
+        // pass): jump to the next non-empty row by binary search instead of
+        // walking them one by one (a replayed mini-batch's capacity buffers
+        // hold ~1e5 trailing empty rows)
+        if (__all_sync(kFull, obuf == rs) && r + 32 < a.R) {
+          int64_t lo = r + 32, hi = a.R;  // first row q >= lo with offsets[q + 1] > rs
+          while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (a.offsets[mid + 1] > rs)
+              hi = mid;
+            else
+              lo = mid + 1;
+          }
+          r = lo;
+          if (r >= rlim) {
+            done = true;
+            break;
+          }
+          obuf = a.offsets[min(r + 1 + lane, a.R)];
+        }
       }
       re = shfl_i64(obuf, bi);
     }
     __syncwarp();  // buffer b fully consumed before issue(sc + 2) refills it
   }
+  // the loop can stop early (live-row limit): a prefetched sub-chunk's bulk copy
+  // must land before the warp (and perhaps its CTA) exits
+  if (last_issued > last_waited)
+    mbar_wait(bar + (last_issued & 1), (uint32_t)((last_issued >> 1) & 1));
   if (!done && re > e1 && re - rs > a.short_max) {  // the range ends inside row r
     group_reduce<G, VPL, VW>(acc);
     if (rs < e0) {         // whole range inside one row: a carry-in piece
@@ -839,8 +875,10 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
   const int gbase = lane & ~(G - 1);
   const int64_t cbase = (int64_t)blockIdx.y * KB;
   const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * NG + g;
-  const bool valid = i < nrows;
+  if (a.dev_counts) nrows = min(nrows, a.dev_counts[3]);
+  bool valid = i < nrows;
   const int64_t r = valid ? rows[i] : 0;
+  if (a.row_limit && r >= *a.row_limit) valid = false;
   const int64_t rs = valid ? a.offsets[r] : 0;
   const int n = valid ? (int)(a.offsets[r + 1] - rs) : 0;  // deg <= short_max
   int nmax = n;
@@ -917,10 +955,12 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
 
 __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                        int64_t nrows) {
+  if (a.dev_counts) nrows = min(nrows, a.dev_counts[1]);
   const int64_t total = nrows * a.K;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / a.K, c = t % a.K;
+    if (a.row_limit && rows[i] >= *a.row_limit) continue;
     int64_t r = out_row(a, rows[i]);
     float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
     a.Y[r * a.ldy + c] = epi_scalar(0.f, r, c, a, 0.f, ps);
@@ -1239,6 +1279,84 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   plan->main_nnz = main_nnz;
   plan->num_short = h[3];
   plan->short_rows = buf + L.o_short;
+  plan->dev_counts = nullptr;
+  plan->row_limit = nullptr;
+  return GNN_OK;
+}
+
+__global__ void plan_counts_kernel(const int64_t *fs, const int64_t *fe, const int64_t *fg,
+                                   const int64_t *fh, int64_t R, int64_t *counts) {
+  counts[0] = fs[R];
+  counts[1] = fe[R];
+  counts[2] = fg[R];
+  counts[3] = fh[R];
+}
+
+int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t P, int64_t short_max, int32_t *buf,
+                            gnn_spmm_plan_t *plan, int64_t *counts, const int64_t *row_limit,
+                            void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (!A || !plan || !buf || !counts || P <= 0 || P % 4 != 0 || A->num_rows < 0 || !A->offsets ||
+      short_max < 0 || A->row_ids)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (A->num_rows >= ((int64_t)1 << 31) || ceil_div(A->nnz, P) >= ((int64_t)1 << 30))
+    return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_spmm_plan_workspace(A->num_rows)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  const int64_t R = A->num_rows;
+  WsArena ar(ws, ws_bytes);
+  int64_t *fs = ar.take<int64_t>(R + 1);
+  int64_t *fe = ar.take<int64_t>(R + 1);
+  int64_t *fg = ar.take<int64_t>(R + 1);
+  int64_t *fh = ar.take<int64_t>(R + 1);
+  size_t sb = scan_i64_workspace(R);
+  void *s1 = ar.take<char>((int64_t)sb);
+  void *s2 = ar.take<char>((int64_t)sb);
+  void *s3 = ar.take<char>((int64_t)sb);
+  void *s4 = ar.take<char>((int64_t)sb);
+  if (!ar.ok()) return GNN_ERR_WORKSPACE;
+  const int64_t nnz = A->nnz;
+  const PlanLayout L = plan_layout(R, nnz, P);
+  plan_chunk_rows_kernel<<<grid_1d(L.nw + 1, 256), 256, 0, st>>>(A->offsets, R, nnz, P, L.nw,
+                                                                 buf + L.o_chunk);
+  GNN_LAUNCH_CHECK();
+  if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
+  if (R > 0) {
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, nnz, fs, fe,
+                                                       fg, fh);
+    GNN_LAUNCH_CHECK();
+  }
+  GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
+  GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
+  GNN_TRY(exclusive_scan_i64(fg, fg, R, true, s3, sb, st));
+  GNN_TRY(exclusive_scan_i64(fh, fh, R, true, s4, sb, st));
+  if (R > 0) {
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg,
+                                                         buf + L.o_split, buf + L.o_sgb,
+                                                         buf + L.o_csplit, buf + L.o_empty, fh,
+                                                         buf + L.o_short);
+    GNN_LAUNCH_CHECK();
+  }
+  plan_counts_kernel<<<1, 1, 0, st>>>(fs, fe, fg, fh, R, counts);
+  GNN_LAUNCH_CHECK();
+  // capacities: a split row spans >= 2 chunks (<= nw of them); sum over split rows
+  // of ceil(partials / 64) <= num_split + (nw + num_split) / 64
+  const int64_t cap_split = L.nw < R ? L.nw : R;
+  plan->edges_per_warp = P;
+  plan->num_warps = L.nw;
+  plan->chunk_row = buf + L.o_chunk;
+  plan->chunk_split = buf + L.o_csplit;
+  plan->num_split = cap_split;
+  plan->split_rows = buf + L.o_split;
+  plan->split_group_base = buf + L.o_sgb;
+  plan->num_groups = cap_split + (L.nw + cap_split) / 64 + 1;
+  plan->num_empty = R;
+  plan->empty_rows = buf + L.o_empty;
+  plan->short_max = short_max;
+  plan->main_nnz = nnz;
+  plan->num_short = short_max > 0 ? R : 0;
+  plan->short_rows = buf + L.o_short;
+  plan->dev_counts = counts;
+  plan->row_limit = row_limit;
   return GNN_OK;
 }
 
@@ -1300,6 +1418,8 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
   SpmmArgs a{};
   a.R = A->num_rows;
   a.nnz = plan->main_nnz;  // the nnz-split kernel's edge range
+  a.dev_counts = plan->dev_counts;
+  a.row_limit = plan->row_limit;
   a.row_ids = A->row_ids;
   a.offsets = A->offsets;
   a.cols = A->cols;

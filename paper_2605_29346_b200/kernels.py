@@ -20,15 +20,18 @@ from .graph import SparseOperand, spmm_operand
 class SpmmCall:
     def __init__(self, op: SparseOperand, X: torch.Tensor, Y: torch.Tensor, *, flags=0, heads=1,
                  vals=None, eid=None, bias=None, self_x=None, self_scale=1.0, mask=None,
-                 post_deg_offsets=None, edges_per_warp=None):
+                 post_deg_offsets=None, edges_per_warp=None, plan=None):
+        """``plan``: a prebuilt (e.g. device-count, DevicePlan.plan) schedule for
+        ``op`` itself — the operand is then used as given (no degree-sorted form)."""
         self.lib = _lib.lib()
         self.dev = X.device
         self.K = int(X.shape[1])
         assert Y.shape[1] == self.K and X.stride(1) == 1 and Y.stride(1) == 1
-        op = spmm_operand(op, X, Y, heads=heads, vals=vals, eid=eid, self_x=self_x, mask=mask,
-                          bias=bias)
+        if plan is None:
+            op = spmm_operand(op, X, Y, heads=heads, vals=vals, eid=eid, self_x=self_x, mask=mask,
+                              bias=bias)
         self.view = op.view(vals=vals, eid=eid)
-        self.plan = op.spmm_plan(edges_per_warp)
+        self.plan = plan if plan is not None else op.spmm_plan(edges_per_warp)
         self.epi = _lib.Epilogue()
         self.epi.flags = flags
         self.epi.self_scale = float(self_scale)
@@ -52,6 +55,42 @@ class SpmmCall:
                                      self.Y.stride(0), self.K, C.byref(self.epi),
                                      self.ws.data_ptr(), self.ws.numel(),
                                      _lib.stream_handle(self.dev)), "spmm")
+
+
+class DevicePlan:
+    """Host-sync-free SpMM schedule of an operand whose rows change in place
+    (gnn_spmm_plan_build_dev): fixed buffers, counts on device; ``__call__``
+    rebuilds it for the operand's current offsets (capturable)."""
+
+    def __init__(self, op: SparseOperand, short_max: int, edges_per_warp: int | None = None,
+                 row_limit: torch.Tensor | None = None):
+        """``row_limit``: device int64 scalar, the live rows (rows past it are
+        not computed by the SpMMs run on this plan)."""
+        from .graph import _default_edges_per_warp
+
+        self.lib = _lib.lib()
+        self.dev = op.device
+        if edges_per_warp is None:
+            with torch.cuda.device(self.dev):
+                edges_per_warp = _default_edges_per_warp(op.nnz, self.lib.gnn_device_sm_count())
+        R = op.num_rows
+        nint = self.lib.gnn_spmm_plan_buffer_ints(R, op.nnz, edges_per_warp)
+        self.buf = torch.zeros(max(int(nint), 1), dtype=torch.int32, device=self.dev)
+        self.counts = torch.zeros(4, dtype=torch.int64, device=self.dev)
+        self.ws = _lib.workspace(self.lib.gnn_spmm_plan_workspace(R), self.dev)
+        self.view = op.view()
+        self.P, self.short_max, self.op = int(edges_per_warp), int(short_max), op
+        self.row_limit = row_limit
+        self.plan = _lib.SpmmPlan()
+        self()  # fills the plan's capacities and pointers (fixed from now on)
+
+    def __call__(self):
+        _lib.check(self.lib.gnn_spmm_plan_build_dev(
+            C.byref(self.view), self.P, self.short_max, self.buf.data_ptr(), C.byref(self.plan),
+            self.counts.data_ptr(),
+            self.row_limit.data_ptr() if self.row_limit is not None else None,
+            self.ws.data_ptr(), self.ws.numel(),
+            _lib.stream_handle(self.dev)), "spmm plan (device counts)")
 
 
 class SharedHeadsCall:
@@ -97,9 +136,11 @@ class ParallelCall:
 
 
 class GemmCall:
-    """C = op(A) op(B) (+bias)(relu)."""
+    """C = op(A) op(B) (+bias)(relu).  ``rows_dev``: device int64 scalar of live
+    rows (C rows, or the contraction rows of A^T B) of capacity-sized operands."""
 
-    def __init__(self, A, B, Cout, *, trans_a=False, trans_b=False, bias=None, relu=False):
+    def __init__(self, A, B, Cout, *, trans_a=False, trans_b=False, bias=None, relu=False,
+                 rows_dev=None):
         self.lib = _lib.lib()
         self.dev = A.device
         self.M = A.shape[1] if trans_a else A.shape[0]
@@ -110,8 +151,17 @@ class GemmCall:
         self.ta, self.tb, self.relu = int(trans_a), int(trans_b), int(relu)
         self.ws = _lib.workspace(self.lib.gnn_gemm_workspace(self.M, self.N, self.Kd, self.ta),
                                  self.dev)
+        self.rows_dev = rows_dev
 
     def __call__(self):
+        if self.rows_dev is not None:
+            _lib.check(self.lib.gnn_gemm_rows_dev(
+                self.M, self.N, self.Kd, self.A.data_ptr(), self.A.stride(0), self.ta,
+                self.B.data_ptr(), self.B.stride(0), self.tb, self.C.data_ptr(), self.C.stride(0),
+                self.bias.data_ptr() if self.bias is not None else None, self.relu,
+                self.rows_dev.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                _lib.stream_handle(self.dev)), "gemm (device rows)")
+            return
         _lib.check(self.lib.gnn_gemm(self.M, self.N, self.Kd, self.A.data_ptr(),
                                      self.A.stride(0), self.ta, self.B.data_ptr(),
                                      self.B.stride(0), self.tb, self.C.data_ptr(),
@@ -122,23 +172,30 @@ class GemmCall:
 
 
 class MaskNormColsumCall:
-    def __init__(self, X, out, *, mask=None, deg_offsets=None, colsum=None):
+    def __init__(self, X, out, *, mask=None, deg_offsets=None, colsum=None, rows_dev=None):
         self.lib = _lib.lib()
         self.dev = X.device
         self.M, self.N = X.shape
         self.X, self.out, self.mask, self.deg, self.colsum = X, out, mask, deg_offsets, colsum
+        self.rows_dev = rows_dev  # device int64 scalar: live rows of a capacity buffer
         self.ws = _lib.workspace(self.lib.gnn_mask_norm_colsum_workspace(self.M, self.N), self.dev)
 
     def __call__(self):
+        args = [self.M, self.N, self.X.data_ptr(), self.X.stride(0),
+                self.mask.data_ptr() if self.mask is not None else None,
+                self.mask.stride(0) if self.mask is not None else 0,
+                self.deg.data_ptr() if self.deg is not None else None,
+                self.out.data_ptr() if self.out is not None else None,
+                self.out.stride(0) if self.out is not None else 0,
+                self.colsum.data_ptr() if self.colsum is not None else None]
+        if self.rows_dev is not None:
+            _lib.check(self.lib.gnn_mask_norm_colsum_dev(
+                *args, self.rows_dev.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                _lib.stream_handle(self.dev)), "mask_norm_colsum (device rows)")
+            return
         _lib.check(self.lib.gnn_mask_norm_colsum(
-            self.M, self.N, self.X.data_ptr(), self.X.stride(0),
-            self.mask.data_ptr() if self.mask is not None else None,
-            self.mask.stride(0) if self.mask is not None else 0,
-            self.deg.data_ptr() if self.deg is not None else None,
-            self.out.data_ptr() if self.out is not None else None,
-            self.out.stride(0) if self.out is not None else 0,
-            self.colsum.data_ptr() if self.colsum is not None else None,
-            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)), "mask_norm_colsum")
+            *args, self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+            "mask_norm_colsum")
 
 
 class XentCall:

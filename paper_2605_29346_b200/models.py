@@ -407,8 +407,9 @@ class SampledGCNTrainer:
     and the epoch math of ``GCNTrainer`` runs on A_s with the mean
     cross-entropy over the B seeds only (loss rows = the seed batch,
     sampler.py:299-305); Adam updates the shared weights.  Everything runs on
-    libgnnb200 kernels; per-step calls are rebuilt because the subgraph size
-    changes with every batch."""
+    libgnnb200 kernels.  ``step`` rebuilds its calls per batch (the subgraph
+    size changes); ``capture`` + ``run`` make one mini-batch one CUDA-graph
+    replay over envelope-sized buffers (no host sync)."""
 
     def __init__(self, g: CsrGraph, X: torch.Tensor, labels: torch.Tensor, in_feats: int,
                  hidden: int, classes: int, config, *, lr=0.01, seed: int = 0):
@@ -472,6 +473,164 @@ class SampledGCNTrainer:
         self.forward_backward(A, l2g, B)
         self.k_adam()
         return self.loss
+
+    # ------------------------------------------------------------ replayed form
+    def capture(self, adam: bool = True):
+        """Make every later ``run`` ONE CUDA-graph replay (SURVEY §8f item 4;
+        execmodel.py:430-454 ReplayGraph): device sampling
+        (DeviceSampler), the local subgraph — the hop edges concatenated at
+        device offsets (already in source order: hop frontiers are consecutive
+        local ids, draws frontier-major), CSR offsets from the run boundaries,
+        the CSC by a stable radix sort — host-sync-free SpMM schedules
+        (gnn_spmm_plan_build_dev), the feature gather, the epoch kernels and
+        Adam.  Every buffer is sized for the config's envelope (local vertices
+        <= B + sum_h n_cap_h, edges <= sum_h n_cap_h); past the live counts the
+        edge lists are padded with a dummy vertex N_cap whose row holds the
+        padding edges and never reaches a seed; every kernel stops at the live
+        vertex count n (device scalar: SpMM row limit, GEMM live rows, mask /
+        norm rows, feature gather), so rows past it cost nothing and stay
+        stale, and the math on the live rows is the eager step's (same edge
+        order per row)."""
+        from .graph import SPMM_SHORT_ROWORDER, SparseOperand
+        from .kernels import DevicePlan
+        from .sampling import DeviceSampler
+
+        lib, dev = _lib.lib(), self.dev
+        S = DeviceSampler(self.g, self.cfg)
+        self.sampler = S
+        B, nh = self.cfg.batch_size, len(S.hops)
+        E_cap = sum(h["n_cap"] for h in S.hops)
+        N_cap = B + E_cap
+        R = N_cap + 1  # + the dummy vertex
+        i32 = dict(dtype=torch.int32, device=dev)
+        i64 = dict(dtype=torch.int64, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self._caps = (B, E_cap, N_cap)
+        self._es = torch.full((E_cap,), N_cap, **i32)
+        self._ed = torch.full((E_cap,), N_cap, **i32)
+        self._l2g = torch.zeros(N_cap, **i64)
+        self._cur = torch.zeros(2 * nh + nh + 1, **i64)  # one device cursor per append
+        self._n_dev = self._cur[3 * nh]  # live local vertices (the last l2g append's cursor)
+        self._csr_off = torch.zeros(R + 1, **i64)
+        self._csc_keys, self._csc_cols = torch.empty(E_cap, **i32), torch.empty(E_cap, **i32)
+        self._csc_off = torch.zeros(R + 1, **i64)
+        self._ws_sort = _lib.workspace(lib.gnn_sort_pairs_workspace(E_cap, R), dev)
+        self._ws_off = _lib.workspace(lib.gnn_offsets_from_keys_workspace(R), dev)
+        Fpad = -(-self.F // 32) * 32  # 128-byte rows (TMA)
+        self._Xs_store = torch.zeros(R, Fpad, **f32)
+        Xs = self._Xs_store[:, :self.F]
+        self._ys = torch.zeros(B, **i64)
+        e = lambda: torch.zeros(R, self.Hd, **f32)  # noqa: E731
+        H1, Y1, P2, dZ1, dH1, dP2 = e(), e(), e(), e(), e(), e()  # dP2 rows >= B stay 0
+        A = SparseOperand(R, R, self._csr_off, self._ed, deg_offsets=self._csr_off)
+        AT = SparseOperand(R, R, self._csc_off, self._csc_cols)
+        # rows past the live vertex count are never computed (their values stay
+        # stale and no live row reads them): SpMMs, GEMMs and the mask/norm pass
+        # all stop at n_dev
+        nd = self._n_dev
+        # 64-edge warp ranges: the live part (~half the envelope) still spreads
+        # over thousands of warps (the CSC's hub rows are long, the rest short)
+        self._pA = DevicePlan(A, SPMM_SHORT_ROWORDER, edges_per_warp=64, row_limit=nd)
+        self._pAT = DevicePlan(AT, SPMM_SHORT_ROWORDER, edges_per_warp=64, row_limit=nd)
+        N_, B_, R_, M_ = _lib.EPI_NORM, _lib.EPI_BIAS, _lib.EPI_RELU, _lib.EPI_MASK
+        self._rcalls = [
+            GemmCall(Xs, self.W1, H1, rows_dev=nd),
+            SpmmCall(A, H1, Y1, flags=N_ | B_ | R_, bias=self.b1, plan=self._pA.plan),
+            SpmmCall(A, Y1, P2, flags=N_, plan=self._pA.plan),
+            HeadCall(P2[:B], self.W2, self.b2, self._ys, dP2[:B], self.dW2, self.db2, self.loss,
+                     deg_offsets=self._csr_off[:B + 1]),
+            SpmmCall(AT, dP2, dZ1, flags=M_, mask=Y1, plan=self._pAT.plan),
+            MaskNormColsumCall(dZ1, dZ1, deg_offsets=self._csr_off, colsum=self.db1, rows_dev=nd),
+            SpmmCall(AT, dZ1, dH1, plan=self._pAT.plan),
+            GemmCall(Xs, dH1, self.dW1, trans_a=True, rows_dev=nd)]
+        self._Xs, self._replay_adam = Xs, adam
+        self._rkeep = (A, AT, H1, Y1, P2, dZ1, dH1, dP2)
+        # warm (plans, workspaces), then capture
+        S._stage(np.arange(B), 0)
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            self._replay_body()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self._replay_body()
+        torch.cuda.synchronize(dev)
+        return self._graph
+
+    def _replay_body(self):
+        lib, S, dev = _lib.lib(), self.sampler, self.dev
+        st = _lib.stream_handle(dev)
+        B, E_cap, N_cap = self._caps
+        R, nh, cur = N_cap + 1, len(S.hops), self._cur
+        S._launch()
+        # hop edges at device offsets: hop h after hop h-1's live count; padding -> N_cap
+        for k, (dst, key) in enumerate(((self._es, "src_local"), (self._ed, "dst_local"))):
+            off_in = None
+            for h, hop in enumerate(S.hops):
+                off_out = cur[k * nh + h]
+                _lib.check(lib.gnn_append_dev(dst.data_ptr(), 4, hop[key].data_ptr(),
+                                              hop["count"].data_ptr(), hop["n_cap"],
+                                              None if off_in is None else off_in.data_ptr(),
+                                              off_out.data_ptr(), st), "append_dev")
+                off_in = off_out
+            _lib.check(lib.gnn_fill_tail_dev(dst.data_ptr(), 4, off_in.data_ptr(), E_cap, N_cap,
+                                             st), "fill_tail_dev")
+        # local -> global: seeds, then each hop's new vertices (first-occurrence order)
+        segs = [(S.seeds, S.B_dev, B)] + [(h["new_globals"], h["new_count"], h["n_cap"])
+                                          for h in S.hops]
+        off_in = None
+        for i, (src, cnt, cap) in enumerate(segs):
+            off_out = cur[2 * nh + i]
+            _lib.check(lib.gnn_append_dev(self._l2g.data_ptr(), 8, src.data_ptr(), cnt.data_ptr(),
+                                          cap, None if off_in is None else off_in.data_ptr(),
+                                          off_out.data_ptr(), st), "append_dev")
+            off_in = off_out
+        assert off_in.data_ptr() == self._n_dev.data_ptr()  # live local vertex count
+        _lib.check(lib.gnn_offsets_from_keys(E_cap, R, self._es.data_ptr(), self._csr_off.data_ptr(),
+                                             self._ws_off.data_ptr(), self._ws_off.numel(), st),
+                   "offsets_from_keys")
+        _lib.check(lib.gnn_sort_pairs(E_cap, R, self._ed.data_ptr(), self._es.data_ptr(),
+                                      self._csc_keys.data_ptr(), self._csc_cols.data_ptr(),
+                                      self._ws_sort.data_ptr(), self._ws_sort.numel(), st),
+                   "sort_pairs")
+        _lib.check(lib.gnn_offsets_from_keys(E_cap, R, self._csc_keys.data_ptr(),
+                                             self._csc_off.data_ptr(), self._ws_off.data_ptr(),
+                                             self._ws_off.numel(), st), "offsets_from_keys")
+        self._pA()
+        self._pAT()
+        _lib.check(lib.gnn_gather_rows_dev(self.X.data_ptr(), self.X.stride(0),
+                                           self._l2g.data_ptr(), self._n_dev.data_ptr(), N_cap,
+                                           self.F, self._Xs.data_ptr(), self._Xs.stride(0), st),
+                   "gather_rows_dev")
+        torch.index_select(self.labels, 0, S.seeds, out=self._ys)
+        for c in self._rcalls:
+            c()
+        if self._replay_adam:
+            self.k_adam()
+
+    def run(self, seeds, rng=None):
+        """One mini-batch as one graph replay (``capture`` first): seeds and the
+        per-hop PCG64 states staged in pinned memory, then replayed; no host
+        sync.  Returns the device loss tensor."""
+        S = self.sampler
+        S._stage(seeds, rng)
+        self._graph.replay()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        S._inflight = ev
+        return self.loss
+
+    def replay_subgraph(self):
+        """(offsets, targets, local->global ids, B) of the last replayed batch's
+        live subgraph, read back (synchronises) — the eager ``subgraph``'s CSR."""
+        torch.cuda.synchronize(self.dev)
+        B, E_cap, N_cap = self._caps
+        n = int(self._n_dev.item())
+        off = self._csr_off[:n + 1].cpu().numpy()
+        E = int(off[-1])
+        return off, self._ed[:E].cpu().numpy(), self._l2g[:n].cpu().numpy(), B
 
     def params(self):
         return {"W1": self.W1, "b1": self.b1, "W2": self.W2, "b2": self.b2}

@@ -63,7 +63,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.CsrView) == 80  # 8 x 8 + col_bits + reserved + row_ids
     # uint32 + float + 6 pointer/int64 fields
     assert ctypes.sizeof(_lib.Epilogue) == 8 + 6 * 8
-    assert ctypes.sizeof(_lib.SpmmPlan) == 14 * 8
+    assert ctypes.sizeof(_lib.SpmmPlan) == 16 * 8  # + dev_counts, row_limit
     assert ctypes.sizeof(_lib.EdgeScores) == 4 * 8
 
 

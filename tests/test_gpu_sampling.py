@@ -181,6 +181,70 @@ def test_sampled_gcn_step_matches_oracle(cuda):
         assert ok, (k, worst)
 
 
+def test_sampled_gcn_replay_matches_eager_and_oracle(cuda):
+    """the replayed mini-batch step (capture + run: one CUDA
+    graph per batch, envelope-sized buffers, device counts) builds exactly the
+    eager step's local subgraph (CSR offsets / targets / local->global ids) and
+    its loss and gradients equal the float64 oracle on that subgraph; replaying
+    the same batch twice is bit-identical."""
+    import paper_2605_29346_b200 as gb
+    from oracle import graph as og
+    from oracle import ops as oo
+    from paper_2605_29346_b200.models import SampledGCNTrainer
+    from paper_2605_29346_b200.sampling import SampleConfig
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 6000, 150_000, exponent=2.1), 12)
+    rng = np.random.default_rng(5)
+    F, Hd, C, B = 50, 16, 7, 128
+    X = torch.from_numpy(rng.uniform(-1, 1, (6000, F)).astype(np.float32)).cuda()
+    y = torch.from_numpy(rng.integers(0, C, 6000)).cuda()
+    cfg = SampleConfig(batch_size=B, fanouts=(6, 4))
+    tr = SampledGCNTrainer(g, X, y, F, Hd, C, cfg, seed=0)
+    ref_tr = SampledGCNTrainer(g, X, y, F, Hd, C, cfg, seed=0)
+    tr.capture(adam=False)
+    Xh, yh = X.cpu().numpy(), y.cpu().numpy()
+    for it in range(3):
+        seeds = rng.choice(6000, B, replace=False)
+        tr.run(seeds, rng=100 + it)
+        off, tgt, ids, B_ = tr.replay_subgraph()
+        A, l2g, _ = ref_tr.subgraph(seeds, rng=100 + it)
+        assert np.array_equal(off, A.offsets) and np.array_equal(tgt, A.targets)
+        assert np.array_equal(ids, l2g.cpu().numpy())
+        n = off.size - 1
+        t_off, t_rows, _ = og.transpose(n, n, off, tgt)
+        p = {k: v.double().cpu().numpy() for k, v in tr.params().items()}
+        ref = oo.gcn2_step(off, tgt, t_off, t_rows, Xh[ids], p["W1"], p["b1"], p["W2"], p["b2"],
+                           yh[ids], loss_rows=B)
+        assert abs(tr.loss.item() - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+        got = {k: v.clone() for k, v in tr.grads().items()}
+        for k, gv in got.items():
+            ok, worst = oo.close(gv.cpu().numpy(), ref[k], ref["abs"][k])
+            assert ok, (it, k, worst)
+        loss0 = tr.loss.item()
+        tr.run(seeds, rng=100 + it)  # same batch again: bit-identical
+        torch.cuda.synchronize()
+        assert tr.loss.item() == loss0
+        for k, gv in tr.grads().items():
+            assert torch.equal(gv, got[k]), k
+
+
+def test_sampled_gcn_replay_trains(cuda):
+    import paper_2605_29346_b200 as gb
+    from paper_2605_29346_b200.models import SampledGCNTrainer
+    from paper_2605_29346_b200.sampling import SampleConfig
+
+    g = gb.generate(gb.GraphGenSpec("power-law", 3000, 60_000, exponent=2.1), 5)
+    rng = np.random.default_rng(1)
+    yy = np.where(rng.random(3000) < 0.85, 0, rng.integers(0, 4, 3000))
+    y = torch.from_numpy(yy).cuda()
+    X = torch.randn(3000, 16, device="cuda")
+    tr = SampledGCNTrainer(g, X, y, 16, 16, 4, SampleConfig(batch_size=128, fanouts=(5, 5)),
+                           lr=0.05, seed=0)
+    tr.capture()
+    losses = [tr.run(rng.choice(3000, 128, replace=False), rng=it).item() for it in range(40)]
+    assert np.mean(losses[-5:]) < np.mean(losses[:5]) - 0.1, losses
+
+
 def test_sampled_gcn_training_lowers_the_loss(cuda):
     import paper_2605_29346_b200 as gb
     from paper_2605_29346_b200.models import SampledGCNTrainer
