@@ -173,6 +173,15 @@ constexpr int stage_of() {
 
 // Lane-invariant part of the gather: per-vector base pointers (column offset
 // folded in; columns past K are clamped to column 0 and simply not stored).
+// Column of a lane's slot v: slots interleave across the G lanes of a group
+// (coalesced scalar / vector accesses), except the <G, 4, 4> shape — used only
+// by the four-heads-over-one-row form (WM_SHARED4) — whose 4 slots are
+// contiguous per lane, so its 4 X columns arrive in ONE 16-byte gather.
+template <int G, int VPL, int VW>
+__device__ __forceinline__ int slot_col(int v, int gl) {
+  return (VPL == 4 && VW == 4) ? (gl * VPL + v) * VW : (v * G + gl) * VW;
+}
+
 template <int G, int VPL, int VW, bool PEER = false>
 struct LaneCols {
   const char *xb[VPL];  // PEER: byte offset of the lane's column (no base)
@@ -181,7 +190,7 @@ struct LaneCols {
     const int gl = (int)lane_id() % G;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      int64_t col = cbase + (int64_t)(v * G + gl) * VW;
+      int64_t col = cbase + (int64_t)slot_col<G, VPL, VW>(v, gl);
       if (col >= a.K) col = 0;
       const int64_t xc = a.xdiv > 1 ? col / a.xdiv : col;
       xb[v] = PEER ? reinterpret_cast<const char *>(xc * 4)
@@ -249,6 +258,38 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
 #define GNN_SH4_U 4
 #endif
     constexpr int US = GNN_SH4_U;  // edges in flight per group (scalar gathers: cheap registers)
+    if constexpr (VPL == 4 && VW == 4) {
+      // contiguous slots: one float4 gather of the lane's 4 X columns per edge,
+      // 16 FMAs (4 columns x 4 heads) against the edge's float4 of head weights
+      for (; i < ie; i += NG * US) {
+        int32_t c[US];
+        bool ok[US];
+#pragma unroll
+        for (int u = 0; u < US; ++u) {
+          ok[u] = i + u * NG < ie;
+          c[u] = ok[u] ? scol[i + u * NG] : 0;
+        }
+        float4 xv[US], w4[US];
+#pragma unroll
+        for (int u = 0; u < US; ++u) {
+          xv[u] = ok[u] ? ldg_f4(reinterpret_cast<const float *>(lc.xb[0] + (uint64_t)(uint32_t)c[u] * ldxb))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          w4[u] = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < US; ++u) {
+          const float xs4[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            acc[v].x = fmaf(w4[u].x, xs4[v], acc[v].x);
+            acc[v].y = fmaf(w4[u].y, xs4[v], acc[v].y);
+            acc[v].z = fmaf(w4[u].z, xs4[v], acc[v].z);
+            acc[v].w = fmaf(w4[u].w, xs4[v], acc[v].w);
+          }
+        }
+      }
+      return;
+    }
     for (; i < ie; i += NG * US) {
       int32_t c[US];
       bool ok[US];
@@ -358,7 +399,7 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, float *dst, int64_t
   }
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    int64_t col = cbase + (int64_t)(v * G + gl) * VW;
+    int64_t col = cbase + (int64_t)slot_col<G, VPL, VW>(v, gl);
     if (col < a.K) {
       typename V::T y = acc[v];
       if (final_row) {
@@ -1568,6 +1609,8 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
         s = launch_main<16, 1, 4>(a, wm, st);
       else if (K <= 128)
         s = launch_main<32, 1, 4>(a, wm, st);
+      else if (shared)
+        s = launch_main<16, 4, 4>(a, wm, st);  // 4 heads x 64 columns: float4 gathers
       else
         s = launch_main<32, 2, 4>(a, wm, st);  // 256 columns per block-column
     } else {
