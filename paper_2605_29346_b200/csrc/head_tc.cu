@@ -15,7 +15,8 @@
 // x.y ~ x_raw.y_hi + x_raw.y_lo + x_lo.y_hi):
 //   M1  Z[128 x 176]          = P . W^T            (A smem SW64, B smem SW64)   TMEM [0,176)
 //   M2  dP[128 x 16]          = dz . W             (A = dz in TMEM, B smem)     TMEM [352,368)
-//       dW^T[classes 0-127]   = dz^T . [P|1]_(hi|lo) (A smem SW128, B smem)     TMEM [368,416)
+//       dW^T[classes 0-127]   = dz^T . [P|1]_(hi|lo) (A smem MN-major SW128_32B: dz rows as
+//                                                    written, full 128-byte lines per MMA)  TMEM [368,416)
 //   M3  dW^T[classes 128-255] = dz^T . [P|1]_(hi|lo)                            TMEM [416,464)
 // (dW: B = [P_hi|1 ; P_lo|0] stacked along N, so each K step is two MMAs,
 // A = dz^T raw then dz^T lo, and the epilogue adds the two 24-column halves)
@@ -30,6 +31,7 @@
 // model: SURVEY Appendix A.4 output layer, PAPER.md:1736 (172 classes).
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -55,7 +57,7 @@ constexpr int kOffP = kOffWdLo + 6 * 2048;                // P raw [2 stages][12
 constexpr int kOffPlo = kOffP + 2 * 8192;                 // P lo [128][16] SW64 (+ row exchange)
 constexpr int kOffPt = kOffPlo + 8192;                    // [P_hi|1 ; P_lo|0]^T [48][128] SW128: 4 atoms of 6 KB
 constexpr int kPtAtom = kHtNB * 128;
-constexpr int kOffDzHi = kOffPt + 4 * kPtAtom;            // dz^T [128 classes][128 rows] SW128
+constexpr int kOffDzHi = kOffPt + 4 * kPtAtom;            // dz [128 rows][128 classes] MN-major SW128_32B
 constexpr int kOffDzLo = kOffDzHi + 4 * 16384;
 constexpr int kOffBar = kOffDzLo + 4 * 16384;
 constexpr int kOffBias = kOffBar + 256;                   // b [176]
@@ -80,6 +82,21 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int k, int atom_bytes) {
   return (uint32_t)((k >> 5) * atom_bytes + r * 128 + (((((k & 31) >> 2) ^ r) & 7) << 4) + (k & 3) * 4);
 }
 
+// GNN_HT_PROF builds: per-CTA phase clocks of one epilogue thread per half
+// (prof[cta][half][8] accumulated cycles), read by tools/prof_head.py
+#ifdef GNN_HT_PROF
+#define HT_T(k)                                                      \
+  do {                                                               \
+    const long long now_ = clock64();                                \
+    if (lane == 0 && q == 0) ht_acc[k] += now_ - ht_last;            \
+    ht_last = now_;                                                  \
+  } while (0)
+#else
+#define HT_T(k) \
+  do {          \
+  } while (0)
+#endif
+
 struct HeadTcArgs {
   int64_t M;
   int din, C;
@@ -91,6 +108,7 @@ struct HeadTcArgs {
   float *partials;  // [grid][din*C + C]
   double *lpart;    // [grid]
   int64_t ntiles;
+  long long *prof;  // GNN_HT_PROF: [grid][2][8]
 };
 
 __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid_constant__ CUtensorMap tmP,
@@ -173,7 +191,7 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t iZ = tf32_idesc_kk(kHtCP), iP = tf32_idesc_kk(16), iW = tf32_idesc_kk(kHtNB);
+      constexpr uint32_t iZ = tf32_idesc_kk(kHtCP), iP = tf32_idesc_kk(16), iW = tf32_idesc_kk(kHtNB) | (1u << 15);  // A MN-major
       const uint64_t wf_hi = sw64_desc(sb + kOffWfHi), wf_lo = sw64_desc(sb + kOffWfLo);
       const uint64_t pl = sw64_desc(sb + kOffPlo);
       int it = 0;
@@ -200,9 +218,12 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
         auto dw_block = [&](uint32_t dcol) {
 #pragma unroll 2
           for (int j = 0; j < kHtRows / 8; ++j) {
-            const uint64_t ao = (uint64_t)(((j >> 2) * 16384 + (j & 3) * 32) >> 4);
+            // A = dz^T, MN-major (classes contiguous): K-block of 32 rows = 4 class
+            // atoms of 4 KB; 8 rows per MMA = +1 KB inside the K-block
+            const uint32_t ao = (uint32_t)((j >> 2) * 16384 + (j & 3) * 1024);
             const uint64_t bo = (uint64_t)(((j >> 2) * kPtAtom + (j & 3) * 32) >> 4);
-            const uint64_t ah = sw128_desc(sb + kOffDzHi) + ao, al = sw128_desc(sb + kOffDzLo) + ao;
+            const uint64_t ah = mn_desc(sb + kOffDzHi + ao, 4096, 512, 1);
+            const uint64_t al = mn_desc(sb + kOffDzLo + ao, 4096, 512, 1);
             const uint64_t bp = sw128_desc(sb + kOffPt) + bo;  // [P_hi|1 ; P_lo|0]
             tc_mma_tf32(tmem + dcol, ah, bp, iW, j);  // dz_hi.P_hi | dz_hi.P_lo
             tc_mma_tf32(tmem + dcol, al, bp, iW, 1);  // + dz_lo.P_hi | dz_lo.P_lo
@@ -233,20 +254,25 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
     const int cbase = hlf * kHtHalf;                 // this thread's classes [cbase, cbase + 88)
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     float *xchg = reinterpret_cast<float *>(sm + kOffPlo);  // [3][2][128] after M1 consumed P lo
-    // dz^T (class m, tile row rr) lives at atom (rr >> 5), row m, 16-byte chunk
-    // ((rr & 31) >> 2) ^ (m & 7); with m = cbase + j and cbase % 8 == 0 the chunk
-    // depends on j & 7 only: eight per-thread bases, then compile-time offsets
-    static_assert(kHtHalf % 8 == 0, "half boundary on a swizzle period");
-    uint32_t dzb[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      dzb[k] = (uint32_t)((rr >> 5) * 16384 + ((((rr & 31) >> 2) ^ k) << 4) + (rr & 3) * 4);
-    float *dzh = reinterpret_cast<float *>(sm + kOffDzHi), *dzl = reinterpret_cast<float *>(sm + kOffDzLo);
+    // dz (tile row rr, class m), MN-major SWIZZLE_128B_BASE32B (the dW A operand
+    // dz^T read along classes): K-block rr >> 5 (16 KB) / class atom m >> 5
+    // (4 KB) / row rr & 31 (128 B) / 32-byte granule ((m >> 3) & 3) ^ (rr & 3) /
+    // word m & 7.  A thread writes its classes 4 at a time (16-byte stores).
+    const uint32_t dzrow = (uint32_t)((rr >> 5) * 16384 + (rr & 31) * 128);
+    const int rsw = rr & 3;
+    auto dz_off = [&](int m) -> uint32_t {  // byte offset of class m (m % 4 == 0)
+      return dzrow + (uint32_t)((m >> 5) * 4096 + ((((m >> 3) & 3) ^ rsw) << 5) + (m & 7) * 4);
+    };
+    uint8_t *dzh = sm + kOffDzHi, *dzl = sm + kOffDzLo;
     float accw[17];                                  // dW^T row (class) partial: din 0..15, db
 #pragma unroll
     for (int k = 0; k < 17; ++k) accw[k] = 0.f;
     const int my_class = (hlf == 0 ? 0 : 128) + rr;  // the dW^T row this thread accumulates
     double lsum = 0.0;
+#ifdef GNN_HT_PROF
+    long long ht_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ht_last = clock64();
+#endif
     int it = 0;
     for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
       const int s = it & 1;
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
       const bool valid = row < a.M;
       // ---- E1: P lo (half 0) and [P|1]^T (half 1) from the landed P tile
       mbar_wait(p_full + s, (uint32_t)((it >> 1) & 1));
+      HT_T(0);
       {
         const uint8_t *pt = sm + kOffP + s * 8192;
         float p[16];
@@ -287,8 +314,10 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
         const int64_t dg = __ldg(a.deg_offsets + row + 1) - __ldg(a.deg_offsets + row);
         rs = dg > 0 ? 1.f / (float)dg : 0.f;
       }
+      HT_T(1);
       // ---- E2: logits -> softmax -> dz
       mbar_wait(z_full, ph);
+      HT_T(2);
       tc_fence_after();
       float z[kHtHalf];
 #pragma unroll
@@ -340,14 +369,14 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
       }
       // dz^T of classes 0..127 -> shared memory (the dW A operand)
       const int nb0 = hlf == 0 ? kHtHalf : 128 - kHtHalf;  // 88 or 40 classes of block 0
-      const uint32_t rowb = (uint32_t)cbase * 128u;  // row m = cbase + j
 #pragma unroll
-      for (int j = 0; j < kHtHalf; ++j) {
+      for (int j = 0; j < kHtHalf; j += 4) {
         if (j < nb0) {
-          const uint32_t off = (dzb[j & 7] + rowb + (uint32_t)j * 128u) >> 2;
-          const float h = tf32_hi(z[j]);
-          dzh[off] = h;
-          dzl[off] = z[j] - h;
+          const uint32_t off = dz_off(cbase + j);
+          const float4 h = make_float4(tf32_hi(z[j]), tf32_hi(z[j + 1]), tf32_hi(z[j + 2]), tf32_hi(z[j + 3]));
+          *reinterpret_cast<float4 *>(dzh + off) = h;
+          *reinterpret_cast<float4 *>(dzl + off) =
+              make_float4(z[j] - h.x, z[j + 1] - h.y, z[j + 2] - h.z, z[j + 3] - h.w);
         }
       }
       tmem_wait_st();
@@ -355,9 +384,11 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(dz0_ready);
+      HT_T(3);
       // ---- E3 / E4
       if (hlf == 1) {
         mbar_wait(dzt_free, ph);
+        HT_T(4);
         // classes 128..175 of dz^T into the (now free) dW A operand, re-read from
         // TMEM (dz raw / lo stay there until M1 of the next tile, which needs this
         // warp's p_ready): nothing of E2 stays live in registers across the wait
@@ -368,19 +399,26 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
           tmem_ld8(tq + kTmZlo + cbase + c0, vl);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // row m = cbase + c0 + j - 128 (multiple-of-8 base)
-            const uint32_t off = (dzb[j] + (uint32_t)(cbase + c0 - 128) * 128u + (uint32_t)j * 128u) >> 2;
-            dzh[off] = tf32_hi(__uint_as_float(vr[j]));
-            dzl[off] = __uint_as_float(vl[j]);
+          for (int j = 0; j < 8; j += 4) {  // class m = cbase + c0 + j - 128 of block 1
+            const uint32_t off = dz_off(cbase + c0 + j - 128);
+            *reinterpret_cast<float4 *>(dzh + off) =
+                make_float4(tf32_hi(__uint_as_float(vr[j])), tf32_hi(__uint_as_float(vr[j + 1])),
+                            tf32_hi(__uint_as_float(vr[j + 2])), tf32_hi(__uint_as_float(vr[j + 3])));
+            *reinterpret_cast<float4 *>(dzl + off) =
+                make_float4(__uint_as_float(vl[j]), __uint_as_float(vl[j + 1]), __uint_as_float(vl[j + 2]),
+                            __uint_as_float(vl[j + 3]));
           }
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(dz1_ready);
+        HT_T(5);
         mbar_wait(m3_done, ph);
+        HT_T(6);
         tc_fence_after();
       } else {
         mbar_wait(dp_full, ph);  // dW^T block 0 and dP
+        HT_T(6);
         tc_fence_after();
       }
       {
@@ -405,7 +443,12 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
         }
       }
       tc_fence_before();
+      HT_T(7);
     }
+#ifdef GNN_HT_PROF
+    if (lane == 0 && q == 0 && a.prof)
+      for (int k = 0; k < 8; ++k) a.prof[((int64_t)blockIdx.x * 2 + hlf) * 8 + k] = ht_acc[k];
+#endif
     // ---- CTA partials: dW^T row my_class -> partials[cta][k*C + class], db at [din*C + class]
     if (my_class < C) {
       float *out = a.partials + (int64_t)blockIdx.x * ((int64_t)din * C + C);
@@ -482,6 +525,22 @@ int gcn_head_tc(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, 
   a.partials = partials;
   a.lpart = lpart;
   a.ntiles = ceil_div(M, (int64_t)kHtRows);
+#ifdef GNN_HT_PROF
+  {
+    static long long *prof = nullptr;
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 2 * 8 * 1024);
+    a.prof = prof;
+    const char *dump = getenv("GNN_HT_PROF_DUMP");
+    if (dump) {  // previous call's clocks -> file (debug builds only)
+      static long long h[2 * 8 * 1024];
+      cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+      if (FILE *f = fopen(dump, "w")) {
+        for (int i = 0; i < 2 * 8 * 148; ++i) fprintf(f, "%lld%c", h[i], (i % 8 == 7) ? '\n' : ' ');
+        fclose(f);
+      }
+    }
+  }
+#endif
   const int64_t grid = a.ntiles < nb ? a.ntiles : nb;
   GNN_CUDA_TRY(cudaFuncSetAttribute(gcn_head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kHtSmem));

@@ -13,7 +13,7 @@ objs=()
 for f in "$src"/*.cu; do
   o=$out/$(basename "${f%.cu}").o
   /usr/local/cuda/bin/nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a \
-    -I"$root/include" -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr "$@" -c "$f" -o "$o" &
+    -I"$root/include" -I"$src/build" -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr "$@" -c "$f" -o "$o" &
   objs+=("$o")
 done
 wait
