@@ -388,7 +388,7 @@ def run_ours(args, rank, world):
     gather16 = 4 * Hd * g.csr_coalesced().nnz if args.layout == "coalesced" else 4 * Hd * E
     traffic16 = None
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                         "r1_spmm16_traffic.json")
+                         "r2_spmm16_traffic.json")
     if os.path.exists(tpath) and args.layout == "coalesced":
         with open(tpath) as f:
             traffic16 = json.load(f)["traffic_bytes_per_launch"]
@@ -424,7 +424,7 @@ def run_ours(args, rank, world):
         "roofline": {"kernel": "spmm width-16 (4 per epoch, avg, timed in-epoch)", "bound": "hbm",
                      "achieved": round(ach16, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(ach16 / hbm_peak, 4), "traffic": traffic16,
-                     "traffic_source": "profiles/r1_spmm16_traffic.json (ncu --set full)",
+                     "traffic_source": "profiles/r2_spmm16_traffic.json (ncu --set full)",
                      "bytes_per_launch": b16, "peak_source": peak_src,
                      # the binding unit is the L2->SM gather return, not HBM
                      "gather_bytes_per_launch": gather16,
