@@ -21,6 +21,8 @@
 #include <cuda.h>  // CUtensorMap (encode entry point fetched through the runtime)
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gnn {
@@ -1029,41 +1031,53 @@ __global__ void plan_long_prefix_kernel(const int64_t *__restrict__ off, int64_t
     if (lg && r > 0 && off[r] - off[r - 1] <= short_max) atomicOr(info, 1ull);
   }
 }
+// Per-row plan flags, two counters per 64-bit word so one exclusive scan
+// advances both (each count < 2^31, so the low field never carries):
+//   fa = split-row flag | empty-row flag << 32
+//   fb = groups of the split row | short-row flag << 32
+__device__ __forceinline__ int64_t lo32(int64_t v) { return v & 0xffffffffll; }
+__device__ __forceinline__ int64_t hi32(int64_t v) { return v >> 32; }
 __global__ void plan_flags_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                  int64_t short_max, int64_t main_nnz, int64_t *fsplit,
-                                  int64_t *fempty, int64_t *ngroups, int64_t *fshort) {
+                                  int64_t short_max, int64_t main_nnz, int64_t *fa, int64_t *fb) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     int64_t rs = off[r], re = off[r + 1];
-    fempty[r] = re == rs ? 1 : 0;
-    fshort[r] = (re > rs && re - rs <= short_max) ? 1 : 0;
+    const int64_t empty = re == rs ? 1 : 0;
+    const int64_t shrt = (re > rs && re - rs <= short_max) ? 1 : 0;
     // split-row bookkeeping covers short rows too (inside the nnz-split range):
     // a call that does not use the short-row kernel (wide K) finishes them here
     const bool split = re > rs && re <= main_nnz && rs / P != (re - 1) / P;
-    fsplit[r] = split ? 1 : 0;
-    ngroups[r] = split ? ceil_div((re - 1) / P - rs / P + 1, kGroupPartials) : 0;
+    const int64_t groups = split ? ceil_div((re - 1) / P - rs / P + 1, kGroupPartials) : 0;
+    fa[r] = (split ? 1 : 0) | (empty << 32);
+    fb[r] = groups | (shrt << 32);
   }
 }
 __global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, int64_t P,
-                                    const int64_t *__restrict__ us, const int64_t *__restrict__ ue,
-                                    const int64_t *__restrict__ ug, int32_t *split_rows,
-                                    int32_t *split_group_base, int32_t *chunk_split,
-                                    int32_t *empty_rows, const int64_t *__restrict__ ush,
-                                    int32_t *short_rows) {
+                                    const int64_t *__restrict__ fa, const int64_t *__restrict__ fb,
+                                    int32_t *split_rows, int32_t *split_group_base,
+                                    int32_t *chunk_split, int32_t *empty_rows, int32_t *short_rows) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    if (us[r + 1] != us[r]) {
-      const int64_t si = us[r];
+    const int64_t a0 = fa[r], a1 = fa[r + 1], b0 = fb[r], b1 = fb[r + 1];
+    if (lo32(a1) != lo32(a0)) {
+      const int64_t si = lo32(a0);
       split_rows[si] = (int32_t)r;
-      split_group_base[si] = (int32_t)ug[r];
+      split_group_base[si] = (int32_t)lo32(b0);
       const int64_t wa = off[r] / P, wb = (off[r + 1] - 1) / P;
       chunk_split[2 * wa + 1] = (int32_t)si;  // trailing partial of the owner chunk
       for (int64_t w = wa + 1; w <= wb; ++w) chunk_split[2 * w] = (int32_t)si;  // carry-ins
     }
-    if (ue[r + 1] != ue[r]) empty_rows[ue[r]] = (int32_t)r;
-    if (ush[r + 1] != ush[r]) short_rows[ush[r]] = (int32_t)r;
-    if (r == 0) split_group_base[us[R]] = (int32_t)ug[R];
+    if (hi32(a1) != hi32(a0)) empty_rows[hi32(a0)] = (int32_t)r;
+    if (hi32(b1) != hi32(b0)) short_rows[hi32(b0)] = (int32_t)r;
+    if (r == 0) split_group_base[lo32(fa[R])] = (int32_t)lo32(fb[R]);
   }
+}
+// [num_split, num_empty, num_groups, num_short] from the scanned totals
+__global__ void plan_counts_kernel(const int64_t *fa, const int64_t *fb, int64_t R, int64_t *counts) {
+  counts[0] = lo32(fa[R]);
+  counts[1] = hi32(fa[R]);
+  counts[2] = lo32(fb[R]);
+  counts[3] = hi32(fb[R]);
 }
 
 // Degree order of the short-row list (longest first): the NG rows a warp of
@@ -1239,15 +1253,11 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   cudaStream_t st = as_stream(stream);
   const int64_t R = A->num_rows;
   WsArena ar(ws, ws_bytes);
-  int64_t *fs = ar.take<int64_t>(R + 1);
-  int64_t *fe = ar.take<int64_t>(R + 1);
-  int64_t *fg = ar.take<int64_t>(R + 1);
-  int64_t *fh = ar.take<int64_t>(R + 1);
+  int64_t *fa = ar.take<int64_t>(R + 1);
+  int64_t *fb = ar.take<int64_t>(R + 1);
   size_t sb = scan_i64_workspace(R);
   void *s1 = ar.take<char>((int64_t)sb);
   void *s2 = ar.take<char>((int64_t)sb);
-  void *s3 = ar.take<char>((int64_t)sb);
-  void *s4 = ar.take<char>((int64_t)sb);
   int64_t *dh = ar.take<int64_t>(R + 1);   // short rows: degree histogram -> cursors
   int32_t *srt = ar.take<int32_t>(R + 1);  // short rows in degree order
   void *s5 = ar.take<char>((int64_t)sb);
@@ -1275,27 +1285,26 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   GNN_LAUNCH_CHECK();
   if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, main_nnz, fs,
-                                                       fe, fg, fh);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, main_nnz, fa,
+                                                       fb);
     GNN_LAUNCH_CHECK();
   }
-  GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
-  GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
-  GNN_TRY(exclusive_scan_i64(fg, fg, R, true, s3, sb, st));
-  GNN_TRY(exclusive_scan_i64(fh, fh, R, true, s4, sb, st));
+  GNN_TRY(exclusive_scan_i64(fa, fa, R, true, s1, sb, st));
+  GNN_TRY(exclusive_scan_i64(fb, fb, R, true, s2, sb, st));
   if (R > 0) {
-    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg,
-                                                         buf + L.o_split, buf + L.o_sgb,
-                                                         buf + L.o_csplit, buf + L.o_empty, fh,
-                                                         buf + L.o_short);
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fa, fb, buf + L.o_split,
+                                                         buf + L.o_sgb, buf + L.o_csplit,
+                                                         buf + L.o_empty, buf + L.o_short);
     GNN_LAUNCH_CHECK();
   }
-  int64_t h[4] = {0, 0, 0, 0};
-  GNN_CUDA_TRY(cudaMemcpyAsync(&h[0], fs + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GNN_CUDA_TRY(cudaMemcpyAsync(&h[1], fe + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GNN_CUDA_TRY(cudaMemcpyAsync(&h[2], fg + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GNN_CUDA_TRY(cudaMemcpyAsync(&h[3], fh + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int64_t tot[2] = {0, 0}, h[4];
+  GNN_CUDA_TRY(cudaMemcpyAsync(&tot[0], fa + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GNN_CUDA_TRY(cudaMemcpyAsync(&tot[1], fb + R, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GNN_CUDA_TRY(cudaStreamSynchronize(st));
+  h[0] = tot[0] & 0xffffffffll;
+  h[1] = tot[0] >> 32;
+  h[2] = tot[1] & 0xffffffffll;
+  h[3] = tot[1] >> 32;
   if (h[3] > 1) {  // longest-first order of the short rows
     int32_t *sr = buf + L.o_short;
     GNN_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(int64_t) * (R + 1), st));
@@ -1325,13 +1334,6 @@ int gnn_spmm_plan_build_ex(const gnn_csr_view_t *A, int64_t P, int64_t short_max
   return GNN_OK;
 }
 
-__global__ void plan_counts_kernel(const int64_t *fs, const int64_t *fe, const int64_t *fg,
-                                   const int64_t *fh, int64_t R, int64_t *counts) {
-  counts[0] = fs[R];
-  counts[1] = fe[R];
-  counts[2] = fg[R];
-  counts[3] = fh[R];
-}
 
 int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t P, int64_t short_max, int32_t *buf,
                             gnn_spmm_plan_t *plan, int64_t *counts, const int64_t *row_limit,
@@ -1345,15 +1347,11 @@ int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t P, int64_t short_ma
   cudaStream_t st = as_stream(stream);
   const int64_t R = A->num_rows;
   WsArena ar(ws, ws_bytes);
-  int64_t *fs = ar.take<int64_t>(R + 1);
-  int64_t *fe = ar.take<int64_t>(R + 1);
-  int64_t *fg = ar.take<int64_t>(R + 1);
-  int64_t *fh = ar.take<int64_t>(R + 1);
+  int64_t *fa = ar.take<int64_t>(R + 1);
+  int64_t *fb = ar.take<int64_t>(R + 1);
   size_t sb = scan_i64_workspace(R);
   void *s1 = ar.take<char>((int64_t)sb);
   void *s2 = ar.take<char>((int64_t)sb);
-  void *s3 = ar.take<char>((int64_t)sb);
-  void *s4 = ar.take<char>((int64_t)sb);
   if (!ar.ok()) return GNN_ERR_WORKSPACE;
   const int64_t nnz = A->nnz;
   const PlanLayout L = plan_layout(R, nnz, P);
@@ -1362,22 +1360,18 @@ int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t P, int64_t short_ma
   GNN_LAUNCH_CHECK();
   if (L.nw > 0) GNN_CUDA_TRY(cudaMemsetAsync(buf + L.o_csplit, 0xff, sizeof(int32_t) * 2 * L.nw, st));
   if (R > 0) {
-    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, nnz, fs, fe,
-                                                       fg, fh);
+    plan_flags_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, short_max, nnz, fa, fb);
     GNN_LAUNCH_CHECK();
   }
-  GNN_TRY(exclusive_scan_i64(fs, fs, R, true, s1, sb, st));
-  GNN_TRY(exclusive_scan_i64(fe, fe, R, true, s2, sb, st));
-  GNN_TRY(exclusive_scan_i64(fg, fg, R, true, s3, sb, st));
-  GNN_TRY(exclusive_scan_i64(fh, fh, R, true, s4, sb, st));
+  GNN_TRY(exclusive_scan_i64(fa, fa, R, true, s1, sb, st));
+  GNN_TRY(exclusive_scan_i64(fb, fb, R, true, s2, sb, st));
   if (R > 0) {
-    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fs, fe, fg,
-                                                         buf + L.o_split, buf + L.o_sgb,
-                                                         buf + L.o_csplit, buf + L.o_empty, fh,
-                                                         buf + L.o_short);
+    plan_scatter_kernel<<<grid_1d(R, 256), 256, 0, st>>>(A->offsets, R, P, fa, fb, buf + L.o_split,
+                                                         buf + L.o_sgb, buf + L.o_csplit,
+                                                         buf + L.o_empty, buf + L.o_short);
     GNN_LAUNCH_CHECK();
   }
-  plan_counts_kernel<<<1, 1, 0, st>>>(fs, fe, fg, fh, R, counts);
+  plan_counts_kernel<<<1, 1, 0, st>>>(fa, fb, R, counts);
   GNN_LAUNCH_CHECK();
   // capacities: a split row spans >= 2 chunks (<= nw of them); sum over split rows
   // of ceil(partials / 64) <= num_split + (nw + num_split) / 64
@@ -1623,8 +1617,12 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
   }
   if (side) GNN_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
   if (plan->num_empty > 0) {
-    spmm_empty_rows_kernel<<<grid_1d(plan->num_empty * K, 256), 256, 0, st>>>(a, plan->empty_rows,
-                                                                            plan->num_empty);
+    // grid-stride; a device-count plan's capacity (every row) is no reason for a
+    // grid of every row
+    const unsigned eg = plan->dev_counts ? (unsigned)std::min<int64_t>(grid_1d(plan->num_empty * K, 256),
+                                                                       (int64_t)sm_count() * 4)
+                                         : grid_1d(plan->num_empty * K, 256);
+    spmm_empty_rows_kernel<<<eg, 256, 0, st>>>(a, plan->empty_rows, plan->num_empty);
     GNN_LAUNCH_CHECK();
   }
   return GNN_OK;
