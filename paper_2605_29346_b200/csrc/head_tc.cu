@@ -70,6 +70,11 @@ static_assert(kHtSmem <= 227 * 1024, "fits one SM");
 // dW^T blocks: [dz.P_hi | dz.P_lo] halves of 24 columns, summed by the epilogue
 constexpr uint32_t kTmZ = 0, kTmZlo = 176, kTmDp = 352, kTmDw0 = 368, kTmDw1 = 416;
 
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2 (as __expf uses)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // byte offset of (row r, fp32 column k) in a K-major SWIZZLE_64B tile (64-byte rows)
@@ -105,6 +110,7 @@ struct HeadTcArgs {
   float scale;
   float *dP;
   int64_t lddp;
+  int dp_vec;       // din == 16 and 16-byte dP rows: vector stores
   float *partials;  // [grid][din*C + C]
   double *lpart;    // [grid]
   int64_t ntiles;
@@ -328,25 +334,33 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
         for (int j = 0; j < 8; ++j) z[c0 + j] = __uint_as_float(v[j]);
       }
       tmem_wait_ld();
-      float mx = -INFINITY, zy = 0.f;
+      float zy = 0.f;
       const int yl = (y >= cbase && y < cbase + kHtHalf) ? (int)(y - cbase) : -1;  // label column here
       const bool has_y = yl >= 0;
+      // 8 independent partial maxima / sums: no 88-deep dependent chains
+      float m8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
 #pragma unroll
       for (int j = 0; j < kHtHalf; ++j) {
         z[j] += sbias[cbase + j];
-        mx = fmaxf(mx, z[j]);
+        m8[j & 7] = fmaxf(m8[j & 7], z[j]);
         if (j == yl) zy = z[j];
       }
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       const int bar_id = 1 + q;  // the two warps (same warp % 4) holding the halves of these 32 rows
       xchg[(0 * 2 + hlf) * kHtRows + rr] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
       mx = fmaxf(mx, xchg[(0 * 2 + (hlf ^ 1)) * kHtRows + rr]);
-      float se = 0.f;
+      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const float mxl = mx * 1.4426950408889634f;  // exp(z - mx) = 2^(z log2e - mx log2e)
 #pragma unroll
       for (int j = 0; j < kHtHalf; ++j) {
-        z[j] = __expf(z[j] - mx);
-        se += z[j];
+        z[j] = ex2_approx(fmaf(z[j], 1.4426950408889634f, -mxl));
+        s8[j & 7] += z[j];
       }
+      float se = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
       xchg[(1 * 2 + hlf) * kHtRows + rr] = se;
       xchg[(2 * 2 + hlf) * kHtRows + rr] = has_y ? zy : 0.f;
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
@@ -437,9 +451,17 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
         accw[16] += __uint_as_float(w8[0]) + __uint_as_float(u8[0]);
         if (hlf == 0 && valid) {
           float *dst = a.dP + row * a.lddp;
+          if (a.dp_vec) {  // 16 columns, 16-byte rows: four 128-bit stores
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-            if (k < din) dst[k] = __uint_as_float(dp[k]) * rs;
+            for (int k = 0; k < 16; k += 4)
+              *reinterpret_cast<float4 *>(dst + k) =
+                  make_float4(__uint_as_float(dp[k]) * rs, __uint_as_float(dp[k + 1]) * rs,
+                              __uint_as_float(dp[k + 2]) * rs, __uint_as_float(dp[k + 3]) * rs);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (k < din) dst[k] = __uint_as_float(dp[k]) * rs;
+          }
         }
       }
       tc_fence_before();
@@ -522,6 +544,7 @@ int gcn_head_tc(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, 
   a.scale = scale;
   a.dP = dP;
   a.lddp = lddp;
+  a.dp_vec = Din == 16 && lddp % 4 == 0 && (reinterpret_cast<uintptr_t>(dP) & 15u) == 0;
   a.partials = partials;
   a.lpart = lpart;
   a.ntiles = ceil_div(M, (int64_t)kHtRows);
