@@ -54,14 +54,19 @@ constexpr int kOffWfLo = kOffWfHi + kHtCP * 64;           // 11264
 constexpr int kOffWdHi = kOffWfLo + kHtCP * 64;           // W [16][192] SW128: dP B (6 atoms of 2 KB)
 constexpr int kOffWdLo = kOffWdHi + 6 * 2048;
 constexpr int kOffP = kOffWdLo + 6 * 2048;                // P raw [2 stages][128][16] SW64
-constexpr int kOffPlo = kOffP + 2 * 8192;                 // P lo [128][16] SW64 (+ row exchange)
+constexpr int kOffPlo = kOffP + 2 * 8192;                 // P lo [128][16] SW64
 constexpr int kOffPt = kOffPlo + 8192;                    // [P_hi|1 ; P_lo|0]^T [48][128] SW128: 4 atoms of 6 KB
 constexpr int kPtAtom = kHtNB * 128;
 constexpr int kOffDzHi = kOffPt + 4 * kPtAtom;            // dz [128 rows][128 classes] MN-major SW128_32B
 constexpr int kOffDzLo = kOffDzHi + 4 * 16384;
 constexpr int kOffBar = kOffDzLo + 4 * 16384;
 constexpr int kOffBias = kOffBar + 256;                   // b [176]
-constexpr int kHtSmem = kOffBias + kHtCP * 4 + 1024;      // + alignment slack
+constexpr int kOffXchg = kOffBias + kHtCP * 4;            // partner-row exchange [3][2][128]
+constexpr int kOffLred = kOffXchg + 3 * 2 * 128 * 4;      // loss partials [4] (double)
+// No alignment slack: the kernel has no static shared memory, so the dynamic
+// buffer starts at the CTA's (1024-aligned) shared window base — checked at
+// run time (a misaligned base would trap, never silently corrupt).
+constexpr int kHtSmem = kOffLred + 4 * 8;
 static_assert(kOffWdHi % 1024 == 0 && kOffP % 1024 == 0 && kOffPt % 1024 == 0 &&
                   kOffDzHi % 1024 == 0 && kOffBar % 8 == 0,
               "1024-aligned operand regions");
@@ -120,15 +125,15 @@ struct HeadTcArgs {
 __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid_constant__ CUtensorMap tmP,
                                                                    HeadTcArgs a) {
   extern __shared__ __align__(1024) uint8_t ht_raw[];
-  // 1024-aligned base as an offset into the shared array (keeps the accesses STS / LDS)
-  uint8_t *sm = ht_raw + ((1024u - (smem_u32(ht_raw) & 1023u)) & 1023u);
+  uint8_t *sm = ht_raw;  // the window base: 1024-aligned (no static shared memory precedes it)
+  if (smem_u32(ht_raw) & 1023u) __trap();
   const uint32_t sb = smem_u32(sm);
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + kOffBar);
   uint64_t *p_full = bars, *p_empty = bars + 2;                     // [2] each
   uint64_t *p_ready = bars + 4, *z_full = bars + 5, *dz0_ready = bars + 6;
   uint64_t *dzt_free = bars + 7, *dz1_ready = bars + 8, *m3_done = bars + 9, *dp_full = bars + 10;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 11);
-  __shared__ double lred[4];
+  double *lred = reinterpret_cast<double *>(sm + kOffLred);  // [quarter]
 
   const int warp = threadIdx.x >> 5, lane = (int)lane_id();
   const int din = a.din, C = a.C;
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
     const int rr = q * 32 + lane;                    // row within the tile = TMEM lane
     const int cbase = hlf * kHtHalf;                 // this thread's classes [cbase, cbase + 88)
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    float *xchg = reinterpret_cast<float *>(sm + kOffPlo);  // [3][2][128] after M1 consumed P lo
+    float *xchg = reinterpret_cast<float *>(sm + kOffXchg);  // [3][2][128]: max, sum, label logit
     // dz (tile row rr, class m), MN-major SWIZZLE_128B_BASE32B (the dW A operand
     // dz^T read along classes): K-block rr >> 5 (16 KB) / class atom m >> 5
     // (4 KB) / row rr & 31 (128 B) / 32-byte granule ((m >> 3) & 3) ^ (rr & 3) /
@@ -398,10 +403,20 @@ __global__ void __launch_bounds__(kHtThreads, 1) gcn_head_tc_kernel(const __grid
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(dz0_ready);
+      // block-0 rows of these 32 tile rows written: the partner (half 1) rewrites
+      // classes 0..47 of the same rows with block 1 after dzt_free.  That order
+      // already follows from dz0_ready -> MMA -> dzt_free; the named barrier makes
+      // it explicit to every observer (compute-sanitizer racecheck included)
+#ifndef HT_NO_NAMEDBAR
+      if (hlf == 0) asm volatile("bar.arrive %0, 64;" ::"r"(5 + q) : "memory");
+#endif
       HT_T(3);
       // ---- E3 / E4
       if (hlf == 1) {
         mbar_wait(dzt_free, ph);
+#ifndef HT_NO_NAMEDBAR
+        asm volatile("bar.sync %0, 64;" ::"r"(5 + q) : "memory");
+#endif
         HT_T(4);
         // classes 128..175 of dz^T into the (now free) dW A operand, re-read from
         // TMEM (dz raw / lo stay there until M1 of the next tile, which needs this

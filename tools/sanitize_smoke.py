@@ -35,9 +35,29 @@ for co in (False, True):
     t = GCNTrainer(pl, 40, 16, 7, seed=0, coalesced=co)
     t.set_inputs(Xh, yh)
     t.step()
-t = GCNTrainer(pl, 40, 16, 90, seed=0)  # wide output layer
+t = GCNTrainer(pl, 40, 16, 90, seed=0)  # wide output layer (tcgen05 head, head_tc.cu)
 t.set_inputs(Xh, torch.randint(0, 90, (2000,)))
 t.step()
+t = GCNTrainer(pl, 40, 16, 172, seed=0)  # 172 classes: both epilogue halves, both dW blocks
+t.set_inputs(Xh, torch.randint(0, 172, (2000,)))
+t.step()
+# device builders: stable radix sorts (1-3 passes), offsets with long empty gaps
+from paper_2605_29346_b200.graph import _offsets_from_keys, _sort_pairs  # noqa: E402
+
+for R in (300, 100_000, 1 << 27):
+    k = torch.randint(0, R, (50_001,), device="cuda", dtype=torch.int32)
+    ko, vo = _sort_pairs(k, torch.arange(50_001, device="cuda", dtype=torch.int32), R)
+    _offsets_from_keys(ko, R if R < (1 << 20) else 1 << 20) if R < (1 << 20) else None
+gb.csr_from_edges(3000, src, dst).csc(with_eid=True)
+# replayed sampled mini-batch step (device-count plans, live-row limits)
+from paper_2605_29346_b200.models import SampledGCNTrainer  # noqa: E402
+from paper_2605_29346_b200.sampling import SampleConfig  # noqa: E402
+
+st = SampledGCNTrainer(pl, Xh.cuda(), yh.cuda(), 40, 16, 7, SampleConfig(batch_size=64, fanouts=(5, 4)),
+                       seed=0)
+st.capture()
+for i in range(2):
+    st.run(rng.choice(2000, 64, replace=False), rng=i)
 t = GINTrainer(pl, 40, 64, 7, seed=0)
 t.set_inputs(Xh, yh)
 t.step()
