@@ -476,6 +476,15 @@ int gnn_gat_rowstat_mean(int64_t V, int64_t F1, int64_t Cp, const float *dZ, int
                          const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
                          const float *er, const float *rowstat, float *stat, int64_t ldst,
                          gnn_stream_t stream);
+/* The same on the tensor cores (split-TF32 tcgen05: G = dZ W_h^T per head,
+ * reduced against Yc in the GEMM epilogue, G never stored); W dense
+ * (ldw == 4*Cp), V >= 128; GNN_ERR_UNSUPPORTED otherwise.  Same statistics
+ * layout as gnn_gat_rowstat_mean; caller-owned workspace. */
+size_t gnn_gat_rowstat_mean_tc_workspace(int64_t F1, int64_t Cp);
+int gnn_gat_rowstat_mean_tc(int64_t V, int64_t F1, int64_t Cp, const float *dZ, int64_t ldz,
+                            const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
+                            const float *er, const float *rowstat, float *stat, int64_t ldst,
+                            void *ws, size_t ws_bytes, gnn_stream_t stream);
 /* One pass over the CSC (AT with its edge-ID array): edge (v -> u) recomputes
  * alpha_h = exp(LeakyReLU(el[u,h] + er[v,h]) - m[v,h]) * inv[v,h] and forms
  *   dWh[u,:]  = sum alpha_h dY[v, head h cols]          (SpMMve^T)

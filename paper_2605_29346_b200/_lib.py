@@ -261,6 +261,10 @@ SIGNATURES = {
                                 c_ptr, c_i64, c_ptr]),
     "gnn_gat_rowstat_mean": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
                                      c_i64, C.c_float, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
+    "gnn_gat_rowstat_mean_tc_workspace": (c_sz, [c_i64, c_i64]),
+    "gnn_gat_rowstat_mean_tc": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
+                                        c_i64, C.c_float, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_sz,
+                                        c_ptr]),
     "gnn_gat_bwd_rc_workspace": (c_sz, [C.POINTER(SpmmPlan), c_i64]),
     "gnn_gat_bwd_rc": (
         c_int,

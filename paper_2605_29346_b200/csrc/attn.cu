@@ -2428,3 +2428,60 @@ int gnn_invert_permutation(int64_t n, const int32_t *perm, int32_t *inv, gnn_str
 }
 
 }  // extern "C"
+
+namespace gnn {
+int gemm_tc_rowdot(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *Bt,
+                   int64_t ldb, const float *Y, int64_t ldy, float *S, int64_t ldS, int64_t hs,
+                   void *ws, size_t ws_bytes, cudaStream_t st);
+size_t gemm_tc_workspace(int64_t N, int64_t K);
+namespace {
+// stat[v] = {er, m, inv, scale * S} per head, S already in the w slots
+__global__ void gat_rowstat_pack_kernel(int64_t V, float scale, const float *__restrict__ er,
+                                        const float *__restrict__ mstat, float *__restrict__ P,
+                                        int64_t ldp) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= V * 4) return;
+  const int64_t v = t >> 2;
+  const int h = (int)(t & 3);
+  float4 *d = reinterpret_cast<float4 *>(P + v * ldp) + h;
+  const float S = d->w;
+  *d = make_float4(__ldg(er + v * 4 + h), __ldg(mstat + v * 8 + h), __ldg(mstat + v * 8 + 4 + h),
+                   scale * S);
+}
+}  // namespace
+}  // namespace gnn
+
+extern "C" {
+
+size_t gnn_gat_rowstat_mean_tc_workspace(int64_t F1, int64_t Cp) {
+  if (F1 <= 0 || Cp <= 0) return 0;
+  return gemm_tc_workspace(4 * F1 < 128 ? 4 * F1 : 128, Cp);
+}
+
+// gnn_gat_rowstat_mean on the tensor cores: G = dZ . W^T viewed [4*F1, Cp]
+// (row 4i+h = W[i, h*Cp:(h+1)*Cp], so W must be dense: ldw == 4*Cp) in
+// split-TF32, reduced against Yc in the GEMM epilogue — S[v,h] = sum_i
+// Yc[v,4i+h] G[v,4i+h], the G tile never leaving the SM; then the row
+// statistics are packed beside S.  UNSUPPORTED when the shapes do not fit
+// the tensor-core path (the caller keeps gnn_gat_rowstat_mean).
+int gnn_gat_rowstat_mean_tc(int64_t V, int64_t F1, int64_t Cp, const float *dZ, int64_t ldz,
+                            const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
+                            const float *er, const float *rowstat, float *stat, int64_t ldst,
+                            void *ws, size_t ws_bytes, gnn_stream_t stream) {
+  if (V < 0 || F1 <= 0 || Cp <= 0 || Cp % 4 || ldz < Cp || ldc < 4 * F1 || ldw < 4 * Cp)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (V == 0) return GNN_OK;
+  if (!dZ || !Yc || !W || !er || !rowstat || !stat || !al16(stat) || ldst < 16 || ldst % 4)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (ldw != 4 * Cp) return GNN_ERR_UNSUPPORTED;
+  if (ws_bytes < gnn_gat_rowstat_mean_tc_workspace(F1, Cp)) return GNN_ERR_WORKSPACE;
+  cudaStream_t st = as_stream(stream);
+  GNN_TRY(gemm_tc_rowdot(V, 4 * F1, Cp, dZ, ldz, W, Cp, Yc, ldc, stat + 3, ldst, 4, ws, ws_bytes,
+                         st));
+  gat_rowstat_pack_kernel<<<(unsigned)ceil_div(V * 4, 256), 256, 0, st>>>(V, scale, er, rowstat,
+                                                                          stat, ldst);
+  GNN_LAUNCH_CHECK();
+  return GNN_OK;
+}
+
+}  // extern "C"

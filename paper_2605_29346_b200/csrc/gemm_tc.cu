@@ -49,6 +49,13 @@ struct TcArgs {
   int relu;
   int vec_store;  // C rows 16-byte aligned: 128-bit epilogue stores
   const int64_t *rows_dev;  // live rows on device (tiles past them skipped), or null
+  // row-dot epilogue (C not stored): S[row, c mod 4] (+)= sum_c C[row, c] * dotY[row, c]
+  // over the block's N columns, S[row, h] at dotS[row * ldS + h * dot_hs]
+  const float *dotY;
+  int64_t lddot;
+  float *dotS;
+  int64_t ldS, dot_hs;
+  int dot_acc;  // add to S (a later column block) instead of overwriting it
 };
 
 template <int NPAD>
@@ -56,7 +63,7 @@ constexpr size_t tc_smem_bytes() {
   return (size_t)tc_stages<NPAD>() * (2 * kTcM * kTcBK + 2 * NPAD * kTcBK) * 4 + 1024 + 1024;
 }
 
-template <int NPAD>
+template <int NPAD, bool DOT = false>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                 const __grid_constant__ CUtensorMap tmBhi,
                                                                 const __grid_constant__ CUtensorMap tmBlo,
@@ -207,7 +214,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       tc_fence_after();
       const int64_t row = t * kTcM + q * 32 + lane;
       float *crow = p.C + row * p.ldc;
-      for (int c0 = 0; c0 < NPAD; c0 += 16) {
+      float4 dacc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (DOT) {
+        // row-dot epilogue: the row's Y slice is fetched 64 columns at a time
+        // (16 loads in flight per thread) ahead of the TMEM reads it meets
+        constexpr int kDR = NPAD < 64 ? NPAD : 64;
+        for (int r0 = 0; r0 < NPAD; r0 += kDR) {
+          float4 y4[kDR / 4];
+#pragma unroll
+          for (int j = 0; j < kDR / 4; ++j)
+            y4[j] = row < p.M && r0 + 4 * j < p.N ? ldg_f4(p.dotY + row * p.lddot + r0 + 4 * j)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int c1 = 0; c1 < kDR; c1 += 16) {
+            uint32_t v[16], u[16];
+            const uint32_t taddr =
+                tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + r0 + c1);
+            tmem_ld16(taddr, v);
+            tmem_ld16(taddr + NPAD, u);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 y = y4[c1 / 4 + j];
+              dacc.x = fmaf(__uint_as_float(v[4 * j]) + __uint_as_float(u[4 * j]), y.x, dacc.x);
+              dacc.y = fmaf(__uint_as_float(v[4 * j + 1]) + __uint_as_float(u[4 * j + 1]), y.y, dacc.y);
+              dacc.z = fmaf(__uint_as_float(v[4 * j + 2]) + __uint_as_float(u[4 * j + 2]), y.z, dacc.z);
+              dacc.w = fmaf(__uint_as_float(v[4 * j + 3]) + __uint_as_float(u[4 * j + 3]), y.w, dacc.w);
+            }
+          }
+        }
+      }
+      for (int c0 = 0; c0 < NPAD && !DOT; c0 += 16) {
         uint32_t v[16], u[16];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
         tmem_ld16(taddr, v);
@@ -237,6 +274,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
             }
           }
         }
+      }
+      if (DOT && row < p.M) {
+        float *sr = p.dotS + row * p.ldS;
+        const float d[4] = {dacc.x, dacc.y, dacc.z, dacc.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) sr[h * p.dot_hs] = p.dot_acc ? sr[h * p.dot_hs] + d[h] : d[h];
       }
       tc_fence_before();
       __syncwarp();
@@ -610,14 +653,14 @@ bool map_2d(CUtensorMap *tm, const float *base, int64_t inner, int64_t outer, in
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NPAD>
+template <int NPAD, bool DOT = false>
 int launch_tc(const CUtensorMap &ta, const CUtensorMap &tbh, const CUtensorMap &tbl,
               const TcArgs &p, cudaStream_t st) {
   const size_t smem = tc_smem_bytes<NPAD>();
-  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<NPAD>,
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<NPAD, DOT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = p.mtiles < sm_count() ? p.mtiles : sm_count();
-  gemm_tc_kernel<NPAD><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tbh, tbl, p);
+  gemm_tc_kernel<NPAD, DOT><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tbh, tbl, p);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -673,6 +716,54 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const 
     case 64: return launch_tc<64>(ta, tbh, tbl, p, st);
     default: return launch_tc<128>(ta, tbh, tbl, p, st);
   }
+}
+
+// Row-dot form: S[m, h] = sum over columns c = h (mod 4) of (A Bt^T)[m, c] * Y[m, c],
+// Bt [N, K] row-major (ldb), N % 4 == 0; the product never leaves the SM
+// (128-column blocks, the later ones accumulating into S in block order).
+int gemm_tc_rowdot(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *Bt,
+                   int64_t ldb, const float *Y, int64_t ldy, float *S, int64_t ldS, int64_t hs,
+                   void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (N % 4 || !gemm_tc_supported(M, 128, K, A, lda, 0) || (ldy % 4) ||
+      (reinterpret_cast<uintptr_t>(Y) & 15u))
+    return GNN_ERR_UNSUPPORTED;
+  for (int64_t n0 = 0; n0 < N; n0 += 128) {
+    const int64_t nb = N - n0 < 128 ? N - n0 : 128;
+    const int npad = tc_npad(nb);
+    const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
+    if (ws_bytes < gemm_tc_workspace(nb, K)) return GNN_ERR_WORKSPACE;
+    float *bhi = static_cast<float *>(ws);
+    float *blo = bhi + (size_t)npad * kpad;
+    split_b_kernel<<<(unsigned)ceil_div((int64_t)npad * kpad, 256), 256, 0, st>>>(
+        Bt + n0 * ldb, ldb, 1, nb, K, npad, kpad, bhi, blo);
+    GNN_LAUNCH_CHECK();
+    CUtensorMap ta, tbh, tbl;
+    if (!map_2d_sw128(&ta, A, K, M, lda, kTcM) || !map_2d_sw128(&tbh, bhi, kpad, npad, kpad, npad) ||
+        !map_2d_sw128(&tbl, blo, kpad, npad, kpad, npad))
+      return GNN_ERR_UNSUPPORTED;
+    TcArgs p{};
+    p.M = M;
+    p.N = nb;
+    p.K = K;
+    p.Npad = npad;
+    p.nkb = (int)(kpad / kTcBK);
+    p.mtiles = ceil_div(M, kTcM);
+    p.dotY = Y + n0;
+    p.lddot = ldy;
+    p.dotS = S;
+    p.ldS = ldS;
+    p.dot_hs = hs;
+    p.dot_acc = n0 > 0;
+    int rc;
+    switch (npad) {
+      case 16: rc = launch_tc<16, true>(ta, tbh, tbl, p, st); break;
+      case 32: rc = launch_tc<32, true>(ta, tbh, tbl, p, st); break;
+      case 64: rc = launch_tc<64, true>(ta, tbh, tbl, p, st); break;
+      default: rc = launch_tc<128, true>(ta, tbh, tbl, p, st); break;
+    }
+    if (rc != GNN_OK) return rc;
+  }
+  return GNN_OK;
 }
 
 // ---- A^T B (weight gradient) on tcgen05

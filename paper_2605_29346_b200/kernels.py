@@ -517,7 +517,9 @@ class GatRowStatCall:
     four float4 into ``stat`` (a [V, 16] view, usually the 16 columns after
     the gradient row the recompute backward gathers).  Concatenated heads:
     S = <dYm_h, Y_h - b_h>.  ``mean`` (head-mean output layer,
-    aggregate-then-transform): S = scale <dZ, Yc_h W_h>."""
+    aggregate-then-transform): S = scale <dZ, Yc_h W_h>, on the tensor cores
+    (gnn_gat_rowstat_mean_tc: dZ W_h^T reduced against Yc in the GEMM
+    epilogue) where the shapes allow, else the SIMT kernel."""
 
     def __init__(self, er, rowstat, stat, *, dYm=None, Y=None, bias=None, mean=None):
         self.lib = _lib.lib()
@@ -525,6 +527,15 @@ class GatRowStatCall:
         self.V = int(er.shape[0])
         self.er, self.rowstat, self.stat = er, rowstat, stat
         self.dYm, self.Y, self.bias, self.mean = dYm, Y, bias, mean
+        self.tc = False
+        if mean is not None and os.environ.get("GNN_GAT_ROWSTAT_TC", "1") != "0":
+            dZ, Yc, W, F1, Cp, _ = mean
+            self.tc = (self.V >= 128 and W.stride(0) == 4 * Cp and dZ.stride(0) % 4 == 0
+                       and dZ.data_ptr() % 16 == 0 and Yc.stride(0) % 4 == 0
+                       and Yc.data_ptr() % 16 == 0)
+            if self.tc:
+                self.ws = _lib.workspace(self.lib.gnn_gat_rowstat_mean_tc_workspace(F1, Cp),
+                                         self.dev)
 
     def __call__(self):
         st = _lib.stream_handle(self.dev)
@@ -537,6 +548,13 @@ class GatRowStatCall:
                 self.stat.stride(0), st), "gat_rowstat")
         else:
             dZ, Yc, W, F1, Cp, scale = self.mean
+            if self.tc:
+                _lib.check(self.lib.gnn_gat_rowstat_mean_tc(
+                    self.V, F1, Cp, dZ.data_ptr(), dZ.stride(0), Yc.data_ptr(), Yc.stride(0),
+                    W.data_ptr(), W.stride(0), scale, self.er.data_ptr(), self.rowstat.data_ptr(),
+                    self.stat.data_ptr(), self.stat.stride(0), self.ws.data_ptr(), self.ws.numel(),
+                    st), "gat_rowstat_mean_tc")
+                return
             _lib.check(self.lib.gnn_gat_rowstat_mean(
                 self.V, F1, Cp, dZ.data_ptr(), dZ.stride(0), Yc.data_ptr(), Yc.stride(0),
                 W.data_ptr(), W.stride(0), scale, self.er.data_ptr(), self.rowstat.data_ptr(),

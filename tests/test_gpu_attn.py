@@ -336,3 +336,36 @@ def test_spmm_shared_heads(gb, graphs, gname, F):
         np.add.at(ra[:, :, h], rows, np.abs(al[:, h:h + 1].astype(np.float64) * X[tgt]))
     ok, worst = oo.close(Y.cpu().numpy(), 0.25 * ref.reshape(V, 4 * F), 0.25 * ra.reshape(V, 4 * F))
     assert ok, worst
+
+
+@pytest.mark.parametrize("V,F1,Cp", [(1000, 16, 48), (300, 64, 48), (4099, 64, 8), (129, 8, 64)])
+@pytest.mark.parametrize("tc", [True, False])
+def test_gat_rowstat_mean(gb, V, F1, Cp, tc, monkeypatch):
+    """Head-mean layer statistics S[v,h] = scale sum_i Yc[v,4i+h] (W_h dZ[v])_i
+    (tensor-core epilogue form and the SIMT kernel) packed beside er / m /
+    1/sum, vs float64."""
+    from paper_2605_29346_b200.kernels import GatRowStatCall
+
+    monkeypatch.setenv("GNN_GAT_ROWSTAT_TC", "1" if tc else "0")
+    g = torch.Generator(device="cuda").manual_seed(V + F1)
+    dZs = torch.randn(V, Cp + 16, device="cuda", generator=g)
+    dZ = dZs[:, :Cp]
+    Yc = torch.randn(V, 4 * F1, device="cuda", generator=g)
+    W = torch.randn(F1, 4 * Cp, device="cuda", generator=g)
+    er = torch.randn(V, 4, device="cuda", generator=g)
+    ms = torch.randn(V, 8, device="cuda", generator=g)
+    stat = dZs[:, Cp:]
+    call = GatRowStatCall(er, ms, stat, mean=(dZ, Yc, W, F1, Cp, 0.25))
+    assert call.tc == tc
+    call()
+    got = stat.reshape(V, 4, 4).cpu().numpy()
+    z = dZ.double().cpu().numpy()
+    y = Yc.double().cpu().numpy().reshape(V, F1, 4)
+    w = W.double().cpu().numpy().reshape(F1, 4, Cp)
+    G = np.einsum("ihc,vc->vih", w, z)
+    S = 0.25 * np.einsum("vih,vih->vh", y, G)
+    Sa = 0.25 * np.einsum("vih,vih->vh", np.abs(y), np.einsum("ihc,vc->vih", np.abs(w), np.abs(z)))
+    assert_close(got[:, :, 3], S, Sa, "S")
+    assert np.array_equal(got[:, :, 0], er.cpu().numpy())
+    assert np.array_equal(got[:, :, 1], ms[:, :4].cpu().numpy())
+    assert np.array_equal(got[:, :, 2], ms[:, 4:].cpu().numpy())
