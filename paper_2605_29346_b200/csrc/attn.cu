@@ -457,6 +457,87 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
   }
 }
 
+// Short whole rows, GAT, 4 heads: a run of consecutive rows holding at most
+// 32 edges in total (all inside the warp's chunk) is one warp step, one edge
+// per lane.  Row boundaries become a bit mask of segment heads; the row max
+// and the row sum of exponentials are segmented inclusive scans over the
+// lanes (fixed order), read back from each segment's last lane.  A row of
+// ~10 edges then costs a third of a warp step instead of a whole one.
+// Returns the number of rows consumed (>= 1: row r itself is whole and
+// at most 32 long).
+#ifndef GNN_SOFTMAX_BATCH
+#define GNN_SOFTMAX_BATCH 1
+#endif
+__device__ __forceinline__ unsigned lanes_le(int l) { return l >= 31 ? ~0u : (2u << l) - 1u; }
+
+template <bool MAX>
+__device__ __forceinline__ void seg_scan4(float (&x)[4], int lane, int ss) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float t = __shfl_up_sync(kFull, x[h], d);
+      if (lane - d >= ss) x[h] = MAX ? fmaxf(x[h], t) : x[h] + t;
+    }
+  }
+}
+
+__device__ __forceinline__ int softmax_batch_gat4(const SoftmaxArgs &a, int64_t r, int64_t bs,
+                                                  int64_t e1) {
+  const int lane = (int)lane_id();
+  const bool in = r + lane < a.R;
+  const int64_t o = a.offsets[in ? r + 1 + lane : a.R];  // row ends
+  const bool valid = in && o - bs <= 32 && o <= e1;        // a prefix of the lanes
+  const int nb = __popc(__ballot_sync(kFull, valid));
+  const int64_t be = RowWalk::shfl64(o, nb - 1);
+  const int n = (int)(be - bs);
+  int64_t os = RowWalk::shfl64(o, lane > 0 ? lane - 1 : 0);  // row starts
+  if (lane == 0) os = bs;
+  const bool ne = lane < nb && o > os;
+  const unsigned nem = __ballot_sync(kFull, ne);
+  const unsigned heads = __reduce_or_sync(kFull, ne ? 1u << (int)(os - bs) : 0u);
+  const unsigned below = heads & lanes_le(lane);
+  const int ss = below ? 31 - __clz(below) : 0;          // this edge's segment start
+  const unsigned above = heads & ~lanes_le(lane);
+  const int se = above ? __ffs(above) - 1 : n;           // its end (exclusive)
+  const int k = __popc(below) - 1;                       // segment index
+  const bool act = lane < n;
+  const int64_t row = r + (act ? __fns(nem, 0, k + 1) : 0);
+  float s[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
+  const int64_t e = bs + lane;
+  if (act) {
+    const float4 er4 = ldg_f4(a.er + row * 4);
+    const float4 l4 = ldg_f4(a.el + (int64_t)a.cols[e] * 4);
+    const float t[4] = {l4.x + er4.x, l4.y + er4.y, l4.z + er4.z, l4.w + er4.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) s[h] = t[h] > 0.f ? t[h] : a.slope * t[h];
+  }
+  float m[4] = {s[0], s[1], s[2], s[3]};
+  seg_scan4<true>(m, lane, ss);
+  const int last = se - 1 >= 0 ? se - 1 : 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) m[h] = __shfl_sync(kFull, m[h], last);
+  float ex[4], l[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    ex[h] = act ? __expf(s[h] - m[h]) : 0.f;
+    l[h] = ex[h];
+  }
+  seg_scan4<false>(l, lane, ss);
+  float inv[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) inv[h] = 1.f / __shfl_sync(kFull, l[h], last);
+  if (act) {
+    *reinterpret_cast<float4 *>(a.alpha + e * 4) =
+        make_float4(ex[0] * inv[0], ex[1] * inv[1], ex[2] * inv[2], ex[3] * inv[3]);
+    if (a.mstat && lane == ss) {
+      reinterpret_cast<float4 *>(a.mstat + row * 8)[0] = make_float4(m[0], m[1], m[2], m[3]);
+      reinterpret_cast<float4 *>(a.mstat + row * 8)[1] = make_float4(inv[0], inv[1], inv[2], inv[3]);
+    }
+  }
+  return nb;
+}
+
 // Backward of one row piece: S = sum alpha*dalpha; whole rows write
 // ds = alpha (dalpha - S) (* LeakyReLU'(pre) in GAT mode).
 template <int HM, bool GAT>
@@ -550,6 +631,16 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(SoftmaxArgs a) {
   RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
   while (true) {
     const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if constexpr (GAT && !BWD && HM == 4 && GNN_SOFTMAX_BATCH) {
+      if (a.H == 4 && rw.rs >= e0 && rw.re <= e1 && rw.re - rw.rs <= 32) {
+        const int nb = softmax_batch_gat4(a, rw.r, rw.rs, e1);
+        const int64_t r1 = rw.r + nb;
+        const int64_t end = RowWalk::shfl64(a.offsets[min(r1, a.R)], 0);
+        if (end >= e1 || r1 >= a.R) break;
+        rw = RowWalk(a.offsets, a.R, r1);
+        continue;
+      }
+    }
     if (hi > lo) {
       const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
       float *slot = a.slots + (w * 2 + (carry ? 0 : 1)) * 2 * a.H;
