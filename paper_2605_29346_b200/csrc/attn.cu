@@ -770,6 +770,45 @@ __device__ __forceinline__ void segsum_piece(const SoftmaxArgs &a, int64_t r, in
       if (h < a.H) (whole ? a.ds + r * a.H : slot)[h] = S[h];
 }
 
+// Runs of short whole rows (<= 32 edges together), 4 heads: one edge per
+// lane, a segmented sum scan, the segment's last lane writes the row (rows
+// without edges write 0).  Returns the rows consumed.
+template <bool EID>
+__device__ __forceinline__ int segsum_batch4(const SoftmaxArgs &a, int64_t r, int64_t bs, int64_t e1) {
+  const int lane = (int)lane_id();
+  const bool in = r + lane < a.R;
+  const int64_t o = a.offsets[in ? r + 1 + lane : a.R];
+  const bool valid = in && o - bs <= 32 && o <= e1;
+  const int nb = __popc(__ballot_sync(kFull, valid));
+  const int n = (int)(RowWalk::shfl64(o, nb - 1) - bs);
+  int64_t os = RowWalk::shfl64(o, lane > 0 ? lane - 1 : 0);
+  if (lane == 0) os = bs;
+  const bool ne = lane < nb && o > os;
+  const unsigned heads = __reduce_or_sync(kFull, ne ? 1u << (int)(os - bs) : 0u);
+  const unsigned below = heads & lanes_le(lane);
+  const int ss = below ? 31 - __clz(below) : 0;
+  float x[4] = {0.f, 0.f, 0.f, 0.f};
+  if (lane < n) {
+    const int64_t e = bs + lane;
+    const int64_t src = EID ? (int64_t)a.eid[e] : e;
+    const float4 v = *reinterpret_cast<const float4 *>(a.alpha_in + src * 4);
+    x[0] = v.x;
+    x[1] = v.y;
+    x[2] = v.z;
+    x[3] = v.w;
+  }
+  seg_scan4<false>(x, lane, ss);
+  // row j (< nb): its sum sits at the lane of its last edge, o_j - bs - 1
+  float t[4];
+  const int src_lane = ne ? (int)(o - bs) - 1 : 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) t[h] = __shfl_sync(kFull, x[h], src_lane);
+  if (lane < nb)
+    *reinterpret_cast<float4 *>(a.ds + (r + lane) * 4) =
+        ne ? make_float4(t[0], t[1], t[2], t[3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  return nb;
+}
+
 template <int HM, bool EID>
 __global__ void __launch_bounds__(256) segsum_rows_kernel(SoftmaxArgs a) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -778,6 +817,15 @@ __global__ void __launch_bounds__(256) segsum_rows_kernel(SoftmaxArgs a) {
   RowWalk rw(a.offsets, a.R, a.chunk_row[w]);
   while (true) {
     const int64_t lo = max(rw.rs, e0), hi = min(rw.re, e1);
+    if constexpr (HM == 4 && GNN_SOFTMAX_BATCH) {
+      if (a.H == 4 && rw.rs >= e0 && rw.re <= e1 && rw.re - rw.rs <= 32) {
+        const int64_t r1 = rw.r + segsum_batch4<EID>(a, rw.r, rw.rs, e1);
+        const int64_t end = RowWalk::shfl64(a.offsets[min(r1, a.R)], 0);
+        if (end >= e1 || r1 >= a.R) break;
+        rw = RowWalk(a.offsets, a.R, r1);
+        continue;
+      }
+    }
     if (hi > lo) {
       const bool carry = rw.rs < e0, trail = !carry && rw.re > e1;
       float *slot = a.slots + (w * 2 + (carry ? 0 : 1)) * 2 * a.H;
