@@ -1314,6 +1314,46 @@ __global__ void sample_active_scatter_kernel(const int64_t *__restrict__ pos, in
     if (i == 0) *count = pos[F] * fanout;
   }
 }
+// One thread's chunk of kDrawChunk consecutive draws p (the reference's
+// draw order: p = active-vertex rank * fanout + j): jump the PCG64 stream to
+// p0, then run the chunk in phases — all uniforms, then all vertex lookups,
+// then all degree reads, then all target reads — so each phase's loads are
+// independent and in flight together instead of one dependent chain per draw.
+__device__ __forceinline__ void draw_chunk(const int64_t *__restrict__ offsets,
+                                           const int32_t *__restrict__ targets,
+                                           const int64_t *__restrict__ frontier,
+                                           const int64_t *__restrict__ active, int64_t fanout,
+                                           U128 state0, U128 inc, int64_t p0, int64_t n,
+                                           int64_t *src, int64_t *dst) {
+  U128 s = pcg_advance(state0, inc, (uint64_t)p0);
+  double u[kDrawChunk];
+  int64_t v[kDrawChunk], base[kDrawChunk], deg[kDrawChunk];
+#pragma unroll
+  for (int k = 0; k < kDrawChunk; ++k) {
+    s = u128_add(u128_mul(s, kPcgMult), inc);
+    u[k] = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+  }
+#pragma unroll
+  for (int k = 0; k < kDrawChunk; ++k) v[k] = p0 + k < n ? frontier[active[(p0 + k) / fanout]] : 0;
+#pragma unroll
+  for (int k = 0; k < kDrawChunk; ++k) {
+    base[k] = p0 + k < n ? offsets[v[k]] : 0;
+    deg[k] = p0 + k < n ? offsets[v[k] + 1] : 0;
+  }
+  int32_t t[kDrawChunk];
+#pragma unroll
+  for (int k = 0; k < kDrawChunk; ++k) {
+    const int64_t pick = (int64_t)(u[k] * (double)(deg[k] - base[k]));  // numpy astype(int64)
+    t[k] = p0 + k < n ? targets[base[k] + pick] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kDrawChunk; ++k)
+    if (p0 + k < n) {
+      src[p0 + k] = v[k];
+      dst[p0 + k] = t[k];
+    }
+}
+
 __global__ void __launch_bounds__(256) sample_draw_kernel(
     const int64_t *__restrict__ offsets, const int32_t *__restrict__ targets,
     const int64_t *__restrict__ frontier, const int64_t *__restrict__ active,
@@ -1323,17 +1363,8 @@ __global__ void __launch_bounds__(256) sample_draw_kernel(
   const int64_t nchunks = ceil_div(n, kDrawChunk);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p0 = c * kDrawChunk, p1 = min(p0 + kDrawChunk, n);
-    U128 s = pcg_advance(state0, inc, (uint64_t)p0);
-    for (int64_t p = p0; p < p1; ++p) {
-      s = u128_add(u128_mul(s, kPcgMult), inc);
-      const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
-      const int64_t v = frontier[active[p / fanout]];
-      const int64_t base = offsets[v];
-      const int64_t pick = (int64_t)(u * (double)(offsets[v + 1] - base));  // numpy astype(int64)
-      src[p] = v;
-      dst[p] = targets[base + pick];
-    }
+    draw_chunk(offsets, targets, frontier, active, fanout, state0, inc, c * kDrawChunk, n, src,
+               dst);
   }
 }
 
@@ -1591,17 +1622,8 @@ __global__ void sample_draw_dev_kernel(const int64_t *__restrict__ offsets,
   const int64_t nchunks = ceil_div(n, kDrawChunk);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p0 = c * kDrawChunk, p1 = min(p0 + kDrawChunk, n);
-    U128 s = pcg_advance(state0, inc, (uint64_t)p0);
-    for (int64_t p = p0; p < p1; ++p) {
-      s = u128_add(u128_mul(s, kPcgMult), inc);
-      const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
-      const int64_t v = frontier[active[p / fanout]];
-      const int64_t base = offsets[v];
-      const int64_t pick = (int64_t)(u * (double)(offsets[v + 1] - base));
-      src[p] = v;
-      dst[p] = targets[base + pick];
-    }
+    draw_chunk(offsets, targets, frontier, active, fanout, state0, inc, c * kDrawChunk, n, src,
+               dst);
   }
 }
 
