@@ -999,11 +999,29 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
 __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                        int64_t nrows) {
   if (a.dev_counts) nrows = min(nrows, a.dev_counts[1]);
+  if (a.row_limit) {
+    // the list is ascending: only its prefix below the live-row limit has work
+    // (a replayed mini-batch's capacity rows past the limit are ~80% of it)
+    __shared__ int64_t s_n;
+    if (threadIdx.x == 0) {
+      const int64_t lim = *a.row_limit;
+      int64_t lo = 0, hi = nrows;
+      while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (rows[mid] < lim)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      s_n = lo;
+    }
+    __syncthreads();
+    nrows = s_n;
+  }
   const int64_t total = nrows * a.K;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / a.K, c = t % a.K;
-    if (a.row_limit && rows[i] >= *a.row_limit) continue;
     int64_t r = out_row(a, rows[i]);
     float ps = (a.epi.flags & GNN_EPI_POSTNORM) ? inv_deg(a.epi.post_deg_offsets, r) : 1.f;
     a.Y[r * a.ldy + c] = epi_scalar(0.f, r, c, a, 0.f, ps);
