@@ -998,26 +998,9 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
 
 __global__ void spmm_empty_rows_kernel(SpmmArgs a, const int32_t *__restrict__ rows,
                                        int64_t nrows) {
+  // device-count plans count only the empty rows below the live-row limit
+  // (plan_counts_kernel), the list being ascending
   if (a.dev_counts) nrows = min(nrows, a.dev_counts[1]);
-  if (a.row_limit) {
-    // the list is ascending: only its prefix below the live-row limit has work
-    // (a replayed mini-batch's capacity rows past the limit are ~80% of it)
-    __shared__ int64_t s_n;
-    if (threadIdx.x == 0) {
-      const int64_t lim = *a.row_limit;
-      int64_t lo = 0, hi = nrows;
-      while (lo < hi) {
-        const int64_t mid = lo + ((hi - lo) >> 1);
-        if (rows[mid] < lim)
-          lo = mid + 1;
-        else
-          hi = mid;
-      }
-      s_n = lo;
-    }
-    __syncthreads();
-    nrows = s_n;
-  }
   const int64_t total = nrows * a.K;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1090,10 +1073,13 @@ __global__ void plan_scatter_kernel(const int64_t *__restrict__ off, int64_t R, 
     if (r == 0) split_group_base[lo32(fa[R])] = (int32_t)lo32(fb[R]);
   }
 }
-// [num_split, num_empty, num_groups, num_short] from the scanned totals
-__global__ void plan_counts_kernel(const int64_t *fa, const int64_t *fb, int64_t R, int64_t *counts) {
+// [num_split, num_empty, num_groups, num_short] from the scanned totals; with
+// a live-row limit, num_empty counts the (ascending) empty rows below it only —
+// a replayed mini-batch's capacity rows past the limit need no epilogue
+__global__ void plan_counts_kernel(const int64_t *fa, const int64_t *fb, int64_t R,
+                                   const int64_t *row_limit, int64_t *counts) {
   counts[0] = lo32(fa[R]);
-  counts[1] = hi32(fa[R]);
+  counts[1] = hi32(fa[row_limit ? min(max(*row_limit, (int64_t)0), R) : R]);
   counts[2] = lo32(fb[R]);
   counts[3] = hi32(fb[R]);
 }
@@ -1389,7 +1375,7 @@ int gnn_spmm_plan_build_dev(const gnn_csr_view_t *A, int64_t P, int64_t short_ma
                                                          buf + L.o_empty, buf + L.o_short);
     GNN_LAUNCH_CHECK();
   }
-  plan_counts_kernel<<<1, 1, 0, st>>>(fa, fb, R, counts);
+  plan_counts_kernel<<<1, 1, 0, st>>>(fa, fb, R, row_limit, counts);
   GNN_LAUNCH_CHECK();
   // capacities: a split row spans >= 2 chunks (<= nw of them); sum over split rows
   // of ceil(partials / 64) <= num_split + (nw + num_split) / 64
