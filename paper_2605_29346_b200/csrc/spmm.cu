@@ -155,7 +155,8 @@ __device__ __forceinline__ typename VecT<VW>::T epi_vec(typename VecT<VW>::T y, 
 // (the TMA engine) while the warp reads its row bounds; the gather loop then
 // only waits on the feature loads.  U edges per group are in flight per
 // iteration (U*32/G per warp).
-enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
+enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2, STAGE_VALS4 = 3 };
+constexpr int kSub = 512;  // edges per ring sub-chunk of the nnz-split kernel
 // Where an edge's weight comes from (compile-time, so the gather loop carries
 // no per-edge mode test):
 //   WM_NONE    implicit 1 (SpMMv)
@@ -165,12 +166,21 @@ enum StageMode : int { STAGE_NONE = 0, STAGE_VALS = 1, STAGE_EID = 2 };
 //   WM_PACKED  small integer weight in the high bits of the column id (the
 //              coalesced multigraph operand: one 4-byte word per edge)
 //   WM_SHARED4 four heads over ONE shared feature row: output column 4i+h =
-//              sum_e vals[e*4+h] * X[col_e, i] (gnn_spmm_shared_heads)
+//              sum_e vals[e*4+h] * X[col_e, i] (gnn_spmm_shared_heads); the
+//              float4 of head weights per edge staged in the ring (STAGE_VALS4,
+//              128-edge sub-chunks) so no register holds it during the gathers
+//   WM_HEADS4  four heads, vals[e*4 + head] staged in the ring like WM_SHARED4's
+//              (multi-head SpMMve over its own per-head columns)
 enum WeightMode : int { WM_NONE = 0, WM_GLOBAL = 1, WM_SVALS = 2, WM_SEID = 3, WM_PACKED = 4,
-                        WM_SHARED4 = 5 };
+                        WM_SHARED4 = 5, WM_HEADS4 = 6 };
 template <int WM>
 constexpr int stage_of() {
-  return WM == WM_SVALS ? STAGE_VALS : WM == WM_SEID ? STAGE_EID : STAGE_NONE;
+  return WM == WM_SVALS ? STAGE_VALS : WM == WM_SEID ? STAGE_EID : (WM == WM_SHARED4 || WM == WM_HEADS4) ? STAGE_VALS4 : STAGE_NONE;
+}
+// edges per ring sub-chunk
+template <int WM>
+constexpr int sub_of() {
+  return (WM == WM_SHARED4 || WM == WM_HEADS4) ? 128 : kSub;
 }
 
 // Lane-invariant part of the gather: per-vector base pointers (column offset
@@ -244,6 +254,7 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
   auto weight = [&](int i, int v, int32_t p) -> float {
     if constexpr (WM == WM_PACKED) return (float)((uint32_t)p >> a.col_bits);
     if constexpr (WM == WM_SVALS) return static_cast<const float *>(sval)[i];
+    if constexpr (WM == WM_HEADS4) return static_cast<const float *>(sval)[i * 4 + lc.head[v]];
     const int64_t vi =
         WM == WM_SEID ? (int64_t) static_cast<const int32_t *>(sval)[i] : ebase + i;
     return __ldg(a.vals + vi * a.heads + lc.head[v]);
@@ -259,7 +270,7 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
 #ifndef GNN_SH4_U
 #define GNN_SH4_U 4
 #endif
-    constexpr int US = GNN_SH4_U;  // edges in flight per group (scalar gathers: cheap registers)
+    constexpr int US = GNN_SH4_U;  // edges in flight per group (weights staged: only the gathers hold registers)
     if constexpr (VPL == 4 && VW == 4) {
       // contiguous slots: one float4 gather of the lane's 4 X columns per edge,
       // 16 FMAs (4 columns x 4 heads) against the edge's float4 of head weights
@@ -271,22 +282,23 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
           ok[u] = i + u * NG < ie;
           c[u] = ok[u] ? scol[i + u * NG] : 0;
         }
-        float4 xv[US], w4[US];
+        float4 xv[US];
 #pragma unroll
-        for (int u = 0; u < US; ++u) {
+        for (int u = 0; u < US; ++u)
           xv[u] = ok[u] ? ldg_f4(reinterpret_cast<const float *>(lc.xb[0] + (uint64_t)(uint32_t)c[u] * ldxb))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
-          w4[u] = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
 #pragma unroll
         for (int u = 0; u < US; ++u) {
+          // the edge's head weights from the staged ring (broadcast within the group)
+          const float4 w4u = ok[u] ? static_cast<const float4 *>(sval)[i + u * NG]
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
           const float xs4[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
-            acc[v].x = fmaf(w4[u].x, xs4[v], acc[v].x);
-            acc[v].y = fmaf(w4[u].y, xs4[v], acc[v].y);
-            acc[v].z = fmaf(w4[u].z, xs4[v], acc[v].z);
-            acc[v].w = fmaf(w4[u].w, xs4[v], acc[v].w);
+            acc[v].x = fmaf(w4u.x, xs4[v], acc[v].x);
+            acc[v].y = fmaf(w4u.y, xs4[v], acc[v].y);
+            acc[v].z = fmaf(w4u.z, xs4[v], acc[v].z);
+            acc[v].w = fmaf(w4u.w, xs4[v], acc[v].w);
           }
         }
       }
@@ -310,7 +322,7 @@ __device__ __forceinline__ void seg_accumulate(const SpmmArgs &a, const LaneCols
       float4 w4[US];  // (the scale is applied once at the row's final store)
 #pragma unroll
       for (int u = 0; u < US; ++u)
-        w4[u] = ok[u] ? ldg_f4(a.vals + (ebase + i + u * NG) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w4[u] = ok[u] ? static_cast<const float4 *>(sval)[i + u * NG] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < US; ++u)
 #pragma unroll
@@ -506,7 +518,6 @@ __device__ __forceinline__ void split_arrive(const SpmmArgs &a, int64_t s, int64
 // engine): column ids (+ edge values or edge ids).  Row accumulators carry
 // across sub-chunk boundaries in registers; only rows crossing the warp's
 // range boundaries produce partials (split rows, finished by split_arrive).
-constexpr int kSub = 512;
 
 template <int G, int VPL, int VW, int WM, bool PEER = false>
 #ifndef GNN_SPMM_MINB
@@ -521,14 +532,16 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= a.nwarps) return;
   constexpr int stage = stage_of<WM>();
+  constexpr int SUB = sub_of<WM>();
+  constexpr int VW4 = stage == STAGE_VALS4 ? 4 : 1;              // ring words per edge value
   uint8_t *wbase = spmm_smem + (size_t)warp * a.warp_smem;
   uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);           // [2]
-  int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);       // [2][kSub]
-  int32_t *sval = scol + 2 * kSub;                               // [2][kSub] (vals or eid bits)
+  int32_t *scol = reinterpret_cast<int32_t *>(wbase + 16);       // [2][SUB]
+  int32_t *sval = scol + 2 * SUB;                                // [2][SUB * VW4] (vals or eid bits)
   const int64_t cbase = (int64_t)blockIdx.y * KB;
   const int64_t e0 = w * a.P;
   const int64_t e1 = min(e0 + a.P, a.nnz);
-  const int nsub = (int)ceil_div(e1 - e0, kSub);
+  const int nsub = (int)ceil_div(e1 - e0, SUB);
 
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -538,23 +551,26 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
   __syncwarp();
   auto issue = [&](int sc) {
     const int b = sc & 1;
-    const int64_t s0 = e0 + (int64_t)sc * kSub;
-    const int n = (int)min((int64_t)kSub, e1 - s0);
+    const int64_t s0 = e0 + (int64_t)sc * SUB;
+    const int n = (int)min((int64_t)SUB, e1 - s0);
     const int nbulk = a.bulk_ok ? (n & ~3) : 0;
-    int32_t *dc = scol + b * kSub;
-    int32_t *dv = sval + b * kSub;
+    int32_t *dc = scol + b * SUB;
+    int32_t *dv = sval + b * SUB * VW4;
     for (int i = nbulk + lane; i < n; i += 32) {
       dc[i] = a.cols[s0 + i];
       if (stage == STAGE_VALS) dv[i] = __float_as_int(a.vals[s0 + i]);
       if (stage == STAGE_EID) dv[i] = a.eid[s0 + i];
+      if (stage == STAGE_VALS4)
+        reinterpret_cast<float4 *>(dv)[i] = ldg_f4(a.vals + (s0 + i) * 4);
     }
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)nbulk * 4u;
-      mbar_arrive_expect_tx(bar + b, stage != STAGE_NONE ? 2u * bytes : bytes);
+      mbar_arrive_expect_tx(bar + b, stage != STAGE_NONE ? (1u + VW4) * bytes : bytes);
       if (bytes) {
         bulk_g2s(dc, a.cols + s0, bytes, bar + b);
         if (stage == STAGE_VALS) bulk_g2s(dv, a.vals + s0, bytes, bar + b);
         if (stage == STAGE_EID) bulk_g2s(dv, a.eid + s0, bytes, bar + b);
+        if (stage == STAGE_VALS4) bulk_g2s(dv, a.vals + s0 * 4, 4u * bytes, bar + b);
       }
     }
   };
@@ -580,8 +596,8 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
   int last_issued = 0, last_waited = -1;
   for (int sc = 0; sc < nsub && !done; ++sc) {
     const int b = sc & 1;
-    const int64_t s0 = e0 + (int64_t)sc * kSub;
-    const int64_t s1 = min(s0 + kSub, e1);
+    const int64_t s0 = e0 + (int64_t)sc * SUB;
+    const int64_t s1 = min(s0 + SUB, e1);
     if (sc + 1 < nsub) {
       issue(sc + 1);
       last_issued = sc + 1;
@@ -589,8 +605,8 @@ __global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3)
     mbar_wait(bar + b, (uint32_t)((sc >> 1) & 1));
     last_waited = sc;
     __syncwarp();
-    const int32_t *bc = scol + b * kSub;
-    const int32_t *bv = sval + b * kSub;
+    const int32_t *bc = scol + b * SUB;
+    const int32_t *bv = sval + b * SUB * VW4;
     while (true) {
       const int64_t lo = max(rs, s0), hi = min(re, s1);
       const bool is_short = re - rs <= a.short_max;  // owned by the short-row kernel
@@ -1133,6 +1149,7 @@ auto pick_wm(int wm) {
     case WM_SEID: return K<G, VPL, VW, WM_SEID, PEER>::fn;
     case WM_PACKED: return K<G, VPL, VW, WM_PACKED, PEER>::fn;
     case WM_SHARED4: return K<G, VPL, VW, WM_SHARED4, PEER>::fn;
+    case WM_HEADS4: return K<G, VPL, VW, WM_HEADS4, PEER>::fn;
     default: return K<G, VPL, VW, WM_NONE, PEER>::fn;
   }
 }
@@ -1157,6 +1174,10 @@ int launch_main(const SpmmArgs &a, int wm, cudaStream_t st) {
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool env_is_zero(const char *name) {
+  const char *v = getenv(name);
+  return v && v[0] == '0' && v[1] == 0;
+}
 
 // Per-thread, per-device side stream + fork/join events for the concurrent
 // short-row launch (GNN_SPMM_CONCURRENT=0 serialises it on the caller's stream).
@@ -1191,7 +1212,7 @@ int launch_short(const SpmmArgs &a, int wm, const gnn_spmm_plan_t *plan, cudaStr
   const int64_t warps = ceil_div(plan->num_short, NG);
   dim3 grid((unsigned)ceil_div(warps * 32, 256), (unsigned)ceil_div(a.K, KB));
   // the short kernel reads vals / eid straight from global: SVALS == GLOBAL there
-  auto kern = pick_wm<ShortKernel, G, VPL, VW, PEER>(wm == WM_SVALS ? WM_GLOBAL : wm);
+  auto kern = pick_wm<ShortKernel, G, VPL, VW, PEER>((wm == WM_SVALS || wm == WM_HEADS4) ? WM_GLOBAL : wm);
   kern<<<grid, 256, 0, st>>>(a, plan->short_rows, plan->num_short);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
@@ -1495,18 +1516,24 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
   if (plan->num_groups + plan->num_split > 0)
     GNN_CUDA_TRY(cudaMemsetAsync(
         a.cnt1, 0, sizeof(int) * (plan->num_groups + plan->num_split) * a.ncb, st));
-  a.stage = !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
+  // four heads' weights staged in the ring (float4 per edge) instead of read per lane
+  const bool heads4 = !shared && !packed && A->vals && !A->eid && heads == 4 && !peer &&
+                      aligned16(A->vals) && !env_is_zero("GNN_SPMM_HEADS4_STAGE");
+  a.stage = (shared || heads4) ? STAGE_VALS4
+                   : !A->vals ? STAGE_NONE : (A->eid ? STAGE_EID : (heads == 1 ? STAGE_VALS : STAGE_NONE));
   const int wm = shared ? WM_SHARED4
                  : packed ? WM_PACKED
                           : !A->vals ? WM_NONE
-                                     : (A->eid ? WM_SEID : (heads == 1 ? WM_SVALS : WM_GLOBAL));
+                                     : (A->eid ? WM_SEID : (heads == 1 ? WM_SVALS : heads4 ? WM_HEADS4 : WM_GLOBAL));
   a.xdiv = shared ? 4 : 1;
   a.wscale = shared ? shared_scale : 1.f;
   a.col_bits = packed ? A->col_bits : 0;
   a.col_mask = packed ? (uint32_t)((1ull << A->col_bits) - 1) : 0xffffffffu;
-  a.bulk_ok = aligned16(A->cols) && (a.stage != STAGE_VALS || aligned16(A->vals)) &&
+  a.bulk_ok = aligned16(A->cols) &&
+              ((a.stage != STAGE_VALS && a.stage != STAGE_VALS4) || aligned16(A->vals)) &&
               (a.stage != STAGE_EID || aligned16(A->eid));
-  a.warp_smem = (int)(16 + 2 * kSub * 4 * (a.stage != STAGE_NONE ? 2 : 1));
+  a.warp_smem = a.stage == STAGE_VALS4 ? (int)(16 + 2 * 128 * 4 + 2 * 128 * 16)
+                                       : (int)(16 + 2 * kSub * 4 * (a.stage != STAGE_NONE ? 2 : 1));
   // short-row kernel only where it runs several rows per warp (32/G >= 2)
   {
     const bool v4 = K % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(X) && aligned16(Y) &&
