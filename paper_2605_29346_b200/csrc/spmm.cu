@@ -523,7 +523,10 @@ template <int G, int VPL, int VW, int WM, bool PEER = false>
 #ifndef GNN_SPMM_MINB
 #define GNN_SPMM_MINB 4  // resident CTAs per SM for column blocks <= 16 wide (64 regs); wider: 3
 #endif
-__global__ void __launch_bounds__(256, (G * VPL * VW <= 16) ? GNN_SPMM_MINB : 3) spmm_main_kernel(SpmmArgs a) {
+#ifndef GNN_SPMM_MINB_KB
+#define GNN_SPMM_MINB_KB 32  // widest column block that runs at GNN_SPMM_MINB CTAs per SM
+#endif
+__global__ void __launch_bounds__(256, (G * VPL * VW <= GNN_SPMM_MINB_KB) ? GNN_SPMM_MINB : 3) spmm_main_kernel(SpmmArgs a) {
   using V = VecT<VW>;
   constexpr int KB = G * VPL * VW;
   extern __shared__ __align__(16) uint8_t spmm_smem[];
@@ -1163,7 +1166,7 @@ int launch_main(const SpmmArgs &a, int wm, cudaStream_t st) {
   // unified L1/shared array to L1 so hot feature rows stay cached.
   auto kern = pick_wm<MainKernel, G, VPL, VW, PEER>(wm);
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  constexpr int minb = (KB <= 16) ? GNN_SPMM_MINB : 3;  // resident CTAs (see the kernel)
+  constexpr int minb = (KB <= GNN_SPMM_MINB_KB) ? GNN_SPMM_MINB : 3;  // resident CTAs (see the kernel)
   const int per_sm_kb = (int)((smem * minb + 1023) / 1024);
   const int carve = per_sm_kb * 100 / 228 + 1;
   GNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
