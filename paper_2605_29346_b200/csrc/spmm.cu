@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -954,18 +955,23 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
   typename V::T acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = V::zero();
-  for (int e = 0; e < nmax; e += U) {
+  // one block of U edges per group; FULL (every group of the warp has U edges
+  // left — the common case, rows being sorted longest first) runs without the
+  // per-edge predicates, whose address / constant rematerialisation doubled
+  // the instruction count of this (issue-bound at K >= 32) loop
+  auto block = [&](int e, auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
     int32_t mine[KL];
 #pragma unroll
     for (int k = 0; k < KL; ++k) {
       const int j = gl + k * G;
-      mine[k] = (j < U && e + j < n) ? __ldg(cp + e + j) : 0;
+      mine[k] = (j < U && (FULL || e + j < n)) ? __ldg(cp + e + j) : 0;
     }
     int32_t c[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ok[u] = e + u < n;
+      ok[u] = FULL || e + u < n;
       c[u] = __shfl_sync(kFull, mine[u / G], gbase + u % G);
     }
     float pw[U];  // packed weights
@@ -1001,6 +1007,12 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
         for (int v = 0; v < VPL; ++v) acc[v] = V::add(acc[v], x[u][v]);
       }
     }
+  };
+  for (int e = 0; e < nmax; e += U) {
+    if (__all_sync(kFull, e + U <= n))
+      block(e, std::integral_constant<bool, true>());
+    else
+      block(e, std::integral_constant<bool, false>());
   }
   if (!valid) return;
   const int64_t orow = out_row(a, r);
