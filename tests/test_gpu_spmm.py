@@ -77,9 +77,17 @@ def test_spmmv_transpose_and_coalesced(gb, graphs, gname, K):
     assert_close(Ytc, oo.spmm(t_off, t_rows, X), oo.spmm(t_off, t_rows, np.abs(X)), "csc coalesced")
 
 
-@pytest.mark.parametrize("heads,F", [(1, 16), (4, 16), (2, 3), (3, 5)])
-def test_spmmve_forward_and_transpose(gb, graphs, heads, F):
-    g = graphs["pl_10k"]
+@pytest.mark.parametrize("heads,F", [(1, 16), (4, 16), (2, 3), (3, 5), (4, 8), (4, 3)])
+@pytest.mark.parametrize("gname", ["pl_10k", "mega", "pl_big"])
+def test_spmmve_forward_and_transpose(gb, graphs, heads, F, gname):
+    """Multi-head SpMMve and its transpose through the edge ids; four heads take
+    the staged-weights path (WM_HEADS4) of the nnz-split kernel, on row-order
+    (pl_10k, mega: split and empty rows) and degree-sorted (pl_big, >= 2^20
+    entries) operands."""
+    if gname == "pl_big" and "pl_big" not in graphs:
+        graphs["pl_big"] = gb.generate(gb.GraphGenSpec("power-law", 40_000, 1_500_000,
+                                                       exponent=2.1), 11)
+    g = graphs[gname]
     off, tgt = host(g)
     t_off, t_rows, eid = og.transpose(g.num_vertices, g.num_vertices, off, tgt)
     rng = np.random.default_rng(heads * 10 + F)
