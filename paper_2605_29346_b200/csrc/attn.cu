@@ -352,6 +352,92 @@ __device__ __forceinline__ void warp_max_reduce(float (&t)[HM]) {
   }
 }
 
+// GAT, 4 heads, rows longer than a warp: two passes instead of three, each
+// with 4 edges per lane in flight (column ids first, then the four el rows —
+// the dependent id -> el chain is paid once per 4 edges).  Pass 1 keeps a
+// per-lane online (max, sum): l <- s > m ? l e^(m-s) + 1 : l + e^(s-m), one
+// exponential per edge and head, merged by a fixed xor tree; pass 2 (whole
+// rows) writes alpha = e^(s-m) / l.
+#ifndef GNN_SOFTMAX_ONLINE
+#define GNN_SOFTMAX_ONLINE 1
+#endif
+constexpr int kSmU = 4;
+
+__device__ __forceinline__ void gat4_scores(const SoftmaxArgs &a, int64_t e0, int64_t hi,
+                                            const float (&erow)[4], float (&s)[kSmU][4]) {
+  int32_t c[kSmU];
+#pragma unroll
+  for (int u = 0; u < kSmU; ++u) c[u] = e0 + 32 * u < hi ? a.cols[e0 + 32 * u] : -1;
+#pragma unroll
+  for (int u = 0; u < kSmU; ++u) {
+    const float4 l = c[u] >= 0 ? ldg_f4(a.el + (int64_t)c[u] * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float t[4] = {l.x + erow[0], l.y + erow[1], l.z + erow[2], l.w + erow[3]};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) s[u][h] = t[h] > 0.f ? t[h] : a.slope * t[h];
+  }
+}
+
+__device__ __forceinline__ void gat4_write_alpha(const SoftmaxArgs &a, int64_t lo, int64_t hi,
+                                                 const float (&erow)[4], const float (&m)[4],
+                                                 const float (&inv)[4]) {
+  const int lane = (int)lane_id();
+  for (int64_t e0 = lo + lane; e0 < hi; e0 += 32 * kSmU) {
+    float s[kSmU][4];
+    gat4_scores(a, e0, hi, erow, s);
+#pragma unroll
+    for (int u = 0; u < kSmU; ++u)
+      if (e0 + 32 * u < hi)
+        *reinterpret_cast<float4 *>(a.alpha + (e0 + 32 * u) * 4) =
+            make_float4(__expf(s[u][0] - m[0]) * inv[0], __expf(s[u][1] - m[1]) * inv[1],
+                        __expf(s[u][2] - m[2]) * inv[2], __expf(s[u][3] - m[3]) * inv[3]);
+  }
+}
+
+__device__ __forceinline__ void softmax_piece_gat4(const SoftmaxArgs &a, int64_t r, int64_t lo,
+                                                   int64_t hi, bool whole, float *slot,
+                                                   const float (&erow)[4]) {
+  const int lane = (int)lane_id();
+  float m[4], l[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    m[h] = kNegInf;
+    l[h] = 0.f;
+  }
+  for (int64_t e0 = lo + lane; e0 < hi; e0 += 32 * kSmU) {
+    float s[kSmU][4];
+    gat4_scores(a, e0, hi, erow, s);
+#pragma unroll
+    for (int u = 0; u < kSmU; ++u)
+      if (e0 + 32 * u < hi)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float d = s[u][h] - m[h];
+          const float t = __expf(-fabsf(d));  // e^(m-s) when s > m (m = -inf: 0)
+          const bool up = d > 0.f;
+          l[h] = up ? fmaf(l[h], t, 1.f) : l[h] + t;
+          m[h] = up ? s[u][h] : m[h];
+        }
+  }
+  warp_ml_reduce<4>(m, l);
+  if (!whole) {
+    if (lane == 0)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        slot[h] = m[h];
+        slot[4 + h] = l[h];
+      }
+    return;
+  }
+  float inv[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) inv[h] = 1.f / l[h];
+  if (a.mstat && lane == 0) {
+    reinterpret_cast<float4 *>(a.mstat + r * 8)[0] = make_float4(m[0], m[1], m[2], m[3]);
+    reinterpret_cast<float4 *>(a.mstat + r * 8)[1] = make_float4(inv[0], inv[1], inv[2], inv[3]);
+  }
+  gat4_write_alpha(a, lo, hi, erow, m, inv);
+}
+
 template <int HM, bool GAT>
 __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, int64_t lo, int64_t hi,
                                               bool whole, float *slot) {
@@ -407,6 +493,12 @@ __device__ __forceinline__ void softmax_piece(const SoftmaxArgs &a, int64_t r, i
       }
     }
     return;
+  }
+  if constexpr (GAT && HM == 4 && GNN_SOFTMAX_ONLINE) {
+    if (a.H == 4) {
+      softmax_piece_gat4(a, r, lo, hi, whole, slot, erow);
+      return;
+    }
   }
   for (int64_t e = lo + lane; e < hi; e += 32) {
     float s[HM];
@@ -728,6 +820,12 @@ __global__ void __launch_bounds__(256) softmax_split_apply_kernel(SoftmaxArgs a)
     float inv[HM];
 #pragma unroll
     for (int h = 0; h < HM; ++h) inv[h] = 1.f / l[h];
+    if constexpr (GAT && HM == 4 && GNN_SOFTMAX_ONLINE) {
+      if (a.H == 4) {
+        gat4_write_alpha(a, lo, hi, erow, m, inv);
+        continue;
+      }
+    }
     for (int64_t e = lo + lane; e < hi; e += 32) {
       float s[HM];
       load_scores<HM, GAT>(a, e, erow, s);
