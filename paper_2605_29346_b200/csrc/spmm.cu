@@ -1008,8 +1008,10 @@ __global__ void __launch_bounds__(256, 4) spmm_short_rows_kernel(SpmmArgs a, con
       }
     }
   };
+  // (column blocks >= 32 wide only: at 16 the loop is L1-bound, not issue-bound,
+  // and the extra vote cost ~1% on the papers100M shape)
   for (int e = 0; e < nmax; e += U) {
-    if (__all_sync(kFull, e + U <= n))
+    if (KB >= 32 && __all_sync(kFull, e + U <= n))
       block(e, std::integral_constant<bool, true>());
     else
       block(e, std::integral_constant<bool, false>());
