@@ -455,15 +455,26 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(int64_t M, int64_t C,
   float lsum = 0.f;
   const int64_t rows_per_cta = 8 * 16;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-  for (int64_t r = r0 + warp; r < min(M, r0 + rows_per_cta); r += 8) {
-    const float *z = Z + r * ldz;
-    const int64_t y = __ldg(labels + r);
-    float v[NPL];
+  // the next row's logits and label are loaded before this row is reduced, so a
+  // warp's 16 rows cost one memory round trip each only at the start
+  const int64_t r_end = min(M, r0 + rows_per_cta);
+  float vn[NPL];
+  int64_t yn = 0;
+  auto load_row = [&](int64_t r) {
+    yn = r < r_end ? __ldg(labels + r) : 0;
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
       const int64_t c = lane + 32 * j;
-      v[j] = c < C ? __ldg(z + c) : -INFINITY;
+      vn[j] = (r < r_end && c < C) ? __ldg(Z + r * ldz + c) : -INFINITY;
     }
+  };
+  load_row(r0 + warp);
+  for (int64_t r = r0 + warp; r < r_end; r += 8) {
+    float v[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) v[j] = vn[j];
+    const int64_t y = yn;
+    load_row(r + 8);
     float mx = v[0];
 #pragma unroll
     for (int j = 1; j < NPL; ++j) mx = fmaxf(mx, v[j]);
