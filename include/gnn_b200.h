@@ -485,6 +485,16 @@ int gnn_gat_rowstat_mean_tc(int64_t V, int64_t F1, int64_t Cp, const float *dZ, 
                             const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
                             const float *er, const float *rowstat, float *stat, int64_t ldst,
                             void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* GAT concatenated-heads layer, the GEMM feeding its recompute backward:
+ *   C[r, c] = (A Bt^T)[r, c] * (Y[r, c] > 0)                    (ReLU backward)
+ *   C[r, N + 4h .. N + 4h + 3] = {er[r,h], m[r,h], inv[r,h], S[r,h]},
+ *   S[r,h] = sum over head h's N/4 columns of C[r, c] * (Y[r, c] - bias[c])
+ * (the gnn_gat_rowstat statistics) in the tcgen05 GEMM's epilogue.  Bt [N, Kd]
+ * row-major, N in {64, 128}, ldc >= N + 16; workspace gnn_gemm_workspace(M, N, Kd, 0). */
+int gnn_gemm_gat_relu_stat(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda,
+                           const float *Bt, int64_t ldb, float *C, int64_t ldc, const float *Y,
+                           int64_t ldy, const float *bias, const float *er, const float *rowstat,
+                           void *ws, size_t ws_bytes, gnn_stream_t stream);
 /* One pass over the CSC (AT with its edge-ID array): edge (v -> u) recomputes
  * alpha_h = exp(LeakyReLU(el[u,h] + er[v,h]) - m[v,h]) * inv[v,h] and forms
  *   dWh[u,:]  = sum alpha_h dY[v, head h cols]          (SpMMve^T)

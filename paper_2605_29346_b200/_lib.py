@@ -265,6 +265,9 @@ SIGNATURES = {
     "gnn_gat_rowstat_mean_tc": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
                                         c_i64, C.c_float, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_sz,
                                         c_ptr]),
+    "gnn_gemm_gat_relu_stat": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
+                                       c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_sz,
+                                       c_ptr]),
     "gnn_gat_bwd_rc_workspace": (c_sz, [C.POINTER(SpmmPlan), c_i64]),
     "gnn_gat_bwd_rc": (
         c_int,

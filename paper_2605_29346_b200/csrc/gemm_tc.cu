@@ -56,6 +56,12 @@ struct TcArgs {
   float *dotS;
   int64_t ldS, dot_hs;
   int dot_acc;  // add to S (a later column block) instead of overwriting it
+  // GAT concatenated-heads backward epilogue (EPI_GAT): with G = the product row,
+  // C[r, c] = G[r, c] * (Y[r, c] > 0) (ReLU backward) and C[r, N + 4h .. 4h + 3] =
+  // {er[r, h], m[r, h], inv[r, h], S[r, h]}, S[r, h] = sum over head h's F = N/4
+  // columns of C[r, c] * (Y[r, c] - bias[c])  (the recompute backward's row stats)
+  const float *gY, *gbias, *ger, *grs;
+  int64_t ldgy;
 };
 
 template <int NPAD>
@@ -63,7 +69,8 @@ constexpr size_t tc_smem_bytes() {
   return (size_t)tc_stages<NPAD>() * (2 * kTcM * kTcBK + 2 * NPAD * kTcBK) * 4 + 1024 + 1024;
 }
 
-template <int NPAD, bool DOT = false>
+constexpr int EPI_PLAIN = 0, EPI_DOT = 1, EPI_GAT = 2;
+template <int NPAD, int EPI = EPI_PLAIN>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                 const __grid_constant__ CUtensorMap tmBhi,
                                                                 const __grid_constant__ CUtensorMap tmBlo,
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
       const int64_t row = t * kTcM + q * 32 + lane;
       float *crow = p.C + row * p.ldc;
       float4 dacc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if constexpr (DOT) {
+      if constexpr (EPI == EPI_DOT) {
         // row-dot epilogue: the row's Y slice is fetched 64 columns at a time
         // (16 loads in flight per thread) ahead of the TMEM reads it meets
         constexpr int kDR = NPAD < 64 ? NPAD : 64;
@@ -244,7 +251,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
           }
         }
       }
-      for (int c0 = 0; c0 < NPAD && !DOT; c0 += 16) {
+      if constexpr (EPI == EPI_GAT) {
+        // ReLU backward + per-head row statistics; F = N / 4 columns per head, a
+        // multiple of 16 (each 16-column chunk lies in one head)
+        float S[4] = {0.f, 0.f, 0.f, 0.f};
+        const int F = (int)(p.N >> 2);
+        for (int c0 = 0; c0 < p.N; c0 += 16) {
+          uint32_t v[16], u[16];
+          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
+          tmem_ld16(taddr, v);
+          tmem_ld16(taddr + NPAD, u);
+          float4 y4[4], b4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            y4[j] = row < p.M ? ldg_f4(p.gY + row * p.ldgy + c0 + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            b4[j] = ldg_f4(p.gbias + c0 + 4 * j);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float sh = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float yv[4] = {y4[j].x, y4[j].y, y4[j].z, y4[j].w};
+            const float bv[4] = {b4[j].x, b4[j].y, b4[j].z, b4[j].w};
+            float mv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float gv = __uint_as_float(v[4 * j + t]) + __uint_as_float(u[4 * j + t]);
+              mv[t] = yv[t] > 0.f ? gv : 0.f;
+              sh = fmaf(mv[t], yv[t] - bv[t], sh);
+            }
+            if (row < p.M)
+              *reinterpret_cast<float4 *>(crow + c0 + 4 * j) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+          }
+          const int h = c0 / F;
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh) S[hh] += hh == h ? sh : 0.f;
+        }
+        if (row < p.M) {
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh)
+            *reinterpret_cast<float4 *>(crow + p.N + 4 * hh) =
+                make_float4(__ldg(p.ger + row * 4 + hh), __ldg(p.grs + row * 8 + hh),
+                            __ldg(p.grs + row * 8 + 4 + hh), S[hh]);
+        }
+      }
+      for (int c0 = 0; c0 < NPAD && EPI == EPI_PLAIN; c0 += 16) {
         uint32_t v[16], u[16];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
         tmem_ld16(taddr, v);
@@ -275,7 +326,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
           }
         }
       }
-      if (DOT && row < p.M) {
+      if (EPI == EPI_DOT && row < p.M) {
         float *sr = p.dotS + row * p.ldS;
         const float d[4] = {dacc.x, dacc.y, dacc.z, dacc.w};
 #pragma unroll
@@ -653,14 +704,14 @@ bool map_2d(CUtensorMap *tm, const float *base, int64_t inner, int64_t outer, in
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NPAD, bool DOT = false>
+template <int NPAD, int EPI = EPI_PLAIN>
 int launch_tc(const CUtensorMap &ta, const CUtensorMap &tbh, const CUtensorMap &tbl,
               const TcArgs &p, cudaStream_t st) {
   const size_t smem = tc_smem_bytes<NPAD>();
-  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<NPAD, DOT>,
+  GNN_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel<NPAD, EPI>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = p.mtiles < sm_count() ? p.mtiles : sm_count();
-  gemm_tc_kernel<NPAD, DOT><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tbh, tbl, p);
+  gemm_tc_kernel<NPAD, EPI><<<(unsigned)grid, kTcThreads, smem, st>>>(ta, tbh, tbl, p);
   GNN_LAUNCH_CHECK();
   return GNN_OK;
 }
@@ -756,14 +807,54 @@ int gemm_tc_rowdot(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
     p.dot_acc = n0 > 0;
     int rc;
     switch (npad) {
-      case 16: rc = launch_tc<16, true>(ta, tbh, tbl, p, st); break;
-      case 32: rc = launch_tc<32, true>(ta, tbh, tbl, p, st); break;
-      case 64: rc = launch_tc<64, true>(ta, tbh, tbl, p, st); break;
-      default: rc = launch_tc<128, true>(ta, tbh, tbl, p, st); break;
+      case 16: rc = launch_tc<16, EPI_DOT>(ta, tbh, tbl, p, st); break;
+      case 32: rc = launch_tc<32, EPI_DOT>(ta, tbh, tbl, p, st); break;
+      case 64: rc = launch_tc<64, EPI_DOT>(ta, tbh, tbl, p, st); break;
+      default: rc = launch_tc<128, EPI_DOT>(ta, tbh, tbl, p, st); break;
     }
     if (rc != GNN_OK) return rc;
   }
   return GNN_OK;
+}
+
+// GAT concatenated-heads backward GEMM: dYm = relu'(Y) * (A Bt^T) with the
+// per-head row statistics written after each row's N columns (EPI_GAT above).
+// N = 4F, F % 16 == 0, N <= 128; C rows hold N + 16 floats.
+int gemm_tc_gat_relu_stat(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
+                          const float *Bt, int64_t ldb, float *C, int64_t ldc, const float *Y,
+                          int64_t ldy, const float *bias, const float *er, const float *rowstat,
+                          void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (N % 64 || N > 128 || ldc < N + 16 || ldc % 4 || ldy % 4 || !gemm_tc_supported(M, N, K, A, lda, 0) ||
+      (reinterpret_cast<uintptr_t>(C) & 15u) || (reinterpret_cast<uintptr_t>(Y) & 15u) ||
+      (reinterpret_cast<uintptr_t>(bias) & 15u))
+    return GNN_ERR_UNSUPPORTED;
+  const int npad = tc_npad(N);
+  const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
+  if (ws_bytes < gemm_tc_workspace(N, K)) return GNN_ERR_WORKSPACE;
+  float *bhi = static_cast<float *>(ws);
+  float *blo = bhi + (size_t)npad * kpad;
+  split_b_kernel<<<(unsigned)ceil_div((int64_t)npad * kpad, 256), 256, 0, st>>>(Bt, ldb, 1, N, K, npad,
+                                                                              kpad, bhi, blo);
+  GNN_LAUNCH_CHECK();
+  CUtensorMap ta, tbh, tbl;
+  if (!map_2d_sw128(&ta, A, K, M, lda, kTcM) || !map_2d_sw128(&tbh, bhi, kpad, npad, kpad, npad) ||
+      !map_2d_sw128(&tbl, blo, kpad, npad, kpad, npad))
+    return GNN_ERR_UNSUPPORTED;
+  TcArgs p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Npad = npad;
+  p.nkb = (int)(kpad / kTcBK);
+  p.mtiles = ceil_div(M, kTcM);
+  p.C = C;
+  p.ldc = ldc;
+  p.gY = Y;
+  p.ldgy = ldy;
+  p.gbias = bias;
+  p.ger = er;
+  p.grs = rowstat;
+  return npad == 64 ? launch_tc<64, EPI_GAT>(ta, tbh, tbl, p, st) : launch_tc<128, EPI_GAT>(ta, tbh, tbl, p, st);
 }
 
 // ---- A^T B (weight gradient) on tcgen05

@@ -561,6 +561,29 @@ class GatRowStatCall:
                 self.stat.data_ptr(), self.stat.stride(0), st), "gat_rowstat_mean")
 
 
+class GatReluStatGemmCall:
+    """dYm = ReLU'(Y) * (A W^T) with the recompute backward's per-head row
+    statistics {er, m, 1/sum, S} written after each row's N columns, in the
+    tcgen05 GEMM's epilogue (gnn_gemm_gat_relu_stat): the GAT hidden layer's
+    dY = dWh2 W2^T, its ReLU backward and its statistics in one pass."""
+
+    def __init__(self, A, Wt, dYms, Y, bias, er, rowstat):
+        self.lib = _lib.lib()
+        self.dev = A.device
+        self.M, self.Kd = int(A.shape[0]), int(A.shape[1])
+        self.N = int(Wt.shape[0])
+        self.t = (A, Wt, dYms, Y, bias, er, rowstat)
+        self.ws = _lib.workspace(self.lib.gnn_gemm_workspace(self.M, self.N, self.Kd, 0), self.dev)
+
+    def __call__(self):
+        A, Wt, C_, Y, bias, er, rs = self.t
+        _lib.check(self.lib.gnn_gemm_gat_relu_stat(
+            self.M, self.N, self.Kd, A.data_ptr(), A.stride(0), Wt.data_ptr(), Wt.stride(0),
+            C_.data_ptr(), C_.stride(0), Y.data_ptr(), Y.stride(0), bias.data_ptr(), er.data_ptr(),
+            rs.data_ptr(), self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+            "gemm_gat_relu_stat")
+
+
 class GatBwdRcCall:
     """GAT backward over the CSC with alpha recomputed from the row statistics
     (gnn_gat_bwd_rc / _mean): dWh, del and ds (CSR edge order) in one pass.

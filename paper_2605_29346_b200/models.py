@@ -943,8 +943,9 @@ class GATTrainer(_FusedEpoch):
     def __init__(self, g: CsrGraph, in_feats: int, hidden: int, classes: int, heads: int = 4, *,
                  lr=0.01, slope=0.2, seed: int = 0):
         from .kernels import (AttnProjBwdCall, AttnProjCall, ColsumCall, EdgeSoftmaxCall,
-                              GatBwdCscCall, GatBwdCscMeanCall, GatBwdRcCall, GatRowStatCall,
-                              GatSoftmaxStatsCall, HeadMeanCall, SegmentSumCall, SharedHeadsCall)
+                              GatBwdCscCall, GatBwdCscMeanCall, GatBwdRcCall, GatReluStatGemmCall,
+                              GatRowStatCall, GatSoftmaxStatsCall, HeadMeanCall, SegmentSumCall,
+                              SharedHeadsCall)
 
         self.g = g
         dev = g.device
@@ -1071,12 +1072,22 @@ class GATTrainer(_FusedEpoch):
         k["proj2_bwd"] = AttnProjBwdCall(self.Wh2, self.al2, self.ar2, self.del_, self.der,
                                          self.dWh2, self.dal2, self.dar2, H)
         k["Y1^T.dWh2"] = GemmCall(self.Y1, self.dWh2, self.dW2, trans_a=True)
-        k["dWh2.W2^T"] = GemmCall(self.dWh2, self.W2, self.dY1, trans_b=True)
-        # backward, layer 1
-        k["relu1_bwd"] = MaskNormColsumCall(self.dY1, self.dY1m, mask=self.Y1, colsum=self.db1)
+        # hidden layer's gradient: with the recompute backward and 16-column heads,
+        # the GEMM's epilogue applies the ReLU backward and writes the row statistics
+        # the CSC pass gathers (gnn_gemm_gat_relu_stat) — dY1 never stored
+        self.fr = (self.rc and K1 in (64, 128) and os.environ.get("GNN_GAT_FUSED_STAT", "1") != "0")
+        if self.fr:
+            k["dWh2.W2^T"] = GatReluStatGemmCall(self.dWh2, self.W2, self._dY1ms, self.Y1, self.b1,
+                                                 self.er1, self.rowstat1)
+            k["db1"] = ColsumCall(self.dY1m, self.db1)
+        else:
+            k["dWh2.W2^T"] = GemmCall(self.dWh2, self.W2, self.dY1, trans_b=True)
+            # backward, layer 1
+            k["relu1_bwd"] = MaskNormColsumCall(self.dY1, self.dY1m, mask=self.Y1, colsum=self.db1)
         if self.rc:
-            k["stat1"] = GatRowStatCall(self.er1, self.rowstat1, self._dY1ms[:, K1:],
-                                        dYm=self.dY1m, Y=self.Y1, bias=self.b1)
+            if not self.fr:
+                k["stat1"] = GatRowStatCall(self.er1, self.rowstat1, self._dY1ms[:, K1:],
+                                            dYm=self.dY1m, Y=self.Y1, bias=self.b1)
             k["bagg1+sddmm1"] = GatBwdRcCall(AT, self.el1, self.dY1m, self.Wh1, self.dWh1,
                                              self.del_, self.ds, slope=slope)
             k["der1"] = SegmentSumCall(A, self.ds, self.der, H)

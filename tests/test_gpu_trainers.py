@@ -48,19 +48,22 @@ def _check(tr, ref):
 @pytest.mark.parametrize("gname", ["cora_pl", "mega"])
 @pytest.mark.parametrize("classes", [7, 8])
 @pytest.mark.parametrize("rc", [True, False])
-def test_gat_trainer_matches_oracle(env, gname, classes, rc, monkeypatch):
+@pytest.mark.parametrize("Hd", [8, 16])
+def test_gat_trainer_matches_oracle(env, gname, classes, rc, Hd, monkeypatch):
     """rc: the backward recomputes alpha from the forward softmax's row
     statistics (gnn_gat_bwd_rc / _mean, the default); else the fused CSC
-    kernel reading alpha through the edge-ID array + softmax backward."""
+    kernel reading alpha through the edge-ID array + softmax backward.  With
+    rc and 16-column heads the hidden layer's dWh2 W2^T GEMM applies the ReLU
+    backward and writes the row statistics in its epilogue."""
     from paper_2605_29346_b200.models import GATTrainer
 
     gb, graphs = env
     g = graphs[gname]
-    V, F, Hd, H = g.num_vertices, 50, 8, 4
+    V, F, H = g.num_vertices, 50, 4
     X, y = _inputs(V, F, classes)
     monkeypatch.setenv("GNN_GAT_RC", "1" if rc else "0")
     tr = GATTrainer(g, F, Hd, classes, heads=H, seed=3)
-    assert tr.rc == rc
+    assert tr.rc == rc and tr.fr == (rc and Hd == 16)
     tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
     tr.forward_backward()
     torch.cuda.synchronize()
