@@ -485,6 +485,14 @@ int gnn_gat_rowstat_mean_tc(int64_t V, int64_t F1, int64_t Cp, const float *dZ, 
                             const float *Yc, int64_t ldc, const float *W, int64_t ldw, float scale,
                             const float *er, const float *rowstat, float *stat, int64_t ldst,
                             void *ws, size_t ws_bytes, gnn_stream_t stream);
+/* GAT layer transform with its attention projections in the tcgen05 GEMM's
+ * epilogue: C = A B (B [Kd, N] row-major, N = 4F, F % 16 == 0), el[r, h] =
+ * <C[r, hF:(h+1)F], a_l[h]>, er[r, h] = <C[r, hF:(h+1)F], a_r[h]> (a_l / a_r
+ * [4, F] contiguous; el / er [M, 4]).  Workspace gnn_gemm_workspace(M, N, Kd, 0). */
+int gnn_gemm_gat_proj(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda,
+                      const float *B, int64_t ldb, float *C, int64_t ldc, int64_t F,
+                      const float *a_l, const float *a_r, float *el, float *er, void *ws,
+                      size_t ws_bytes, gnn_stream_t stream);
 /* GAT concatenated-heads layer, the GEMM feeding its recompute backward:
  *   C[r, c] = (A Bt^T)[r, c] * (Y[r, c] > 0)                    (ReLU backward)
  *   C[r, N + 4h .. N + 4h + 3] = {er[r,h], m[r,h], inv[r,h], S[r,h]},

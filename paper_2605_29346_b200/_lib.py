@@ -265,6 +265,8 @@ SIGNATURES = {
     "gnn_gat_rowstat_mean_tc": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
                                         c_i64, C.c_float, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_sz,
                                         c_ptr]),
+    "gnn_gemm_gat_proj": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_i64,
+                                  c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_sz, c_ptr]),
     "gnn_gemm_gat_relu_stat": (c_int, [c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_ptr,
                                        c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_sz,
                                        c_ptr]),

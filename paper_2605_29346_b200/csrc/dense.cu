@@ -194,6 +194,9 @@ int gcn_head_tc(int64_t M, int64_t Din, int64_t C, const float *P, int64_t ldp, 
 // tcgen05 tensor-core path (gemm_tc.cu)
 bool gemm_tc_supported(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, int trans_a);
 size_t gemm_tc_workspace(int64_t N, int64_t K);
+int gemm_tc_gat_proj(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+                     int64_t ldb, float *C, int64_t ldc, int F, const float *al, const float *ar,
+                     float *el, float *er, void *ws, size_t ws_bytes, cudaStream_t st);
 int gemm_tc_gat_relu_stat(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
                           const float *Bt, int64_t ldb, float *C, int64_t ldc, const float *Y,
                           int64_t ldy, const float *bias, const float *er, const float *rowstat,
@@ -316,6 +319,18 @@ static int gemm_impl(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t l
   if (rows_dev) return GNN_ERR_UNSUPPORTED;
   return gemm_simt(M, N, Kd, A, lda, trans_a, B, ldb, trans_b, C, ldc, bias, relu, ws, ws_bytes,
                    st);
+}
+
+int gnn_gemm_gat_proj(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda,
+                      const float *B, int64_t ldb, float *C, int64_t ldc, int64_t F,
+                      const float *a_l, const float *a_r, float *el, float *er, void *ws,
+                      size_t ws_bytes, gnn_stream_t stream) {
+  if (M < 0 || N <= 0 || Kd <= 0 || F <= 0 || !A || !B || !C || !a_l || !a_r || !el || !er ||
+      ldb < N || ldc < N)
+    return GNN_ERR_INVALID_ARGUMENT;
+  if (M == 0) return GNN_OK;
+  return gemm_tc_gat_proj(M, N, Kd, A, lda, B, ldb, C, ldc, (int)F, a_l, a_r, el, er, ws,
+                          ws_bytes, as_stream(stream));
 }
 
 int gnn_gemm_gat_relu_stat(int64_t M, int64_t N, int64_t Kd, const float *A, int64_t lda,

@@ -62,6 +62,14 @@ struct TcArgs {
   // columns of C[r, c] * (Y[r, c] - bias[c])  (the recompute backward's row stats)
   const float *gY, *gbias, *ger, *grs;
   int64_t ldgy;
+  // GAT attention projections epilogue (EPI_PROJ): with C stored as usual, for
+  // the 4 heads of width pF (a multiple of 16) el[r, h] (+)= sum_c C[r, c] al[c0g + c],
+  // er likewise, over this column block [pn0, pn0 + N) of the full row (flat
+  // [4 * pF] attention vectors); a head begun by an earlier block accumulates
+  const float *pal, *par;
+  float *pel, *per;
+  int pF;
+  int64_t pn0;
 };
 
 template <int NPAD>
@@ -69,7 +77,7 @@ constexpr size_t tc_smem_bytes() {
   return (size_t)tc_stages<NPAD>() * (2 * kTcM * kTcBK + 2 * NPAD * kTcBK) * 4 + 1024 + 1024;
 }
 
-constexpr int EPI_PLAIN = 0, EPI_DOT = 1, EPI_GAT = 2;
+constexpr int EPI_PLAIN = 0, EPI_DOT = 1, EPI_GAT = 2, EPI_PROJ = 3;
 template <int NPAD, int EPI = EPI_PLAIN>
 __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                 const __grid_constant__ CUtensorMap tmBhi,
@@ -295,7 +303,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
                             __ldg(p.grs + row * 8 + 4 + hh), S[hh]);
         }
       }
-      for (int c0 = 0; c0 < NPAD && EPI == EPI_PLAIN; c0 += 16) {
+      float pl[4] = {0.f, 0.f, 0.f, 0.f}, pr[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int c0 = 0; c0 < NPAD && (EPI == EPI_PLAIN || EPI == EPI_PROJ); c0 += 16) {
         uint32_t v[16], u[16];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * kAcc + c0);
         tmem_ld16(taddr, v);
@@ -313,6 +322,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
             *reinterpret_cast<float4 *>(crow + c0 + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+          if constexpr (EPI == EPI_PROJ) {
+            const int64_t cg = p.pn0 + c0;     // the chunk's first column of the full row
+            const int h = (int)(cg / p.pF);    // one head per 16-column chunk
+            float sl = 0.f, sr = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              sl = fmaf(y[j], __ldg(p.pal + cg + j), sl);
+              sr = fmaf(y[j], __ldg(p.par + cg + j), sr);
+            }
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+              pl[hh] += hh == h ? sl : 0.f;
+              pr[hh] += hh == h ? sr : 0.f;
+            }
+          }
         } else if (row < p.M) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -325,6 +349,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const __grid_con
             }
           }
         }
+      }
+      if (EPI == EPI_PROJ && row < p.M) {
+        // heads this block touches: [pn0 / pF, (pn0 + N - 1) / pF]; one begun by an
+        // earlier block (its first column < pn0) accumulates
+        const int h0 = (int)(p.pn0 / p.pF), h1 = (int)((p.pn0 + p.N - 1) / p.pF);
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh)
+          if (hh >= h0 && hh <= h1) {
+            const bool acc = (int64_t)hh * p.pF < p.pn0;
+            p.pel[row * 4 + hh] = acc ? p.pel[row * 4 + hh] + pl[hh] : pl[hh];
+            p.per[row * 4 + hh] = acc ? p.per[row * 4 + hh] + pr[hh] : pr[hh];
+          }
       }
       if (EPI == EPI_DOT && row < p.M) {
         float *sr = p.dotS + row * p.ldS;
@@ -811,6 +847,58 @@ int gemm_tc_rowdot(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda,
       case 32: rc = launch_tc<32, EPI_DOT>(ta, tbh, tbl, p, st); break;
       case 64: rc = launch_tc<64, EPI_DOT>(ta, tbh, tbl, p, st); break;
       default: rc = launch_tc<128, EPI_DOT>(ta, tbh, tbl, p, st); break;
+    }
+    if (rc != GNN_OK) return rc;
+  }
+  return GNN_OK;
+}
+
+// GAT layer transform with the attention projections in the epilogue:
+// C = A B (B [K, N] row-major, N = 4F, F % 16 == 0, 16-byte aligned C rows),
+// el[r, h] = <C[r, hF:(h+1)F], al[h]>, er likewise (al / ar flat [4F]);
+// 128-column blocks, heads straddling two blocks accumulate in block order.
+int gemm_tc_gat_proj(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+                     int64_t ldb, float *C, int64_t ldc, int F, const float *al, const float *ar,
+                     float *el, float *er, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (N != 4 * (int64_t)F || F % 16 || ldc % 4 || (reinterpret_cast<uintptr_t>(C) & 15u) ||
+      !gemm_tc_supported(M, 128, K, A, lda, 0))
+    return GNN_ERR_UNSUPPORTED;
+  for (int64_t n0 = 0; n0 < N; n0 += 128) {
+    const int64_t nb = N - n0 < 128 ? N - n0 : 128;
+    const int npad = tc_npad(nb);
+    const int64_t kpad = ceil_div(K, kTcBK) * kTcBK;
+    if (ws_bytes < gemm_tc_workspace(nb, K)) return GNN_ERR_WORKSPACE;
+    float *bhi = static_cast<float *>(ws);
+    float *blo = bhi + (size_t)npad * kpad;
+    split_b_kernel<<<(unsigned)ceil_div((int64_t)npad * kpad, 256), 256, 0, st>>>(
+        B + n0, ldb, 0, nb, K, npad, kpad, bhi, blo);
+    GNN_LAUNCH_CHECK();
+    CUtensorMap ta, tbh, tbl;
+    if (!map_2d_sw128(&ta, A, K, M, lda, kTcM) || !map_2d_sw128(&tbh, bhi, kpad, npad, kpad, npad) ||
+        !map_2d_sw128(&tbl, blo, kpad, npad, kpad, npad))
+      return GNN_ERR_UNSUPPORTED;
+    TcArgs p{};
+    p.M = M;
+    p.N = nb;
+    p.K = K;
+    p.Npad = npad;
+    p.nkb = (int)(kpad / kTcBK);
+    p.mtiles = ceil_div(M, kTcM);
+    p.C = C + n0;
+    p.ldc = ldc;
+    p.vec_store = 1;
+    p.pal = al;
+    p.par = ar;
+    p.pel = el;
+    p.per = er;
+    p.pF = F;
+    p.pn0 = n0;
+    int rc;
+    switch (npad) {
+      case 16: rc = launch_tc<16, EPI_PROJ>(ta, tbh, tbl, p, st); break;
+      case 32: rc = launch_tc<32, EPI_PROJ>(ta, tbh, tbl, p, st); break;
+      case 64: rc = launch_tc<64, EPI_PROJ>(ta, tbh, tbl, p, st); break;
+      default: rc = launch_tc<128, EPI_PROJ>(ta, tbh, tbl, p, st); break;
     }
     if (rc != GNN_OK) return rc;
   }

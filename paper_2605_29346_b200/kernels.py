@@ -561,6 +561,29 @@ class GatRowStatCall:
                 self.stat.data_ptr(), self.stat.stride(0), st), "gat_rowstat_mean")
 
 
+class GatProjGemmCall:
+    """Wh = X W with the GAT attention projections el / er (4 heads of F =
+    N/4 columns) in the same tcgen05 pass (gnn_gemm_gat_proj): Wh is not read
+    back for them."""
+
+    def __init__(self, X, W, Wh, a_l, a_r, el, er):
+        self.lib = _lib.lib()
+        self.dev = X.device
+        self.M, self.Kd = int(X.shape[0]), int(X.shape[1])
+        self.N = int(W.shape[1])
+        self.F = self.N // 4
+        self.t = (X, W, Wh, a_l, a_r, el, er)
+        self.ws = _lib.workspace(self.lib.gnn_gemm_workspace(self.M, self.N, self.Kd, 0), self.dev)
+
+    def __call__(self):
+        X, W, Wh, a_l, a_r, el, er = self.t
+        _lib.check(self.lib.gnn_gemm_gat_proj(
+            self.M, self.N, self.Kd, X.data_ptr(), X.stride(0), W.data_ptr(), W.stride(0),
+            Wh.data_ptr(), Wh.stride(0), self.F, a_l.data_ptr(), a_r.data_ptr(), el.data_ptr(),
+            er.data_ptr(), self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+            "gemm_gat_proj")
+
+
 class GatReluStatGemmCall:
     """dYm = ReLU'(Y) * (A W^T) with the recompute backward's per-head row
     statistics {er, m, 1/sum, S} written after each row's N columns, in the
