@@ -1023,7 +1023,7 @@ class GATTrainer(_FusedEpoch):
         # forward
         # layer 1's attention projections ride in the X W1 GEMM's epilogue when the
         # head width is a multiple of 16 (gnn_gemm_gat_proj; 0.72 -> 0.60 ms)
-        self.fp = (H == 4 and hidden % 16 == 0 and K1 <= 128
+        self.fp = (H == 4 and hidden % 16 == 0 and K1 <= 128 and V >= 128
                    and os.environ.get("GNN_GAT_FUSED_PROJ", "1") != "0")
         if self.fp:
             k["X.W1+proj1"] = GatProjGemmCall(self.X, self.W1, self.Wh1, self.al1, self.ar1,
@@ -1085,7 +1085,8 @@ class GATTrainer(_FusedEpoch):
         # hidden layer's gradient: with the recompute backward and 16-column heads,
         # the GEMM's epilogue applies the ReLU backward and writes the row statistics
         # the CSC pass gathers (gnn_gemm_gat_relu_stat) — dY1 never stored
-        self.fr = (self.rc and K1 in (64, 128) and os.environ.get("GNN_GAT_FUSED_STAT", "1") != "0")
+        self.fr = (self.rc and K1 in (64, 128) and V >= 128
+                   and os.environ.get("GNN_GAT_FUSED_STAT", "1") != "0")
         if self.fr:
             k["dWh2.W2^T"] = GatReluStatGemmCall(self.dWh2, self.W2, self._dY1ms, self.Y1, self.b1,
                                                  self.er1, self.rowstat1)

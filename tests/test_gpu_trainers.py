@@ -76,6 +76,25 @@ def test_gat_trainer_matches_oracle(env, gname, classes, rc, Hd, monkeypatch):
     assert ok, worst
 
 
+def test_gat_trainer_tiny_graph(env):
+    """Fewer vertices than one 128-row tensor-core tile: the fused GEMM epilogues
+    (projections, ReLU-backward statistics, head-mean statistics) step aside for
+    the general kernels, results unchanged."""
+    from paper_2605_29346_b200.models import GATTrainer
+
+    gb, _ = env
+    g = gb.generate(gb.GraphGenSpec("power-law", 100, 900, exponent=2.1), 5)
+    V, F, Hd, H, C = 100, 20, 16, 4, 6
+    X, y = _inputs(V, F, C, seed=2)
+    tr = GATTrainer(g, F, Hd, C, heads=H, seed=1)
+    assert not tr.fp and not tr.fr
+    tr.set_inputs(torch.from_numpy(X), torch.from_numpy(y))
+    tr.forward_backward()
+    torch.cuda.synchronize()
+    p = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in tr.params().items()}
+    _check(tr, oo.gat2_step(g.offsets, g.targets, X, p, y, H))
+
+
 @pytest.mark.parametrize("gname", ["cora_pl", "mega"])
 @pytest.mark.parametrize("coalesced", [False, True])
 @pytest.mark.parametrize("hidden", [32, 64])
