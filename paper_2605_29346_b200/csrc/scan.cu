@@ -105,6 +105,38 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const T *in, T 
   if (write_total && blockIdx.x == 0 && threadIdx.x == 0) out[n] = *total;
 }
 
+// Small scans (<= kScanFusedTiles tiles, e.g. a replayed mini-batch's capacity
+// arrays): the spine pass folds into the down-sweep — each block sums the tile
+// totals before it (integers: exact, order-free), so a scan is two launches.
+constexpr int64_t kScanFusedTiles = 512;
+template <class T>
+__global__ void __launch_bounds__(kScanThreads) scan_down_fused_kernel(const T *in, T *out, int64_t n,
+                                                                       const T *block_sums,
+                                                                       bool write_total) {
+  __shared__ T sw[kScanThreads / 32 + 1];
+  const int64_t nb = ceil_div(n, (int64_t)kScanTile);
+  T pre = 0;
+  for (int64_t i = threadIdx.x; i < (int64_t)blockIdx.x; i += kScanThreads) pre += block_sums[i];
+  T ptot;
+  block_excl_scan<T>(pre, sw, &ptot);  // block-wide sum of the preceding tiles' totals
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  T v[kScanItems];
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : T(0);
+    s += v[i];
+  }
+  T tot;
+  T ex = block_excl_scan<T>(s, sw, &tot) + ptot;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = ex;
+    ex += v[i];
+  }
+  if (write_total && blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = ptot + tot;
+}
+
 template <class T>
 size_t scan_ws(int64_t n) {
   int64_t nb = ceil_div(n > 0 ? n : 1, kScanTile);
@@ -128,6 +160,11 @@ int scan_impl(const T *in, T *out, int64_t n, bool write_total, void *ws, size_t
   if (!a.ok()) return GNN_ERR_WORKSPACE;
   scan_reduce_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
   GNN_LAUNCH_CHECK();
+  if (nb <= kScanFusedTiles) {
+    scan_down_fused_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums, write_total);
+    GNN_LAUNCH_CHECK();
+    return GNN_OK;
+  }
   scan_spine_kernel<T><<<1, kScanThreads, 0, st>>>(sums, nb, total);
   GNN_LAUNCH_CHECK();
   scan_down_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums, total, write_total);
