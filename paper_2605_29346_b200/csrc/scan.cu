@@ -158,6 +158,11 @@ int scan_impl(const T *in, T *out, int64_t n, bool write_total, void *ws, size_t
   T *sums = a.take<T>(nb);
   T *total = a.take<T>(1);
   if (!a.ok()) return GNN_ERR_WORKSPACE;
+  if (nb == 1) {  // one tile: no preceding totals, one launch
+    scan_down_fused_kernel<T><<<1, kScanThreads, 0, st>>>(in, out, n, sums, write_total);
+    GNN_LAUNCH_CHECK();
+    return GNN_OK;
+  }
   scan_reduce_kernel<T><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
   GNN_LAUNCH_CHECK();
   if (nb <= kScanFusedTiles) {
