@@ -58,6 +58,13 @@ typedef enum gnn_status {
 
 /* ---------------------------------------------------------------- misc */
 int gnn_abi_version(void);                 /* bumped on any signature change */
+/* Persisting-L2 controls (gathers whose hot rows are a prefix of the gathered
+ * array, e.g. a degree-ordered numbering): the set-aside size, the largest
+ * access-policy window, and a stream's window (hot prefix persisting, misses
+ * streaming; bytes = 0 clears it). */
+int64_t gnn_l2_max_window(void);
+int gnn_l2_persist_limit(int64_t bytes);
+int gnn_l2_window(gnn_stream_t stream, const void *base, int64_t bytes, float hit_ratio);
 /* "src:<sha256[:16] of the library's sources> git:<sha> sm_100a" — the
  * provenance smoke() and bench.py check against the shipped sources. */
 const char *gnn_build_id(void);

@@ -104,6 +104,9 @@ class SpmmPlan(C.Structure):
 # test suite checks that every declared symbol is exported.
 SIGNATURES = {
     "gnn_abi_version": (c_int, []),
+    "gnn_l2_max_window": (c_i64, []),
+    "gnn_l2_persist_limit": (c_int, [c_i64]),
+    "gnn_l2_window": (c_int, [c_ptr, c_ptr, c_i64, C.c_float]),
     "gnn_build_id": (C.c_char_p, []),
     "gnn_strerror": (C.c_char_p, [c_int]),
     "gnn_last_cuda_error": (c_int, []),

@@ -1605,6 +1605,11 @@ static int spmm_impl(const gnn_csr_view_t *A, const gnn_spmm_plan_t *plan, int64
       side = &side_stream();
       GNN_CUDA_TRY(cudaEventRecord(side->fork, st));
       GNN_CUDA_TRY(cudaStreamWaitEvent(side->s, side->fork, 0));
+      {  // the side stream inherits the caller's L2 access-policy window (gnn_l2_window)
+        cudaStreamAttrValue pv = {};
+        if (cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &pv) == cudaSuccess)
+          cudaStreamSetAttribute(side->s, cudaStreamAttributeAccessPolicyWindow, &pv);
+      }
       GNN_TRY(launch_short_rows(side->s));
       GNN_CUDA_TRY(cudaEventRecord(side->join, side->s));
     } else {

@@ -17,6 +17,45 @@ from . import _lib
 from .graph import SparseOperand, spmm_operand
 
 
+_L2_STATE = {}
+
+
+def l2_hot_window(X) -> int:
+    """Bytes of a persisting-L2 window over the gathered array's low-id prefix
+    (GNN_L2_PERSIST_MB, default 48 MB; measured best on the papers100M shape),
+    for arrays at least twice the size of L2 only: with a degree-ordered
+    numbering (the power-law generator's hubs are its low ids) the prefix holds
+    the rows most gathered, and pinning it keeps the streaming tail from
+    evicting them.  0 = no window."""
+    mb = int(os.environ.get("GNN_L2_PERSIST_MB", "48"))
+    if mb <= 0 or X.device.type != "cuda":
+        return 0
+    dev = X.device.index if X.device.index is not None else torch.cuda.current_device()
+    if dev not in _L2_STATE:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        _L2_STATE[dev] = l2
+        _lib.lib().gnn_l2_persist_limit(mb << 20)
+    if int(X.shape[0]) * X.stride(0) * X.element_size() <= 2 * _L2_STATE[dev]:
+        return 0
+    return mb << 20
+
+
+class _L2Window:
+    """Sets / clears a stream's access-policy window around one launch (kept in
+    the launches' kernel nodes when captured into a CUDA graph)."""
+
+    def __init__(self, lib, X):
+        self.lib, self.X, self.n = lib, X, l2_hot_window(X)
+
+    def __enter__(self):
+        if self.n:
+            self.lib.gnn_l2_window(_lib.stream_handle(self.X.device), self.X.data_ptr(), self.n, 1.0)
+
+    def __exit__(self, *exc):
+        if self.n:
+            self.lib.gnn_l2_window(_lib.stream_handle(self.X.device), None, 0, 0.0)
+
+
 class SpmmCall:
     def __init__(self, op: SparseOperand, X: torch.Tensor, Y: torch.Tensor, *, flags=0, heads=1,
                  vals=None, eid=None, bias=None, self_x=None, self_scale=1.0, mask=None,
@@ -48,13 +87,15 @@ class SpmmCall:
         self._keep = (op, vals, eid, bias, self_x, mask, post_deg_offsets)
         nbytes = self.lib.gnn_spmm_workspace(C.byref(self.view), C.byref(self.plan), self.K)
         self.ws = _lib.workspace(nbytes, self.dev)
+        self.l2 = _L2Window(self.lib, X)  # hub-prefix persisting window (large X only)
 
     def __call__(self):
-        _lib.check(self.lib.gnn_spmm(C.byref(self.view), C.byref(self.plan), self.heads,
-                                     self.X.data_ptr(), self.X.stride(0), self.Y.data_ptr(),
-                                     self.Y.stride(0), self.K, C.byref(self.epi),
-                                     self.ws.data_ptr(), self.ws.numel(),
-                                     _lib.stream_handle(self.dev)), "spmm")
+        with self.l2:
+            _lib.check(self.lib.gnn_spmm(C.byref(self.view), C.byref(self.plan), self.heads,
+                                         self.X.data_ptr(), self.X.stride(0), self.Y.data_ptr(),
+                                         self.Y.stride(0), self.K, C.byref(self.epi),
+                                         self.ws.data_ptr(), self.ws.numel(),
+                                         _lib.stream_handle(self.dev)), "spmm")
 
 
 class DevicePlan:
@@ -111,10 +152,14 @@ class SharedHeadsCall:
         self.ws = _lib.workspace(nbytes, self.dev)
 
     def __call__(self):
-        _lib.check(self.lib.gnn_spmm_shared_heads(
-            C.byref(self.view), C.byref(self.plan), self.X.data_ptr(), self.X.stride(0), self.F,
-            self.Y.data_ptr(), self.Y.stride(0), self.scale, C.byref(self.epi), self.ws.data_ptr(),
-            self.ws.numel(), _lib.stream_handle(self.dev)), "spmm_shared_heads")
+        if not hasattr(self, "l2"):
+            self.l2 = _L2Window(self.lib, self.X)
+        with self.l2:
+            _lib.check(self.lib.gnn_spmm_shared_heads(
+                C.byref(self.view), C.byref(self.plan), self.X.data_ptr(), self.X.stride(0),
+                self.F, self.Y.data_ptr(), self.Y.stride(0), self.scale, C.byref(self.epi),
+                self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(self.dev)),
+                "spmm_shared_heads")
 
 
 class ParallelCall:
@@ -630,6 +675,12 @@ class GatBwdRcCall:
 
     def __call__(self):
         el, dY, Wh, dWh, del_, ds = self.t
+        if not hasattr(self, "l2"):
+            self.l2 = _L2Window(self.lib, dY)  # the gathered gradient rows' hub prefix
+        with self.l2:
+            self._launch(el, dY, Wh, dWh, del_, ds)
+
+    def _launch(self, el, dY, Wh, dWh, del_, ds):
         st = _lib.stream_handle(self.dev)
         if self.mean_F is None:
             _lib.check(self.lib.gnn_gat_bwd_rc(
