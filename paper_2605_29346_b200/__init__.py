@@ -24,6 +24,7 @@ from .graph import (
     total_degree,
 )
 from .ops import colsum, degree_norm_, gemm, linear, spmmv, spmmve
+from .torch_ops import register_graph, release_graph  # torch.ops.gnnb200.* (torch.library)
 
 __version__ = "0.1.0"
 
@@ -32,4 +33,5 @@ __all__ = [
     "OFFSET_DTYPE", "TARGET_DTYPE", "CsrGraph", "GraphGenSpec", "build_subgraph_csr",
     "csr_from_edges", "generate", "load_csr", "load_edge_list", "make_csr", "save_csr",
     "total_degree", "colsum", "degree_norm_", "gemm", "linear", "spmmv", "spmmve",
+    "register_graph", "release_graph",
 ]
